@@ -1,0 +1,153 @@
+/*
+ * hbg.h — C ABI of the B200-native feature-histogram path (arXiv 1706.08359 hot path).
+ *
+ * Plain C types only (no torch / CUDA types in the signatures; streams are
+ * passed as `void*` holding a cudaStream_t, NULL = the handle's own stream).
+ * Every entry point returns an HBG_* status; on failure hbg_last_error()
+ * returns a message (thread-local), mirroring the reference's exceptions.
+ *
+ * Reference seam being replaced (paths under /root/reference/proj):
+ *   HistogramSet build_histograms_partitioned(const BinnedDataset&, const LeafState&,
+ *                                             PrecisionMode, int)   include/histoboost/histogram.hpp:133-134
+ *   dispatched from build_leaf_histograms                           src/tree.cpp:138-161
+ *   selected by enum class HistogramBackend {partitioned, lockstep} include/histoboost/tree.hpp:78
+ * INTEGRATION.md shows the `HistogramBackend::cuda` arm a maintainer adds.
+ */
+#ifndef HBG_H
+#define HBG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (error behaviour of the reference, histogram.cpp / tree.cpp) ---- */
+#define HBG_OK 0
+#define HBG_ERR_INVALID_ARGUMENT 1 /* std::invalid_argument: shape / config (histogram.cpp:27-40,148-154) */
+#define HBG_ERR_LOGIC 2            /* std::logic_error: empty split side (tree.cpp:124-126) */
+#define HBG_ERR_CUDA 3             /* CUDA runtime failure (no CPU fallback exists) */
+#define HBG_ERR_OUT_OF_MEMORY 4
+#define HBG_ERR_NCCL 5
+
+/* g/h addressing for the device builder (hbg_build_histograms_device). */
+#define HBG_GH_LEAF_ALIGNED 0 /* g[i] belongs to leaf position i (LeafState::gradients, leaf.hpp:15-16) */
+#define HBG_GH_ROW_INDEXED 1  /* g[indices[i]] — gather fused into the histogram kernel */
+
+/* One histogram bin; identical layout to histoboost::HistogramBin (histogram_set.hpp:17-21). */
+typedef struct hbg_bin {
+  double grad_sum;
+  double hess_sum;
+  int64_t count;
+} hbg_bin;
+
+/* Best split of a leaf; the fields of histoboost::SplitInfo (tree.hpp:15-24) except
+ * threshold_value, which the caller maps through its BinBoundaries (tree.cpp:174-180). */
+typedef struct hbg_split {
+  int32_t feature; /* -1: no positive-gain split (std::nullopt) */
+  int32_t threshold_bin;
+  double gain;
+  double left_grad, left_hess, right_grad, right_hess;
+  int64_t left_count, right_count;
+  double left_value, right_value;
+} hbg_split;
+
+/* Device-resident packed dataset (subsystem 1). */
+typedef struct hbg_dataset hbg_dataset;
+
+/* How the dataset sits in HBM: row-major, one row = num_groups slices of
+ * slice_bytes; a slice holds 32 features (8-bit: 4 per 32-bit word; 4-bit:
+ * 8 per word), at the bit positions of pack_feature_tuples (binning.cpp:123-158). */
+typedef struct hbg_layout {
+  int64_t num_rows;
+  int32_t num_features;
+  int32_t max_bin;           /* k: 16, 64 or 256 (any 2..256 accepted) */
+  int32_t bits_per_bin;      /* 4 iff max_bin <= 16 (prepare_packed, binning.cpp:230) else 8 */
+  int32_t features_per_word; /* 8 or 4 */
+  int32_t words_per_row;     /* ceil(num_features / features_per_word) */
+  int32_t row_stride_bytes;  /* num_groups * slice_bytes */
+  int32_t slice_bytes;       /* 16 (4-bit) or 32 (8-bit) */
+  int32_t num_groups;        /* ceil(num_features / 32) */
+  int32_t device;
+} hbg_layout;
+
+const char* hbg_last_error(void);
+int32_t hbg_version(void);
+
+/* ---- dataset (rows a1 -> a2 of SURVEY §8) ----
+ * columns[f] points at num_rows uint8 bins of feature f (BinnedColumn::bins,
+ * dataset.hpp:21-26); every bin must be < max_bin (checked on device).
+ * Multi-GPU row shards pass columns[f] + row_begin and the shard's row count. */
+int hbg_dataset_create(const uint8_t* const* columns, int32_t num_features, int64_t num_rows,
+                       int32_t max_bin, int32_t device, hbg_dataset** out);
+int hbg_dataset_destroy(hbg_dataset* ds);
+int hbg_dataset_layout(const hbg_dataset* ds, hbg_layout* out);
+/* Copies the packed rows to host: num_rows * words_per_row uint32 (row-major, pad words dropped). */
+int hbg_dataset_packed_words(const hbg_dataset* ds, uint32_t* host_words);
+
+/* ---- histogram construction (rows a5-a7) ----
+ * Host drop-in for build_histograms_partitioned: indices/gradients/hessians
+ * are the LeafState arrays (leaf-aligned doubles, leaf.hpp:13-21); `out`
+ * receives num_features * max_bin bins, feature-major (HistogramSet order).
+ * Synchronous. count == 0 gives an all-zero histogram. */
+int hbg_build_histograms(hbg_dataset* ds, const int32_t* indices, int64_t count,
+                         const double* gradients, const double* hessians, hbg_bin* out);
+
+/* Device builder (the performance path). d_indices may be NULL for the
+ * identity leaf [0, count) (the root). d_grad/d_hess are fp32, addressed per
+ * gh_mode. d_hist receives the device histogram: SoA fp64
+ * [3][num_features][max_bin] = grad, hess, count (counts exact in fp64).
+ * Asynchronous on `stream`; not re-entrant per handle. */
+int hbg_build_histograms_device(hbg_dataset* ds, const int32_t* d_indices, int64_t count,
+                                const float* d_grad, const float* d_hess, int32_t gh_mode,
+                                double* d_hist, void* stream);
+
+/* Device SoA histogram -> hbg_bin[num_features * max_bin] (device pointer). */
+int hbg_hist_to_bins_device(const double* d_hist, int32_t num_features, int32_t max_bin,
+                            hbg_bin* d_bins, void* stream);
+
+/* ---- histogram subtraction (row a10): sibling = parent - child, elementwise over
+ * n_values = 3 * num_features * max_bin doubles (counts stay exact). */
+int hbg_subtract_device(const double* d_parent, const double* d_child, double* d_sibling,
+                        int64_t n_values, void* stream);
+
+/* ---- leaf gather (row a4): leaf_g[i] = g[idx[i]], leaf_h[i] = h[idx[i]] in fp32,
+ * d_totals[0..1] = fp64 sums in a fixed order (grad_total, hess_total). */
+int hbg_gather_leaf_device(const int32_t* d_indices, int64_t count, const float* d_grad,
+                           const float* d_hess, float* d_leaf_grad, float* d_leaf_hess,
+                           double* d_totals, void* stream);
+
+/* ---- best-split scan (row a11): find_best_split (tree.cpp:163-182) over a device
+ * SoA histogram, fp64, the reference's tie rules (smallest bin, then lowest
+ * feature). Parent totals come from the caller (LeafState totals, tree.cpp:167).
+ * d_out: device hbg_split; feature = -1 when no split. */
+int hbg_best_split_device(const double* d_hist, int32_t num_features, int32_t max_bin,
+                          double grad_total, double hess_total, int64_t count,
+                          int64_t min_data_in_leaf, double lambda, hbg_split* d_out, void* stream);
+/* Same, totals read from device memory (d_totals = {grad, hess}, d_count int64). */
+int hbg_best_split_device_totals(const double* d_hist, int32_t num_features, int32_t max_bin,
+                                 const double* d_totals, const int64_t* d_count,
+                                 int64_t min_data_in_leaf, double lambda, hbg_split* d_out,
+                                 void* stream);
+/* Host convenience: hists are host hbg_bin[num_features * max_bin]; runs the same
+ * device scan and returns 1 if a split was found (0 otherwise) in *found. */
+int hbg_find_best_split(const hbg_bin* hists, int32_t num_features, int32_t max_bin,
+                        double grad_total, double hess_total, int64_t count,
+                        int64_t min_data_in_leaf, double lambda, hbg_split* out, int32_t* found);
+
+/* ---- measurement hooks (bench.py roofline) ----
+ * When enabled, the handle records a CUDA event pair around every histogram
+ * kernel launch (in-stream, no host sync). hbg_dataset_kernel_time waits for
+ * the recorded launches, returns their summed duration and count, and clears
+ * the record. */
+int hbg_dataset_set_profiling(hbg_dataset* ds, int32_t enabled);
+int hbg_dataset_kernel_time(hbg_dataset* ds, double* total_ms, int64_t* launches);
+
+/* ---- stream helpers for callers without a CUDA runtime binding ---- */
+int hbg_stream_synchronize(void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HBG_H */

@@ -1,0 +1,362 @@
+"""B200-native feature-histogram construction (arXiv 1706.08359 hot path).
+
+Host-side mirror of the reference's histogram interface
+(/root/reference/proj/include/histoboost/histogram.hpp:129-134, tree.hpp:59-99)
+over the C ABI in ``include/hbg.h`` (``libhbg.so``, CUDA sm_100a). Names,
+argument meaning and error behaviour follow the reference:
+
+* :class:`Dataset`                 — device-resident packed ``BinnedDataset`` (dataset.hpp:80-91)
+* :class:`LeafState`               — ``LeafState`` (leaf.hpp:13-21)
+* :func:`gather_leaf_statistics`   — tree.cpp:11-25
+* :func:`build_histograms_partitioned` — the drop-in for histogram.hpp:133
+* :func:`find_best_split` / :func:`find_best_threshold` — tree.cpp:76-112,163-182
+
+There is no CPU fallback: if ``libhbg.so`` is missing or no GPU is present,
+every call raises. ``InvalidArgument`` mirrors ``std::invalid_argument`` and
+``LogicError`` mirrors ``std::logic_error``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(HERE)
+LIB_PATH = os.path.join(HERE, "libhbg.so")
+HEADER = os.path.join(REPO, "include", "hbg.h")
+
+HBG_OK = 0
+HBG_ERR_INVALID_ARGUMENT = 1
+HBG_ERR_LOGIC = 2
+HBG_ERR_CUDA = 3
+HBG_ERR_OUT_OF_MEMORY = 4
+HBG_ERR_NCCL = 5
+HBG_GH_LEAF_ALIGNED = 0
+HBG_GH_ROW_INDEXED = 1
+
+#: numpy view of ``hbg_bin`` == ``histoboost::HistogramBin`` (histogram_set.hpp:17-21)
+BIN_DTYPE = np.dtype([("grad_sum", "<f8"), ("hess_sum", "<f8"), ("count", "<i8")])
+#: numpy view of ``hbg_split`` (SplitInfo minus threshold_value, tree.hpp:15-24)
+SPLIT_DTYPE = np.dtype(
+    [
+        ("feature", "<i4"),
+        ("threshold_bin", "<i4"),
+        ("gain", "<f8"),
+        ("left_grad", "<f8"),
+        ("left_hess", "<f8"),
+        ("right_grad", "<f8"),
+        ("right_hess", "<f8"),
+        ("left_count", "<i8"),
+        ("right_count", "<i8"),
+        ("left_value", "<f8"),
+        ("right_value", "<f8"),
+    ]
+)
+
+
+class HbgError(RuntimeError):
+    """Base class; ``code`` is the HBG_* status."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+class InvalidArgument(HbgError, ValueError):
+    """std::invalid_argument analogue (histogram.cpp:27-40,148-154)."""
+
+
+class LogicError(HbgError):
+    """std::logic_error analogue (tree.cpp:124-126,143-145)."""
+
+
+class CudaError(HbgError):
+    """CUDA runtime failure — there is no CPU fallback."""
+
+
+class hbg_layout(C.Structure):
+    _fields_ = [
+        ("num_rows", C.c_int64),
+        ("num_features", C.c_int32),
+        ("max_bin", C.c_int32),
+        ("bits_per_bin", C.c_int32),
+        ("features_per_word", C.c_int32),
+        ("words_per_row", C.c_int32),
+        ("row_stride_bytes", C.c_int32),
+        ("slice_bytes", C.c_int32),
+        ("num_groups", C.c_int32),
+        ("device", C.c_int32),
+    ]
+
+
+#: every symbol include/hbg.h declares (checked by tests/test_abi.py)
+EXPORTED_SYMBOLS = (
+    "hbg_last_error",
+    "hbg_version",
+    "hbg_dataset_create",
+    "hbg_dataset_destroy",
+    "hbg_dataset_layout",
+    "hbg_dataset_packed_words",
+    "hbg_build_histograms",
+    "hbg_build_histograms_device",
+    "hbg_hist_to_bins_device",
+    "hbg_subtract_device",
+    "hbg_gather_leaf_device",
+    "hbg_best_split_device",
+    "hbg_best_split_device_totals",
+    "hbg_find_best_split",
+    "hbg_dataset_set_profiling",
+    "hbg_dataset_kernel_time",
+    "hbg_stream_synchronize",
+)
+
+_P = C.c_void_p
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile libhbg.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
+    if force or not os.path.exists(LIB_PATH):
+        subprocess.run(["make", "-s", "-C", HERE, "-j4"], check=True)
+    return LIB_PATH
+
+
+def lib() -> C.CDLL:
+    """Load libhbg.so; raises if it was never built (no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: run paper_1706_08359_b200.build() (or __graft_entry__.build())"
+            )
+        L = C.CDLL(LIB_PATH)
+        L.hbg_last_error.restype = C.c_char_p
+        L.hbg_version.restype = C.c_int32
+        L.hbg_dataset_create.argtypes = [_P, C.c_int32, C.c_int64, C.c_int32, C.c_int32, _P]
+        L.hbg_dataset_destroy.argtypes = [_P]
+        L.hbg_dataset_layout.argtypes = [_P, _P]
+        L.hbg_dataset_packed_words.argtypes = [_P, _P]
+        L.hbg_build_histograms.argtypes = [_P, _P, C.c_int64, _P, _P, _P]
+        L.hbg_build_histograms_device.argtypes = [_P, _P, C.c_int64, _P, _P, C.c_int32, _P, _P]
+        L.hbg_hist_to_bins_device.argtypes = [_P, C.c_int32, C.c_int32, _P, _P]
+        L.hbg_subtract_device.argtypes = [_P, _P, _P, C.c_int64, _P]
+        L.hbg_gather_leaf_device.argtypes = [_P, C.c_int64, _P, _P, _P, _P, _P, _P]
+        L.hbg_best_split_device.argtypes = [_P, C.c_int32, C.c_int32, C.c_double, C.c_double,
+                                            C.c_int64, C.c_int64, C.c_double, _P, _P]
+        L.hbg_best_split_device_totals.argtypes = [_P, C.c_int32, C.c_int32, _P, _P, C.c_int64,
+                                                   C.c_double, _P, _P]
+        L.hbg_find_best_split.argtypes = [_P, C.c_int32, C.c_int32, C.c_double, C.c_double,
+                                          C.c_int64, C.c_int64, C.c_double, _P, _P]
+        L.hbg_dataset_set_profiling.argtypes = [_P, C.c_int32]
+        L.hbg_dataset_kernel_time.argtypes = [_P, _P, _P]
+        L.hbg_stream_synchronize.argtypes = [_P]
+        _lib = L
+    return _lib
+
+
+def check(status: int) -> None:
+    if status == HBG_OK:
+        return
+    msg = lib().hbg_last_error().decode(errors="replace")
+    cls = {HBG_ERR_INVALID_ARGUMENT: InvalidArgument, HBG_ERR_LOGIC: LogicError}.get(status, CudaError)
+    raise cls(status, msg)
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data_as(C.c_void_p)
+    if isinstance(a, int):
+        return C.c_void_p(a)
+    return C.c_void_p(a.data_ptr())  # torch.Tensor
+
+
+# --------------------------------------------------------------------------- types
+@dataclass
+class LeafState:
+    """Rows of one leaf with leaf-aligned gradients/hessians (leaf.hpp:13-21)."""
+
+    indices: np.ndarray
+    gradients: np.ndarray
+    hessians: np.ndarray
+    grad_total: float = 0.0
+    hess_total: float = 0.0
+
+    def count(self) -> int:
+        return int(len(self.indices))
+
+
+def gather_leaf_statistics(indices, gradients, hessians) -> LeafState:
+    """tree.cpp:11-25 (host arrays): leaf-aligned g/h and double totals in index order."""
+    idx = np.ascontiguousarray(indices, dtype=np.int32)
+    g = np.asarray(gradients, dtype=np.float64)[idx]
+    h = np.asarray(hessians, dtype=np.float64)[idx]
+    gt = 0.0
+    ht = 0.0
+    # sequential double sums, as the reference loop does
+    for v in g.tolist():
+        gt += v
+    for v in h.tolist():
+        ht += v
+    return LeafState(idx, g, h, gt, ht)
+
+
+class Dataset:
+    """Device-resident packed binned dataset (subsystem 1; rows a1-a2).
+
+    ``columns`` is (num_features, num_rows) uint8 — one ``BinnedColumn::bins``
+    per feature (dataset.hpp:21-26), every bin < ``max_bin``.
+    """
+
+    def __init__(self, columns: np.ndarray, max_bin: int, device: int = 0):
+        cols = np.ascontiguousarray(columns, dtype=np.uint8)
+        if cols.ndim != 2:
+            raise InvalidArgument(HBG_ERR_INVALID_ARGUMENT, "columns must be (features, rows)")
+        d, n = cols.shape
+        ptrs = (C.c_void_p * max(d, 1))(*[cols[f].ctypes.data for f in range(d)])
+        h = C.c_void_p()
+        check(lib().hbg_dataset_create(ptrs, d, n, max_bin, device, C.byref(h)))
+        self._h = h
+        self.num_features = d
+        self.num_rows = n
+        self.max_bin = max_bin
+        self.device = device
+
+    @property
+    def handle(self) -> C.c_void_p:
+        if not self._h:
+            raise InvalidArgument(HBG_ERR_INVALID_ARGUMENT, "dataset is closed")
+        return self._h
+
+    def layout(self) -> dict:
+        L = hbg_layout()
+        check(lib().hbg_dataset_layout(self.handle, C.byref(L)))
+        return {name: getattr(L, name) for name, _ in L._fields_}
+
+    def packed_words(self) -> np.ndarray:
+        L = self.layout()
+        out = np.zeros((L["num_rows"], L["words_per_row"]), dtype=np.uint32)
+        check(lib().hbg_dataset_packed_words(self.handle, _ptr(out)))
+        return out
+
+    def hist_values(self) -> int:
+        """Doubles in one device SoA histogram: 3 * num_features * max_bin."""
+        return 3 * self.num_features * self.max_bin
+
+    def build_histograms_device(self, indices, count: int, grad, hess, hist,
+                                gh_mode: int = HBG_GH_LEAF_ALIGNED, stream=None) -> None:
+        """Device builder: pointers are torch tensors / raw ints; async on ``stream``."""
+        check(lib().hbg_build_histograms_device(self.handle, _ptr(indices), count, _ptr(grad),
+                                                _ptr(hess), gh_mode, _ptr(hist), _ptr(stream)))
+
+    def set_profiling(self, enabled: bool) -> None:
+        """Record CUDA events around each histogram kernel launch (measurement only)."""
+        check(lib().hbg_dataset_set_profiling(self.handle, 1 if enabled else 0))
+
+    def kernel_time(self) -> tuple[float, int]:
+        """(summed ms, launches) of the histogram kernels recorded since the last call."""
+        ms = C.c_double()
+        n = C.c_int64()
+        check(lib().hbg_dataset_kernel_time(self.handle, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            check(lib().hbg_dataset_destroy(self._h))
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# --------------------------------------------------------------------- operators
+def build_histograms_partitioned(data: Dataset, leaf: LeafState) -> np.ndarray:
+    """Drop-in for ``build_histograms_partitioned`` (histogram.hpp:133-134).
+
+    Returns the HistogramSet as a (num_features, max_bin) ``BIN_DTYPE`` array
+    (feature-major, one entry per feature id). Counts are exact; sums are fp32
+    accumulations reduced in fp64 (tolerance documented in DESIGN.md §5).
+    """
+    n = leaf.count()
+    idx = np.ascontiguousarray(leaf.indices, dtype=np.int32)
+    g = np.ascontiguousarray(leaf.gradients, dtype=np.float64)
+    h = np.ascontiguousarray(leaf.hessians, dtype=np.float64)
+    if len(g) != n or len(h) != n:
+        raise InvalidArgument(HBG_ERR_INVALID_ARGUMENT, "leaf arrays disagree on length")
+    out = np.zeros((data.num_features, data.max_bin), dtype=BIN_DTYPE)
+    check(lib().hbg_build_histograms(data.handle, _ptr(idx), n, _ptr(g), _ptr(h), _ptr(out)))
+    return out
+
+
+def find_best_split(hists: np.ndarray, leaf_totals, min_data_in_leaf: int = 1, lam: float = 0.0):
+    """find_best_split (tree.cpp:163-182) on the GPU; ``leaf_totals`` = (grad, hess, count).
+
+    Returns a ``SPLIT_DTYPE`` record or None (std::nullopt)."""
+    hists = np.ascontiguousarray(hists, dtype=BIN_DTYPE)
+    d, k = hists.shape
+    gt, ht, cnt = leaf_totals
+    out = np.zeros(1, dtype=SPLIT_DTYPE)
+    found = C.c_int32()
+    check(lib().hbg_find_best_split(_ptr(hists), d, k, float(gt), float(ht), int(cnt),
+                                    int(min_data_in_leaf), float(lam), _ptr(out), C.byref(found)))
+    return out[0] if found.value else None
+
+
+def find_best_threshold(hist: np.ndarray, feature_id: int, leaf_totals, min_data_in_leaf: int = 1,
+                        lam: float = 0.0):
+    """find_best_threshold (tree.cpp:76-112) for one feature's bins, on the GPU."""
+    hist = np.ascontiguousarray(hist, dtype=BIN_DTYPE).reshape(1, -1)
+    s = find_best_split(hist, leaf_totals, min_data_in_leaf, lam)
+    if s is not None:
+        s = s.copy()
+        s["feature"] = feature_id
+    return s
+
+
+def subtract_device(parent, child, sibling, n_values: int, stream=None) -> None:
+    """Histogram subtraction: sibling = parent - child (device SoA histograms)."""
+    check(lib().hbg_subtract_device(_ptr(parent), _ptr(child), _ptr(sibling), n_values, _ptr(stream)))
+
+
+def gather_leaf_device(indices, count: int, grad, hess, leaf_grad, leaf_hess, totals, stream=None):
+    check(lib().hbg_gather_leaf_device(_ptr(indices), count, _ptr(grad), _ptr(hess), _ptr(leaf_grad),
+                                       _ptr(leaf_hess), _ptr(totals), _ptr(stream)))
+
+
+def best_split_device(hist, num_features: int, max_bin: int, grad_total: float, hess_total: float,
+                      count: int, min_data_in_leaf: int, lam: float, out, stream=None) -> None:
+    check(lib().hbg_best_split_device(_ptr(hist), num_features, max_bin, grad_total, hess_total,
+                                      count, min_data_in_leaf, lam, _ptr(out), _ptr(stream)))
+
+
+def best_split_device_totals(hist, num_features: int, max_bin: int, totals, count_dev,
+                             min_data_in_leaf: int, lam: float, out, stream=None) -> None:
+    check(lib().hbg_best_split_device_totals(_ptr(hist), num_features, max_bin, _ptr(totals),
+                                             _ptr(count_dev), min_data_in_leaf, lam, _ptr(out),
+                                             _ptr(stream)))
+
+
+def hist_to_bins_device(hist, num_features: int, max_bin: int, bins, stream=None) -> None:
+    check(lib().hbg_hist_to_bins_device(_ptr(hist), num_features, max_bin, _ptr(bins), _ptr(stream)))
+
+
+def stats_close(a, b, tolerance: float):
+    """histogram.cpp:12-15, vectorised."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    scale = np.maximum(1.0, np.maximum(np.abs(a), np.abs(b)))
+    return np.abs(a - b) <= tolerance * scale

@@ -1,0 +1,413 @@
+// capi.cu — the extern "C" boundary declared in include/hbg.h.
+//
+// C++ host logic: argument validation with the reference's error classes
+// (std::invalid_argument -> HBG_ERR_INVALID_ARGUMENT, std::logic_error ->
+// HBG_ERR_LOGIC), device memory ownership, launch planning. There is no CPU
+// fallback anywhere: a missing GPU or CUDA failure is an error status.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "hbg_internal.h"
+
+namespace hbg {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
+  char buf[512];
+  std::snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e),
+                cudaGetErrorString(e), file, line, what);
+  throw Error(e == cudaErrorMemoryAllocation ? HBG_ERR_OUT_OF_MEMORY : HBG_ERR_CUDA, buf);
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return HBG_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return HBG_ERR_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return HBG_ERR_LOGIC;
+  }
+}
+
+// A grow-only device buffer.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void* get(size_t need) {
+    if (need > bytes) {
+      if (p) HBG_CUDA(cudaFree(p));
+      p = nullptr;
+      bytes = 0;
+      HBG_CUDA(cudaMalloc(&p, std::max<size_t>(need, 256)));
+      bytes = std::max<size_t>(need, 256);
+    }
+    return p;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    HBG_CUDA(cudaGetDevice(&prev));
+    if (prev != dev) HBG_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace hbg
+
+struct hbg_dataset {
+  hbg_layout layout{};
+  uint32_t* packed = nullptr;  // num_rows * row_stride_bytes
+  cudaStream_t stream = nullptr;
+  // workspace (not re-entrant per handle)
+  hbg::DevBuf part, host_idx, host_gd, host_hd, host_gf, host_hf, host_hist, host_bins;
+  // measurement hooks
+  bool profiling = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;  // recorded, not yet read
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spare;
+  std::pair<cudaEvent_t, cudaEvent_t> event_pair() {
+    if (!spare.empty()) {
+      auto e = spare.back();
+      spare.pop_back();
+      return e;
+    }
+    std::pair<cudaEvent_t, cudaEvent_t> e;
+    HBG_CUDA(cudaEventCreate(&e.first));
+    HBG_CUDA(cudaEventCreate(&e.second));
+    return e;
+  }
+  ~hbg_dataset() {
+    for (auto& e : events) spare.push_back(e);
+    for (auto& e : spare) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+    if (stream) cudaStreamSynchronize(stream);
+    if (packed) cudaFree(packed);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+using namespace hbg;
+
+namespace {
+
+void check_ds(const hbg_dataset* ds) { require(ds != nullptr, "null dataset handle"); }
+
+cudaStream_t pick(hbg_dataset* ds, void* stream) {
+  return stream ? static_cast<cudaStream_t>(stream) : ds->stream;
+}
+
+void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const float* d_g,
+                  const float* d_h, int gh_mode, double* d_hist, cudaStream_t s) {
+  const hbg_layout& L = ds->layout;
+  require(count >= 0, "negative leaf size");
+  require(count <= L.num_rows || d_idx != nullptr, "identity leaf larger than the dataset");
+  require(gh_mode == HBG_GH_LEAF_ALIGNED || gh_mode == HBG_GH_ROW_INDEXED, "bad gh_mode");
+  require(d_hist != nullptr, "null histogram output");
+  const size_t D = static_cast<size_t>(L.num_features) * L.max_bin;
+  if (count == 0 || L.num_features == 0) {
+    HBG_CUDA(cudaMemsetAsync(d_hist, 0, 3 * D * sizeof(double), s));
+    return;
+  }
+  require(d_g != nullptr && d_h != nullptr, "null gradient/hessian pointer");
+  HistPlan plan = plan_histogram(L.bits_per_bin, L.max_bin, L.num_groups, count, L.device);
+  float* part = static_cast<float*>(ds->part.get(plan.part_values * 12));
+  HistArgs a{};
+  a.packed = reinterpret_cast<const uint8_t*>(ds->packed);
+  a.row_stride = L.row_stride_bytes;
+  a.idx = d_idx;
+  a.n = count;
+  a.g = d_g;
+  a.h = d_h;
+  a.gh_indexed = gh_mode == HBG_GH_ROW_INDEXED;
+  a.num_groups = L.num_groups;
+  a.gb = plan.gb;
+  a.wpg = plan.wpg;
+  a.nblocks = plan.nblocks;
+  a.seg_len = plan.seg_len;
+  a.part_g = part;
+  a.part_h = part + plan.part_values;
+  a.part_c = reinterpret_cast<uint32_t*>(part + 2 * plan.part_values);
+  if (ds->profiling) {
+    auto ev = ds->event_pair();
+    HBG_CUDA(cudaEventRecord(ev.first, s));
+    launch_histogram(plan, a, s);
+    HBG_CUDA(cudaEventRecord(ev.second, s));
+    ds->events.push_back(ev);
+  } else {
+    launch_histogram(plan, a, s);
+  }
+  launch_reduce_partials(plan, a, L.num_features, L.max_bin, d_hist, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hbg_last_error(void) { return g_last_error.c_str(); }
+
+int32_t hbg_version(void) { return 1; }
+
+int hbg_dataset_create(const uint8_t* const* columns, int32_t num_features, int64_t num_rows,
+                       int32_t max_bin, int32_t device, hbg_dataset** out) {
+  return guarded([&] {
+    require(out != nullptr, "null output handle");
+    *out = nullptr;
+    require(num_features >= 0 && num_rows >= 0, "negative shape");
+    require(max_bin >= 2 && max_bin <= 256, "max_bin out of range [2, 256]");
+    require(num_rows <= INT32_MAX, "row ids are int32 (row_index_t, dataset.hpp:9)");
+    require(num_features == 0 || columns != nullptr, "null columns");
+    int ndev = 0;
+    HBG_CUDA(cudaGetDeviceCount(&ndev));
+    require(device >= 0 && device < ndev, "device ordinal out of range");
+    DeviceGuard dg(device);
+    auto ds = std::make_unique<hbg_dataset>();
+    hbg_layout& L = ds->layout;
+    L.num_rows = num_rows;
+    L.num_features = num_features;
+    L.max_bin = max_bin;
+    L.bits_per_bin = max_bin <= 16 ? 4 : 8;
+    L.features_per_word = 32 / L.bits_per_bin;
+    L.words_per_row = (num_features + L.features_per_word - 1) / L.features_per_word;
+    L.slice_bytes = L.bits_per_bin == 4 ? 16 : 32;
+    L.num_groups = (num_features + 31) / 32;
+    L.row_stride_bytes = L.num_groups * L.slice_bytes;
+    L.device = device;
+    HBG_CUDA(cudaStreamCreateWithFlags(&ds->stream, cudaStreamNonBlocking));
+    const size_t packed_bytes = static_cast<size_t>(num_rows) * L.row_stride_bytes;
+    HBG_CUDA(cudaMalloc(&ds->packed, std::max<size_t>(packed_bytes, 16)));
+    if (packed_bytes > 0) {
+      for (int f = 0; f < num_features; ++f) require(columns[f] != nullptr, "null column pointer");
+      // Upload column-major bins (a1) and pack on device (a2), one 32-feature
+      // slice group at a time so the staging buffer stays small.
+      DevBuf cols_buf, bad_buf;
+      int* d_bad = static_cast<int*>(bad_buf.get(sizeof(int)));
+      HBG_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), ds->stream));
+      const int stride_words = L.row_stride_bytes / 4;
+      for (int f0 = 0; f0 < num_features; f0 += 32) {
+        const int nf = std::min(32, num_features - f0);
+        uint8_t* d_cols = static_cast<uint8_t*>(cols_buf.get(static_cast<size_t>(nf) * num_rows));
+        for (int f = 0; f < nf; ++f) {
+          HBG_CUDA(cudaMemcpyAsync(d_cols + static_cast<size_t>(f) * num_rows, columns[f0 + f],
+                                   static_cast<size_t>(num_rows), cudaMemcpyHostToDevice, ds->stream));
+        }
+        launch_pack(d_cols, f0, nf, num_features, num_rows, max_bin, L.bits_per_bin,
+                    stride_words, ds->packed, d_bad, ds->stream);
+      }
+      int bad = 0;
+      HBG_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, ds->stream));
+      HBG_CUDA(cudaStreamSynchronize(ds->stream));
+      require(bad == 0, "bin value >= max_bin in input columns");
+    }
+    *out = ds.release();
+  });
+}
+
+int hbg_dataset_destroy(hbg_dataset* ds) {
+  return guarded([&] {
+    if (!ds) return;
+    DeviceGuard dg(ds->layout.device);
+    delete ds;
+  });
+}
+
+int hbg_dataset_layout(const hbg_dataset* ds, hbg_layout* out) {
+  return guarded([&] {
+    check_ds(ds);
+    require(out != nullptr, "null output");
+    *out = ds->layout;
+  });
+}
+
+int hbg_dataset_packed_words(const hbg_dataset* ds, uint32_t* host_words) {
+  return guarded([&] {
+    check_ds(ds);
+    const hbg_layout& L = ds->layout;
+    if (L.num_rows == 0 || L.words_per_row == 0) return;
+    require(host_words != nullptr, "null output");
+    DeviceGuard dg(L.device);
+    HBG_CUDA(cudaMemcpy2D(host_words, static_cast<size_t>(L.words_per_row) * 4, ds->packed,
+                          static_cast<size_t>(L.row_stride_bytes), static_cast<size_t>(L.words_per_row) * 4,
+                          static_cast<size_t>(L.num_rows), cudaMemcpyDeviceToHost));
+  });
+}
+
+int hbg_build_histograms(hbg_dataset* ds, const int32_t* indices, int64_t count,
+                         const double* gradients, const double* hessians, hbg_bin* out) {
+  return guarded([&] {
+    check_ds(ds);
+    const hbg_layout& L = ds->layout;
+    require(count >= 0, "negative leaf size");
+    require(out != nullptr, "null output");
+    require(count == 0 || (indices && gradients && hessians), "null leaf arrays");
+    DeviceGuard dg(L.device);
+    cudaStream_t s = ds->stream;
+    const size_t D = static_cast<size_t>(L.num_features) * L.max_bin;
+    double* d_hist = static_cast<double*>(ds->host_hist.get(3 * D * sizeof(double) + 8));
+    hbg_bin* d_bins = static_cast<hbg_bin*>(ds->host_bins.get(D * sizeof(hbg_bin) + 8));
+    int32_t* d_idx = nullptr;
+    float *d_gf = nullptr, *d_hf = nullptr;
+    if (count > 0) {
+      const size_t n = static_cast<size_t>(count);
+      d_idx = static_cast<int32_t*>(ds->host_idx.get(n * 4));
+      double* d_gd = static_cast<double*>(ds->host_gd.get(n * 8));
+      double* d_hd = static_cast<double*>(ds->host_hd.get(n * 8));
+      d_gf = static_cast<float*>(ds->host_gf.get(n * 4));
+      d_hf = static_cast<float*>(ds->host_hf.get(n * 4));
+      HBG_CUDA(cudaMemcpyAsync(d_idx, indices, n * 4, cudaMemcpyHostToDevice, s));
+      HBG_CUDA(cudaMemcpyAsync(d_gd, gradients, n * 8, cudaMemcpyHostToDevice, s));
+      HBG_CUDA(cudaMemcpyAsync(d_hd, hessians, n * 8, cudaMemcpyHostToDevice, s));
+      launch_f64_to_f32(d_gd, d_gf, count, s);
+      launch_f64_to_f32(d_hd, d_hf, count, s);
+    }
+    build_device(ds, d_idx, count, d_gf, d_hf, HBG_GH_LEAF_ALIGNED, d_hist, s);
+    launch_hist_to_bins(d_hist, static_cast<int64_t>(D), d_bins, s);
+    if (D > 0) HBG_CUDA(cudaMemcpyAsync(out, d_bins, D * sizeof(hbg_bin), cudaMemcpyDeviceToHost, s));
+    HBG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int hbg_build_histograms_device(hbg_dataset* ds, const int32_t* d_indices, int64_t count,
+                                const float* d_grad, const float* d_hess, int32_t gh_mode,
+                                double* d_hist, void* stream) {
+  return guarded([&] {
+    check_ds(ds);
+    DeviceGuard dg(ds->layout.device);
+    build_device(ds, d_indices, count, d_grad, d_hess, gh_mode, d_hist, pick(ds, stream));
+  });
+}
+
+int hbg_hist_to_bins_device(const double* d_hist, int32_t num_features, int32_t max_bin,
+                            hbg_bin* d_bins, void* stream) {
+  return guarded([&] {
+    require(num_features >= 0 && max_bin >= 1, "bad shape");
+    launch_hist_to_bins(d_hist, static_cast<int64_t>(num_features) * max_bin, d_bins,
+                        static_cast<cudaStream_t>(stream));
+  });
+}
+
+int hbg_subtract_device(const double* d_parent, const double* d_child, double* d_sibling,
+                        int64_t n_values, void* stream) {
+  return guarded([&] {
+    require(n_values >= 0, "negative size");
+    launch_subtract(d_parent, d_child, d_sibling, n_values, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int hbg_gather_leaf_device(const int32_t* d_indices, int64_t count, const float* d_grad,
+                           const float* d_hess, float* d_leaf_grad, float* d_leaf_hess,
+                           double* d_totals, void* stream) {
+  return guarded([&] {
+    require(count >= 0, "negative leaf size");
+    require(d_totals != nullptr, "null totals");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    static thread_local DevBuf scratch;
+    int dev = 0;
+    HBG_CUDA(cudaGetDevice(&dev));
+    (void)dev;
+    double* sc = static_cast<double*>(scratch.get(gather_scratch_doubles(count) * sizeof(double)));
+    launch_gather(d_indices, count, d_grad, d_hess, d_leaf_grad, d_leaf_hess, d_totals, sc, s);
+  });
+}
+
+int hbg_best_split_device(const double* d_hist, int32_t num_features, int32_t max_bin,
+                          double grad_total, double hess_total, int64_t count,
+                          int64_t min_data_in_leaf, double lambda, hbg_split* d_out, void* stream) {
+  return guarded([&] {
+    require(num_features >= 0 && max_bin >= 1, "bad shape");
+    require(d_out != nullptr, "null output");
+    launch_best_split(d_hist, num_features, max_bin, nullptr, nullptr, grad_total, hess_total,
+                      count, min_data_in_leaf, lambda, d_out, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int hbg_best_split_device_totals(const double* d_hist, int32_t num_features, int32_t max_bin,
+                                 const double* d_totals, const int64_t* d_count,
+                                 int64_t min_data_in_leaf, double lambda, hbg_split* d_out,
+                                 void* stream) {
+  return guarded([&] {
+    require(num_features >= 0 && max_bin >= 1, "bad shape");
+    require(d_out != nullptr && d_totals != nullptr && d_count != nullptr, "null pointer");
+    launch_best_split(d_hist, num_features, max_bin, d_totals, d_count, 0.0, 0.0, 0,
+                      min_data_in_leaf, lambda, d_out, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int hbg_find_best_split(const hbg_bin* hists, int32_t num_features, int32_t max_bin,
+                        double grad_total, double hess_total, int64_t count,
+                        int64_t min_data_in_leaf, double lambda, hbg_split* out, int32_t* found) {
+  return guarded([&] {
+    require(num_features >= 0 && max_bin >= 1, "bad shape");
+    require(out != nullptr && found != nullptr, "null output");
+    require(num_features == 0 || hists != nullptr, "null histograms");
+    const size_t D = static_cast<size_t>(num_features) * max_bin;
+    std::vector<double> soa(3 * D);
+    for (size_t i = 0; i < D; ++i) {
+      soa[i] = hists[i].grad_sum;
+      soa[D + i] = hists[i].hess_sum;
+      soa[2 * D + i] = static_cast<double>(hists[i].count);
+    }
+    DevBuf dh, ds;
+    double* d_hist = static_cast<double*>(dh.get(soa.size() * sizeof(double) + 8));
+    hbg_split* d_out = static_cast<hbg_split*>(ds.get(sizeof(hbg_split)));
+    if (D) HBG_CUDA(cudaMemcpy(d_hist, soa.data(), soa.size() * sizeof(double), cudaMemcpyHostToDevice));
+    launch_best_split(d_hist, num_features, max_bin, nullptr, nullptr, grad_total, hess_total,
+                      count, min_data_in_leaf, lambda, d_out, nullptr);
+    HBG_CUDA(cudaMemcpy(out, d_out, sizeof(hbg_split), cudaMemcpyDeviceToHost));
+    *found = out->feature >= 0 ? 1 : 0;
+  });
+}
+
+int hbg_dataset_set_profiling(hbg_dataset* ds, int32_t enabled) {
+  return guarded([&] {
+    check_ds(ds);
+    ds->profiling = enabled != 0;
+  });
+}
+
+int hbg_dataset_kernel_time(hbg_dataset* ds, double* total_ms, int64_t* launches) {
+  return guarded([&] {
+    check_ds(ds);
+    require(total_ms != nullptr && launches != nullptr, "null output");
+    DeviceGuard dg(ds->layout.device);
+    double t = 0.0;
+    for (auto& e : ds->events) {
+      HBG_CUDA(cudaEventSynchronize(e.second));
+      float ms = 0.f;
+      HBG_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
+      t += ms;
+      ds->spare.push_back(e);
+    }
+    *total_ms = t;
+    *launches = static_cast<int64_t>(ds->events.size());
+    ds->events.clear();
+  });
+}
+
+int hbg_stream_synchronize(void* stream) {
+  return guarded([&] { HBG_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream))); });
+}
+
+}  // extern "C"

@@ -1,0 +1,86 @@
+// hbg_internal.h — shared declarations between the C-ABI layer (capi.cu) and
+// the kernels (hist_kernels.cu, leaf_kernels.cu). Not a public header.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "hbg.h"
+
+namespace hbg {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void throw_cuda(cudaError_t e, const char* what, const char* file, int line);
+
+#define HBG_CUDA(call)                                                    \
+  do {                                                                    \
+    cudaError_t hbg_e_ = (call);                                          \
+    if (hbg_e_ != cudaSuccess) ::hbg::throw_cuda(hbg_e_, #call, __FILE__, __LINE__); \
+  } while (0)
+#define HBG_LAUNCH_CHECK() HBG_CUDA(cudaGetLastError())
+
+inline void require(bool ok, const std::string& msg) {
+  if (!ok) throw Error(HBG_ERR_INVALID_ARGUMENT, msg);
+}
+
+// Geometry of one histogram launch (chosen on the host by plan_histogram()).
+struct HistPlan {
+  int k_alloc;      // power-of-two bin slots per feature in shared memory (16/64/128/256)
+  int bits;         // 4 or 8
+  int warps;        // warps per CTA
+  int gb;           // slice groups per CTA ("group block")
+  int wpg;          // warps per group (row-interleaved over 32-row tiles)
+  int nblocks;      // ceil(num_groups / gb)
+  int nseg;         // row segments
+  int64_t seg_len;  // leaf positions per segment (multiple of 32)
+  int ctas;         // nblocks * nseg
+  size_t smem;      // dynamic shared memory per CTA
+  size_t part_values;  // entries in each partial array (ctas * gb * 32 * k_alloc)
+};
+
+struct HistArgs {
+  const uint8_t* packed;
+  int64_t row_stride;  // bytes
+  const int32_t* idx;  // nullptr: identity leaf
+  int64_t n;
+  const float* g;
+  const float* h;
+  int gh_indexed;
+  int num_groups;
+  int gb, wpg, nblocks;
+  int64_t seg_len;
+  float* part_g;
+  float* part_h;
+  uint32_t* part_c;
+};
+
+HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int device);
+
+void launch_histogram(const HistPlan& plan, const HistArgs& args, cudaStream_t s);
+void launch_reduce_partials(const HistPlan& plan, const HistArgs& args, int num_features,
+                            int max_bin, double* d_hist, cudaStream_t s);
+// Packs features [f0, f0 + nf) (one 32-feature slice group; d_cols holds
+// their column-major bins) into the group's words of every row.
+void launch_pack(const uint8_t* d_cols, int f0, int nf, int num_features, int64_t num_rows,
+                 int max_bin, int bits, int row_stride_words, uint32_t* d_packed, int* d_bad,
+                 cudaStream_t s);
+void launch_f64_to_f32(const double* in, float* out, int64_t n, cudaStream_t s);
+void launch_hist_to_bins(const double* d_hist, int64_t cells, hbg_bin* d_bins, cudaStream_t s);
+void launch_subtract(const double* a, const double* b, double* out, int64_t n, cudaStream_t s);
+void launch_gather(const int32_t* idx, int64_t n, const float* g, const float* h, float* lg,
+                   float* lh, double* totals, double* scratch, cudaStream_t s);
+size_t gather_scratch_doubles(int64_t n);
+void launch_best_split(const double* d_hist, int d, int k, const double* d_totals,
+                       const int64_t* d_count, double gt, double ht, int64_t count,
+                       int64_t min_data, double lambda, hbg_split* out, cudaStream_t s);
+
+int sm_count(int device);
+
+}  // namespace hbg

@@ -1,0 +1,372 @@
+// hist_kernels.cu — sm_100a kernels for subsystems (1) packed layout and
+// (3) the feature-histogram build.
+//
+// Histogram kernel design (DESIGN.md §3 has the measurements behind it):
+//  * Rows in lanes. A warp takes a 32-row tile of the leaf; lane l owns leaf
+//    position t+l and loads that row's 32-feature slice (32 B at 8-bit, 16 B
+//    at 4-bit) with 128-bit loads, plus its fp32 g/h.
+//  * Feature rotation (the paper's Alg. 2 "rotated" schedule, reference
+//    lockstep.cpp:98-105): at step p lane l updates feature (l + p) mod 32, so
+//    the 32 lanes of every shared-memory instruction hit 32 distinct feature
+//    columns. With the [bin][feature] cell layout the bank is the feature,
+//    so every LDS/STS/ATOMS is bank-conflict-free whatever the bins are.
+//  * Per-warp private fp32 {g,h} cells (plain LDS.64/FADD/STS.64 — sm_100a has
+//    no native shared fp32 atomic; atomicAdd(float) is a CAS loop measured 5x
+//    slower) and CTA-shared u32 counts via the native ATOMS.POPC.INC. The
+//    RMW steps stay in program order (volatile asm), which keeps lane A's
+//    step-p store ahead of lane B's step-(p+1) load of the same cell.
+//  * Each CTA folds its warps' cells in a fixed order and writes one fp32/u32
+//    partial; reduce_partials_kernel sums partials over row segments in a
+//    fixed order in fp64. Results are therefore deterministic for a given
+//    (leaf size, feature count, GPU), like the reference's fixed 64 Ki-chunk
+//    reduction (histogram.cpp:159-215).
+#include <algorithm>
+#include <mutex>
+
+#include "hbg_internal.h"
+
+namespace hbg {
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void lds_f2(uint32_t a, float& x, float& y) {
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(x), "=f"(y) : "r"(a));
+}
+
+__device__ __forceinline__ void sts_f2(uint32_t a, float x, float y) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(x), "f"(y));
+}
+
+template <int BITS>
+struct Slice {
+  static constexpr int kWords = BITS == 8 ? 8 : 4;  // 32 features per slice
+  static constexpr int kFeatPerWord = 32 / BITS;
+  uint32_t w[kWords];
+};
+
+template <int BITS>
+__device__ __forceinline__ void load_slice(const unsigned char* p, Slice<BITS>& s) {
+  const uint4 a = __ldg(reinterpret_cast<const uint4*>(p));
+  s.w[0] = a.x;
+  s.w[1] = a.y;
+  s.w[2] = a.z;
+  s.w[3] = a.w;
+  if constexpr (BITS == 8) {
+    const uint4 b = __ldg(reinterpret_cast<const uint4*>(p) + 1);
+    s.w[4] = b.x;
+    s.w[5] = b.y;
+    s.w[6] = b.z;
+    s.w[7] = b.w;
+  }
+}
+
+// Rotate the 32-feature slice so that feature (lane + p) mod 32 sits at
+// position p: word rotation by a lane-dependent amount (select network),
+// then a funnel shift for the sub-word part.
+template <int BITS>
+__device__ __forceinline__ void rotate_slice(Slice<BITS>& s, int lane) {
+  constexpr int W = Slice<BITS>::kWords;
+  const int fpw = Slice<BITS>::kFeatPerWord;
+  const int q = lane / fpw;          // whole words
+  const int r = (lane % fpw) * BITS;  // bits within a word
+  uint32_t t[W];
+#pragma unroll
+  for (int step = W / 2; step >= 1; step >>= 1) {
+    const bool on = (q & step) != 0;
+#pragma unroll
+    for (int j = 0; j < W; ++j) t[j] = on ? s.w[(j + step) % W] : s.w[j];
+#pragma unroll
+    for (int j = 0; j < W; ++j) s.w[j] = t[j];
+  }
+#pragma unroll
+  for (int j = 0; j < W; ++j) t[j] = __funnelshift_r(s.w[j], s.w[(j + 1) % W], r);
+#pragma unroll
+  for (int j = 0; j < W; ++j) s.w[j] = t[j];
+}
+
+template <int BITS, int K>
+__device__ __forceinline__ void update_step(const Slice<BITS>& s, int p, int lane, uint32_t gh_base,
+                                            uint32_t* cnt, float g, float h) {
+  constexpr int fpw = Slice<BITS>::kFeatPerWord;
+  const uint32_t b = (s.w[p / fpw] >> (BITS * (p % fpw))) & (K - 1);
+  const uint32_t cell = (b << 5) | ((lane + p) & 31);
+  const uint32_t a = gh_base + cell * 8u;
+  float x, y;
+  lds_f2(a, x, y);
+  x += g;
+  y += h;
+  sts_f2(a, x, y);
+  atomicAdd(cnt + cell, 1u);  // ATOMS.POPC.INC
+}
+
+struct TileIn {
+  int64_t row;
+  float g, h;
+};
+
+template <int BITS, int K>
+__global__ void __launch_bounds__(512) hist_kernel(HistArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int kCells = K * 32;
+  const int warps = blockDim.x >> 5;
+  float2* gh = reinterpret_cast<float2*>(smem);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + static_cast<size_t>(warps) * kCells * 8);
+  {
+    const int n16 = (warps * kCells * 8 + a.gb * kCells * 4) / 16;
+    uint4* z = reinterpret_cast<uint4*>(smem);
+    for (int i = threadIdx.x; i < n16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+  }
+  __syncthreads();
+
+  const int bi = blockIdx.x % a.nblocks;
+  const int seg = blockIdx.x / a.nblocks;
+  const int w = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int gl = w % a.gb;
+  const int sub = w / a.gb;
+  const int group = bi * a.gb + gl;
+  if (sub < a.wpg && group < a.num_groups) {
+    const int64_t s0 = static_cast<int64_t>(seg) * a.seg_len;
+    const int64_t s1 = min(s0 + a.seg_len, a.n);
+    const uint32_t gh_base = smem_addr(gh + static_cast<size_t>(w) * kCells);
+    uint32_t* cnt_g = cnt + static_cast<size_t>(gl) * kCells;
+    const unsigned char* base = a.packed + static_cast<size_t>(group) * Slice<BITS>::kWords * 4;
+    const int64_t step = static_cast<int64_t>(a.wpg) * 32;
+
+    auto fetch = [&](int64_t t, TileIn& in, Slice<BITS>& sl) {
+      const int64_t pos = t + lane;
+      if (pos < s1) {
+        const int64_t row = a.idx ? static_cast<int64_t>(__ldg(a.idx + pos)) : pos;
+        const int64_t gi = a.gh_indexed ? row : pos;
+        in.row = row;
+        in.g = __ldg(a.g + gi);
+        in.h = __ldg(a.h + gi);
+        load_slice<BITS>(base + row * a.row_stride, sl);
+      } else {
+        in.row = -1;
+        in.g = 0.f;
+        in.h = 0.f;
+#pragma unroll
+        for (int j = 0; j < Slice<BITS>::kWords; ++j) sl.w[j] = 0;
+      }
+    };
+
+    int64_t t = s0 + static_cast<int64_t>(sub) * 32;
+    TileIn cur_in;
+    Slice<BITS> cur;
+    if (t < s1) fetch(t, cur_in, cur);
+    for (; t < s1; t += step) {
+      TileIn nxt_in;
+      Slice<BITS> nxt;
+      const bool more = t + step < s1;
+      if (more) fetch(t + step, nxt_in, nxt);
+      rotate_slice<BITS>(cur, lane);
+      if (t + 32 <= s1) {
+#pragma unroll
+        for (int p = 0; p < 32; ++p)
+          update_step<BITS, K>(cur, p, lane, gh_base, cnt_g, cur_in.g, cur_in.h);
+      } else {
+        const bool valid = cur_in.row >= 0;
+#pragma unroll
+        for (int p = 0; p < 32; ++p)
+          if (valid) update_step<BITS, K>(cur, p, lane, gh_base, cnt_g, cur_in.g, cur_in.h);
+      }
+      if (more) {
+        cur_in = nxt_in;
+        cur = nxt;
+      }
+    }
+  }
+  __syncthreads();
+
+  // Fold the warps of each group in a fixed order; one partial per CTA.
+  for (int i = threadIdx.x; i < a.gb * kCells; i += blockDim.x) {
+    const int g2 = i / kCells;
+    const int c = i - g2 * kCells;
+    float sg = 0.f, sh = 0.f;
+    for (int s = 0; s < a.wpg; ++s) {
+      const float2 v = gh[static_cast<size_t>(s * a.gb + g2) * kCells + c];
+      sg += v.x;
+      sh += v.y;
+    }
+    const size_t o = (static_cast<size_t>(blockIdx.x) * a.gb + g2) * kCells + c;
+    a.part_g[o] = sg;
+    a.part_h[o] = sh;
+    a.part_c[o] = cnt[static_cast<size_t>(g2) * kCells + c];
+  }
+}
+
+// out (SoA fp64 [3][d][max_bin]) = fixed-order fp64 sum of the CTA partials
+// over row segments. Thread = (bin, feature-in-slice) cell, feature fastest,
+// so partial reads are coalesced.
+__global__ void reduce_partials_kernel(HistArgs a, int nseg, int k_alloc, int d, int max_bin,
+                                       double* out) {
+  const int cells = k_alloc * 32;
+  const int group = blockIdx.y;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cells) return;
+  const int bin = c >> 5;
+  const int fl = c & 31;
+  const int f = group * 32 + fl;
+  if (f >= d || bin >= max_bin) return;
+  const int bi = group / a.gb;
+  const int gl = group - bi * a.gb;
+  double sg = 0.0, sh = 0.0;
+  uint64_t sc = 0;
+  for (int s = 0; s < nseg; ++s) {
+    const size_t cta = static_cast<size_t>(s) * a.nblocks + bi;
+    const size_t o = (cta * a.gb + gl) * cells + c;
+    sg += static_cast<double>(a.part_g[o]);
+    sh += static_cast<double>(a.part_h[o]);
+    sc += a.part_c[o];
+  }
+  const size_t D = static_cast<size_t>(d) * max_bin;
+  const size_t o = static_cast<size_t>(f) * max_bin + bin;
+  out[o] = sg;
+  out[D + o] = sh;
+  out[2 * D + o] = static_cast<double>(sc);
+}
+
+// Column-major uint8 bins -> row-major packed words at pack_feature_tuples
+// bit positions (binning.cpp:141-156): word w of a row holds features
+// w*fpw .. w*fpw+fpw-1 at bits*p. One launch covers one 32-feature slice
+// group (its words_per_slice words); pad slots are 0.
+__global__ void pack_kernel(const uint8_t* cols, int f0, int nf, int64_t n, int max_bin, int bits,
+                            int stride_words, uint32_t* packed, int* bad) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int fpw = 32 / bits;
+  const int w = f0 / fpw + blockIdx.y;
+  uint32_t word = 0;
+  for (int p = 0; p < fpw; ++p) {
+    const int fl = blockIdx.y * fpw + p;  // feature within the group
+    if (fl >= nf) break;
+    const uint32_t b = cols[static_cast<size_t>(fl) * n + r];
+    if (b >= static_cast<uint32_t>(max_bin)) atomicOr(bad, 1);
+    word |= b << (bits * p);
+  }
+  packed[static_cast<size_t>(r) * stride_words + w] = word;
+}
+
+__global__ void f64_to_f32_kernel(const double* in, float* out, int64_t n) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<float>(in[i]);
+}
+
+template <int BITS, int K>
+void set_smem_attr(int device) {
+  static std::once_flag once[64];
+  std::call_once(once[device & 63], [] {
+    HBG_CUDA(cudaFuncSetAttribute(hist_kernel<BITS, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  232448));
+  });
+}
+
+template <int BITS, int K>
+int occupancy(int threads, size_t smem, int device) {
+  set_smem_attr<BITS, K>(device);
+  int blocks = 0;
+  HBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, hist_kernel<BITS, K>, threads, smem));
+  return std::max(blocks, 1);
+}
+
+int occupancy_for(int bits, int k_alloc, int threads, size_t smem, int device) {
+  if (bits == 4) return occupancy<4, 16>(threads, smem, device);
+  if (k_alloc == 64) return occupancy<8, 64>(threads, smem, device);
+  if (k_alloc == 128) return occupancy<8, 128>(threads, smem, device);
+  return occupancy<8, 256>(threads, smem, device);
+}
+
+}  // namespace
+
+int sm_count(int device) {
+  static int cache[64] = {0};
+  int& c = cache[device & 63];
+  if (c == 0) HBG_CUDA(cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, device));
+  return c;
+}
+
+HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int device) {
+  HistPlan p{};
+  p.bits = bits;
+  p.k_alloc = bits == 4 ? 16 : (max_bin <= 64 ? 64 : (max_bin <= 128 ? 128 : 256));
+  const size_t cells = static_cast<size_t>(p.k_alloc) * 32;
+  const size_t ghw = cells * 8;   // per-warp private {g,h}
+  const size_t cntw = cells * 4;  // per-group shared counts
+  const size_t smem_max = 232448;
+  const int max_warps = 16;
+  int gb = std::min(num_groups, max_warps);
+  int warps = 0;
+  for (; gb >= 1; --gb) {
+    if (gb * cntw >= smem_max) continue;
+    warps = static_cast<int>(std::min<size_t>(max_warps, (smem_max - gb * cntw) / ghw));
+    if (warps >= gb) break;
+  }
+  require(gb >= 1 && warps >= 1, "histogram footprint exceeds shared memory");
+  p.gb = gb;
+  p.wpg = warps / gb;
+  p.warps = gb * p.wpg;
+  p.smem = p.warps * ghw + gb * cntw;
+  p.nblocks = (num_groups + gb - 1) / gb;
+  const int occ = occupancy_for(bits, p.k_alloc, p.warps * 32, p.smem, device);
+  const int64_t target = static_cast<int64_t>(sm_count(device)) * occ;
+  int64_t nseg = (target + p.nblocks - 1) / p.nblocks;
+  const int64_t min_rows = static_cast<int64_t>(p.wpg) * 32 * 2;  // >= 2 tiles per warp
+  nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, (n + min_rows - 1) / min_rows));
+  int64_t seg_len = (n + nseg - 1) / nseg;
+  seg_len = std::max<int64_t>(32, (seg_len + 31) / 32 * 32);
+  p.seg_len = seg_len;
+  p.nseg = static_cast<int>(std::max<int64_t>(1, (n + seg_len - 1) / seg_len));
+  p.ctas = p.nblocks * p.nseg;
+  p.part_values = static_cast<size_t>(p.ctas) * gb * cells;
+  return p;
+}
+
+void launch_histogram(const HistPlan& plan, const HistArgs& args, cudaStream_t s) {
+  const dim3 grid(plan.ctas), block(plan.warps * 32);
+  if (plan.bits == 4) {
+    hist_kernel<4, 16><<<grid, block, plan.smem, s>>>(args);
+  } else if (plan.k_alloc == 64) {
+    hist_kernel<8, 64><<<grid, block, plan.smem, s>>>(args);
+  } else if (plan.k_alloc == 128) {
+    hist_kernel<8, 128><<<grid, block, plan.smem, s>>>(args);
+  } else {
+    hist_kernel<8, 256><<<grid, block, plan.smem, s>>>(args);
+  }
+  HBG_LAUNCH_CHECK();
+}
+
+void launch_reduce_partials(const HistPlan& plan, const HistArgs& args, int num_features,
+                            int max_bin, double* d_hist, cudaStream_t s) {
+  const int cells = plan.k_alloc * 32;
+  const dim3 block(256), grid((cells + 255) / 256, args.num_groups);
+  reduce_partials_kernel<<<grid, block, 0, s>>>(args, plan.nseg, plan.k_alloc, num_features,
+                                                max_bin, d_hist);
+  HBG_LAUNCH_CHECK();
+}
+
+void launch_pack(const uint8_t* d_cols, int f0, int nf, int num_features, int64_t num_rows,
+                 int max_bin, int bits, int row_stride_words, uint32_t* d_packed, int* d_bad,
+                 cudaStream_t s) {
+  (void)num_features;
+  if (num_rows == 0) return;
+  const int words_per_slice = bits == 4 ? 4 : 8;  // 32 features per slice
+  const dim3 block(256), grid(static_cast<unsigned>((num_rows + 255) / 256), words_per_slice);
+  pack_kernel<<<grid, block, 0, s>>>(d_cols, f0, nf, num_rows, max_bin, bits, row_stride_words,
+                                     d_packed, d_bad);
+  HBG_LAUNCH_CHECK();
+}
+
+void launch_f64_to_f32(const double* in, float* out, int64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 4096);
+  f64_to_f32_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(in, out, n);
+  HBG_LAUNCH_CHECK();
+}
+
+}  // namespace hbg

@@ -1,0 +1,307 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (north_star / SURVEY §8c):
+  * counts bit-exact;
+  * grad/hess sums within stats_close tolerance 1e-5 (relative, floor 1,
+    histogram.cpp:12-15) of the oracle's bits64 — fp32 accumulation order
+    differs from the reference's, so sums cannot be bit-identical;
+  * split (feature, threshold_bin) identical, gains bit-identical when the scan
+    runs on the same histogram;
+  * subtracted sibling == from-scratch histogram (counts exact).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5  # fp32 accumulation vs bits64 oracle, stats_close semantics
+SEED_STEP = 0x51ED270B
+
+
+def torch_cuda():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch
+
+
+def assert_hist_close(got, want, tol=TOL):
+    assert got.shape == want.shape
+    assert (got["count"] == want["count"]).all(), "counts must be bit-exact"
+    for key in ("grad_sum", "hess_sum"):
+        a, b = got[key], want[key]
+        scale = np.maximum(1.0, np.maximum(np.abs(a), np.abs(b)))
+        err = np.abs(a - b) / scale
+        assert err.max() <= tol, (key, float(err.max()))
+
+
+def make_case(oracle, rows, d, k, depth, seed=0):
+    cols = oracle.gen_synthetic_bins(rows, d, k, seed)
+    g, h = oracle.gen_grad_hess(rows, seed)
+    idx = oracle.leaf_index_sample(rows, depth, seed + SEED_STEP * depth)
+    return cols, g, h, idx
+
+
+# --------------------------------------------------------------------- layout
+@pytest.mark.parametrize("d,k", [(1, 64), (5, 256), (28, 64), (28, 16), (33, 64), (64, 16), (70, 200), (100, 8)])
+def test_packed_layout_matches_pack_feature_tuples(hbg, oracle, d, k):
+    rows = 777
+    cols = np.random.default_rng(d * 1000 + k).integers(0, k, size=(d, rows), dtype=np.uint8)
+    bits = 4 if k <= 16 else 8
+    with hbg.Dataset(cols, k) as ds:
+        L = ds.layout()
+        assert L["bits_per_bin"] == bits
+        words = ds.packed_words()
+    want = oracle.pack_feature_tuples(cols, bits, k)  # tuple-major (T, rows)
+    assert (words == want.T).all()
+
+
+def test_dataset_rejects_bad_bins_and_shapes(hbg):
+    cols = np.full((3, 50), 64, dtype=np.uint8)
+    with pytest.raises(hbg.InvalidArgument):
+        hbg.Dataset(cols, 64)  # bin 64 >= max_bin
+    with pytest.raises(hbg.InvalidArgument):
+        hbg.Dataset(cols, 300)
+    with pytest.raises(hbg.InvalidArgument):
+        hbg.Dataset(cols, 1)
+
+
+# ----------------------------------------------------------- histogram parity
+@pytest.mark.parametrize("k,d", [(64, 28), (16, 28), (256, 37), (64, 1), (16, 70), (64, 100), (128, 33), (2, 5)])
+@pytest.mark.parametrize("depth", [0, 2, 5, 8])
+def test_host_dropin_matches_oracle(hbg, oracle, k, d, depth):
+    rows = 50000
+    cols, g, h, idx = make_case(oracle, rows, d, k, depth, seed=d + k)
+    leaf = hbg.gather_leaf_statistics(idx, g, h)
+    with hbg.Dataset(cols, k) as ds:
+        got = hbg.build_histograms_partitioned(ds, leaf)
+    want = oracle.build_histograms(cols, k, idx, leaf.gradients, leaf.hessians, 64)
+    assert_hist_close(got, want)
+
+
+def test_matches_reference_golden_histograms(hbg, oracle):
+    """The committed outputs of the unmodified reference (bits64), not just the oracle."""
+    import os
+
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_histograms.npz"))
+    for k, rows, d in ((64, 70000, 28), (16, 9000, 28), (256, 5000, 37), (64, 3000, 1)):
+        cols = oracle.gen_synthetic_bins(rows, d, k, 11)
+        g, h = oracle.gen_grad_hess(rows, 11)
+        with hbg.Dataset(cols, k) as ds:
+            for depth in (0, 3):
+                tag = f"k{k}_r{rows}_d{d}_D{depth}"
+                idx = z[f"{tag}_idx"]
+                got = hbg.build_histograms_partitioned(ds, hbg.LeafState(idx, g[idx], h[idx]))
+                assert_hist_close(got, z[f"{tag}_h64"])
+                # and within the reference's own bits32 tolerance of its bits32 output
+                assert_hist_close(got, z[f"{tag}_h32"], tol=1e-4)
+
+
+def test_edge_cases(hbg, oracle):
+    rng = np.random.default_rng(3)
+    cols = rng.integers(0, 64, size=(28, 1000), dtype=np.uint8)
+    cols[3, :] = 63  # constant max bin (the paper's constant-bin worst case)
+    cols[4, :] = 0
+    with hbg.Dataset(cols, 64) as ds:
+        # empty leaf -> all zero (test_histogram.cpp:83-94)
+        empty = hbg.build_histograms_partitioned(ds, hbg.LeafState(np.zeros(0, np.int32), np.zeros(0), np.zeros(0)))
+        assert (empty["count"] == 0).all() and (empty["grad_sum"] == 0).all()
+        for n in (1, 2, 31, 32, 33, 63, 65, 999):
+            idx = np.sort(rng.choice(1000, n, replace=False)).astype(np.int32)
+            g = rng.normal(size=n)
+            h = 0.1 + rng.random(n)
+            got = hbg.build_histograms_partitioned(ds, hbg.LeafState(idx, g, h))
+            want = oracle.build_histograms(cols, 64, idx, g, h, 64)
+            assert_hist_close(got, want)
+            assert got["count"][3, 63] == n and got["count"][4, 0] == n
+
+
+def test_unsorted_and_duplicate_free_indices(hbg, oracle):
+    """Leaf order only changes fp32 rounding; counts stay exact."""
+    rng = np.random.default_rng(9)
+    cols = rng.integers(0, 16, size=(9, 20000), dtype=np.uint8)
+    idx = rng.permutation(20000)[:7000].astype(np.int32)
+    g = rng.normal(size=7000)
+    h = rng.random(7000)
+    with hbg.Dataset(cols, 16) as ds:
+        got = hbg.build_histograms_partitioned(ds, hbg.LeafState(idx, g, h))
+    assert_hist_close(got, oracle.build_histograms(cols, 16, idx, g, h, 64))
+
+
+def test_deterministic_across_calls(hbg, oracle):
+    cols, g, h, idx = make_case(oracle, 300000, 28, 64, 1, seed=5)
+    leaf = hbg.gather_leaf_statistics(idx, g, h)
+    with hbg.Dataset(cols, 64) as ds:
+        a = hbg.build_histograms_partitioned(ds, leaf)
+        b = hbg.build_histograms_partitioned(ds, leaf)
+    assert a.tobytes() == b.tobytes()
+
+
+# --------------------------------------------------------------- device paths
+def test_device_row_indexed_and_leaf_aligned_agree(hbg, oracle):
+    torch = torch_cuda()
+    rows, d, k = 200000, 28, 64
+    cols, g, h, idx = make_case(oracle, rows, d, k, 3, seed=1)
+    dev = torch.device("cuda:0")
+    with hbg.Dataset(cols, k) as ds:
+        ti = torch.from_numpy(idx).to(dev)
+        tg = torch.from_numpy(g.astype(np.float32)).to(dev)
+        th = torch.from_numpy(h.astype(np.float32)).to(dev)
+        n = len(idx)
+        lg = torch.empty(n, dtype=torch.float32, device=dev)
+        lh = torch.empty(n, dtype=torch.float32, device=dev)
+        tot = torch.empty(2, dtype=torch.float64, device=dev)
+        s = torch.cuda.current_stream().cuda_stream
+        hbg.gather_leaf_device(ti, n, tg, th, lg, lh, tot, s)
+        h1 = torch.empty(ds.hist_values(), dtype=torch.float64, device=dev)
+        h2 = torch.empty_like(h1)
+        ds.build_histograms_device(ti, n, lg, lh, h1, hbg.HBG_GH_LEAF_ALIGNED, s)
+        ds.build_histograms_device(ti, n, tg, th, h2, hbg.HBG_GH_ROW_INDEXED, s)
+        bins = torch.empty(d * k * 3, dtype=torch.float64, device=dev)
+        hbg.hist_to_bins_device(h1, d, k, bins, s)
+        torch.cuda.synchronize()
+        got = bins.cpu().numpy().view(hbg.BIN_DTYPE).reshape(d, k)
+    assert torch.equal(h1, h2)  # same fp32 values, same order
+    assert torch.equal(lg.cpu(), torch.from_numpy(g[idx].astype(np.float32)))
+    want = oracle.build_histograms(cols, k, idx, g[idx], h[idx], 64)
+    assert_hist_close(got, want)
+    gt, ht = tot.cpu().numpy()
+    assert abs(gt - g[idx].astype(np.float32).astype(np.float64).sum()) <= 1e-9 * max(1, abs(gt))
+    assert abs(ht - h[idx].astype(np.float32).astype(np.float64).sum()) <= 1e-9 * max(1, abs(ht))
+
+
+def test_identity_leaf_device(hbg, oracle):
+    torch = torch_cuda()
+    rows, d, k = 100003, 40, 16
+    cols = oracle.gen_synthetic_bins(rows, d, k, 2)
+    g, h = oracle.gen_grad_hess(rows, 2)
+    dev = torch.device("cuda:0")
+    with hbg.Dataset(cols, k) as ds:
+        tg = torch.from_numpy(g.astype(np.float32)).to(dev)
+        th = torch.from_numpy(h.astype(np.float32)).to(dev)
+        out = torch.empty(ds.hist_values(), dtype=torch.float64, device=dev)
+        ds.build_histograms_device(None, rows, tg, th, out, hbg.HBG_GH_LEAF_ALIGNED,
+                                   torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        o = out.cpu().numpy().reshape(3, d, k)
+    want = oracle.build_histograms(cols, k, np.arange(rows, dtype=np.int32), g, h, 64)
+    got = np.zeros((d, k), dtype=hbg.BIN_DTYPE)
+    got["grad_sum"], got["hess_sum"], got["count"] = o[0], o[1], o[2].astype(np.int64)
+    assert_hist_close(got, want)
+
+
+# --------------------------------------------------------------- subtraction
+def test_subtraction_equals_from_scratch_sibling(hbg, oracle):
+    torch = torch_cuda()
+    rows, d, k = 120000, 28, 64
+    cols = oracle.gen_synthetic_bins(rows, d, k, 4)
+    g, h = oracle.gen_grad_hess(rows, 4)
+    parent = oracle.leaf_index_sample(rows, 1, 77)
+    left, right = oracle.partition_leaf(parent, cols[7], 30)
+    dev = torch.device("cuda:0")
+    with hbg.Dataset(cols, k) as ds:
+        tg = torch.from_numpy(g.astype(np.float32)).to(dev)
+        th = torch.from_numpy(h.astype(np.float32)).to(dev)
+        s = torch.cuda.current_stream().cuda_stream
+        hists = {}
+        for name, ix in (("parent", parent), ("small", left if len(left) < len(right) else right)):
+            t = torch.from_numpy(ix).to(dev)
+            hists[name] = torch.empty(ds.hist_values(), dtype=torch.float64, device=dev)
+            ds.build_histograms_device(t, len(ix), tg, th, hists[name], hbg.HBG_GH_ROW_INDEXED, s)
+        sib = torch.empty_like(hists["parent"])
+        hbg.subtract_device(hists["parent"], hists["small"], sib, ds.hist_values(), s)
+        torch.cuda.synchronize()
+        o = sib.cpu().numpy().reshape(3, d, k)
+    big = right if len(left) < len(right) else left
+    want = oracle.build_histograms(cols, k, big, g[big], h[big], 64)
+    got = np.zeros((d, k), dtype=hbg.BIN_DTYPE)
+    got["grad_sum"], got["hess_sum"], got["count"] = o[0], o[1], o[2].astype(np.int64)
+    assert_hist_close(got, want)
+
+
+# --------------------------------------------------------------- split scan
+def _hist(rows, dtype):
+    out = np.zeros(len(rows), dtype=dtype)
+    for i, r in enumerate(rows):
+        out[i] = tuple(r)
+    return out
+
+
+def test_split_scan_known_answers(hbg):
+    """test_tree.cpp:84-136 through the GPU scan."""
+    H = _hist([[1.0, 1.0, 2], [-3.0, 1.0, 3], [2.0, 1.0, 3], [0.0, 1.0, 2]], hbg.BIN_DTYPE)
+    tot = (0.0, 4.0, 10)
+    s = hbg.find_best_threshold(H, 0, tot, 1, 1.0)
+    assert s["threshold_bin"] == 1 and s["gain"] == pytest.approx(8 / 3, rel=1e-15)
+    assert s["left_count"] == 5 and s["right_count"] == 5 and s["left_grad"] == -2.0
+    assert hbg.find_best_threshold(H, 0, tot, 5, 1.0)["threshold_bin"] == 1
+    assert hbg.find_best_threshold(H, 0, tot, 6, 1.0) is None
+    T = _hist([[1.0, 1.0, 1], [-1.0, 1.0, 1], [-1.0, 1.0, 1], [1.0, 1.0, 1]], hbg.BIN_DTYPE)
+    s = hbg.find_best_threshold(T, 0, (0.0, 4.0, 4), 1, 1.0)
+    assert s["threshold_bin"] == 0 and s["gain"] == pytest.approx(0.75, rel=1e-15)
+    N = _hist([[1.0, 1.0, 5], [1.0, 1.0, 5]], hbg.BIN_DTYPE)
+    assert hbg.find_best_threshold(N, 0, (2.0, 2.0, 10), 1, 0.0) is None
+
+
+@pytest.mark.parametrize("d,k,min_data,lam", [(28, 64, 1, 0.0), (2000, 64, 20, 1.0), (968, 256, 1, 0.0),
+                                              (28, 16, 100, 0.5), (3, 4, 1, 0.0)])
+def test_split_scan_bit_identical_to_oracle(hbg, oracle, d, k, min_data, lam):
+    rng = np.random.default_rng(d + k)
+    hist = np.zeros((d, k), dtype=hbg.BIN_DTYPE)
+    hist["count"] = rng.integers(0, 50, size=(d, k))
+    hist["grad_sum"] = rng.normal(size=(d, k)) * hist["count"]
+    hist["hess_sum"] = rng.random((d, k)) * hist["count"]
+    gt = float(hist["grad_sum"][0].sum())
+    ht = float(hist["hess_sum"][0].sum())
+    n = int(hist["count"][0].sum())
+    got = hbg.find_best_split(hist, (gt, ht, n), min_data, lam)
+    want = oracle.find_best_split(hist.view(oracle.BIN_DTYPE), gt, ht, n, min_data, lam)
+    assert (got is None) == (want is None)
+    if got is not None:
+        assert got.tobytes() == want.tobytes()
+
+
+def test_split_on_gpu_histogram_matches_oracle_split(hbg, oracle):
+    """End to end: device histogram -> device scan picks the oracle's (feature, bin)."""
+    rows, d, k = 400000, 28, 64
+    cols, g, h, idx = make_case(oracle, rows, d, k, 1, seed=12)
+    # plant signal so the best split is unambiguous
+    g = g + 0.5 * (cols[9].astype(np.float64) > 40)
+    leaf = hbg.gather_leaf_statistics(idx, g, h)
+    with hbg.Dataset(cols, k) as ds:
+        got_h = hbg.build_histograms_partitioned(ds, leaf)
+    tot = (leaf.grad_total, leaf.hess_total, leaf.count())
+    s_gpu = hbg.find_best_split(got_h, tot, 1, 0.0)
+    want_h = oracle.build_histograms(cols, k, idx, leaf.gradients, leaf.hessians, 64)
+    s_ref = oracle.find_best_split(want_h, *tot, 1, 0.0)
+    assert (s_gpu["feature"], s_gpu["threshold_bin"]) == (s_ref["feature"], s_ref["threshold_bin"])
+    assert s_gpu["left_count"] == s_ref["left_count"]
+    assert s_gpu["gain"] == pytest.approx(s_ref["gain"], rel=1e-6)
+
+
+# ------------------------------------------------- full size (BASELINE config)
+@pytest.mark.parametrize("k", [64, 16])
+def test_full_size_higgs_root_properties(hbg, oracle, k):
+    """10.5M x 28 (BASELINE configs[1]): oracle parity at the root plus
+    size-independent properties (every feature's counts sum to the leaf size,
+    bin sums add up to the leaf totals)."""
+    torch = torch_cuda()
+    rows, d = 10_500_000, 28
+    cols = oracle.gen_synthetic_bins(rows, d, k, 0)
+    g, h = oracle.gen_grad_hess(rows, 0)
+    dev = torch.device("cuda:0")
+    with hbg.Dataset(cols, k) as ds:
+        tg = torch.from_numpy(g.astype(np.float32)).to(dev)
+        th = torch.from_numpy(h.astype(np.float32)).to(dev)
+        out = torch.empty(ds.hist_values(), dtype=torch.float64, device=dev)
+        ds.build_histograms_device(None, rows, tg, th, out, hbg.HBG_GH_LEAF_ALIGNED,
+                                   torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        o = out.cpu().numpy().reshape(3, d, k)
+    assert (o[2].sum(axis=1) == rows).all()
+    gsum = g.astype(np.float32).astype(np.float64).sum()
+    assert np.allclose(o[0].sum(axis=1), gsum, rtol=0, atol=1e-6 * rows ** 0.5 + 1e-3)
+    got = np.zeros((d, k), dtype=hbg.BIN_DTYPE)
+    got["grad_sum"], got["hess_sum"], got["count"] = o[0], o[1], o[2].astype(np.int64)
+    want = oracle.build_histograms(cols, k, np.arange(rows, dtype=np.int32), g, h, 64)
+    assert_hist_close(got, want)
