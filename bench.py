@@ -239,7 +239,10 @@ def run_hbg(args):
     tg = torch.from_numpy(g.astype(np.float32)).to(dev)
     th = torch.from_numpy(h.astype(np.float32)).to(dev)
     hist = torch.empty(ds.hist_values(), dtype=torch.float64, device=dev)
-    stream = torch.cuda.current_stream()
+    # A real (non-default) stream: the C ABI maps a NULL stream to the handle's
+    # own stream, and the CUDA events must sit on the stream the kernels run on.
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
     sp = stream.cuda_stream
 
     def step():

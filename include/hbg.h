@@ -2,7 +2,7 @@
  * hbg.h — C ABI of the B200-native feature-histogram path (arXiv 1706.08359 hot path).
  *
  * Plain C types only (no torch / CUDA types in the signatures; streams are
- * passed as `void*` holding a cudaStream_t, NULL = the handle's own stream).
+ * passed as `void*` holding a cudaStream_t, NULL = the legacy default stream).
  * Every entry point returns an HBG_* status; on failure hbg_last_error()
  * returns a message (thread-local), mirroring the reference's exceptions.
  *

@@ -115,9 +115,10 @@ namespace {
 
 void check_ds(const hbg_dataset* ds) { require(ds != nullptr, "null dataset handle"); }
 
-cudaStream_t pick(hbg_dataset* ds, void* stream) {
-  return stream ? static_cast<cudaStream_t>(stream) : ds->stream;
-}
+// Device entry points run on the caller's stream; NULL is the CUDA legacy
+// default stream (as everywhere in CUDA). The handle's own stream serves only
+// the synchronous host drop-in.
+cudaStream_t pick(hbg_dataset*, void* stream) { return static_cast<cudaStream_t>(stream); }
 
 void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const float* d_g,
                   const float* d_h, int gh_mode, double* d_hist, cudaStream_t s) {

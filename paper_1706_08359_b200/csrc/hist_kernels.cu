@@ -137,48 +137,64 @@ __global__ void __launch_bounds__(512) hist_kernel(HistArgs a) {
     const unsigned char* base = a.packed + static_cast<size_t>(group) * Slice<BITS>::kWords * 4;
     const int64_t step = static_cast<int64_t>(a.wpg) * 32;
 
-    auto fetch = [&](int64_t t, TileIn& in, Slice<BITS>& sl) {
+    // Two-stage software pipeline, so no load waits on another load in the
+    // same iteration (issue is in order): stage A fetches the leaf entries
+    // (row id, g, h) of tile t+2s, stage B fetches the packed slice of tile
+    // t+s using the row ids stage A delivered one iteration earlier, and the
+    // update loop consumes tile t.
+    auto fetch_entry = [&](int64_t t, TileIn& in) {
       const int64_t pos = t + lane;
       if (pos < s1) {
         const int64_t row = a.idx ? static_cast<int64_t>(__ldg(a.idx + pos)) : pos;
-        const int64_t gi = a.gh_indexed ? row : pos;
         in.row = row;
-        in.g = __ldg(a.g + gi);
-        in.h = __ldg(a.h + gi);
-        load_slice<BITS>(base + row * a.row_stride, sl);
+        if (!a.gh_indexed) {
+          in.g = __ldg(a.g + pos);
+          in.h = __ldg(a.h + pos);
+        }
       } else {
         in.row = -1;
         in.g = 0.f;
         in.h = 0.f;
+      }
+    };
+    auto fetch_slice = [&](TileIn& in, Slice<BITS>& sl) {
+      if (in.row >= 0) {
+        if (a.gh_indexed) {
+          in.g = __ldg(a.g + in.row);
+          in.h = __ldg(a.h + in.row);
+        }
+        load_slice<BITS>(base + in.row * a.row_stride, sl);
+      } else {
 #pragma unroll
         for (int j = 0; j < Slice<BITS>::kWords; ++j) sl.w[j] = 0;
       }
     };
 
     int64_t t = s0 + static_cast<int64_t>(sub) * 32;
-    TileIn cur_in;
+    TileIn e0, e1;
     Slice<BITS> cur;
-    if (t < s1) fetch(t, cur_in, cur);
+    fetch_entry(t, e0);
+    fetch_entry(t + step, e1);
+    fetch_slice(e0, cur);
     for (; t < s1; t += step) {
-      TileIn nxt_in;
+      TileIn e2;
       Slice<BITS> nxt;
-      const bool more = t + step < s1;
-      if (more) fetch(t + step, nxt_in, nxt);
+      fetch_entry(t + 2 * step, e2);  // stage A (t + 2s)
+      fetch_slice(e1, nxt);           // stage B (t + s)
       rotate_slice<BITS>(cur, lane);
       if (t + 32 <= s1) {
 #pragma unroll
         for (int p = 0; p < 32; ++p)
-          update_step<BITS, K>(cur, p, lane, gh_base, cnt_g, cur_in.g, cur_in.h);
+          update_step<BITS, K>(cur, p, lane, gh_base, cnt_g, e0.g, e0.h);
       } else {
-        const bool valid = cur_in.row >= 0;
+        const bool valid = e0.row >= 0;
 #pragma unroll
         for (int p = 0; p < 32; ++p)
-          if (valid) update_step<BITS, K>(cur, p, lane, gh_base, cnt_g, cur_in.g, cur_in.h);
+          if (valid) update_step<BITS, K>(cur, p, lane, gh_base, cnt_g, e0.g, e0.h);
       }
-      if (more) {
-        cur_in = nxt_in;
-        cur = nxt;
-      }
+      e0 = e1;
+      e1 = e2;
+      cur = nxt;
     }
   }
   __syncthreads();
