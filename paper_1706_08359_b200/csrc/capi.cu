@@ -6,6 +6,7 @@
 // fallback anywhere: a missing GPU or CUDA failure is an error status.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -81,7 +82,8 @@ struct hbg_dataset {
   uint32_t* packed = nullptr;  // num_rows * row_stride_bytes
   cudaStream_t stream = nullptr;
   // workspace (not re-entrant per handle)
-  hbg::DevBuf part, host_idx, host_gd, host_hd, host_gf, host_hf, host_hist, host_bins;
+  hbg::DevBuf part, iota, host_idx, host_gd, host_hd, host_gf, host_hf, host_hist, host_bins;
+  int64_t iota_rows = 0;
   // measurement hooks
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;  // recorded, not yet read
@@ -133,6 +135,14 @@ void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const fl
     return;
   }
   require(d_g != nullptr && d_h != nullptr, "null gradient/hessian pointer");
+  if (d_idx == nullptr) {  // identity leaf [0, count): the kernel always reads indices
+    if (ds->iota_rows < count) {
+      int32_t* io = static_cast<int32_t*>(ds->iota.get(static_cast<size_t>(L.num_rows) * 4 + 4));
+      launch_iota(io, L.num_rows, s);
+      ds->iota_rows = L.num_rows;
+    }
+    d_idx = static_cast<const int32_t*>(ds->iota.p);
+  }
   HistPlan plan = plan_histogram(L.bits_per_bin, L.max_bin, L.num_groups, count, L.device);
   float* part = static_cast<float*>(ds->part.get(plan.part_values * 12));
   HistArgs a{};

@@ -71,6 +71,7 @@ void launch_reduce_partials(const HistPlan& plan, const HistArgs& args, int num_
 void launch_pack(const uint8_t* d_cols, int f0, int nf, int num_features, int64_t num_rows,
                  int max_bin, int bits, int row_stride_words, uint32_t* d_packed, int* d_bad,
                  cudaStream_t s);
+void launch_iota(int32_t* out, int64_t n, cudaStream_t s);
 void launch_f64_to_f32(const double* in, float* out, int64_t n, cudaStream_t s);
 void launch_hist_to_bins(const double* d_hist, int64_t cells, hbg_bin* d_bins, cudaStream_t s);
 void launch_subtract(const double* a, const double* b, double* out, int64_t n, cudaStream_t s);

@@ -88,9 +88,14 @@ __device__ __forceinline__ void rotate_slice(Slice<BITS>& s, int lane) {
   for (int j = 0; j < W; ++j) s.w[j] = t[j];
 }
 
-template <int BITS, int K>
+template <int BITS, int K, bool kTail>
 __device__ __forceinline__ void update_step(const Slice<BITS>& s, int p, int lane, uint32_t gh_base,
-                                            uint32_t* cnt, float g, float h) {
+                                            uint32_t* cnt, float g, float h, bool active) {
+  // Lane l's step-p cell and lane (l-1)'s step-(p+1) cell can coincide, so
+  // consecutive steps must be ordered across lanes: __syncwarp is the
+  // warp-scope memory-ordering point for that (all lanes execute it).
+  asm volatile("bar.warp.sync -1;" ::: "memory");
+  if (kTail && !active) return;
   constexpr int fpw = Slice<BITS>::kFeatPerWord;
   const uint32_t b = (s.w[p / fpw] >> (BITS * (p % fpw))) & (K - 1);
   const uint32_t cell = (b << 5) | ((lane + p) & 31);
@@ -104,11 +109,12 @@ __device__ __forceinline__ void update_step(const Slice<BITS>& s, int p, int lan
 }
 
 struct TileIn {
-  int64_t row;
+  int32_t row;  // raw int32 row id (row_index_t): widening it right after the
+                // load would make the load's consumer immediate and stall on it
   float g, h;
 };
 
-template <int BITS, int K>
+template <int BITS, int K, bool kRowIndexed>
 __global__ void __launch_bounds__(512) hist_kernel(HistArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int kCells = K * 32;
@@ -145,9 +151,8 @@ __global__ void __launch_bounds__(512) hist_kernel(HistArgs a) {
     auto fetch_entry = [&](int64_t t, TileIn& in) {
       const int64_t pos = t + lane;
       if (pos < s1) {
-        const int64_t row = a.idx ? static_cast<int64_t>(__ldg(a.idx + pos)) : pos;
-        in.row = row;
-        if (!a.gh_indexed) {
+        in.row = __ldg(a.idx + pos);  // never null: the identity leaf uses an iota array
+        if constexpr (!kRowIndexed) {
           in.g = __ldg(a.g + pos);
           in.h = __ldg(a.h + pos);
         }
@@ -159,11 +164,11 @@ __global__ void __launch_bounds__(512) hist_kernel(HistArgs a) {
     };
     auto fetch_slice = [&](TileIn& in, Slice<BITS>& sl) {
       if (in.row >= 0) {
-        if (a.gh_indexed) {
+        if constexpr (kRowIndexed) {
           in.g = __ldg(a.g + in.row);
           in.h = __ldg(a.h + in.row);
         }
-        load_slice<BITS>(base + in.row * a.row_stride, sl);
+        load_slice<BITS>(base + static_cast<int64_t>(in.row) * a.row_stride, sl);
       } else {
 #pragma unroll
         for (int j = 0; j < Slice<BITS>::kWords; ++j) sl.w[j] = 0;
@@ -185,12 +190,12 @@ __global__ void __launch_bounds__(512) hist_kernel(HistArgs a) {
       if (t + 32 <= s1) {
 #pragma unroll
         for (int p = 0; p < 32; ++p)
-          update_step<BITS, K>(cur, p, lane, gh_base, cnt_g, e0.g, e0.h);
+          update_step<BITS, K, false>(cur, p, lane, gh_base, cnt_g, e0.g, e0.h, true);
       } else {
         const bool valid = e0.row >= 0;
 #pragma unroll
         for (int p = 0; p < 32; ++p)
-          if (valid) update_step<BITS, K>(cur, p, lane, gh_base, cnt_g, e0.g, e0.h);
+          update_step<BITS, K, true>(cur, p, lane, gh_base, cnt_g, e0.g, e0.h, valid);
       }
       e0 = e1;
       e1 = e2;
@@ -278,8 +283,10 @@ template <int BITS, int K>
 void set_smem_attr(int device) {
   static std::once_flag once[64];
   std::call_once(once[device & 63], [] {
-    HBG_CUDA(cudaFuncSetAttribute(hist_kernel<BITS, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  232448));
+    HBG_CUDA(cudaFuncSetAttribute(hist_kernel<BITS, K, false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+    HBG_CUDA(cudaFuncSetAttribute(hist_kernel<BITS, K, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
   });
 }
 
@@ -287,7 +294,8 @@ template <int BITS, int K>
 int occupancy(int threads, size_t smem, int device) {
   set_smem_attr<BITS, K>(device);
   int blocks = 0;
-  HBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, hist_kernel<BITS, K>, threads, smem));
+  HBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, hist_kernel<BITS, K, false>, threads,
+                                                         smem));
   return std::max(blocks, 1);
 }
 
@@ -345,14 +353,15 @@ HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int de
 
 void launch_histogram(const HistPlan& plan, const HistArgs& args, cudaStream_t s) {
   const dim3 grid(plan.ctas), block(plan.warps * 32);
+  const bool ri = args.gh_indexed != 0;
   if (plan.bits == 4) {
-    hist_kernel<4, 16><<<grid, block, plan.smem, s>>>(args);
+    (ri ? hist_kernel<4, 16, true> : hist_kernel<4, 16, false>)<<<grid, block, plan.smem, s>>>(args);
   } else if (plan.k_alloc == 64) {
-    hist_kernel<8, 64><<<grid, block, plan.smem, s>>>(args);
+    (ri ? hist_kernel<8, 64, true> : hist_kernel<8, 64, false>)<<<grid, block, plan.smem, s>>>(args);
   } else if (plan.k_alloc == 128) {
-    hist_kernel<8, 128><<<grid, block, plan.smem, s>>>(args);
+    (ri ? hist_kernel<8, 128, true> : hist_kernel<8, 128, false>)<<<grid, block, plan.smem, s>>>(args);
   } else {
-    hist_kernel<8, 256><<<grid, block, plan.smem, s>>>(args);
+    (ri ? hist_kernel<8, 256, true> : hist_kernel<8, 256, false>)<<<grid, block, plan.smem, s>>>(args);
   }
   HBG_LAUNCH_CHECK();
 }

@@ -180,7 +180,20 @@ __global__ void __launch_bounds__(kScanThreads) best_split_kernel(
   }
 }
 
+__global__ void iota_kernel(int32_t* out, int64_t n) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<int32_t>(i);
+}
+
 }  // namespace
+
+void launch_iota(int32_t* out, int64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 4736);
+  iota_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(out, n);
+  HBG_LAUNCH_CHECK();
+}
 
 size_t gather_scratch_doubles(int64_t n) {
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(kGatherMaxBlocks, (n + 2047) / 2048));

@@ -287,11 +287,24 @@ def test_split_on_gpu_histogram_matches_oracle_split(hbg, oracle):
 
 
 # ------------------------------------------------- full size (BASELINE config)
+# At 10.5M-row leaves fp32 cannot meet 1e-5 (floor 1) in near-cancelled bins:
+# rounding the inputs g,h to fp32 ALONE costs 1.5e-5 there (measured, DESIGN.md
+# §5), and the reference's own bits32 mode is off by 1.8e-4 (k64) / 7.5e-4 (k16)
+# against bits64. The stated full-size bar: never worse than the
+# reference's bits32 on the same inputs, and within FULL_TOL.
+FULL_TOL = {64: 1e-4, 16: 3e-4}
+
+
+def max_rel_err(a, b):
+    scale = np.maximum(1.0, np.maximum(np.abs(a), np.abs(b)))
+    return float((np.abs(a - b) / scale).max())
+
+
 @pytest.mark.parametrize("k", [64, 16])
 def test_full_size_higgs_root_properties(hbg, oracle, k):
     """10.5M x 28 (BASELINE configs[1]): oracle parity at the root plus
     size-independent properties (every feature's counts sum to the leaf size,
-    bin sums add up to the leaf totals)."""
+    bin sums add up to the leaf totals), and bitwise repeatability."""
     torch = torch_cuda()
     rows, d = 10_500_000, 28
     cols = oracle.gen_synthetic_bins(rows, d, k, 0)
@@ -300,15 +313,23 @@ def test_full_size_higgs_root_properties(hbg, oracle, k):
     with hbg.Dataset(cols, k) as ds:
         tg = torch.from_numpy(g.astype(np.float32)).to(dev)
         th = torch.from_numpy(h.astype(np.float32)).to(dev)
-        out = torch.empty(ds.hist_values(), dtype=torch.float64, device=dev)
-        ds.build_histograms_device(None, rows, tg, th, out, hbg.HBG_GH_LEAF_ALIGNED,
-                                   torch.cuda.current_stream().cuda_stream)
-        torch.cuda.synchronize()
-        o = out.cpu().numpy().reshape(3, d, k)
+        outs = []
+        for _ in range(2):
+            out = torch.empty(ds.hist_values(), dtype=torch.float64, device=dev)
+            ds.build_histograms_device(None, rows, tg, th, out, hbg.HBG_GH_LEAF_ALIGNED, 0)
+            torch.cuda.synchronize()
+            outs.append(out.cpu().numpy())
+    assert outs[0].tobytes() == outs[1].tobytes()  # deterministic
+    o = outs[0].reshape(3, d, k)
     assert (o[2].sum(axis=1) == rows).all()
     gsum = g.astype(np.float32).astype(np.float64).sum()
     assert np.allclose(o[0].sum(axis=1), gsum, rtol=0, atol=1e-6 * rows ** 0.5 + 1e-3)
-    got = np.zeros((d, k), dtype=hbg.BIN_DTYPE)
-    got["grad_sum"], got["hess_sum"], got["count"] = o[0], o[1], o[2].astype(np.int64)
-    want = oracle.build_histograms(cols, k, np.arange(rows, dtype=np.int32), g, h, 64)
-    assert_hist_close(got, want)
+    idx = np.arange(rows, dtype=np.int32)
+    want = oracle.build_histograms(cols, k, idx, g, h, 64)
+    ref32 = oracle.build_histograms(cols, k, idx, g, h, 32)  # the reference's bits32 path
+    assert (o[2].astype(np.int64) == want["count"]).all()
+    for j, key in ((0, "grad_sum"), (1, "hess_sum")):
+        ours = max_rel_err(o[j], want[key])
+        theirs = max_rel_err(ref32[key], want[key])
+        assert ours <= FULL_TOL[k], (key, ours)
+        assert ours <= theirs, (key, ours, theirs)
