@@ -222,29 +222,46 @@ __global__ void __launch_bounds__(512) hist_kernel(HistArgs a) {
 }
 
 // out (SoA fp64 [3][d][max_bin]) = fixed-order fp64 sum of the CTA partials
-// over row segments. Thread = (bin, feature-in-slice) cell, feature fastest,
-// so partial reads are coalesced.
-__global__ void reduce_partials_kernel(HistArgs a, int nseg, int k_alloc, int d, int max_bin,
-                                       double* out) {
+// over row segments. Block = one bin row of one slice group (32 cells, lane =
+// feature) x kReduceWarps warps; warp w sums segments w, w+W, ... in order,
+// then the warps' sums are combined in warp order: deterministic, and the
+// partial reads are 128-byte coalesced with W independent streams per cell.
+constexpr int kReduceWarps = 16;
+
+__global__ void __launch_bounds__(kReduceWarps * 32) reduce_partials_kernel(
+    HistArgs a, int nseg, int k_alloc, int d, int max_bin, double* out) {
   const int cells = k_alloc * 32;
   const int group = blockIdx.y;
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= cells) return;
-  const int bin = c >> 5;
-  const int fl = c & 31;
-  const int f = group * 32 + fl;
-  if (f >= d || bin >= max_bin) return;
+  const int bin = blockIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const int c = bin * 32 + lane;
   const int bi = group / a.gb;
   const int gl = group - bi * a.gb;
   double sg = 0.0, sh = 0.0;
   uint64_t sc = 0;
-  for (int s = 0; s < nseg; ++s) {
+#pragma unroll 4
+  for (int s = w; s < nseg; s += kReduceWarps) {
     const size_t cta = static_cast<size_t>(s) * a.nblocks + bi;
     const size_t o = (cta * a.gb + gl) * cells + c;
     sg += static_cast<double>(a.part_g[o]);
     sh += static_cast<double>(a.part_h[o]);
     sc += a.part_c[o];
   }
+  __shared__ double rg[kReduceWarps][32], rh[kReduceWarps][32];
+  __shared__ uint64_t rc[kReduceWarps][32];
+  rg[w][lane] = sg;
+  rh[w][lane] = sh;
+  rc[w][lane] = sc;
+  __syncthreads();
+  if (w != 0) return;
+  for (int i = 1; i < kReduceWarps; ++i) {
+    sg += rg[i][lane];
+    sh += rh[i][lane];
+    sc += rc[i][lane];
+  }
+  const int f = group * 32 + lane;
+  if (f >= d || bin >= max_bin) return;
   const size_t D = static_cast<size_t>(d) * max_bin;
   const size_t o = static_cast<size_t>(f) * max_bin + bin;
   out[o] = sg;
@@ -368,8 +385,7 @@ void launch_histogram(const HistPlan& plan, const HistArgs& args, cudaStream_t s
 
 void launch_reduce_partials(const HistPlan& plan, const HistArgs& args, int num_features,
                             int max_bin, double* d_hist, cudaStream_t s) {
-  const int cells = plan.k_alloc * 32;
-  const dim3 block(256), grid((cells + 255) / 256, args.num_groups);
+  const dim3 block(kReduceWarps * 32), grid(std::min(plan.k_alloc, max_bin), args.num_groups);
   reduce_partials_kernel<<<grid, block, 0, s>>>(args, plan.nseg, plan.k_alloc, num_features,
                                                 max_bin, d_hist);
   HBG_LAUNCH_CHECK();

@@ -3,12 +3,16 @@
 // test_tree.cpp:264-299 ("the lock-step backend grows the same tree as the
 // partitioned one") for a `cuda` backend: histograms from
 // build_histograms_cuda vs build_histograms_partitioned(bits64) under the
-// reference's histograms_equivalent (counts exact, stats within 1e-5), and
-// the same find_best_threshold winner per leaf.
+// reference's histograms_equivalent at stats_tolerance(bits32) = 1e-4 — the
+// bar the reference applies to its own fp32 path (acceptance.cpp:204-223) —
+// with exact counts, the max deviation printed, and the same
+// find_best_threshold winner per leaf.
 //
 // Built here by oracle/Makefile against /root/reference (headers + objects)
 // into oracle/_ref/backend_swap, which travels to the GPU box; run by
 // tests/test_gpu_backend_swap.py.
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <optional>
 #include <random>
@@ -35,8 +39,17 @@ int main() {
       HistogramSet want = build_histograms_partitioned(data, leaf, PrecisionMode::bits64);
       HistogramSet got = hbg::histoboost_backend::build_histograms_cuda(dev, leaf, PrecisionMode::bits32);
       bool ok = got.size() == want.size();
+      double worst = 0.0;
       for (std::size_t f = 0; ok && f < want.size(); ++f) {
-        ok = got[f].feature_id == want[f].feature_id && histograms_equivalent(got[f], want[f], 1e-5);
+        ok = got[f].feature_id == want[f].feature_id &&
+             histograms_equivalent(got[f], want[f], stats_tolerance(PrecisionMode::bits32));
+        for (std::size_t b = 0; ok && b < want[f].bins.size(); ++b) {
+          for (auto [x, y] : {std::pair{got[f].bins[b].grad_sum, want[f].bins[b].grad_sum},
+                              std::pair{got[f].bins[b].hess_sum, want[f].bins[b].hess_sum}}) {
+            double scale = std::max({1.0, std::fabs(x), std::fabs(y)});
+            worst = std::max(worst, std::fabs(x - y) / scale);
+          }
+        }
       }
       LeafTotals tot{leaf.grad_total, leaf.hess_total, leaf.count()};
       std::optional<SplitInfo> bw, bg;
@@ -50,9 +63,9 @@ int main() {
                       (!bw || (bw->feature == bg->feature && bw->threshold_bin == bg->threshold_bin));
       ++checks;
       if (!ok || !split_ok) ++failures;
-      std::printf("[%s] rows=%d d=%d k=%d depth=%d leaf=%lld hist=%s split=%s (%d,%d)\n",
+      std::printf("[%s] rows=%d d=%d k=%d depth=%d leaf=%lld hist=%s (max rel dev %.2e) split=%s (%d,%d)\n",
                   ok && split_ok ? "PASS" : "FAIL", s[0], s[1], s[2], depth,
-                  static_cast<long long>(leaf.count()), ok ? "equivalent" : "DIFF",
+                  static_cast<long long>(leaf.count()), ok ? "equivalent" : "DIFF", worst,
                   split_ok ? "same" : "DIFF", bw ? bw->feature : -1, bw ? bw->threshold_bin : -1);
     }
   }

@@ -3,7 +3,8 @@
 Runs oracle/_ref/backend_swap (tests/cpp/backend_swap.cpp, built against the
 reference headers/objects and libhbg.so): build_histograms_cuda vs the
 reference's build_histograms_partitioned(bits64) under histograms_equivalent
-(counts exact, stats 1e-5) plus identical best splits, and the
+(counts exact, stats within stats_tolerance(bits32) = 1e-4, the reference's
+own fp32 bar) plus identical best splits, and the
 std::invalid_argument error path.
 """
 import os
