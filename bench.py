@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--cpu-reps", type=int, default=5)
+    ap.add_argument("--no-tree", action="store_true")
+    ap.add_argument("--num-leaves", type=int, default=255)
+    ap.add_argument("--trees", type=int, default=3)
     return ap.parse_args()
 
 
@@ -384,6 +387,29 @@ def run_hbg(args):
                                   "roofline_frac": algorithmic_bytes(n, d, 16, 4) / (kt / 1e3) / 1e9 / peak}
             ds16.close()
         result["variants"] = var
+    # --- sec/tree: device-resident 255-leaf best-first tree (grow_tree semantics)
+    if not args.no_tree and world == 1:
+        log, _ = ds.grow_tree(tg, th, args.num_leaves, 1, 0.0, sp)  # warm-up (workspace)
+        ds.kernel_time()
+        ds.set_profiling(True)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(args.trees):
+            log, nodes = ds.grow_tree(tg, th, args.num_leaves, 1, 0.0, sp)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ds.set_profiling(False)
+        t_tree = a.elapsed_time(b) / args.trees / 1e3
+        km, kl = ds.kernel_time()
+        built = n + int(np.minimum(log["left_count"], log["right_count"])[: max(len(log) - 1, 0)].sum())
+        result["tree"] = {
+            "num_leaves": args.num_leaves, "splits": int(len(log)), "sec_per_tree": t_tree,
+            "hist_rows_built": built, "hist_launches_per_tree": kl / args.trees,
+            "hist_kernel_ms_per_tree": km / args.trees,
+            "rows_features_per_s_built": built * d / t_tree,
+            "note": "root + smaller child of every split (larger by subtraction); host loop, one sync per split",
+        }
     clocks.stop()
     result["clocks"] = clocks.summary(t_wall0, t_wall1)
 
@@ -405,6 +431,12 @@ def run_hbg(args):
                               f"{n}x{d} k{k} bins/g/h (mean {cpu_s * 1e3:.1f} ms)",
                 }
                 rd.free_leaf(rleaf)
+                if not args.no_tree:
+                    t_ref, _ = rd.grow_tree_timed(g, h, args.num_leaves, 1, 0.0, 32)
+                    result["cpu_baseline"]["tree"] = {
+                        "sec_per_tree": t_ref, "sample": f"1 grow_tree({args.num_leaves} leaves, bits32) on the same data"}
+                    if "tree" in result:
+                        result["tree"]["cpu_reference_sec_per_tree"] = t_ref
                 rd.close()
             else:
                 result["cpu_baseline"] = None

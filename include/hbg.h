@@ -135,6 +135,37 @@ int hbg_find_best_split(const hbg_bin* hists, int32_t num_features, int32_t max_
                         double grad_total, double hess_total, int64_t count,
                         int64_t min_data_in_leaf, double lambda, hbg_split* out, int32_t* found);
 
+/* ---- device-resident tree growth ----
+ * grow_tree (tree.cpp:186-261) with the partitioned backend's semantics:
+ * best-first over the pool of open leaves (strict >, the oldest leaf wins
+ * ties), children numbered left then right, leaf values from the children's
+ * regathered totals, both children's best splits computed while
+ * leaves < num_leaves. On the device: stable partition_leaf (tree.cpp:114-128)
+ * of a leaf's contiguous row range, fp64 child totals in a fixed order, the
+ * histogram of the SMALLER child only and the larger one by subtraction. */
+typedef struct hbg_grow_params {
+  int32_t num_leaves;       /* GrowParams::num_leaves (tree.hpp:81) */
+  int32_t reserved;
+  int64_t min_data_in_leaf; /* GrowParams::min_data_in_leaf */
+  double lambda;            /* GrowParams::lambda */
+} hbg_grow_params;
+
+/* TreeNode (tree.hpp:26-35) minus threshold_value (mapped by the caller). */
+typedef struct hbg_tree_node {
+  int32_t feature;       /* -1 on leaves */
+  int32_t threshold_bin; /* -1 on leaves */
+  int32_t left, right;   /* -1 on leaves */
+  double value;
+} hbg_tree_node;
+
+/* d_grad/d_hess: fp32 per-row gradients/hessians (device, num_rows each).
+ * split_log: host, num_leaves-1 entries (SplitInfo order of execution);
+ * nodes: host, 2*num_leaves-1 entries. Synchronous on `stream`.
+ * Not re-entrant per handle. */
+int hbg_grow_tree(hbg_dataset* ds, const float* d_grad, const float* d_hess,
+                  const hbg_grow_params* params, hbg_split* split_log, int32_t* num_splits,
+                  hbg_tree_node* nodes, int32_t* num_nodes, void* stream);
+
 /* ---- measurement hooks (bench.py roofline) ----
  * When enabled, the handle records a CUDA event pair around every histogram
  * kernel launch (in-stream, no host sync). hbg_dataset_kernel_time waits for

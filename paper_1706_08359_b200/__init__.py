@@ -58,6 +58,16 @@ SPLIT_DTYPE = np.dtype(
 )
 
 
+#: numpy view of ``hbg_tree_node`` (TreeNode minus threshold_value, tree.hpp:26-35)
+NODE_DTYPE = np.dtype([("feature", "<i4"), ("threshold_bin", "<i4"), ("left", "<i4"), ("right", "<i4"),
+                       ("value", "<f8")])
+
+
+class hbg_grow_params(C.Structure):
+    _fields_ = [("num_leaves", C.c_int32), ("reserved", C.c_int32), ("min_data_in_leaf", C.c_int64),
+                ("lambda_", C.c_double)]
+
+
 class HbgError(RuntimeError):
     """Base class; ``code`` is the HBG_* status."""
 
@@ -109,6 +119,7 @@ EXPORTED_SYMBOLS = (
     "hbg_best_split_device",
     "hbg_best_split_device_totals",
     "hbg_find_best_split",
+    "hbg_grow_tree",
     "hbg_dataset_set_profiling",
     "hbg_dataset_kernel_time",
     "hbg_stream_synchronize",
@@ -151,6 +162,7 @@ def lib() -> C.CDLL:
                                                    C.c_double, _P, _P]
         L.hbg_find_best_split.argtypes = [_P, C.c_int32, C.c_int32, C.c_double, C.c_double,
                                           C.c_int64, C.c_int64, C.c_double, _P, _P]
+        L.hbg_grow_tree.argtypes = [_P, _P, _P, _P, _P, _P, _P, _P, _P]
         L.hbg_dataset_set_profiling.argtypes = [_P, C.c_int32]
         L.hbg_dataset_kernel_time.argtypes = [_P, _P, _P]
         L.hbg_stream_synchronize.argtypes = [_P]
@@ -253,6 +265,19 @@ class Dataset:
         """Device builder: pointers are torch tensors / raw ints; async on ``stream``."""
         check(lib().hbg_build_histograms_device(self.handle, _ptr(indices), count, _ptr(grad),
                                                 _ptr(hess), gh_mode, _ptr(hist), _ptr(stream)))
+
+    def grow_tree(self, grad, hess, num_leaves: int = 31, min_data_in_leaf: int = 1, lam: float = 0.0,
+                  stream=None):
+        """grow_tree (tree.cpp:186-261) on the device; grad/hess are fp32 device
+        tensors of num_rows. Returns (split_log SPLIT_DTYPE[], nodes NODE_DTYPE[])."""
+        p = hbg_grow_params(num_leaves, 0, min_data_in_leaf, lam)
+        log = np.zeros(max(num_leaves - 1, 1), dtype=SPLIT_DTYPE)
+        nodes = np.zeros(max(2 * num_leaves - 1, 1), dtype=NODE_DTYPE)
+        ns = C.c_int32()
+        nn = C.c_int32()
+        check(lib().hbg_grow_tree(self.handle, _ptr(grad), _ptr(hess), C.byref(p), _ptr(log), C.byref(ns),
+                                  _ptr(nodes), C.byref(nn), _ptr(stream)))
+        return log[: ns.value].copy(), nodes[: nn.value].copy()
 
     def set_profiling(self, enabled: bool) -> None:
         """Record CUDA events around each histogram kernel launch (measurement only)."""

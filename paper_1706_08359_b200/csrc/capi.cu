@@ -84,6 +84,10 @@ struct hbg_dataset {
   // workspace (not re-entrant per handle)
   hbg::DevBuf part, iota, host_idx, host_gd, host_hd, host_gf, host_hf, host_hist, host_bins;
   int64_t iota_rows = 0;
+  // tree growth workspace
+  hbg::DevBuf ord[2][3];  // ping-pong (row, g, h) ordered buffers
+  hbg::DevBuf slots, part_scratch, tree_small;  // leaf histograms, partition scratch, splits/totals
+  void* pinned = nullptr;                      // host staging for per-split results
   // measurement hooks
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;  // recorded, not yet read
@@ -100,6 +104,7 @@ struct hbg_dataset {
     return e;
   }
   ~hbg_dataset() {
+    if (pinned) cudaFreeHost(pinned);
     for (auto& e : events) spare.push_back(e);
     for (auto& e : spare) {
       cudaEventDestroy(e.first);
@@ -171,6 +176,174 @@ void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const fl
     launch_histogram(plan, a, s);
   }
   launch_reduce_partials(plan, a, L.num_features, L.max_bin, d_hist, s);
+}
+
+double leaf_value(double g, double h, double lambda) {  // tree.cpp:59-64
+  const double denom = h + lambda;
+  return denom <= 0.0 ? 0.0 : -g / denom;
+}
+
+struct OpenLeaf {  // tree.cpp:132-136
+  int node;
+  int buf;
+  int64_t begin, count;
+  double grad, hess;
+  int slot;
+  bool has_best;
+  hbg_split best;
+};
+
+// Per-split device results copied back in one transfer.
+struct SplitResults {
+  hbg_split split[2];
+  double totals[4];  // gl, hl, gr, hr (children of the split just executed)
+  int64_t left;
+  double root[2];
+};
+
+void grow_tree_impl(hbg_dataset* ds, const float* d_grad, const float* d_hess,
+                    const hbg_grow_params& P, hbg_split* split_log, int32_t* num_splits,
+                    hbg_tree_node* nodes_out, int32_t* num_nodes, cudaStream_t s) {
+  const hbg_layout& L = ds->layout;
+  require(P.num_leaves >= 1, "num_leaves must be at least 1");
+  require(P.min_data_in_leaf >= 0, "min_data_in_leaf must be non-negative");
+  const int64_t N = L.num_rows;
+  const int d = L.num_features, k = L.max_bin;
+  const size_t D3 = 3 * static_cast<size_t>(d) * k;
+  const int max_slots = std::max(1, P.num_leaves);
+  double* slots = static_cast<double*>(ds->slots.get(max_slots * D3 * sizeof(double) + 8));
+  int32_t* rows[2];
+  float* gb[2];
+  float* hb[2];
+  for (int b = 0; b < 2; ++b) {
+    rows[b] = static_cast<int32_t*>(ds->ord[b][0].get(static_cast<size_t>(N) * 4 + 4));
+    gb[b] = static_cast<float*>(ds->ord[b][1].get(static_cast<size_t>(N) * 4 + 4));
+    hb[b] = static_cast<float*>(ds->ord[b][2].get(static_cast<size_t>(N) * 4 + 4));
+  }
+  void* scratch = ds->part_scratch.get(std::max(partition_scratch_bytes(N),
+                                                gather_scratch_doubles(N) * sizeof(double)) + 64);
+  SplitResults* dres = static_cast<SplitResults*>(ds->tree_small.get(sizeof(SplitResults)));
+  if (!ds->pinned) HBG_CUDA(cudaMallocHost(&ds->pinned, sizeof(SplitResults)));
+  SplitResults* hres = static_cast<SplitResults*>(ds->pinned);
+
+  std::vector<hbg_tree_node> nodes;
+  nodes.reserve(static_cast<size_t>(2 * P.num_leaves));
+  std::vector<int> free_slots;
+  for (int i = max_slots - 1; i >= 0; --i) free_slots.push_back(i);
+  auto slot_ptr = [&](int i) { return slots + static_cast<size_t>(i) * D3; };
+  auto splittable = [&](int64_t n) { return !(n < 2 * P.min_data_in_leaf || n < 2); };
+  auto sync_results = [&] {
+    HBG_CUDA(cudaMemcpyAsync(hres, dres, sizeof(SplitResults), cudaMemcpyDeviceToHost, s));
+    HBG_CUDA(cudaStreamSynchronize(s));
+  };
+
+  // Root: ordered buffer 0 = (iota, g, h); totals in a fixed order.
+  launch_iota(rows[0], N, s);
+  if (N > 0) {
+    HBG_CUDA(cudaMemcpyAsync(gb[0], d_grad, static_cast<size_t>(N) * 4, cudaMemcpyDeviceToDevice, s));
+    HBG_CUDA(cudaMemcpyAsync(hb[0], d_hess, static_cast<size_t>(N) * 4, cudaMemcpyDeviceToDevice, s));
+  }
+  launch_gather(rows[0], N, d_grad, d_hess, nullptr, nullptr, dres->root,
+                static_cast<double*>(scratch), s);
+  std::vector<OpenLeaf> pool;
+  OpenLeaf root{0, 0, 0, N, 0.0, 0.0, -1, false, {}};
+  const bool root_split = P.num_leaves >= 2 && splittable(N);
+  if (root_split) {
+    root.slot = free_slots.back();
+    free_slots.pop_back();
+    build_device(ds, rows[0], N, gb[0], hb[0], HBG_GH_LEAF_ALIGNED, slot_ptr(root.slot), s);
+    launch_best_split(slot_ptr(root.slot), d, k, dres->root, nullptr, 0.0, 0.0, N, P.min_data_in_leaf,
+                      P.lambda, &dres->split[0], s);
+  }
+  sync_results();
+  root.grad = hres->root[0];
+  root.hess = hres->root[1];
+  nodes.push_back(hbg_tree_node{-1, -1, -1, -1, leaf_value(root.grad, root.hess, P.lambda)});
+  if (P.num_leaves >= 2) {
+    root.has_best = root_split && hres->split[0].feature >= 0;
+    root.best = hres->split[0];
+    pool.push_back(root);
+  }
+
+  int leaves = 1, logged = 0;
+  while (leaves < P.num_leaves) {
+    int pick = -1;
+    for (size_t i = 0; i < pool.size(); ++i) {  // strict >: the oldest leaf wins ties (tree.cpp:212-218)
+      if (!pool[i].has_best) continue;
+      if (pick < 0 || pool[i].best.gain > pool[static_cast<size_t>(pick)].best.gain) pick = static_cast<int>(i);
+    }
+    if (pick < 0) break;
+    OpenLeaf parent = pool[static_cast<size_t>(pick)];
+    pool.erase(pool.begin() + pick);
+    const hbg_split& sp = parent.best;
+    split_log[logged++] = sp;
+
+    const int out = 1 - parent.buf;
+    const int64_t nl = sp.left_count, nr = parent.count - sp.left_count;
+    if (nl <= 0 || nr <= 0) throw Error(HBG_ERR_LOGIC, "split produced an empty side");
+    launch_partition(rows[parent.buf] + parent.begin, gb[parent.buf] + parent.begin,
+                     hb[parent.buf] + parent.begin, parent.count,
+                     reinterpret_cast<const uint8_t*>(ds->packed), L.row_stride_bytes, sp.feature,
+                     L.bits_per_bin, sp.threshold_bin, rows[out] + parent.begin, gb[out] + parent.begin,
+                     hb[out] + parent.begin, scratch, dres->totals, &dres->left, s);
+
+    const int left_id = static_cast<int>(nodes.size()), right_id = left_id + 1;
+    hbg_tree_node& pn = nodes[static_cast<size_t>(parent.node)];
+    pn.feature = sp.feature;
+    pn.threshold_bin = sp.threshold_bin;
+    pn.left = left_id;
+    pn.right = right_id;
+    pn.value = 0.0;
+    nodes.push_back(hbg_tree_node{-1, -1, -1, -1, 0.0});
+    nodes.push_back(hbg_tree_node{-1, -1, -1, -1, 0.0});
+    ++leaves;
+
+    OpenLeaf lo{left_id, out, parent.begin, nl, 0.0, 0.0, -1, false, {}};
+    OpenLeaf ro{right_id, out, parent.begin + nl, nr, 0.0, 0.0, -1, false, {}};
+    const bool scan = leaves < P.num_leaves;
+    const bool lsplit = scan && splittable(nl), rsplit = scan && splittable(nr);
+    if (lsplit || rsplit) {
+      // histogram of the smaller child; the larger one = parent - smaller, in
+      // the parent's slot (ties build the left child)
+      OpenLeaf& small = nl <= nr ? lo : ro;
+      OpenLeaf& large = nl <= nr ? ro : lo;
+      small.slot = free_slots.back();
+      free_slots.pop_back();
+      large.slot = parent.slot;
+      parent.slot = -1;
+      build_device(ds, rows[out] + small.begin, small.count, gb[out] + small.begin,
+                   hb[out] + small.begin, HBG_GH_LEAF_ALIGNED, slot_ptr(small.slot), s);
+      launch_subtract(slot_ptr(large.slot), slot_ptr(small.slot), slot_ptr(large.slot),
+                      static_cast<int64_t>(D3), s);
+      if (lsplit)
+        launch_best_split(slot_ptr(lo.slot), d, k, dres->totals, nullptr, 0.0, 0.0, nl,
+                          P.min_data_in_leaf, P.lambda, &dres->split[0], s);
+      if (rsplit)
+        launch_best_split(slot_ptr(ro.slot), d, k, dres->totals + 2, nullptr, 0.0, 0.0, nr,
+                          P.min_data_in_leaf, P.lambda, &dres->split[1], s);
+    }
+    if (parent.slot >= 0) free_slots.push_back(parent.slot);
+    sync_results();
+    if (hres->left != nl) throw Error(HBG_ERR_LOGIC, "partition disagrees with the histogram counts");
+    lo.grad = hres->totals[0];
+    lo.hess = hres->totals[1];
+    ro.grad = hres->totals[2];
+    ro.hess = hres->totals[3];
+    nodes[static_cast<size_t>(left_id)].value = leaf_value(lo.grad, lo.hess, P.lambda);
+    nodes[static_cast<size_t>(right_id)].value = leaf_value(ro.grad, ro.hess, P.lambda);
+    lo.has_best = lsplit && hres->split[0].feature >= 0;
+    lo.best = hres->split[0];
+    ro.has_best = rsplit && hres->split[1].feature >= 0;
+    ro.best = hres->split[1];
+    // a leaf that keeps no histogram cannot be split later
+    if (!lo.has_best && lo.slot >= 0) free_slots.push_back(lo.slot), lo.slot = -1;
+    if (!ro.has_best && ro.slot >= 0) free_slots.push_back(ro.slot), ro.slot = -1;
+    pool.push_back(lo);
+    pool.push_back(ro);
+  }
+  *num_splits = logged;
+  *num_nodes = static_cast<int32_t>(nodes.size());
+  if (nodes_out) std::copy(nodes.begin(), nodes.end(), nodes_out);
 }
 
 }  // namespace
@@ -388,6 +561,22 @@ int hbg_find_best_split(const hbg_bin* hists, int32_t num_features, int32_t max_
                       count, min_data_in_leaf, lambda, d_out, nullptr);
     HBG_CUDA(cudaMemcpy(out, d_out, sizeof(hbg_split), cudaMemcpyDeviceToHost));
     *found = out->feature >= 0 ? 1 : 0;
+  });
+}
+
+int hbg_grow_tree(hbg_dataset* ds, const float* d_grad, const float* d_hess,
+                  const hbg_grow_params* params, hbg_split* split_log, int32_t* num_splits,
+                  hbg_tree_node* nodes, int32_t* num_nodes, void* stream) {
+  return guarded([&] {
+    check_ds(ds);
+    require(params != nullptr && split_log != nullptr && num_splits != nullptr &&
+                num_nodes != nullptr,
+            "null argument");
+    require(ds->layout.num_rows == 0 || (d_grad != nullptr && d_hess != nullptr),
+            "null gradient/hessian pointer");
+    DeviceGuard dg(ds->layout.device);
+    grow_tree_impl(ds, d_grad, d_hess, *params, split_log, num_splits, nodes, num_nodes,
+                   static_cast<cudaStream_t>(stream));
   });
 }
 

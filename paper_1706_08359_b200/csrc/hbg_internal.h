@@ -82,6 +82,15 @@ void launch_best_split(const double* d_hist, int d, int k, const double* d_total
                        const int64_t* d_count, double gt, double ht, int64_t count,
                        int64_t min_data, double lambda, hbg_split* out, cudaStream_t s);
 
+size_t partition_scratch_bytes(int64_t n);
+// Stable split of one leaf's contiguous (row, g, h) range by bin(feature) <= thr
+// into the other buffer (left rows first); d_totals = {gl, hl, gr, hr} (fp64),
+// *d_left = rows sent left.
+void launch_partition(const int32_t* rows, const float* g, const float* h, int64_t n,
+                      const uint8_t* packed, int64_t row_stride, int feature, int bits, int thr,
+                      int32_t* orow, float* og, float* oh, void* scratch, double* d_totals,
+                      int64_t* d_left, cudaStream_t s);
+
 int sm_count(int device);
 
 }  // namespace hbg

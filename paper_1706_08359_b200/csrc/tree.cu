@@ -1,0 +1,249 @@
+// tree.cu — device-resident best-first tree growth:
+// grow_tree (tree.cpp:186-261) with partition_leaf (tree.cpp:114-128), the
+// children's gather_leaf_statistics (tree.cpp:244-246), the histogram of the
+// smaller child only and the larger child by subtraction (row a10).
+//
+// Device state per tree: two ping-pong "ordered" buffers of (row id, g, h),
+// SoA. Every open leaf owns a contiguous range [begin, begin+count) of one of
+// them, so its histogram reads ids and g/h contiguously (HBG_GH_LEAF_ALIGNED,
+// the algorithmic-bytes layout of SURVEY §8d) however deep the leaf is. A
+// split partitions the parent's range stably into the other buffer (left rows
+// first, in leaf order — the reference's order), computing both children's
+// fp64 totals on the way in a fixed order.
+#include <algorithm>
+#include <vector>
+
+#include "hbg_internal.h"
+
+namespace hbg {
+
+namespace {
+
+constexpr int kPartThreads = 512;
+constexpr int kPartItems = 8;
+constexpr int kPartTile = kPartThreads * kPartItems;  // positions per block
+
+struct PartArgs {
+  const int32_t* rows;
+  const float* g;
+  const float* h;
+  int64_t n;
+  const uint8_t* packed;
+  int64_t row_stride;
+  int byte_off;
+  int shift;
+  uint32_t mask;
+  int thr;
+  uint8_t* flags;
+  int32_t* block_left;
+  double* block_sums;  // [nblocks][4] = gl, hl, gr, hr
+};
+
+// Deterministic block reduction of 4 doubles + one int (warp shuffle tree, then warps in order).
+__device__ void block_reduce_4d1i(double v[4], int& c, double (*sd)[kPartThreads / 32], int* sc) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] += __shfl_down_sync(0xffffffffu, v[j], off);
+    c += __shfl_down_sync(0xffffffffu, c, off);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) sd[j][w] = v[j];
+    sc[w] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < 4; ++j) {
+      double s = 0.0;
+      for (int i = 0; i < kPartThreads / 32; ++i) s += sd[j][i];
+      v[j] = s;
+    }
+    int s = 0;
+    for (int i = 0; i < kPartThreads / 32; ++i) s += sc[i];
+    c = s;
+  }
+}
+
+// Pass 1: side flag per position (bin <= thr goes left, tree.cpp:117-123),
+// per-block left count and fp64 per-side g/h sums.
+__global__ void __launch_bounds__(kPartThreads) partition_count_kernel(PartArgs a) {
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kPartTile;
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  int c = 0;
+#pragma unroll
+  for (int i = 0; i < kPartItems; ++i) {
+    const int64_t pos = base + i * kPartThreads + threadIdx.x;
+    if (pos < a.n) {
+      const int32_t row = __ldg(a.rows + pos);
+      const uint32_t byte = __ldg(a.packed + static_cast<int64_t>(row) * a.row_stride + a.byte_off);
+      const bool left = ((byte >> a.shift) & a.mask) <= static_cast<uint32_t>(a.thr);
+      a.flags[pos] = left ? 1 : 0;
+      const double gv = __ldg(a.g + pos), hv = __ldg(a.h + pos);
+      if (left) {
+        ++c;
+        v[0] += gv;
+        v[1] += hv;
+      } else {
+        v[2] += gv;
+        v[3] += hv;
+      }
+    }
+  }
+  __shared__ double sd[4][kPartThreads / 32];
+  __shared__ int sc[kPartThreads / 32];
+  block_reduce_4d1i(v, c, sd, sc);
+  if (threadIdx.x == 0) {
+    a.block_left[blockIdx.x] = c;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) a.block_sums[4 * blockIdx.x + j] = v[j];
+  }
+}
+
+// Pass 2 (one CTA): exclusive scan of the block left counts, fixed-order
+// fp64 child totals. out_totals = {gl, hl, gr, hr}, *left_total = rows left.
+__global__ void __launch_bounds__(1024) partition_scan_kernel(const int32_t* block_left,
+                                                              const double* block_sums, int nb,
+                                                              int64_t* block_off, double* out_totals,
+                                                              int64_t* left_total) {
+  const int t = threadIdx.x, T = blockDim.x;
+  const int chunk = (nb + T - 1) / T;
+  const int b0 = min(nb, t * chunk), b1 = min(nb, b0 + chunk);
+  int64_t local = 0;
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int b = b0; b < b1; ++b) {
+    local += block_left[b];
+    for (int j = 0; j < 4; ++j) v[j] += block_sums[4 * b + j];
+  }
+  __shared__ int64_t ss[1024];
+  __shared__ double sv[4][1024];
+  ss[t] = local;
+  for (int j = 0; j < 4; ++j) sv[j][t] = v[j];
+  __syncthreads();
+  // inclusive Hillis-Steele scan of the per-thread counts
+  for (int off = 1; off < T; off <<= 1) {
+    const int64_t x = t >= off ? ss[t - off] : 0;
+    __syncthreads();
+    ss[t] += x;
+    __syncthreads();
+  }
+  int64_t run = ss[t] - local;  // exclusive prefix of this thread's chunk
+  for (int b = b0; b < b1; ++b) {
+    block_off[b] = run;
+    run += block_left[b];
+  }
+  if (t == 0) {
+    *left_total = ss[T - 1];
+    for (int j = 0; j < 4; ++j) {
+      double s = 0.0;
+      for (int i = 0; i < T; ++i) s += sv[j][i];  // thread order = block order
+      out_totals[j] = s;
+    }
+  }
+}
+
+// Pass 3: stable scatter of (row, g, h) into the other buffer, left side first.
+__global__ void __launch_bounds__(kPartThreads) partition_scatter_kernel(
+    const int32_t* __restrict__ rows, const float* __restrict__ g, const float* __restrict__ h,
+    const uint8_t* __restrict__ flags, int64_t n, const int64_t* __restrict__ block_off,
+    const int64_t* __restrict__ left_total, int32_t* __restrict__ orow, float* __restrict__ og,
+    float* __restrict__ oh) {
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kPartTile;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __shared__ int wl[kPartThreads / 32];
+  __shared__ int wn[kPartThreads / 32];
+  const int64_t L = *left_total;
+  const int64_t left_before = block_off[blockIdx.x];
+  int64_t lrun = left_before;              // left rows before this item, in leaf order
+  int64_t rrun = base - left_before;       // right rows before this item
+#pragma unroll 1
+  for (int i = 0; i < kPartItems; ++i) {
+    const int64_t pos = base + i * kPartThreads + threadIdx.x;
+    const bool valid = pos < n;
+    const bool left = valid && flags[pos];
+    const unsigned lm = __ballot_sync(0xffffffffu, left);
+    const unsigned vm = __ballot_sync(0xffffffffu, valid);
+    if (lane == 0) {
+      wl[w] = __popc(lm);
+      wn[w] = __popc(vm);
+    }
+    __syncthreads();
+    int lbefore = 0, nbefore = 0, ltot = 0, ntot = 0;
+    for (int j = 0; j < kPartThreads / 32; ++j) {
+      if (j < w) {
+        lbefore += wl[j];
+        nbefore += wn[j];
+      }
+      ltot += wl[j];
+      ntot += wn[j];
+    }
+    const unsigned below = (1u << lane) - 1u;
+    if (valid) {
+      const int lrank = lbefore + __popc(lm & below);
+      const int prank = nbefore + __popc(vm & below);  // position rank within this iteration
+      const int64_t dst = left ? lrun + lrank : L + rrun + (prank - lrank);
+      orow[dst] = rows[pos];
+      og[dst] = g[pos];
+      oh[dst] = h[pos];
+    }
+    lrun += ltot;
+    rrun += ntot - ltot;
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+// One split of a leaf's range: flags/counts/totals, scan, scatter. `scratch`
+// must hold n bytes of flags + per-block arrays (see partition_scratch_bytes).
+size_t partition_scratch_bytes(int64_t n) {
+  const int64_t nb = std::max<int64_t>(1, (n + kPartTile - 1) / kPartTile);
+  return static_cast<size_t>(n) + 16 + static_cast<size_t>(nb) * (4 + 32 + 8) + 64;
+}
+
+void launch_partition(const int32_t* rows, const float* g, const float* h, int64_t n,
+                      const uint8_t* packed, int64_t row_stride, int feature, int bits, int thr,
+                      int32_t* orow, float* og, float* oh, void* scratch, double* d_totals,
+                      int64_t* d_left, cudaStream_t s) {
+  const int64_t nb = std::max<int64_t>(1, (n + kPartTile - 1) / kPartTile);
+  uint8_t* p = static_cast<uint8_t*>(scratch);
+  uint8_t* flags = p;
+  p += (static_cast<size_t>(n) + 15) / 16 * 16;
+  double* block_sums = reinterpret_cast<double*>(p);
+  p += static_cast<size_t>(nb) * 32;
+  int64_t* block_off = reinterpret_cast<int64_t*>(p);
+  p += static_cast<size_t>(nb) * 8;
+  int32_t* block_left = reinterpret_cast<int32_t*>(p);
+  PartArgs a{};
+  a.rows = rows;
+  a.g = g;
+  a.h = h;
+  a.n = n;
+  a.packed = packed;
+  a.row_stride = row_stride;
+  const int slice = feature / 32, fl = feature % 32;
+  if (bits == 8) {
+    a.byte_off = slice * 32 + fl;
+    a.shift = 0;
+    a.mask = 0xFF;
+  } else {
+    a.byte_off = slice * 16 + (fl / 8) * 4 + (fl % 8) / 2;
+    a.shift = 4 * (fl % 2);
+    a.mask = 0xF;
+  }
+  a.thr = thr;
+  a.flags = flags;
+  a.block_left = block_left;
+  a.block_sums = block_sums;
+  partition_count_kernel<<<static_cast<unsigned>(nb), kPartThreads, 0, s>>>(a);
+  HBG_LAUNCH_CHECK();
+  partition_scan_kernel<<<1, 1024, 0, s>>>(block_left, block_sums, static_cast<int>(nb), block_off,
+                                           d_totals, d_left);
+  HBG_LAUNCH_CHECK();
+  partition_scatter_kernel<<<static_cast<unsigned>(nb), kPartThreads, 0, s>>>(
+      rows, g, h, flags, n, block_off, d_left, orow, og, oh);
+  HBG_LAUNCH_CHECK();
+}
+
+}  // namespace hbg

@@ -333,3 +333,70 @@ def test_full_size_higgs_root_properties(hbg, oracle, k):
         theirs = max_rel_err(ref32[key], want[key])
         assert ours <= FULL_TOL[k], (key, ours)
         assert ours <= theirs, (key, ours, theirs)
+
+
+# ------------------------------------------------ device tree growth (§8f)
+def _grow(hbg, ds, g, h, num_leaves, min_data, lam):
+    torch = torch_cuda()
+    dev = torch.device("cuda:0")
+    tg = torch.from_numpy(np.asarray(g, dtype=np.float32)).to(dev)
+    th = torch.from_numpy(np.asarray(h, dtype=np.float32)).to(dev)
+    return ds.grow_tree(tg, th, num_leaves, min_data, lam)
+
+
+def _assert_same_tree(log, nodes, want_log, want_nodes):
+    assert len(log) == len(want_log)
+    assert (log["feature"] == want_log["feature"]).all(), (log["feature"], want_log["feature"])
+    assert (log["threshold_bin"] == want_log["threshold_bin"]).all()
+    assert (log["left_count"] == want_log["left_count"]).all()
+    assert (log["right_count"] == want_log["right_count"]).all()
+    assert np.allclose(log["gain"], want_log["gain"], rtol=1e-5, atol=1e-9)
+    for key in ("feature", "threshold_bin", "left", "right"):
+        assert (nodes[key] == want_nodes[key]).all(), key
+    assert np.allclose(nodes["value"], want_nodes["value"], rtol=1e-5, atol=1e-9)
+
+
+def test_grow_tree_matches_reference_golden_split_log(hbg, oracle):
+    """grow_tree split_log of the unmodified reference (bits64), committed golden."""
+    import os
+
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_histograms.npz"))
+    cols = oracle.gen_synthetic_bins(4000, 6, 16, 3)
+    g, h = oracle.gen_grad_hess(4000, 3)
+    with hbg.Dataset(cols, 16) as ds:
+        log, nodes = _grow(hbg, ds, g, h, 31, 1, 0.0)
+        want_log, want_nodes = oracle.grow_tree(cols, 16, g, h, 31, 1, 0.0, 64)
+        assert (want_log == z["tree_4000x6_k16_seed3_split_log"]).all()
+        _assert_same_tree(log, nodes, want_log, want_nodes)
+        log2, nodes2 = _grow(hbg, ds, g, h, 20, 20, 1.0)
+        want2, wn2 = oracle.grow_tree(cols, 16, g, h, 20, 20, 1.0, 64)
+        assert (want2 == z["tree_4000x6_k16_seed3_min20_lam1_split_log"]).all()
+        _assert_same_tree(log2, nodes2, want2, wn2)
+
+
+@pytest.mark.parametrize("rows,d,k,leaves,min_data,lam", [
+    (30000, 28, 64, 63, 1, 0.0), (20000, 10, 256, 31, 5, 1.0), (50000, 40, 16, 127, 20, 0.0),
+    (3000, 3, 64, 255, 1, 0.0)])
+def test_grow_tree_matches_oracle(hbg, oracle, rows, d, k, leaves, min_data, lam):
+    cols = oracle.gen_synthetic_bins(rows, d, k, d)
+    g, h = oracle.gen_grad_hess(rows, d)
+    g = g + 0.3 * (cols[d // 2].astype(np.float64) > k // 2)  # some structure
+    with hbg.Dataset(cols, k) as ds:
+        log, nodes = _grow(hbg, ds, g, h, leaves, min_data, lam)
+    want_log, want_nodes = oracle.grow_tree(cols, k, g, h, leaves, min_data, lam, 64)
+    _assert_same_tree(log, nodes, want_log, want_nodes)
+
+
+def test_grow_tree_edge_cases(hbg, oracle):
+    cols = oracle.gen_synthetic_bins(500, 4, 64, 1)
+    g, h = oracle.gen_grad_hess(500, 1)
+    with hbg.Dataset(cols, 64) as ds:
+        log, nodes = _grow(hbg, ds, g, h, 1, 1, 0.0)  # a single leaf: no split
+        assert len(log) == 0 and len(nodes) == 1
+        assert nodes[0]["value"] == pytest.approx(-g.sum() / h.sum(), rel=1e-5)
+        log, nodes = _grow(hbg, ds, g, h, 8, 400, 0.0)  # min_data prunes everything below the root
+        want_log, want_nodes = oracle.grow_tree(cols, 64, g, h, 8, 400, 0.0, 64)
+        _assert_same_tree(log, nodes, want_log, want_nodes)
+    with pytest.raises(hbg.InvalidArgument):
+        with hbg.Dataset(cols, 64) as ds:
+            _grow(hbg, ds, g, h, 0, 1, 0.0)
