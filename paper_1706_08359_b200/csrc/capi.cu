@@ -127,8 +127,11 @@ void check_ds(const hbg_dataset* ds) { require(ds != nullptr, "null dataset hand
 // the synchronous host drop-in.
 cudaStream_t pick(hbg_dataset*, void* stream) { return static_cast<cudaStream_t>(stream); }
 
+// Device histogram of one leaf into d_hist; with `parent` also writes
+// sibling = parent - d_hist in the same pass (sibling may alias parent).
 void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const float* d_g,
-                  const float* d_h, int gh_mode, double* d_hist, cudaStream_t s) {
+                  const float* d_h, int gh_mode, double* d_hist, cudaStream_t s,
+                  const double* parent = nullptr, double* sibling = nullptr) {
   const hbg_layout& L = ds->layout;
   require(count >= 0, "negative leaf size");
   require(count <= L.num_rows || d_idx != nullptr, "identity leaf larger than the dataset");
@@ -137,6 +140,8 @@ void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const fl
   const size_t D = static_cast<size_t>(L.num_features) * L.max_bin;
   if (count == 0 || L.num_features == 0) {
     HBG_CUDA(cudaMemsetAsync(d_hist, 0, 3 * D * sizeof(double), s));
+    if (parent && sibling != parent)
+      HBG_CUDA(cudaMemcpyAsync(sibling, parent, 3 * D * sizeof(double), cudaMemcpyDeviceToDevice, s));
     return;
   }
   require(d_g != nullptr && d_h != nullptr, "null gradient/hessian pointer");
@@ -175,7 +180,7 @@ void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const fl
   } else {
     launch_histogram(plan, a, s);
   }
-  launch_reduce_partials(plan, a, L.num_features, L.max_bin, d_hist, s);
+  launch_reduce_partials(plan, a, L.num_features, L.max_bin, d_hist, s, parent, sibling);
 }
 
 double leaf_value(double g, double h, double lambda) {  // tree.cpp:59-64
@@ -312,15 +317,19 @@ void grow_tree_impl(hbg_dataset* ds, const float* d_grad, const float* d_hess,
       large.slot = parent.slot;
       parent.slot = -1;
       build_device(ds, rows[out] + small.begin, small.count, gb[out] + small.begin,
-                   hb[out] + small.begin, HBG_GH_LEAF_ALIGNED, slot_ptr(small.slot), s);
-      launch_subtract(slot_ptr(large.slot), slot_ptr(small.slot), slot_ptr(large.slot),
-                      static_cast<int64_t>(D3), s);
-      if (lsplit)
+                   hb[out] + small.begin, HBG_GH_LEAF_ALIGNED, slot_ptr(small.slot), s,
+                   slot_ptr(large.slot), slot_ptr(large.slot));  // larger = parent - smaller
+      if (lsplit && rsplit) {  // both children's scans in one launch
+        launch_best_split_batch(slot_ptr(lo.slot), slot_ptr(ro.slot) - slot_ptr(lo.slot), 2, d, k,
+                                dres->totals, 2, nullptr, nl, nr, 0.0, 0.0, P.min_data_in_leaf,
+                                P.lambda, &dres->split[0], s);
+      } else if (lsplit) {
         launch_best_split(slot_ptr(lo.slot), d, k, dres->totals, nullptr, 0.0, 0.0, nl,
                           P.min_data_in_leaf, P.lambda, &dres->split[0], s);
-      if (rsplit)
+      } else {
         launch_best_split(slot_ptr(ro.slot), d, k, dres->totals + 2, nullptr, 0.0, 0.0, nr,
                           P.min_data_in_leaf, P.lambda, &dres->split[1], s);
+      }
     }
     if (parent.slot >= 0) free_slots.push_back(parent.slot);
     sync_results();

@@ -64,8 +64,12 @@ struct HistArgs {
 HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int device);
 
 void launch_histogram(const HistPlan& plan, const HistArgs& args, cudaStream_t s);
+// d_hist = reduced histogram; when `parent` is non-null also writes
+// sibling = parent - d_hist (histogram subtraction fused into the reduction;
+// sibling may alias parent).
 void launch_reduce_partials(const HistPlan& plan, const HistArgs& args, int num_features,
-                            int max_bin, double* d_hist, cudaStream_t s);
+                            int max_bin, double* d_hist, cudaStream_t s,
+                            const double* parent = nullptr, double* sibling = nullptr);
 // Packs features [f0, f0 + nf) (one 32-feature slice group; d_cols holds
 // their column-major bins) into the group's words of every row.
 void launch_pack(const uint8_t* d_cols, int f0, int nf, int num_features, int64_t num_rows,
@@ -78,6 +82,13 @@ void launch_subtract(const double* a, const double* b, double* out, int64_t n, c
 void launch_gather(const int32_t* idx, int64_t n, const float* g, const float* h, float* lg,
                    float* lh, double* totals, double* scratch, cudaStream_t s);
 size_t gather_scratch_doubles(int64_t n);
+// Split scans of 1-2 histograms in one launch (one CTA each): histogram i at
+// d_hist + i*hist_stride, totals at d_totals + i*totals_stride, count
+// d_counts[i] (or count0/count1 when d_counts is null), result out[i].
+void launch_best_split_batch(const double* d_hist, int64_t hist_stride, int leaves, int d, int k,
+                             const double* d_totals, int64_t totals_stride, const int64_t* d_counts,
+                             int64_t count0, int64_t count1, double gt, double ht, int64_t min_data,
+                             double lambda, hbg_split* out, cudaStream_t s);
 void launch_best_split(const double* d_hist, int d, int k, const double* d_totals,
                        const int64_t* d_count, double gt, double ht, int64_t count,
                        int64_t min_data, double lambda, hbg_split* out, cudaStream_t s);

@@ -108,14 +108,55 @@ __device__ __forceinline__ void update_step(const Slice<BITS>& s, int p, int lan
   atomicAdd(cnt + cell, 1u);  // ATOMS.POPC.INC
 }
 
+// Dual-row step: lane l updates the same feature (l+p) mod 32 for its R rows.
+// The R read-modify-writes are issued together (R-fold more shared-memory work
+// per ordered step, i.e. more independent MIO traffic per warp); when two of
+// a lane's rows hit the same cell, the later one builds on the earlier sum so
+// the last store carries both.
+template <int BITS, int K, int R>
+__device__ __forceinline__ void update_step_rows(const Slice<BITS> (&s)[R], int p, int lane,
+                                                 uint32_t gh_base, uint32_t* cnt, const float (&g)[R],
+                                                 const float (&h)[R]) {
+  asm volatile("bar.warp.sync -1;" ::: "memory");
+  constexpr int fpw = Slice<BITS>::kFeatPerWord;
+  uint32_t c[R];
+  float x[R], y[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint32_t b = (s[r].w[p / fpw] >> (BITS * (p % fpw))) & (K - 1);
+    c[r] = (b << 5) | ((lane + p) & 31);
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) lds_f2(gh_base + c[r] * 8u, x[r], y[r]);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+#pragma unroll
+    for (int q = 0; q < r; ++q) {
+      if (c[q] == c[r]) {
+        x[r] = x[q];
+        y[r] = y[q];
+      }
+    }
+    x[r] += g[r];
+    y[r] += h[r];
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) sts_f2(gh_base + c[r] * 8u, x[r], y[r]);
+#pragma unroll
+  for (int r = 0; r < R; ++r) atomicAdd(cnt + c[r], 1u);  // ATOMS.POPC.INC
+}
+
 struct TileIn {
   int32_t row;  // raw int32 row id (row_index_t): widening it right after the
                 // load would make the load's consumer immediate and stall on it
   float g, h;
 };
 
+// Rows per lane per tile (see update_step_rows).
+constexpr int kRowsPerLane = 2;
+
 template <int BITS, int K, bool kRowIndexed>
-__global__ void __launch_bounds__(512) hist_kernel(HistArgs a) {
+__global__ void __launch_bounds__(512, BITS == 4 ? 2 : 1) hist_kernel(HistArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int kCells = K * 32;
   const int warps = blockDim.x >> 5;
@@ -141,65 +182,85 @@ __global__ void __launch_bounds__(512) hist_kernel(HistArgs a) {
     const uint32_t gh_base = smem_addr(gh + static_cast<size_t>(w) * kCells);
     uint32_t* cnt_g = cnt + static_cast<size_t>(gl) * kCells;
     const unsigned char* base = a.packed + static_cast<size_t>(group) * Slice<BITS>::kWords * 4;
-    const int64_t step = static_cast<int64_t>(a.wpg) * 32;
+    constexpr int R = kRowsPerLane;
+    const int64_t step = static_cast<int64_t>(a.wpg) * 32 * R;
 
     // Two-stage software pipeline, so no load waits on another load in the
     // same iteration (issue is in order): stage A fetches the leaf entries
-    // (row id, g, h) of tile t+2s, stage B fetches the packed slice of tile
+    // (row id, g, h) of tile t+2s, stage B fetches the packed slices of tile
     // t+s using the row ids stage A delivered one iteration earlier, and the
-    // update loop consumes tile t.
-    auto fetch_entry = [&](int64_t t, TileIn& in) {
-      const int64_t pos = t + lane;
-      if (pos < s1) {
-        in.row = __ldg(a.idx + pos);  // never null: the identity leaf uses an iota array
-        if constexpr (!kRowIndexed) {
-          in.g = __ldg(a.g + pos);
-          in.h = __ldg(a.h + pos);
+    // update loop consumes tile t. A tile is 32*R rows; lane l owns rows
+    // t + 32r + l.
+    auto fetch_entry = [&](int64_t t, TileIn (&in)[R]) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int64_t pos = t + 32 * r + lane;
+        if (pos < s1) {
+          in[r].row = __ldg(a.idx + pos);  // never null: the identity leaf uses an iota array
+          if constexpr (!kRowIndexed) {
+            in[r].g = __ldg(a.g + pos);
+            in[r].h = __ldg(a.h + pos);
+          }
+        } else {
+          in[r].row = -1;
+          in[r].g = 0.f;
+          in[r].h = 0.f;
         }
-      } else {
-        in.row = -1;
-        in.g = 0.f;
-        in.h = 0.f;
       }
     };
-    auto fetch_slice = [&](TileIn& in, Slice<BITS>& sl) {
-      if (in.row >= 0) {
-        if constexpr (kRowIndexed) {
-          in.g = __ldg(a.g + in.row);
-          in.h = __ldg(a.h + in.row);
-        }
-        load_slice<BITS>(base + static_cast<int64_t>(in.row) * a.row_stride, sl);
-      } else {
+    auto fetch_slice = [&](TileIn (&in)[R], Slice<BITS> (&sl)[R]) {
 #pragma unroll
-        for (int j = 0; j < Slice<BITS>::kWords; ++j) sl.w[j] = 0;
+      for (int r = 0; r < R; ++r) {
+        if (in[r].row >= 0) {
+          if constexpr (kRowIndexed) {
+            in[r].g = __ldg(a.g + in[r].row);
+            in[r].h = __ldg(a.h + in[r].row);
+          }
+          load_slice<BITS>(base + static_cast<int64_t>(in[r].row) * a.row_stride, sl[r]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < Slice<BITS>::kWords; ++j) sl[r].w[j] = 0;
+        }
       }
     };
 
-    int64_t t = s0 + static_cast<int64_t>(sub) * 32;
-    TileIn e0, e1;
-    Slice<BITS> cur;
+    int64_t t = s0 + static_cast<int64_t>(sub) * 32 * R;
+    TileIn e0[R], e1[R];
+    Slice<BITS> cur[R];
     fetch_entry(t, e0);
     fetch_entry(t + step, e1);
     fetch_slice(e0, cur);
     for (; t < s1; t += step) {
-      TileIn e2;
-      Slice<BITS> nxt;
+      TileIn e2[R];
+      Slice<BITS> nxt[R];
       fetch_entry(t + 2 * step, e2);  // stage A (t + 2s)
       fetch_slice(e1, nxt);           // stage B (t + s)
-      rotate_slice<BITS>(cur, lane);
-      if (t + 32 <= s1) {
 #pragma unroll
-        for (int p = 0; p < 32; ++p)
-          update_step<BITS, K, false>(cur, p, lane, gh_base, cnt_g, e0.g, e0.h, true);
+      for (int r = 0; r < R; ++r) rotate_slice<BITS>(cur[r], lane);
+      if (t + 32 * R <= s1) {
+        float g[R], h[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          g[r] = e0[r].g;
+          h[r] = e0[r].h;
+        }
+#pragma unroll
+        for (int p = 0; p < 32; ++p) update_step_rows<BITS, K, R>(cur, p, lane, gh_base, cnt_g, g, h);
       } else {
-        const bool valid = e0.row >= 0;
 #pragma unroll
-        for (int p = 0; p < 32; ++p)
-          update_step<BITS, K, true>(cur, p, lane, gh_base, cnt_g, e0.g, e0.h, valid);
+        for (int r = 0; r < R; ++r) {
+          const bool valid = e0[r].row >= 0;
+#pragma unroll
+          for (int p = 0; p < 32; ++p)
+            update_step<BITS, K, true>(cur[r], p, lane, gh_base, cnt_g, e0[r].g, e0[r].h, valid);
+        }
       }
-      e0 = e1;
-      e1 = e2;
-      cur = nxt;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        e0[r] = e1[r];
+        e1[r] = e2[r];
+        cur[r] = nxt[r];
+      }
     }
   }
   __syncthreads();
@@ -229,7 +290,8 @@ __global__ void __launch_bounds__(512) hist_kernel(HistArgs a) {
 constexpr int kReduceWarps = 16;
 
 __global__ void __launch_bounds__(kReduceWarps * 32) reduce_partials_kernel(
-    HistArgs a, int nseg, int k_alloc, int d, int max_bin, double* out) {
+    HistArgs a, int nseg, int k_alloc, int d, int max_bin, double* out, const double* parent,
+    double* sibling) {
   const int cells = k_alloc * 32;
   const int group = blockIdx.y;
   const int bin = blockIdx.x;
@@ -267,6 +329,12 @@ __global__ void __launch_bounds__(kReduceWarps * 32) reduce_partials_kernel(
   out[o] = sg;
   out[D + o] = sh;
   out[2 * D + o] = static_cast<double>(sc);
+  if (parent) {  // histogram subtraction (row a10), fused
+    const double pg = parent[o], ph = parent[D + o], pc = parent[2 * D + o];
+    sibling[o] = pg - sg;
+    sibling[D + o] = ph - sh;
+    sibling[2 * D + o] = pc - static_cast<double>(sc);
+  }
 }
 
 // Column-major uint8 bins -> row-major packed words at pack_feature_tuples
@@ -349,6 +417,16 @@ HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int de
     if (warps >= gb) break;
   }
   require(gb >= 1 && warps >= 1, "histogram footprint exceeds shared memory");
+  // Small leaves: shrink the CTA (less shared memory to clear and fold) so the
+  // grid still spreads over the SMs with >= 4 tiles per warp.
+  {
+    const int64_t tile_rows = static_cast<int64_t>(32) * kRowsPerLane;
+    const int64_t warps_needed =
+        std::max<int64_t>(1, (n + 4 * tile_rows - 1) / (4 * tile_rows)) * num_groups;
+    const int64_t per_cta = (warps_needed + sm_count(device) - 1) / sm_count(device);
+    const int64_t want = std::max<int64_t>(gb, (per_cta + gb - 1) / gb * gb);
+    if (want < warps) warps = static_cast<int>(want);
+  }
   p.gb = gb;
   p.wpg = warps / gb;
   p.warps = gb * p.wpg;
@@ -357,7 +435,7 @@ HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int de
   const int occ = occupancy_for(bits, p.k_alloc, p.warps * 32, p.smem, device);
   const int64_t target = static_cast<int64_t>(sm_count(device)) * occ;
   int64_t nseg = (target + p.nblocks - 1) / p.nblocks;
-  const int64_t min_rows = static_cast<int64_t>(p.wpg) * 32 * 2;  // >= 2 tiles per warp
+  const int64_t min_rows = static_cast<int64_t>(p.wpg) * 32 * kRowsPerLane * 2;  // >= 2 tiles per warp
   nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, (n + min_rows - 1) / min_rows));
   int64_t seg_len = (n + nseg - 1) / nseg;
   seg_len = std::max<int64_t>(32, (seg_len + 31) / 32 * 32);
@@ -384,10 +462,11 @@ void launch_histogram(const HistPlan& plan, const HistArgs& args, cudaStream_t s
 }
 
 void launch_reduce_partials(const HistPlan& plan, const HistArgs& args, int num_features,
-                            int max_bin, double* d_hist, cudaStream_t s) {
+                            int max_bin, double* d_hist, cudaStream_t s, const double* parent,
+                            double* sibling) {
   const dim3 block(kReduceWarps * 32), grid(std::min(plan.k_alloc, max_bin), args.num_groups);
   reduce_partials_kernel<<<grid, block, 0, s>>>(args, plan.nseg, plan.k_alloc, num_features,
-                                                max_bin, d_hist);
+                                                max_bin, d_hist, parent, sibling);
   HBG_LAUNCH_CHECK();
 }
 

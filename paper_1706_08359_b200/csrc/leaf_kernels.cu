@@ -49,15 +49,30 @@ __global__ void gather_kernel(const int32_t* __restrict__ idx, int64_t n, const 
   }
 }
 
+// Fixed-order combine of the per-block partials: thread t sums a contiguous
+// run of blocks, then a pairwise tree in thread order.
 __global__ void gather_finalize_kernel(const double* partial, int blocks, double* totals) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double sg = 0.0, sh = 0.0;
-    for (int b = 0; b < blocks; ++b) {
-      sg += partial[2 * b];
-      sh += partial[2 * b + 1];
+  __shared__ double r[2][256];
+  const int t = threadIdx.x;
+  const int chunk = (blocks + 255) / 256;
+  double sg = 0.0, sh = 0.0;
+  for (int b = t * chunk; b < min(blocks, (t + 1) * chunk); ++b) {
+    sg += partial[2 * b];
+    sh += partial[2 * b + 1];
+  }
+  r[0][t] = sg;
+  r[1][t] = sh;
+  __syncthreads();
+  for (int st = 128; st > 0; st >>= 1) {
+    if (t < st) {
+      r[0][t] += r[0][t + st];
+      r[1][t] += r[1][t + st];
     }
-    totals[0] = sg;
-    totals[1] = sh;
+    __syncthreads();
+  }
+  if (t == 0) {
+    totals[0] = r[0][0];
+    totals[1] = r[1][0];
   }
 }
 
@@ -102,79 +117,115 @@ __device__ __forceinline__ double gain_of(double lg, double lh, double rg, doubl
 struct Cand {
   double gain;
   int f, b;
-  double lg, lh;
-  int64_t lc;
 };
 
+// max gain; ties -> lowest feature, then lowest bin (tree.cpp:95,172)
 __device__ __forceinline__ bool better(const Cand& a, const Cand& b) {
   if (a.f < 0) return false;
   if (b.f < 0) return true;
-  return a.gain > b.gain || (a.gain == b.gain && a.f < b.f);
+  if (a.gain != b.gain) return a.gain > b.gain;
+  return a.f < b.f || (a.f == b.f && a.b < b.b);
 }
 
-constexpr int kScanThreads = 1024;
+constexpr int kScanThreads = 256;
+constexpr int kScanChunkCells = 1792;  // features*bins staged per chunk (3 x 14 KB; Higgs 28x64 in one)
 
-// One CTA. Thread t scans features t, t+T, ... sequentially over bins in the
-// reference order (find_best_threshold, tree.cpp:76-112: fp64 prefix sums,
-// min_data skip/break, strict > so the smallest bin wins); the CTA then takes
-// the max gain with the lowest feature id on ties (find_best_split :172).
+// One CTA per leaf histogram (blockIdx.x selects the leaf of a batch). The
+// scan reproduces find_best_threshold (tree.cpp:76-112) exactly: per feature
+// the prefix sums run sequentially in bin order in fp64 (one thread per
+// feature over a shared-memory copy of the chunk), then every candidate bin's
+// gain is evaluated in parallel with the reference's expression, and the
+// winner is the max gain, lowest feature, lowest bin — the outcome of the
+// reference's strict `>` loops (the `break` when the right side gets too
+// small only removes bins whose right count is already below min_data).
 __global__ void __launch_bounds__(kScanThreads) best_split_kernel(
-    const double* __restrict__ hist, int d, int k, const double* d_totals, const int64_t* d_count,
-    double gt, double ht, int64_t count, int64_t min_data, double lambda, hbg_split* out) {
+    const double* __restrict__ hist_base, int64_t hist_stride, int d, int k,
+    const double* d_totals, int64_t totals_stride, const int64_t* counts_dev, int64_t count0,
+    int64_t count1, double gt, double ht, int64_t min_data, double lambda, hbg_split* out_base) {
+  const double* hist = hist_base + blockIdx.x * hist_stride;
+  hbg_split* out = out_base + blockIdx.x;
   if (d_totals) {
-    gt = d_totals[0];
-    ht = d_totals[1];
+    gt = d_totals[blockIdx.x * totals_stride];
+    ht = d_totals[blockIdx.x * totals_stride + 1];
   }
-  if (d_count) count = *d_count;
-  Cand best{0.0, -1, -1, 0.0, 0.0, 0};
-  if (!(count < 2 * min_data || count < 2)) {  // early exit, tree.cpp:165
-    const size_t D = static_cast<size_t>(d) * k;
-    for (int f = threadIdx.x; f < d; f += blockDim.x) {
-      const double* hg = hist + static_cast<size_t>(f) * k;
-      const double* hh = hg + D;
-      const double* hc = hg + 2 * D;
+  const int64_t count = counts_dev ? counts_dev[blockIdx.x] : (blockIdx.x == 0 ? count0 : count1);
+  __shared__ double pg[kScanChunkCells], ph[kScanChunkCells];
+  __shared__ int64_t pc[kScanChunkCells];
+  __shared__ Cand red[kScanThreads];
+  Cand best{0.0, -1, -1};
+  const bool splittable = !(count < 2 * min_data || count < 2);  // tree.cpp:165
+  const size_t D = static_cast<size_t>(d) * k;
+  const int fchunk = max(1, kScanChunkCells / k);
+  for (int f0 = 0; splittable && f0 < d; f0 += fchunk) {
+    const int nf = min(fchunk, d - f0);
+    const int cells = nf * k;
+    __syncthreads();
+    for (int i = threadIdx.x; i < cells; i += blockDim.x) {
+      const size_t o = static_cast<size_t>(f0) * k + i;
+      pg[i] = hist[o];
+      ph[i] = hist[D + o];
+      pc[i] = static_cast<int64_t>(hist[2 * D + o]);
+    }
+    __syncthreads();
+    for (int f = threadIdx.x; f < nf; f += blockDim.x) {  // sequential prefix, bin order
       double lg = 0.0, lh = 0.0;
       int64_t lc = 0;
-      for (int b = 0; b < k - 1; ++b) {
-        lg += hg[b];
-        lh += hh[b];
-        lc += static_cast<int64_t>(hc[b]);
-        if (lc < min_data) continue;
-        const int64_t rc = count - lc;
-        if (rc < min_data) break;
-        const double gain = gain_of(lg, lh, gt - lg, ht - lh, lambda);
-        if (gain <= 0.0) continue;
-        if (best.f < 0 || gain > best.gain || (gain == best.gain && f < best.f)) {
-          best = Cand{gain, f, b, lg, lh, lc};
-        }
+      for (int b = 0; b < k; ++b) {
+        lg += pg[f * k + b];
+        lh += ph[f * k + b];
+        lc += pc[f * k + b];
+        pg[f * k + b] = lg;
+        ph[f * k + b] = lh;
+        pc[f * k + b] = lc;
       }
     }
+    __syncthreads();
+    for (int i = threadIdx.x; i < cells; i += blockDim.x) {
+      const int f = i / k, b = i - f * k;
+      if (b >= k - 1) continue;  // thresholds 0 .. k-2
+      const int64_t lc = pc[i];
+      const int64_t rc = count - lc;
+      if (lc < min_data || rc < min_data) continue;
+      const double lg = pg[i], lh = ph[i];
+      const double gain = gain_of(lg, lh, gt - lg, ht - lh, lambda);
+      if (gain <= 0.0) continue;
+      const Cand c{gain, f0 + f, b};
+      if (better(c, best)) best = c;
+    }
   }
-  __shared__ Cand red[kScanThreads];
   red[threadIdx.x] = best;
   __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s && better(red[threadIdx.x + s], red[threadIdx.x]))
-      red[threadIdx.x] = red[threadIdx.x + s];
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st && better(red[threadIdx.x + st], red[threadIdx.x]))
+      red[threadIdx.x] = red[threadIdx.x + st];
     __syncthreads();
   }
   if (threadIdx.x == 0) {
     const Cand c = red[0];
-    hbg_split o;
+    hbg_split o{};
     o.feature = c.f;
     o.threshold_bin = c.b;
-    o.gain = c.gain;
-    o.left_grad = c.lg;
-    o.left_hess = c.lh;
-    o.left_count = c.lc;
-    o.right_grad = gt - c.lg;
-    o.right_hess = ht - c.lh;
-    o.right_count = count - c.lc;
-    o.left_value = leaf_value(c.lg, c.lh, lambda);
-    o.right_value = leaf_value(gt - c.lg, ht - c.lh, lambda);
-    if (c.f < 0) {
+    if (c.f >= 0) {
+      // recompute the winner's left sums in the reference's sequential order
+      const double* hg = hist + static_cast<size_t>(c.f) * k;
+      double lg = 0.0, lh = 0.0;
+      int64_t lc = 0;
+      for (int b = 0; b <= c.b; ++b) {
+        lg += hg[b];
+        lh += hg[D + b];
+        lc += static_cast<int64_t>(hg[2 * D + b]);
+      }
+      o.gain = c.gain;
+      o.left_grad = lg;
+      o.left_hess = lh;
+      o.left_count = lc;
+      o.right_grad = gt - lg;
+      o.right_hess = ht - lh;
+      o.right_count = count - lc;
+      o.left_value = leaf_value(lg, lh, lambda);
+      o.right_value = leaf_value(gt - lg, ht - lh, lambda);
+    } else {
       o.threshold_bin = -1;
-      o.gain = 0.0;
     }
     *out = o;
   }
@@ -207,7 +258,7 @@ void launch_gather(const int32_t* idx, int64_t n, const float* g, const float* h
   gather_kernel<<<static_cast<unsigned>(blocks), kGatherThreads, 0, s>>>(idx, n, g, h, lg, lh,
                                                                          std::max<int64_t>(chunk, 1), scratch);
   HBG_LAUNCH_CHECK();
-  gather_finalize_kernel<<<1, 32, 0, s>>>(scratch, static_cast<int>(blocks), totals);
+  gather_finalize_kernel<<<1, 256, 0, s>>>(scratch, static_cast<int>(blocks), totals);
   HBG_LAUNCH_CHECK();
 }
 
@@ -228,12 +279,19 @@ void launch_hist_to_bins(const double* d_hist, int64_t cells, hbg_bin* d_bins, c
 void launch_best_split(const double* d_hist, int d, int k, const double* d_totals,
                        const int64_t* d_count, double gt, double ht, int64_t count,
                        int64_t min_data, double lambda, hbg_split* out, cudaStream_t s) {
-  int threads = std::min(kScanThreads, std::max(32, (d + 31) / 32 * 32));
-  // power of two for the tree reduction
-  int p2 = 32;
-  while (p2 < threads) p2 <<= 1;
-  best_split_kernel<<<1, p2, 0, s>>>(d_hist, d, k, d_totals, d_count, gt, ht, count, min_data,
-                                     lambda, out);
+  launch_best_split_batch(d_hist, 0, 1, d, k, d_totals, 0, d_count, count, 0, gt, ht, min_data,
+                          lambda, out, s);
+}
+
+void launch_best_split_batch(const double* d_hist, int64_t hist_stride, int leaves, int d, int k,
+                             const double* d_totals, int64_t totals_stride, const int64_t* d_counts,
+                             int64_t count0, int64_t count1, double gt, double ht, int64_t min_data,
+                             double lambda, hbg_split* out, cudaStream_t s) {
+  require(k <= kScanChunkCells, "max_bin too large for the split scan");
+  require(leaves >= 1 && leaves <= 2, "split-scan batches hold one or two leaves");
+  best_split_kernel<<<leaves, kScanThreads, 0, s>>>(d_hist, hist_stride, d, k, d_totals, totals_stride,
+                                                   d_counts, count0, count1, gt, ht, min_data, lambda,
+                                                   out);
   HBG_LAUNCH_CHECK();
 }
 

@@ -101,45 +101,54 @@ __global__ void __launch_bounds__(kPartThreads) partition_count_kernel(PartArgs 
   }
 }
 
-// Pass 2 (one CTA): exclusive scan of the block left counts, fixed-order
+// Pass 2 (one CTA): exclusive scan of the block left counts and fixed-order
 // fp64 child totals. out_totals = {gl, hl, gr, hr}, *left_total = rows left.
-__global__ void __launch_bounds__(1024) partition_scan_kernel(const int32_t* block_left,
-                                                              const double* block_sums, int nb,
-                                                              int64_t* block_off, double* out_totals,
-                                                              int64_t* left_total) {
-  const int t = threadIdx.x, T = blockDim.x;
-  const int chunk = (nb + T - 1) / T;
+// Thread t owns a contiguous run of blocks; runs are combined by a pairwise
+// tree in thread order, so the totals do not depend on timing.
+constexpr int kScanT = 256;
+
+__global__ void __launch_bounds__(kScanT) partition_scan_kernel(const int32_t* block_left,
+                                                                const double* block_sums, int nb,
+                                                                int64_t* block_off, double* out_totals,
+                                                                int64_t* left_total) {
+  const int t = threadIdx.x;
+  const int chunk = (nb + kScanT - 1) / kScanT;
   const int b0 = min(nb, t * chunk), b1 = min(nb, b0 + chunk);
   int64_t local = 0;
   double v[4] = {0.0, 0.0, 0.0, 0.0};
   for (int b = b0; b < b1; ++b) {
     local += block_left[b];
+#pragma unroll
     for (int j = 0; j < 4; ++j) v[j] += block_sums[4 * b + j];
   }
-  __shared__ int64_t ss[1024];
-  __shared__ double sv[4][1024];
+  __shared__ int64_t ss[kScanT];
+  __shared__ double sv[4][kScanT];
   ss[t] = local;
+#pragma unroll
   for (int j = 0; j < 4; ++j) sv[j][t] = v[j];
   __syncthreads();
-  // inclusive Hillis-Steele scan of the per-thread counts
-  for (int off = 1; off < T; off <<= 1) {
+  for (int off = 1; off < kScanT; off <<= 1) {  // inclusive Hillis-Steele scan of counts
     const int64_t x = t >= off ? ss[t - off] : 0;
     __syncthreads();
     ss[t] += x;
     __syncthreads();
   }
-  int64_t run = ss[t] - local;  // exclusive prefix of this thread's chunk
+  int64_t run = ss[t] - local;  // exclusive prefix of this thread's run
   for (int b = b0; b < b1; ++b) {
     block_off[b] = run;
     run += block_left[b];
   }
-  if (t == 0) {
-    *left_total = ss[T - 1];
-    for (int j = 0; j < 4; ++j) {
-      double s = 0.0;
-      for (int i = 0; i < T; ++i) s += sv[j][i];  // thread order = block order
-      out_totals[j] = s;
+  for (int st = kScanT / 2; st > 0; st >>= 1) {  // pairwise tree, fixed shape
+    if (t < st) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) sv[j][t] += sv[j][t + st];
     }
+    __syncthreads();
+  }
+  if (t == 0) {
+    *left_total = ss[kScanT - 1];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) out_totals[j] = sv[j][0];
   }
 }
 
@@ -238,7 +247,7 @@ void launch_partition(const int32_t* rows, const float* g, const float* h, int64
   a.block_sums = block_sums;
   partition_count_kernel<<<static_cast<unsigned>(nb), kPartThreads, 0, s>>>(a);
   HBG_LAUNCH_CHECK();
-  partition_scan_kernel<<<1, 1024, 0, s>>>(block_left, block_sums, static_cast<int>(nb), block_off,
+  partition_scan_kernel<<<1, kScanT, 0, s>>>(block_left, block_sums, static_cast<int>(nb), block_off,
                                            d_totals, d_left);
   HBG_LAUNCH_CHECK();
   partition_scatter_kernel<<<static_cast<unsigned>(nb), kPartThreads, 0, s>>>(
