@@ -166,6 +166,24 @@ int hbg_grow_tree(hbg_dataset* ds, const float* d_grad, const float* d_hess,
                   const hbg_grow_params* params, hbg_split* split_log, int32_t* num_splits,
                   hbg_tree_node* nodes, int32_t* num_nodes, void* stream);
 
+/* ---- row-sharded growth ----
+ * One process (or thread) per GPU; each rank's dataset and d_grad/d_hess hold
+ * its own rows (hbg_dataset_create on columns + row_begin). The hook sums
+ * n doubles in place across ranks on `stream` (the leaf histograms, SoA fp64
+ * with exact counts, and leaf totals), so every rank scans identical
+ * histograms and grows the identical tree. Returns HBG_OK or an error status.
+ * hbg_comm_allreduce (below) is the NCCL implementation. */
+typedef int (*hbg_allreduce_fn)(double* d_buf, int64_t n_values, void* stream, void* ctx);
+int hbg_grow_tree_sharded(hbg_dataset* ds, const float* d_grad, const float* d_hess,
+                          const hbg_grow_params* params, hbg_allreduce_fn allreduce, void* ctx,
+                          hbg_split* split_log, int32_t* num_splits, hbg_tree_node* nodes,
+                          int32_t* num_nodes, void* stream);
+
+/* reduce_private_histograms (histogram.cpp:147-157) on the device: d_out =
+ * sum of nparts device buffers of n_values doubles, added in part order. */
+int hbg_reduce_histograms_device(const double* const* d_parts, int32_t nparts, int64_t n_values,
+                                 double* d_out, void* stream);
+
 /* ---- measurement hooks (bench.py roofline) ----
  * When enabled, the handle records a CUDA event pair around every histogram
  * kernel launch (in-stream, no host sync). hbg_dataset_kernel_time waits for

@@ -191,8 +191,9 @@ double leaf_value(double g, double h, double lambda) {  // tree.cpp:59-64
 struct OpenLeaf {  // tree.cpp:132-136
   int node;
   int buf;
-  int64_t begin, count;
-  double grad, hess;
+  int64_t begin, count;  // this rank's rows of the leaf: [begin, begin+count) of buffer `buf`
+  int64_t gcount;        // rows of the leaf over all ranks
+  double grad, hess;     // global totals
   int slot;
   bool has_best;
   hbg_split best;
@@ -201,17 +202,32 @@ struct OpenLeaf {  // tree.cpp:132-136
 // Per-split device results copied back in one transfer.
 struct SplitResults {
   hbg_split split[2];
-  double totals[4];  // gl, hl, gr, hr (children of the split just executed)
-  int64_t left;
-  double root[2];
+  double totals[4];  // gl, hl, gr, hr (children of the split just executed; global)
+  int64_t left;      // this rank's rows sent left
+  double root[3];    // root grad, hess, rows (global)
+};
+
+// Row-sharded growth: every rank holds its own rows; the leaf
+// histograms and totals are summed across ranks by `allreduce` (NCCL in
+// production, hbg_comm_allreduce), so every rank scans identical histograms
+// and takes identical decisions. allreduce == nullptr: single rank.
+struct Reducer {
+  hbg_allreduce_fn fn;
+  void* ctx;
+  void operator()(double* buf, int64_t n, cudaStream_t s) const {
+    if (!fn) return;
+    const int st = fn(buf, n, s, ctx);
+    if (st != HBG_OK) throw Error(st, std::string("allreduce hook failed: ") + hbg_last_error());
+  }
 };
 
 void grow_tree_impl(hbg_dataset* ds, const float* d_grad, const float* d_hess,
-                    const hbg_grow_params& P, hbg_split* split_log, int32_t* num_splits,
-                    hbg_tree_node* nodes_out, int32_t* num_nodes, cudaStream_t s) {
+                    const hbg_grow_params& P, const Reducer& reduce, hbg_split* split_log,
+                    int32_t* num_splits, hbg_tree_node* nodes_out, int32_t* num_nodes, cudaStream_t s) {
   const hbg_layout& L = ds->layout;
   require(P.num_leaves >= 1, "num_leaves must be at least 1");
   require(P.min_data_in_leaf >= 0, "min_data_in_leaf must be non-negative");
+  const bool sharded = reduce.fn != nullptr;
   const int64_t N = L.num_rows;
   const int d = L.num_features, k = L.max_bin;
   const size_t D3 = 3 * static_cast<size_t>(d) * k;
@@ -242,7 +258,8 @@ void grow_tree_impl(hbg_dataset* ds, const float* d_grad, const float* d_hess,
     HBG_CUDA(cudaStreamSynchronize(s));
   };
 
-  // Root: ordered buffer 0 = (iota, g, h); totals in a fixed order.
+  // Root: ordered buffer 0 = (iota, g, h); totals in a fixed order; global
+  // totals and row count (summed across ranks).
   launch_iota(rows[0], N, s);
   if (N > 0) {
     HBG_CUDA(cudaMemcpyAsync(gb[0], d_grad, static_cast<size_t>(N) * 4, cudaMemcpyDeviceToDevice, s));
@@ -250,23 +267,26 @@ void grow_tree_impl(hbg_dataset* ds, const float* d_grad, const float* d_hess,
   }
   launch_gather(rows[0], N, d_grad, d_hess, nullptr, nullptr, dres->root,
                 static_cast<double*>(scratch), s);
-  std::vector<OpenLeaf> pool;
-  OpenLeaf root{0, 0, 0, N, 0.0, 0.0, -1, false, {}};
-  const bool root_split = P.num_leaves >= 2 && splittable(N);
-  if (root_split) {
-    root.slot = free_slots.back();
-    free_slots.pop_back();
-    build_device(ds, rows[0], N, gb[0], hb[0], HBG_GH_LEAF_ALIGNED, slot_ptr(root.slot), s);
-    launch_best_split(slot_ptr(root.slot), d, k, dres->root, nullptr, 0.0, 0.0, N, P.min_data_in_leaf,
-                      P.lambda, &dres->split[0], s);
-  }
+  hres->root[2] = static_cast<double>(N);  // pinned staging; the stream orders the copy
+  HBG_CUDA(cudaMemcpyAsync(&dres->root[2], &hres->root[2], sizeof(double), cudaMemcpyHostToDevice, s));
+  reduce(dres->root, 3, s);
   sync_results();
-  root.grad = hres->root[0];
-  root.hess = hres->root[1];
+  const int64_t NG = static_cast<int64_t>(hres->root[2]);
+  std::vector<OpenLeaf> pool;
+  OpenLeaf root{0, 0, 0, N, NG, hres->root[0], hres->root[1], -1, false, {}};
   nodes.push_back(hbg_tree_node{-1, -1, -1, -1, leaf_value(root.grad, root.hess, P.lambda)});
   if (P.num_leaves >= 2) {
-    root.has_best = root_split && hres->split[0].feature >= 0;
-    root.best = hres->split[0];
+    if (splittable(NG)) {
+      root.slot = free_slots.back();
+      free_slots.pop_back();
+      build_device(ds, rows[0], N, gb[0], hb[0], HBG_GH_LEAF_ALIGNED, slot_ptr(root.slot), s);
+      reduce(slot_ptr(root.slot), static_cast<int64_t>(D3), s);
+      launch_best_split(slot_ptr(root.slot), d, k, dres->root, nullptr, 0.0, 0.0, NG,
+                        P.min_data_in_leaf, P.lambda, &dres->split[0], s);
+      sync_results();
+      root.has_best = hres->split[0].feature >= 0;
+      root.best = hres->split[0];
+    }
     pool.push_back(root);
   }
 
@@ -284,13 +304,20 @@ void grow_tree_impl(hbg_dataset* ds, const float* d_grad, const float* d_hess,
     split_log[logged++] = sp;
 
     const int out = 1 - parent.buf;
-    const int64_t nl = sp.left_count, nr = parent.count - sp.left_count;
-    if (nl <= 0 || nr <= 0) throw Error(HBG_ERR_LOGIC, "split produced an empty side");
+    const int64_t gl_n = sp.left_count, gr_n = parent.gcount - sp.left_count;  // global sizes
+    if (gl_n <= 0 || gr_n <= 0) throw Error(HBG_ERR_LOGIC, "split produced an empty side");
     launch_partition(rows[parent.buf] + parent.begin, gb[parent.buf] + parent.begin,
                      hb[parent.buf] + parent.begin, parent.count,
                      reinterpret_cast<const uint8_t*>(ds->packed), L.row_stride_bytes, sp.feature,
                      L.bits_per_bin, sp.threshold_bin, rows[out] + parent.begin, gb[out] + parent.begin,
                      hb[out] + parent.begin, scratch, dres->totals, &dres->left, s);
+    reduce(dres->totals, 4, s);  // global child totals
+    int64_t nl_local = gl_n;
+    if (sharded) {  // this rank's left count is needed before the children can be addressed
+      HBG_CUDA(cudaMemcpyAsync(&hres->left, &dres->left, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      HBG_CUDA(cudaStreamSynchronize(s));
+      nl_local = hres->left;
+    }
 
     const int left_id = static_cast<int>(nodes.size()), right_id = left_id + 1;
     hbg_tree_node& pn = nodes[static_cast<size_t>(parent.node)];
@@ -303,37 +330,47 @@ void grow_tree_impl(hbg_dataset* ds, const float* d_grad, const float* d_hess,
     nodes.push_back(hbg_tree_node{-1, -1, -1, -1, 0.0});
     ++leaves;
 
-    OpenLeaf lo{left_id, out, parent.begin, nl, 0.0, 0.0, -1, false, {}};
-    OpenLeaf ro{right_id, out, parent.begin + nl, nr, 0.0, 0.0, -1, false, {}};
+    OpenLeaf lo{left_id, out, parent.begin, nl_local, gl_n, 0.0, 0.0, -1, false, {}};
+    OpenLeaf ro{right_id, out, parent.begin + nl_local, parent.count - nl_local, gr_n, 0.0, 0.0, -1,
+                false, {}};
     const bool scan = leaves < P.num_leaves;
-    const bool lsplit = scan && splittable(nl), rsplit = scan && splittable(nr);
+    const bool lsplit = scan && splittable(gl_n), rsplit = scan && splittable(gr_n);
     if (lsplit || rsplit) {
-      // histogram of the smaller child; the larger one = parent - smaller, in
-      // the parent's slot (ties build the left child)
-      OpenLeaf& small = nl <= nr ? lo : ro;
-      OpenLeaf& large = nl <= nr ? ro : lo;
+      // histogram of the globally smaller child; the larger = parent - smaller
+      // in the parent's slot (ties build the left child)
+      OpenLeaf& small = gl_n <= gr_n ? lo : ro;
+      OpenLeaf& large = gl_n <= gr_n ? ro : lo;
       small.slot = free_slots.back();
       free_slots.pop_back();
       large.slot = parent.slot;
       parent.slot = -1;
-      build_device(ds, rows[out] + small.begin, small.count, gb[out] + small.begin,
-                   hb[out] + small.begin, HBG_GH_LEAF_ALIGNED, slot_ptr(small.slot), s,
-                   slot_ptr(large.slot), slot_ptr(large.slot));  // larger = parent - smaller
+      if (!sharded) {
+        build_device(ds, rows[out] + small.begin, small.count, gb[out] + small.begin,
+                     hb[out] + small.begin, HBG_GH_LEAF_ALIGNED, slot_ptr(small.slot), s,
+                     slot_ptr(large.slot), slot_ptr(large.slot));  // subtraction fused
+      } else {
+        build_device(ds, rows[out] + small.begin, small.count, gb[out] + small.begin,
+                     hb[out] + small.begin, HBG_GH_LEAF_ALIGNED, slot_ptr(small.slot), s);
+        reduce(slot_ptr(small.slot), static_cast<int64_t>(D3), s);  // global smaller child
+        launch_subtract(slot_ptr(large.slot), slot_ptr(small.slot), slot_ptr(large.slot),
+                        static_cast<int64_t>(D3), s);
+      }
       if (lsplit && rsplit) {  // both children's scans in one launch
         launch_best_split_batch(slot_ptr(lo.slot), slot_ptr(ro.slot) - slot_ptr(lo.slot), 2, d, k,
-                                dres->totals, 2, nullptr, nl, nr, 0.0, 0.0, P.min_data_in_leaf,
+                                dres->totals, 2, nullptr, gl_n, gr_n, 0.0, 0.0, P.min_data_in_leaf,
                                 P.lambda, &dres->split[0], s);
       } else if (lsplit) {
-        launch_best_split(slot_ptr(lo.slot), d, k, dres->totals, nullptr, 0.0, 0.0, nl,
+        launch_best_split(slot_ptr(lo.slot), d, k, dres->totals, nullptr, 0.0, 0.0, gl_n,
                           P.min_data_in_leaf, P.lambda, &dres->split[0], s);
       } else {
-        launch_best_split(slot_ptr(ro.slot), d, k, dres->totals + 2, nullptr, 0.0, 0.0, nr,
+        launch_best_split(slot_ptr(ro.slot), d, k, dres->totals + 2, nullptr, 0.0, 0.0, gr_n,
                           P.min_data_in_leaf, P.lambda, &dres->split[1], s);
       }
     }
     if (parent.slot >= 0) free_slots.push_back(parent.slot);
     sync_results();
-    if (hres->left != nl) throw Error(HBG_ERR_LOGIC, "partition disagrees with the histogram counts");
+    if (!sharded && hres->left != gl_n)
+      throw Error(HBG_ERR_LOGIC, "partition disagrees with the histogram counts");
     lo.grad = hres->totals[0];
     lo.hess = hres->totals[1];
     ro.grad = hres->totals[2];
@@ -376,6 +413,7 @@ int hbg_dataset_create(const uint8_t* const* columns, int32_t num_features, int6
     HBG_CUDA(cudaGetDeviceCount(&ndev));
     require(device >= 0 && device < ndev, "device ordinal out of range");
     DeviceGuard dg(device);
+    configure_kernels(device);
     auto ds = std::make_unique<hbg_dataset>();
     hbg_layout& L = ds->layout;
     L.num_rows = num_rows;
@@ -584,8 +622,34 @@ int hbg_grow_tree(hbg_dataset* ds, const float* d_grad, const float* d_hess,
     require(ds->layout.num_rows == 0 || (d_grad != nullptr && d_hess != nullptr),
             "null gradient/hessian pointer");
     DeviceGuard dg(ds->layout.device);
-    grow_tree_impl(ds, d_grad, d_hess, *params, split_log, num_splits, nodes, num_nodes,
-                   static_cast<cudaStream_t>(stream));
+    grow_tree_impl(ds, d_grad, d_hess, *params, Reducer{nullptr, nullptr}, split_log, num_splits,
+                   nodes, num_nodes, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int hbg_grow_tree_sharded(hbg_dataset* ds, const float* d_grad, const float* d_hess,
+                          const hbg_grow_params* params, hbg_allreduce_fn allreduce, void* ctx,
+                          hbg_split* split_log, int32_t* num_splits, hbg_tree_node* nodes,
+                          int32_t* num_nodes, void* stream) {
+  return guarded([&] {
+    check_ds(ds);
+    require(params != nullptr && split_log != nullptr && num_splits != nullptr &&
+                num_nodes != nullptr && allreduce != nullptr,
+            "null argument");
+    require(ds->layout.num_rows == 0 || (d_grad != nullptr && d_hess != nullptr),
+            "null gradient/hessian pointer");
+    DeviceGuard dg(ds->layout.device);
+    grow_tree_impl(ds, d_grad, d_hess, *params, Reducer{allreduce, ctx}, split_log, num_splits,
+                   nodes, num_nodes, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int hbg_reduce_histograms_device(const double* const* d_parts, int32_t nparts, int64_t n_values,
+                                 double* d_out, void* stream) {
+  return guarded([&] {
+    require(nparts >= 1 && d_parts != nullptr && d_out != nullptr && n_values >= 0, "bad arguments");
+    std::vector<const double*> parts(d_parts, d_parts + nparts);
+    launch_reduce_parts(parts, n_values, d_out, static_cast<cudaStream_t>(stream));
   });
 }
 

