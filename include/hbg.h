@@ -179,6 +179,17 @@ int hbg_grow_tree_sharded(hbg_dataset* ds, const float* d_grad, const float* d_h
                           hbg_split* split_log, int32_t* num_splits, hbg_tree_node* nodes,
                           int32_t* num_nodes, void* stream);
 
+/* NCCL communicator implementing the hook: one process per GPU, the 128-byte
+ * unique id produced by rank 0 is shared out of band. Pass the hbg_comm* as
+ * `ctx` with hbg_comm_allreduce as `allreduce`. */
+#define HBG_COMM_ID_BYTES 128
+typedef struct hbg_comm hbg_comm;
+int hbg_comm_get_unique_id(uint8_t* out /* HBG_COMM_ID_BYTES */);
+int hbg_comm_init(hbg_comm** out, int32_t nranks, int32_t rank, const uint8_t* unique_id,
+                  int32_t device);
+int hbg_comm_destroy(hbg_comm* comm);
+int hbg_comm_allreduce(double* d_buf, int64_t n_values, void* stream, void* ctx);
+
 /* reduce_private_histograms (histogram.cpp:147-157) on the device: d_out =
  * sum of nparts device buffers of n_values doubles, added in part order. */
 int hbg_reduce_histograms_device(const double* const* d_parts, int32_t nparts, int64_t n_values,

@@ -68,6 +68,10 @@ class hbg_grow_params(C.Structure):
                 ("lambda_", C.c_double)]
 
 
+#: hbg_allreduce_fn: int (*)(double* d_buf, int64_t n, void* stream, void* ctx)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
+
+
 class HbgError(RuntimeError):
     """Base class; ``code`` is the HBG_* status."""
 
@@ -120,6 +124,12 @@ EXPORTED_SYMBOLS = (
     "hbg_best_split_device_totals",
     "hbg_find_best_split",
     "hbg_grow_tree",
+    "hbg_grow_tree_sharded",
+    "hbg_comm_get_unique_id",
+    "hbg_comm_init",
+    "hbg_comm_destroy",
+    "hbg_comm_allreduce",
+    "hbg_reduce_histograms_device",
     "hbg_dataset_set_profiling",
     "hbg_dataset_kernel_time",
     "hbg_stream_synchronize",
@@ -163,6 +173,12 @@ def lib() -> C.CDLL:
         L.hbg_find_best_split.argtypes = [_P, C.c_int32, C.c_int32, C.c_double, C.c_double,
                                           C.c_int64, C.c_int64, C.c_double, _P, _P]
         L.hbg_grow_tree.argtypes = [_P, _P, _P, _P, _P, _P, _P, _P, _P]
+        L.hbg_grow_tree_sharded.argtypes = [_P, _P, _P, _P, ALLREDUCE_FN, _P, _P, _P, _P, _P, _P]
+        L.hbg_comm_get_unique_id.argtypes = [_P]
+        L.hbg_comm_init.argtypes = [_P, C.c_int32, C.c_int32, _P, C.c_int32]
+        L.hbg_comm_destroy.argtypes = [_P]
+        L.hbg_comm_allreduce.argtypes = [_P, C.c_int64, _P, _P]
+        L.hbg_reduce_histograms_device.argtypes = [_P, C.c_int32, C.c_int64, _P, _P]
         L.hbg_dataset_set_profiling.argtypes = [_P, C.c_int32]
         L.hbg_dataset_kernel_time.argtypes = [_P, _P, _P]
         L.hbg_stream_synchronize.argtypes = [_P]
@@ -279,6 +295,20 @@ class Dataset:
                                   _ptr(nodes), C.byref(nn), _ptr(stream)))
         return log[: ns.value].copy(), nodes[: nn.value].copy()
 
+    def grow_tree_sharded(self, grad, hess, allreduce, ctx=None, num_leaves: int = 31,
+                          min_data_in_leaf: int = 1, lam: float = 0.0, stream=None):
+        """Row-sharded grow_tree: this rank's rows; `allreduce` (an ALLREDUCE_FN,
+        e.g. Comm.allreduce_fn) sums leaf histograms/totals across ranks."""
+        p = hbg_grow_params(num_leaves, 0, min_data_in_leaf, lam)
+        log = np.zeros(max(num_leaves - 1, 1), dtype=SPLIT_DTYPE)
+        nodes = np.zeros(max(2 * num_leaves - 1, 1), dtype=NODE_DTYPE)
+        ns = C.c_int32()
+        nn = C.c_int32()
+        check(lib().hbg_grow_tree_sharded(self.handle, _ptr(grad), _ptr(hess), C.byref(p), allreduce,
+                                          _ptr(ctx), _ptr(log), C.byref(ns), _ptr(nodes), C.byref(nn),
+                                          _ptr(stream)))
+        return log[: ns.value].copy(), nodes[: nn.value].copy()
+
     def set_profiling(self, enabled: bool) -> None:
         """Record CUDA events around each histogram kernel launch (measurement only)."""
         check(lib().hbg_dataset_set_profiling(self.handle, 1 if enabled else 0))
@@ -377,6 +407,40 @@ def best_split_device_totals(hist, num_features: int, max_bin: int, totals, coun
 
 def hist_to_bins_device(hist, num_features: int, max_bin: int, bins, stream=None) -> None:
     check(lib().hbg_hist_to_bins_device(_ptr(hist), num_features, max_bin, _ptr(bins), _ptr(stream)))
+
+
+def reduce_histograms_device(parts, n_values: int, out, stream=None) -> None:
+    """reduce_private_histograms (histogram.cpp:147-157): out = sum of parts in order."""
+    arr = (C.c_void_p * len(parts))(*[_ptr(p).value for p in parts])
+    check(lib().hbg_reduce_histograms_device(arr, len(parts), n_values, _ptr(out), _ptr(stream)))
+
+
+class Comm:
+    """NCCL communicator for row-sharded growth (one process per GPU)."""
+
+    ID_BYTES = 128
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * Comm.ID_BYTES)()
+        check(lib().hbg_comm_get_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, nranks: int, rank: int, unique_id: bytes, device: int):
+        buf = (C.c_uint8 * Comm.ID_BYTES).from_buffer_copy(unique_id)
+        h = C.c_void_p()
+        check(lib().hbg_comm_init(C.byref(h), nranks, rank, buf, device))
+        self._h = h
+        self.allreduce_fn = ALLREDUCE_FN(C.cast(lib().hbg_comm_allreduce, C.c_void_p).value)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            check(lib().hbg_comm_destroy(self._h))
+            self._h = None
 
 
 def stats_close(a, b, tolerance: float):

@@ -44,6 +44,10 @@ int guarded(F&& f) {
   }
 }
 
+int guarded_call_impl(void (*fn)(void*), void* arg) {
+  return guarded([&] { fn(arg); });
+}
+
 // A grow-only device buffer.
 struct DevBuf {
   void* p = nullptr;

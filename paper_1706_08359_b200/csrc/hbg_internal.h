@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "hbg.h"
@@ -113,5 +114,12 @@ void configure_tree_kernels();
 void configure_kernels(int device);  // carveout for every non-histogram kernel, once per device
 
 int sm_count(int device);
+
+// Runs f, mapping exceptions to HBG_* status codes + the thread-local last error.
+int guarded_call_impl(void (*fn)(void*), void* arg);
+template <typename F>
+int guarded_call(F&& f) {
+  return guarded_call_impl([](void* p) { (*static_cast<F*>(p))(); }, &f);
+}
 
 }  // namespace hbg

@@ -1,0 +1,97 @@
+"""Row-sharded tree growth on one GPU with an in-process collective (GPU).
+
+Only one GPU is available to the tests, so the N-GPU path is exercised the
+way the reference tests distribution without a cluster: two
+"ranks" run as threads, each owning a row shard (its own hbg Dataset) and
+calling hbg_grow_tree_sharded; the allreduce hook is a fake collective that
+sums the ranks' device buffers in rank order with hbg_reduce_histograms_device
+(the reduce_private_histograms analogue) and hands the sum back to both. The
+sharded trees must be identical on both ranks and equal the reference's tree
+on the unsharded data. hbg_comm_allreduce (NCCL) plugs into the same hook.
+"""
+import ctypes as C
+import threading
+
+import numpy as np
+import pytest
+
+from paper_1706_08359_b200 import dist as hdist
+
+pytestmark = pytest.mark.gpu
+
+
+class FakeCollective:
+    def __init__(self, hbg, world, max_values, torch):
+        self.hbg = hbg
+        self.world = world
+        self.barrier = threading.Barrier(world)
+        self.bufs = [None] * world
+        self.tmp = torch.empty(max_values, dtype=torch.float64, device="cuda:0")
+        self.calls = 0
+        self.fns = [hbg.ALLREDUCE_FN(self._make(r)) for r in range(world)]
+
+    def _make(self, rank):
+        lib = self.hbg.lib()
+
+        def cb(buf, n, stream, ctx):
+            try:
+                lib.hbg_stream_synchronize(stream)
+                self.bufs[rank] = buf
+                self.barrier.wait()
+                if rank == 0:
+                    self.calls += 1
+                    parts = (C.c_void_p * self.world)(*self.bufs)
+                    assert n <= self.tmp.numel()
+                    lib.hbg_reduce_histograms_device(parts, self.world, n, C.c_void_p(self.tmp.data_ptr()), None)
+                    lib.hbg_stream_synchronize(None)
+                self.barrier.wait()
+                lib.hbg_reduce_histograms_device((C.c_void_p * 1)(self.tmp.data_ptr()), 1, n, C.c_void_p(buf), stream)
+                lib.hbg_stream_synchronize(stream)
+                self.barrier.wait()
+                return 0
+            except Exception:  # never raise through the C boundary
+                self.barrier.abort()
+                return 5
+
+        return cb
+
+
+@pytest.mark.parametrize("rows,d,k,leaves,min_data", [(40000, 28, 64, 63, 50), (30001, 12, 16, 31, 100),
+                                                     (20000, 9, 256, 31, 80)])
+def test_two_rank_sharded_tree_equals_reference(hbg, oracle, rows, d, k, leaves, min_data):
+    import torch
+
+    world = 2
+    cols = oracle.gen_synthetic_bins(rows, d, k, 5)
+    g, h = oracle.gen_grad_hess(rows, 5)
+    g = g + 0.3 * (cols[1].astype(np.float64) > k // 2)
+    coll = FakeCollective(hbg, world, 3 * d * k + 64, torch)
+    results = [None] * world
+    errors = []
+
+    def run(rank):
+        try:
+            b, e = hdist.shard_rows(rows, rank, world)
+            with hbg.Dataset(np.ascontiguousarray(cols[:, b:e]), k) as ds:
+                tg = torch.from_numpy(g[b:e].astype(np.float32)).cuda()
+                th = torch.from_numpy(h[b:e].astype(np.float32)).cuda()
+                s = torch.cuda.Stream()
+                results[rank] = ds.grow_tree_sharded(tg, th, coll.fns[rank], None, leaves, min_data, 0.0,
+                                                     s.cuda_stream)
+        except Exception as ex:  # surfaced below
+            errors.append(ex)
+            coll.barrier.abort()
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    (log0, nodes0), (log1, nodes1) = results
+    assert log0.tobytes() == log1.tobytes() and nodes0.tobytes() == nodes1.tobytes()  # identical on every rank
+    want_log, want_nodes = oracle.grow_tree(cols, k, g, h, leaves, min_data, 0.0, 64)
+    from test_gpu_parity import _assert_same_tree
+
+    assert _assert_same_tree(log0, nodes0, want_log, want_nodes) == len(want_log)
+    assert coll.calls >= 2 * len(log0)  # totals + smaller-child histogram per split
