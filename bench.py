@@ -248,10 +248,16 @@ def run_hbg(args):
     torch.cuda.set_stream(stream)
     sp = stream.cuda_stream
 
+    comm = None
+    if world > 1:  # NCCL communicator of the library (the sharded allreduce hook)
+        uid = [hbg.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = hbg.Comm(world, rank, uid[0], local)
+
     def step():
         ds.build_histograms_device(ti, n, tg, th, hist, hbg.HBG_GH_LEAF_ALIGNED, sp)
-        if world > 1:
-            dist.all_reduce(hist)  # the per-leaf exchange of row-sharded training
+        if comm is not None:  # the per-leaf exchange of row-sharded training (NCCL over NVLink)
+            hbg.check(hbg.lib().hbg_comm_allreduce(hbg._ptr(hist), hist.numel(), hbg._ptr(sp), comm.handle))
 
     clocks = ClockSampler(local)
     clocks.start()
@@ -387,24 +393,36 @@ def run_hbg(args):
                                   "roofline_frac": algorithmic_bytes(n, d, 16, 4) / (kt / 1e3) / 1e9 / peak}
             ds16.close()
         result["variants"] = var
-    # --- sec/tree: device-resident 255-leaf best-first tree (grow_tree semantics)
-    if not args.no_tree and world == 1:
-        log, _ = ds.grow_tree(tg, th, args.num_leaves, 1, 0.0, sp)  # warm-up (workspace)
+    # --- sec/tree: device-resident 255-leaf best-first tree (grow_tree semantics);
+    # row-sharded over the ranks with the NCCL hook when N > 1
+    if not args.no_tree:
+        def grow():
+            if comm is None:
+                return ds.grow_tree(tg, th, args.num_leaves, 1, 0.0, sp)
+            return ds.grow_tree_sharded(tg, th, comm.allreduce_fn, comm.handle, args.num_leaves, 1, 0.0, sp)
+
+        log, _ = grow()  # warm-up (workspace)
         ds.kernel_time()
         ds.set_profiling(True)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         a.record(stream)
         for _ in range(args.trees):
-            log, nodes = ds.grow_tree(tg, th, args.num_leaves, 1, 0.0, sp)
+            log, nodes = grow()
         b.record(stream)
         torch.cuda.synchronize()
         ds.set_profiling(False)
-        t_tree = a.elapsed_time(b) / args.trees / 1e3
+        t_tree = torch.tensor([a.elapsed_time(b) / args.trees / 1e3], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t_tree, op=dist.ReduceOp.MAX)
+        t_tree = float(t_tree.item())
         km, kl = ds.kernel_time()
-        built = n + int(np.minimum(log["left_count"], log["right_count"])[: max(len(log) - 1, 0)].sum())
+        built = world * n + int(np.minimum(log["left_count"], log["right_count"])[: max(len(log) - 1, 0)].sum())
         result["tree"] = {
             "num_leaves": args.num_leaves, "splits": int(len(log)), "sec_per_tree": t_tree,
+            "rows_total": world * n,
             "hist_rows_built": built, "hist_launches_per_tree": kl / args.trees,
             "hist_kernel_ms_per_tree": km / args.trees,
             "rows_features_per_s_built": built * d / t_tree,
@@ -443,6 +461,8 @@ def run_hbg(args):
         except Exception as e:  # informational leg; never masks the GPU number
             result["cpu_baseline"] = {"error": str(e)}
     ds.close()
+    if comm is not None:
+        comm.close()
     if rank == 0:
         print(json.dumps(result))
     if world > 1:

@@ -158,7 +158,7 @@ void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const fl
     d_idx = static_cast<const int32_t*>(ds->iota.p);
   }
   HistPlan plan = plan_histogram(L.bits_per_bin, L.max_bin, L.num_groups, count, L.device);
-  float* part = static_cast<float*>(ds->part.get(plan.part_values * 12));
+  float* part = static_cast<float*>(ds->part.get(plan.part_values * 12 + 16));
   HistArgs a{};
   a.packed = reinterpret_cast<const uint8_t*>(ds->packed);
   a.row_stride = L.row_stride_bytes;
@@ -175,6 +175,12 @@ void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const fl
   a.part_g = part;
   a.part_h = part + plan.part_values;
   a.part_c = reinterpret_cast<uint32_t*>(part + 2 * plan.part_values);
+  a.direct = plan.nseg == 1 ? 1 : 0;
+  a.d = L.num_features;
+  a.max_bin = L.max_bin;
+  a.out = d_hist;
+  a.parent = parent;
+  a.sibling = sibling;
   if (ds->profiling) {
     auto ev = ds->event_pair();
     HBG_CUDA(cudaEventRecord(ev.first, s));
@@ -184,7 +190,7 @@ void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const fl
   } else {
     launch_histogram(plan, a, s);
   }
-  launch_reduce_partials(plan, a, L.num_features, L.max_bin, d_hist, s, parent, sibling);
+  if (!a.direct) launch_reduce_partials(plan, a, L.num_features, L.max_bin, d_hist, s, parent, sibling);
 }
 
 double leaf_value(double g, double h, double lambda) {  // tree.cpp:59-64

@@ -61,6 +61,14 @@ struct HistArgs {
   float* part_g;
   float* part_h;
   uint32_t* part_c;
+  // direct mode (a single row segment): the CTAs write the final fp64
+  // histogram (and the fused sibling) themselves, no partials / reduce launch
+  int direct;
+  int d;
+  int max_bin;
+  double* out;
+  const double* parent;
+  double* sibling;
 };
 
 HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int device);

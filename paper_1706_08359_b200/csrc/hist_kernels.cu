@@ -280,10 +280,30 @@ __global__ void __launch_bounds__(512, BITS == 4 ? 2 : 1) hist_kernel(HistArgs a
       sg += v.x;
       sh += v.y;
     }
-    const size_t o = (static_cast<size_t>(blockIdx.x) * a.gb + g2) * kCells + c;
-    a.part_g[o] = sg;
-    a.part_h[o] = sh;
-    a.part_c[o] = cnt[static_cast<size_t>(g2) * kCells + c];
+    const uint32_t cc = cnt[static_cast<size_t>(g2) * kCells + c];
+    if (a.direct) {
+      const int bin = c >> 5;
+      const int f = (bi * a.gb + g2) * 32 + (c & 31);
+      if (f < a.d && bin < a.max_bin) {
+        const size_t D = static_cast<size_t>(a.d) * a.max_bin;
+        const size_t o = static_cast<size_t>(f) * a.max_bin + bin;
+        const double dg = sg, dh = sh, dc = cc;
+        a.out[o] = dg;
+        a.out[D + o] = dh;
+        a.out[2 * D + o] = dc;
+        if (a.parent) {
+          const double pg = a.parent[o], ph = a.parent[D + o], pc = a.parent[2 * D + o];
+          a.sibling[o] = pg - dg;
+          a.sibling[D + o] = ph - dh;
+          a.sibling[2 * D + o] = pc - dc;
+        }
+      }
+    } else {
+      const size_t o = (static_cast<size_t>(blockIdx.x) * a.gb + g2) * kCells + c;
+      a.part_g[o] = sg;
+      a.part_h[o] = sh;
+      a.part_c[o] = cc;
+    }
   }
 }
 
@@ -435,6 +455,9 @@ int sm_count(int device) {
   return c;
 }
 
+// Leaves up to this many rows take the single-segment direct path.
+constexpr int64_t kDirectRows = 1024;
+
 HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int device) {
   HistPlan p{};
   p.bits = bits;
@@ -467,6 +490,18 @@ HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int de
   p.warps = gb * p.wpg;
   p.smem = p.warps * ghw + gb * cntw;
   p.nblocks = (num_groups + gb - 1) / gb;
+  if (n <= kDirectRows) {
+    // one row segment: each CTA folds and writes the final histogram itself
+    const int64_t w = std::min<int64_t>(p.wpg, std::max<int64_t>(2, (n + 63) / 64));
+    p.wpg = static_cast<int>(w);
+    p.warps = gb * p.wpg;
+    p.smem = p.warps * ghw + gb * cntw;
+    p.nseg = 1;
+    p.seg_len = std::max<int64_t>(32, (n + 31) / 32 * 32);
+    p.ctas = p.nblocks;
+    p.part_values = 0;
+    return p;
+  }
   const int occ = occupancy_for(bits, p.k_alloc, p.warps * 32, p.smem, device);
   const int64_t target = static_cast<int64_t>(sm_count(device)) * occ;
   int64_t nseg = (target + p.nblocks - 1) / p.nblocks;

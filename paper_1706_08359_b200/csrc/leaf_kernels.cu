@@ -162,28 +162,50 @@ __global__ void __launch_bounds__(kScanThreads) best_split_kernel(
     const int nf = min(fchunk, d - f0);
     const int cells = nf * k;
     __syncthreads();
+    // stage transposed, [bin][feature]: the per-feature prefix threads then
+    // read consecutive addresses (no bank conflicts)
     for (int i = threadIdx.x; i < cells; i += blockDim.x) {
       const size_t o = static_cast<size_t>(f0) * k + i;
-      pg[i] = hist[o];
-      ph[i] = hist[D + o];
-      pc[i] = static_cast<int64_t>(hist[2 * D + o]);
+      const int f = i / k, b = i - f * k;
+      pg[b * nf + f] = hist[o];
+      ph[b * nf + f] = hist[D + o];
+      pc[b * nf + f] = static_cast<int64_t>(hist[2 * D + o]);
     }
     __syncthreads();
-    for (int f = threadIdx.x; f < nf; f += blockDim.x) {  // sequential prefix, bin order
-      double lg = 0.0, lh = 0.0;
-      int64_t lc = 0;
-      for (int b = 0; b < k; ++b) {
-        lg += pg[f * k + b];
-        lh += ph[f * k + b];
-        lc += pc[f * k + b];
-        pg[f * k + b] = lg;
-        ph[f * k + b] = lh;
-        pc[f * k + b] = lc;
+    // sequential prefix in bin order, one thread per (feature, statistic);
+    // loads are batched ahead of the dependent adds
+    for (int t = threadIdx.x; t < 3 * nf; t += blockDim.x) {
+      const int f = t % nf, stat = t / nf;
+      if (stat < 2) {
+        double* a = stat == 0 ? pg : ph;
+        double run = 0.0;
+        for (int b0 = 0; b0 < k; b0 += 8) {
+          double v[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = b0 + j < k ? a[(b0 + j) * nf + f] : 0.0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            run += v[j];
+            if (b0 + j < k) a[(b0 + j) * nf + f] = run;
+          }
+        }
+      } else {
+        int64_t run = 0;
+        for (int b0 = 0; b0 < k; b0 += 8) {
+          int64_t v[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = b0 + j < k ? pc[(b0 + j) * nf + f] : 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            run += v[j];
+            if (b0 + j < k) pc[(b0 + j) * nf + f] = run;
+          }
+        }
       }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < cells; i += blockDim.x) {
-      const int f = i / k, b = i - f * k;
+      const int b = i / nf, f = i - b * nf;
       if (b >= k - 1) continue;  // thresholds 0 .. k-2
       const int64_t lc = pc[i];
       const int64_t rc = count - lc;

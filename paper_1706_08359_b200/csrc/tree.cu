@@ -202,9 +202,88 @@ __global__ void __launch_bounds__(kPartThreads) partition_scatter_kernel(
   }
 }
 
+// Leaves of at most one tile: flags, totals, ranks and the stable scatter in a
+// single CTA (one launch instead of three).
+__global__ void __launch_bounds__(kPartThreads) partition_small_kernel(PartArgs a, int32_t* __restrict__ orow,
+                                                                       float* __restrict__ og, float* __restrict__ oh,
+                                                                       double* out_totals, int64_t* left_total) {
+  __shared__ uint8_t flag[kPartTile];
+  __shared__ double sd[4][kPartThreads / 32];
+  __shared__ int sc[kPartThreads / 32];
+  __shared__ int wl[kPartThreads / 32];
+  __shared__ int wn[kPartThreads / 32];
+  __shared__ int64_t L_sh;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  int c = 0;
+#pragma unroll
+  for (int i = 0; i < kPartItems; ++i) {
+    const int pos = i * kPartThreads + threadIdx.x;
+    if (pos < a.n) {
+      const int32_t row = __ldg(a.rows + pos);
+      const uint32_t byte = __ldg(a.packed + static_cast<int64_t>(row) * a.row_stride + a.byte_off);
+      const bool left = ((byte >> a.shift) & a.mask) <= static_cast<uint32_t>(a.thr);
+      flag[pos] = left ? 1 : 0;
+      const double gv = __ldg(a.g + pos), hv = __ldg(a.h + pos);
+      if (left) {
+        ++c;
+        v[0] += gv;
+        v[1] += hv;
+      } else {
+        v[2] += gv;
+        v[3] += hv;
+      }
+    }
+  }
+  block_reduce_4d1i(v, c, sd, sc);  // thread 0 holds the totals
+  if (threadIdx.x == 0) {
+    L_sh = c;
+    *left_total = c;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) out_totals[j] = v[j];
+  }
+  __syncthreads();
+  const int64_t L = L_sh;
+  int64_t lrun = 0, rrun = 0;
+  for (int i = 0; i < kPartItems; ++i) {
+    const int pos = i * kPartThreads + threadIdx.x;
+    const bool valid = pos < a.n;
+    const bool left = valid && flag[pos];
+    const unsigned lm = __ballot_sync(0xffffffffu, left);
+    const unsigned vm = __ballot_sync(0xffffffffu, valid);
+    if (lane == 0) {
+      wl[w] = __popc(lm);
+      wn[w] = __popc(vm);
+    }
+    __syncthreads();
+    int lbefore = 0, nbefore = 0, ltot = 0, ntot = 0;
+    for (int j = 0; j < kPartThreads / 32; ++j) {
+      if (j < w) {
+        lbefore += wl[j];
+        nbefore += wn[j];
+      }
+      ltot += wl[j];
+      ntot += wn[j];
+    }
+    const unsigned below = (1u << lane) - 1u;
+    if (valid) {
+      const int lrank = lbefore + __popc(lm & below);
+      const int prank = nbefore + __popc(vm & below);
+      const int64_t dst = left ? lrun + lrank : L + rrun + (prank - lrank);
+      orow[dst] = a.rows[pos];
+      og[dst] = a.g[pos];
+      oh[dst] = a.h[pos];
+    }
+    lrun += ltot;
+    rrun += ntot - ltot;
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 void configure_tree_kernels() {
+  set_max_shared_carveout(reinterpret_cast<const void*>(partition_small_kernel));
   set_max_shared_carveout(reinterpret_cast<const void*>(partition_count_kernel));
   set_max_shared_carveout(reinterpret_cast<const void*>(partition_scan_kernel));
   set_max_shared_carveout(reinterpret_cast<const void*>(partition_scatter_kernel));
@@ -251,6 +330,11 @@ void launch_partition(const int32_t* rows, const float* g, const float* h, int64
   a.flags = flags;
   a.block_left = block_left;
   a.block_sums = block_sums;
+  if (n <= kPartTile) {
+    partition_small_kernel<<<1, kPartThreads, 0, s>>>(a, orow, og, oh, d_totals, d_left);
+    HBG_LAUNCH_CHECK();
+    return;
+  }
   partition_count_kernel<<<static_cast<unsigned>(nb), kPartThreads, 0, s>>>(a);
   HBG_LAUNCH_CHECK();
   partition_scan_kernel<<<1, kScanT, 0, s>>>(block_left, block_sums, static_cast<int>(nb), block_off,
