@@ -190,6 +190,19 @@ int hbg_comm_init(hbg_comm** out, int32_t nranks, int32_t rank, const uint8_t* u
 int hbg_comm_destroy(hbg_comm* comm);
 int hbg_comm_allreduce(double* d_buf, int64_t n_values, void* stream, void* ctx);
 
+/* ---- one boosting iteration on the device ----
+ * boost_one_iteration (boosting.cpp:26-51): g,h of the loss at the cached
+ * scores (losses.cpp:24-26 squared, :57-60 logistic; fp64 math, fp32
+ * storage), grow_tree as hbg_grow_tree, then d_scores[row] +=
+ * learning_rate * value(row's leaf). d_targets/d_scores: fp64 device arrays of
+ * num_rows. allreduce may be NULL (single rank) or the row-sharded hook. */
+#define HBG_LOSS_SQUARED 0
+#define HBG_LOSS_LOGISTIC 1
+int hbg_boost_one_iteration(hbg_dataset* ds, const double* d_targets, double* d_scores, int32_t loss,
+                            double learning_rate, const hbg_grow_params* params, hbg_allreduce_fn allreduce,
+                            void* ctx, hbg_split* split_log, int32_t* num_splits, hbg_tree_node* nodes,
+                            int32_t* num_nodes, void* stream);
+
 /* reduce_private_histograms (histogram.cpp:147-157) on the device: d_out =
  * sum of nparts device buffers of n_values doubles, added in part order. */
 int hbg_reduce_histograms_device(const double* const* d_parts, int32_t nparts, int64_t n_values,

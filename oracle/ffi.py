@@ -84,6 +84,8 @@ def lib() -> C.CDLL:
         L.hbo_partition_leaf.restype = _I64
         L.hbo_grow_tree.argtypes = [_P, _I, _I64, _I, _P, _P, _I, _I64, _D, _I, _P, _P, _P, _P, _P, _P, _P]
         L.hbo_stats_close.argtypes = [_D, _D, _D]
+        L.hbo_grad_hess.argtypes = [_I, _P, _P, _I64, _P, _P]
+        L.hbo_boost_one_iteration.argtypes = [_P, _I, _I64, _I, _P, _I, _D, _I, _I64, _D, _I, _P, _P]
         _lib = L
     return _lib
 
@@ -114,6 +116,8 @@ def ref() -> C.CDLL:
         L.ref_build_timed.restype = _D
         L.ref_grow_tree_timed.argtypes = [_P, _P, _P, _I, _I64, _D, _I, _P, _P]
         L.ref_grow_tree_timed.restype = _D
+        L.ref_boost_one_iteration.argtypes = [_P, _P, _I, _D, _I, _I64, _D, _I, _P, _P, _P]
+        L.ref_boost_one_iteration.restype = _D
         _ref = L
     return _ref
 
@@ -234,6 +238,29 @@ def grow_tree(cols: np.ndarray, max_bin: int, g: np.ndarray, h: np.ndarray, num_
     return log[:n].copy(), nodes
 
 
+def grad_hess(loss: int, scores: np.ndarray, targets: np.ndarray):
+    """losses.cpp:24-26 (0 = squared) / :57-60 (1 = logistic)."""
+    n = len(scores)
+    g = np.empty(n)
+    h = np.empty(n)
+    lib().hbo_grad_hess(loss, _ptr(np.ascontiguousarray(scores, dtype=np.float64)),
+                        _ptr(np.ascontiguousarray(targets, dtype=np.float64)), n, _ptr(g), _ptr(h))
+    return g, h
+
+
+def boost_one_iteration(cols, max_bin, targets, scores, loss=0, learning_rate=0.1, num_leaves=31,
+                        min_data_in_leaf=1, lam=0.0, precision=64):
+    """boosting.cpp:26-51 — updates `scores` in place, returns the split log."""
+    d, rows = cols.shape
+    log = np.zeros(max(num_leaves - 1, 1), dtype=SPLIT_DTYPE)
+    assert scores.dtype == np.float64 and scores.flags.c_contiguous
+    n = lib().hbo_boost_one_iteration(_ptr(np.ascontiguousarray(cols)), d, rows, max_bin,
+                                      _ptr(np.ascontiguousarray(targets, dtype=np.float64)), loss,
+                                      learning_rate, num_leaves, min_data_in_leaf, lam, precision,
+                                      _ptr(scores), _ptr(log))
+    return log[:n].copy()
+
+
 # -------------------------------------------------------------- reference API
 def ref_gen_synthetic_bins(rows, features, max_bin, seed=0):
     out = np.empty((features, rows), dtype=np.uint8)
@@ -302,6 +329,14 @@ class RefDataset:
         t = ref().ref_grow_tree_timed(self.h, _ptr(g), _ptr(h), num_leaves, min_data, lam,
                                       precision, _ptr(log), C.byref(n))
         return t, log[: n.value].copy()
+
+    def boost_one_iteration_timed(self, targets, scores, loss=0, learning_rate=0.1, num_leaves=31,
+                                  min_data=1, lam=0.0, precision=32):
+        n = C.c_int()
+        t = ref().ref_boost_one_iteration(self.h, _ptr(np.ascontiguousarray(targets, dtype=np.float64)), loss,
+                                          learning_rate, num_leaves, min_data, lam, precision, _ptr(scores),
+                                          None, C.byref(n))
+        return t
 
     @staticmethod
     def free_leaf(leaf):

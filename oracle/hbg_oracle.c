@@ -473,6 +473,54 @@ int hbo_grow_tree(const uint8_t* cols, int d, int64_t rows, int k, const double*
   return logged;
 }
 
+/* losses.cpp:14,24-26,57-60 */
+void hbo_grad_hess(int loss, const double* scores, const double* targets, int64_t n, double* g,
+                   double* h) {
+  for (int64_t i = 0; i < n; ++i) {
+    if (loss == 0) {
+      g[i] = scores[i] - targets[i];
+      h[i] = 1.0;
+    } else {
+      double p = 1.0 / (1.0 + exp(-scores[i]));
+      g[i] = p - targets[i];
+      double hh = p * (1.0 - p);
+      h[i] = hh > 1e-16 ? hh : 1e-16;
+    }
+  }
+}
+
+/* boosting.cpp:26-51; the score update routes every row through the tree by
+ * its bins (Tree::predict_binned, tree.cpp:47-57). */
+int hbo_boost_one_iteration(const uint8_t* cols, int d, int64_t rows, int k, const double* targets,
+                            int loss, double learning_rate, int num_leaves, int64_t min_data_in_leaf,
+                            double lambda, int precision, double* scores, hbo_split* split_log) {
+  double* g = (double*)malloc(sizeof(double) * (size_t)(rows > 0 ? rows : 1));
+  double* h = (double*)malloc(sizeof(double) * (size_t)(rows > 0 ? rows : 1));
+  int max_nodes = 2 * num_leaves - 1;
+  int32_t* nf = (int32_t*)malloc(sizeof(int32_t) * (size_t)max_nodes);
+  int32_t* nt = (int32_t*)malloc(sizeof(int32_t) * (size_t)max_nodes);
+  int32_t* nl = (int32_t*)malloc(sizeof(int32_t) * (size_t)max_nodes);
+  int32_t* nr = (int32_t*)malloc(sizeof(int32_t) * (size_t)max_nodes);
+  double* nv = (double*)malloc(sizeof(double) * (size_t)max_nodes);
+  int nn = 0;
+  hbo_grad_hess(loss, scores, targets, rows, g, h);
+  int logged = hbo_grow_tree(cols, d, rows, k, g, h, num_leaves, min_data_in_leaf, lambda, precision,
+                             split_log, nf, nt, nl, nr, nv, &nn);
+  for (int64_t i = 0; i < rows; ++i) {
+    int at = 0;
+    while (nf[at] >= 0) at = cols[(int64_t)nf[at] * rows + i] <= nt[at] ? nl[at] : nr[at];
+    scores[i] += learning_rate * nv[at];
+  }
+  free(g);
+  free(h);
+  free(nf);
+  free(nt);
+  free(nl);
+  free(nr);
+  free(nv);
+  return logged;
+}
+
 /* histogram.cpp:12-15 */
 int hbo_stats_close(double a, double b, double tolerance) {
   double scale = 1.0;

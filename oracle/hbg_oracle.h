@@ -106,6 +106,17 @@ int hbo_grow_tree(const uint8_t* cols, int d, int64_t rows, int k, const double*
                   int32_t* node_threshold_bin, int32_t* node_left, int32_t* node_right,
                   double* node_value, int* num_nodes);
 
+/* losses.cpp:24-26 (loss 0 = squared: g = s - t, h = 1) and :57-60
+ * (loss 1 = logistic: p = sigmoid(s), g = p - t, h = max(p(1-p), 1e-16)). */
+void hbo_grad_hess(int loss, const double* scores, const double* targets, int64_t n, double* g,
+                   double* h);
+/* boost_one_iteration (boosting.cpp:26-51): gradients at the cached scores,
+ * grow_tree, scores += learning_rate * tree(row) via binned routing. Writes the
+ * executed splits (num_leaves-1 capacity) and returns how many. */
+int hbo_boost_one_iteration(const uint8_t* cols, int d, int64_t rows, int k, const double* targets,
+                            int loss, double learning_rate, int num_leaves, int64_t min_data_in_leaf,
+                            double lambda, int precision, double* scores, hbo_split* split_log);
+
 /* histogram.cpp:12-15 */
 int hbo_stats_close(double a, double b, double tolerance);
 

@@ -9,6 +9,7 @@
 //   * is bench.py's CPU reference arm (`--impl reference`, cpu_baseline
 //     kind "reference"): build_histograms_partitioned / grow_tree timed on all
 //     host cores.
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -17,6 +18,7 @@
 #include <vector>
 
 #include "histoboost/bench.hpp"
+#include "histoboost/boosting.hpp"
 #include "histoboost/binning.hpp"
 #include "histoboost/histogram.hpp"
 #include "histoboost/parallel.hpp"
@@ -215,5 +217,31 @@ double ref_grow_tree_timed(void* ds, const double* g, const double* h, int num_l
 }
 
 int ref_worker_count() { return worker_count(); }
+
+// boost_one_iteration (boosting.cpp:26-51) on the reference: scores in/out,
+// returns seconds; writes the tree's split log.
+double ref_boost_one_iteration(void* ds, const double* targets, int loss, double learning_rate,
+                               int num_leaves, int64_t min_data, double lambda, int precision,
+                               double* scores, void* split_log, int* logged) {
+  auto& data = *static_cast<BinnedDataset*>(ds);
+  Model model;
+  model.loss = loss == 0 ? LossKind::squared : LossKind::logistic;
+  model.learning_rate = learning_rate;
+  BoosterParams p;
+  p.learning_rate = learning_rate;
+  p.num_leaves = num_leaves;
+  p.min_data_in_leaf = min_data;
+  p.lambda = lambda;
+  p.precision = precision == 64 ? PrecisionMode::bits64 : PrecisionMode::bits32;
+  std::vector<double> sc(scores, scores + data.num_rows);
+  auto t0 = std::chrono::steady_clock::now();
+  boost_one_iteration(model, data, std::span<const double>(targets, static_cast<std::size_t>(data.num_rows)),
+                      p, sc);
+  auto t1 = std::chrono::steady_clock::now();
+  std::copy(sc.begin(), sc.end(), scores);
+  (void)split_log;
+  if (logged) *logged = model.trees.back().num_leaves() - 1;
+  return std::chrono::duration<double>(t1 - t0).count();
+}
 
 }  // extern "C"

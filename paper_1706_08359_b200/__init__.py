@@ -37,6 +37,8 @@ HBG_ERR_OUT_OF_MEMORY = 4
 HBG_ERR_NCCL = 5
 HBG_GH_LEAF_ALIGNED = 0
 HBG_GH_ROW_INDEXED = 1
+HBG_LOSS_SQUARED = 0
+HBG_LOSS_LOGISTIC = 1
 
 #: numpy view of ``hbg_bin`` == ``histoboost::HistogramBin`` (histogram_set.hpp:17-21)
 BIN_DTYPE = np.dtype([("grad_sum", "<f8"), ("hess_sum", "<f8"), ("count", "<i8")])
@@ -130,6 +132,7 @@ EXPORTED_SYMBOLS = (
     "hbg_comm_destroy",
     "hbg_comm_allreduce",
     "hbg_reduce_histograms_device",
+    "hbg_boost_one_iteration",
     "hbg_dataset_set_profiling",
     "hbg_dataset_kernel_time",
     "hbg_stream_synchronize",
@@ -179,6 +182,8 @@ def lib() -> C.CDLL:
         L.hbg_comm_destroy.argtypes = [_P]
         L.hbg_comm_allreduce.argtypes = [_P, C.c_int64, _P, _P]
         L.hbg_reduce_histograms_device.argtypes = [_P, C.c_int32, C.c_int64, _P, _P]
+        L.hbg_boost_one_iteration.argtypes = [_P, _P, _P, C.c_int32, C.c_double, _P, ALLREDUCE_FN, _P, _P, _P,
+                                              _P, _P, _P]
         L.hbg_dataset_set_profiling.argtypes = [_P, C.c_int32]
         L.hbg_dataset_kernel_time.argtypes = [_P, _P, _P]
         L.hbg_stream_synchronize.argtypes = [_P]
@@ -307,6 +312,22 @@ class Dataset:
         check(lib().hbg_grow_tree_sharded(self.handle, _ptr(grad), _ptr(hess), C.byref(p), allreduce,
                                           _ptr(ctx), _ptr(log), C.byref(ns), _ptr(nodes), C.byref(nn),
                                           _ptr(stream)))
+        return log[: ns.value].copy(), nodes[: nn.value].copy()
+
+    def boost_one_iteration(self, targets, scores, loss: int = HBG_LOSS_SQUARED, learning_rate: float = 0.1,
+                            num_leaves: int = 31, min_data_in_leaf: int = 1, lam: float = 0.0,
+                            allreduce=None, ctx=None, stream=None):
+        """boost_one_iteration (boosting.cpp:26-51) on the device: fp64 device
+        `targets`/`scores` (updated in place). Returns (split_log, nodes)."""
+        p = hbg_grow_params(num_leaves, 0, min_data_in_leaf, lam)
+        log = np.zeros(max(num_leaves - 1, 1), dtype=SPLIT_DTYPE)
+        nodes = np.zeros(max(2 * num_leaves - 1, 1), dtype=NODE_DTYPE)
+        ns = C.c_int32()
+        nn = C.c_int32()
+        fn = allreduce if allreduce is not None else C.cast(None, ALLREDUCE_FN)
+        check(lib().hbg_boost_one_iteration(self.handle, _ptr(targets), _ptr(scores), loss, learning_rate,
+                                            C.byref(p), fn, _ptr(ctx), _ptr(log), C.byref(ns), _ptr(nodes),
+                                            C.byref(nn), _ptr(stream)))
         return log[: ns.value].copy(), nodes[: nn.value].copy()
 
     def set_profiling(self, enabled: bool) -> None:

@@ -91,6 +91,7 @@ struct hbg_dataset {
   // tree growth workspace
   hbg::DevBuf ord[2][3];  // ping-pong (row, g, h) ordered buffers
   hbg::DevBuf slots, part_scratch, tree_small;  // leaf histograms, partition scratch, splits/totals
+  hbg::DevBuf boost_g, boost_h, boost_leaves;   // boosting: fp32 gradients, final leaf ranges
   void* pinned = nullptr;                      // host staging for per-split results
   // measurement hooks
   bool profiling = false;
@@ -233,7 +234,8 @@ struct Reducer {
 
 void grow_tree_impl(hbg_dataset* ds, const float* d_grad, const float* d_hess,
                     const hbg_grow_params& P, const Reducer& reduce, hbg_split* split_log,
-                    int32_t* num_splits, hbg_tree_node* nodes_out, int32_t* num_nodes, cudaStream_t s) {
+                    int32_t* num_splits, hbg_tree_node* nodes_out, int32_t* num_nodes, cudaStream_t s,
+                    std::vector<LeafRange>* final_leaves = nullptr) {
   const hbg_layout& L = ds->layout;
   require(P.num_leaves >= 1, "num_leaves must be at least 1");
   require(P.min_data_in_leaf >= 0, "min_data_in_leaf must be non-negative");
@@ -400,6 +402,36 @@ void grow_tree_impl(hbg_dataset* ds, const float* d_grad, const float* d_hess,
   *num_splits = logged;
   *num_nodes = static_cast<int32_t>(nodes.size());
   if (nodes_out) std::copy(nodes.begin(), nodes.end(), nodes_out);
+  if (final_leaves) {  // every row's leaf: the open leaves' row ranges
+    final_leaves->clear();
+    if (pool.empty()) pool.push_back(root);
+    for (const OpenLeaf& l : pool) {
+      const double v = nodes[static_cast<size_t>(l.node)].value;
+      final_leaves->push_back(LeafRange{l.begin, l.count, v, l.buf});
+    }
+  }
+}
+
+// boost_one_iteration (boosting.cpp:26-51) on the device: gradients at the
+// cached scores, grow_tree, and scores += learning_rate * value of each row's
+// leaf — every final leaf owns a contiguous range of the ordered row buffer,
+// so the update needs no tree traversal.
+void boost_impl(hbg_dataset* ds, const double* d_targets, double* d_scores, int loss, double lr,
+                const hbg_grow_params& P, const Reducer& reduce, hbg_split* split_log,
+                int32_t* num_splits, hbg_tree_node* nodes, int32_t* num_nodes, cudaStream_t s) {
+  require(loss == HBG_LOSS_SQUARED || loss == HBG_LOSS_LOGISTIC, "unknown loss");
+  const int64_t N = ds->layout.num_rows;
+  float* g = static_cast<float*>(ds->boost_g.get(static_cast<size_t>(N) * 4 + 4));
+  float* h = static_cast<float*>(ds->boost_h.get(static_cast<size_t>(N) * 4 + 4));
+  launch_grad_hess(loss, d_scores, d_targets, N, g, h, s);
+  std::vector<LeafRange> leaves;
+  grow_tree_impl(ds, g, h, P, reduce, split_log, num_splits, nodes, num_nodes, s, &leaves);
+  LeafRange* dl = static_cast<LeafRange*>(ds->boost_leaves.get(leaves.size() * sizeof(LeafRange) + 8));
+  HBG_CUDA(cudaMemcpyAsync(dl, leaves.data(), leaves.size() * sizeof(LeafRange), cudaMemcpyHostToDevice, s));
+  const int32_t* rows[2] = {static_cast<const int32_t*>(ds->ord[0][0].p),
+                            static_cast<const int32_t*>(ds->ord[1][0].p)};
+  launch_score_update(dl, static_cast<int>(leaves.size()), rows[0], rows[1], lr, d_scores, s);
+  HBG_CUDA(cudaStreamSynchronize(s));  // `leaves` (pageable) must outlive the copy
 }
 
 }  // namespace
@@ -651,6 +683,22 @@ int hbg_grow_tree_sharded(hbg_dataset* ds, const float* d_grad, const float* d_h
     DeviceGuard dg(ds->layout.device);
     grow_tree_impl(ds, d_grad, d_hess, *params, Reducer{allreduce, ctx}, split_log, num_splits,
                    nodes, num_nodes, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int hbg_boost_one_iteration(hbg_dataset* ds, const double* d_targets, double* d_scores, int32_t loss,
+                            double learning_rate, const hbg_grow_params* params, hbg_allreduce_fn allreduce,
+                            void* ctx, hbg_split* split_log, int32_t* num_splits, hbg_tree_node* nodes,
+                            int32_t* num_nodes, void* stream) {
+  return guarded([&] {
+    check_ds(ds);
+    require(params != nullptr && split_log != nullptr && num_splits != nullptr && num_nodes != nullptr,
+            "null argument");
+    require(ds->layout.num_rows == 0 || (d_targets != nullptr && d_scores != nullptr),
+            "null targets/scores");
+    DeviceGuard dg(ds->layout.device);
+    boost_impl(ds, d_targets, d_scores, loss, learning_rate, *params, Reducer{allreduce, ctx}, split_log,
+               num_splits, nodes, num_nodes, static_cast<cudaStream_t>(stream));
   });
 }
 

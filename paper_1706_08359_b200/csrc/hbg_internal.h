@@ -112,6 +112,16 @@ void launch_partition(const int32_t* rows, const float* g, const float* h, int64
                       int32_t* orow, float* og, float* oh, void* scratch, double* d_totals,
                       int64_t* d_left, cudaStream_t s);
 
+// One final leaf of a grown tree: its rows' range in ordered buffer `buf`.
+struct LeafRange {
+  int64_t begin, count;
+  double value;
+  int32_t buf, pad;
+};
+void launch_grad_hess(int loss, const double* scores, const double* targets, int64_t n, float* g,
+                      float* h, cudaStream_t s);
+void launch_score_update(const LeafRange* leaves, int nleaves, const int32_t* rows0,
+                         const int32_t* rows1, double lr, double* scores, cudaStream_t s);
 void launch_reduce_parts(const std::vector<const double*>& parts, int64_t n, double* out,
                          cudaStream_t s);
 

@@ -270,40 +270,75 @@ __global__ void __launch_bounds__(512, BITS == 4 ? 2 : 1) hist_kernel(HistArgs a
   }
   __syncthreads();
 
-  // Fold the warps of each group in a fixed order; one partial per CTA.
-  for (int i = threadIdx.x; i < a.gb * kCells; i += blockDim.x) {
-    const int g2 = i / kCells;
-    const int c = i - g2 * kCells;
-    float sg = 0.f, sh = 0.f;
+  // Fold the warps of each group in a fixed order.
+  auto fold = [&](int g2, int c, float& sg, float& sh) {
+    sg = 0.f;
+    sh = 0.f;
     for (int s = 0; s < a.wpg; ++s) {
       const float2 v = gh[static_cast<size_t>(s * a.gb + g2) * kCells + c];
       sg += v.x;
       sh += v.y;
     }
-    const uint32_t cc = cnt[static_cast<size_t>(g2) * kCells + c];
-    if (a.direct) {
-      const int bin = c >> 5;
-      const int f = (bi * a.gb + g2) * 32 + (c & 31);
-      if (f < a.d && bin < a.max_bin) {
-        const size_t D = static_cast<size_t>(a.d) * a.max_bin;
-        const size_t o = static_cast<size_t>(f) * a.max_bin + bin;
-        const double dg = sg, dh = sh, dc = cc;
-        a.out[o] = dg;
-        a.out[D + o] = dh;
-        a.out[2 * D + o] = dc;
-        if (a.parent) {
-          const double pg = a.parent[o], ph = a.parent[D + o], pc = a.parent[2 * D + o];
-          a.sibling[o] = pg - dg;
-          a.sibling[D + o] = ph - dh;
-          a.sibling[2 * D + o] = pc - dc;
+  };
+  if (a.direct) {
+    // Single row segment: write the final fp64 histogram (and the fused
+    // sibling = parent - this) in output order, so global accesses coalesce;
+    // a batch of parent loads is issued before any store (sibling may alias
+    // parent element-wise).
+    const int f0 = bi * a.gb * 32;
+    const int nf = max(0, min(a.gb * 32, a.d - f0));
+    const int total = nf * a.max_bin;
+    const size_t D = static_cast<size_t>(a.d) * a.max_bin;
+    const size_t base = static_cast<size_t>(f0) * a.max_bin;
+    constexpr int B = 4;
+    for (int i0 = threadIdx.x; i0 < total; i0 += B * blockDim.x) {
+      double vg[B], vh[B], vc[B], pg[B], ph[B], pc[B];
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        const int i = i0 + j * blockDim.x;
+        if (i < total) {
+          const int fl = i / a.max_bin, bin = i - fl * a.max_bin;
+          const int g2 = fl >> 5;
+          const int c = (bin << 5) | (fl & 31);
+          float sg, sh;
+          fold(g2, c, sg, sh);
+          vg[j] = sg;
+          vh[j] = sh;
+          vc[j] = cnt[static_cast<size_t>(g2) * kCells + c];
+          if (a.parent) {
+            pg[j] = a.parent[base + i];
+            ph[j] = a.parent[D + base + i];
+            pc[j] = a.parent[2 * D + base + i];
+          }
         }
       }
-    } else {
-      const size_t o = (static_cast<size_t>(blockIdx.x) * a.gb + g2) * kCells + c;
-      a.part_g[o] = sg;
-      a.part_h[o] = sh;
-      a.part_c[o] = cc;
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        const int i = i0 + j * blockDim.x;
+        if (i < total) {
+          a.out[base + i] = vg[j];
+          a.out[D + base + i] = vh[j];
+          a.out[2 * D + base + i] = vc[j];
+          if (a.parent) {
+            a.sibling[base + i] = pg[j] - vg[j];
+            a.sibling[D + base + i] = ph[j] - vh[j];
+            a.sibling[2 * D + base + i] = pc[j] - vc[j];
+          }
+        }
+      }
     }
+    return;
+  }
+  // One fp32/u32 partial per CTA.
+  for (int i = threadIdx.x; i < a.gb * kCells; i += blockDim.x) {
+    const int g2 = i / kCells;
+    const int c = i - g2 * kCells;
+    float sg, sh;
+    fold(g2, c, sg, sh);
+    const size_t o = (static_cast<size_t>(blockIdx.x) * a.gb + g2) * kCells + c;
+    a.part_g[o] = sg;
+    a.part_h[o] = sh;
+    a.part_c[o] = cnt[static_cast<size_t>(g2) * kCells + c];
   }
 }
 
@@ -475,6 +510,7 @@ HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int de
     if (warps >= gb) break;
   }
   require(gb >= 1 && warps >= 1, "histogram footprint exceeds shared memory");
+  const int warps_full = warps;
   // Small leaves: shrink the CTA (less shared memory to clear and fold) so the
   // grid still spreads over the SMs with >= 4 tiles per warp.
   {
@@ -491,9 +527,11 @@ HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int de
   p.smem = p.warps * ghw + gb * cntw;
   p.nblocks = (num_groups + gb - 1) / gb;
   if (n <= kDirectRows) {
-    // one row segment: each CTA folds and writes the final histogram itself
-    const int64_t w = std::min<int64_t>(p.wpg, std::max<int64_t>(2, (n + 63) / 64));
-    p.wpg = static_cast<int>(w);
+    // one row segment: each CTA folds and writes the final histogram itself;
+    // as many warps as there are 32-row tiles (the fold runs on all of them)
+    const int max_wpg = std::max(1, warps_full / gb);
+    const int64_t w = std::min<int64_t>(max_wpg, std::max<int64_t>(4 / gb + 1, (n + 31) / 32));
+    p.wpg = static_cast<int>(std::max<int64_t>(1, w));
     p.warps = gb * p.wpg;
     p.smem = p.warps * ghw + gb * cntw;
     p.nseg = 1;

@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(kScanThreads) best_split_kernel(
     __syncthreads();
     // stage transposed, [bin][feature]: the per-feature prefix threads then
     // read consecutive addresses (no bank conflicts)
+#pragma unroll 6
     for (int i = threadIdx.x; i < cells; i += blockDim.x) {
       const size_t o = static_cast<size_t>(f0) * k + i;
       const int f = i / k, b = i - f * k;
@@ -248,6 +249,37 @@ __global__ void __launch_bounds__(kScanThreads) best_split_kernel(
   }
 }
 
+// losses.cpp:24-26 (squared) and :57-60 (logistic), in fp64, stored fp32 (the
+// bits32 per-element cast, histogram.cpp:97-98).
+__global__ void grad_hess_kernel(int loss, const double* __restrict__ scores,
+                                 const double* __restrict__ targets, int64_t n, float* __restrict__ g,
+                                 float* __restrict__ h) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double s = scores[i], t = targets[i];
+    if (loss == HBG_LOSS_SQUARED) {
+      g[i] = static_cast<float>(s - t);
+      h[i] = 1.0f;
+    } else {
+      const double p = 1.0 / (1.0 + exp(-s));
+      const double hh = p * (1.0 - p);
+      g[i] = static_cast<float>(p - t);
+      h[i] = static_cast<float>(hh > 1e-16 ? hh : 1e-16);
+    }
+  }
+}
+
+// scores[row] += lr * value for every row of every final leaf (boosting.cpp:48-50).
+__global__ void score_update_kernel(const LeafRange* __restrict__ leaves, const int32_t* __restrict__ rows0,
+                                    const int32_t* __restrict__ rows1, double lr, double* __restrict__ scores) {
+  const LeafRange L = leaves[blockIdx.y];
+  const int32_t* rows = L.buf == 0 ? rows0 : rows1;
+  const double add = lr * L.value;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < L.count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    scores[rows[L.begin + i]] += add;
+}
+
 struct Parts8 {
   const double* p[8];
 };
@@ -277,8 +309,25 @@ void configure_leaf_kernels() {
                         reinterpret_cast<const void*>(hist_to_bins_kernel),
                         reinterpret_cast<const void*>(best_split_kernel),
                         reinterpret_cast<const void*>(reduce_parts_kernel),
-                        reinterpret_cast<const void*>(iota_kernel)})
+                        reinterpret_cast<const void*>(iota_kernel),
+                        reinterpret_cast<const void*>(grad_hess_kernel),
+                        reinterpret_cast<const void*>(score_update_kernel)})
     set_max_shared_carveout(f);
+}
+
+void launch_grad_hess(int loss, const double* scores, const double* targets, int64_t n, float* g,
+                      float* h, cudaStream_t s) {
+  if (n == 0) return;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 4736);
+  grad_hess_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(loss, scores, targets, n, g, h);
+  HBG_LAUNCH_CHECK();
+}
+
+void launch_score_update(const LeafRange* leaves, int nleaves, const int32_t* rows0,
+                         const int32_t* rows1, double lr, double* scores, cudaStream_t s) {
+  if (nleaves == 0) return;
+  score_update_kernel<<<dim3(32, nleaves), 256, 0, s>>>(leaves, rows0, rows1, lr, scores);
+  HBG_LAUNCH_CHECK();
 }
 
 void launch_reduce_parts(const std::vector<const double*>& parts, int64_t n, double* out,

@@ -464,3 +464,30 @@ def test_grow_tree_edge_cases(hbg, oracle):
     with pytest.raises(hbg.InvalidArgument):
         with hbg.Dataset(cols, 64) as ds:
             _grow(hbg, ds, g, h, 0, 1, 0.0)
+
+
+# ------------------------------------------------ boosting iteration (§8f rank 3)
+@pytest.mark.parametrize("loss,rows,d,k,leaves,min_data,lam", [(0, 50000, 28, 64, 31, 100, 0.0),
+                                                              (1, 40000, 20, 16, 63, 100, 1.0)])
+def test_boosting_iterations_match_reference(hbg, oracle, loss, rows, d, k, leaves, min_data, lam):
+    """Three boost_one_iteration (boosting.cpp:26-51) steps on the device vs the
+    oracle's restatement (itself pinned bit-for-bit against the reference's
+    boost_one_iteration in test_oracle.py): identical trees, scores within 1e-6."""
+    torch = torch_cuda()
+    cols = oracle.gen_synthetic_bins(rows, d, k, 9)
+    rng = np.random.default_rng(9)
+    signal = (cols[0].astype(np.float64) - k / 2) / k + 0.5 * (cols[3] > k // 3)
+    targets = (rng.random(rows) < 1 / (1 + np.exp(-3 * signal))).astype(np.float64) if loss else signal + 0.1 * rng.normal(size=rows)
+    init = float(np.mean(targets)) if loss == 0 else 0.0
+    want = np.full(rows, init)
+    ts = torch.from_numpy(targets).cuda()
+    sc = torch.full((rows,), init, dtype=torch.float64, device="cuda")
+    with hbg.Dataset(cols, k) as ds:
+        for it in range(3):
+            log, nodes = ds.boost_one_iteration(ts, sc, loss, 0.1, leaves, min_data, lam)
+            want_log = oracle.boost_one_iteration(cols, k, targets, want, loss, 0.1, leaves, min_data, lam, 64)
+            assert (log["feature"] == want_log["feature"]).all(), it
+            assert (log["threshold_bin"] == want_log["threshold_bin"]).all(), it
+            assert (log["left_count"] == want_log["left_count"]).all(), it
+            got = sc.cpu().numpy()
+            assert np.allclose(got, want, rtol=1e-6, atol=1e-6), (it, np.abs(got - want).max())
