@@ -48,19 +48,22 @@ struct Slice {
   uint32_t w[kWords];
 };
 
+// One lane fetches its row's whole slice: a 256-bit load (LDG.E.ENL2.256,
+// sm_100) for the 32-byte 8-bit slice — one L1 request per gathered row
+// instead of two — and a 128-bit load for the 16-byte 4-bit slice.
 template <int BITS>
 __device__ __forceinline__ void load_slice(const unsigned char* p, Slice<BITS>& s) {
-  const uint4 a = __ldg(reinterpret_cast<const uint4*>(p));
-  s.w[0] = a.x;
-  s.w[1] = a.y;
-  s.w[2] = a.z;
-  s.w[3] = a.w;
   if constexpr (BITS == 8) {
-    const uint4 b = __ldg(reinterpret_cast<const uint4*>(p) + 1);
-    s.w[4] = b.x;
-    s.w[5] = b.y;
-    s.w[6] = b.z;
-    s.w[7] = b.w;
+    asm volatile("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(s.w[0]), "=r"(s.w[1]), "=r"(s.w[2]), "=r"(s.w[3]), "=r"(s.w[4]), "=r"(s.w[5]),
+                   "=r"(s.w[6]), "=r"(s.w[7])
+                 : "l"(p));
+  } else {
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(p));
+    s.w[0] = a.x;
+    s.w[1] = a.y;
+    s.w[2] = a.z;
+    s.w[3] = a.w;
   }
 }
 
@@ -154,14 +157,16 @@ struct TileIn {
 
 // Rows per lane per tile (see update_step_rows). One row keeps the 13-warp
 // k<=128 kernels at their measured best (the shared-memory data pipe is ~85%
-// busy either way); k=256 runs 3 warps/SM and needs the extra independent work.
+// busy either way); k=256 runs 3 warps/SM and needs the extra independent work
+// (4 rows per lane = 12 independent chains per SM).
 template <int K>
 __host__ __device__ constexpr int rows_per_lane() {
-  return K >= 256 ? 2 : 1;
+  return K >= 256 ? 4 : 1;
 }
+inline int rows_per_lane_of(int k_alloc) { return k_alloc >= 256 ? 4 : 1; }
 
 template <int BITS, int K, bool kRowIndexed>
-__global__ void __launch_bounds__(512, BITS == 4 ? 2 : 1) hist_kernel(HistArgs a) {
+__global__ void __launch_bounds__(K >= 256 ? 128 : 512, BITS == 4 ? 2 : 1) hist_kernel(HistArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int kCells = K * 32;
   const int warps = blockDim.x >> 5;
@@ -502,19 +507,25 @@ HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int de
   const size_t cntw = cells * 4;  // per-group shared counts
   const size_t smem_max = 232448;
   const int max_warps = 16;
-  int gb = std::min(num_groups, max_warps);
-  int warps = 0;
-  for (; gb >= 1; --gb) {
-    if (gb * cntw >= smem_max) continue;
-    warps = static_cast<int>(std::min<size_t>(max_warps, (smem_max - gb * cntw) / ghw));
-    if (warps >= gb) break;
+  // The group block (slice groups per CTA) that maximises warps per CTA (the
+  // latency hiding of the ordered read-modify-write chains); ties -> more
+  // groups per CTA (fewer re-reads of the leaf entries).
+  int gb = 0, warps = 0;
+  for (int cand = 1; cand <= std::min(num_groups, max_warps); ++cand) {
+    if (cand * cntw >= smem_max) break;
+    const int w_per_group = static_cast<int>(std::min<size_t>(max_warps, (smem_max - cand * cntw) / ghw)) / cand;
+    if (w_per_group < 1) break;
+    if (cand * w_per_group >= warps) {
+      gb = cand;
+      warps = cand * w_per_group;
+    }
   }
   require(gb >= 1 && warps >= 1, "histogram footprint exceeds shared memory");
   const int warps_full = warps;
   // Small leaves: shrink the CTA (less shared memory to clear and fold) so the
   // grid still spreads over the SMs with >= 4 tiles per warp.
   {
-    const int64_t tile_rows = static_cast<int64_t>(32) * (p.k_alloc >= 256 ? 2 : 1);
+    const int64_t tile_rows = static_cast<int64_t>(32) * rows_per_lane_of(p.k_alloc);
     const int64_t warps_needed =
         std::max<int64_t>(1, (n + 4 * tile_rows - 1) / (4 * tile_rows)) * num_groups;
     const int64_t per_cta = (warps_needed + sm_count(device) - 1) / sm_count(device);
@@ -541,9 +552,22 @@ HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int de
     return p;
   }
   const int occ = occupancy_for(bits, p.k_alloc, p.warps * 32, p.smem, device);
-  const int64_t target = static_cast<int64_t>(sm_count(device)) * occ;
-  int64_t nseg = (target + p.nblocks - 1) / p.nblocks;
-  const int64_t min_rows = static_cast<int64_t>(p.wpg) * 32 * (p.k_alloc >= 256 ? 2 : 1) * 2;  // >= 2 tiles per warp
+  const int64_t slots = static_cast<int64_t>(sm_count(device)) * occ;  // CTAs per wave
+  // Row segments: fill whole waves (1..4) as evenly as possible.
+  int64_t nseg = 1;
+  {
+    double best_eff = -1.0;
+    for (int64_t waves = 1; waves <= 4; ++waves) {
+      const int64_t ns = std::max<int64_t>(1, slots * waves / p.nblocks);
+      const double eff = static_cast<double>(p.nblocks * ns) /
+                         static_cast<double>(slots * ((p.nblocks * ns + slots - 1) / slots));
+      if (eff > best_eff + 0.02) {
+        best_eff = eff;
+        nseg = ns;
+      }
+    }
+  }
+  const int64_t min_rows = static_cast<int64_t>(p.wpg) * 32 * rows_per_lane_of(p.k_alloc) * 2;  // >= 2 tiles per warp
   nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, (n + min_rows - 1) / min_rows));
   int64_t seg_len = (n + nseg - 1) / nseg;
   seg_len = std::max<int64_t>(32, (seg_len + 31) / 32 * 32);

@@ -4,6 +4,7 @@
 //   (5) best-split scan over bins, fp64       (row a11, tree.cpp:59-112,163-182)
 // plus the SoA -> HistogramBin conversion used by the host drop-in.
 #include <algorithm>
+#include <mutex>
 
 #include "hbg_internal.h"
 
@@ -130,7 +131,7 @@ __device__ __forceinline__ bool better(const Cand& a, const Cand& b) {
 }
 
 constexpr int kScanThreads = 256;
-constexpr int kScanChunkCells = 1536;  // features*bins staged per chunk (3 x 12 KB of fp64)
+constexpr int kScanMaxChunkCells = 6144;  // features*bins staged per CTA (24 B each, dynamic smem)
 
 // One CTA per leaf histogram (blockIdx.x selects the leaf of a batch). The
 // scan reproduces find_best_threshold (tree.cpp:76-112) exactly: per feature
@@ -140,26 +141,80 @@ constexpr int kScanChunkCells = 1536;  // features*bins staged per chunk (3 x 12
 // winner is the max gain, lowest feature, lowest bin — the outcome of the
 // reference's strict `>` loops (the `break` when the right side gets too
 // small only removes bins whose right count is already below min_data).
-__global__ void __launch_bounds__(kScanThreads) best_split_kernel(
-    const double* __restrict__ hist_base, int64_t hist_stride, int d, int k,
-    const double* d_totals, int64_t totals_stride, const int64_t* counts_dev, int64_t count0,
-    int64_t count1, double gt, double ht, int64_t min_data, double lambda, hbg_split* out_base) {
-  const double* hist = hist_base + blockIdx.x * hist_stride;
-  hbg_split* out = out_base + blockIdx.x;
-  if (d_totals) {
-    gt = d_totals[blockIdx.x * totals_stride];
-    ht = d_totals[blockIdx.x * totals_stride + 1];
+struct ScanArgs {
+  const double* hist_base;
+  int64_t hist_stride;
+  int d, k;
+  const double* d_totals;
+  int64_t totals_stride;
+  const int64_t* counts_dev;
+  int64_t count0, count1;
+  double gt, ht;
+  int64_t min_data;
+  double lambda;
+  hbg_split* out_base;
+  Cand* partial;  // [leaf][chunk] when gridDim.x > 1
+  int fchunk;     // features per CTA
+};
+
+__device__ __forceinline__ void leaf_scalars(const ScanArgs& a, int leaf, double& gt, double& ht,
+                                             int64_t& count) {
+  gt = a.gt;
+  ht = a.ht;
+  if (a.d_totals) {
+    gt = a.d_totals[leaf * a.totals_stride];
+    ht = a.d_totals[leaf * a.totals_stride + 1];
   }
-  const int64_t count = counts_dev ? counts_dev[blockIdx.x] : (blockIdx.x == 0 ? count0 : count1);
-  __shared__ double pg[kScanChunkCells], ph[kScanChunkCells];
-  __shared__ int64_t pc[kScanChunkCells];
+  count = a.counts_dev ? a.counts_dev[leaf] : (leaf == 0 ? a.count0 : a.count1);
+}
+
+__device__ void write_split(const Cand& c, double gt, double ht, int64_t count, double lambda,
+                            hbg_split* out) {
+  hbg_split o{};
+  o.feature = c.f;
+  o.threshold_bin = c.b;
+  if (c.f >= 0) {
+    o.gain = c.gain;
+    o.left_grad = c.lg;
+    o.left_hess = c.lh;
+    o.left_count = c.lc;
+    o.right_grad = gt - c.lg;
+    o.right_hess = ht - c.lh;
+    o.right_count = count - c.lc;
+    o.left_value = leaf_value(c.lg, c.lh, lambda);
+    o.right_value = leaf_value(gt - c.lg, ht - c.lh, lambda);
+  } else {
+    o.threshold_bin = -1;
+  }
+  *out = o;
+}
+
+// grid = (feature chunks, leaves). Each CTA scans fchunk features of one leaf;
+// with several chunks the per-chunk winners go to `partial` and
+// split_final_kernel picks among them. `better` is a strict total order on
+// (gain, feature, bin), so the winner does not depend on the chunking.
+__global__ void __launch_bounds__(kScanThreads) best_split_kernel(ScanArgs a) {
+  const int leaf = blockIdx.y;
+  const double* hist = a.hist_base + leaf * a.hist_stride;
+  const int d = a.d, k = a.k;
+  const int64_t min_data = a.min_data;
+  const double lambda = a.lambda;
+  double gt, ht;
+  int64_t count;
+  leaf_scalars(a, leaf, gt, ht, count);
+  extern __shared__ __align__(16) unsigned char scan_smem[];
+  const int chunk_cells = a.fchunk * k;
+  double* pg = reinterpret_cast<double*>(scan_smem);
+  double* ph = pg + chunk_cells;
+  int64_t* pc = reinterpret_cast<int64_t*>(ph + chunk_cells);
   __shared__ Cand red[kScanThreads];
   Cand best{0.0, -1, -1, 0.0, 0.0, 0};
   const bool splittable = !(count < 2 * min_data || count < 2);  // tree.cpp:165
   const size_t D = static_cast<size_t>(d) * k;
-  const int fchunk = max(1, kScanChunkCells / k);
-  for (int f0 = 0; splittable && f0 < d; f0 += fchunk) {
-    const int nf = min(fchunk, d - f0);
+  const int fchunk = a.fchunk;
+  {
+    const int f0 = blockIdx.x * fchunk;
+    const int nf = splittable ? max(0, min(fchunk, d - f0)) : 0;
     const int cells = nf * k;
     __syncthreads();
     // stage transposed, [bin][feature]: the per-feature prefix threads then
@@ -178,16 +233,16 @@ __global__ void __launch_bounds__(kScanThreads) best_split_kernel(
     for (int t = threadIdx.x; t < 3 * nf; t += blockDim.x) {
       const int f = t % nf, stat = t / nf;
       if (stat < 2) {
-        double* a = stat == 0 ? pg : ph;
+        double* arr = stat == 0 ? pg : ph;
         double run = 0.0;
         for (int b0 = 0; b0 < k; b0 += 8) {
           double v[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] = b0 + j < k ? a[(b0 + j) * nf + f] : 0.0;
+          for (int j = 0; j < 8; ++j) v[j] = b0 + j < k ? arr[(b0 + j) * nf + f] : 0.0;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             run += v[j];
-            if (b0 + j < k) a[(b0 + j) * nf + f] = run;
+            if (b0 + j < k) arr[(b0 + j) * nf + f] = run;
           }
         }
       } else {
@@ -226,26 +281,34 @@ __global__ void __launch_bounds__(kScanThreads) best_split_kernel(
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    const Cand c = red[0];
-    hbg_split o{};
-    o.feature = c.f;
-    o.threshold_bin = c.b;
-    if (c.f >= 0) {
-      const double lg = c.lg, lh = c.lh;
-      const int64_t lc = c.lc;
-      o.gain = c.gain;
-      o.left_grad = lg;
-      o.left_hess = lh;
-      o.left_count = lc;
-      o.right_grad = gt - lg;
-      o.right_hess = ht - lh;
-      o.right_count = count - lc;
-      o.left_value = leaf_value(lg, lh, lambda);
-      o.right_value = leaf_value(gt - lg, ht - lh, lambda);
+    if (gridDim.x == 1) {
+      write_split(red[0], gt, ht, count, lambda, a.out_base + leaf);
     } else {
-      o.threshold_bin = -1;
+      a.partial[leaf * gridDim.x + blockIdx.x] = red[0];
     }
-    *out = o;
+  }
+}
+
+__global__ void split_final_kernel(ScanArgs a, int nchunks) {
+  const int leaf = blockIdx.x;
+  __shared__ Cand red[kScanThreads];
+  Cand best{0.0, -1, -1, 0.0, 0.0, 0};
+  for (int i = threadIdx.x; i < nchunks; i += blockDim.x) {
+    const Cand c = a.partial[leaf * nchunks + i];
+    if (better(c, best)) best = c;
+  }
+  red[threadIdx.x] = best;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st && better(red[threadIdx.x + st], red[threadIdx.x]))
+      red[threadIdx.x] = red[threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double gt, ht;
+    int64_t count;
+    leaf_scalars(a, leaf, gt, ht, count);
+    write_split(red[0], gt, ht, count, a.lambda, a.out_base + leaf);
   }
 }
 
@@ -308,6 +371,7 @@ void configure_leaf_kernels() {
                         reinterpret_cast<const void*>(subtract_kernel),
                         reinterpret_cast<const void*>(hist_to_bins_kernel),
                         reinterpret_cast<const void*>(best_split_kernel),
+                        reinterpret_cast<const void*>(split_final_kernel),
                         reinterpret_cast<const void*>(reduce_parts_kernel),
                         reinterpret_cast<const void*>(iota_kernel),
                         reinterpret_cast<const void*>(grad_hess_kernel),
@@ -380,6 +444,25 @@ void launch_hist_to_bins(const double* d_hist, int64_t cells, hbg_bin* d_bins, c
   HBG_LAUNCH_CHECK();
 }
 
+// Per-device grow-only scratch for the split scan's per-chunk winners. Calls
+// on one device must be stream-ordered (documented: not re-entrant).
+void* scan_scratch(size_t bytes) {
+  static std::mutex mu;
+  static void* buf[64] = {nullptr};
+  static size_t cap[64] = {0};
+  int dev = 0;
+  HBG_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (cap[dev & 63] < bytes) {
+    if (buf[dev & 63]) HBG_CUDA(cudaFree(buf[dev & 63]));
+    buf[dev & 63] = nullptr;
+    cap[dev & 63] = 0;
+    HBG_CUDA(cudaMalloc(&buf[dev & 63], bytes));
+    cap[dev & 63] = bytes;
+  }
+  return buf[dev & 63];
+}
+
 void launch_best_split(const double* d_hist, int d, int k, const double* d_totals,
                        const int64_t* d_count, double gt, double ht, int64_t count,
                        int64_t min_data, double lambda, hbg_split* out, cudaStream_t s) {
@@ -391,12 +474,43 @@ void launch_best_split_batch(const double* d_hist, int64_t hist_stride, int leav
                              const double* d_totals, int64_t totals_stride, const int64_t* d_counts,
                              int64_t count0, int64_t count1, double gt, double ht, int64_t min_data,
                              double lambda, hbg_split* out, cudaStream_t s) {
-  require(k <= kScanChunkCells, "max_bin too large for the split scan");
+  require(k <= kScanMaxChunkCells, "max_bin too large for the split scan");
   require(leaves >= 1 && leaves <= 2, "split-scan batches hold one or two leaves");
-  best_split_kernel<<<leaves, kScanThreads, 0, s>>>(d_hist, hist_stride, d, k, d_totals, totals_stride,
-                                                   d_counts, count0, count1, gt, ht, min_data, lambda,
-                                                   out);
+  static std::once_flag once[64];
+  int dev = 0;
+  HBG_CUDA(cudaGetDevice(&dev));
+  std::call_once(once[dev & 63], [] {
+    HBG_CUDA(cudaFuncSetAttribute(best_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kScanMaxChunkCells * 24));
+  });
+  ScanArgs a{};
+  a.hist_base = d_hist;
+  a.hist_stride = hist_stride;
+  a.d = d;
+  a.k = k;
+  a.d_totals = d_totals;
+  a.totals_stride = totals_stride;
+  a.counts_dev = d_counts;
+  a.count0 = count0;
+  a.count1 = count1;
+  a.gt = gt;
+  a.ht = ht;
+  a.min_data = min_data;
+  a.lambda = lambda;
+  a.out_base = out;
+  // Spread wide histograms over ~one wave of CTAs; narrow ones stay in one CTA.
+  const int64_t cells = static_cast<int64_t>(d) * k;
+  const int64_t per_cta = std::min<int64_t>(kScanMaxChunkCells, std::max<int64_t>(2048, (cells + 147) / 148));
+  a.fchunk = static_cast<int>(std::max<int64_t>(1, per_cta / k));
+  const int nchunks = std::max(1, (d + a.fchunk - 1) / a.fchunk);
+  if (nchunks > 1) a.partial = static_cast<Cand*>(scan_scratch(static_cast<size_t>(leaves) * nchunks * sizeof(Cand)));
+  const size_t smem = static_cast<size_t>(a.fchunk) * k * 24;
+  best_split_kernel<<<dim3(nchunks, leaves), kScanThreads, smem, s>>>(a);
   HBG_LAUNCH_CHECK();
+  if (nchunks > 1) {
+    split_final_kernel<<<leaves, kScanThreads, 0, s>>>(a, nchunks);
+    HBG_LAUNCH_CHECK();
+  }
 }
 
 }  // namespace hbg
