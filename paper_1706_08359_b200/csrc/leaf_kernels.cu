@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(kScanThreads) best_split_kernel(ScanArgs a) {
   const int chunk_cells = a.fchunk * k;
   double* pg = reinterpret_cast<double*>(scan_smem);
   double* ph = pg + chunk_cells;
-  int64_t* pc = reinterpret_cast<int64_t*>(ph + chunk_cells);
+  double* pc = ph + chunk_cells;  // counts as exact doubles (< 2^53)
   __shared__ Cand red[kScanThreads];
   Cand best{0.0, -1, -1, 0.0, 0.0, 0};
   const bool splittable = !(count < 2 * min_data || count < 2);  // tree.cpp:165
@@ -225,52 +225,49 @@ __global__ void __launch_bounds__(kScanThreads) best_split_kernel(ScanArgs a) {
       const int f = i / k, b = i - f * k;
       pg[b * nf + f] = hist[o];
       ph[b * nf + f] = hist[D + o];
-      pc[b * nf + f] = static_cast<int64_t>(hist[2 * D + o]);
+      pc[b * nf + f] = hist[2 * D + o];
     }
     __syncthreads();
     // sequential prefix in bin order, one thread per (feature, statistic);
     // loads are batched ahead of the dependent adds
     for (int t = threadIdx.x; t < 3 * nf; t += blockDim.x) {
       const int f = t % nf, stat = t / nf;
-      if (stat < 2) {
-        double* arr = stat == 0 ? pg : ph;
-        double run = 0.0;
-        for (int b0 = 0; b0 < k; b0 += 8) {
-          double v[8];
+      double* arr = stat == 0 ? pg : (stat == 1 ? ph : pc);
+      double run = 0.0;  // integer-valued for counts: exact
+      for (int b0 = 0; b0 < k; b0 += 8) {
+        double v[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] = b0 + j < k ? arr[(b0 + j) * nf + f] : 0.0;
+        for (int j = 0; j < 8; ++j) v[j] = b0 + j < k ? arr[(b0 + j) * nf + f] : 0.0;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            run += v[j];
-            if (b0 + j < k) arr[(b0 + j) * nf + f] = run;
-          }
-        }
-      } else {
-        int64_t run = 0;
-        for (int b0 = 0; b0 < k; b0 += 8) {
-          int64_t v[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] = b0 + j < k ? pc[(b0 + j) * nf + f] : 0;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            run += v[j];
-            if (b0 + j < k) pc[(b0 + j) * nf + f] = run;
-          }
+        for (int j = 0; j < 8; ++j) {
+          run += v[j];
+          if (b0 + j < k) arr[(b0 + j) * nf + f] = run;
         }
       }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < cells; i += blockDim.x) {
-      const int b = i / nf, f = i - b * nf;
-      if (b >= k - 1) continue;  // thresholds 0 .. k-2
-      const int64_t lc = pc[i];
-      const int64_t rc = count - lc;
-      if (lc < min_data || rc < min_data) continue;
-      const double lg = pg[i], lh = ph[i];
-      const double gain = gain_of(lg, lh, gt - lg, ht - lh, lambda);
-      if (gain <= 0.0) continue;
-      const Cand c{gain, f0 + f, b, lg, lh, lc};
-      if (better(c, best)) best = c;
+    // every candidate bin's gain, evaluated branch-free in batches of 4 so the
+    // fp64 divisions of independent cells overlap
+    const double cnt = static_cast<double>(count), md = static_cast<double>(min_data);
+    for (int i0 = threadIdx.x; i0 < cells; i0 += 4 * blockDim.x) {
+      double gain[4];
+      bool ok[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int i = min(i0 + j * static_cast<int>(blockDim.x), cells - 1);
+        const int b = i / nf;
+        const double lc = pc[i], lg = pg[i], lh = ph[i];
+        ok[j] = i0 + j * static_cast<int>(blockDim.x) < cells && b < k - 1 && lc >= md && cnt - lc >= md;
+        gain[j] = gain_of(lg, lh, gt - lg, ht - lh, lambda);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int i = i0 + j * static_cast<int>(blockDim.x);
+        if (!ok[j] || !(gain[j] > 0.0)) continue;
+        const int b = i / nf, f = i - b * nf;
+        const Cand c{gain[j], f0 + f, b, pg[i], ph[i], static_cast<int64_t>(pc[i])};
+        if (better(c, best)) best = c;
+      }
     }
   }
   red[threadIdx.x] = best;

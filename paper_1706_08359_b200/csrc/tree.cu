@@ -66,6 +66,45 @@ __device__ void block_reduce_4d1i(double v[4], int& c, double (*sd)[kPartThreads
   }
 }
 
+// Per-iteration block ranks: each warp's ballot counts -> exclusive warp
+// offsets (computed by warp 0 with shuffles) + iteration totals.
+struct RankScratch {
+  int wl[kPartThreads / 32], wn[kPartThreads / 32];
+  int ol[kPartThreads / 32], on[kPartThreads / 32];
+  int tl, tn;
+};
+
+__device__ __forceinline__ void block_ranks(unsigned lm, unsigned vm, RankScratch& rs) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) {
+    rs.wl[w] = __popc(lm);
+    rs.wn[w] = __popc(vm);
+  }
+  __syncthreads();
+  if (w == 0) {
+    constexpr int W = kPartThreads / 32;
+    int l = lane < W ? rs.wl[lane] : 0, nn = lane < W ? rs.wn[lane] : 0;
+    int il = l, in = nn;  // inclusive scans
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, il, off), b = __shfl_up_sync(0xffffffffu, in, off);
+      if (lane >= off) {
+        il += a;
+        in += b;
+      }
+    }
+    if (lane < W) {
+      rs.ol[lane] = il - l;
+      rs.on[lane] = in - nn;
+    }
+    if (lane == W - 1) {
+      rs.tl = il;
+      rs.tn = in;
+    }
+  }
+  __syncthreads();
+}
+
 // Pass 1: side flag per position (bin <= thr goes left, tree.cpp:117-123),
 // per-block left count and fp64 per-side g/h sums.
 __global__ void __launch_bounds__(kPartThreads) partition_count_kernel(PartArgs a) {
@@ -160,44 +199,31 @@ __global__ void __launch_bounds__(kPartThreads) partition_scatter_kernel(
     float* __restrict__ oh) {
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kPartTile;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  __shared__ int wl[kPartThreads / 32];
-  __shared__ int wn[kPartThreads / 32];
+  __shared__ RankScratch rs;
   const int64_t L = *left_total;
   const int64_t left_before = block_off[blockIdx.x];
-  int64_t lrun = left_before;              // left rows before this item, in leaf order
-  int64_t rrun = base - left_before;       // right rows before this item
-#pragma unroll 1
-  for (int i = 0; i < kPartItems; ++i) {
+  int64_t lrun = left_before;         // left rows before this item, in leaf order
+  int64_t rrun = base - left_before;  // right rows before this item
+  const int64_t rem = (n - base + kPartThreads - 1) / kPartThreads;
+  const int iters = static_cast<int>(rem < kPartItems ? rem : kPartItems);
+  for (int i = 0; i < iters; ++i) {
     const int64_t pos = base + i * kPartThreads + threadIdx.x;
     const bool valid = pos < n;
     const bool left = valid && flags[pos];
     const unsigned lm = __ballot_sync(0xffffffffu, left);
     const unsigned vm = __ballot_sync(0xffffffffu, valid);
-    if (lane == 0) {
-      wl[w] = __popc(lm);
-      wn[w] = __popc(vm);
-    }
-    __syncthreads();
-    int lbefore = 0, nbefore = 0, ltot = 0, ntot = 0;
-    for (int j = 0; j < kPartThreads / 32; ++j) {
-      if (j < w) {
-        lbefore += wl[j];
-        nbefore += wn[j];
-      }
-      ltot += wl[j];
-      ntot += wn[j];
-    }
+    block_ranks(lm, vm, rs);
     const unsigned below = (1u << lane) - 1u;
     if (valid) {
-      const int lrank = lbefore + __popc(lm & below);
-      const int prank = nbefore + __popc(vm & below);  // position rank within this iteration
+      const int lrank = rs.ol[w] + __popc(lm & below);
+      const int prank = rs.on[w] + __popc(vm & below);  // position rank within this iteration
       const int64_t dst = left ? lrun + lrank : L + rrun + (prank - lrank);
       orow[dst] = rows[pos];
       og[dst] = g[pos];
       oh[dst] = h[pos];
     }
-    lrun += ltot;
-    rrun += ntot - ltot;
+    lrun += rs.tl;
+    rrun += rs.tn - rs.tl;
     __syncthreads();
   }
 }
@@ -210,8 +236,7 @@ __global__ void __launch_bounds__(kPartThreads) partition_small_kernel(PartArgs 
   __shared__ uint8_t flag[kPartTile];
   __shared__ double sd[4][kPartThreads / 32];
   __shared__ int sc[kPartThreads / 32];
-  __shared__ int wl[kPartThreads / 32];
-  __shared__ int wn[kPartThreads / 32];
+  __shared__ RankScratch rs;
   __shared__ int64_t L_sh;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   double v[4] = {0.0, 0.0, 0.0, 0.0};
@@ -245,37 +270,25 @@ __global__ void __launch_bounds__(kPartThreads) partition_small_kernel(PartArgs 
   __syncthreads();
   const int64_t L = L_sh;
   int64_t lrun = 0, rrun = 0;
-  for (int i = 0; i < kPartItems; ++i) {
+  const int iters = static_cast<int>((a.n + kPartThreads - 1) / kPartThreads);
+  for (int i = 0; i < iters; ++i) {
     const int pos = i * kPartThreads + threadIdx.x;
     const bool valid = pos < a.n;
     const bool left = valid && flag[pos];
     const unsigned lm = __ballot_sync(0xffffffffu, left);
     const unsigned vm = __ballot_sync(0xffffffffu, valid);
-    if (lane == 0) {
-      wl[w] = __popc(lm);
-      wn[w] = __popc(vm);
-    }
-    __syncthreads();
-    int lbefore = 0, nbefore = 0, ltot = 0, ntot = 0;
-    for (int j = 0; j < kPartThreads / 32; ++j) {
-      if (j < w) {
-        lbefore += wl[j];
-        nbefore += wn[j];
-      }
-      ltot += wl[j];
-      ntot += wn[j];
-    }
+    block_ranks(lm, vm, rs);
     const unsigned below = (1u << lane) - 1u;
     if (valid) {
-      const int lrank = lbefore + __popc(lm & below);
-      const int prank = nbefore + __popc(vm & below);
+      const int lrank = rs.ol[w] + __popc(lm & below);
+      const int prank = rs.on[w] + __popc(vm & below);
       const int64_t dst = left ? lrun + lrank : L + rrun + (prank - lrank);
       orow[dst] = a.rows[pos];
       og[dst] = a.g[pos];
       oh[dst] = a.h[pos];
     }
-    lrun += ltot;
-    rrun += ntot - ltot;
+    lrun += rs.tl;
+    rrun += rs.tn - rs.tl;
     __syncthreads();
   }
 }

@@ -1,11 +1,12 @@
-"""Grow one Higgs-shaped tree (for ncu captures of the per-split kernels)."""
-import sys, os
+"""Grow Higgs-shaped trees (for ncu launch lists / captures of the per-split kernels)."""
+import sys, os, time
 import numpy as np
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1706_08359_b200 as hbg  # noqa: E402
 
 rows = int(sys.argv[1]) if len(sys.argv) > 1 else 2_000_000
+trees = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 rng = np.random.default_rng(0)
 cols = rng.integers(1, 64, size=(28, rows), dtype=np.uint8)
 g = (2 * rng.random(rows) - 1).astype(np.float32)
@@ -13,7 +14,9 @@ h = rng.random(rows).astype(np.float32)
 with hbg.Dataset(cols, 64) as ds:
     tg, th = torch.from_numpy(g).cuda(), torch.from_numpy(h).cuda()
     s = torch.cuda.Stream()
-    for _ in range(2):
+    for _ in range(trees):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
         log, nodes = ds.grow_tree(tg, th, 255, 1, 0.0, s.cuda_stream)
-    torch.cuda.synchronize()
-print("splits", len(log))
+        torch.cuda.synchronize()
+        print(f"tree {1e3 * (time.perf_counter() - t0):.2f} ms, splits {len(log)}", flush=True)
