@@ -95,3 +95,32 @@ def test_two_rank_sharded_tree_equals_reference(hbg, oracle, rows, d, k, leaves,
 
     assert _assert_same_tree(log0, nodes0, want_log, want_nodes) == len(want_log)
     assert coll.calls >= len(log0) + 2  # root totals + root histogram + per-split child totals (+ histograms)
+
+
+def test_nccl_comm_single_rank_tree(hbg, oracle):
+    """The NCCL hook itself (hbg_comm_*, dlopen'ed libnccl) on one rank: the
+    sharded grower over a 1-rank communicator equals the unsharded grower."""
+    import torch
+
+    cols = oracle.gen_synthetic_bins(30000, 16, 64, 8)
+    g, h = oracle.gen_grad_hess(30000, 8)
+    comm = hbg.Comm(1, 0, hbg.Comm.unique_id(), 0)
+    try:
+        with hbg.Dataset(cols, 64) as ds:
+            tg = torch.from_numpy(g.astype(np.float32)).cuda()
+            th = torch.from_numpy(h.astype(np.float32)).cuda()
+            s = torch.cuda.Stream()
+            a = ds.grow_tree_sharded(tg, th, comm.allreduce_fn, comm.handle, 63, 20, 0.0, s.cuda_stream)
+            b = ds.grow_tree(tg, th, 63, 20, 0.0, s.cuda_stream)
+            # the same boosting iteration through the hook
+            ts = torch.from_numpy(g).cuda()
+            s1 = torch.zeros(30000, dtype=torch.float64, device="cuda")
+            s2 = torch.zeros(30000, dtype=torch.float64, device="cuda")
+            ds.boost_one_iteration(ts, s1, hbg.HBG_LOSS_SQUARED, 0.1, 31, 20, 0.0, comm.allreduce_fn, comm.handle,
+                                   s.cuda_stream)
+            ds.boost_one_iteration(ts, s2, hbg.HBG_LOSS_SQUARED, 0.1, 31, 20, 0.0, stream=s.cuda_stream)
+            torch.cuda.synchronize()
+    finally:
+        comm.close()
+    assert a[0].tobytes() == b[0].tobytes() and a[1].tobytes() == b[1].tobytes()
+    assert torch.equal(s1, s2)
