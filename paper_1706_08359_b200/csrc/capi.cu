@@ -92,6 +92,7 @@ struct hbg_dataset {
   hbg::DevBuf ord[2][3];  // ping-pong (row, g, h) ordered buffers
   hbg::DevBuf slots, part_scratch, tree_small;  // leaf histograms, partition scratch, splits/totals
   hbg::DevBuf boost_g, boost_h, boost_leaves;   // boosting: fp32 gradients, final leaf ranges
+  hbg::DevBuf small_acc, small_exps;            // fixed-point accumulator for small leaves
   void* pinned = nullptr;                      // host staging for per-split results
   // measurement hooks
   bool profiling = false;
@@ -279,6 +280,24 @@ void grow_tree_impl(hbg_dataset* ds, const float* d_grad, const float* d_hess,
   }
   launch_gather(rows[0], N, d_grad, d_hess, nullptr, nullptr, dres->root,
                 static_cast<double*>(scratch), s);
+  // fixed-point scale for the small-leaf histogram path, accumulator cleared
+  int* exps = static_cast<int*>(ds->small_exps.get(16));
+  void* acc = ds->small_acc.get(small_hist_acc_bytes(d, k));
+  launch_fixed_scale(gb[0], hb[0], N, exps, s);
+  HBG_CUDA(cudaMemsetAsync(acc, 0, small_hist_acc_bytes(d, k), s));
+  const uint32_t* packed = ds->packed;
+  const int stride_words = L.row_stride_bytes / 4;
+  // histogram of one leaf range into `out` (+ sibling = parent - out)
+  auto leaf_hist = [&](int buf, int64_t begin, int64_t count, double* out, const double* parent,
+                       double* sibling) {
+    if (count <= kAtomicHistRows) {
+      launch_small_hist(rows[buf] + begin, gb[buf] + begin, hb[buf] + begin, count, packed, stride_words,
+                        L.words_per_row, L.bits_per_bin, d, k, exps, acc, out, parent, sibling, s);
+    } else {
+      build_device(ds, rows[buf] + begin, count, gb[buf] + begin, hb[buf] + begin, HBG_GH_LEAF_ALIGNED,
+                   out, s, parent, sibling);
+    }
+  };
   hres->root[2] = static_cast<double>(N);  // pinned staging; the stream orders the copy
   HBG_CUDA(cudaMemcpyAsync(&dres->root[2], &hres->root[2], sizeof(double), cudaMemcpyHostToDevice, s));
   reduce(dres->root, 3, s);
@@ -357,12 +376,10 @@ void grow_tree_impl(hbg_dataset* ds, const float* d_grad, const float* d_hess,
       large.slot = parent.slot;
       parent.slot = -1;
       if (!sharded) {
-        build_device(ds, rows[out] + small.begin, small.count, gb[out] + small.begin,
-                     hb[out] + small.begin, HBG_GH_LEAF_ALIGNED, slot_ptr(small.slot), s,
-                     slot_ptr(large.slot), slot_ptr(large.slot));  // subtraction fused
+        leaf_hist(out, small.begin, small.count, slot_ptr(small.slot), slot_ptr(large.slot),
+                  slot_ptr(large.slot));  // subtraction fused
       } else {
-        build_device(ds, rows[out] + small.begin, small.count, gb[out] + small.begin,
-                     hb[out] + small.begin, HBG_GH_LEAF_ALIGNED, slot_ptr(small.slot), s);
+        leaf_hist(out, small.begin, small.count, slot_ptr(small.slot), nullptr, nullptr);
         reduce(slot_ptr(small.slot), static_cast<int64_t>(D3), s);  // global smaller child
         launch_subtract(slot_ptr(large.slot), slot_ptr(small.slot), slot_ptr(large.slot),
                         static_cast<int64_t>(D3), s);

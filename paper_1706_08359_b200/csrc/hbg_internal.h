@@ -131,6 +131,15 @@ void configure_leaf_kernels();
 void configure_tree_kernels();
 void configure_kernels(int device);  // carveout for every non-histogram kernel, once per device
 
+// Small leaves (tree grower): fixed-point histogram through L2 atomics.
+constexpr int64_t kAtomicHistRows = 4096;
+size_t small_hist_acc_bytes(int d, int k);
+void launch_fixed_scale(const float* g, const float* h, int64_t n, int* exps, cudaStream_t s);
+void launch_small_hist(const int32_t* rows, const float* g, const float* h, int64_t n,
+                       const uint32_t* packed, int stride_words, int words_per_row, int bits, int d, int k,
+                       const int* exps, void* acc, double* out, const double* parent, double* sibling,
+                       cudaStream_t s);
+
 int sm_count(int device);
 
 // Runs f, mapping exceptions to HBG_* status codes + the thread-local last error.

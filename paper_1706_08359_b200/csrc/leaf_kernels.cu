@@ -131,6 +131,40 @@ __device__ __forceinline__ bool better(const Cand& a, const Cand& b) {
 }
 
 constexpr int kScanThreads = 256;
+
+__device__ __forceinline__ Cand shfl_cand(const Cand& c, int src) {
+  Cand o;
+  o.gain = __shfl_sync(0xffffffffu, c.gain, src);
+  o.f = __shfl_sync(0xffffffffu, c.f, src);
+  o.b = __shfl_sync(0xffffffffu, c.b, src);
+  o.lg = __shfl_sync(0xffffffffu, c.lg, src);
+  o.lh = __shfl_sync(0xffffffffu, c.lh, src);
+  o.lc = __shfl_sync(0xffffffffu, c.lc, src);
+  return o;
+}
+
+// Best candidate of the CTA (strict total order `better`), in thread 0.
+// Warp butterfly with shuffles, then one warp over the warp winners.
+__device__ Cand block_best(Cand c, Cand* warp_best) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const Cand o = shfl_cand(c, lane ^ off);
+    if (better(o, c)) c = o;
+  }
+  if (lane == 0) warp_best[w] = c;
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    c = lane < nw ? warp_best[lane] : Cand{0.0, -1, -1, 0.0, 0.0, 0};
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const Cand o = shfl_cand(c, lane ^ off);
+      if (better(o, c)) c = o;
+    }
+  }
+  return c;
+}
 constexpr int kScanMaxChunkCells = 6144;  // features*bins staged per CTA (24 B each, dynamic smem)
 
 // One CTA per leaf histogram (blockIdx.x selects the leaf of a batch). The
@@ -207,7 +241,7 @@ __global__ void __launch_bounds__(kScanThreads) best_split_kernel(ScanArgs a) {
   double* pg = reinterpret_cast<double*>(scan_smem);
   double* ph = pg + chunk_cells;
   double* pc = ph + chunk_cells;  // counts as exact doubles (< 2^53)
-  __shared__ Cand red[kScanThreads];
+  __shared__ Cand warp_best[kScanThreads / 32];
   Cand best{0.0, -1, -1, 0.0, 0.0, 0};
   const bool splittable = !(count < 2 * min_data || count < 2);  // tree.cpp:165
   const size_t D = static_cast<size_t>(d) * k;
@@ -270,42 +304,30 @@ __global__ void __launch_bounds__(kScanThreads) best_split_kernel(ScanArgs a) {
       }
     }
   }
-  red[threadIdx.x] = best;
-  __syncthreads();
-  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
-    if (threadIdx.x < st && better(red[threadIdx.x + st], red[threadIdx.x]))
-      red[threadIdx.x] = red[threadIdx.x + st];
-    __syncthreads();
-  }
+  best = block_best(best, warp_best);
   if (threadIdx.x == 0) {
     if (gridDim.x == 1) {
-      write_split(red[0], gt, ht, count, lambda, a.out_base + leaf);
+      write_split(best, gt, ht, count, lambda, a.out_base + leaf);
     } else {
-      a.partial[leaf * gridDim.x + blockIdx.x] = red[0];
+      a.partial[leaf * gridDim.x + blockIdx.x] = best;
     }
   }
 }
 
 __global__ void split_final_kernel(ScanArgs a, int nchunks) {
   const int leaf = blockIdx.x;
-  __shared__ Cand red[kScanThreads];
+  __shared__ Cand warp_best[kScanThreads / 32];
   Cand best{0.0, -1, -1, 0.0, 0.0, 0};
   for (int i = threadIdx.x; i < nchunks; i += blockDim.x) {
     const Cand c = a.partial[leaf * nchunks + i];
     if (better(c, best)) best = c;
   }
-  red[threadIdx.x] = best;
-  __syncthreads();
-  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
-    if (threadIdx.x < st && better(red[threadIdx.x + st], red[threadIdx.x]))
-      red[threadIdx.x] = red[threadIdx.x + st];
-    __syncthreads();
-  }
+  best = block_best(best, warp_best);
   if (threadIdx.x == 0) {
     double gt, ht;
     int64_t count;
     leaf_scalars(a, leaf, gt, ht, count);
-    write_split(red[0], gt, ht, count, a.lambda, a.out_base + leaf);
+    write_split(best, gt, ht, count, a.lambda, a.out_base + leaf);
   }
 }
 

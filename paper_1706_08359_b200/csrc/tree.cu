@@ -293,9 +293,138 @@ __global__ void __launch_bounds__(kPartThreads) partition_small_kernel(PartArgs 
   }
 }
 
+// ---- small leaves: deterministic fixed-point histogram through L2 atomics ----
+// For a leaf of a few thousand rows the shared-memory kernel's fixed cost
+// (clearing and folding per-warp cells) dominates. Here every (row, feature)
+// adds int64 fixed-point g and h (scale 2^S per tree, |q| <= 2^39 per element,
+// so any leaf of < 2^23 rows sums without overflow) and a u32 count straight
+// into an L2-resident accumulator with native 64-bit reductions (REDG.E.ADD.64)
+// from all SMs. Integer addition commutes, so the result is bitwise
+// deterministic and more precise than fp32 accumulation (2^-40 of max|g| per
+// element).
+
+// max |g|, max |h| over n values -> power-of-two scale exponents (one CTA).
+__global__ void fixed_scale_kernel(const float* __restrict__ g, const float* __restrict__ h, int64_t n,
+                                   int* __restrict__ exps) {
+  float mg = 0.f, mh = 0.f;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    mg = fmaxf(mg, fabsf(g[i]));
+    mh = fmaxf(mh, fabsf(h[i]));
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    mg = fmaxf(mg, __shfl_xor_sync(0xffffffffu, mg, off));
+    mh = fmaxf(mh, __shfl_xor_sync(0xffffffffu, mh, off));
+  }
+  __shared__ float sg[32], sh[32];
+  if ((threadIdx.x & 31) == 0) {
+    sg[threadIdx.x >> 5] = mg;
+    sh[threadIdx.x >> 5] = mh;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      mg = fmaxf(mg, sg[w]);
+      mh = fmaxf(mh, sh[w]);
+    }
+    int eg = 0, eh = 0;
+    frexpf(mg, &eg);  // mg < 2^eg
+    frexpf(mh, &eh);
+    exps[0] = 39 - eg;  // q = g * 2^exps[0], |q| <= 2^39
+    exps[1] = 39 - eh;
+  }
+}
+
+// Thread = (row, 32-bit word of the packed row): the word's features.
+__global__ void small_hist_atomic_kernel(const int32_t* __restrict__ rows, const float* __restrict__ g,
+                                         const float* __restrict__ h, int64_t n,
+                                         const uint32_t* __restrict__ packed, int stride_words,
+                                         int words_per_row, int bits, int d, int k,
+                                         const int* __restrict__ exps, unsigned long long* __restrict__ acc) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n * words_per_row) return;
+  const int64_t pos = t / words_per_row;
+  const int w = static_cast<int>(t - pos * words_per_row);
+  const int32_t row = rows[pos];
+  const uint32_t word = __ldg(packed + static_cast<int64_t>(row) * stride_words + w);
+  const int64_t qg = __double2ll_rn(ldexp(static_cast<double>(g[pos]), exps[0]));
+  const int64_t qh = __double2ll_rn(ldexp(static_cast<double>(h[pos]), exps[1]));
+  const int fpw = 32 / bits;
+  const uint32_t mask = (1u << bits) - 1u;
+  const size_t D = static_cast<size_t>(d) * k;
+  unsigned int* cnt = reinterpret_cast<unsigned int*>(acc + 2 * D);
+  for (int p = 0; p < fpw; ++p) {
+    // slice-major word index -> feature id (32 features per slice)
+    const int f = (w * fpw) + p;
+    if (f >= d) break;
+    const uint32_t b = (word >> (bits * p)) & mask;
+    const size_t o = static_cast<size_t>(f) * k + b;
+    atomicAdd(acc + o, static_cast<unsigned long long>(qg));
+    atomicAdd(acc + D + o, static_cast<unsigned long long>(qh));
+    atomicAdd(cnt + o, 1u);
+  }
+}
+
+// Fixed point -> SoA fp64 histogram (+ sibling = parent - hist when given),
+// and clear the accumulator for the next leaf.
+__global__ void small_hist_finish_kernel(unsigned long long* __restrict__ acc, const int* __restrict__ exps,
+                                         int64_t cells, double* __restrict__ out, const double* parent,
+                                         double* sibling) {
+  const double sg = ldexp(1.0, -exps[0]), sh = ldexp(1.0, -exps[1]);
+  unsigned int* cnt = reinterpret_cast<unsigned int*>(acc + 2 * cells);
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < cells;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double vg = static_cast<double>(static_cast<long long>(acc[i])) * sg;
+    const double vh = static_cast<double>(static_cast<long long>(acc[cells + i])) * sh;
+    const double vc = static_cast<double>(cnt[i]);
+    acc[i] = 0ull;
+    acc[cells + i] = 0ull;
+    cnt[i] = 0u;
+    out[i] = vg;
+    out[cells + i] = vh;
+    out[2 * cells + i] = vc;
+    if (parent) {
+      const double pg = parent[i], ph = parent[cells + i], pc = parent[2 * cells + i];
+      sibling[i] = pg - vg;
+      sibling[cells + i] = ph - vh;
+      sibling[2 * cells + i] = pc - vc;
+    }
+  }
+}
+
 }  // namespace
 
+size_t small_hist_acc_bytes(int d, int k) {
+  const size_t D = static_cast<size_t>(d) * k;
+  return D * 8 * 2 + D * 4 + 16;
+}
+
+void launch_fixed_scale(const float* g, const float* h, int64_t n, int* exps, cudaStream_t s) {
+  fixed_scale_kernel<<<1, 1024, 0, s>>>(g, h, n, exps);
+  HBG_LAUNCH_CHECK();
+}
+
+void launch_small_hist(const int32_t* rows, const float* g, const float* h, int64_t n,
+                       const uint32_t* packed, int stride_words, int words_per_row, int bits, int d, int k,
+                       const int* exps, void* acc, double* out, const double* parent, double* sibling,
+                       cudaStream_t s) {
+  unsigned long long* a = static_cast<unsigned long long*>(acc);
+  const int64_t items = n * words_per_row;
+  if (items > 0) {
+    small_hist_atomic_kernel<<<static_cast<unsigned>((items + 255) / 256), 256, 0, s>>>(
+        rows, g, h, n, packed, stride_words, words_per_row, bits, d, k, exps, a);
+    HBG_LAUNCH_CHECK();
+  }
+  const int64_t cells = static_cast<int64_t>(d) * k;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((cells + 255) / 256, 296));
+  small_hist_finish_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(a, exps, cells, out, parent, sibling);
+  HBG_LAUNCH_CHECK();
+}
+
 void configure_tree_kernels() {
+  set_max_shared_carveout(reinterpret_cast<const void*>(fixed_scale_kernel));
+  set_max_shared_carveout(reinterpret_cast<const void*>(small_hist_atomic_kernel));
+  set_max_shared_carveout(reinterpret_cast<const void*>(small_hist_finish_kernel));
   set_max_shared_carveout(reinterpret_cast<const void*>(partition_small_kernel));
   set_max_shared_carveout(reinterpret_cast<const void*>(partition_count_kernel));
   set_max_shared_carveout(reinterpret_cast<const void*>(partition_scan_kernel));
