@@ -206,6 +206,8 @@ def _ptr(a):
         return a.ctypes.data_as(C.c_void_p)
     if isinstance(a, int):
         return C.c_void_p(a)
+    if isinstance(a, C.c_void_p):
+        return a
     return C.c_void_p(a.data_ptr())  # torch.Tensor
 
 

@@ -375,6 +375,18 @@ void grow_tree_impl(hbg_dataset* ds, const float* d_grad, const float* d_hess,
       free_slots.pop_back();
       large.slot = parent.slot;
       parent.slot = -1;
+      if (!sharded && small.count <= kAtomicHistRows) {
+        // small child: L2-atomic histogram, then one fused launch for the
+        // conversion, the subtraction and both children's scans
+        launch_small_hist_atomic(rows[out] + small.begin, gb[out] + small.begin, hb[out] + small.begin,
+                                 small.count, packed, stride_words, L.words_per_row, L.bits_per_bin, d, k,
+                                 exps, acc, s);
+        FinishScanArgsHost fa{acc, exps, d, k, slot_ptr(small.slot), slot_ptr(large.slot),
+                              &small == &lo ? 1 : 0, dres->totals, gl_n, gr_n, lsplit ? 1 : 0,
+                              rsplit ? 1 : 0, P.min_data_in_leaf, P.lambda, &dres->split[0]};
+        launch_finish_scan(fa, s);
+        goto scanned;
+      }
       if (!sharded) {
         leaf_hist(out, small.begin, small.count, slot_ptr(small.slot), slot_ptr(large.slot),
                   slot_ptr(large.slot));  // subtraction fused
@@ -395,6 +407,7 @@ void grow_tree_impl(hbg_dataset* ds, const float* d_grad, const float* d_hess,
         launch_best_split(slot_ptr(ro.slot), d, k, dres->totals + 2, nullptr, 0.0, 0.0, gr_n,
                           P.min_data_in_leaf, P.lambda, &dres->split[1], s);
       }
+    scanned:;
     }
     if (parent.slot >= 0) free_slots.push_back(parent.slot);
     sync_results();

@@ -140,6 +140,26 @@ void launch_small_hist(const int32_t* rows, const float* g, const float* h, int6
                        const int* exps, void* acc, double* out, const double* parent, double* sibling,
                        cudaStream_t s);
 
+// Small-leaf split tail fused: accumulator -> small/large histograms + both scans.
+struct FinishScanArgsHost {
+  void* acc;
+  const int* exps;
+  int d, k;
+  double* small_out;
+  double* large_io;
+  int small_is_left;
+  const double* totals;  // gl, hl, gr, hr
+  int64_t nl, nr;
+  int lsplit, rsplit;
+  int64_t min_data;
+  double lambda;
+  hbg_split* out;  // [2]
+};
+void launch_finish_scan(const FinishScanArgsHost& a, cudaStream_t s);
+void launch_small_hist_atomic(const int32_t* rows, const float* g, const float* h, int64_t n,
+                              const uint32_t* packed, int stride_words, int words_per_row, int bits, int d,
+                              int k, const int* exps, void* acc, cudaStream_t s);
+
 int sm_count(int device);
 
 // Runs f, mapping exceptions to HBG_* status codes + the thread-local last error.

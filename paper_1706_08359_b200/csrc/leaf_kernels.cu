@@ -175,6 +175,23 @@ constexpr int kScanMaxChunkCells = 6144;  // features*bins staged per CTA (24 B 
 // winner is the max gain, lowest feature, lowest bin — the outcome of the
 // reference's strict `>` loops (the `break` when the right side gets too
 // small only removes bins whose right count is already below min_data).
+struct FinishScanArgs {
+  unsigned long long* acc;
+  const int* exps;
+  int d, k;
+  double* small_out;
+  double* large_io;
+  int small_is_left;
+  const double* totals;
+  int64_t nl, nr;
+  int lsplit, rsplit;
+  int64_t min_data;
+  double lambda;
+  hbg_split* out;
+  Cand* partial;
+  int fchunk;
+};
+
 struct ScanArgs {
   const double* hist_base;
   int64_t hist_stride;
@@ -227,12 +244,60 @@ __device__ void write_split(const Cand& c, double gt, double ht, int64_t count, 
 // with several chunks the per-chunk winners go to `partial` and
 // split_final_kernel picks among them. `better` is a strict total order on
 // (gain, feature, bin), so the winner does not depend on the chunking.
+// Scan of one staged chunk ([bin][feature] fp64 g/h/count, nf features from
+// feature f0) -> this thread's best candidate. Staging must be complete
+// (caller syncs); the prefix runs in place.
+__device__ Cand scan_staged(double* pg, double* ph, double* pc, int nf, int k, int f0, double gt,
+                            double ht, double cnt, double md, double lambda) {
+  // sequential prefix in bin order (the reference's order, tree.cpp:80-83),
+  // one thread per (feature, statistic); loads batched ahead of the adds
+  for (int t = threadIdx.x; t < 3 * nf; t += blockDim.x) {
+    const int f = t % nf, stat = t / nf;
+    double* arr = stat == 0 ? pg : (stat == 1 ? ph : pc);
+    double run = 0.0;  // integer-valued for counts: exact
+    for (int b0 = 0; b0 < k; b0 += 8) {
+      double v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = b0 + j < k ? arr[(b0 + j) * nf + f] : 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        run += v[j];
+        if (b0 + j < k) arr[(b0 + j) * nf + f] = run;
+      }
+    }
+  }
+  __syncthreads();
+  // every candidate bin's gain, branch-free in batches of 4 so the fp64
+  // divisions of independent cells overlap
+  Cand best{0.0, -1, -1, 0.0, 0.0, 0};
+  const int cells = nf * k;
+  for (int i0 = threadIdx.x; i0 < cells; i0 += 4 * blockDim.x) {
+    double gain[4];
+    bool ok[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = min(i0 + j * static_cast<int>(blockDim.x), cells - 1);
+      const int b = i / nf;
+      const double lc = pc[i], lg = pg[i], lh = ph[i];
+      ok[j] = i0 + j * static_cast<int>(blockDim.x) < cells && b < k - 1 && lc >= md && cnt - lc >= md;
+      gain[j] = gain_of(lg, lh, gt - lg, ht - lh, lambda);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = i0 + j * static_cast<int>(blockDim.x);
+      if (!ok[j] || !(gain[j] > 0.0)) continue;
+      const int b = i / nf, f = i - b * nf;
+      const Cand c{gain[j], f0 + f, b, pg[i], ph[i], static_cast<int64_t>(pc[i])};
+      if (better(c, best)) best = c;
+    }
+  }
+  return best;
+}
+
 __global__ void __launch_bounds__(kScanThreads) best_split_kernel(ScanArgs a) {
   const int leaf = blockIdx.y;
   const double* hist = a.hist_base + leaf * a.hist_stride;
   const int d = a.d, k = a.k;
-  const int64_t min_data = a.min_data;
-  const double lambda = a.lambda;
   double gt, ht;
   int64_t count;
   leaf_scalars(a, leaf, gt, ht, count);
@@ -242,75 +307,94 @@ __global__ void __launch_bounds__(kScanThreads) best_split_kernel(ScanArgs a) {
   double* ph = pg + chunk_cells;
   double* pc = ph + chunk_cells;  // counts as exact doubles (< 2^53)
   __shared__ Cand warp_best[kScanThreads / 32];
-  Cand best{0.0, -1, -1, 0.0, 0.0, 0};
-  const bool splittable = !(count < 2 * min_data || count < 2);  // tree.cpp:165
+  const bool splittable = !(count < 2 * a.min_data || count < 2);  // tree.cpp:165
   const size_t D = static_cast<size_t>(d) * k;
-  const int fchunk = a.fchunk;
-  {
-    const int f0 = blockIdx.x * fchunk;
-    const int nf = splittable ? max(0, min(fchunk, d - f0)) : 0;
-    const int cells = nf * k;
-    __syncthreads();
-    // stage transposed, [bin][feature]: the per-feature prefix threads then
-    // read consecutive addresses (no bank conflicts)
+  const int f0 = blockIdx.x * a.fchunk;
+  const int nf = splittable ? max(0, min(a.fchunk, d - f0)) : 0;
+  const int cells = nf * k;
+  // stage transposed, [bin][feature]: the prefix threads read consecutive addresses
 #pragma unroll 6
-    for (int i = threadIdx.x; i < cells; i += blockDim.x) {
-      const size_t o = static_cast<size_t>(f0) * k + i;
-      const int f = i / k, b = i - f * k;
-      pg[b * nf + f] = hist[o];
-      ph[b * nf + f] = hist[D + o];
-      pc[b * nf + f] = hist[2 * D + o];
-    }
-    __syncthreads();
-    // sequential prefix in bin order, one thread per (feature, statistic);
-    // loads are batched ahead of the dependent adds
-    for (int t = threadIdx.x; t < 3 * nf; t += blockDim.x) {
-      const int f = t % nf, stat = t / nf;
-      double* arr = stat == 0 ? pg : (stat == 1 ? ph : pc);
-      double run = 0.0;  // integer-valued for counts: exact
-      for (int b0 = 0; b0 < k; b0 += 8) {
-        double v[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = b0 + j < k ? arr[(b0 + j) * nf + f] : 0.0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          run += v[j];
-          if (b0 + j < k) arr[(b0 + j) * nf + f] = run;
-        }
-      }
-    }
-    __syncthreads();
-    // every candidate bin's gain, evaluated branch-free in batches of 4 so the
-    // fp64 divisions of independent cells overlap
-    const double cnt = static_cast<double>(count), md = static_cast<double>(min_data);
-    for (int i0 = threadIdx.x; i0 < cells; i0 += 4 * blockDim.x) {
-      double gain[4];
-      bool ok[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int i = min(i0 + j * static_cast<int>(blockDim.x), cells - 1);
-        const int b = i / nf;
-        const double lc = pc[i], lg = pg[i], lh = ph[i];
-        ok[j] = i0 + j * static_cast<int>(blockDim.x) < cells && b < k - 1 && lc >= md && cnt - lc >= md;
-        gain[j] = gain_of(lg, lh, gt - lg, ht - lh, lambda);
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int i = i0 + j * static_cast<int>(blockDim.x);
-        if (!ok[j] || !(gain[j] > 0.0)) continue;
-        const int b = i / nf, f = i - b * nf;
-        const Cand c{gain[j], f0 + f, b, pg[i], ph[i], static_cast<int64_t>(pc[i])};
-        if (better(c, best)) best = c;
-      }
-    }
+  for (int i = threadIdx.x; i < cells; i += blockDim.x) {
+    const size_t o = static_cast<size_t>(f0) * k + i;
+    const int f = i / k, b = i - f * k;
+    pg[b * nf + f] = hist[o];
+    ph[b * nf + f] = hist[D + o];
+    pc[b * nf + f] = hist[2 * D + o];
   }
+  __syncthreads();
+  Cand best = scan_staged(pg, ph, pc, nf, k, f0, gt, ht, static_cast<double>(count),
+                          static_cast<double>(a.min_data), a.lambda);
   best = block_best(best, warp_best);
   if (threadIdx.x == 0) {
     if (gridDim.x == 1) {
-      write_split(best, gt, ht, count, lambda, a.out_base + leaf);
+      write_split(best, gt, ht, count, a.lambda, a.out_base + leaf);
     } else {
       a.partial[leaf * gridDim.x + blockIdx.x] = best;
     }
+  }
+}
+
+// Small-leaf split tail, fused: fixed-point accumulator (small child) ->
+// fp64 small histogram, larger child = parent - small in the parent's slot,
+// accumulator cleared, and both children's split scans — one launch.
+// grid = feature chunks; a CTA handles its chunk for both children.
+__global__ void __launch_bounds__(kScanThreads) finish_scan_kernel(FinishScanArgs a) {
+  const int d = a.d, k = a.k;
+  const size_t D = static_cast<size_t>(d) * k;
+  extern __shared__ __align__(16) unsigned char scan_smem[];
+  const int chunk_cells = a.fchunk * k;
+  double* st = reinterpret_cast<double*>(scan_smem);  // [child][stat][cells]
+  __shared__ Cand warp_best[kScanThreads / 32];
+  const int f0 = blockIdx.x * a.fchunk;
+  const int nf = max(0, min(a.fchunk, d - f0));
+  const int cells = nf * k;
+  const double sg = ldexp(1.0, -a.exps[0]), sh = ldexp(1.0, -a.exps[1]);
+  unsigned int* cnt = reinterpret_cast<unsigned int*>(a.acc + 2 * D);
+  double* sm = st + (a.small_is_left ? 0 : 3 * chunk_cells);
+  double* lg = st + (a.small_is_left ? 3 * chunk_cells : 0);
+#pragma unroll 4
+  for (int i = threadIdx.x; i < cells; i += blockDim.x) {
+    const size_t o = static_cast<size_t>(f0) * k + i;
+    const double vg = static_cast<double>(static_cast<long long>(a.acc[o])) * sg;
+    const double vh = static_cast<double>(static_cast<long long>(a.acc[D + o])) * sh;
+    const double vc = static_cast<double>(cnt[o]);
+    a.acc[o] = 0ull;
+    a.acc[D + o] = 0ull;
+    cnt[o] = 0u;
+    const double pg = a.large_io[o], ph = a.large_io[D + o], pc = a.large_io[2 * D + o];
+    a.small_out[o] = vg;
+    a.small_out[D + o] = vh;
+    a.small_out[2 * D + o] = vc;
+    a.large_io[o] = pg - vg;
+    a.large_io[D + o] = ph - vh;
+    a.large_io[2 * D + o] = pc - vc;
+    const int f = i / k, b = i - f * k;
+    const int t = b * nf + f;
+    sm[t] = vg;
+    sm[chunk_cells + t] = vh;
+    sm[2 * chunk_cells + t] = vc;
+    lg[t] = pg - vg;
+    lg[chunk_cells + t] = ph - vh;
+    lg[2 * chunk_cells + t] = pc - vc;
+  }
+  __syncthreads();
+  for (int child = 0; child < 2; ++child) {
+    const bool want = child == 0 ? a.lsplit : a.rsplit;
+    if (!want) continue;  // uniform across the CTA
+    double* base = st + child * 3 * chunk_cells;
+    const double gt = a.totals[2 * child], ht = a.totals[2 * child + 1];
+    const int64_t count = child == 0 ? a.nl : a.nr;
+    Cand best = scan_staged(base, base + chunk_cells, base + 2 * chunk_cells, nf, k, f0, gt, ht,
+                            static_cast<double>(count), static_cast<double>(a.min_data), a.lambda);
+    best = block_best(best, warp_best);
+    if (threadIdx.x == 0) {
+      if (gridDim.x == 1) {
+        write_split(best, gt, ht, count, a.lambda, a.out + child);
+      } else {
+        a.partial[child * gridDim.x + blockIdx.x] = best;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -391,6 +475,7 @@ void configure_leaf_kernels() {
                         reinterpret_cast<const void*>(hist_to_bins_kernel),
                         reinterpret_cast<const void*>(best_split_kernel),
                         reinterpret_cast<const void*>(split_final_kernel),
+                        reinterpret_cast<const void*>(finish_scan_kernel),
                         reinterpret_cast<const void*>(reduce_parts_kernel),
                         reinterpret_cast<const void*>(iota_kernel),
                         reinterpret_cast<const void*>(grad_hess_kernel),
@@ -461,6 +546,56 @@ void launch_hist_to_bins(const double* d_hist, int64_t cells, hbg_bin* d_bins, c
   const int64_t blocks = std::min<int64_t>((cells + 255) / 256, 2368);
   hist_to_bins_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(d_hist, cells, d_bins);
   HBG_LAUNCH_CHECK();
+}
+
+void* scan_scratch(size_t bytes);
+
+void launch_finish_scan(const FinishScanArgsHost& h, cudaStream_t s) {
+  static std::once_flag once[64];
+  int dev = 0;
+  HBG_CUDA(cudaGetDevice(&dev));
+  std::call_once(once[dev & 63], [] {
+    HBG_CUDA(cudaFuncSetAttribute(finish_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  2 * 3 * 2048 * 8));
+  });
+  FinishScanArgs a{};
+  a.acc = static_cast<unsigned long long*>(h.acc);
+  a.exps = h.exps;
+  a.d = h.d;
+  a.k = h.k;
+  a.small_out = h.small_out;
+  a.large_io = h.large_io;
+  a.small_is_left = h.small_is_left;
+  a.totals = h.totals;
+  a.nl = h.nl;
+  a.nr = h.nr;
+  a.lsplit = h.lsplit;
+  a.rsplit = h.rsplit;
+  a.min_data = h.min_data;
+  a.lambda = h.lambda;
+  a.out = h.out;
+  const int64_t cells = static_cast<int64_t>(h.d) * h.k;
+  const int64_t per_cta = std::min<int64_t>(2048, std::max<int64_t>(2048, (cells + 147) / 148));
+  a.fchunk = static_cast<int>(std::max<int64_t>(1, per_cta / h.k));
+  const int nchunks = std::max(1, (h.d + a.fchunk - 1) / a.fchunk);
+  if (nchunks > 1) a.partial = static_cast<Cand*>(scan_scratch(2 * static_cast<size_t>(nchunks) * sizeof(Cand)));
+  finish_scan_kernel<<<nchunks, kScanThreads, static_cast<size_t>(a.fchunk) * h.k * 48, s>>>(a);
+  HBG_LAUNCH_CHECK();
+  if (nchunks > 1) {
+    ScanArgs f{};
+    f.d = h.d;
+    f.k = h.k;
+    f.d_totals = h.totals;
+    f.totals_stride = 2;
+    f.count0 = h.nl;
+    f.count1 = h.nr;
+    f.min_data = h.min_data;
+    f.lambda = h.lambda;
+    f.out_base = h.out;
+    f.partial = a.partial;
+    split_final_kernel<<<2, kScanThreads, 0, s>>>(f, nchunks);
+    HBG_LAUNCH_CHECK();
+  }
 }
 
 // Per-device grow-only scratch for the split scan's per-chunk winners. Calls

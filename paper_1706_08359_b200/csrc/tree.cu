@@ -303,11 +303,13 @@ __global__ void __launch_bounds__(kPartThreads) partition_small_kernel(PartArgs 
 // deterministic and more precise than fp32 accumulation (2^-40 of max|g| per
 // element).
 
-// max |g|, max |h| over n values -> power-of-two scale exponents (one CTA).
-__global__ void fixed_scale_kernel(const float* __restrict__ g, const float* __restrict__ h, int64_t n,
-                                   int* __restrict__ exps) {
+// max |g|, max |h| over n values (grid-wide; the max is order-free, so the
+// integer atomicMax on the non-negative floats' bit patterns is deterministic).
+__global__ void fixed_max_kernel(const float* __restrict__ g, const float* __restrict__ h, int64_t n,
+                                 unsigned int* __restrict__ maxbits) {
   float mg = 0.f, mh = 0.f;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     mg = fmaxf(mg, fabsf(g[i]));
     mh = fmaxf(mh, fabsf(h[i]));
   }
@@ -316,23 +318,19 @@ __global__ void fixed_scale_kernel(const float* __restrict__ g, const float* __r
     mg = fmaxf(mg, __shfl_xor_sync(0xffffffffu, mg, off));
     mh = fmaxf(mh, __shfl_xor_sync(0xffffffffu, mh, off));
   }
-  __shared__ float sg[32], sh[32];
   if ((threadIdx.x & 31) == 0) {
-    sg[threadIdx.x >> 5] = mg;
-    sh[threadIdx.x >> 5] = mh;
+    atomicMax(maxbits, __float_as_uint(mg));
+    atomicMax(maxbits + 1, __float_as_uint(mh));
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
-      mg = fmaxf(mg, sg[w]);
-      mh = fmaxf(mh, sh[w]);
-    }
-    int eg = 0, eh = 0;
-    frexpf(mg, &eg);  // mg < 2^eg
-    frexpf(mh, &eh);
-    exps[0] = 39 - eg;  // q = g * 2^exps[0], |q| <= 2^39
-    exps[1] = 39 - eh;
-  }
+}
+
+// -> power-of-two scale exponents: q = v * 2^exps, |q| <= 2^39.
+__global__ void fixed_scale_kernel(const unsigned int* __restrict__ maxbits, int* __restrict__ exps) {
+  int eg = 0, eh = 0;
+  frexpf(__uint_as_float(maxbits[0]), &eg);
+  frexpf(__uint_as_float(maxbits[1]), &eh);
+  exps[0] = 39 - eg;
+  exps[1] = 39 - eh;
 }
 
 // Thread = (row, 32-bit word of the packed row): the word's features.
@@ -400,7 +398,23 @@ size_t small_hist_acc_bytes(int d, int k) {
 }
 
 void launch_fixed_scale(const float* g, const float* h, int64_t n, int* exps, cudaStream_t s) {
-  fixed_scale_kernel<<<1, 1024, 0, s>>>(g, h, n, exps);
+  unsigned int* maxbits = reinterpret_cast<unsigned int*>(exps + 2);  // exps holds 4 ints
+  HBG_CUDA(cudaMemsetAsync(maxbits, 0, 2 * sizeof(unsigned int), s));
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n + 1023) / 1024, 1184));
+  fixed_max_kernel<<<static_cast<unsigned>(blocks), 1024, 0, s>>>(g, h, n, maxbits);
+  HBG_LAUNCH_CHECK();
+  fixed_scale_kernel<<<1, 1, 0, s>>>(maxbits, exps);
+  HBG_LAUNCH_CHECK();
+}
+
+void launch_small_hist_atomic(const int32_t* rows, const float* g, const float* h, int64_t n,
+                              const uint32_t* packed, int stride_words, int words_per_row, int bits, int d,
+                              int k, const int* exps, void* acc, cudaStream_t s) {
+  const int64_t items = n * words_per_row;
+  if (items == 0) return;
+  small_hist_atomic_kernel<<<static_cast<unsigned>((items + 255) / 256), 256, 0, s>>>(
+      rows, g, h, n, packed, stride_words, words_per_row, bits, d, k, exps,
+      static_cast<unsigned long long*>(acc));
   HBG_LAUNCH_CHECK();
 }
 
@@ -422,6 +436,7 @@ void launch_small_hist(const int32_t* rows, const float* g, const float* h, int6
 }
 
 void configure_tree_kernels() {
+  set_max_shared_carveout(reinterpret_cast<const void*>(fixed_max_kernel));
   set_max_shared_carveout(reinterpret_cast<const void*>(fixed_scale_kernel));
   set_max_shared_carveout(reinterpret_cast<const void*>(small_hist_atomic_kernel));
   set_max_shared_carveout(reinterpret_cast<const void*>(small_hist_finish_kernel));
