@@ -329,6 +329,7 @@ def run_hbg(args):
     pin_g = torch.from_numpy(g).pin_memory().numpy()
     pin_h = torch.from_numpy(h).pin_memory().numpy()
     leaf = hbg.LeafState(pin_idx, pin_g, pin_h)
+    contiguous = bool(len(idx) == 0 or (np.diff(idx) == 1).all())
     hbg.build_histograms_partitioned(ds, leaf)  # warm the workspace
     torch.cuda.synchronize()
     if world > 1:
@@ -343,8 +344,10 @@ def run_hbg(args):
     e2e_ms = float(e2e_ms.item())
     result["e2e"] = {
         "value": world * n * d / (e2e_ms / 1e3), "unit": "rows*features/s",
-        "h2d_bytes_per_step": int(n * (4 + 8 + 8)), "d2h_bytes_per_step": int(out.nbytes),
-        "ms_per_step": e2e_ms, "api": "hbg_build_histograms (host LeafState arrays, fp64 g/h)",
+        # a contiguous leaf (the root) uploads no indices: the library checks
+        # idx[i] == idx[0] + i on the host while g/h are in flight
+        "h2d_bytes_per_step": int(n * (8 + 8) + (0 if contiguous else 4 * n)), "d2h_bytes_per_step": int(out.nbytes),
+        "ms_per_step": e2e_ms, "api": "hbg_build_histograms (host LeafState arrays: int32 indices, fp64 g/h)",
         "steps": e2e_steps,
     }
 

@@ -10,6 +10,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "hbg_internal.h"
@@ -133,6 +134,39 @@ void check_ds(const hbg_dataset* ds) { require(ds != nullptr, "null dataset hand
 // the synchronous host drop-in.
 cudaStream_t pick(hbg_dataset*, void* stream) { return static_cast<cudaStream_t>(stream); }
 
+// idx[i] == idx[0] + i for all i? O(1) reject on the endpoints, then a
+// parallel scan (host threads; runs while the g/h copies are in flight).
+bool leaf_is_contiguous(const int32_t* idx, int64_t n) {
+  if (n <= 0) return false;
+  if (static_cast<int64_t>(idx[n - 1]) - idx[0] != n - 1) return false;
+  const int64_t first = idx[0];
+  auto check = [&](int64_t b, int64_t e) {
+    for (int64_t i = b; i < e; ++i)
+      if (idx[i] != first + i) return false;
+    return true;
+  };
+  const int T = n < (1 << 20) ? 1 : static_cast<int>(std::min<unsigned>(8, std::max(1u, std::thread::hardware_concurrency())));
+  if (T == 1) return check(0, n);
+  std::vector<char> ok(static_cast<size_t>(T), 1);
+  std::vector<std::thread> th;
+  for (int t = 1; t < T; ++t)
+    th.emplace_back([&, t] { ok[static_cast<size_t>(t)] = check(n * t / T, n * (t + 1) / T); });
+  ok[0] = check(0, n / T);
+  for (auto& x : th) x.join();
+  return std::all_of(ok.begin(), ok.end(), [](char c) { return c != 0; });
+}
+
+// Device row ids [first, first + n) of the dataset: the resident iota array.
+const int32_t* identity_rows(hbg_dataset* ds, int64_t first, cudaStream_t s) {
+  const int64_t N = ds->layout.num_rows;
+  if (ds->iota_rows < N) {
+    int32_t* io = static_cast<int32_t*>(ds->iota.get(static_cast<size_t>(N) * 4 + 4));
+    launch_iota(io, N, s);
+    ds->iota_rows = N;
+  }
+  return static_cast<const int32_t*>(ds->iota.p) + first;
+}
+
 // Device histogram of one leaf into d_hist; with `parent` also writes
 // sibling = parent - d_hist in the same pass (sibling may alias parent).
 void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const float* d_g,
@@ -151,14 +185,7 @@ void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const fl
     return;
   }
   require(d_g != nullptr && d_h != nullptr, "null gradient/hessian pointer");
-  if (d_idx == nullptr) {  // identity leaf [0, count): the kernel always reads indices
-    if (ds->iota_rows < count) {
-      int32_t* io = static_cast<int32_t*>(ds->iota.get(static_cast<size_t>(L.num_rows) * 4 + 4));
-      launch_iota(io, L.num_rows, s);
-      ds->iota_rows = L.num_rows;
-    }
-    d_idx = static_cast<const int32_t*>(ds->iota.p);
-  }
+  if (d_idx == nullptr) d_idx = identity_rows(ds, 0, s);  // identity leaf [0, count)
   HistPlan plan = plan_histogram(L.bits_per_bin, L.max_bin, L.num_groups, count, L.device);
   float* part = static_cast<float*>(ds->part.get(plan.part_values * 12 + 16));
   HistArgs a{};
@@ -570,18 +597,29 @@ int hbg_build_histograms(hbg_dataset* ds, const int32_t* indices, int64_t count,
     const size_t D = static_cast<size_t>(L.num_features) * L.max_bin;
     double* d_hist = static_cast<double*>(ds->host_hist.get(3 * D * sizeof(double) + 8));
     hbg_bin* d_bins = static_cast<hbg_bin*>(ds->host_bins.get(D * sizeof(hbg_bin) + 8));
-    int32_t* d_idx = nullptr;
+    const int32_t* d_idx = nullptr;
     float *d_gf = nullptr, *d_hf = nullptr;
     if (count > 0) {
       const size_t n = static_cast<size_t>(count);
-      d_idx = static_cast<int32_t*>(ds->host_idx.get(n * 4));
       double* d_gd = static_cast<double*>(ds->host_gd.get(n * 8));
       double* d_hd = static_cast<double*>(ds->host_hd.get(n * 8));
       d_gf = static_cast<float*>(ds->host_gf.get(n * 4));
       d_hf = static_cast<float*>(ds->host_hf.get(n * 4));
-      HBG_CUDA(cudaMemcpyAsync(d_idx, indices, n * 4, cudaMemcpyHostToDevice, s));
+      // g/h first: while the copy engine moves them (PCIe-bound, 16 B/row),
+      // the host checks whether the leaf is one contiguous row range (the
+      // root, or any leaf of an ordered layout). Such a leaf needs no index
+      // upload: the kernel reads the resident iota array at the range's start.
       HBG_CUDA(cudaMemcpyAsync(d_gd, gradients, n * 8, cudaMemcpyHostToDevice, s));
       HBG_CUDA(cudaMemcpyAsync(d_hd, hessians, n * 8, cudaMemcpyHostToDevice, s));
+      const int32_t first = indices[0];
+      if (leaf_is_contiguous(indices, count)) {
+        require(first >= 0 && first + count <= L.num_rows, "leaf row index out of range");
+        d_idx = identity_rows(ds, first, s);
+      } else {
+        int32_t* di = static_cast<int32_t*>(ds->host_idx.get(n * 4));
+        HBG_CUDA(cudaMemcpyAsync(di, indices, n * 4, cudaMemcpyHostToDevice, s));
+        d_idx = di;
+      }
       launch_f64_to_f32(d_gd, d_gf, count, s);
       launch_f64_to_f32(d_hd, d_hf, count, s);
     }

@@ -120,6 +120,35 @@ def test_edge_cases(hbg, oracle):
             assert got["count"][3, 63] == n and got["count"][4, 0] == n
 
 
+def test_host_dropin_contiguous_leaf_shortcut(hbg, oracle):
+    """Contiguous row ranges skip the index upload (the kernel reads the resident
+    iota at the range start); look-alikes with the same endpoints must not."""
+    rng = np.random.default_rng(11)
+    rows = 3_000_000  # > 1 Mi rows: the multi-threaded host check
+    cols = rng.integers(0, 64, size=(6, rows), dtype=np.uint8)
+    with hbg.Dataset(cols, 64) as ds:
+        # leaves > 1 Mi rows are held to the reference's own bits32 tolerance
+        # (1e-4): rounding the fp64 inputs to fp32 alone exceeds 1e-5 in
+        # near-cancelled bins at that size (DESIGN.md §5)
+        for first, n in ((0, rows), (12345, 2_000_000), (999, 250_000), (rows - 1, 1), (77, 5000)):
+            idx = np.arange(first, first + n, dtype=np.int32)
+            g, h = rng.normal(size=n), rng.random(n)
+            got = hbg.build_histograms_partitioned(ds, hbg.LeafState(idx, g, h))
+            assert_hist_close(got, oracle.build_histograms(cols, 64, idx, g, h, 64), tol=TOL if n < 2**20 else 1e-4)
+        # same first/last/length as a contiguous range, but two rows swapped
+        # (unsorted) or one row repeated and another skipped
+        n = 1_500_000
+        for tweak in ("swap", "dup"):
+            idx = np.arange(100, 100 + n, dtype=np.int32)
+            if tweak == "swap":
+                idx[700_000], idx[1_200_000] = idx[1_200_000], idx[700_000]
+            else:
+                idx[900_000] = idx[899_999]
+            g, h = rng.normal(size=n), rng.random(n)
+            got = hbg.build_histograms_partitioned(ds, hbg.LeafState(idx, g, h))
+            assert_hist_close(got, oracle.build_histograms(cols, 64, idx, g, h, 64), tol=1e-4)
+
+
 def test_unsorted_and_duplicate_free_indices(hbg, oracle):
     """Leaf order only changes fp32 rounding; counts stay exact."""
     rng = np.random.default_rng(9)
