@@ -429,7 +429,7 @@ def run_hbg(args):
             "hist_rows_built": built, "hist_launches_per_tree": kl / args.trees,
             "hist_kernel_ms_per_tree": km / args.trees,
             "rows_features_per_s_built": built * d / t_tree,
-            "note": "root + smaller child of every split (larger by subtraction); host loop, one sync per split",
+            "note": "root + smaller child of every split (larger by subtraction); all splits in one persistent cooperative kernel (grow_persistent.cu)",
         }
     clocks.stop()
     result["clocks"] = clocks.summary(t_wall0, t_wall1)

@@ -87,6 +87,7 @@ struct hbg_dataset {
   uint32_t* packed = nullptr;  // num_rows * row_stride_bytes
   cudaStream_t stream = nullptr;
   // workspace (not re-entrant per handle)
+  hbg::DevBuf colbins;  // column-major uint8 bins [feature][row] (the a1 layout), for partitions
   hbg::DevBuf part, iota, host_idx, host_gd, host_hd, host_gf, host_hf, host_hist, host_bins;
   int64_t iota_rows = 0;
   // tree growth workspace
@@ -94,6 +95,7 @@ struct hbg_dataset {
   hbg::DevBuf slots, part_scratch, tree_small;  // leaf histograms, partition scratch, splits/totals
   hbg::DevBuf boost_g, boost_h, boost_leaves;   // boosting: fp32 gradients, final leaf ranges
   hbg::DevBuf small_acc, small_exps;            // fixed-point accumulator for small leaves
+  hbg::DevBuf grow_nodes, grow_log, grow_tree, grow_counts, grow_scratch, grow_root, grow_prof;  // persistent grower
   void* pinned = nullptr;                      // host staging for per-split results
   // measurement hooks
   bool profiling = false;
@@ -469,6 +471,132 @@ void grow_tree_impl(hbg_dataset* ds, const float* d_grad, const float* d_hess,
   }
 }
 
+// grow_tree on the device with ONE persistent kernel for all splits
+// (grow_persistent.cu). The root (ordered buffers, totals, fixed-point scale,
+// histogram, best split) uses the same kernels as the host loop; everything
+// after it runs without host round trips. Single rank only: the row-sharded
+// path exchanges histograms through the host-visible allreduce hook.
+bool use_host_loop() {
+  const char* e = std::getenv("HBG_GROW");
+  return e != nullptr && std::strcmp(e, "host") == 0;
+}
+
+void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_hess, const hbg_grow_params& P,
+                          hbg_split* split_log, int32_t* num_splits, hbg_tree_node* nodes_out,
+                          int32_t* num_nodes, cudaStream_t s) {
+  const hbg_layout& L = ds->layout;
+  require(P.num_leaves >= 1, "num_leaves must be at least 1");
+  require(P.min_data_in_leaf >= 0, "min_data_in_leaf must be non-negative");
+  const int64_t N = L.num_rows;
+  const int d = L.num_features, k = L.max_bin;
+  const size_t D3 = 3 * static_cast<size_t>(d) * k;
+  const int max_nodes = std::max(1, 2 * P.num_leaves - 1);
+  double* slots = static_cast<double*>(ds->slots.get(static_cast<size_t>(max_nodes) * D3 * sizeof(double) + 8));
+  PersistentGrowArgs a{};
+  a.packed = reinterpret_cast<const uint8_t*>(ds->packed);
+  a.colbins = static_cast<const uint8_t*>(ds->colbins.p);
+  a.row_stride = L.row_stride_bytes;
+  a.words_per_row = L.words_per_row;
+  a.bits = L.bits_per_bin;
+  a.d = d;
+  a.k = k;
+  a.num_groups = L.num_groups;
+  a.num_rows = N;
+  for (int b = 0; b < 2; ++b) {
+    a.rows[b] = static_cast<int32_t*>(ds->ord[b][0].get(static_cast<size_t>(N) * 4 + 4));
+    a.g[b] = static_cast<float*>(ds->ord[b][1].get(static_cast<size_t>(N) * 4 + 4));
+    a.h[b] = static_cast<float*>(ds->ord[b][2].get(static_cast<size_t>(N) * 4 + 4));
+  }
+  a.slots = slots;
+  a.nodes = ds->grow_nodes.get(grow_nodes_bytes(P.num_leaves));
+  a.split_log = static_cast<hbg_split*>(ds->grow_log.get(static_cast<size_t>(max_nodes) * sizeof(hbg_split)));
+  a.tree = static_cast<hbg_tree_node*>(ds->grow_tree.get(static_cast<size_t>(max_nodes) * sizeof(hbg_tree_node)));
+  a.counts = static_cast<int*>(ds->grow_counts.get(4 * sizeof(int)));
+  a.scratch = ds->grow_scratch.get(grow_scratch_bytes(a, L.device));
+  a.acc = static_cast<unsigned long long*>(ds->small_acc.get(small_hist_acc_bytes(d, k)));
+  int* exps = static_cast<int*>(ds->small_exps.get(16));
+  a.exps = exps;
+  double* root = static_cast<double*>(ds->grow_root.get(4 * sizeof(double)));
+  a.root_totals = root;
+  a.num_leaves = P.num_leaves;
+  a.min_data = P.min_data_in_leaf;
+  a.lambda = P.lambda;
+  void* gscratch = ds->part_scratch.get(gather_scratch_doubles(N) * sizeof(double) + 64);
+
+  // root: ordered buffer 0 = (iota, g, h), fp64 totals in a fixed order
+  launch_iota(a.rows[0], N, s);
+  if (N > 0) {
+    HBG_CUDA(cudaMemcpyAsync(a.g[0], d_grad, static_cast<size_t>(N) * 4, cudaMemcpyDeviceToDevice, s));
+    HBG_CUDA(cudaMemcpyAsync(a.h[0], d_hess, static_cast<size_t>(N) * 4, cudaMemcpyDeviceToDevice, s));
+  }
+  launch_gather(a.rows[0], N, d_grad, d_hess, nullptr, nullptr, root, static_cast<double*>(gscratch), s);
+  const bool root_splittable = P.num_leaves >= 2 && !(N < 2 * P.min_data_in_leaf || N < 2);
+  if (!root_splittable) {
+    double tot[2] = {0.0, 0.0};
+    HBG_CUDA(cudaMemcpyAsync(tot, root, sizeof tot, cudaMemcpyDeviceToHost, s));
+    HBG_CUDA(cudaStreamSynchronize(s));
+    if (nodes_out) nodes_out[0] = hbg_tree_node{-1, -1, -1, -1, leaf_value(tot[0], tot[1], P.lambda)};
+    *num_splits = 0;
+    *num_nodes = 1;
+    return;
+  }
+  launch_fixed_scale(a.g[0], a.h[0], N, exps, s);
+  HBG_CUDA(cudaMemsetAsync(a.acc, 0, small_hist_acc_bytes(d, k), s));
+  build_device(ds, a.rows[0], N, a.g[0], a.h[0], HBG_GH_LEAF_ALIGNED, slots, s);
+  hbg_split* root_split = reinterpret_cast<hbg_split*>(static_cast<char*>(a.nodes) + grow_root_split_offset());
+  launch_best_split(slots, d, k, root, nullptr, 0.0, 0.0, N, P.min_data_in_leaf, P.lambda, root_split, s);
+  const char* pe = std::getenv("HBG_GROW_PROFILE");
+  std::vector<unsigned long long> prof;
+  if (pe != nullptr) {  // phase stamps of CTA 0, printed to stderr (development aid)
+    prof.assign(static_cast<size_t>(max_nodes) * 12, 0ull);
+    a.prof = static_cast<unsigned long long*>(ds->grow_prof.get(prof.size() * 8));
+    HBG_CUDA(cudaMemsetAsync(a.prof, 0, prof.size() * 8, s));
+  }
+  launch_grow_persistent(a, L.device, s);
+  int counts[4] = {0, 0, 0, 0};
+  HBG_CUDA(cudaMemcpyAsync(counts, a.counts, sizeof counts, cudaMemcpyDeviceToHost, s));
+  HBG_CUDA(cudaStreamSynchronize(s));
+  if (counts[2] != 0) {
+    static const char* what[] = {"", "grid barrier timed out", "partition disagrees with the histogram counts",
+                                 "split produced an empty side"};
+    throw Error(counts[2] == 3 || counts[2] == 2 ? HBG_ERR_LOGIC : HBG_ERR_CUDA,
+                std::string("persistent tree grower: ") + what[counts[2] & 3]);
+  }
+  *num_splits = counts[0];
+  *num_nodes = counts[1];
+  if (a.prof != nullptr) {
+    HBG_CUDA(cudaMemcpy(prof.data(), a.prof, prof.size() * 8, cudaMemcpyDeviceToHost));
+    // stamps: 0 start, 1 partitioned, 2 small-child histogram, 3 finish+scans, 4 barrier, 5 picked;
+    // slot 7: class = (large parent ? 4 : 0) + path (0 none, 1 direct, 2 shared-memory histogram)
+    static const char* nm[8] = {"partition", "child hist", "finish+scans", "barrier", "winners+pick", "loop",
+                                "(winners)", "(winners 2nd)"};
+    for (int cls = 0; cls < 8; ++cls) {
+      double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      int n[8] = {0, 0, 0, 0, 0, 0, 0, 0}, splits = 0;
+      for (int i = 0; i < counts[0]; ++i) {
+        const unsigned long long* t = prof.data() + static_cast<size_t>(i) * 12;
+        if (static_cast<int>(t[7]) != cls) continue;
+        ++splits;
+        for (int j = 0; j < 5; ++j)
+          if (t[j] && t[j + 1]) acc[j] += (t[j + 1] - t[j]) * 1e-3, ++n[j];
+        if (i + 1 < counts[0] && t[5] && t[12]) acc[5] += (t[12] - t[5]) * 1e-3, ++n[5];
+        if (t[4] && t[8]) acc[6] += (t[8] - t[4]) * 1e-3, ++n[6];
+        if (t[8] && t[9]) acc[7] += (t[9] - t[8]) * 1e-3, ++n[7];
+      }
+      if (splits == 0) continue;
+      std::fprintf(stderr, "grow class %s parent, path %d: %d splits\n", cls >= 4 ? "large" : "small", cls & 3, splits);
+      for (int j = 0; j < 8; ++j)
+        if (n[j]) std::fprintf(stderr, "   %-13s total %9.1f us avg %7.2f us\n", nm[j], acc[j], acc[j] / n[j]);
+    }
+  }
+  if (counts[0] > 0)
+    HBG_CUDA(cudaMemcpy(split_log, a.split_log, static_cast<size_t>(counts[0]) * sizeof(hbg_split),
+                        cudaMemcpyDeviceToHost));
+  if (nodes_out)
+    HBG_CUDA(cudaMemcpy(nodes_out, a.tree, static_cast<size_t>(counts[1]) * sizeof(hbg_tree_node),
+                        cudaMemcpyDeviceToHost));
+}
+
 // boost_one_iteration (boosting.cpp:26-51) on the device: gradients at the
 // cached scores, grow_tree, and scores += learning_rate * value of each row's
 // leaf — every final leaf owns a contiguous range of the ordered row buffer,
@@ -481,6 +609,27 @@ void boost_impl(hbg_dataset* ds, const double* d_targets, double* d_scores, int 
   float* g = static_cast<float*>(ds->boost_g.get(static_cast<size_t>(N) * 4 + 4));
   float* h = static_cast<float*>(ds->boost_h.get(static_cast<size_t>(N) * 4 + 4));
   launch_grad_hess(loss, d_scores, d_targets, N, g, h, s);
+  if (reduce.fn == nullptr && !use_host_loop()) {
+    std::vector<hbg_tree_node> local;
+    if (nodes == nullptr) {
+      local.resize(static_cast<size_t>(std::max(1, 2 * P.num_leaves - 1)));
+      nodes = local.data();
+    }
+    grow_tree_persistent(ds, g, h, P, split_log, num_splits, nodes, num_nodes, s);
+    if (*num_splits == 0) {  // a root-only tree: every row gets the root value
+      LeafRange r{0, N, nodes[0].value, 0, 0};
+      LeafRange* dl = static_cast<LeafRange*>(ds->boost_leaves.get(sizeof(LeafRange) + 8));
+      HBG_CUDA(cudaMemcpyAsync(dl, &r, sizeof r, cudaMemcpyHostToDevice, s));
+      launch_iota(static_cast<int32_t*>(ds->ord[0][0].get(static_cast<size_t>(N) * 4 + 4)), N, s);
+      launch_score_update(dl, 1, static_cast<const int32_t*>(ds->ord[0][0].p), nullptr, lr, d_scores, s);
+    } else {
+      launch_score_update_nodes(ds->grow_nodes.p, static_cast<const hbg_tree_node*>(ds->grow_tree.p), *num_nodes,
+                                static_cast<const int32_t*>(ds->ord[0][0].p),
+                                static_cast<const int32_t*>(ds->ord[1][0].p), lr, d_scores, s);
+    }
+    HBG_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
   std::vector<LeafRange> leaves;
   grow_tree_impl(ds, g, h, P, reduce, split_log, num_splits, nodes, num_nodes, s, &leaves);
   LeafRange* dl = static_cast<LeafRange*>(ds->boost_leaves.get(leaves.size() * sizeof(LeafRange) + 8));
@@ -531,14 +680,17 @@ int hbg_dataset_create(const uint8_t* const* columns, int32_t num_features, int6
     if (packed_bytes > 0) {
       for (int f = 0; f < num_features; ++f) require(columns[f] != nullptr, "null column pointer");
       // Upload column-major bins (a1) and pack on device (a2), one 32-feature
-      // slice group at a time so the staging buffer stays small.
-      DevBuf cols_buf, bad_buf;
+      // slice group at a time. The column-major copy stays resident: the tree
+      // grower's partition reads one byte per row of the split feature from
+      // it (instead of a 32-byte sector of the packed row).
+      DevBuf bad_buf;
+      uint8_t* colbins = static_cast<uint8_t*>(ds->colbins.get(static_cast<size_t>(num_features) * num_rows));
       int* d_bad = static_cast<int*>(bad_buf.get(sizeof(int)));
       HBG_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), ds->stream));
       const int stride_words = L.row_stride_bytes / 4;
       for (int f0 = 0; f0 < num_features; f0 += 32) {
         const int nf = std::min(32, num_features - f0);
-        uint8_t* d_cols = static_cast<uint8_t*>(cols_buf.get(static_cast<size_t>(nf) * num_rows));
+        uint8_t* d_cols = colbins + static_cast<size_t>(f0) * num_rows;
         for (int f = 0; f < nf; ++f) {
           HBG_CUDA(cudaMemcpyAsync(d_cols + static_cast<size_t>(f) * num_rows, columns[f0 + f],
                                    static_cast<size_t>(num_rows), cudaMemcpyHostToDevice, ds->stream));
@@ -732,8 +884,12 @@ int hbg_grow_tree(hbg_dataset* ds, const float* d_grad, const float* d_hess,
     require(ds->layout.num_rows == 0 || (d_grad != nullptr && d_hess != nullptr),
             "null gradient/hessian pointer");
     DeviceGuard dg(ds->layout.device);
-    grow_tree_impl(ds, d_grad, d_hess, *params, Reducer{nullptr, nullptr}, split_log, num_splits,
-                   nodes, num_nodes, static_cast<cudaStream_t>(stream));
+    if (use_host_loop())
+      grow_tree_impl(ds, d_grad, d_hess, *params, Reducer{nullptr, nullptr}, split_log, num_splits,
+                     nodes, num_nodes, static_cast<cudaStream_t>(stream));
+    else
+      grow_tree_persistent(ds, d_grad, d_hess, *params, split_log, num_splits, nodes, num_nodes,
+                           static_cast<cudaStream_t>(stream));
   });
 }
 

@@ -1,0 +1,1328 @@
+// grow_persistent.cu — best-first tree growth (grow_tree, tree.cpp:186-261) as
+// ONE persistent cooperative kernel: one CTA per SM, all splits of a tree run
+// without returning to the host.
+//
+// The host loop (capi.cu grow_tree_impl) pays a launch sequence and a
+// device->host round trip per split (~50 us/split measured) against a few us
+// of device work for the typical small leaf. Here the per-split decisions are
+// recomputed REDUNDANTLY by every CTA from the same data in the same order
+// (so every CTA reaches bit-identical results without a leader/broadcast
+// round trip); CTA 0 alone writes the persistent outputs. A typical split
+// (parent <= one tile of rows) costs ONE grid barrier:
+//
+//   pick        the open leaf with the largest gain, lowest node id on ties
+//               (the reference's pool order, strict > at tree.cpp:212-218)
+//   partition   partition_leaf (tree.cpp:114-128): stable, left rows first,
+//               into the other ordered buffer. Small parents: every CTA ranks
+//               the whole parent (registers), writes its share of the output;
+//               fp64 child totals (gather_leaf_statistics, tree.cpp:244-246)
+//               in a fixed order. Large parents: per-CTA chunks + one barrier.
+//   histogram   of the SMALLER child only (row a10). <= kDirectRows rows: each
+//               scan CTA accumulates its feature chunk directly (int64 fixed
+//               point in shared memory: deterministic); larger: the
+//               shared-memory rows-in-lanes schedule of hist_kernel over
+//               (segment, slice-group) items + a fixed-order fp64 reduction
+//   finish      per feature chunk: larger child = parent - small (every node
+//               owns a slot, no aliasing), both children's split scans
+//               (scan_device.cuh: the reference's fp64 operation order)
+//   barrier     then every CTA reduces the per-chunk winners and picks again
+//
+// Cross-CTA data written inside the kernel is read through L2 (__ldcg); only
+// the packed dataset uses the read-only path.
+#include <algorithm>
+#include <cstdio>
+#include <mutex>
+
+#include "hbg_internal.h"
+#include "hist_device.cuh"
+#include "scan_device.cuh"
+
+namespace hbg {
+
+namespace {
+
+using namespace dev;
+
+constexpr int kItems = 8;               // parent rows per thread in the small-parent path
+constexpr int64_t kDirectRows = 8192;   // smaller child: direct per-chunk histogram up to this size
+
+template <int K>
+__host__ __device__ constexpr int grow_threads() {
+  return K >= 256 ? 256 : 512;
+}
+
+struct NodeDev {
+  int64_t begin, count;  // rows [begin, begin+count) of ordered buffer `buf`
+  double grad, hess;     // fp64 totals (gather_leaf_statistics)
+  hbg_split best;        // valid when has_best
+  int32_t buf, has_best;
+};
+
+enum Path { kNoHist = 0, kDirect = 1, kSmem = 2 };
+
+// The split being executed (every CTA holds its own copy in shared memory).
+struct Desc {
+  int32_t done, iter;
+  int32_t parent, left_id, right_id;
+  int32_t buf_in, buf_out;
+  int32_t feature, thr;
+  int32_t lsplit, rsplit, small_is_left, path;
+  int32_t nseg, items;
+  int64_t begin, count;  // parent range
+  int64_t nl, nr;        // rows left / right (the split's left_count)
+  int64_t seg_len;
+  double tot[4];         // gl, hl, gr, hr (partition)
+};
+
+struct GrowArgs {
+  const uint8_t* packed;
+  const uint8_t* colbins;  // [d][N] uint8: one byte per (feature, row)
+  int64_t nrows;
+  int64_t row_stride;
+  int words_per_row, bits, d, k, num_groups;
+  int32_t* rows[2];
+  float* g[2];
+  float* h[2];
+  double* slots;  // node id -> 3*D doubles (SoA grad|hess|count)
+  NodeDev* nodes;
+  double* node_gain;  // gain of a node's best split, -1 without one
+  int* picked;        // split index + 1 at which the node was split, 0 = open
+  hbg_split* split_log;
+  hbg_tree_node* tree;
+  int* counts;    // [0] num_splits, [1] num_nodes, [2] error
+  unsigned* bar;  // grid barrier word
+  uint8_t* flags;
+  int64_t* cta_left;
+  double* cta_sums;
+  float* part_g;
+  float* part_h;
+  uint32_t* part_c;
+  Cand* cand;  // [2][nchunks]
+  const int* exps;
+  const double* root_tot;  // {G, H}
+  int64_t root_count;
+  int num_leaves;
+  int64_t min_data;
+  double lambda;
+  // launch geometry
+  int gb, wpg, nblocks;  // histogram: slice groups per CTA item, warps per group
+  int rpl;               // rows per lane of the histogram schedule
+  int fchunk, nchunks;   // finish/scan: features per chunk
+  long long timeout_cycles;
+  unsigned long long* prof;  // optional: [iter][kProfSlots] globaltimer stamps of CTA 0
+};
+
+constexpr int kProfSlots = 12;
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// CTA 0 stamps phase boundaries of iteration `iter` when profiling is on.
+__device__ __forceinline__ void stamp(const GrowArgs& a, int iter, int slot) {
+  if (a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0)
+    a.prof[static_cast<size_t>(iter) * kProfSlots + slot] = global_ns();
+}
+
+enum GrowError { kErrNone = 0, kErrBarrierTimeout = 1, kErrPartition = 2, kErrEmptySide = 3 };
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ int error_of(const GrowArgs& a) {
+  return *reinterpret_cast<volatile int*>(a.counts + 2);
+}
+
+__device__ __forceinline__ void set_error(const GrowArgs& a, int e) { atomicCAS(a.counts + 2, 0, e); }
+
+// Grid barrier with one atomic per CTA: CTA 0 adds 2^31 - (G-1), the others
+// 1, so the word's top bit flips exactly when the last CTA arrives (no reset,
+// no second round trip). Writes before the barrier are visible after it.
+__device__ __forceinline__ void grid_sync(const GrowArgs& a) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
+    const unsigned old = atom_add_acq_rel(a.bar, inc);
+    const long long t0 = clock64();
+    while (((old ^ ld_acquire(a.bar)) & 0x80000000u) == 0) {
+      if (clock64() - t0 > a.timeout_cycles) {
+        set_error(a, kErrBarrierTimeout);
+        break;
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <int NT>
+struct PartShared {
+  double sd[4][NT / 32];
+  long long sc[NT / 32];
+  int wl[NT / 32], wn[NT / 32], ol[NT / 32], on[NT / 32];
+  int tl, tn;
+  double tot[4];
+  long long cnt;
+  long long scan[NT / 32];
+};
+
+// Fixed-order block sum of 4 doubles + a count: warp shuffle tree, then the
+// warps in order (thread 0). Result in ps.tot / ps.cnt for every thread.
+template <int NT>
+__device__ void block_sum_4d1(double v[4], long long c, PartShared<NT>& ps) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] += __shfl_down_sync(0xffffffffu, v[j], off);
+    c += __shfl_down_sync(0xffffffffu, c, off);
+  }
+  __syncthreads();  // ps reuse
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ps.sd[j][w] = v[j];
+    ps.sc[w] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) {  // one thread per statistic, warps in order
+    const int j = threadIdx.x;
+    double s = 0.0;
+    for (int i = 0; i < NT / 32; ++i) s += ps.sd[j][i];
+    ps.tot[j] = s;
+  } else if (threadIdx.x == 32) {
+    long long s = 0;
+    for (int i = 0; i < NT / 32; ++i) s += ps.sc[i];
+    ps.cnt = s;
+  }
+  __syncthreads();
+}
+
+// Exclusive block scan of one count per thread (thread order).
+template <int NT>
+__device__ long long block_excl_scan(long long x, PartShared<NT>& ps) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  long long inc = x;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, inc, off);
+    if (lane >= off) inc += y;
+  }
+  __syncthreads();
+  if (lane == 31) ps.scan[w] = inc;
+  __syncthreads();
+  long long base = 0;
+  for (int i = 0; i < w; ++i) base += ps.scan[i];
+  return base + inc - x;
+}
+
+// Per-iteration block ranks of the left / valid ballots.
+template <int NT>
+__device__ __forceinline__ void block_ranks(unsigned lm, unsigned vm, PartShared<NT>& ps) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int W = NT / 32;
+  if (lane == 0) {
+    ps.wl[w] = __popc(lm);
+    ps.wn[w] = __popc(vm);
+  }
+  __syncthreads();
+  if (w == 0) {
+    int l = lane < W ? ps.wl[lane] : 0, nn = lane < W ? ps.wn[lane] : 0;
+    int il = l, in = nn;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int x = __shfl_up_sync(0xffffffffu, il, off), y = __shfl_up_sync(0xffffffffu, in, off);
+      if (lane >= off) {
+        il += x;
+        in += y;
+      }
+    }
+    if (lane < W) {
+      ps.ol[lane] = il - l;
+      ps.on[lane] = in - nn;
+    }
+    if (lane == W - 1) {
+      ps.tl = il;
+      ps.tn = in;
+    }
+  }
+  __syncthreads();
+}
+
+struct SplitFeat {
+  int feature, thr;
+};
+
+__device__ __forceinline__ SplitFeat split_feat(int feature, int /*bits*/, int thr) { return SplitFeat{feature, thr}; }
+
+// Bin of (row, feature) from the resident column-major copy: one byte.
+__device__ __forceinline__ uint32_t col_bin(const GrowArgs& a, int32_t row, int feature) {
+  return __ldg(a.colbins + static_cast<size_t>(feature) * a.nrows + row);
+}
+
+__device__ __forceinline__ bool goes_left(const GrowArgs& a, int32_t row, const SplitFeat& sf) {
+  return col_bin(a, row, sf.feature) <= static_cast<uint32_t>(sf.thr);  // tree.cpp:117-123
+}
+
+__device__ __forceinline__ bool splittable(int64_t n, int64_t min_data) { return !(n < 2 * min_data || n < 2); }
+
+__device__ __forceinline__ double* slot_of(const GrowArgs& a, int node) {
+  return a.slots + static_cast<size_t>(node) * 3 * static_cast<size_t>(a.d) * a.k;
+}
+
+__device__ __forceinline__ hbg_split load_split(const hbg_split* p) {
+  hbg_split s;
+  const double* src = reinterpret_cast<const double*>(p);
+  double* dst = reinterpret_cast<double*>(&s);
+#pragma unroll
+  for (int j = 0; j < static_cast<int>(sizeof(hbg_split) / 8); ++j) dst[j] = __ldcg(src + j);
+  return s;
+}
+
+__device__ __forceinline__ Cand warp_best(Cand c) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const Cand o = shfl_cand(c, (threadIdx.x & 31) ^ off);
+    if (better(o, c)) c = o;
+  }
+  return c;
+}
+
+// ---------------------------------------------------------------------- pick
+
+// Children of the split just executed, as every CTA computed them.
+struct Kid {
+  int64_t begin, count;
+  double grad, hess;
+  hbg_split best;
+  int32_t buf, has_best;
+};
+
+// Every CTA (warp 0): choose the parent of split `i` and fill `D` (identical
+// in every CTA: same data, same order). kid_l/kid_l+1: the newest nodes,
+// whose state comes from the CTA's own `kid` copies (CTA 0's global writes
+// of them are not yet visible). CTA 0 records the split.
+template <int NT>
+__device__ void pick(const GrowArgs& a, int i, int kid_l, const Kid* kid, Desc& D) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const int nnodes = 1 + 2 * i;
+    int err = lane == 0 ? error_of(a) : 0;
+    err = __shfl_sync(0xffffffffu, err, 0);
+    Cand c{0.0, -1, 0, 0.0, 0.0, 0};
+    if (i < a.num_leaves - 1 && err == kErrNone) {
+      for (int n0 = 0; n0 < nnodes; n0 += 4 * 32) {
+        double gain[4];
+        int pk[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {  // loads first, then the compares
+          const int n = n0 + u * 32 + lane;
+          gain[u] = n < nnodes ? __ldcg(a.node_gain + n) : -1.0;
+          pk[u] = n < nnodes ? __ldcg(a.picked + n) : 1;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int n = n0 + u * 32 + lane;
+          if (n >= nnodes) continue;
+          double g = gain[u];
+          if (kid_l >= 0 && (n == kid_l || n == kid_l + 1)) {
+            const Kid& q = kid[n - kid_l];
+            g = q.has_best ? q.best.gain : -1.0;
+          } else if (pk[u] != 0 && pk[u] != i + 1) {
+            g = -1.0;  // split earlier (i+1: CTA 0 already recorded this very pick)
+          }
+          if (g > 0.0) {
+            const Cand o{g, n, 0, 0.0, 0.0, 0};
+            if (better(o, c)) c = o;  // max gain, lowest node id on ties
+          }
+        }
+      }
+    }
+    c = warp_best(c);
+    const int p = c.f;
+    if (lane == 0) {
+      if (p < 0) {
+        D.done = 1;
+        if (blockIdx.x == 0) {
+          a.counts[0] = i;
+          a.counts[1] = nnodes;
+        }
+      } else {
+        int64_t begin, count;
+        int buf;
+        hbg_split bs;
+        if (kid_l >= 0 && (p == kid_l || p == kid_l + 1)) {
+          const Kid& q = kid[p - kid_l];
+          begin = q.begin;
+          count = q.count;
+          buf = q.buf;
+          bs = q.best;
+        } else {
+          const NodeDev* P = a.nodes + p;
+          begin = __ldcg(&P->begin);
+          count = __ldcg(&P->count);
+          buf = __ldcg(&P->buf);
+          bs = load_split(&P->best);
+        }
+        const int left = 1 + 2 * i, right = 2 + 2 * i;
+        if (blockIdx.x == 0) {
+          a.picked[p] = i + 1;
+          a.split_log[i] = bs;
+          a.tree[p] = hbg_tree_node{bs.feature, bs.threshold_bin, left, right, 0.0};
+        }
+        const int64_t nl = bs.left_count, nr = count - nl;
+        D.done = 0;
+        D.iter = i;
+        D.parent = p;
+        D.left_id = left;
+        D.right_id = right;
+        D.buf_in = buf;
+        D.buf_out = 1 - buf;
+        D.begin = begin;
+        D.count = count;
+        D.feature = bs.feature;
+        D.thr = bs.threshold_bin;
+        D.nl = nl;
+        D.nr = nr;
+        if (nl <= 0 || nr <= 0) {  // tree.cpp:124-126 (logic_error)
+          set_error(a, kErrEmptySide);
+          D.done = 1;
+        }
+        const bool scan = i + 2 < a.num_leaves;  // leaves after this split < num_leaves
+        D.lsplit = scan && splittable(nl, a.min_data);
+        D.rsplit = scan && splittable(nr, a.min_data);
+        D.small_is_left = nl <= nr;
+        const int64_t ns = nl <= nr ? nl : nr;
+        D.path = !(D.lsplit || D.rsplit) ? kNoHist : (ns <= kDirectRows ? kDirect : kSmem);
+        if (D.path == kSmem) {
+          // row segments x slice-group blocks ~ one item per CTA, >= 2 tiles per warp
+          const int64_t min_rows = static_cast<int64_t>(a.wpg) * 32 * 2 * a.rpl;
+          int64_t nseg = gridDim.x / a.nblocks;
+          if (nseg < 1) nseg = 1;
+          const int64_t cap = (ns + min_rows - 1) / min_rows;
+          if (nseg > cap) nseg = cap;
+          int64_t seg_len = (ns + nseg - 1) / nseg;
+          seg_len = (seg_len + 31) / 32 * 32;
+          nseg = (ns + seg_len - 1) / seg_len;
+          D.seg_len = seg_len;
+          D.nseg = static_cast<int32_t>(nseg);
+          D.items = static_cast<int32_t>(nseg * a.nblocks);
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// After the partition (all CTAs): the children's local records; CTA 0
+// writes their leaf values.
+__device__ void set_children(const GrowArgs& a, const Desc& D, Kid* kid) {
+  if (threadIdx.x == 0) {
+    kid[0] = Kid{D.begin, D.nl, D.tot[0], D.tot[1], hbg_split{}, D.buf_out, 0};
+    kid[1] = Kid{D.begin + D.nl, D.nr, D.tot[2], D.tot[3], hbg_split{}, D.buf_out, 0};
+    kid[0].best.feature = kid[1].best.feature = -1;
+    if (blockIdx.x == 0) {
+      a.tree[D.left_id] = hbg_tree_node{-1, -1, -1, -1, leaf_value(D.tot[0], D.tot[1], a.lambda)};
+      a.tree[D.right_id] = hbg_tree_node{-1, -1, -1, -1, leaf_value(D.tot[2], D.tot[3], a.lambda)};
+    }
+  }
+  __syncthreads();
+}
+
+// CTA 0: the children's persistent records (read by later picks, after at
+// least one more barrier).
+__device__ void store_children(const GrowArgs& a, const Desc& D, const Kid* kid) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  for (int c = 0; c < 2; ++c) {
+    const int id = c == 0 ? D.left_id : D.right_id;
+    const Kid& q = kid[c];
+    a.nodes[id] = NodeDev{q.begin, q.count, q.grad, q.hess, q.best, q.buf, q.has_best};
+    a.node_gain[id] = q.has_best ? q.best.gain : -1.0;
+  }
+}
+
+// ------------------------------------------------------------------ partition
+
+// Small parent (<= kItems*NT rows): EVERY CTA reads and ranks the whole parent
+// (thread t holds positions [t*kItems, t*kItems+kItems) in registers), so the
+// fp64 totals and the left count are known everywhere without a barrier; each
+// CTA writes only its share of the output positions. Returns the rows kept in
+// registers for the direct histogram.
+struct RegRows {
+  int32_t row[kItems];
+  float g[kItems], h[kItems];
+  uint32_t left;  // bit j: item j goes left
+  int nvalid;
+};
+
+template <int NT>
+__device__ void partition_redundant(const GrowArgs& a, Desc& D, RegRows& rr, PartShared<NT>& ps, int parts) {
+  const int64_t n = D.count;
+  const int32_t* rin = a.rows[D.buf_in] + D.begin;
+  const float* gin = a.g[D.buf_in] + D.begin;
+  const float* hin = a.h[D.buf_in] + D.begin;
+  const SplitFeat sf = split_feat(D.feature, a.bits, D.thr);
+  const int64_t p0 = static_cast<int64_t>(threadIdx.x) * kItems;
+  {
+    int64_t nv = n - p0;
+    nv = nv < 0 ? 0 : (nv > kItems ? kItems : nv);
+    rr.nvalid = static_cast<int>(nv);
+  }
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) rr.row[j] = j < rr.nvalid ? __ldcg(rin + p0 + j) : 0;
+  bool lf[kItems];
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) lf[j] = j < rr.nvalid && goes_left(a, rr.row[j], sf);
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    rr.g[j] = j < rr.nvalid ? __ldcg(gin + p0 + j) : 0.f;
+    rr.h[j] = j < rr.nvalid ? __ldcg(hin + p0 + j) : 0.f;
+  }
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  long long c = 0;
+  rr.left = 0;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    if (j >= rr.nvalid) continue;
+    if (lf[j]) {
+      rr.left |= 1u << j;
+      ++c;
+      v[0] += rr.g[j];
+      v[1] += rr.h[j];
+    } else {
+      v[2] += rr.g[j];
+      v[3] += rr.h[j];
+    }
+  }
+  const long long lbase = block_excl_scan<NT>(c, ps);  // left rows before this thread's positions
+  block_sum_4d1<NT>(v, c, ps);
+  const int64_t L = ps.cnt;
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < 4; ++j) D.tot[j] = ps.tot[j];
+    if (L != D.nl) set_error(a, kErrPartition);
+  }
+  // this CTA's share of the output positions (the first `parts` CTAs partition)
+  const int64_t share = (n + parts - 1) / parts;
+  const int64_t s0 = static_cast<int64_t>(blockIdx.x) * share, s1 = min(n, s0 + share);
+  int32_t* rout = a.rows[D.buf_out] + D.begin;
+  float* gout = a.g[D.buf_out] + D.begin;
+  float* hout = a.h[D.buf_out] + D.begin;
+  long long lr = lbase;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    if (j >= rr.nvalid) continue;
+    const int64_t pos = p0 + j;
+    const bool left = (rr.left >> j) & 1u;
+    const int64_t dst = left ? lr : L + (pos - lr);
+    if (pos >= s0 && pos < s1) {
+      rout[dst] = rr.row[j];
+      gout[dst] = rr.g[j];
+      hout[dst] = rr.h[j];
+    }
+    lr += left ? 1 : 0;
+  }
+  __syncthreads();
+}
+
+// Large parents: CTA b owns positions [b*chunk, (b+1)*chunk), processed in
+// tiles of NT*kItems positions; thread t holds tile positions
+// [t*kItems, t*kItems + kItems) so its loads are independent and its ranks
+// come from one block scan per tile.
+// Positions per thread per tile: up to kItems, fewer for parents that would
+// otherwise leave CTAs idle.
+template <int NT>
+__device__ __forceinline__ int part_ipt(int64_t n) {
+  const int64_t per = (n + static_cast<int64_t>(gridDim.x) * NT - 1) / (static_cast<int64_t>(gridDim.x) * NT);
+  return static_cast<int>(per < 1 ? 1 : (per > kItems ? kItems : per));
+}
+
+template <int NT>
+__device__ __forceinline__ int64_t part_chunk(int64_t n) {
+  const int64_t tile = static_cast<int64_t>(NT) * part_ipt<NT>(n);
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  return (per + tile - 1) / tile * tile;
+}
+
+// Pass 1 (every CTA, its chunk): side flags, left count, fp64 side sums.
+template <int NT>
+__device__ void partition_count(const GrowArgs& a, const Desc& D, PartShared<NT>& ps) {
+  const int64_t n = D.count, chunk = part_chunk<NT>(n);
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * chunk, e = min(n, s + chunk);
+  const int32_t* rin = a.rows[D.buf_in] + D.begin;
+  const float* gin = a.g[D.buf_in] + D.begin;
+  const float* hin = a.h[D.buf_in] + D.begin;
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  long long c = 0;
+  const int ipt = part_ipt<NT>(n);
+  for (int64_t t0 = s; t0 < e; t0 += static_cast<int64_t>(NT) * ipt) {
+    const int64_t p0 = t0 + static_cast<int64_t>(threadIdx.x) * ipt;
+    const int64_t pe = min(e, p0 + ipt);
+    int32_t r[kItems];
+    float gv[kItems], hv[kItems];
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+      const bool ok = p0 + j < pe;
+      r[j] = ok ? __ldcg(rin + p0 + j) : 0;
+      gv[j] = ok ? __ldcg(gin + p0 + j) : 0.f;
+      hv[j] = ok ? __ldcg(hin + p0 + j) : 0.f;
+    }
+    uint32_t bin[kItems];
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) bin[j] = p0 + j < pe ? col_bin(a, r[j], D.feature) : 0u;
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+      if (p0 + j >= pe) continue;
+      const bool left = bin[j] <= static_cast<uint32_t>(D.thr);  // tree.cpp:117-123
+      a.flags[p0 + j] = left ? 1 : 0;
+      if (left) {
+        ++c;
+        v[0] += gv[j];
+        v[1] += hv[j];
+      } else {
+        v[2] += gv[j];
+        v[3] += hv[j];
+      }
+    }
+  }
+  block_sum_4d1<NT>(v, c, ps);
+  if (threadIdx.x == 0) {
+    a.cta_left[blockIdx.x] = ps.cnt;
+    for (int j = 0; j < 4; ++j) a.cta_sums[4 * blockIdx.x + j] = ps.tot[j];
+  }
+}
+
+// After the barrier (every CTA, redundantly): this CTA's offset among the
+// left rows, the left total and the children's totals (fixed-order sum over
+// CTAs), then pass 2: the stable scatter of this CTA's chunk, tile by tile.
+template <int NT>
+__device__ void partition_scatter(const GrowArgs& a, Desc& D, PartShared<NT>& ps) {
+  const int G = gridDim.x;
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  long long c = 0;
+  for (int b = threadIdx.x; b < G; b += NT) {  // G <= NT: one CTA record per thread
+    c = __ldcg(a.cta_left + b);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = __ldcg(a.cta_sums + 4 * b + j);
+  }
+  const long long before_t = block_excl_scan<NT>(c, ps);
+  __shared__ long long s_before;
+  if (static_cast<int>(threadIdx.x) == static_cast<int>(blockIdx.x)) s_before = before_t;
+  block_sum_4d1<NT>(v, c, ps);
+  const int64_t L = ps.cnt;
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < 4; ++j) D.tot[j] = ps.tot[j];
+    if (L != D.nl) set_error(a, kErrPartition);
+  }
+  __syncthreads();
+  const int64_t n = D.count, chunk = part_chunk<NT>(n);
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * chunk, e = min(n, s + chunk);
+  if (s >= e) return;
+  const int32_t* rin = a.rows[D.buf_in] + D.begin;
+  const float* gin = a.g[D.buf_in] + D.begin;
+  const float* hin = a.h[D.buf_in] + D.begin;
+  int32_t* rout = a.rows[D.buf_out] + D.begin;
+  float* gout = a.g[D.buf_out] + D.begin;
+  float* hout = a.h[D.buf_out] + D.begin;
+  int64_t lrun = s_before;  // left rows before this tile
+  const int ipt = part_ipt<NT>(n);
+  for (int64_t t0 = s; t0 < e; t0 += static_cast<int64_t>(NT) * ipt) {
+    const int64_t p0 = t0 + static_cast<int64_t>(threadIdx.x) * ipt;
+    const int64_t pe = min(e, p0 + ipt);
+    int32_t r[kItems];
+    float gv[kItems], hv[kItems];
+    uint32_t lf = 0;
+    int cl = 0;
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+      const bool ok = p0 + j < pe;
+      const bool left = ok && __ldcg(a.flags + p0 + j);
+      lf |= left ? 1u << j : 0u;
+      cl += left ? 1 : 0;
+      r[j] = ok ? __ldcg(rin + p0 + j) : 0;
+      gv[j] = ok ? __ldcg(gin + p0 + j) : 0.f;
+      hv[j] = ok ? __ldcg(hin + p0 + j) : 0.f;
+    }
+    const long long lb = block_excl_scan<NT>(cl, ps);  // left rows of this tile before this thread
+    __shared__ long long s_tile_left;
+    if (threadIdx.x == NT - 1) s_tile_left = lb + cl;
+    int64_t lr = lrun + lb;
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+      const int64_t pos = p0 + j;
+      if (pos >= pe) continue;
+      const bool left = (lf >> j) & 1u;
+      const int64_t dst = left ? lr : L + (pos - lr);
+      rout[dst] = r[j];
+      gout[dst] = gv[j];
+      hout[dst] = hv[j];
+      lr += left ? 1 : 0;
+    }
+    __syncthreads();
+    lrun += s_tile_left;
+  }
+}
+
+// ------------------------------------------------------------------ histogram
+
+__device__ __forceinline__ void small_child(const GrowArgs& a, const Desc& D, const int32_t*& rows,
+                                            const float*& g, const float*& h, int64_t& n) {
+  const int64_t off = D.small_is_left ? 0 : D.nl;
+  n = D.small_is_left ? D.nl : D.nr;
+  rows = a.rows[D.buf_out] + D.begin + off;
+  g = a.g[D.buf_out] + D.begin + off;
+  h = a.h[D.buf_out] + D.begin + off;
+}
+
+// int64 fixed-point accumulation in shared memory from native 32-bit atomics:
+// the low word's returned old value gives the carry into the high word.
+// Integer addition commutes: the sum is exact and order-independent.
+__device__ __forceinline__ void smem_add_i64(unsigned* lohi, long long q) {
+  const unsigned lo = static_cast<unsigned>(q);
+  const unsigned hi = static_cast<unsigned>(static_cast<unsigned long long>(q) >> 32);
+  const unsigned old = atomicAdd(lohi, lo);
+  const unsigned carry = old + lo < old ? 1u : 0u;
+  if (hi + carry) atomicAdd(lohi + 1, hi + carry);
+}
+
+// Direct histogram of up to kItems (row, g, h) (bit u of `mask` set) into the
+// chunk's fixed-point cells [f][bin]: acc holds 2 words per cell for g, then
+// h, then a u32 count. sg, sh: exact powers of two, so the products equal
+// ldexp(v, e). All loads of a feature are issued before its atomics.
+__device__ __forceinline__ void direct_accumulate(const GrowArgs& a, unsigned* acc, int cells, int f0, int nf,
+                                                  const int32_t (&row)[kItems], const float (&g)[kItems],
+                                                  const float (&h)[kItems], uint32_t mask, double sg, double sh) {
+  long long qg[kItems], qh[kItems];
+#pragma unroll
+  for (int u = 0; u < kItems; ++u) {
+    qg[u] = __double2ll_rn(static_cast<double>(g[u]) * sg);
+    qh[u] = __double2ll_rn(static_cast<double>(h[u]) * sh);
+  }
+  for (int f = 0; f < nf; ++f) {
+    uint32_t b[kItems];
+#pragma unroll
+    for (int u = 0; u < kItems; ++u) b[u] = ((mask >> u) & 1u) ? col_bin(a, row[u], f0 + f) : 0u;
+#pragma unroll
+    for (int u = 0; u < kItems; ++u) {
+      if (!((mask >> u) & 1u)) continue;
+      const int cell = f * a.k + static_cast<int>(b[u]);
+      smem_add_i64(acc + 2 * cell, qg[u]);
+      smem_add_i64(acc + 2 * (cells + cell), qh[u]);
+      atomicAdd(acc + 4 * cells + cell, 1u);
+    }
+  }
+}
+
+// ------------------------------------------------------------ finish and scan
+
+// Smem layout of the finish phase: staging [child][stat][bin][feature] fp64
+// (6 * fchunk * k doubles), then the direct accumulator (20 B per cell).
+__device__ __forceinline__ unsigned* direct_acc(const GrowArgs& a, unsigned char* smem) {
+  return reinterpret_cast<unsigned*>(smem + static_cast<size_t>(6) * a.fchunk * a.k * sizeof(double));
+}
+
+__device__ __forceinline__ void zero_direct(const GrowArgs& a, unsigned char* smem, int cells, int NT) {
+  unsigned* acc = direct_acc(a, smem);
+  for (int i = threadIdx.x; i < 5 * cells; i += NT) acc[i] = 0u;
+}
+
+// Per feature chunk c: the smaller child's fp64 histogram (from the direct
+// accumulator, or the fixed-order fp64 sum of the item partials), the larger
+// child = parent - small, both written to their node slots and staged for
+// the two scans; per-chunk winners -> a.cand.
+template <int K, int NT>
+__device__ void finish_chunk(const GrowArgs& a, const Desc& D, int c_idx, unsigned char* smem, Cand* wb) {
+  const int c = c_idx;
+  constexpr int kCells = K * 32;
+  const int d = a.d, k = a.k;
+  const size_t Dc = static_cast<size_t>(d) * k;
+  const int small_id = D.small_is_left ? D.left_id : D.right_id;
+  const int large_id = D.small_is_left ? D.right_id : D.left_id;
+  const double* par = slot_of(a, D.parent);
+  double* so = slot_of(a, small_id);
+  double* lo = slot_of(a, large_id);
+  double* st = reinterpret_cast<double*>(smem);
+  const int chunk_cells = a.fchunk * k;
+  double* sm = st + (D.small_is_left ? 0 : 3 * chunk_cells);
+  double* lg = st + (D.small_is_left ? 3 * chunk_cells : 0);
+  const int f0 = c * a.fchunk;
+  const int nf = min(a.fchunk, d - f0);
+  const int cells = nf * k;
+  if (D.path == kDirect) {
+    const double sg = ldexp(1.0, -a.exps[0]), sh = ldexp(1.0, -a.exps[1]);
+    const unsigned* acc = direct_acc(a, smem);
+    for (int i = threadIdx.x; i < cells; i += NT) {  // i = f * k + b
+      const auto rd = [&](int w) {
+        return static_cast<long long>((static_cast<unsigned long long>(acc[2 * w + 1]) << 32) | acc[2 * w]);
+      };
+      const int f = i / k, b = i - f * k;
+      const int t = b * nf + f;
+      sm[t] = static_cast<double>(rd(i)) * sg;
+      sm[chunk_cells + t] = static_cast<double>(rd(cells + i)) * sh;
+      sm[2 * chunk_cells + t] = static_cast<double>(acc[4 * cells + i]);
+    }
+  } else {
+    // tpc threads per cell sum strided segments; combined in a fixed order
+    int tpc = NT / cells;
+    tpc = tpc >= 32 ? 32 : (tpc >= 16 ? 16 : (tpc >= 8 ? 8 : (tpc >= 4 ? 4 : (tpc >= 2 ? 2 : 1))));
+    const int per_pass = NT / tpc;
+    for (int i0 = 0; i0 < cells; i0 += per_pass) {
+      const int i = i0 + static_cast<int>(threadIdx.x) / tpc;
+      const int j = threadIdx.x % tpc;
+      double vg = 0.0, vh = 0.0;
+      unsigned long long vc = 0;
+      if (i < cells) {
+        const int f = f0 + i / k, b = i % k;
+        const int gr = f >> 5, bi = gr / a.gb, gl = gr - bi * a.gb;
+        const int cl = b * 32 + (f & 31);
+#pragma unroll 4
+        for (int s = j; s < D.nseg; s += tpc) {
+          const size_t o = ((static_cast<size_t>(s) * a.nblocks + bi) * a.gb + gl) * kCells + cl;
+          vg += static_cast<double>(__ldcg(a.part_g + o));
+          vh += static_cast<double>(__ldcg(a.part_h + o));
+          vc += __ldcg(a.part_c + o);
+        }
+      }
+      for (int off = tpc >> 1; off > 0; off >>= 1) {  // fixed-shape tree within the group
+        vg += __shfl_down_sync(0xffffffffu, vg, off, tpc);
+        vh += __shfl_down_sync(0xffffffffu, vh, off, tpc);
+        vc += __shfl_down_sync(0xffffffffu, vc, off, tpc);
+      }
+      if (j == 0 && i < cells) {
+        const int f = i / k, b = i - f * k;
+        const int t = b * nf + f;
+        sm[t] = vg;
+        sm[chunk_cells + t] = vh;
+        sm[2 * chunk_cells + t] = static_cast<double>(vc);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < cells; i += NT) {
+    const size_t o = static_cast<size_t>(f0) * k + i;
+    const int f = i / k, b = i - f * k;
+    const int t = b * nf + f;
+    const double pg = __ldcg(par + o), ph = __ldcg(par + Dc + o), pc = __ldcg(par + 2 * Dc + o);
+    const double vg = sm[t], vh = sm[chunk_cells + t], vc = sm[2 * chunk_cells + t];
+    so[o] = vg;
+    so[Dc + o] = vh;
+    so[2 * Dc + o] = vc;
+    const double xg = pg - vg, xh = ph - vh, xc = pc - vc;
+    lo[o] = xg;
+    lo[Dc + o] = xh;
+    lo[2 * Dc + o] = xc;
+    lg[t] = xg;
+    lg[chunk_cells + t] = xh;
+    lg[2 * chunk_cells + t] = xc;
+  }
+  __syncthreads();
+  // both children's scans at once: threads [0, NT/2) child 0, the rest child 1
+  {
+    constexpr int half = NT / 2, W = NT / 32;
+    const int child = static_cast<int>(threadIdx.x) < half ? 0 : 1;
+    const int tid = static_cast<int>(threadIdx.x) - child * half;
+    const bool want = child == 0 ? D.lsplit : D.rsplit;
+    double* base = st + child * 3 * chunk_cells;
+    const double gt = D.tot[2 * child], ht = D.tot[2 * child + 1];
+    const int64_t count = child == 0 ? D.nl : D.nr;
+    Cand best = scan_staged_t(base, base + chunk_cells, base + 2 * chunk_cells, want ? nf : 0, k, f0, gt, ht,
+                              static_cast<double>(count), static_cast<double>(a.min_data), a.lambda, tid, half);
+    best = warp_best(best);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) wb[w] = best;
+    __syncthreads();
+    if (w == 0 || w == W / 2) {
+      Cand c = lane < W / 2 ? wb[w + lane] : Cand{0.0, -1, -1, 0.0, 0.0, 0};
+      c = warp_best(c);
+      if (lane == 0 && want) a.cand[child * a.nchunks + c_idx] = c;
+    }
+    __syncthreads();
+  }
+}
+
+// Every CTA (warp 0): per-child winner over the chunks (bit-identical in every
+// CTA); lanes 0-15 child 0, lanes 16-31 child 1.
+template <int NT>
+__device__ void winners(const GrowArgs& a, const Desc& D, Kid* kid) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x, child = lane >> 4, sub = lane & 15;
+    const bool want = child == 0 ? D.lsplit : D.rsplit;
+    Cand c{0.0, -1, -1, 0.0, 0.0, 0};
+    if (want) {
+      for (int i = sub; i < a.nchunks; i += 16) {
+        const Cand* p = a.cand + child * a.nchunks + i;
+        Cand o;
+        o.gain = __ldcg(&p->gain);
+        o.f = __ldcg(&p->f);
+        o.b = __ldcg(&p->b);
+        o.lg = __ldcg(&p->lg);
+        o.lh = __ldcg(&p->lh);
+        o.lc = __ldcg(&p->lc);
+        if (better(o, c)) c = o;
+      }
+    }
+#pragma unroll
+    for (int off = 8; off > 0; off >>= 1) {  // within each half-warp
+      const Cand o = shfl_cand(c, lane ^ off);
+      if (better(o, c)) c = o;
+    }
+    if (sub == 0 && want) {
+      const double gt = D.tot[2 * child], ht = D.tot[2 * child + 1];
+      const int64_t count = child == 0 ? D.nl : D.nr;
+      write_split(c, gt, ht, count, a.lambda, &kid[child].best);
+      kid[child].has_best = c.f >= 0 ? 1 : 0;
+    }
+  }
+  __syncthreads();
+}
+
+struct TileIn {
+  int32_t row;
+  float g, h;
+};
+
+// The rows-in-lanes, feature-rotated accumulation of hist_kernel
+// (hist_kernels.cu) over positions [s0, s1) of one slice group, for one warp
+// of `wpg` row-interleaved warps. idx/g/h were written by this kernel's
+// partition, so they are read through L2.
+template <int BITS, int K>
+__device__ __forceinline__ void accumulate_rows(const GrowArgs& a, const int32_t* idx, const float* gp,
+                                                const float* hp, int64_t s0, int64_t s1, int sub,
+                                                const unsigned char* base, uint32_t gh_base, uint32_t* cnt_g) {
+  constexpr int R = rows_per_lane<K>();
+  const int lane = threadIdx.x & 31;
+  const int64_t step = static_cast<int64_t>(a.wpg) * 32 * R;
+  auto fetch_entry = [&](int64_t t, TileIn(&in)[R]) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t pos = t + 32 * r + lane;
+      if (pos < s1) {
+        in[r].row = __ldcg(idx + pos);
+        in[r].g = __ldcg(gp + pos);
+        in[r].h = __ldcg(hp + pos);
+      } else {
+        in[r].row = -1;
+        in[r].g = 0.f;
+        in[r].h = 0.f;
+      }
+    }
+  };
+  auto fetch_slice = [&](TileIn(&in)[R], Slice<BITS>(&sl)[R]) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (in[r].row >= 0) {
+        load_slice<BITS>(base + static_cast<int64_t>(in[r].row) * a.row_stride, sl[r]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < Slice<BITS>::kWords; ++j) sl[r].w[j] = 0;
+      }
+    }
+  };
+  int64_t t = s0 + static_cast<int64_t>(sub) * 32 * R;
+  TileIn e0[R], e1[R];
+  Slice<BITS> cur[R];
+  fetch_entry(t, e0);
+  fetch_entry(t + step, e1);
+  fetch_slice(e0, cur);
+  for (; t < s1; t += step) {
+    TileIn e2[R];
+    Slice<BITS> nxt[R];
+    fetch_entry(t + 2 * step, e2);
+    fetch_slice(e1, nxt);
+#pragma unroll
+    for (int r = 0; r < R; ++r) rotate_slice<BITS>(cur[r], lane);
+    if (t + 32 * R <= s1) {
+      float g[R], h[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        g[r] = e0[r].g;
+        h[r] = e0[r].h;
+      }
+#pragma unroll
+      for (int p = 0; p < 32; ++p) update_step_rows<BITS, K, R>(cur, p, lane, gh_base, cnt_g, g, h);
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const bool valid = e0[r].row >= 0;
+#pragma unroll
+        for (int p = 0; p < 32; ++p)
+          update_step<BITS, K, true>(cur[r], p, lane, gh_base, cnt_g, e0[r].g, e0[r].h, valid);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      e0[r] = e1[r];
+      e1[r] = e2[r];
+      cur[r] = nxt[r];
+    }
+  }
+}
+
+// Shared-memory histogram of the smaller child: items = (row segment, slice
+// group block); each item -> one fp32/u32 partial per group of the block.
+template <int BITS, int K, int NT>
+__device__ void hist_smem(const GrowArgs& a, const Desc& D, unsigned char* smem) {
+  constexpr int kCells = K * 32;
+  const int32_t* rows;
+  const float* g;
+  const float* h;
+  int64_t n;
+  small_child(a, D, rows, g, h, n);
+  const int warps = a.gb * a.wpg;
+  float2* gh = reinterpret_cast<float2*>(smem);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + static_cast<size_t>(warps) * kCells * 8);
+  const int w = threadIdx.x >> 5;
+  for (int item = blockIdx.x; item < D.items; item += gridDim.x) {
+    const int bi = item % a.nblocks, seg = item / a.nblocks;
+    {
+      const int n16 = (warps * kCells * 8 + a.gb * kCells * 4) / 16;
+      uint4* z = reinterpret_cast<uint4*>(smem);
+      for (int i = threadIdx.x; i < n16; i += NT) z[i] = make_uint4(0, 0, 0, 0);
+    }
+    __syncthreads();
+    if (w < warps) {
+      const int gl = w % a.gb, sub = w / a.gb;
+      const int group = bi * a.gb + gl;
+      if (group < a.num_groups) {
+        const int64_t s0 = static_cast<int64_t>(seg) * D.seg_len;
+        const int64_t s1 = min(s0 + D.seg_len, n);
+        const uint32_t gh_base = smem_addr(gh + static_cast<size_t>(w) * kCells);
+        const unsigned char* base = a.packed + static_cast<size_t>(group) * Slice<BITS>::kWords * 4;
+        accumulate_rows<BITS, K>(a, rows, g, h, s0, s1, sub, base, gh_base,
+                                 cnt + static_cast<size_t>(gl) * kCells);
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < a.gb * kCells; i += NT) {
+      const int g2 = i / kCells, c = i - g2 * kCells;
+      float sg = 0.f, sh = 0.f;
+      for (int s = 0; s < a.wpg; ++s) {  // warps of the group in a fixed order
+        const float2 v = gh[static_cast<size_t>(s * a.gb + g2) * kCells + c];
+        sg += v.x;
+        sh += v.y;
+      }
+      const size_t o = (static_cast<size_t>(item) * a.gb + g2) * kCells + c;
+      a.part_g[o] = sg;
+      a.part_h[o] = sh;
+      a.part_c[o] = cnt[static_cast<size_t>(g2) * kCells + c];
+    }
+    __syncthreads();
+  }
+}
+
+template <int BITS, int K>
+__global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) {
+  constexpr int NT = grow_threads<K>();
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ Cand wb[NT / 32];
+  __shared__ PartShared<NT> ps;
+  __shared__ Desc D;
+  __shared__ Kid kid[2];
+  // root: histogram, totals and best split were computed by the host-launched
+  // kernels; every CTA builds the root record and picks split 0
+  if (threadIdx.x == 0) {
+    const double G = __ldcg(a.root_tot), H = __ldcg(a.root_tot + 1);
+    kid[0] = Kid{0, a.root_count, G, H, load_split(&a.nodes[0].best), 0, 0};
+    kid[0].has_best = kid[0].best.feature >= 0 ? 1 : 0;
+    if (blockIdx.x == 0) {
+      a.tree[0] = hbg_tree_node{-1, -1, -1, -1, leaf_value(G, H, a.lambda)};
+      a.nodes[0] = NodeDev{0, a.root_count, G, H, kid[0].best, 0, kid[0].has_best};
+      a.node_gain[0] = kid[0].has_best ? kid[0].best.gain : -1.0;
+    }
+  }
+  __syncthreads();
+  pick<NT>(a, 0, 0, kid, D);  // node 0 is "kid_l" (kid[1] is never consulted: nnodes = 1)
+  const double eg = ldexp(1.0, a.exps[0]), eh = ldexp(1.0, a.exps[1]);  // fixed-point scales
+  while (!D.done) {
+    const int it = D.iter;
+    stamp(a, it, 0);
+    const bool small_parent = D.count <= static_cast<int64_t>(kItems) * NT;
+    if (a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0)  // class of this split
+      a.prof[static_cast<size_t>(it) * kProfSlots + 7] = (small_parent ? 0 : 4) + D.path;
+    const bool chunk_cta = static_cast<int>(blockIdx.x) < a.nchunks;
+    const int f0 = blockIdx.x * a.fchunk;
+    const int nf = chunk_cta ? min(a.fchunk, a.d - f0) : 0;
+    if (small_parent) {
+      // the scan CTAs (one feature chunk each) rank the whole parent and share
+      // the scatter; the others only wait at the barrier
+      if (chunk_cta) {
+        RegRows rr;
+        if (D.path == kDirect) zero_direct(a, smem, nf * a.k, NT);
+        partition_redundant<NT>(a, D, rr, ps, a.nchunks);
+        set_children(a, D, kid);
+        stamp(a, it, 1);
+        if (D.path == kDirect) {
+          // the smaller child's rows are in registers already: accumulate this
+          // CTA's feature chunk, then finish and scan it
+          const uint32_t valid = rr.nvalid >= 32 ? ~0u : ((1u << rr.nvalid) - 1u);
+          const uint32_t want = (D.small_is_left ? rr.left : ~rr.left) & valid;
+          direct_accumulate(a, direct_acc(a, smem), nf * a.k, f0, nf, rr.row, rr.g, rr.h, want, eg, eh);
+          __syncthreads();
+          stamp(a, it, 2);
+          finish_chunk<K, NT>(a, D, blockIdx.x, smem, wb);
+        }
+        // (kSmem cannot occur: the smaller child of a small parent is <= kDirectRows)
+      } else {
+        if (threadIdx.x == 0) D.tot[0] = D.tot[1] = D.tot[2] = D.tot[3] = 0.0;  // not used here
+        __syncthreads();
+        set_children(a, D, kid);
+      }
+      stamp(a, it, 3);
+      grid_sync(a);
+    } else {
+      partition_count<NT>(a, D, ps);
+      grid_sync(a);
+      partition_scatter<NT>(a, D, ps);
+      set_children(a, D, kid);
+      stamp(a, it, 1);
+      grid_sync(a);
+      if (D.path == kDirect) {
+        if (chunk_cta) {
+          zero_direct(a, smem, nf * a.k, NT);
+          __syncthreads();
+          const int32_t* rows;
+          const float* g;
+          const float* h;
+          int64_t n;
+          small_child(a, D, rows, g, h, n);
+          for (int64_t j0 = 0; j0 < n; j0 += static_cast<int64_t>(NT) * kItems) {
+            int32_t r[kItems];
+            float gg[kItems], hh[kItems];
+            uint32_t mask = 0;
+#pragma unroll
+            for (int u = 0; u < kItems; ++u) {
+              const int64_t j = j0 + static_cast<int64_t>(u) * NT + threadIdx.x;
+              const bool ok = j < n;
+              r[u] = ok ? __ldcg(rows + j) : 0;
+              gg[u] = ok ? __ldcg(g + j) : 0.f;
+              hh[u] = ok ? __ldcg(h + j) : 0.f;
+              mask |= ok ? 1u << u : 0u;
+            }
+            direct_accumulate(a, direct_acc(a, smem), nf * a.k, f0, nf, r, gg, hh, mask, eg, eh);
+          }
+          __syncthreads();
+          stamp(a, it, 2);
+          finish_chunk<K, NT>(a, D, blockIdx.x, smem, wb);
+        }
+        stamp(a, it, 3);
+        grid_sync(a);
+      } else if (D.path == kSmem) {
+        hist_smem<BITS, K, NT>(a, D, smem);
+        stamp(a, it, 2);
+        grid_sync(a);
+        for (int c = blockIdx.x; c < a.nchunks; c += gridDim.x) finish_chunk<K, NT>(a, D, c, smem, wb);
+        stamp(a, it, 3);
+        grid_sync(a);
+      }
+    }
+    stamp(a, it, 4);
+    if (D.path != kNoHist) winners<NT>(a, D, kid);
+    stamp(a, it, 8);
+    store_children(a, D, kid);
+    stamp(a, it, 6);
+    pick<NT>(a, it + 1, D.left_id, kid, D);
+    stamp(a, it, 5);
+  }
+}
+
+// scores[row] += lr * value for every leaf node (tree[i].left < 0) of a grown
+// tree (boosting.cpp:48-50); every leaf owns a contiguous ordered-buffer range.
+__global__ void score_update_nodes_kernel(const NodeDev* __restrict__ nodes,
+                                          const hbg_tree_node* __restrict__ tree,
+                                          const int32_t* __restrict__ rows0, const int32_t* __restrict__ rows1,
+                                          double lr, double* __restrict__ scores) {
+  const int i = blockIdx.y;
+  if (tree[i].left >= 0) return;
+  const NodeDev L = nodes[i];
+  const int32_t* rows = L.buf == 0 ? rows0 : rows1;
+  const double add = lr * tree[i].value;
+  for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < L.count;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    scores[rows[L.begin + j]] += add;
+}
+
+template <int BITS, int K>
+struct GrowKernel {
+  static void* fn() { return reinterpret_cast<void*>(grow_kernel<BITS, K>); }
+};
+
+void* grow_fn(int bits, int k_alloc) {
+  if (bits == 4) return GrowKernel<4, 16>::fn();
+  if (k_alloc == 64) return GrowKernel<8, 64>::fn();
+  if (k_alloc == 128) return GrowKernel<8, 128>::fn();
+  return GrowKernel<8, 256>::fn();
+}
+
+int grow_nt(int k_alloc) { return k_alloc >= 256 ? grow_threads<256>() : grow_threads<64>(); }
+
+constexpr size_t kSmemMax = 232448;  // static + dynamic shared memory per CTA
+
+size_t grow_static_smem(void* fn) {
+  cudaFuncAttributes attr{};
+  HBG_CUDA(cudaFuncGetAttributes(&attr, fn));
+  return attr.sharedSizeBytes;
+}
+
+struct GrowGeom {
+  int k_alloc, nt, gb, wpg, nblocks, fchunk, nchunks, ctas;
+  size_t smem, part_values;
+};
+
+GrowGeom grow_geometry(const PersistentGrowArgs& h, int device) {
+  GrowGeom g{};
+  g.k_alloc = h.bits == 4 ? 16 : (h.k <= 64 ? 64 : (h.k <= 128 ? 128 : 256));
+  g.nt = grow_nt(g.k_alloc);
+  const size_t cells = static_cast<size_t>(g.k_alloc) * 32;
+  const size_t ghw = cells * 8, cntw = cells * 4;
+  const size_t smem_max = kSmemMax - grow_static_smem(grow_fn(h.bits, g.k_alloc));
+  const int max_warps = g.nt / 32;
+  int gb = 0, warps = 0;
+  for (int cand = 1; cand <= std::min(h.num_groups, max_warps); ++cand) {
+    if (cand * cntw >= smem_max) break;
+    const int wpg = static_cast<int>(std::min<size_t>(max_warps, (smem_max - cand * cntw) / ghw)) / cand;
+    if (wpg < 1) break;
+    if (cand * wpg >= warps) {
+      gb = cand;
+      warps = cand * wpg;
+    }
+  }
+  require(gb >= 1, "histogram footprint exceeds shared memory");
+  g.gb = gb;
+  g.wpg = warps / gb;
+  g.nblocks = (h.num_groups + gb - 1) / gb;
+  g.ctas = sm_count(device);
+  // scan chunks: >= ceil(d / CTAs) features, <= 2048 staged cells
+  const int max_f = std::max(1, 2048 / h.k);  // staged cells per chunk
+  g.fchunk = std::max(1, std::min(max_f, (h.d + g.ctas - 1) / g.ctas));
+  g.nchunks = std::max(1, (h.d + g.fchunk - 1) / g.fchunk);
+  const size_t hist_smem = static_cast<size_t>(g.gb * g.wpg) * ghw + g.gb * cntw;
+  // finish: fp64 staging of both children + the direct fixed-point accumulator
+  const size_t scan_smem = static_cast<size_t>(g.fchunk) * h.k * (6 * sizeof(double) + 20);
+  g.smem = std::max(hist_smem, scan_smem);
+  require(g.ctas <= g.nt, "more CTAs than threads per CTA (per-CTA records are scanned one per thread)");
+  require(g.smem <= smem_max, "tree grower shared memory footprint too large");
+  const size_t items = static_cast<size_t>(std::max(g.ctas, g.nblocks));
+  g.part_values = items * g.gb * cells;
+  return g;
+}
+
+}  // namespace
+
+size_t grow_nodes_bytes(int num_leaves) {
+  return static_cast<size_t>(std::max(1, 2 * num_leaves - 1)) * sizeof(NodeDev);
+}
+
+size_t grow_root_split_offset() { return offsetof(NodeDev, best); }
+
+size_t grow_scratch_bytes(const PersistentGrowArgs& h, int device) {
+  const GrowGeom g = grow_geometry(h, device);
+  const size_t max_nodes = static_cast<size_t>(std::max(1, 2 * h.num_leaves - 1));
+  size_t b = 0;
+  auto add = [&](size_t n) { b += (n + 255) / 256 * 256; };
+  add(sizeof(unsigned));                      // barrier
+  add(max_nodes * sizeof(double));            // node_gain
+  add(max_nodes * sizeof(int));               // picked
+  add(static_cast<size_t>(h.num_rows) + 16);  // flags
+  add(static_cast<size_t>(g.ctas) * 8);       // cta_left
+  add(static_cast<size_t>(g.ctas) * 32);      // cta_sums
+  add(g.part_values * 4 * 3);                 // part_g/h/c
+  add(static_cast<size_t>(2 * g.nchunks) * sizeof(Cand));
+  return b;
+}
+
+void configure_grow_kernels() {
+  for (int v = 0; v < 4; ++v) {
+    const int bits = v == 0 ? 4 : 8, k = v == 0 ? 16 : (v == 1 ? 64 : (v == 2 ? 128 : 256));
+    void* fn = grow_fn(bits, k);
+    HBG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kSmemMax - grow_static_smem(fn))));
+    set_max_shared_carveout(fn);
+  }
+}
+
+void launch_score_update_nodes(const void* nodes, const hbg_tree_node* tree, int num_nodes,
+                               const int32_t* rows0, const int32_t* rows1, double lr, double* scores,
+                               cudaStream_t s) {
+  if (num_nodes <= 0) return;
+  score_update_nodes_kernel<<<dim3(16, num_nodes), 256, 0, s>>>(static_cast<const NodeDev*>(nodes), tree, rows0,
+                                                                rows1, lr, scores);
+  HBG_LAUNCH_CHECK();
+}
+
+void launch_grow_persistent(const PersistentGrowArgs& h, int device, cudaStream_t s) {
+  const GrowGeom g = grow_geometry(h, device);
+  GrowArgs a{};
+  a.packed = h.packed;
+  a.colbins = h.colbins;
+  a.nrows = h.num_rows;
+  a.row_stride = h.row_stride;
+  a.words_per_row = h.words_per_row;
+  a.bits = h.bits;
+  a.d = h.d;
+  a.k = h.k;
+  a.num_groups = h.num_groups;
+  for (int b = 0; b < 2; ++b) {
+    a.rows[b] = h.rows[b];
+    a.g[b] = h.g[b];
+    a.h[b] = h.h[b];
+  }
+  a.slots = h.slots;
+  a.nodes = static_cast<NodeDev*>(h.nodes);
+  a.split_log = h.split_log;
+  a.tree = h.tree;
+  a.counts = h.counts;
+  a.exps = h.exps;
+  a.root_tot = h.root_totals;
+  a.root_count = h.num_rows;
+  a.num_leaves = h.num_leaves;
+  a.min_data = h.min_data;
+  a.lambda = h.lambda;
+  a.gb = g.gb;
+  a.wpg = g.wpg;
+  a.nblocks = g.nblocks;
+  a.rpl = g.k_alloc >= 256 ? rows_per_lane<256>() : rows_per_lane<64>();
+  a.fchunk = g.fchunk;
+  a.nchunks = g.nchunks;
+  a.timeout_cycles = 4000000000LL;
+  a.prof = h.prof;  // ~2 s: a hung barrier becomes an error, not a hang
+  unsigned char* p = static_cast<unsigned char*>(h.scratch);
+  auto take = [&](size_t n) {
+    unsigned char* q = p;
+    p += (n + 255) / 256 * 256;
+    return q;
+  };
+  const size_t max_nodes = static_cast<size_t>(std::max(1, 2 * h.num_leaves - 1));
+  a.bar = reinterpret_cast<unsigned*>(take(sizeof(unsigned)));
+  a.node_gain = reinterpret_cast<double*>(take(max_nodes * sizeof(double)));
+  a.picked = reinterpret_cast<int*>(take(max_nodes * sizeof(int)));
+  a.flags = take(static_cast<size_t>(h.num_rows) + 16);
+  a.cta_left = reinterpret_cast<int64_t*>(take(static_cast<size_t>(g.ctas) * 8));
+  a.cta_sums = reinterpret_cast<double*>(take(static_cast<size_t>(g.ctas) * 32));
+  float* part = reinterpret_cast<float*>(take(g.part_values * 12));
+  a.part_g = part;
+  a.part_h = part + g.part_values;
+  a.part_c = reinterpret_cast<uint32_t*>(part + 2 * g.part_values);
+  a.cand = reinterpret_cast<Cand*>(take(static_cast<size_t>(2 * g.nchunks) * sizeof(Cand)));
+  require(static_cast<size_t>(p - static_cast<unsigned char*>(h.scratch)) <= grow_scratch_bytes(h, device),
+          "grow scratch layout");
+  HBG_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned), s));
+  HBG_CUDA(cudaMemsetAsync(a.picked, 0, max_nodes * sizeof(int), s));
+  HBG_CUDA(cudaMemsetAsync(a.counts, 0, 4 * sizeof(int), s));
+  void* fn = grow_fn(h.bits, g.k_alloc);
+  int occ = 0;
+  HBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, g.nt, g.smem));
+  require(occ >= 1, "tree grower kernel cannot be resident");
+  void* args[] = {&a};
+  HBG_CUDA(cudaLaunchCooperativeKernel(fn, dim3(g.ctas), dim3(g.nt), args, g.smem, s));
+}
+
+}  // namespace hbg

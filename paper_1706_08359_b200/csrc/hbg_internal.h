@@ -160,6 +160,41 @@ void launch_small_hist_atomic(const int32_t* rows, const float* g, const float* 
                               const uint32_t* packed, int stride_words, int words_per_row, int bits, int d,
                               int k, const int* exps, void* acc, cudaStream_t s);
 
+// Persistent tree grower (grow_persistent.cu): all splits of one tree in a
+// single cooperative kernel, one CTA per SM.
+struct PersistentGrowArgs {
+  const uint8_t* packed;
+  const uint8_t* colbins;  // [d][num_rows] uint8 bins
+  int64_t row_stride;
+  int words_per_row, bits, d, k, num_groups;
+  int64_t num_rows;
+  int32_t* rows[2];
+  float* g[2];
+  float* h[2];
+  double* slots;         // (2*num_leaves-1) node slots of 3*d*k doubles
+  void* nodes;           // grow_nodes_bytes(num_leaves), nodes[0].best = root split
+  hbg_split* split_log;  // device, num_leaves-1
+  hbg_tree_node* tree;   // device, 2*num_leaves-1
+  int* counts;           // device, 4 ints: num_splits, num_nodes, error
+  void* scratch;         // grow_scratch_bytes()
+  unsigned long long* acc;
+  const int* exps;
+  const double* root_totals;  // device {G, H}
+  int num_leaves;
+  int64_t min_data;
+  double lambda;
+  unsigned long long* prof;  // optional phase stamps (HBG_GROW_PROFILE)
+};
+size_t grow_nodes_bytes(int num_leaves);
+size_t grow_root_split_offset();
+size_t grow_scratch_bytes(const PersistentGrowArgs& a, int device);
+void configure_grow_kernels();
+void launch_grow_persistent(const PersistentGrowArgs& a, int device, cudaStream_t s);
+// scores[row] += lr * value for the rows of every leaf node of a persistent-grown tree
+void launch_score_update_nodes(const void* nodes, const hbg_tree_node* tree, int num_nodes,
+                               const int32_t* rows0, const int32_t* rows1, double lr, double* scores,
+                               cudaStream_t s);
+
 int sm_count(int device);
 
 // Runs f, mapping exceptions to HBG_* status codes + the thread-local last error.

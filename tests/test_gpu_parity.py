@@ -441,10 +441,12 @@ def _assert_same_tree(log, nodes, want_log, want_nodes, cols=None, g=None, h=Non
     return i
 
 
-def test_grow_tree_matches_reference_golden_split_log(hbg, oracle):
+@pytest.mark.parametrize("grower", ["persistent", "host"])
+def test_grow_tree_matches_reference_golden_split_log(hbg, oracle, grower, monkeypatch):
     """grow_tree split_log of the unmodified reference (bits64), committed golden."""
     import os
 
+    monkeypatch.setenv("HBG_GROW", grower)
     z = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_histograms.npz"))
     cols = oracle.gen_synthetic_bins(4000, 6, 16, 3)
     g, h = oracle.gen_grad_hess(4000, 3)
@@ -465,13 +467,16 @@ def test_grow_tree_matches_reference_golden_split_log(hbg, oracle):
     (30000, 28, 64, 63, 50, 0.0, True), (20000, 10, 256, 31, 100, 1.0, True),
     (50000, 40, 16, 127, 100, 0.0, True), (300000, 28, 64, 255, 200, 0.0, True),
     (30000, 28, 64, 63, 1, 0.0, False), (3000, 3, 64, 255, 1, 0.0, False)])
-def test_grow_tree_matches_oracle(hbg, oracle, rows, d, k, leaves, min_data, lam, exact):
-    """Non-tied inputs (min_data large enough that no near-ties arise): the
+@pytest.mark.parametrize("grower", ["persistent", "host"])
+def test_grow_tree_matches_oracle(hbg, oracle, rows, d, k, leaves, min_data, lam, exact, grower, monkeypatch):
+    """Both growers (the persistent one-kernel tree and the host loop,
+    HBG_GROW=host). Non-tied inputs (min_data large enough that no near-ties arise): the
     identical tree. Tiny leaves: identical up to the first near-tie, which must
     be a tie in fp64 to 1e-6 (see _assert_same_tree)."""
     cols = oracle.gen_synthetic_bins(rows, d, k, d)
     g, h = oracle.gen_grad_hess(rows, d)
     g = g + 0.3 * (cols[d // 2].astype(np.float64) > k // 2)  # some structure
+    monkeypatch.setenv("HBG_GROW", grower)
     with hbg.Dataset(cols, k) as ds:
         log, nodes = _grow(hbg, ds, g, h, leaves, min_data, lam)
     want_log, want_nodes = oracle.grow_tree(cols, k, g, h, leaves, min_data, lam, 64)
@@ -480,7 +485,9 @@ def test_grow_tree_matches_oracle(hbg, oracle, rows, d, k, leaves, min_data, lam
         assert same == len(want_log)
 
 
-def test_grow_tree_edge_cases(hbg, oracle):
+@pytest.mark.parametrize("grower", ["persistent", "host"])
+def test_grow_tree_edge_cases(hbg, oracle, grower, monkeypatch):
+    monkeypatch.setenv("HBG_GROW", grower)
     cols = oracle.gen_synthetic_bins(500, 4, 64, 1)
     g, h = oracle.gen_grad_hess(500, 1)
     with hbg.Dataset(cols, 64) as ds:
@@ -498,11 +505,14 @@ def test_grow_tree_edge_cases(hbg, oracle):
 # ------------------------------------------------ boosting iteration (§8f rank 3)
 @pytest.mark.parametrize("loss,rows,d,k,leaves,min_data,lam", [(0, 50000, 28, 64, 31, 100, 0.0),
                                                               (1, 40000, 20, 16, 63, 100, 1.0)])
-def test_boosting_iterations_match_reference(hbg, oracle, loss, rows, d, k, leaves, min_data, lam):
+@pytest.mark.parametrize("grower", ["persistent", "host"])
+def test_boosting_iterations_match_reference(hbg, oracle, loss, rows, d, k, leaves, min_data, lam, grower,
+                                             monkeypatch):
     """Three boost_one_iteration (boosting.cpp:26-51) steps on the device vs the
     oracle's restatement (itself pinned bit-for-bit against the reference's
     boost_one_iteration in test_oracle.py): identical trees, scores within 1e-6."""
     torch = torch_cuda()
+    monkeypatch.setenv("HBG_GROW", grower)
     cols = oracle.gen_synthetic_bins(rows, d, k, 9)
     rng = np.random.default_rng(9)
     signal = (cols[0].astype(np.float64) - k / 2) / k + 0.5 * (cols[3] > k // 3)
