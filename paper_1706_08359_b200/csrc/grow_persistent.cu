@@ -854,6 +854,7 @@ __device__ void finish_chunk(const GrowArgs& a, const Desc& D, int c_idx, unsign
 template <int NT>
 __device__ void winners(const GrowArgs& a, const Desc& D, Kid* kid) {
   if (threadIdx.x < 32) {
+    const long long c0 = clock64();
     const int lane = threadIdx.x, child = lane >> 4, sub = lane & 15;
     const bool want = child == 0 ? D.lsplit : D.rsplit;
     Cand c{0.0, -1, -1, 0.0, 0.0, 0};
@@ -870,10 +871,16 @@ __device__ void winners(const GrowArgs& a, const Desc& D, Kid* kid) {
         if (better(o, c)) c = o;
       }
     }
+    const long long c1 = clock64();
 #pragma unroll
     for (int off = 8; off > 0; off >>= 1) {  // within each half-warp
       const Cand o = shfl_cand(c, lane ^ off);
       if (better(o, c)) c = o;
+    }
+    const long long c2 = clock64();
+    if (a.prof != nullptr && blockIdx.x == 0 && lane == 0) {
+      a.prof[static_cast<size_t>(D.iter) * kProfSlots + 9] = c1 - c0;
+      a.prof[static_cast<size_t>(D.iter) * kProfSlots + 10] = c2 - c1;
     }
     if (sub == 0 && want) {
       const double gt = D.tot[2 * child], ht = D.tot[2 * child + 1];
@@ -881,6 +888,8 @@ __device__ void winners(const GrowArgs& a, const Desc& D, Kid* kid) {
       write_split(c, gt, ht, count, a.lambda, &kid[child].best);
       kid[child].has_best = c.f >= 0 ? 1 : 0;
     }
+    const long long c3 = clock64();
+    if (a.prof != nullptr && blockIdx.x == 0 && lane == 0) a.prof[static_cast<size_t>(D.iter) * kProfSlots + 11] = c3 - c2;
   }
   __syncthreads();
 }
