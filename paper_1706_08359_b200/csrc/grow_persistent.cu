@@ -31,6 +31,7 @@
 // the packed dataset uses the read-only path.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "hbg_internal.h"
@@ -1302,7 +1303,8 @@ void launch_grow_persistent(const PersistentGrowArgs& h, int device, cudaStream_
   a.fchunk = g.fchunk;
   a.nchunks = g.nchunks;
   a.timeout_cycles = 4000000000LL;
-  a.prof = h.prof;  // ~2 s: a hung barrier becomes an error, not a hang
+  a.prof = h.prof;
+  a.spin_ns = std::getenv("HBG_SPIN_NS") ? static_cast<unsigned>(std::atoi(std::getenv("HBG_SPIN_NS"))) : 0u;  // ~2 s: a hung barrier becomes an error, not a hang
   unsigned char* p = static_cast<unsigned char*>(h.scratch);
   auto take = [&](size_t n) {
     unsigned char* q = p;

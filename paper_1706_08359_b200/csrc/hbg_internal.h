@@ -126,7 +126,7 @@ void launch_reduce_parts(const std::vector<const double*>& parts, int64_t n, dou
                          cudaStream_t s);
 
 void set_max_shared_carveout(const void* func);
-void configure_hist_kernels();
+void configure_hist_kernels(int device);
 void configure_leaf_kernels();
 void configure_tree_kernels();
 void configure_kernels(int device);  // carveout for every non-histogram kernel, once per device

@@ -346,7 +346,13 @@ int occupancy_for(int bits, int k_alloc, int threads, size_t smem, int device) {
 
 }  // namespace
 
-void configure_hist_kernels() {
+void configure_hist_kernels(int device) {
+  // every shared-memory histogram variant may be launched without a prior
+  // occupancy query (direct small-leaf plans): set their limits up front
+  set_smem_attr<4, 16>(device);
+  set_smem_attr<8, 64>(device);
+  set_smem_attr<8, 128>(device);
+  set_smem_attr<8, 256>(device);
   set_max_shared_carveout(reinterpret_cast<const void*>(reduce_partials_kernel));
   set_max_shared_carveout(reinterpret_cast<const void*>(pack_kernel));
   set_max_shared_carveout(reinterpret_cast<const void*>(f64_to_f32_kernel));
@@ -354,8 +360,8 @@ void configure_hist_kernels() {
 
 void configure_kernels(int device) {
   static std::once_flag once[64];
-  std::call_once(once[device & 63], [] {
-    configure_hist_kernels();
+  std::call_once(once[device & 63], [device] {
+    configure_hist_kernels(device);
     configure_leaf_kernels();
     configure_tree_kernels();
     configure_grow_kernels();
