@@ -1302,9 +1302,8 @@ void launch_grow_persistent(const PersistentGrowArgs& h, int device, cudaStream_
   a.rpl = g.k_alloc >= 256 ? rows_per_lane<256>() : rows_per_lane<64>();
   a.fchunk = g.fchunk;
   a.nchunks = g.nchunks;
-  a.timeout_cycles = 4000000000LL;
+  a.timeout_cycles = 4000000000LL;  // ~2 s: a hung barrier becomes an error, not a hang
   a.prof = h.prof;
-  a.spin_ns = std::getenv("HBG_SPIN_NS") ? static_cast<unsigned>(std::atoi(std::getenv("HBG_SPIN_NS"))) : 0u;  // ~2 s: a hung barrier becomes an error, not a hang
   unsigned char* p = static_cast<unsigned char*>(h.scratch);
   auto take = [&](size_t n) {
     unsigned char* q = p;
