@@ -97,11 +97,14 @@ def test_two_rank_sharded_tree_equals_reference(hbg, oracle, rows, d, k, leaves,
     assert coll.calls >= len(log0) + 2  # root totals + root histogram + per-split child totals (+ histograms)
 
 
-def test_nccl_comm_single_rank_tree(hbg, oracle):
+def test_nccl_comm_single_rank_tree(hbg, oracle, monkeypatch):
     """The NCCL hook itself (hbg_comm_*, dlopen'ed libnccl) on one rank: the
-    sharded grower over a 1-rank communicator equals the unsharded grower."""
+    sharded grower over a 1-rank communicator equals the unsharded host-loop
+    grower bit for bit (same kernels, same order), and the persistent grower
+    in structure (its fp64 totals are summed in a different fixed order)."""
     import torch
 
+    monkeypatch.setenv("HBG_GROW", "host")
     cols = oracle.gen_synthetic_bins(30000, 16, 64, 8)
     g, h = oracle.gen_grad_hess(30000, 8)
     comm = hbg.Comm(1, 0, hbg.Comm.unique_id(), 0)
@@ -119,8 +122,16 @@ def test_nccl_comm_single_rank_tree(hbg, oracle):
             ds.boost_one_iteration(ts, s1, hbg.HBG_LOSS_SQUARED, 0.1, 31, 20, 0.0, comm.allreduce_fn, comm.handle,
                                    s.cuda_stream)
             ds.boost_one_iteration(ts, s2, hbg.HBG_LOSS_SQUARED, 0.1, 31, 20, 0.0, stream=s.cuda_stream)
+            monkeypatch.setenv("HBG_GROW", "persistent")
+            c = ds.grow_tree(tg, th, 63, 20, 0.0, s.cuda_stream)
             torch.cuda.synchronize()
     finally:
         comm.close()
     assert a[0].tobytes() == b[0].tobytes() and a[1].tobytes() == b[1].tobytes()
     assert torch.equal(s1, s2)
+    for key in ("feature", "threshold_bin", "left_count", "right_count"):
+        assert (c[0][key] == a[0][key]).all(), key
+    for key in ("feature", "threshold_bin", "left", "right"):
+        assert (c[1][key] == a[1][key]).all(), key
+    assert np.allclose(c[1]["value"], a[1]["value"], rtol=1e-9, atol=1e-12)
+    assert np.allclose(c[0]["gain"], a[0]["gain"], rtol=1e-5)  # histograms: fp32 vs fixed-point rounding
