@@ -568,11 +568,11 @@ void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_h
     HBG_CUDA(cudaMemcpy(prof.data(), a.prof, prof.size() * 8, cudaMemcpyDeviceToHost));
     // stamps: 0 start, 1 partitioned, 2 small-child histogram, 3 finish+scans, 4 barrier, 5 picked;
     // slot 7: class = (large parent ? 4 : 0) + path (0 none, 1 direct, 2 shared-memory histogram)
-    static const char* nm[8] = {"partition", "child hist", "finish+scans", "barrier", "winners+pick", "loop",
-                                "(winners)", "(w: loads)"};
+    static const char* nm[7] = {"partition", "child hist", "finish+scans", "barrier", "winners+pick", "loop",
+                                "(winners)"};
     for (int cls = 0; cls < 8; ++cls) {
-      double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      int n[8] = {0, 0, 0, 0, 0, 0, 0, 0}, splits = 0;
+      double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+      int n[7] = {0, 0, 0, 0, 0, 0, 0}, splits = 0;
       for (int i = 0; i < counts[0]; ++i) {
         const unsigned long long* t = prof.data() + static_cast<size_t>(i) * 12;
         if (static_cast<int>(t[7]) != cls) continue;
@@ -581,17 +581,10 @@ void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_h
           if (t[j] && t[j + 1]) acc[j] += (t[j + 1] - t[j]) * 1e-3, ++n[j];
         if (i + 1 < counts[0] && t[5] && t[12]) acc[5] += (t[12] - t[5]) * 1e-3, ++n[5];
         if (t[4] && t[8]) acc[6] += (t[8] - t[4]) * 1e-3, ++n[6];
-        if (t[9]) acc[7] += t[9] / 1965.0, ++n[7];
       }
       if (splits == 0) continue;
-      double c10 = 0, c11 = 0;
-      for (int i = 0; i < counts[0]; ++i) {
-        const unsigned long long* t = prof.data() + static_cast<size_t>(i) * 12;
-        if (static_cast<int>(t[7]) == cls) c10 += t[10], c11 += t[11];
-      }
-      std::fprintf(stderr, "   (w: shuffles %.0f cyc, write_split %.0f cyc avg)\n", c10 / splits, c11 / splits);
       std::fprintf(stderr, "grow class %s parent, path %d: %d splits\n", cls >= 4 ? "large" : "small", cls & 3, splits);
-      for (int j = 0; j < 8; ++j)
+      for (int j = 0; j < 7; ++j)
         if (n[j]) std::fprintf(stderr, "   %-13s total %9.1f us avg %7.2f us\n", nm[j], acc[j], acc[j] / n[j]);
     }
   }

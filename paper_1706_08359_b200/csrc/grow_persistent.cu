@@ -299,6 +299,27 @@ __device__ __forceinline__ Cand warp_best(Cand c) {
   return c;
 }
 
+// Branch-free warp argmax on a 96-bit key (hi, lo), max wins; every lane
+// ends with the winning key. For a candidate split: hi = the bits of its gain
+// (a positive double orders like its bit pattern; no candidate = 0), lo =
+// ~((f << 12) | b) so the lowest feature, then the lowest bin wins ties —
+// the reference's strict `>` scans (tree.cpp:95,172).
+__device__ __forceinline__ void warp_argmax_key(unsigned long long& hi, unsigned& lo, int width = 32) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    if (off >= width) continue;
+    const unsigned long long oh = __shfl_xor_sync(0xffffffffu, hi, off);
+    const unsigned ol = __shfl_xor_sync(0xffffffffu, lo, off);
+    const bool take = oh > hi || (oh == hi && ol > lo);
+    hi = take ? oh : hi;
+    lo = take ? ol : lo;
+  }
+}
+
+__device__ __forceinline__ unsigned long long gain_key(double gain) {
+  return gain > 0.0 ? static_cast<unsigned long long>(__double_as_longlong(gain)) : 0ull;
+}
+
 // ---------------------------------------------------------------------- pick
 
 // Children of the split just executed, as every CTA computed them.
@@ -320,21 +341,22 @@ __device__ void pick(const GrowArgs& a, int i, int kid_l, const Kid* kid, Desc& 
     const int nnodes = 1 + 2 * i;
     int err = lane == 0 ? error_of(a) : 0;
     err = __shfl_sync(0xffffffffu, err, 0);
-    Cand c{0.0, -1, 0, 0.0, 0.0, 0};
+    unsigned long long hk = 0ull;
+    unsigned lk = 0u;
     if (i < a.num_leaves - 1 && err == kErrNone) {
-      for (int n0 = 0; n0 < nnodes; n0 += 4 * 32) {
-        double gain[4];
-        int pk[4];
+      constexpr int kU = 16;  // 16 x 32 lanes >= 509 nodes: one round of loads
+      for (int n0 = 0; n0 < nnodes; n0 += kU * 32) {
+        double gain[kU];
+        int pk[kU];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {  // loads first, then the compares
+        for (int u = 0; u < kU; ++u) {  // loads first, then the compares
           const int n = n0 + u * 32 + lane;
           gain[u] = n < nnodes ? __ldcg(a.node_gain + n) : -1.0;
           pk[u] = n < nnodes ? __ldcg(a.picked + n) : 1;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kU; ++u) {
           const int n = n0 + u * 32 + lane;
-          if (n >= nnodes) continue;
           double g = gain[u];
           if (kid_l >= 0 && (n == kid_l || n == kid_l + 1)) {
             const Kid& q = kid[n - kid_l];
@@ -342,15 +364,16 @@ __device__ void pick(const GrowArgs& a, int i, int kid_l, const Kid* kid, Desc& 
           } else if (pk[u] != 0 && pk[u] != i + 1) {
             g = -1.0;  // split earlier (i+1: CTA 0 already recorded this very pick)
           }
-          if (g > 0.0) {
-            const Cand o{g, n, 0, 0.0, 0.0, 0};
-            if (better(o, c)) c = o;  // max gain, lowest node id on ties
-          }
+          const unsigned long long h = n < nnodes ? gain_key(g) : 0ull;
+          const unsigned l = 0xFFFFFFFFu - static_cast<unsigned>(n);  // lowest node id wins ties
+          const bool take = h > hk || (h == hk && l > lk);
+          hk = take ? h : hk;
+          lk = take ? l : lk;
         }
       }
     }
-    c = warp_best(c);
-    const int p = c.f;
+    warp_argmax_key(hk, lk);
+    const int p = hk == 0ull ? -1 : static_cast<int>(0xFFFFFFFFu - lk);
     if (lane == 0) {
       if (p < 0) {
         D.done = 1;
@@ -855,33 +878,46 @@ __device__ void finish_chunk(const GrowArgs& a, const Desc& D, int c_idx, unsign
 template <int NT>
 __device__ void winners(const GrowArgs& a, const Desc& D, Kid* kid) {
   if (threadIdx.x < 32) {
-    const long long c0 = clock64();
     const int lane = threadIdx.x, child = lane >> 4, sub = lane & 15;
     const bool want = child == 0 ? D.lsplit : D.rsplit;
     Cand c{0.0, -1, -1, 0.0, 0.0, 0};
+    unsigned long long hk = 0ull;
+    unsigned lk = 0u;
     if (want) {
-      for (int i = sub; i < a.nchunks; i += 16) {
-        const Cand* p = a.cand + child * a.nchunks + i;
-        Cand o;
-        o.gain = __ldcg(&p->gain);
-        o.f = __ldcg(&p->f);
-        o.b = __ldcg(&p->b);
-        o.lg = __ldcg(&p->lg);
-        o.lh = __ldcg(&p->lh);
-        o.lc = __ldcg(&p->lc);
-        if (better(o, c)) c = o;
+      for (int i0 = 0; i0 < a.nchunks; i0 += 4 * 16) {
+        Cand o[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {  // loads first
+          const int i = i0 + u * 16 + sub;
+          const Cand* q = a.cand + child * a.nchunks + (i < a.nchunks ? i : 0);
+          o[u].gain = i < a.nchunks ? __ldcg(&q->gain) : 0.0;
+          o[u].f = __ldcg(&q->f);
+          o[u].b = __ldcg(&q->b);
+          o[u].lg = __ldcg(&q->lg);
+          o[u].lh = __ldcg(&q->lh);
+          o[u].lc = __ldcg(&q->lc);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const unsigned long long h = o[u].f >= 0 ? gain_key(o[u].gain) : 0ull;
+          const unsigned l = 0xFFFFFFFFu - ((static_cast<unsigned>(o[u].f) << 12) | static_cast<unsigned>(o[u].b));
+          const bool take = h > hk || (h == hk && l > lk);
+          hk = take ? h : hk;
+          lk = take ? l : lk;
+          if (take) c = o[u];
+        }
       }
     }
-    const long long c1 = clock64();
-#pragma unroll
-    for (int off = 8; off > 0; off >>= 1) {  // within each half-warp
-      const Cand o = shfl_cand(c, lane ^ off);
-      if (better(o, c)) c = o;
-    }
-    const long long c2 = clock64();
-    if (a.prof != nullptr && blockIdx.x == 0 && lane == 0) {
-      a.prof[static_cast<size_t>(D.iter) * kProfSlots + 9] = c1 - c0;
-      a.prof[static_cast<size_t>(D.iter) * kProfSlots + 10] = c2 - c1;
+    warp_argmax_key(hk, lk, 16);  // within each half-warp (xor offsets < 16)
+    {
+      // the lane holding the winner hands over its left sums
+      const unsigned mine = (hk != 0ull && c.f >= 0 && gain_key(c.gain) == hk &&
+                             0xFFFFFFFFu - ((static_cast<unsigned>(c.f) << 12) | static_cast<unsigned>(c.b)) == lk)
+                                ? 1u : 0u;
+      const unsigned bal = __ballot_sync(0xffffffffu, mine) & (child == 0 ? 0x0000FFFFu : 0xFFFF0000u);
+      const int src = bal ? __ffs(bal) - 1 : lane;
+      const Cand w = shfl_cand(c, src);
+      c = hk == 0ull ? Cand{0.0, -1, -1, 0.0, 0.0, 0} : w;
     }
     if (sub == 0 && want) {
       const double gt = D.tot[2 * child], ht = D.tot[2 * child + 1];
@@ -889,8 +925,6 @@ __device__ void winners(const GrowArgs& a, const Desc& D, Kid* kid) {
       write_split(c, gt, ht, count, a.lambda, &kid[child].best);
       kid[child].has_best = c.f >= 0 ? 1 : 0;
     }
-    const long long c3 = clock64();
-    if (a.prof != nullptr && blockIdx.x == 0 && lane == 0) a.prof[static_cast<size_t>(D.iter) * kProfSlots + 11] = c3 - c2;
   }
   __syncthreads();
 }
