@@ -858,16 +858,37 @@ __device__ void finish_chunk(const GrowArgs& a, const Desc& D, int c_idx, unsign
     double* base = st + child * 3 * chunk_cells;
     const double gt = D.tot[2 * child], ht = D.tot[2 * child + 1];
     const int64_t count = child == 0 ? D.nl : D.nr;
-    Cand best = scan_staged_t(base, base + chunk_cells, base + 2 * chunk_cells, want ? nf : 0, k, f0, gt, ht,
-                              static_cast<double>(count), static_cast<double>(a.min_data), a.lambda, tid, half);
-    best = warp_best(best);
+    const Cand best = scan_staged_t(base, base + chunk_cells, base + 2 * chunk_cells, want ? nf : 0, k, f0, gt,
+                                    ht, static_cast<double>(count), static_cast<double>(a.min_data), a.lambda, tid,
+                                    half);
+    // argmax on (gain bits, ~(f,b)) keys, then the winner's left sums from
+    // the staged prefix sums
+    unsigned long long hk = best.f >= 0 ? gain_key(best.gain) : 0ull;
+    unsigned lk = best.f >= 0 ? 0xFFFFFFFFu - ((static_cast<unsigned>(best.f) << 12) | static_cast<unsigned>(best.b)) : 0u;
+    warp_argmax_key(hk, lk);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    if (lane == 0) wb[w] = best;
+    __shared__ unsigned long long s_hk[W];
+    __shared__ unsigned s_lk[W];
+    if (lane == 0) {
+      s_hk[w] = hk;
+      s_lk[w] = lk;
+    }
     __syncthreads();
     if (w == 0 || w == W / 2) {
-      Cand c = lane < W / 2 ? wb[w + lane] : Cand{0.0, -1, -1, 0.0, 0.0, 0};
-      c = warp_best(c);
-      if (lane == 0 && want) a.cand[child * a.nchunks + c_idx] = c;
+      hk = lane < W / 2 ? s_hk[w + lane] : 0ull;
+      lk = lane < W / 2 ? s_lk[w + lane] : 0u;
+      warp_argmax_key(hk, lk);
+      if (lane == 0 && want) {
+        Cand c{0.0, -1, -1, 0.0, 0.0, 0};
+        if (hk != 0ull) {
+          const unsigned fb = 0xFFFFFFFFu - lk;
+          const int f = static_cast<int>(fb >> 12), b = static_cast<int>(fb & 0xFFFu);
+          const int t = b * nf + (f - f0);
+          c = Cand{__longlong_as_double(static_cast<long long>(hk)), f, b, base[t], base[chunk_cells + t],
+                   static_cast<int64_t>(base[2 * chunk_cells + t])};
+        }
+        a.cand[child * a.nchunks + c_idx] = c;
+      }
     }
     __syncthreads();
   }
