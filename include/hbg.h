@@ -166,6 +166,15 @@ int hbg_grow_tree(hbg_dataset* ds, const float* d_grad, const float* d_hess,
                   const hbg_grow_params* params, hbg_split* split_log, int32_t* num_splits,
                   hbg_tree_node* nodes, int32_t* num_nodes, void* stream);
 
+/* Host-pointer drop-in for grow_tree (tree.cpp:186-261): fp64 per-row
+ * gradients/hessians in host memory (the reference's std::span<const double>
+ * arguments), uploaded and cast to fp32 on the device (the bits32 per-element
+ * cast, histogram.cpp:97-98), then grown as hbg_grow_tree. split_log: host,
+ * num_leaves-1 entries; nodes: host, 2*num_leaves-1 entries. Synchronous. */
+int hbg_grow_tree_host(hbg_dataset* ds, const double* gradients, const double* hessians,
+                       const hbg_grow_params* params, hbg_split* split_log, int32_t* num_splits,
+                       hbg_tree_node* nodes, int32_t* num_nodes);
+
 /* ---- row-sharded growth ----
  * One process (or thread) per GPU; each rank's dataset and d_grad/d_hess hold
  * its own rows (hbg_dataset_create on columns + row_begin). The hook sums

@@ -17,8 +17,12 @@
 // on the CPU pair path (sparse.cpp), as the paper does.
 #pragma once
 
+#include <algorithm>
+#include <cstdint>
 #include <cstring>
+#include <limits>
 #include <memory>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -91,6 +95,65 @@ inline histoboost::HistogramSet build_histograms_cuda(const DeviceDataset& dev,
                 sizeof(hbg_bin) * static_cast<std::size_t>(k));
   }
   return out;
+}
+
+// The whole-tree drop-in for grow_tree (tree.hpp, tree.cpp:186-261): same
+// arguments (fp64 per-row gradients/hessians, GrowParams, optional split
+// log), same Tree (node numbering, values from the children's fp64 totals,
+// threshold_value from data.boundaries as find_best_split does,
+// tree.cpp:174-180). The histogram, subtraction, split scans and partitions
+// run on the device; `params.backend`/`precision` are accepted for signature
+// parity (the device builds fp32 histograms reduced in fp64).
+inline histoboost::Tree grow_tree_cuda(const DeviceDataset& dev, const histoboost::BinnedDataset& data,
+                                       std::span<const double> gradients, std::span<const double> hessians,
+                                       const histoboost::GrowParams& params,
+                                       std::vector<histoboost::SplitInfo>* split_log = nullptr) {
+  if (params.num_leaves < 1) throw std::invalid_argument("num_leaves must be at least 1");
+  if (gradients.size() != static_cast<std::size_t>(data.num_rows) ||
+      hessians.size() != static_cast<std::size_t>(data.num_rows)) {
+    throw std::invalid_argument("gradient/hessian length differs from the row count");
+  }
+  const hbg_grow_params p{params.num_leaves, 0, params.min_data_in_leaf, params.lambda};
+  std::vector<hbg_split> log(static_cast<std::size_t>(std::max(1, params.num_leaves - 1)));
+  std::vector<hbg_tree_node> nodes(static_cast<std::size_t>(std::max(1, 2 * params.num_leaves - 1)));
+  std::int32_t ns = 0, nn = 0;
+  check(hbg_grow_tree_host(dev.get(), gradients.data(), hessians.data(), &p, log.data(), &ns, nodes.data(), &nn));
+  auto threshold_value = [&](int feature, int bin) {
+    if (bin == 0) return -std::numeric_limits<double>::infinity();
+    return data.boundaries[static_cast<std::size_t>(feature)].upper_bounds[static_cast<std::size_t>(bin - 1)];
+  };
+  histoboost::Tree tree;
+  for (std::int32_t i = 0; i < nn; ++i) {
+    const hbg_tree_node& n = nodes[static_cast<std::size_t>(i)];
+    histoboost::TreeNode t;
+    t.feature = n.feature;
+    t.threshold_bin = n.threshold_bin;
+    t.threshold_value = n.feature >= 0 ? threshold_value(n.feature, n.threshold_bin) : 0.0;
+    t.left = n.left;
+    t.right = n.right;
+    t.value = n.value;
+    tree.nodes().push_back(t);
+  }
+  if (split_log) {
+    for (std::int32_t i = 0; i < ns; ++i) {
+      const hbg_split& s = log[static_cast<std::size_t>(i)];
+      histoboost::SplitInfo si;
+      si.feature = s.feature;
+      si.threshold_bin = s.threshold_bin;
+      si.threshold_value = threshold_value(s.feature, s.threshold_bin);
+      si.gain = s.gain;
+      si.left_grad = s.left_grad;
+      si.left_hess = s.left_hess;
+      si.right_grad = s.right_grad;
+      si.right_hess = s.right_hess;
+      si.left_count = s.left_count;
+      si.right_count = s.right_count;
+      si.left_value = s.left_value;
+      si.right_value = s.right_value;
+      split_log->push_back(si);
+    }
+  }
+  return tree;
 }
 
 }  // namespace hbg::histoboost_backend

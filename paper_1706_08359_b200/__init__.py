@@ -126,6 +126,7 @@ EXPORTED_SYMBOLS = (
     "hbg_best_split_device_totals",
     "hbg_find_best_split",
     "hbg_grow_tree",
+    "hbg_grow_tree_host",
     "hbg_grow_tree_sharded",
     "hbg_comm_get_unique_id",
     "hbg_comm_init",
@@ -176,6 +177,7 @@ def lib() -> C.CDLL:
         L.hbg_find_best_split.argtypes = [_P, C.c_int32, C.c_int32, C.c_double, C.c_double,
                                           C.c_int64, C.c_int64, C.c_double, _P, _P]
         L.hbg_grow_tree.argtypes = [_P, _P, _P, _P, _P, _P, _P, _P, _P]
+        L.hbg_grow_tree_host.argtypes = [_P, _P, _P, _P, _P, _P, _P, _P]
         L.hbg_grow_tree_sharded.argtypes = [_P, _P, _P, _P, ALLREDUCE_FN, _P, _P, _P, _P, _P, _P]
         L.hbg_comm_get_unique_id.argtypes = [_P]
         L.hbg_comm_init.argtypes = [_P, C.c_int32, C.c_int32, _P, C.c_int32]
@@ -300,6 +302,21 @@ class Dataset:
         nn = C.c_int32()
         check(lib().hbg_grow_tree(self.handle, _ptr(grad), _ptr(hess), C.byref(p), _ptr(log), C.byref(ns),
                                   _ptr(nodes), C.byref(nn), _ptr(stream)))
+        return log[: ns.value].copy(), nodes[: nn.value].copy()
+
+    def grow_tree_host(self, gradients: np.ndarray, hessians: np.ndarray, num_leaves: int = 31,
+                       min_data_in_leaf: int = 1, lam: float = 0.0):
+        """grow_tree (tree.cpp:186-261) from host fp64 per-row gradients/hessians
+        (the reference's span<const double> arguments). Returns (split_log, nodes)."""
+        g = np.ascontiguousarray(gradients, dtype=np.float64)
+        h = np.ascontiguousarray(hessians, dtype=np.float64)
+        p = hbg_grow_params(num_leaves, 0, min_data_in_leaf, lam)
+        log = np.zeros(max(num_leaves - 1, 1), dtype=SPLIT_DTYPE)
+        nodes = np.zeros(max(2 * num_leaves - 1, 1), dtype=NODE_DTYPE)
+        ns = C.c_int32()
+        nn = C.c_int32()
+        check(lib().hbg_grow_tree_host(self.handle, g.ctypes.data, h.ctypes.data, C.byref(p), log.ctypes.data,
+                                       C.byref(ns), nodes.ctypes.data, C.byref(nn)))
         return log[: ns.value].copy(), nodes[: nn.value].copy()
 
     def grow_tree_sharded(self, grad, hess, allreduce, ctx=None, num_leaves: int = 31,

@@ -892,6 +892,37 @@ int hbg_grow_tree(hbg_dataset* ds, const float* d_grad, const float* d_hess,
   });
 }
 
+int hbg_grow_tree_host(hbg_dataset* ds, const double* gradients, const double* hessians,
+                       const hbg_grow_params* params, hbg_split* split_log, int32_t* num_splits,
+                       hbg_tree_node* nodes, int32_t* num_nodes) {
+  return guarded([&] {
+    check_ds(ds);
+    require(params != nullptr && split_log != nullptr && num_splits != nullptr && num_nodes != nullptr,
+            "null argument");
+    const int64_t N = ds->layout.num_rows;
+    require(N == 0 || (gradients != nullptr && hessians != nullptr), "null gradient/hessian pointer");
+    DeviceGuard dg(ds->layout.device);
+    cudaStream_t s = ds->stream;
+    float *gf = nullptr, *hf = nullptr;
+    if (N > 0) {
+      const size_t n = static_cast<size_t>(N);
+      double* gd = static_cast<double*>(ds->host_gd.get(n * 8));
+      double* hd = static_cast<double*>(ds->host_hd.get(n * 8));
+      gf = static_cast<float*>(ds->boost_g.get(n * 4 + 4));
+      hf = static_cast<float*>(ds->boost_h.get(n * 4 + 4));
+      HBG_CUDA(cudaMemcpyAsync(gd, gradients, n * 8, cudaMemcpyHostToDevice, s));
+      HBG_CUDA(cudaMemcpyAsync(hd, hessians, n * 8, cudaMemcpyHostToDevice, s));
+      launch_f64_to_f32(gd, gf, N, s);
+      launch_f64_to_f32(hd, hf, N, s);
+    }
+    if (use_host_loop())
+      grow_tree_impl(ds, gf, hf, *params, Reducer{nullptr, nullptr}, split_log, num_splits, nodes, num_nodes, s);
+    else
+      grow_tree_persistent(ds, gf, hf, *params, split_log, num_splits, nodes, num_nodes, s);
+    HBG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
 int hbg_grow_tree_sharded(hbg_dataset* ds, const float* d_grad, const float* d_hess,
                           const hbg_grow_params* params, hbg_allreduce_fn allreduce, void* ctx,
                           hbg_split* split_log, int32_t* num_splits, hbg_tree_node* nodes,

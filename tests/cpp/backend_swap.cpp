@@ -12,6 +12,7 @@
 // into oracle/_ref/backend_swap, which travels to the GPU box; run by
 // tests/test_gpu_backend_swap.py.
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <optional>
@@ -68,6 +69,48 @@ int main() {
                   static_cast<long long>(leaf.count()), ok ? "equivalent" : "DIFF", worst,
                   split_ok ? "same" : "DIFF", bw ? bw->feature : -1, bw ? bw->threshold_bin : -1);
     }
+  }
+  // whole-tree drop-in: grow_tree_cuda vs the reference's grow_tree (bits64)
+  // on inputs without near-ties (min_data_in_leaf large enough): the same
+  // split sequence, node numbering and thresholds; leaf values within 1e-7
+  // relative (test_tree.cpp:264-299 allows 1e-10 between its own backends,
+  // which share the fp64 inputs; the device keeps the per-row g/h as fp32 —
+  // the bits32 cast of histogram.cpp:97-98 — so its fp64 totals sum the
+  // rounded values: ~1e-9 measured)
+  for (const auto& s : {std::array<int, 4>{200000, 28, 64, 255}, std::array<int, 4>{100000, 40, 16, 63},
+                        std::array<int, 4>{50000, 12, 256, 31}}) {
+    BinnedDataset data = gen_synthetic_bins(s[0], s[1], s[2], 3 + s[1]);
+    std::vector<double> g(static_cast<std::size_t>(s[0])), h(static_cast<std::size_t>(s[0]));
+    for (auto& v : g) v = normal_double(rng);
+    for (auto& v : h) v = 0.1 + uniform_double(rng);
+    for (int r = 0; r < s[0]; ++r)  // some structure on feature 5
+      g[static_cast<std::size_t>(r)] += 0.5 * (data.columns[5].bins[static_cast<std::size_t>(r)] > s[2] / 2);
+    GrowParams gp;
+    gp.num_leaves = s[3];
+    gp.min_data_in_leaf = 400;
+    gp.precision = PrecisionMode::bits64;
+    std::vector<SplitInfo> want_log, got_log;
+    Tree want = grow_tree(data, g, h, gp, &want_log);
+    hbg::histoboost_backend::DeviceDataset dev(data);
+    Tree got = hbg::histoboost_backend::grow_tree_cuda(dev, data, g, h, gp, &got_log);
+    bool ok = want_log.size() == got_log.size() && want.nodes().size() == got.nodes().size();
+    double worst = 0.0;
+    for (std::size_t i = 0; ok && i < want_log.size(); ++i) {
+      ok = want_log[i].feature == got_log[i].feature && want_log[i].threshold_bin == got_log[i].threshold_bin &&
+           want_log[i].left_count == got_log[i].left_count &&
+           want_log[i].threshold_value == got_log[i].threshold_value;
+    }
+    for (std::size_t i = 0; ok && i < want.nodes().size(); ++i) {
+      const TreeNode &a = want.nodes()[i], &b = got.nodes()[i];
+      ok = a.feature == b.feature && a.threshold_bin == b.threshold_bin && a.left == b.left && a.right == b.right;
+      const double dev_ = std::fabs(a.value - b.value) / std::max(1.0, std::fabs(a.value));
+      worst = std::max(worst, dev_);
+      ok = ok && dev_ <= 1e-7;
+    }
+    ++checks;
+    if (!ok) ++failures;
+    std::printf("[%s] grow_tree_cuda rows=%d d=%d k=%d leaves=%d: %zu splits %s (max value dev %.1e)\n",
+                ok ? "PASS" : "FAIL", s[0], s[1], s[2], s[3], want_log.size(), ok ? "identical" : "DIFFER", worst);
   }
   // error behaviour: bins beyond the capacity are rejected like invalid_argument
   {

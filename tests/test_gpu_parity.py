@@ -485,6 +485,18 @@ def test_grow_tree_matches_oracle(hbg, oracle, rows, d, k, leaves, min_data, lam
         assert same == len(want_log)
 
 
+def test_grow_tree_host_pointer_dropin(hbg, oracle):
+    """hbg_grow_tree_host: grow_tree from host fp64 g/h (the reference's
+    span<const double> arguments) — the identical tree on non-tied inputs."""
+    cols = oracle.gen_synthetic_bins(60000, 20, 64, 5)
+    g, h = oracle.gen_grad_hess(60000, 5)
+    g = g + 0.4 * (cols[7].astype(np.float64) > 30)
+    with hbg.Dataset(cols, 64) as ds:
+        log, nodes = ds.grow_tree_host(g, h, 63, 100, 0.5)
+    want_log, want_nodes = oracle.grow_tree(cols, 64, g, h, 63, 100, 0.5, 64)
+    assert _assert_same_tree(log, nodes, want_log, want_nodes) == len(want_log)
+
+
 @pytest.mark.parametrize("grower", ["persistent", "host"])
 def test_grow_tree_edge_cases(hbg, oracle, grower, monkeypatch):
     monkeypatch.setenv("HBG_GROW", grower)
