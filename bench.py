@@ -431,6 +431,17 @@ def run_hbg(args):
             "rows_features_per_s_built": built * d / t_tree,
             "note": "root + smaller child of every split (larger by subtraction); all splits in one persistent cooperative kernel (grow_persistent.cu)",
         }
+        if comm is None:
+            # end to end through the whole-tree drop-in (hbg_grow_tree_host):
+            # host fp64 g/h (pinned) in, split log + nodes out, H2D inside
+            pg64 = torch.from_numpy(g.astype(np.float64)).pin_memory().numpy()
+            ph64 = torch.from_numpy(h.astype(np.float64)).pin_memory().numpy()
+            ds.grow_tree_host(pg64, ph64, args.num_leaves, 1, 0.0)
+            t0 = time.perf_counter()
+            for _ in range(args.trees):
+                ds.grow_tree_host(pg64, ph64, args.num_leaves, 1, 0.0)
+            result["tree"]["e2e_sec_per_tree"] = (time.perf_counter() - t0) / args.trees
+            result["tree"]["e2e_api"] = "hbg_grow_tree_host (host fp64 g/h, 16 B/row H2D; split log + nodes D2H)"
     clocks.stop()
     result["clocks"] = clocks.summary(t_wall0, t_wall1)
 
