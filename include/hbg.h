@@ -188,6 +188,38 @@ int hbg_grow_tree_sharded(hbg_dataset* ds, const float* d_grad, const float* d_h
                           hbg_split* split_log, int32_t* num_splits, hbg_tree_node* nodes,
                           int32_t* num_nodes, void* stream);
 
+/* ---- row-sharded growth inside the persistent kernel ----
+ * Each rank owns an exchange area on its GPU; every rank maps every rank's
+ * area (CUDA IPC across processes: hbg_peer_handle + hbg_peer_open; same
+ * process: hbg_peer_attach). hbg_grow_tree_peer then grows the tree with the
+ * per-split exchange of the smaller child's histogram chunks and the
+ * partition totals done INSIDE the one-kernel grower over NVLink peer memory
+ * (every rank sums all ranks' contributions in rank order: identical
+ * histograms, identical trees on every rank). d_grad/d_hess/dataset: this
+ * rank's rows. All ranks call it for the same tree with the same params.
+ * ctas: CTAs per rank (0 = one per SM; a partial grid lets several ranks
+ * share one GPU, as the tests do). Trees grown through the peer must not
+ * exceed params->num_leaves of hbg_peer_create (workspace reserved there). */
+/* The dataset's own CUDA stream (created with the handle; the host drop-ins
+ * run on it). Ranks sharing one GPU should each grow on their dataset's
+ * stream: consecutively created streams land on distinct hardware queues
+ * (with CUDA_DEVICE_MAX_CONNECTIONS >= the rank count), so the ranks'
+ * persistent grids run concurrently. */
+void* hbg_dataset_stream(const hbg_dataset* ds);
+
+#define HBG_PEER_HANDLE_BYTES 64
+typedef struct hbg_peer hbg_peer;
+int hbg_peer_create(hbg_dataset* ds, int32_t nranks, int32_t rank, int32_t ctas,
+                    const hbg_grow_params* params /* the largest tree: its workspace is reserved */,
+                    hbg_peer** out);
+int hbg_peer_handle(hbg_peer* p, uint8_t* out /* HBG_PEER_HANDLE_BYTES */);
+int hbg_peer_open(hbg_peer* p, int32_t peer_rank, const uint8_t* handle);
+int hbg_peer_attach(hbg_peer* p, int32_t peer_rank, const hbg_peer* q);
+int hbg_peer_destroy(hbg_peer* p);
+int hbg_grow_tree_peer(hbg_dataset* ds, const float* d_grad, const float* d_hess, const hbg_grow_params* params,
+                       hbg_peer* peer, hbg_split* split_log, int32_t* num_splits, hbg_tree_node* nodes,
+                       int32_t* num_nodes, void* stream);
+
 /* NCCL communicator implementing the hook: one process per GPU, the 128-byte
  * unique id produced by rank 0 is shared out of band. Pass the hbg_comm* as
  * `ctx` with hbg_comm_allreduce as `allreduce`. */

@@ -128,6 +128,13 @@ EXPORTED_SYMBOLS = (
     "hbg_grow_tree",
     "hbg_grow_tree_host",
     "hbg_grow_tree_sharded",
+    "hbg_dataset_stream",
+    "hbg_peer_create",
+    "hbg_peer_handle",
+    "hbg_peer_open",
+    "hbg_peer_attach",
+    "hbg_peer_destroy",
+    "hbg_grow_tree_peer",
     "hbg_comm_get_unique_id",
     "hbg_comm_init",
     "hbg_comm_destroy",
@@ -178,6 +185,14 @@ def lib() -> C.CDLL:
                                           C.c_int64, C.c_int64, C.c_double, _P, _P]
         L.hbg_grow_tree.argtypes = [_P, _P, _P, _P, _P, _P, _P, _P, _P]
         L.hbg_grow_tree_host.argtypes = [_P, _P, _P, _P, _P, _P, _P, _P]
+        L.hbg_dataset_stream.argtypes = [_P]
+        L.hbg_dataset_stream.restype = _P
+        L.hbg_peer_create.argtypes = [_P, C.c_int32, C.c_int32, C.c_int32, _P, _P]
+        L.hbg_peer_handle.argtypes = [_P, _P]
+        L.hbg_peer_open.argtypes = [_P, C.c_int32, _P]
+        L.hbg_peer_attach.argtypes = [_P, C.c_int32, _P]
+        L.hbg_peer_destroy.argtypes = [_P]
+        L.hbg_grow_tree_peer.argtypes = [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P]
         L.hbg_grow_tree_sharded.argtypes = [_P, _P, _P, _P, ALLREDUCE_FN, _P, _P, _P, _P, _P, _P]
         L.hbg_comm_get_unique_id.argtypes = [_P]
         L.hbg_comm_init.argtypes = [_P, C.c_int32, C.c_int32, _P, C.c_int32]
@@ -319,6 +334,23 @@ class Dataset:
                                        C.byref(ns), nodes.ctypes.data, C.byref(nn)))
         return log[: ns.value].copy(), nodes[: nn.value].copy()
 
+    def stream(self) -> int:
+        """The dataset's own CUDA stream (cudaStream_t as an int)."""
+        return lib().hbg_dataset_stream(self.handle) or 0
+
+    def grow_tree_peer(self, grad, hess, peer: "Peer", num_leaves: int = 31, min_data_in_leaf: int = 1,
+                       lam: float = 0.0, stream=None):
+        """Row-sharded grow_tree with the histogram exchange inside the
+        persistent kernel over peer memory (every rank calls it; this rank's rows)."""
+        p = hbg_grow_params(num_leaves, 0, min_data_in_leaf, lam)
+        log = np.zeros(max(num_leaves - 1, 1), dtype=SPLIT_DTYPE)
+        nodes = np.zeros(max(2 * num_leaves - 1, 1), dtype=NODE_DTYPE)
+        ns = C.c_int32()
+        nn = C.c_int32()
+        check(lib().hbg_grow_tree_peer(self.handle, _ptr(grad), _ptr(hess), C.byref(p), peer.handle, _ptr(log),
+                                       C.byref(ns), _ptr(nodes), C.byref(nn), _ptr(stream)))
+        return log[: ns.value].copy(), nodes[: nn.value].copy()
+
     def grow_tree_sharded(self, grad, hess, allreduce, ctx=None, num_leaves: int = 31,
                           min_data_in_leaf: int = 1, lam: float = 0.0, stream=None):
         """Row-sharded grow_tree: this rank's rows; `allreduce` (an ALLREDUCE_FN,
@@ -453,6 +485,42 @@ def reduce_histograms_device(parts, n_values: int, out, stream=None) -> None:
     """reduce_private_histograms (histogram.cpp:147-157): out = sum of parts in order."""
     arr = (C.c_void_p * len(parts))(*[_ptr(p).value for p in parts])
     check(lib().hbg_reduce_histograms_device(arr, len(parts), n_values, _ptr(out), _ptr(stream)))
+
+
+class Peer:
+    """Exchange area of one rank for row-sharded growth inside the persistent
+    kernel (hbg_peer_*): attach (same process) or open (IPC handle from
+    another process) every other rank's area before growing."""
+
+    HANDLE_BYTES = 64
+
+    def __init__(self, ds: "Dataset", nranks: int, rank: int, ctas: int = 0, max_leaves: int = 255):
+        h = C.c_void_p()
+        p = hbg_grow_params(max_leaves, 0, 1, 0.0)
+        check(lib().hbg_peer_create(ds.handle, nranks, rank, ctas, C.byref(p), C.byref(h)))
+        self._h = h
+        self.rank = rank
+
+    @property
+    def handle(self):
+        return self._h
+
+    def ipc_handle(self) -> bytes:
+        buf = (C.c_uint8 * Peer.HANDLE_BYTES)()
+        check(lib().hbg_peer_handle(self._h, buf))
+        return bytes(buf)
+
+    def open(self, peer_rank: int, handle: bytes):
+        buf = (C.c_uint8 * Peer.HANDLE_BYTES).from_buffer_copy(handle)
+        check(lib().hbg_peer_open(self._h, peer_rank, buf))
+
+    def attach(self, other: "Peer"):
+        check(lib().hbg_peer_attach(self._h, other.rank, other._h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            check(lib().hbg_peer_destroy(self._h))
+            self._h = None
 
 
 class Comm:

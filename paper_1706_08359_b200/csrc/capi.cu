@@ -125,6 +125,23 @@ struct hbg_dataset {
   }
 };
 
+// Row-sharding exchange area of one rank (grow_persistent.cu): allocated on
+// the rank's device, exported as a CUDA IPC handle (other processes) or
+// attached directly (same process); every rank maps every rank's area.
+struct hbg_peer {
+  int nranks = 1, rank = 0, device = 0, ctas = 0;
+  double* xbuf = nullptr;
+  size_t xdoubles = 0;
+  const double* peers[8] = {nullptr};
+  void* opened[8] = {nullptr};  // IPC mappings to close
+  unsigned long long gen = 0;   // tree generation
+  ~hbg_peer() {
+    for (void* p : opened)
+      if (p) cudaIpcCloseMemHandle(p);
+    if (xbuf) cudaFree(xbuf);
+  }
+};
+
 using namespace hbg;
 
 namespace {
@@ -481,17 +498,16 @@ bool use_host_loop() {
   return e != nullptr && std::strcmp(e, "host") == 0;
 }
 
-void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_hess, const hbg_grow_params& P,
-                          hbg_split* split_log, int32_t* num_splits, hbg_tree_node* nodes_out,
-                          int32_t* num_nodes, cudaStream_t s) {
+// Every device buffer of one persistent-grower call, acquired up front (and,
+// for row-sharded ranks sharing a GPU, reserved at hbg_peer_create): a
+// cudaMalloc/cudaFree while another rank's grid waits in an exchange would
+// serialise behind it.
+PersistentGrowArgs grow_workspace(hbg_dataset* ds, const hbg_grow_params& P, int ctas) {
   const hbg_layout& L = ds->layout;
-  require(P.num_leaves >= 1, "num_leaves must be at least 1");
-  require(P.min_data_in_leaf >= 0, "min_data_in_leaf must be non-negative");
   const int64_t N = L.num_rows;
   const int d = L.num_features, k = L.max_bin;
   const size_t D3 = 3 * static_cast<size_t>(d) * k;
   const int max_nodes = std::max(1, 2 * P.num_leaves - 1);
-  double* slots = static_cast<double*>(ds->slots.get(static_cast<size_t>(max_nodes) * D3 * sizeof(double) + 8));
   PersistentGrowArgs a{};
   a.packed = reinterpret_cast<const uint8_t*>(ds->packed);
   a.colbins = static_cast<const uint8_t*>(ds->colbins.p);
@@ -502,26 +518,47 @@ void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_h
   a.k = k;
   a.num_groups = L.num_groups;
   a.num_rows = N;
+  a.ctas = ctas;
+  a.slots = static_cast<double*>(ds->slots.get(static_cast<size_t>(max_nodes) * D3 * sizeof(double) + 8));
   for (int b = 0; b < 2; ++b) {
     a.rows[b] = static_cast<int32_t*>(ds->ord[b][0].get(static_cast<size_t>(N) * 4 + 4));
     a.g[b] = static_cast<float*>(ds->ord[b][1].get(static_cast<size_t>(N) * 4 + 4));
     a.h[b] = static_cast<float*>(ds->ord[b][2].get(static_cast<size_t>(N) * 4 + 4));
   }
-  a.slots = slots;
   a.nodes = ds->grow_nodes.get(grow_nodes_bytes(P.num_leaves));
   a.split_log = static_cast<hbg_split*>(ds->grow_log.get(static_cast<size_t>(max_nodes) * sizeof(hbg_split)));
   a.tree = static_cast<hbg_tree_node*>(ds->grow_tree.get(static_cast<size_t>(max_nodes) * sizeof(hbg_tree_node)));
-  a.counts = static_cast<int*>(ds->grow_counts.get(4 * sizeof(int)));
+  a.counts = static_cast<int*>(ds->grow_counts.get(8 * sizeof(int)));
   a.scratch = ds->grow_scratch.get(grow_scratch_bytes(a, L.device));
   a.acc = static_cast<unsigned long long*>(ds->small_acc.get(small_hist_acc_bytes(d, k)));
-  int* exps = static_cast<int*>(ds->small_exps.get(16));
-  a.exps = exps;
-  double* root = static_cast<double*>(ds->grow_root.get(4 * sizeof(double)));
-  a.root_totals = root;
+  a.exps = static_cast<int*>(ds->small_exps.get(16));
+  a.root_totals = static_cast<double*>(ds->grow_root.get(4 * sizeof(double)));
   a.num_leaves = P.num_leaves;
   a.min_data = P.min_data_in_leaf;
   a.lambda = P.lambda;
-  void* gscratch = ds->part_scratch.get(gather_scratch_doubles(N) * sizeof(double) + 64);
+  ds->part_scratch.get(gather_scratch_doubles(N) * sizeof(double) + 64);
+  if (N > 0 && d > 0) {  // the root histogram's partials (build_device)
+    const HistPlan plan = plan_histogram(L.bits_per_bin, L.max_bin, L.num_groups, N, L.device);
+    ds->part.get(plan.part_values * 12 + 16);
+  }
+  return a;
+}
+
+void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_hess, const hbg_grow_params& P,
+                          hbg_split* split_log, int32_t* num_splits, hbg_tree_node* nodes_out,
+                          int32_t* num_nodes, cudaStream_t s, hbg_peer* peer = nullptr) {
+  const hbg_layout& L = ds->layout;
+  require(P.num_leaves >= 1, "num_leaves must be at least 1");
+  require(P.min_data_in_leaf >= 0, "min_data_in_leaf must be non-negative");
+  const int64_t N = L.num_rows;
+  const int d = L.num_features, k = L.max_bin;
+  const int max_nodes = std::max(1, 2 * P.num_leaves - 1);
+  const bool sharded = peer != nullptr && peer->nranks > 1;
+  PersistentGrowArgs a = grow_workspace(ds, P, sharded ? peer->ctas : 0);
+  double* slots = a.slots;
+  int* exps = const_cast<int*>(a.exps);
+  double* root = const_cast<double*>(a.root_totals);
+  void* gscratch = ds->part_scratch.p;
 
   // root: ordered buffer 0 = (iota, g, h), fp64 totals in a fixed order
   launch_iota(a.rows[0], N, s);
@@ -530,7 +567,20 @@ void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_h
     HBG_CUDA(cudaMemcpyAsync(a.h[0], d_hess, static_cast<size_t>(N) * 4, cudaMemcpyDeviceToDevice, s));
   }
   launch_gather(a.rows[0], N, d_grad, d_hess, nullptr, nullptr, root, static_cast<double*>(gscratch), s);
-  const bool root_splittable = P.num_leaves >= 2 && !(N < 2 * P.min_data_in_leaf || N < 2);
+  if (sharded) {
+    require(peer->device == L.device, "exchange area on another device");
+    a.nranks = peer->nranks;
+    a.rank = peer->rank;
+    a.xown = peer->xbuf;
+    for (int r = 0; r < peer->nranks; ++r) {
+      require(peer->peers[r] != nullptr, "exchange area of a rank not attached");
+      a.xpeer[r] = peer->peers[r];
+    }
+    require(grow_exchange_doubles(a, L.device) <= peer->xdoubles, "exchange area too small for this dataset");
+    a.gen = ++peer->gen;
+  }
+  // root splittability over all ranks is decided in the kernel when sharded
+  const bool root_splittable = sharded || (P.num_leaves >= 2 && !(N < 2 * P.min_data_in_leaf || N < 2));
   if (!root_splittable) {
     double tot[2] = {0.0, 0.0};
     HBG_CUDA(cudaMemcpyAsync(tot, root, sizeof tot, cudaMemcpyDeviceToHost, s));
@@ -543,8 +593,10 @@ void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_h
   launch_fixed_scale(a.g[0], a.h[0], N, exps, s);
   HBG_CUDA(cudaMemsetAsync(a.acc, 0, small_hist_acc_bytes(d, k), s));
   build_device(ds, a.rows[0], N, a.g[0], a.h[0], HBG_GH_LEAF_ALIGNED, slots, s);
-  hbg_split* root_split = reinterpret_cast<hbg_split*>(static_cast<char*>(a.nodes) + grow_root_split_offset());
-  launch_best_split(slots, d, k, root, nullptr, 0.0, 0.0, N, P.min_data_in_leaf, P.lambda, root_split, s);
+  if (!sharded) {  // sharded: the kernel sums the ranks' root histograms first, then scans
+    hbg_split* root_split = reinterpret_cast<hbg_split*>(static_cast<char*>(a.nodes) + grow_root_split_offset());
+    launch_best_split(slots, d, k, root, nullptr, 0.0, 0.0, N, P.min_data_in_leaf, P.lambda, root_split, s);
+  }
   const char* pe = std::getenv("HBG_GROW_PROFILE");
   std::vector<unsigned long long> prof;
   if (pe != nullptr) {  // phase stamps of CTA 0, printed to stderr (development aid)
@@ -553,14 +605,18 @@ void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_h
     HBG_CUDA(cudaMemsetAsync(a.prof, 0, prof.size() * 8, s));
   }
   launch_grow_persistent(a, L.device, s);
-  int counts[4] = {0, 0, 0, 0};
+  int counts[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   HBG_CUDA(cudaMemcpyAsync(counts, a.counts, sizeof counts, cudaMemcpyDeviceToHost, s));
   HBG_CUDA(cudaStreamSynchronize(s));
   if (counts[2] != 0) {
     static const char* what[] = {"", "grid barrier timed out", "partition disagrees with the histogram counts",
-                                 "split produced an empty side"};
+                                 "split produced an empty side", "peer exchange timed out"};
+    char where[128] = "";
+    if (counts[2] == 4)
+      std::snprintf(where, sizeof where, " (rank %d CTA %d awaited tag %d, saw %d)", a.rank, counts[5], counts[3],
+                    counts[4]);
     throw Error(counts[2] == 3 || counts[2] == 2 ? HBG_ERR_LOGIC : HBG_ERR_CUDA,
-                std::string("persistent tree grower: ") + what[counts[2] & 3]);
+                std::string("persistent tree grower: ") + what[counts[2] % 5] + where);
   }
   *num_splits = counts[0];
   *num_nodes = counts[1];
@@ -920,6 +976,108 @@ int hbg_grow_tree_host(hbg_dataset* ds, const double* gradients, const double* h
     else
       grow_tree_persistent(ds, gf, hf, *params, split_log, num_splits, nodes, num_nodes, s);
     HBG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+void* hbg_dataset_stream(const hbg_dataset* ds) { return ds ? static_cast<void*>(ds->stream) : nullptr; }
+
+int hbg_peer_create(hbg_dataset* ds, int32_t nranks, int32_t rank, int32_t ctas, const hbg_grow_params* params,
+                    hbg_peer** out) {
+  return guarded([&] {
+    check_ds(ds);
+    require(out != nullptr && params != nullptr, "null argument");
+    require(params->num_leaves >= 1, "num_leaves must be at least 1");
+    *out = nullptr;
+    require(nranks >= 1 && nranks <= 8 && rank >= 0 && rank < nranks, "bad rank / rank count (1..8)");
+    require(ctas >= 0, "negative CTA count");
+    const hbg_layout& L = ds->layout;
+    DeviceGuard dg(L.device);
+    configure_kernels(L.device);
+    PersistentGrowArgs a{};
+    a.bits = L.bits_per_bin;
+    a.d = L.num_features;
+    a.k = L.max_bin;
+    a.num_groups = L.num_groups;
+    a.num_rows = L.num_rows;
+    a.ctas = ctas;
+    auto p = std::make_unique<hbg_peer>();
+    p->nranks = nranks;
+    p->rank = rank;
+    p->device = L.device;
+    p->ctas = ctas;
+    p->xdoubles = grow_exchange_doubles(a, L.device);
+    HBG_CUDA(cudaMalloc(&p->xbuf, p->xdoubles * sizeof(double)));
+    HBG_CUDA(cudaMemset(p->xbuf, 0, p->xdoubles * sizeof(double)));
+    p->peers[rank] = p->xbuf;
+    grow_workspace(ds, *params, ctas);  // reserve: no allocation while the ranks' grids exchange
+    HBG_CUDA(cudaDeviceSynchronize());
+    *out = p.release();
+  });
+}
+
+int hbg_peer_handle(hbg_peer* p, uint8_t* out) {
+  return guarded([&] {
+    require(p != nullptr && out != nullptr, "null argument");
+    DeviceGuard dg(p->device);
+    cudaIpcMemHandle_t h;
+    HBG_CUDA(cudaIpcGetMemHandle(&h, p->xbuf));
+    static_assert(sizeof(h) <= HBG_PEER_HANDLE_BYTES, "IPC handle size");
+    std::memset(out, 0, HBG_PEER_HANDLE_BYTES);
+    std::memcpy(out, &h, sizeof h);
+  });
+}
+
+int hbg_peer_open(hbg_peer* p, int32_t peer_rank, const uint8_t* handle) {
+  return guarded([&] {
+    require(p != nullptr && handle != nullptr, "null argument");
+    require(peer_rank >= 0 && peer_rank < p->nranks && peer_rank != p->rank, "bad peer rank");
+    DeviceGuard dg(p->device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    void* ptr = nullptr;
+    HBG_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    if (p->opened[peer_rank]) cudaIpcCloseMemHandle(p->opened[peer_rank]);
+    p->opened[peer_rank] = ptr;
+    p->peers[peer_rank] = static_cast<const double*>(ptr);
+  });
+}
+
+int hbg_peer_attach(hbg_peer* p, int32_t peer_rank, const hbg_peer* q) {
+  return guarded([&] {
+    require(p != nullptr && q != nullptr, "null argument");
+    require(peer_rank >= 0 && peer_rank < p->nranks && peer_rank == q->rank && q->nranks == p->nranks,
+            "bad peer rank");
+    if (q->device != p->device) {  // same process, two GPUs: direct peer access over NVLink
+      DeviceGuard dg(p->device);
+      const cudaError_t e = cudaDeviceEnablePeerAccess(q->device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else HBG_CUDA(e);
+    }
+    p->peers[peer_rank] = q->xbuf;
+  });
+}
+
+int hbg_peer_destroy(hbg_peer* p) {
+  return guarded([&] {
+    if (!p) return;
+    DeviceGuard dg(p->device);
+    delete p;
+  });
+}
+
+int hbg_grow_tree_peer(hbg_dataset* ds, const float* d_grad, const float* d_hess, const hbg_grow_params* params,
+                       hbg_peer* peer, hbg_split* split_log, int32_t* num_splits, hbg_tree_node* nodes,
+                       int32_t* num_nodes, void* stream) {
+  return guarded([&] {
+    check_ds(ds);
+    require(params != nullptr && peer != nullptr && split_log != nullptr && num_splits != nullptr &&
+                num_nodes != nullptr,
+            "null argument");
+    require(ds->layout.num_rows == 0 || (d_grad != nullptr && d_hess != nullptr),
+            "null gradient/hessian pointer");
+    DeviceGuard dg(ds->layout.device);
+    grow_tree_persistent(ds, d_grad, d_hess, *params, split_log, num_splits, nodes, num_nodes,
+                         static_cast<cudaStream_t>(stream), peer);
   });
 }
 

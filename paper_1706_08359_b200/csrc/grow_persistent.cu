@@ -45,6 +45,9 @@ namespace {
 using namespace dev;
 
 constexpr int kItems = 8;               // parent rows per thread in the small-parent path
+constexpr int kMaxRanks = 8;            // row shards exchanging through peer memory
+constexpr int kXHeader = 16;            // doubles before the exchange blocks (done flag)
+constexpr int kXBlockHeader = 16;       // doubles per block before the histogram: flag, totals
 constexpr int64_t kDirectRows = 8192;   // smaller child: direct per-chunk histogram up to this size
 
 template <int K>
@@ -53,8 +56,9 @@ __host__ __device__ constexpr int grow_threads() {
 }
 
 struct NodeDev {
-  int64_t begin, count;  // rows [begin, begin+count) of ordered buffer `buf`
-  double grad, hess;     // fp64 totals (gather_leaf_statistics)
+  int64_t begin, count;  // this rank's rows [begin, begin+count) of ordered buffer `buf`
+  int64_t gcount;        // rows of the node over all ranks
+  double grad, hess;     // fp64 totals over all ranks (gather_leaf_statistics)
   hbg_split best;        // valid when has_best
   int32_t buf, has_best;
 };
@@ -70,9 +74,11 @@ struct Desc {
   int32_t lsplit, rsplit, small_is_left, path;
   int32_t nseg, items;
   int64_t begin, count;  // parent range
-  int64_t nl, nr;        // rows left / right (the split's left_count)
+  int64_t nl, nr;        // rows left / right over all ranks (the split's left_count)
   int64_t seg_len;
-  double tot[4];         // gl, hl, gr, hr (partition)
+  int64_t nl_loc;        // this rank's rows sent left (partition)
+  double tot_loc[4];     // this rank's gl, hl, gr, hr (partition)
+  double tot[4];         // gl, hl, gr, hr over all ranks
 };
 
 struct GrowArgs {
@@ -111,6 +117,14 @@ struct GrowArgs {
   int fchunk, nchunks;   // finish/scan: features per chunk
   long long timeout_cycles;
   unsigned long long* prof;  // optional: [iter][kProfSlots] globaltimer stamps of CTA 0
+  // row sharding (nranks > 1): per-split exchange of the smaller child's
+  // histogram chunks and the partition totals through peer memory
+  int nranks, rank;
+  double* xown;                    // this rank's exchange area
+  const double* xpeer[kMaxRanks];  // every rank's exchange area (xpeer[rank] == xown), mapped
+  size_t xblock;                   // doubles per (parity, chunk) block
+  unsigned long long gen;          // tree generation (tags are monotonic across trees)
+  int debug;                       // HBG_GROW_DEBUG: CTA 0 prints every pick
 };
 
 constexpr int kProfSlots = 12;
@@ -127,7 +141,7 @@ __device__ __forceinline__ void stamp(const GrowArgs& a, int iter, int slot) {
     a.prof[static_cast<size_t>(iter) * kProfSlots + slot] = global_ns();
 }
 
-enum GrowError { kErrNone = 0, kErrBarrierTimeout = 1, kErrPartition = 2, kErrEmptySide = 3 };
+enum GrowError { kErrNone = 0, kErrBarrierTimeout = 1, kErrPartition = 2, kErrEmptySide = 3, kErrPeerTimeout = 4 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
@@ -165,6 +179,110 @@ __device__ __forceinline__ void grid_sync(const GrowArgs& a) {
     __threadfence();
   }
   __syncthreads();
+}
+
+// ---- peer exchange (row sharding) -------------------------------------------
+// Rank r's exchange area: a header (done flag) + blocks [parity][chunk], each
+// = {flag, this rank's totals: gl, hl, gr, hr, rows left, rows; the chunk's
+// smaller-child histogram [stat][cell] fp64}. Writer: data, fence.sys, flag =
+// tag (release.sys). Reader: poll the flag (acquire.sys), read. Every rank
+// sums all ranks' blocks in rank order, so every rank holds bit-identical
+// global histograms and totals and takes the identical decisions. Parities
+// alternate per split: a rank publishes split i only after it read every
+// peer's split i-1, which every peer published only after finishing its reads
+// of split i-2 (the same parity). Tags carry the tree generation, so flags
+// never need resetting; a done handshake ends every tree.
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const double* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(double* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ const double* xblock(const GrowArgs& a, const double* base, int parity, int c) {
+  return base + kXHeader + (static_cast<size_t>(parity) * a.nchunks + c) * a.xblock;
+}
+
+__device__ __forceinline__ unsigned long long xtag(const GrowArgs& a, int iter) {
+  return (a.gen << 24) | static_cast<unsigned long long>(iter + 2);  // root: iter = -1
+}
+
+// Thread 0: wait until `p` carries `tag` (bounded: a dead peer is an error).
+__device__ __forceinline__ bool wait_flag(const GrowArgs& a, const double* p, unsigned long long tag) {
+  const long long t0 = clock64();
+  unsigned long long v;
+  while ((v = ld_acquire_sys(p)) != tag) {
+    if (clock64() - t0 > a.timeout_cycles) {
+      if (atomicCAS(a.counts + 2, 0, kErrPeerTimeout) == 0) {  // where: the awaited tag and the value seen
+        a.counts[3] = static_cast<int>(tag & 0xFFFFFF);
+        a.counts[4] = static_cast<int>(v & 0xFFFFFF);
+        a.counts[5] = static_cast<int>(blockIdx.x);
+      }
+      return false;
+    }
+  }
+  return true;
+}
+
+// Publish this rank's chunk (vals: 3 stats x `stride` doubles in shared
+// memory, `cells` used) and totals tot[0..5] into block (parity, c); then
+// replace vals and tot by the rank-order sums over all ranks. Whole CTA.
+template <int NT>
+__device__ void exchange_chunk(const GrowArgs& a, int parity, int c, unsigned long long tag, double* vals,
+                               int stride, int cells, double* tot /* smem, 6 */) {
+  double* mine = const_cast<double*>(xblock(a, a.xown, parity, c));
+  for (int i = threadIdx.x; i < cells; i += NT) {
+    mine[kXBlockHeader + i] = vals[i];
+    mine[kXBlockHeader + cells + i] = vals[stride + i];
+    mine[kXBlockHeader + 2 * cells + i] = vals[2 * stride + i];
+  }
+  if (threadIdx.x == 0)
+    for (int j = 0; j < 6; ++j) mine[1 + j] = tot[j];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    st_release_sys(mine, tag);
+  }
+  __shared__ double s_tot[6];
+  for (int r = 0; r < a.nranks; ++r) {
+    const double* blk = xblock(a, a.xpeer[r], parity, c);
+    if (threadIdx.x == 0) wait_flag(a, blk, tag);
+    __syncthreads();
+    for (int i = threadIdx.x; i < cells; i += NT) {
+      const double g = __ldcv(blk + kXBlockHeader + i), h = __ldcv(blk + kXBlockHeader + cells + i),
+                   n = __ldcv(blk + kXBlockHeader + 2 * cells + i);
+      vals[i] = r == 0 ? g : vals[i] + g;
+      vals[stride + i] = r == 0 ? h : vals[stride + i] + h;
+      vals[2 * stride + i] = r == 0 ? n : vals[2 * stride + i] + n;
+    }
+    if (threadIdx.x == 0)
+      for (int j = 0; j < 6; ++j) s_tot[j] = r == 0 ? __ldcv(blk + 1 + j) : s_tot[j] + __ldcv(blk + 1 + j);
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) tot[threadIdx.x] = s_tot[threadIdx.x];
+  __syncthreads();
+}
+
+// Thread 0 only: publish totals into block (parity, c) (when `publish`), then
+// the rank-order sum of every rank's block totals.
+__device__ void exchange_totals(const GrowArgs& a, int parity, int c, unsigned long long tag, bool publish,
+                                double* tot /* 6 */) {
+  if (publish) {
+    double* mine = const_cast<double*>(xblock(a, a.xown, parity, c));
+    for (int j = 0; j < 6; ++j) mine[1 + j] = tot[j];
+    __threadfence_system();
+    st_release_sys(mine, tag);
+  }
+  double sum[6];
+  for (int r = 0; r < a.nranks; ++r) {
+    const double* blk = xblock(a, a.xpeer[r], parity, c);
+    wait_flag(a, blk, tag);
+    for (int j = 0; j < 6; ++j) sum[j] = r == 0 ? __ldcv(blk + 1 + j) : sum[j] + __ldcv(blk + 1 + j);
+  }
+  for (int j = 0; j < 6; ++j) tot[j] = sum[j];
 }
 
 template <int NT>
@@ -324,7 +442,7 @@ __device__ __forceinline__ unsigned long long gain_key(double gain) {
 
 // Children of the split just executed, as every CTA computed them.
 struct Kid {
-  int64_t begin, count;
+  int64_t begin, count, gcount;
   double grad, hess;
   hbg_split best;
   int32_t buf, has_best;
@@ -382,19 +500,21 @@ __device__ void pick(const GrowArgs& a, int i, int kid_l, const Kid* kid, Desc& 
           a.counts[1] = nnodes;
         }
       } else {
-        int64_t begin, count;
+        int64_t begin, count, gcount;
         int buf;
         hbg_split bs;
         if (kid_l >= 0 && (p == kid_l || p == kid_l + 1)) {
           const Kid& q = kid[p - kid_l];
           begin = q.begin;
           count = q.count;
+          gcount = q.gcount;
           buf = q.buf;
           bs = q.best;
         } else {
           const NodeDev* P = a.nodes + p;
           begin = __ldcg(&P->begin);
           count = __ldcg(&P->count);
+          gcount = __ldcg(&P->gcount);
           buf = __ldcg(&P->buf);
           bs = load_split(&P->best);
         }
@@ -404,7 +524,7 @@ __device__ void pick(const GrowArgs& a, int i, int kid_l, const Kid* kid, Desc& 
           a.split_log[i] = bs;
           a.tree[p] = hbg_tree_node{bs.feature, bs.threshold_bin, left, right, 0.0};
         }
-        const int64_t nl = bs.left_count, nr = count - nl;
+        const int64_t nl = bs.left_count, nr = gcount - nl;  // over all ranks
         D.done = 0;
         D.iter = i;
         D.parent = p;
@@ -418,6 +538,10 @@ __device__ void pick(const GrowArgs& a, int i, int kid_l, const Kid* kid, Desc& 
         D.thr = bs.threshold_bin;
         D.nl = nl;
         D.nr = nr;
+        if (a.debug && (blockIdx.x == 0 || nl <= 0 || nr <= 0))
+          printf("CTA %d ", blockIdx.x), printf("rank %d split %d: parent %d local %lld global %lld feat %d thr %d nl %lld nr %lld gain %g\n", a.rank, i,
+                 p, static_cast<long long>(count), static_cast<long long>(gcount), bs.feature, bs.threshold_bin,
+                 static_cast<long long>(nl), static_cast<long long>(nr), bs.gain);
         if (nl <= 0 || nr <= 0) {  // tree.cpp:124-126 (logic_error)
           set_error(a, kErrEmptySide);
           D.done = 1;
@@ -448,29 +572,28 @@ __device__ void pick(const GrowArgs& a, int i, int kid_l, const Kid* kid, Desc& 
   __syncthreads();
 }
 
-// After the partition (all CTAs): the children's local records; CTA 0
-// writes their leaf values.
+// After the partition (all CTAs): the children's records (this rank's row
+// ranges, global sizes; totals local until the exchange).
 __device__ void set_children(const GrowArgs& a, const Desc& D, Kid* kid) {
   if (threadIdx.x == 0) {
-    kid[0] = Kid{D.begin, D.nl, D.tot[0], D.tot[1], hbg_split{}, D.buf_out, 0};
-    kid[1] = Kid{D.begin + D.nl, D.nr, D.tot[2], D.tot[3], hbg_split{}, D.buf_out, 0};
+    kid[0] = Kid{D.begin, D.nl_loc, D.nl, D.tot[0], D.tot[1], hbg_split{}, D.buf_out, 0};
+    kid[1] = Kid{D.begin + D.nl_loc, D.count - D.nl_loc, D.nr, D.tot[2], D.tot[3], hbg_split{}, D.buf_out, 0};
     kid[0].best.feature = kid[1].best.feature = -1;
-    if (blockIdx.x == 0) {
-      a.tree[D.left_id] = hbg_tree_node{-1, -1, -1, -1, leaf_value(D.tot[0], D.tot[1], a.lambda)};
-      a.tree[D.right_id] = hbg_tree_node{-1, -1, -1, -1, leaf_value(D.tot[2], D.tot[3], a.lambda)};
-    }
   }
   __syncthreads();
 }
 
-// CTA 0: the children's persistent records (read by later picks, after at
-// least one more barrier).
-__device__ void store_children(const GrowArgs& a, const Desc& D, const Kid* kid) {
+// CTA 0: the children's leaf values and persistent records (read by later
+// picks, after at least one more barrier), from the global totals.
+__device__ void store_children(const GrowArgs& a, const Desc& D, Kid* kid) {
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
   for (int c = 0; c < 2; ++c) {
     const int id = c == 0 ? D.left_id : D.right_id;
-    const Kid& q = kid[c];
-    a.nodes[id] = NodeDev{q.begin, q.count, q.grad, q.hess, q.best, q.buf, q.has_best};
+    Kid& q = kid[c];
+    q.grad = D.tot[2 * c];
+    q.hess = D.tot[2 * c + 1];
+    a.tree[id] = hbg_tree_node{-1, -1, -1, -1, leaf_value(q.grad, q.hess, a.lambda)};
+    a.nodes[id] = NodeDev{q.begin, q.count, q.gcount, q.grad, q.hess, q.best, q.buf, q.has_best};
     a.node_gain[id] = q.has_best ? q.best.gain : -1.0;
   }
 }
@@ -532,8 +655,9 @@ __device__ void partition_redundant(const GrowArgs& a, Desc& D, RegRows& rr, Par
   block_sum_4d1<NT>(v, c, ps);
   const int64_t L = ps.cnt;
   if (threadIdx.x == 0) {
-    for (int j = 0; j < 4; ++j) D.tot[j] = ps.tot[j];
-    if (L != D.nl) set_error(a, kErrPartition);
+    for (int j = 0; j < 4; ++j) D.tot_loc[j] = D.tot[j] = ps.tot[j];
+    D.nl_loc = L;
+    if (a.nranks == 1 && L != D.nl) set_error(a, kErrPartition);
   }
   // this CTA's share of the output positions (the first `parts` CTAs partition)
   const int64_t share = (n + parts - 1) / parts;
@@ -644,8 +768,9 @@ __device__ void partition_scatter(const GrowArgs& a, Desc& D, PartShared<NT>& ps
   block_sum_4d1<NT>(v, c, ps);
   const int64_t L = ps.cnt;
   if (threadIdx.x == 0) {
-    for (int j = 0; j < 4; ++j) D.tot[j] = ps.tot[j];
-    if (L != D.nl) set_error(a, kErrPartition);
+    for (int j = 0; j < 4; ++j) D.tot_loc[j] = D.tot[j] = ps.tot[j];
+    D.nl_loc = L;
+    if (a.nranks == 1 && L != D.nl) set_error(a, kErrPartition);
   }
   __syncthreads();
   const int64_t n = D.count, chunk = part_chunk<NT>(n);
@@ -700,8 +825,8 @@ __device__ void partition_scatter(const GrowArgs& a, Desc& D, PartShared<NT>& ps
 
 __device__ __forceinline__ void small_child(const GrowArgs& a, const Desc& D, const int32_t*& rows,
                                             const float*& g, const float*& h, int64_t& n) {
-  const int64_t off = D.small_is_left ? 0 : D.nl;
-  n = D.small_is_left ? D.nl : D.nr;
+  const int64_t off = D.small_is_left ? 0 : D.nl_loc;  // this rank's rows of the (globally) smaller child
+  n = D.small_is_left ? D.nl_loc : D.count - D.nl_loc;
   rows = a.rows[D.buf_out] + D.begin + off;
   g = a.g[D.buf_out] + D.begin + off;
   h = a.h[D.buf_out] + D.begin + off;
@@ -757,6 +882,73 @@ __device__ __forceinline__ unsigned* direct_acc(const GrowArgs& a, unsigned char
 __device__ __forceinline__ void zero_direct(const GrowArgs& a, unsigned char* smem, int cells, int NT) {
   unsigned* acc = direct_acc(a, smem);
   for (int i = threadIdx.x; i < 5 * cells; i += NT) acc[i] = 0u;
+}
+
+// Both children's scans of one staged feature chunk at once: threads
+// [0, NT/2) child 0 (staging st[0..3*stride)), the rest child 1; per-child
+// chunk winner -> a.cand[child][c]. Whole CTA.
+template <int NT>
+__device__ void scan_chunk(const GrowArgs& a, double* st, int chunk_cells, int nf, int f0, int c_idx, bool want0,
+                           bool want1, const double* tot, int64_t n0, int64_t n1) {
+  const int k = a.k;
+  constexpr int half = NT / 2, W = NT / 32;
+  const int child = static_cast<int>(threadIdx.x) < half ? 0 : 1;
+  const int tid = static_cast<int>(threadIdx.x) - child * half;
+  const bool want = child == 0 ? want0 : want1;
+  double* base = st + child * 3 * chunk_cells;
+  const double gt = tot[2 * child], ht = tot[2 * child + 1];
+  const int64_t count = child == 0 ? n0 : n1;
+  const Cand best = scan_staged_t(base, base + chunk_cells, base + 2 * chunk_cells, want ? nf : 0, k, f0, gt, ht,
+                                  static_cast<double>(count), static_cast<double>(a.min_data), a.lambda, tid, half);
+  // argmax on (gain bits, ~(f,b)) keys, then the winner's left sums from
+  // the staged prefix sums
+  unsigned long long hk = best.f >= 0 ? gain_key(best.gain) : 0ull;
+  unsigned lk = best.f >= 0 ? 0xFFFFFFFFu - ((static_cast<unsigned>(best.f) << 12) | static_cast<unsigned>(best.b)) : 0u;
+  warp_argmax_key(hk, lk);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __shared__ unsigned long long s_hk[W];
+  __shared__ unsigned s_lk[W];
+  if (lane == 0) {
+    s_hk[w] = hk;
+    s_lk[w] = lk;
+  }
+  __syncthreads();
+  if (w == 0 || w == W / 2) {
+    hk = lane < W / 2 ? s_hk[w + lane] : 0ull;
+    lk = lane < W / 2 ? s_lk[w + lane] : 0u;
+    warp_argmax_key(hk, lk);
+    if (lane == 0 && want) {
+      Cand c{0.0, -1, -1, 0.0, 0.0, 0};
+      if (hk != 0ull) {
+        const unsigned fb = 0xFFFFFFFFu - lk;
+        const int f = static_cast<int>(fb >> 12), b = static_cast<int>(fb & 0xFFFu);
+        const int t = b * nf + (f - f0);
+        c = Cand{__longlong_as_double(static_cast<long long>(hk)), f, b, base[t], base[chunk_cells + t],
+                 static_cast<int64_t>(base[2 * chunk_cells + t])};
+      }
+      a.cand[child * a.nchunks + c_idx] = c;
+    }
+  }
+  __syncthreads();
+}
+
+// Row sharding, a split without a histogram: the scan CTAs still exchange
+// (totals only), so every chunk's blocks advance in lockstep every split.
+template <int NT>
+__device__ void exchange_totals_chunk(const GrowArgs& a, Desc& D, int c) {
+  __shared__ double s_tot[6];
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < 4; ++j) s_tot[j] = D.tot_loc[j];
+    s_tot[4] = static_cast<double>(D.nl_loc);
+    s_tot[5] = 0.0;
+  }
+  __syncthreads();
+  exchange_chunk<NT>(a, D.iter & 1, c, xtag(a, D.iter), nullptr, 0, 0, s_tot);
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < 4; ++j) D.tot[j] = s_tot[j];
+    if (static_cast<int64_t>(s_tot[4]) != D.nl) set_error(a, kErrPartition);
+  }
+  __syncthreads();
 }
 
 // Per feature chunk c: the smaller child's fp64 histogram (from the direct
@@ -831,6 +1023,21 @@ __device__ void finish_chunk(const GrowArgs& a, const Desc& D, int c_idx, unsign
     }
   }
   __syncthreads();
+  if (a.nranks > 1) {  // this rank's chunk + totals -> every rank's, summed in rank order
+    __shared__ double s_tot[6];
+    if (threadIdx.x == 0) {
+      for (int j = 0; j < 4; ++j) s_tot[j] = D.tot_loc[j];
+      s_tot[4] = static_cast<double>(D.nl_loc);
+      s_tot[5] = 0.0;
+    }
+    __syncthreads();
+    exchange_chunk<NT>(a, D.iter & 1, c, xtag(a, D.iter), sm, chunk_cells, cells, s_tot);
+    if (threadIdx.x == 0) {
+      for (int j = 0; j < 4; ++j) const_cast<Desc&>(D).tot[j] = s_tot[j];
+      if (static_cast<int64_t>(s_tot[4]) != D.nl) set_error(a, kErrPartition);
+    }
+    __syncthreads();
+  }
   for (int i = threadIdx.x; i < cells; i += NT) {
     const size_t o = static_cast<size_t>(f0) * k + i;
     const int f = i / k, b = i - f * k;
@@ -849,49 +1056,7 @@ __device__ void finish_chunk(const GrowArgs& a, const Desc& D, int c_idx, unsign
     lg[2 * chunk_cells + t] = xc;
   }
   __syncthreads();
-  // both children's scans at once: threads [0, NT/2) child 0, the rest child 1
-  {
-    constexpr int half = NT / 2, W = NT / 32;
-    const int child = static_cast<int>(threadIdx.x) < half ? 0 : 1;
-    const int tid = static_cast<int>(threadIdx.x) - child * half;
-    const bool want = child == 0 ? D.lsplit : D.rsplit;
-    double* base = st + child * 3 * chunk_cells;
-    const double gt = D.tot[2 * child], ht = D.tot[2 * child + 1];
-    const int64_t count = child == 0 ? D.nl : D.nr;
-    const Cand best = scan_staged_t(base, base + chunk_cells, base + 2 * chunk_cells, want ? nf : 0, k, f0, gt,
-                                    ht, static_cast<double>(count), static_cast<double>(a.min_data), a.lambda, tid,
-                                    half);
-    // argmax on (gain bits, ~(f,b)) keys, then the winner's left sums from
-    // the staged prefix sums
-    unsigned long long hk = best.f >= 0 ? gain_key(best.gain) : 0ull;
-    unsigned lk = best.f >= 0 ? 0xFFFFFFFFu - ((static_cast<unsigned>(best.f) << 12) | static_cast<unsigned>(best.b)) : 0u;
-    warp_argmax_key(hk, lk);
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    __shared__ unsigned long long s_hk[W];
-    __shared__ unsigned s_lk[W];
-    if (lane == 0) {
-      s_hk[w] = hk;
-      s_lk[w] = lk;
-    }
-    __syncthreads();
-    if (w == 0 || w == W / 2) {
-      hk = lane < W / 2 ? s_hk[w + lane] : 0ull;
-      lk = lane < W / 2 ? s_lk[w + lane] : 0u;
-      warp_argmax_key(hk, lk);
-      if (lane == 0 && want) {
-        Cand c{0.0, -1, -1, 0.0, 0.0, 0};
-        if (hk != 0ull) {
-          const unsigned fb = 0xFFFFFFFFu - lk;
-          const int f = static_cast<int>(fb >> 12), b = static_cast<int>(fb & 0xFFFu);
-          const int t = b * nf + (f - f0);
-          c = Cand{__longlong_as_double(static_cast<long long>(hk)), f, b, base[t], base[chunk_cells + t],
-                   static_cast<int64_t>(base[2 * chunk_cells + t])};
-        }
-        a.cand[child * a.nchunks + c_idx] = c;
-      }
-    }
-    __syncthreads();
-  }
+  scan_chunk<NT>(a, st, chunk_cells, nf, f0, c_idx, D.lsplit, D.rsplit, D.tot, D.nl, D.nr);
 }
 
 // Every CTA (warp 0): per-child winner over the chunks (bit-identical in every
@@ -1092,17 +1257,74 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
   __shared__ PartShared<NT> ps;
   __shared__ Desc D;
   __shared__ Kid kid[2];
-  // root: histogram, totals and best split were computed by the host-launched
-  // kernels; every CTA builds the root record and picks split 0
-  if (threadIdx.x == 0) {
-    const double G = __ldcg(a.root_tot), H = __ldcg(a.root_tot + 1);
-    kid[0] = Kid{0, a.root_count, G, H, load_split(&a.nodes[0].best), 0, 0};
-    kid[0].has_best = kid[0].best.feature >= 0 ? 1 : 0;
-    if (blockIdx.x == 0) {
-      a.tree[0] = hbg_tree_node{-1, -1, -1, -1, leaf_value(G, H, a.lambda)};
-      a.nodes[0] = NodeDev{0, a.root_count, G, H, kid[0].best, 0, kid[0].has_best};
-      a.node_gain[0] = kid[0].has_best ? kid[0].best.gain : -1.0;
+  if (a.nranks == 1) {
+    // root: histogram, totals and best split were computed by the
+    // host-launched kernels; every CTA builds the root record
+    if (threadIdx.x == 0) {
+      const double G = __ldcg(a.root_tot), H = __ldcg(a.root_tot + 1);
+      kid[0] = Kid{0, a.root_count, a.root_count, G, H, load_split(&a.nodes[0].best), 0, 0};
+      kid[0].has_best = kid[0].best.feature >= 0 ? 1 : 0;
     }
+  } else {
+    // row-sharded root: this rank's histogram (slot 0) and totals -> the
+    // rank-order sums over all ranks; the scan CTAs scan their chunk of the
+    // global root histogram
+    const bool chunk_cta = static_cast<int>(blockIdx.x) < a.nchunks;
+    __shared__ double rt[6];
+    if (threadIdx.x == 0) {
+      rt[0] = __ldcg(a.root_tot);
+      rt[1] = __ldcg(a.root_tot + 1);
+      rt[2] = rt[3] = rt[4] = 0.0;
+      rt[5] = static_cast<double>(a.root_count);
+      if (!chunk_cta) exchange_totals(a, 1, 0, xtag(a, -1), false, rt);
+    }
+    __syncthreads();
+    if (chunk_cta) {
+      const int d = a.d, k = a.k, c = blockIdx.x;
+      const size_t Dc = static_cast<size_t>(d) * k;
+      const int f0 = c * a.fchunk, nf = min(a.fchunk, d - f0), cells = nf * k, cc = a.fchunk * k;
+      double* st = reinterpret_cast<double*>(smem);
+      double* root = a.slots;  // node 0's slot
+      for (int i = threadIdx.x; i < cells; i += NT) {
+        const size_t o = static_cast<size_t>(f0) * k + i;
+        const int f = i / k, b = i - f * k, t = b * nf + f;
+        st[t] = __ldcg(root + o);
+        st[cc + t] = __ldcg(root + Dc + o);
+        st[2 * cc + t] = __ldcg(root + 2 * Dc + o);
+      }
+      __syncthreads();
+      exchange_chunk<NT>(a, 1, c, xtag(a, -1), st, cc, cells, rt);
+      for (int i = threadIdx.x; i < cells; i += NT) {  // the global root histogram in slot 0
+        const size_t o = static_cast<size_t>(f0) * k + i;
+        const int f = i / k, b = i - f * k, t = b * nf + f;
+        root[o] = st[t];
+        root[Dc + o] = st[cc + t];
+        root[2 * Dc + o] = st[2 * cc + t];
+      }
+      __syncthreads();
+      const int64_t N = static_cast<int64_t>(rt[5]);
+      const bool ok = a.num_leaves >= 2 && splittable(N, a.min_data);  // tree.cpp:165
+      scan_chunk<NT>(a, st, cc, nf, f0, c, ok, false, rt, N, 0);
+    }
+    grid_sync(a);
+    if (threadIdx.x == 0) {  // the root "split" descriptor for winners(): child 0 = the root
+      const int64_t N = static_cast<int64_t>(rt[5]);
+      D.lsplit = a.num_leaves >= 2 && splittable(N, a.min_data);
+      D.rsplit = 0;
+      D.tot[0] = rt[0];
+      D.tot[1] = rt[1];
+      D.nl = N;
+      kid[0] = Kid{0, a.root_count, N, rt[0], rt[1], hbg_split{}, 0, 0};
+      kid[0].best.feature = -1;
+    }
+    __syncthreads();
+    winners<NT>(a, D, kid);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const Kid& r = kid[0];
+    a.tree[0] = hbg_tree_node{-1, -1, -1, -1, leaf_value(r.grad, r.hess, a.lambda)};
+    a.nodes[0] = NodeDev{0, r.count, r.gcount, r.grad, r.hess, r.best, 0, r.has_best};
+    a.node_gain[0] = r.has_best ? r.best.gain : -1.0;
   }
   __syncthreads();
   pick<NT>(a, 0, 0, kid, D);  // node 0 is "kid_l" (kid[1] is never consulted: nnodes = 1)
@@ -1110,7 +1332,9 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
   while (!D.done) {
     const int it = D.iter;
     stamp(a, it, 0);
-    const bool small_parent = D.count <= static_cast<int64_t>(kItems) * NT;
+    // (with row sharding a rank's part of a parent can be small while the
+    // globally smaller child needs the shared-memory histogram)
+    const bool small_parent = D.count <= static_cast<int64_t>(kItems) * NT && D.path != kSmem;
     if (a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0)  // class of this split
       a.prof[static_cast<size_t>(it) * kProfSlots + 7] = (small_parent ? 0 : 4) + D.path;
     const bool chunk_cta = static_cast<int>(blockIdx.x) < a.nchunks;
@@ -1134,10 +1358,21 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
           __syncthreads();
           stamp(a, it, 2);
           finish_chunk<K, NT>(a, D, blockIdx.x, smem, wb);
+        } else if (a.nranks > 1 && D.path == kNoHist) {
+          exchange_totals_chunk<NT>(a, D, blockIdx.x);
         }
         // (kSmem cannot occur: the smaller child of a small parent is <= kDirectRows)
+      } else if (a.nranks > 1) {
+        // this rank's left count is needed for the children's row ranges:
+        // rank the parent like the scan CTAs (no share of the scatter)
+        RegRows rr;
+        partition_redundant<NT>(a, D, rr, ps, a.nchunks);
+        set_children(a, D, kid);
       } else {
-        if (threadIdx.x == 0) D.tot[0] = D.tot[1] = D.tot[2] = D.tot[3] = 0.0;  // not used here
+        if (threadIdx.x == 0) {
+          D.nl_loc = D.nl;  // one rank: the split's counts are this rank's
+          D.tot[0] = D.tot[1] = D.tot[2] = D.tot[3] = 0.0;  // not used here
+        }
         __syncthreads();
         set_children(a, D, kid);
       }
@@ -1180,6 +1415,9 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
         }
         stamp(a, it, 3);
         grid_sync(a);
+      } else if (D.path == kNoHist) {
+        if (a.nranks > 1)
+          for (int c = blockIdx.x; c < a.nchunks; c += gridDim.x) exchange_totals_chunk<NT>(a, D, c);
       } else if (D.path == kSmem) {
         hist_smem<BITS, K, NT>(a, D, smem);
         stamp(a, it, 2);
@@ -1196,6 +1434,13 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
     stamp(a, it, 6);
     pick<NT>(a, it + 1, D.left_id, kid, D);
     stamp(a, it, 5);
+  }
+  if (a.nranks > 1 && blockIdx.x == 0 && threadIdx.x == 0) {
+    // done handshake: no rank starts the next tree (and overwrites a block)
+    // before every rank has finished reading this tree's blocks
+    __threadfence_system();
+    st_release_sys(a.xown, a.gen);
+    for (int r = 0; r < a.nranks; ++r) wait_flag(a, a.xpeer[r], a.gen);
   }
 }
 
@@ -1264,7 +1509,7 @@ GrowGeom grow_geometry(const PersistentGrowArgs& h, int device) {
   g.gb = gb;
   g.wpg = warps / gb;
   g.nblocks = (h.num_groups + gb - 1) / gb;
-  g.ctas = sm_count(device);
+  g.ctas = h.ctas > 0 ? std::min(h.ctas, sm_count(device)) : sm_count(device);
   // scan chunks: >= ceil(d / CTAs) features, <= 2048 staged cells
   const int max_f = std::max(1, 2048 / h.k);  // staged cells per chunk
   g.fchunk = std::max(1, std::min(max_f, (h.d + g.ctas - 1) / g.ctas));
@@ -1287,6 +1532,12 @@ size_t grow_nodes_bytes(int num_leaves) {
 }
 
 size_t grow_root_split_offset() { return offsetof(NodeDev, best); }
+
+size_t grow_exchange_doubles(const PersistentGrowArgs& h, int device) {
+  const GrowGeom g = grow_geometry(h, device);
+  const size_t block = kXBlockHeader + static_cast<size_t>(3) * g.fchunk * h.k;
+  return kXHeader + static_cast<size_t>(2) * g.nchunks * block;
+}
 
 size_t grow_scratch_bytes(const PersistentGrowArgs& h, int device) {
   const GrowGeom g = grow_geometry(h, device);
@@ -1359,6 +1610,20 @@ void launch_grow_persistent(const PersistentGrowArgs& h, int device, cudaStream_
   a.nchunks = g.nchunks;
   a.timeout_cycles = 4000000000LL;  // ~2 s: a hung barrier becomes an error, not a hang
   a.prof = h.prof;
+  a.nranks = std::max(1, h.nranks);
+  a.debug = std::getenv("HBG_GROW_DEBUG") != nullptr;
+  a.rank = h.rank;
+  require(a.nranks <= kMaxRanks, "at most 8 row shards exchange through peer memory");
+  if (a.nranks > 1) {
+    require(h.xown != nullptr, "row sharding needs the exchange areas");
+    a.xown = h.xown;
+    for (int r = 0; r < a.nranks; ++r) {
+      require(h.xpeer[r] != nullptr, "exchange area of a rank not attached");
+      a.xpeer[r] = h.xpeer[r];
+    }
+    a.xblock = kXBlockHeader + static_cast<size_t>(3) * g.fchunk * h.k;
+    a.gen = h.gen;
+  }
   unsigned char* p = static_cast<unsigned char*>(h.scratch);
   auto take = [&](size_t n) {
     unsigned char* q = p;
@@ -1381,13 +1646,19 @@ void launch_grow_persistent(const PersistentGrowArgs& h, int device, cudaStream_
           "grow scratch layout");
   HBG_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned), s));
   HBG_CUDA(cudaMemsetAsync(a.picked, 0, max_nodes * sizeof(int), s));
-  HBG_CUDA(cudaMemsetAsync(a.counts, 0, 4 * sizeof(int), s));
+  HBG_CUDA(cudaMemsetAsync(a.counts, 0, 8 * sizeof(int), s));
   void* fn = grow_fn(h.bits, g.k_alloc);
   int occ = 0;
   HBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, g.nt, g.smem));
   require(occ >= 1, "tree grower kernel cannot be resident");
   void* args[] = {&a};
-  HBG_CUDA(cudaLaunchCooperativeKernel(fn, dim3(g.ctas), dim3(g.nt), args, g.smem, s));
+  if (g.ctas == sm_count(device)) {
+    HBG_CUDA(cudaLaunchCooperativeKernel(fn, dim3(g.ctas), dim3(g.nt), args, g.smem, s));
+  } else {
+    // a partial grid (several ranks sharing one GPU in tests): a plain launch
+    // of one CTA per SM; every CTA of it is resident while the SMs suffice
+    HBG_CUDA(cudaLaunchKernel(fn, dim3(g.ctas), dim3(g.nt), args, g.smem, s));
+  }
 }
 
 }  // namespace hbg

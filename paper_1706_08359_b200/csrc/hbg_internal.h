@@ -184,7 +184,14 @@ struct PersistentGrowArgs {
   int64_t min_data;
   double lambda;
   unsigned long long* prof;  // optional phase stamps (HBG_GROW_PROFILE)
+  int ctas;                  // 0: one CTA per SM (cooperative launch)
+  // row sharding through peer memory (nranks > 1)
+  int nranks, rank;
+  double* xown;
+  const double* xpeer[8];
+  unsigned long long gen;
 };
+size_t grow_exchange_doubles(const PersistentGrowArgs& a, int device);
 size_t grow_nodes_bytes(int num_leaves);
 size_t grow_root_split_offset();
 size_t grow_scratch_bytes(const PersistentGrowArgs& a, int device);

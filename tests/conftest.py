@@ -10,6 +10,12 @@ import sys
 
 import pytest
 
+# Several "ranks" sharing the one GPU of the tests run persistent grids on
+# different streams that must execute concurrently (they exchange through
+# peer memory); with the default 8 hardware work queues two streams can share
+# a queue and serialise. Must be set before the CUDA context exists.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if REPO not in sys.path:
     sys.path.insert(0, REPO)

@@ -10,6 +10,7 @@ sharded trees must be identical on both ranks and equal the reference's tree
 on the unsharded data. hbg_comm_allreduce (NCCL) plugs into the same hook.
 """
 import ctypes as C
+import os
 import threading
 
 import numpy as np
@@ -135,3 +136,63 @@ def test_nccl_comm_single_rank_tree(hbg, oracle, monkeypatch):
         assert (c[1][key] == a[1][key]).all(), key
     assert np.allclose(c[1]["value"], a[1]["value"], rtol=1e-9, atol=1e-12)
     assert np.allclose(c[0]["gain"], a[0]["gain"], rtol=1e-5)  # histograms: fp32 vs fixed-point rounding
+
+
+@pytest.mark.parametrize("world,rows,d,k,leaves,min_data", [(2, 60000, 28, 64, 63, 60), (3, 50001, 12, 16, 31, 100),
+                                                           (2, 30000, 9, 256, 31, 80), (2, 200000, 28, 64, 255, 200)])
+def test_peer_exchange_sharded_tree_equals_reference(hbg, oracle, world, rows, d, k, leaves, min_data):
+    """Row sharding INSIDE the persistent grower: `world` ranks as threads on
+    one GPU, each a partial grid (SMs / world CTAs) over its own row shard,
+    exchanging the smaller child's histogram chunks and the partition totals
+    through each other's exchange areas (hbg_peer_attach; across processes the
+    same areas are mapped with CUDA IPC). Trees identical on every rank and
+    equal to the reference's tree on the unsharded data."""
+    import torch
+
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    cols = oracle.gen_synthetic_bins(rows, d, k, 6)
+    g, h = oracle.gen_grad_hess(rows, 6)
+    g = g + 0.3 * (cols[1].astype(np.float64) > k // 2)
+    # uneven shards: rank r gets a different share
+    cuts = [0] + [int(rows * (r + 1) * (r + 2) / (world * (world + 1))) for r in range(world)]
+    shards = [np.ascontiguousarray(cols[:, cuts[r]:cuts[r + 1]]) for r in range(world)]
+    dss = [hbg.Dataset(shards[r], k) for r in range(world)]  # consecutive stream creation
+    ctas = int(os.environ.get("HBG_TEST_CTAS", sms // world))  # the ranks split the SMs
+    peers = [hbg.Peer(dss[r], world, r, ctas=ctas) for r in range(world)]
+    grads = [(torch.from_numpy(g[cuts[r]:cuts[r + 1]].astype(np.float32)).cuda(),
+              torch.from_numpy(h[cuts[r]:cuts[r + 1]].astype(np.float32)).cuda()) for r in range(world)]
+    for p in peers:
+        for q in peers:
+            if q is not p:
+                p.attach(q)
+    torch.cuda.synchronize()
+    results = [None] * world
+    errors = []
+
+    def run(r):
+        try:
+            # each rank on its dataset's own stream: created consecutively, so
+            # on distinct hardware queues and the ranks' grids run concurrently
+            for _ in range(2):  # two trees: the generation tags and the done handshake
+                results[r] = dss[r].grow_tree_peer(grads[r][0], grads[r][1], peers[r], leaves, min_data, 0.0,
+                                                   dss[r].stream())
+        except Exception as ex:  # surfaced below
+            errors.append(ex)
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for p in peers:
+        p.close()
+    for ds in dss:
+        ds.close()
+    assert not errors, errors
+    for r in range(1, world):
+        assert results[r][0].tobytes() == results[0][0].tobytes(), r  # identical split logs on every rank
+        assert results[r][1].tobytes() == results[0][1].tobytes(), r
+    want_log, want_nodes = oracle.grow_tree(cols, k, g, h, leaves, min_data, 0.0, 64)
+    from test_gpu_parity import _assert_same_tree
+
+    assert _assert_same_tree(results[0][0], results[0][1], want_log, want_nodes) == len(want_log)
