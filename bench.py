@@ -397,13 +397,48 @@ def run_hbg(args):
             ds16.close()
         result["variants"] = var
     # --- sec/tree: device-resident 255-leaf best-first tree (grow_tree semantics);
-    # row-sharded over the ranks with the NCCL hook when N > 1
+    # row-sharded over the ranks when N > 1: the per-split histogram exchange
+    # runs inside the persistent grower over NVLink peer memory (CUDA IPC
+    # mappings of every rank's exchange area); the NCCL-hook host loop is the
+    # other sharded path, used only if the peer mapping is unavailable
     if not args.no_tree:
+        peer = None
+        tree_path = "persistent kernel, single rank"
+        if comm is not None:
+            try:
+                peer = hbg.Peer(ds, world, rank, 0, args.num_leaves)
+                handles = [None] * world
+                dist.all_gather_object(handles, peer.ipc_handle())
+                for r in range(world):
+                    if r != rank:
+                        peer.open(r, handles[r])
+                tree_path = "persistent kernel, in-kernel peer-memory histogram exchange (NVLink)"
+            except Exception as e:  # noqa: BLE001 — reported in the JSON line
+                if peer is not None:
+                    peer.close()
+                peer = None
+                tree_path = f"host loop + NCCL allreduce hook (peer mapping unavailable: {str(e)[:80]})"
+
         def grow():
             if comm is None:
                 return ds.grow_tree(tg, th, args.num_leaves, 1, 0.0, sp)
+            if peer is not None:
+                return ds.grow_tree_peer(tg, th, peer, args.num_leaves, 1, 0.0, sp)
             return ds.grow_tree_sharded(tg, th, comm.allreduce_fn, comm.handle, args.num_leaves, 1, 0.0, sp)
 
+        if peer is not None:  # warm-up through the peer path; every rank falls back together on failure
+            ok = torch.ones(1, device=dev)
+            try:
+                grow()
+            except Exception as e:  # noqa: BLE001 — reported in the JSON line
+                ok.zero_()
+                tree_path = f"host loop + NCCL allreduce hook (peer path failed: {str(e)[:80]})"
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if ok.item() == 0:
+                peer.close()
+                peer = None
+                if "host loop" not in tree_path:
+                    tree_path = "host loop + NCCL allreduce hook (peer path failed on another rank)"
         log, _ = grow()  # warm-up (workspace)
         ds.kernel_time()
         ds.set_profiling(True)
@@ -430,7 +465,10 @@ def run_hbg(args):
             "hist_kernel_ms_per_tree": km / args.trees,
             "rows_features_per_s_built": built * d / t_tree,
             "note": "root + smaller child of every split (larger by subtraction); all splits in one persistent cooperative kernel (grow_persistent.cu)",
+            "path": tree_path,
         }
+        if peer is not None:
+            peer.close()
         if comm is None:
             # end to end through the whole-tree drop-in (hbg_grow_tree_host):
             # host fp64 g/h (pinned) in, split log + nodes out, H2D inside
