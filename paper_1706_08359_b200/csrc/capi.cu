@@ -529,13 +529,15 @@ PersistentGrowArgs grow_workspace(hbg_dataset* ds, const hbg_grow_params& P, int
   a.split_log = static_cast<hbg_split*>(ds->grow_log.get(static_cast<size_t>(max_nodes) * sizeof(hbg_split)));
   a.tree = static_cast<hbg_tree_node*>(ds->grow_tree.get(static_cast<size_t>(max_nodes) * sizeof(hbg_tree_node)));
   a.counts = static_cast<int*>(ds->grow_counts.get(8 * sizeof(int)));
-  a.scratch = ds->grow_scratch.get(grow_scratch_bytes(a, L.device));
+  a.num_leaves = P.num_leaves;  // (sizes the scratch below)
+  a.min_data = P.min_data_in_leaf;
+  a.lambda = P.lambda;
+  a.scratch_bytes = grow_scratch_bytes(a, L.device);
+  a.scratch = ds->grow_scratch.get(a.scratch_bytes);
+  a.scratch_bytes = ds->grow_scratch.bytes;
   a.acc = static_cast<unsigned long long*>(ds->small_acc.get(small_hist_acc_bytes(d, k)));
   a.exps = static_cast<int*>(ds->small_exps.get(16));
   a.root_totals = static_cast<double*>(ds->grow_root.get(4 * sizeof(double)));
-  a.num_leaves = P.num_leaves;
-  a.min_data = P.min_data_in_leaf;
-  a.lambda = P.lambda;
   ds->part_scratch.get(gather_scratch_doubles(N) * sizeof(double) + 64);
   if (N > 0 && d > 0) {  // the root histogram's partials (build_device)
     const HistPlan plan = plan_histogram(L.bits_per_bin, L.max_bin, L.num_groups, N, L.device);

@@ -46,6 +46,12 @@ using namespace dev;
 
 constexpr int kItems = 8;               // parent rows per thread in the small-parent path
 constexpr int kMaxRanks = 8;            // row shards exchanging through peer memory
+// Data every CTA reads right after a barrier (the per-chunk winners, the node
+// gains and pick stamps) is written kRep times and CTA b reads copy b % kRep:
+// 148 SMs requesting the same L2 line serialise in its slice (a 2 KB
+// broadcast read measured ~700 cycles vs 286 for one reader,
+// microbench/latency.cu).
+constexpr int kRep = 8;
 constexpr int kXHeader = 16;            // doubles before the exchange blocks (done flag)
 constexpr int kXBlockHeader = 16;       // doubles per block before the histogram: flag, totals
 constexpr int64_t kDirectRows = 8192;   // smaller child: direct per-chunk histogram up to this size
@@ -92,8 +98,9 @@ struct GrowArgs {
   float* h[2];
   double* slots;  // node id -> 3*D doubles (SoA grad|hess|count)
   NodeDev* nodes;
-  double* node_gain;  // gain of a node's best split, -1 without one
-  int* picked;        // split index + 1 at which the node was split, 0 = open
+  double* node_gain;  // [kRep][max_nodes] gain of a node's best split, -1 without one
+  int* picked;        // [kRep][max_nodes] split index + 1 at which the node was split, 0 = open
+  int max_nodes;
   hbg_split* split_log;
   hbg_tree_node* tree;
   int* counts;    // [0] num_splits, [1] num_nodes, [2] error
@@ -104,7 +111,7 @@ struct GrowArgs {
   float* part_g;
   float* part_h;
   uint32_t* part_c;
-  Cand* cand;  // [2][nchunks]
+  Cand* cand;  // [kRep][2][nchunks]
   const int* exps;
   const double* root_tot;  // {G, H}
   int64_t root_count;
@@ -167,6 +174,7 @@ __device__ __forceinline__ void set_error(const GrowArgs& a, int e) { atomicCAS(
 __device__ __forceinline__ void grid_sync(const GrowArgs& a) {
   __syncthreads();
   if (threadIdx.x == 0) {
+    __threadfence();  // as cooperative_groups' grid sync: the CTA's writes before the arrival
     const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
     const unsigned old = atom_add_acq_rel(a.bar, inc);
     const long long t0 = clock64();
@@ -457,6 +465,7 @@ __device__ void pick(const GrowArgs& a, int i, int kid_l, const Kid* kid, Desc& 
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     const int nnodes = 1 + 2 * i;
+    const int rep = blockIdx.x % kRep;
     int err = lane == 0 ? error_of(a) : 0;
     err = __shfl_sync(0xffffffffu, err, 0);
     unsigned long long hk = 0ull;
@@ -469,8 +478,8 @@ __device__ void pick(const GrowArgs& a, int i, int kid_l, const Kid* kid, Desc& 
 #pragma unroll
         for (int u = 0; u < kU; ++u) {  // loads first, then the compares
           const int n = n0 + u * 32 + lane;
-          gain[u] = n < nnodes ? __ldcg(a.node_gain + n) : -1.0;
-          pk[u] = n < nnodes ? __ldcg(a.picked + n) : 1;
+          gain[u] = n < nnodes ? __ldcg(a.node_gain + rep * a.max_nodes + n) : -1.0;
+          pk[u] = n < nnodes ? __ldcg(a.picked + rep * a.max_nodes + n) : 1;
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
@@ -520,7 +529,7 @@ __device__ void pick(const GrowArgs& a, int i, int kid_l, const Kid* kid, Desc& 
         }
         const int left = 1 + 2 * i, right = 2 + 2 * i;
         if (blockIdx.x == 0) {
-          a.picked[p] = i + 1;
+          for (int q = 0; q < kRep; ++q) a.picked[q * a.max_nodes + p] = i + 1;
           a.split_log[i] = bs;
           a.tree[p] = hbg_tree_node{bs.feature, bs.threshold_bin, left, right, 0.0};
         }
@@ -594,7 +603,7 @@ __device__ void store_children(const GrowArgs& a, const Desc& D, Kid* kid) {
     q.hess = D.tot[2 * c + 1];
     a.tree[id] = hbg_tree_node{-1, -1, -1, -1, leaf_value(q.grad, q.hess, a.lambda)};
     a.nodes[id] = NodeDev{q.begin, q.count, q.gcount, q.grad, q.hess, q.best, q.buf, q.has_best};
-    a.node_gain[id] = q.has_best ? q.best.gain : -1.0;
+    for (int r = 0; r < kRep; ++r) a.node_gain[r * a.max_nodes + id] = q.has_best ? q.best.gain : -1.0;
   }
 }
 
@@ -926,7 +935,7 @@ __device__ void scan_chunk(const GrowArgs& a, double* st, int chunk_cells, int n
         c = Cand{__longlong_as_double(static_cast<long long>(hk)), f, b, base[t], base[chunk_cells + t],
                  static_cast<int64_t>(base[2 * chunk_cells + t])};
       }
-      a.cand[child * a.nchunks + c_idx] = c;
+      for (int r = 0; r < kRep; ++r) a.cand[(r * 2 + child) * a.nchunks + c_idx] = c;
     }
   }
   __syncthreads();
@@ -1075,7 +1084,7 @@ __device__ void winners(const GrowArgs& a, const Desc& D, Kid* kid) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {  // loads first
           const int i = i0 + u * 16 + sub;
-          const Cand* q = a.cand + child * a.nchunks + (i < a.nchunks ? i : 0);
+          const Cand* q = a.cand + ((blockIdx.x % kRep) * 2 + child) * a.nchunks + (i < a.nchunks ? i : 0);
           o[u].gain = i < a.nchunks ? __ldcg(&q->gain) : 0.0;
           o[u].f = __ldcg(&q->f);
           o[u].b = __ldcg(&q->b);
@@ -1324,7 +1333,7 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
     const Kid& r = kid[0];
     a.tree[0] = hbg_tree_node{-1, -1, -1, -1, leaf_value(r.grad, r.hess, a.lambda)};
     a.nodes[0] = NodeDev{0, r.count, r.gcount, r.grad, r.hess, r.best, 0, r.has_best};
-    a.node_gain[0] = r.has_best ? r.best.gain : -1.0;
+    for (int q = 0; q < kRep; ++q) a.node_gain[q * a.max_nodes] = r.has_best ? r.best.gain : -1.0;
   }
   __syncthreads();
   pick<NT>(a, 0, 0, kid, D);  // node 0 is "kid_l" (kid[1] is never consulted: nnodes = 1)
@@ -1545,13 +1554,13 @@ size_t grow_scratch_bytes(const PersistentGrowArgs& h, int device) {
   size_t b = 0;
   auto add = [&](size_t n) { b += (n + 255) / 256 * 256; };
   add(sizeof(unsigned));                      // barrier
-  add(max_nodes * sizeof(double));            // node_gain
-  add(max_nodes * sizeof(int));               // picked
+  add(kRep * max_nodes * sizeof(double));     // node_gain
+  add(kRep * max_nodes * sizeof(int));        // picked
   add(static_cast<size_t>(h.num_rows) + 16);  // flags
   add(static_cast<size_t>(g.ctas) * 8);       // cta_left
   add(static_cast<size_t>(g.ctas) * 32);      // cta_sums
   add(g.part_values * 4 * 3);                 // part_g/h/c
-  add(static_cast<size_t>(2 * g.nchunks) * sizeof(Cand));
+  add(static_cast<size_t>(kRep * 2 * g.nchunks) * sizeof(Cand));
   return b;
 }
 
@@ -1632,8 +1641,9 @@ void launch_grow_persistent(const PersistentGrowArgs& h, int device, cudaStream_
   };
   const size_t max_nodes = static_cast<size_t>(std::max(1, 2 * h.num_leaves - 1));
   a.bar = reinterpret_cast<unsigned*>(take(sizeof(unsigned)));
-  a.node_gain = reinterpret_cast<double*>(take(max_nodes * sizeof(double)));
-  a.picked = reinterpret_cast<int*>(take(max_nodes * sizeof(int)));
+  a.max_nodes = static_cast<int>(max_nodes);
+  a.node_gain = reinterpret_cast<double*>(take(kRep * max_nodes * sizeof(double)));
+  a.picked = reinterpret_cast<int*>(take(kRep * max_nodes * sizeof(int)));
   a.flags = take(static_cast<size_t>(h.num_rows) + 16);
   a.cta_left = reinterpret_cast<int64_t*>(take(static_cast<size_t>(g.ctas) * 8));
   a.cta_sums = reinterpret_cast<double*>(take(static_cast<size_t>(g.ctas) * 32));
@@ -1641,11 +1651,11 @@ void launch_grow_persistent(const PersistentGrowArgs& h, int device, cudaStream_
   a.part_g = part;
   a.part_h = part + g.part_values;
   a.part_c = reinterpret_cast<uint32_t*>(part + 2 * g.part_values);
-  a.cand = reinterpret_cast<Cand*>(take(static_cast<size_t>(2 * g.nchunks) * sizeof(Cand)));
-  require(static_cast<size_t>(p - static_cast<unsigned char*>(h.scratch)) <= grow_scratch_bytes(h, device),
-          "grow scratch layout");
+  a.cand = reinterpret_cast<Cand*>(take(static_cast<size_t>(kRep * 2 * g.nchunks) * sizeof(Cand)));
+  require(static_cast<size_t>(p - static_cast<unsigned char*>(h.scratch)) <= h.scratch_bytes,
+          "grow scratch smaller than its layout");
   HBG_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned), s));
-  HBG_CUDA(cudaMemsetAsync(a.picked, 0, max_nodes * sizeof(int), s));
+  HBG_CUDA(cudaMemsetAsync(a.picked, 0, kRep * max_nodes * sizeof(int), s));
   HBG_CUDA(cudaMemsetAsync(a.counts, 0, 8 * sizeof(int), s));
   void* fn = grow_fn(h.bits, g.k_alloc);
   int occ = 0;

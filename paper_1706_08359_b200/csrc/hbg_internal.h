@@ -177,6 +177,7 @@ struct PersistentGrowArgs {
   hbg_tree_node* tree;   // device, 2*num_leaves-1
   int* counts;           // device, 4 ints: num_splits, num_nodes, error
   void* scratch;         // grow_scratch_bytes()
+  size_t scratch_bytes;  // allocated size of `scratch`
   unsigned long long* acc;
   const int* exps;
   const double* root_totals;  // device {G, H}
