@@ -520,7 +520,7 @@ __device__ void pick(const GrowArgs& a, int i, int kid_l, const Kid* kid, Desc& 
           buf = q.buf;
           bs = q.best;
         } else {
-          const NodeDev* P = a.nodes + p;
+          const NodeDev* P = a.nodes + rep * a.max_nodes + p;
           begin = __ldcg(&P->begin);
           count = __ldcg(&P->count);
           gcount = __ldcg(&P->gcount);
@@ -595,15 +595,33 @@ __device__ void set_children(const GrowArgs& a, const Desc& D, Kid* kid) {
 // CTA 0: the children's leaf values and persistent records (read by later
 // picks, after at least one more barrier), from the global totals.
 __device__ void store_children(const GrowArgs& a, const Desc& D, Kid* kid) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  for (int c = 0; c < 2; ++c) {
-    const int id = c == 0 ? D.left_id : D.right_id;
-    Kid& q = kid[c];
-    q.grad = D.tot[2 * c];
-    q.hess = D.tot[2 * c + 1];
-    a.tree[id] = hbg_tree_node{-1, -1, -1, -1, leaf_value(q.grad, q.hess, a.lambda)};
-    a.nodes[id] = NodeDev{q.begin, q.count, q.gcount, q.grad, q.hess, q.best, q.buf, q.has_best};
-    for (int r = 0; r < kRep; ++r) a.node_gain[r * a.max_nodes + id] = q.has_best ? q.best.gain : -1.0;
+  if (blockIdx.x != 0) return;  // uniform per CTA
+  __shared__ NodeDev rec[2];
+  __shared__ int ids[2];
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < 2; ++c) {
+      const int id = c == 0 ? D.left_id : D.right_id;
+      Kid& q = kid[c];
+      q.grad = D.tot[2 * c];
+      q.hess = D.tot[2 * c + 1];
+      a.tree[id] = hbg_tree_node{-1, -1, -1, -1, leaf_value(q.grad, q.hess, a.lambda)};
+      rec[c] = NodeDev{q.begin, q.count, q.gcount, q.grad, q.hess, q.best, q.buf, q.has_best};
+      ids[c] = id;
+    }
+  }
+  __syncthreads();
+  // every replica, written by the whole CTA (one thread would serialise
+  // 2 x kRep x 128 B of stores on CTA 0's critical path)
+  constexpr int W = static_cast<int>(sizeof(NodeDev) / 8);
+  static_assert(sizeof(NodeDev) % 8 == 0, "NodeDev is copied in 8-byte words");
+  for (int t = threadIdx.x; t < 2 * kRep * W; t += blockDim.x) {
+    const int c = t / (kRep * W), r = (t / W) % kRep, w = t % W;
+    reinterpret_cast<double*>(a.nodes + static_cast<size_t>(r) * a.max_nodes + ids[c])[w] =
+        reinterpret_cast<const double*>(&rec[c])[w];
+  }
+  if (threadIdx.x < 2 * kRep) {
+    const int c = threadIdx.x / kRep, r = threadIdx.x % kRep;
+    a.node_gain[static_cast<size_t>(r) * a.max_nodes + ids[c]] = rec[c].has_best ? rec[c].best.gain : -1.0;
   }
 }
 
@@ -1332,7 +1350,8 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const Kid& r = kid[0];
     a.tree[0] = hbg_tree_node{-1, -1, -1, -1, leaf_value(r.grad, r.hess, a.lambda)};
-    a.nodes[0] = NodeDev{0, r.count, r.gcount, r.grad, r.hess, r.best, 0, r.has_best};
+    const NodeDev rec{0, r.count, r.gcount, r.grad, r.hess, r.best, 0, r.has_best};
+    for (int q = 0; q < kRep; ++q) a.nodes[q * a.max_nodes] = rec;
     for (int q = 0; q < kRep; ++q) a.node_gain[q * a.max_nodes] = r.has_best ? r.best.gain : -1.0;
   }
   __syncthreads();
@@ -1536,8 +1555,8 @@ GrowGeom grow_geometry(const PersistentGrowArgs& h, int device) {
 
 }  // namespace
 
-size_t grow_nodes_bytes(int num_leaves) {
-  return static_cast<size_t>(std::max(1, 2 * num_leaves - 1)) * sizeof(NodeDev);
+size_t grow_nodes_bytes(int num_leaves) {  // kRep replicas; replica 0 first
+  return static_cast<size_t>(kRep) * std::max(1, 2 * num_leaves - 1) * sizeof(NodeDev);
 }
 
 size_t grow_root_split_offset() { return offsetof(NodeDev, best); }
