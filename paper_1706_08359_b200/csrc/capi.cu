@@ -641,6 +641,13 @@ void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_h
         if (t[4] && t[8]) acc[6] += (t[8] - t[4]) * 1e-3, ++n[6];
       }
       if (splits == 0) continue;
+      if (cls == 6)  // the shared-memory histogram splits one by one
+        for (int i = 0; i < counts[0]; ++i) {
+          const unsigned long long* t = prof.data() + static_cast<size_t>(i) * 12;
+          if (static_cast<int>(t[7]) != cls) continue;
+          std::fprintf(stderr, "   split %3d parent %9llu small %9llu: partition %7.1f hist %7.1f finish %7.1f us\n", i,
+                       t[10], t[11], (t[1] - t[0]) * 1e-3, (t[2] - t[1]) * 1e-3, (t[3] - t[2]) * 1e-3);
+        }
       std::fprintf(stderr, "grow class %s parent, path %d: %d splits\n", cls >= 4 ? "large" : "small", cls & 3, splits);
       for (int j = 0; j < 7; ++j)
         if (n[j]) std::fprintf(stderr, "   %-13s total %9.1f us avg %7.2f us\n", nm[j], acc[j], acc[j] / n[j]);

@@ -45,6 +45,7 @@ namespace {
 using namespace dev;
 
 constexpr int kItems = 8;               // parent rows per thread in the small-parent path
+constexpr int kPartItems = 8;           // positions per thread per tile, large-parent partition
 constexpr int kMaxRanks = 8;            // row shards exchanging through peer memory
 // Data every CTA reads right after a barrier (the per-chunk winners, the node
 // gains and pick stamps) is written kRep times and CTA b reads copy b % kRep:
@@ -710,15 +711,14 @@ __device__ void partition_redundant(const GrowArgs& a, Desc& D, RegRows& rr, Par
 }
 
 // Large parents: CTA b owns positions [b*chunk, (b+1)*chunk), processed in
-// tiles of NT*kItems positions; thread t holds tile positions
-// [t*kItems, t*kItems + kItems) so its loads are independent and its ranks
-// come from one block scan per tile.
-// Positions per thread per tile: up to kItems, fewer for parents that would
-// otherwise leave CTAs idle.
+// tiles of NT*ipt positions (ipt <= kPartItems). Loads and stores are
+// coalesced: position j*NT + t of a tile belongs to thread t (pass 1), and
+// pass 2 stages the tile in shared memory, ranks it there in position order,
+// and writes the left and the right rows of the tile as two contiguous runs.
 template <int NT>
 __device__ __forceinline__ int part_ipt(int64_t n) {
   const int64_t per = (n + static_cast<int64_t>(gridDim.x) * NT - 1) / (static_cast<int64_t>(gridDim.x) * NT);
-  return static_cast<int>(per < 1 ? 1 : (per > kItems ? kItems : per));
+  return static_cast<int>(per < 1 ? 1 : (per > kPartItems ? kPartItems : per));
 }
 
 template <int NT>
@@ -728,7 +728,8 @@ __device__ __forceinline__ int64_t part_chunk(int64_t n) {
   return (per + tile - 1) / tile * tile;
 }
 
-// Pass 1 (every CTA, its chunk): side flags, left count, fp64 side sums.
+// Pass 1 (every CTA, its chunk): side flags, left count, fp64 side sums
+// (each thread in its fixed position order, then a fixed-order block sum).
 template <int NT>
 __device__ void partition_count(const GrowArgs& a, const Desc& D, PartShared<NT>& ps) {
   const int64_t n = D.count, chunk = part_chunk<NT>(n);
@@ -740,25 +741,28 @@ __device__ void partition_count(const GrowArgs& a, const Desc& D, PartShared<NT>
   long long c = 0;
   const int ipt = part_ipt<NT>(n);
   for (int64_t t0 = s; t0 < e; t0 += static_cast<int64_t>(NT) * ipt) {
-    const int64_t p0 = t0 + static_cast<int64_t>(threadIdx.x) * ipt;
-    const int64_t pe = min(e, p0 + ipt);
-    int32_t r[kItems];
-    float gv[kItems], hv[kItems];
+    int32_t r[kPartItems];
+    float gv[kPartItems], hv[kPartItems];
 #pragma unroll
-    for (int j = 0; j < kItems; ++j) {
-      const bool ok = p0 + j < pe;
-      r[j] = ok ? __ldcg(rin + p0 + j) : 0;
-      gv[j] = ok ? __ldcg(gin + p0 + j) : 0.f;
-      hv[j] = ok ? __ldcg(hin + p0 + j) : 0.f;
+    for (int j = 0; j < kPartItems; ++j) {
+      const int64_t pos = t0 + static_cast<int64_t>(j) * NT + threadIdx.x;
+      const bool ok = j < ipt && pos < e;
+      r[j] = ok ? __ldcg(rin + pos) : 0;
+      gv[j] = ok ? __ldcg(gin + pos) : 0.f;
+      hv[j] = ok ? __ldcg(hin + pos) : 0.f;
     }
-    uint32_t bin[kItems];
+    uint32_t bin[kPartItems];
 #pragma unroll
-    for (int j = 0; j < kItems; ++j) bin[j] = p0 + j < pe ? col_bin(a, r[j], D.feature) : 0u;
+    for (int j = 0; j < kPartItems; ++j) {
+      const int64_t pos = t0 + static_cast<int64_t>(j) * NT + threadIdx.x;
+      bin[j] = j < ipt && pos < e ? col_bin(a, r[j], D.feature) : 0u;
+    }
 #pragma unroll
-    for (int j = 0; j < kItems; ++j) {
-      if (p0 + j >= pe) continue;
+    for (int j = 0; j < kPartItems; ++j) {
+      const int64_t pos = t0 + static_cast<int64_t>(j) * NT + threadIdx.x;
+      if (j >= ipt || pos >= e) continue;
       const bool left = bin[j] <= static_cast<uint32_t>(D.thr);  // tree.cpp:117-123
-      a.flags[p0 + j] = left ? 1 : 0;
+      a.flags[pos] = left ? 1 : 0;
       if (left) {
         ++c;
         v[0] += gv[j];
@@ -778,9 +782,10 @@ __device__ void partition_count(const GrowArgs& a, const Desc& D, PartShared<NT>
 
 // After the barrier (every CTA, redundantly): this CTA's offset among the
 // left rows, the left total and the children's totals (fixed-order sum over
-// CTAs), then pass 2: the stable scatter of this CTA's chunk, tile by tile.
+// CTAs), then pass 2: the stable scatter of this CTA's chunk, tile by tile
+// through shared memory (smem: NT*kPartItems x (row, g, h, flag, slot)).
 template <int NT>
-__device__ void partition_scatter(const GrowArgs& a, Desc& D, PartShared<NT>& ps) {
+__device__ void partition_scatter(const GrowArgs& a, Desc& D, PartShared<NT>& ps, unsigned char* smem) {
   const int G = gridDim.x;
   double v[4] = {0.0, 0.0, 0.0, 0.0};
   long long c = 0;
@@ -809,42 +814,66 @@ __device__ void partition_scatter(const GrowArgs& a, Desc& D, PartShared<NT>& ps
   int32_t* rout = a.rows[D.buf_out] + D.begin;
   float* gout = a.g[D.buf_out] + D.begin;
   float* hout = a.h[D.buf_out] + D.begin;
-  int64_t lrun = s_before;  // left rows before this tile
+  constexpr int kTile = NT * kPartItems;
+  int32_t* srow = reinterpret_cast<int32_t*>(smem);
+  float* sg = reinterpret_cast<float*>(srow + kTile);
+  float* sh = sg + kTile;
+  uint16_t* slot = reinterpret_cast<uint16_t*>(sh + kTile);  // tile position of output slot i
+  uint8_t* sflag = reinterpret_cast<uint8_t*>(slot + kTile);
+  int64_t lrun = s_before, rrun = s - s_before;  // left / right rows before this tile
   const int ipt = part_ipt<NT>(n);
   for (int64_t t0 = s; t0 < e; t0 += static_cast<int64_t>(NT) * ipt) {
-    const int64_t p0 = t0 + static_cast<int64_t>(threadIdx.x) * ipt;
-    const int64_t pe = min(e, p0 + ipt);
-    int32_t r[kItems];
-    float gv[kItems], hv[kItems];
+    const int64_t mrem = e - t0, mcap = static_cast<int64_t>(NT) * ipt;
+    const int m = static_cast<int>(mrem < mcap ? mrem : mcap);
+    // coalesced loads into shared memory
+#pragma unroll
+    for (int j = 0; j < kPartItems; ++j) {
+      const int q = j * NT + threadIdx.x;
+      if (j < ipt && q < m) {
+        srow[q] = __ldcg(rin + t0 + q);
+        sg[q] = __ldcg(gin + t0 + q);
+        sh[q] = __ldcg(hin + t0 + q);
+        sflag[q] = __ldcg(a.flags + t0 + q);
+      }
+    }
+    __syncthreads();
+    // this thread's blocked run of tile positions [t*ipt, t*ipt+ipt): flags, ranks
     uint32_t lf = 0;
     int cl = 0;
+    const int q0 = threadIdx.x * ipt;
 #pragma unroll
-    for (int j = 0; j < kItems; ++j) {
-      const bool ok = p0 + j < pe;
-      const bool left = ok && __ldcg(a.flags + p0 + j);
+    for (int j = 0; j < kPartItems; ++j) {
+      const bool ok = j < ipt && q0 + j < m;
+      const bool left = ok && sflag[q0 + j];
       lf |= left ? 1u << j : 0u;
       cl += left ? 1 : 0;
-      r[j] = ok ? __ldcg(rin + p0 + j) : 0;
-      gv[j] = ok ? __ldcg(gin + p0 + j) : 0.f;
-      hv[j] = ok ? __ldcg(hin + p0 + j) : 0.f;
     }
-    const long long lb = block_excl_scan<NT>(cl, ps);  // left rows of this tile before this thread
-    __shared__ long long s_tile_left;
-    if (threadIdx.x == NT - 1) s_tile_left = lb + cl;
-    int64_t lr = lrun + lb;
+    const long long lb = block_excl_scan<NT>(cl, ps);  // left rows of the tile before q0
+    __shared__ int s_tile_left;
+    if (threadIdx.x == NT - 1) s_tile_left = static_cast<int>(lb + cl);
+    __syncthreads();
+    const int tl = s_tile_left;
+    int lr = static_cast<int>(lb);
 #pragma unroll
-    for (int j = 0; j < kItems; ++j) {
-      const int64_t pos = p0 + j;
-      if (pos >= pe) continue;
+    for (int j = 0; j < kPartItems; ++j) {
+      const int q = q0 + j;
+      if (j >= ipt || q >= m) continue;
       const bool left = (lf >> j) & 1u;
-      const int64_t dst = left ? lr : L + (pos - lr);
-      rout[dst] = r[j];
-      gout[dst] = gv[j];
-      hout[dst] = hv[j];
+      slot[left ? lr : tl + (q - lr)] = static_cast<uint16_t>(q);
       lr += left ? 1 : 0;
     }
     __syncthreads();
-    lrun += s_tile_left;
+    // the tile's left rows -> [lrun, lrun+tl), right rows -> [L+rrun, ...): coalesced
+    for (int i = threadIdx.x; i < m; i += NT) {
+      const int q = slot[i];
+      const int64_t dst = i < tl ? lrun + i : L + rrun + (i - tl);
+      rout[dst] = srow[q];
+      gout[dst] = sg[q];
+      hout[dst] = sh[q];
+    }
+    lrun += tl;
+    rrun += m - tl;
+    __syncthreads();
   }
 }
 
@@ -1363,8 +1392,11 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
     // (with row sharding a rank's part of a parent can be small while the
     // globally smaller child needs the shared-memory histogram)
     const bool small_parent = D.count <= static_cast<int64_t>(kItems) * NT && D.path != kSmem;
-    if (a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0)  // class of this split
+    if (a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {  // class and sizes of this split
       a.prof[static_cast<size_t>(it) * kProfSlots + 7] = (small_parent ? 0 : 4) + D.path;
+      a.prof[static_cast<size_t>(it) * kProfSlots + 10] = static_cast<unsigned long long>(D.count);
+      a.prof[static_cast<size_t>(it) * kProfSlots + 11] = static_cast<unsigned long long>(D.nl < D.nr ? D.nl : D.nr);
+    }
     const bool chunk_cta = static_cast<int>(blockIdx.x) < a.nchunks;
     const int f0 = blockIdx.x * a.fchunk;
     const int nf = chunk_cta ? min(a.fchunk, a.d - f0) : 0;
@@ -1409,7 +1441,7 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
     } else {
       partition_count<NT>(a, D, ps);
       grid_sync(a);
-      partition_scatter<NT>(a, D, ps);
+      partition_scatter<NT>(a, D, ps, smem);
       set_children(a, D, kid);
       stamp(a, it, 1);
       grid_sync(a);
