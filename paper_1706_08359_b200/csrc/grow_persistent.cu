@@ -641,12 +641,28 @@ struct RegRows {
 };
 
 template <int NT>
-__device__ void partition_redundant(const GrowArgs& a, Desc& D, RegRows& rr, PartShared<NT>& ps, int parts) {
+__device__ void partition_redundant(const GrowArgs& a, Desc& D, RegRows& rr, PartShared<NT>& ps, int parts,
+                                    unsigned char* stage /* smem, kItems*NT*12 B */) {
   const int64_t n = D.count;
   const int32_t* rin = a.rows[D.buf_in] + D.begin;
   const float* gin = a.g[D.buf_in] + D.begin;
   const float* hin = a.h[D.buf_in] + D.begin;
   const SplitFeat sf = split_feat(D.feature, a.bits, D.thr);
+  // coalesced loads into shared memory, then each thread takes its blocked
+  // run of positions [t*kItems, t*kItems+kItems) (ranks by one block scan)
+  int32_t* srow = reinterpret_cast<int32_t*>(stage);
+  float* sg = reinterpret_cast<float*>(srow + kItems * NT);
+  float* sh = sg + kItems * NT;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const int q = j * NT + threadIdx.x;
+    if (q < n) {
+      srow[q] = __ldcg(rin + q);
+      sg[q] = __ldcg(gin + q);
+      sh[q] = __ldcg(hin + q);
+    }
+  }
+  __syncthreads();
   const int64_t p0 = static_cast<int64_t>(threadIdx.x) * kItems;
   {
     int64_t nv = n - p0;
@@ -654,15 +670,15 @@ __device__ void partition_redundant(const GrowArgs& a, Desc& D, RegRows& rr, Par
     rr.nvalid = static_cast<int>(nv);
   }
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) rr.row[j] = j < rr.nvalid ? __ldcg(rin + p0 + j) : 0;
+  for (int j = 0; j < kItems; ++j) {
+    const int q = static_cast<int>(p0) + j;
+    rr.row[j] = j < rr.nvalid ? srow[q] : 0;
+    rr.g[j] = j < rr.nvalid ? sg[q] : 0.f;
+    rr.h[j] = j < rr.nvalid ? sh[q] : 0.f;
+  }
   bool lf[kItems];
 #pragma unroll
   for (int j = 0; j < kItems; ++j) lf[j] = j < rr.nvalid && goes_left(a, rr.row[j], sf);
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    rr.g[j] = j < rr.nvalid ? __ldcg(gin + p0 + j) : 0.f;
-    rr.h[j] = j < rr.nvalid ? __ldcg(hin + p0 + j) : 0.f;
-  }
   double v[4] = {0.0, 0.0, 0.0, 0.0};
   long long c = 0;
   rr.left = 0;
@@ -933,6 +949,13 @@ __device__ __forceinline__ void direct_accumulate(const GrowArgs& a, unsigned* a
 // (6 * fchunk * k doubles), then the direct accumulator (20 B per cell).
 __device__ __forceinline__ unsigned* direct_acc(const GrowArgs& a, unsigned char* smem) {
   return reinterpret_cast<unsigned*>(smem + static_cast<size_t>(6) * a.fchunk * a.k * sizeof(double));
+}
+
+// Small-parent partition staging: after the finish phase's staging and the
+// direct accumulator (both live while the partition runs).
+__device__ __forceinline__ unsigned char* part_stage(const GrowArgs& a, unsigned char* smem) {
+  const size_t off = static_cast<size_t>(a.fchunk) * a.k * (6 * sizeof(double) + 20);
+  return smem + (off + 15) / 16 * 16;
 }
 
 __device__ __forceinline__ void zero_direct(const GrowArgs& a, unsigned char* smem, int cells, int NT) {
@@ -1406,7 +1429,7 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
       if (chunk_cta) {
         RegRows rr;
         if (D.path == kDirect) zero_direct(a, smem, nf * a.k, NT);
-        partition_redundant<NT>(a, D, rr, ps, a.nchunks);
+        partition_redundant<NT>(a, D, rr, ps, a.nchunks, part_stage(a, smem));
         set_children(a, D, kid);
         stamp(a, it, 1);
         if (D.path == kDirect) {
@@ -1426,7 +1449,7 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
         // this rank's left count is needed for the children's row ranges:
         // rank the parent like the scan CTAs (no share of the scatter)
         RegRows rr;
-        partition_redundant<NT>(a, D, rr, ps, a.nchunks);
+        partition_redundant<NT>(a, D, rr, ps, a.nchunks, part_stage(a, smem));
         set_children(a, D, kid);
       } else {
         if (threadIdx.x == 0) {
@@ -1577,7 +1600,9 @@ GrowGeom grow_geometry(const PersistentGrowArgs& h, int device) {
   const size_t hist_smem = static_cast<size_t>(g.gb * g.wpg) * ghw + g.gb * cntw;
   // finish: fp64 staging of both children + the direct fixed-point accumulator
   const size_t scan_smem = static_cast<size_t>(g.fchunk) * h.k * (6 * sizeof(double) + 20);
-  g.smem = std::max(hist_smem, scan_smem);
+  const size_t part_smem = (scan_smem + 15) / 16 * 16 + static_cast<size_t>(kItems) * g.nt * 12;  // + staging
+  const size_t large_part_smem = static_cast<size_t>(kPartItems) * g.nt * 15;  // row, g, h, slot, flag
+  g.smem = std::max({hist_smem, part_smem, large_part_smem});
   require(g.ctas <= g.nt, "more CTAs than threads per CTA (per-CTA records are scanned one per thread)");
   require(g.smem <= smem_max, "tree grower shared memory footprint too large");
   const size_t items = static_cast<size_t>(std::max(g.ctas, g.nblocks));
