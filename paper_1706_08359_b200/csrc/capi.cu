@@ -88,6 +88,9 @@ struct hbg_dataset {
   cudaStream_t stream = nullptr;
   // workspace (not re-entrant per handle)
   hbg::DevBuf colbins;  // column-major uint8 bins [feature][row] (the a1 layout), for partitions
+  hbg::DevBuf host_parts;                 // host drop-in: per-chunk histograms
+  cudaStream_t copy_stream = nullptr;     // host drop-in: H2D copies overlapped with the kernels
+  cudaEvent_t chunk_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   hbg::DevBuf part, iota, host_idx, host_gd, host_hd, host_gf, host_hf, host_hist, host_bins;
   int64_t iota_rows = 0;
   // tree growth workspace
@@ -120,8 +123,12 @@ struct hbg_dataset {
       cudaEventDestroy(e.second);
     }
     if (stream) cudaStreamSynchronize(stream);
+    if (copy_stream) cudaStreamSynchronize(copy_stream);
+    for (auto& e : chunk_ev)
+      if (e) cudaEventDestroy(e);
     if (packed) cudaFree(packed);
     if (stream) cudaStreamDestroy(stream);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
   }
 };
 
@@ -813,33 +820,67 @@ int hbg_build_histograms(hbg_dataset* ds, const int32_t* indices, int64_t count,
     const size_t D = static_cast<size_t>(L.num_features) * L.max_bin;
     double* d_hist = static_cast<double*>(ds->host_hist.get(3 * D * sizeof(double) + 8));
     hbg_bin* d_bins = static_cast<hbg_bin*>(ds->host_bins.get(D * sizeof(hbg_bin) + 8));
-    const int32_t* d_idx = nullptr;
-    float *d_gf = nullptr, *d_hf = nullptr;
     if (count > 0) {
       const size_t n = static_cast<size_t>(count);
       double* d_gd = static_cast<double*>(ds->host_gd.get(n * 8));
       double* d_hd = static_cast<double*>(ds->host_hd.get(n * 8));
-      d_gf = static_cast<float*>(ds->host_gf.get(n * 4));
-      d_hf = static_cast<float*>(ds->host_hf.get(n * 4));
-      // g/h first: while the copy engine moves them (PCIe-bound, 16 B/row),
-      // the host checks whether the leaf is one contiguous row range (the
-      // root, or any leaf of an ordered layout). Such a leaf needs no index
-      // upload: the kernel reads the resident iota array at the range's start.
-      HBG_CUDA(cudaMemcpyAsync(d_gd, gradients, n * 8, cudaMemcpyHostToDevice, s));
-      HBG_CUDA(cudaMemcpyAsync(d_hd, hessians, n * 8, cudaMemcpyHostToDevice, s));
+      float* d_gf = static_cast<float*>(ds->host_gf.get(n * 4));
+      float* d_hf = static_cast<float*>(ds->host_hf.get(n * 4));
+      // The PCIe copies (16 B/row of g/h) go on the copy stream in C chunks;
+      // chunk c's conversion and histogram run on the compute stream as soon
+      // as its bytes have landed, so only the last chunk's work is exposed.
+      // The chunk histograms are summed in chunk order (deterministic).
+      const int C = count >= (int64_t{1} << 21) ? 4 : 1;
+      if (!ds->copy_stream) HBG_CUDA(cudaStreamCreateWithFlags(&ds->copy_stream, cudaStreamNonBlocking));
+      for (int c = 0; c < 5; ++c)
+        if (!ds->chunk_ev[c]) HBG_CUDA(cudaEventCreateWithFlags(&ds->chunk_ev[c], cudaEventDisableTiming));
+      HBG_CUDA(cudaEventRecord(ds->chunk_ev[4], s));  // the copy stream starts after prior work on s
+      HBG_CUDA(cudaStreamWaitEvent(ds->copy_stream, ds->chunk_ev[4], 0));
+      auto chunk = [&](int c, int64_t& b, int64_t& e) {
+        b = count * c / C;
+        e = count * (c + 1) / C;
+      };
+      for (int c = 0; c < C; ++c) {
+        int64_t b, e;
+        chunk(c, b, e);
+        const size_t m = static_cast<size_t>(e - b);
+        HBG_CUDA(cudaMemcpyAsync(d_gd + b, gradients + b, m * 8, cudaMemcpyHostToDevice, ds->copy_stream));
+        HBG_CUDA(cudaMemcpyAsync(d_hd + b, hessians + b, m * 8, cudaMemcpyHostToDevice, ds->copy_stream));
+        HBG_CUDA(cudaEventRecord(ds->chunk_ev[c], ds->copy_stream));
+      }
+      // while the copy engine moves them, the host checks whether the leaf is
+      // one contiguous row range (the root, or any leaf of an ordered layout):
+      // such a leaf needs no index upload (the kernel reads the resident iota
+      // at the range's start)
       const int32_t first = indices[0];
+      const int32_t* d_idx;
       if (leaf_is_contiguous(indices, count)) {
         require(first >= 0 && first + count <= L.num_rows, "leaf row index out of range");
         d_idx = identity_rows(ds, first, s);
       } else {
         int32_t* di = static_cast<int32_t*>(ds->host_idx.get(n * 4));
-        HBG_CUDA(cudaMemcpyAsync(di, indices, n * 4, cudaMemcpyHostToDevice, s));
+        HBG_CUDA(cudaMemcpyAsync(di, indices, n * 4, cudaMemcpyHostToDevice, ds->copy_stream));
+        HBG_CUDA(cudaEventRecord(ds->chunk_ev[4], ds->copy_stream));
+        HBG_CUDA(cudaStreamWaitEvent(s, ds->chunk_ev[4], 0));
         d_idx = di;
       }
-      launch_f64_to_f32(d_gd, d_gf, count, s);
-      launch_f64_to_f32(d_hd, d_hf, count, s);
+      double* parts = C > 1 ? static_cast<double*>(ds->host_parts.get(static_cast<size_t>(C) * 3 * D * sizeof(double) + 8))
+                            : d_hist;
+      std::vector<const double*> part_ptrs;
+      for (int c = 0; c < C; ++c) {
+        int64_t b, e;
+        chunk(c, b, e);
+        HBG_CUDA(cudaStreamWaitEvent(s, ds->chunk_ev[c], 0));
+        launch_f64_to_f32(d_gd + b, d_gf + b, e - b, s);
+        launch_f64_to_f32(d_hd + b, d_hf + b, e - b, s);
+        double* hc = parts + static_cast<size_t>(c) * (C > 1 ? 3 * D : 0);
+        build_device(ds, d_idx + b, e - b, d_gf + b, d_hf + b, HBG_GH_LEAF_ALIGNED, hc, s);
+        part_ptrs.push_back(hc);
+      }
+      if (C > 1) launch_reduce_parts(part_ptrs, static_cast<int64_t>(3 * D), d_hist, s);
+    } else {
+      build_device(ds, nullptr, 0, nullptr, nullptr, HBG_GH_LEAF_ALIGNED, d_hist, s);
     }
-    build_device(ds, d_idx, count, d_gf, d_hf, HBG_GH_LEAF_ALIGNED, d_hist, s);
     launch_hist_to_bins(d_hist, static_cast<int64_t>(D), d_bins, s);
     if (D > 0) HBG_CUDA(cudaMemcpyAsync(out, d_bins, D * sizeof(hbg_bin), cudaMemcpyDeviceToHost, s));
     HBG_CUDA(cudaStreamSynchronize(s));
