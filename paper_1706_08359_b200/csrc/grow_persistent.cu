@@ -56,6 +56,7 @@ constexpr int kRep = 8;
 constexpr int kXHeader = 16;            // doubles before the exchange blocks (done flag)
 constexpr int kXBlockHeader = 16;       // doubles per block before the histogram: flag, totals
 constexpr int64_t kDirectRows = 8192;   // smaller child: direct per-chunk histogram up to this size
+constexpr int64_t kDirectBudget = 16384;  // ... and up to this many (row, feature) updates per scan CTA
 
 template <int K>
 __host__ __device__ constexpr int grow_threads() {
@@ -561,7 +562,11 @@ __device__ void pick(const GrowArgs& a, int i, int kid_l, const Kid* kid, Desc& 
         D.rsplit = scan && splittable(nr, a.min_data);
         D.small_is_left = nl <= nr;
         const int64_t ns = nl <= nr ? nl : nr;
-        D.path = !(D.lsplit || D.rsplit) ? kNoHist : (ns <= kDirectRows ? kDirect : kSmem);
+        // direct per-chunk accumulation costs ns * fchunk shared-memory
+        // updates per scan CTA; beyond the budget the whole grid shares the
+        // work through the shared-memory histogram
+        const bool direct = ns <= kDirectRows && ns * a.fchunk <= kDirectBudget;
+        D.path = !(D.lsplit || D.rsplit) ? kNoHist : (direct ? kDirect : kSmem);
         if (D.path == kSmem) {
           // row segments x slice-group blocks ~ one item per CTA, >= 2 tiles per warp
           const int64_t min_rows = static_cast<int64_t>(a.wpg) * 32 * 2 * a.rpl;
