@@ -761,9 +761,10 @@ __device__ void partition_count(const GrowArgs& a, const Desc& D, PartShared<NT>
   double v[4] = {0.0, 0.0, 0.0, 0.0};
   long long c = 0;
   const int ipt = part_ipt<NT>(n);
-  for (int64_t t0 = s; t0 < e; t0 += static_cast<int64_t>(NT) * ipt) {
-    int32_t r[kPartItems];
-    float gv[kPartItems], hv[kPartItems];
+  const int64_t step = static_cast<int64_t>(NT) * ipt;
+  // software pipeline: tile t+1's (row, g, h) loads are in flight while tile
+  // t's bins (dependent on its rows) are fetched and its flags written
+  auto load = [&](int64_t t0, int32_t(&r)[kPartItems], float(&gv)[kPartItems], float(&hv)[kPartItems]) {
 #pragma unroll
     for (int j = 0; j < kPartItems; ++j) {
       const int64_t pos = t0 + static_cast<int64_t>(j) * NT + threadIdx.x;
@@ -772,12 +773,20 @@ __device__ void partition_count(const GrowArgs& a, const Desc& D, PartShared<NT>
       gv[j] = ok ? __ldcg(gin + pos) : 0.f;
       hv[j] = ok ? __ldcg(hin + pos) : 0.f;
     }
+  };
+  int32_t r[kPartItems];
+  float gv[kPartItems], hv[kPartItems];
+  load(s, r, gv, hv);
+  for (int64_t t0 = s; t0 < e; t0 += step) {
     uint32_t bin[kPartItems];
 #pragma unroll
     for (int j = 0; j < kPartItems; ++j) {
       const int64_t pos = t0 + static_cast<int64_t>(j) * NT + threadIdx.x;
       bin[j] = j < ipt && pos < e ? col_bin(a, r[j], D.feature) : 0u;
     }
+    int32_t r2[kPartItems];
+    float g2[kPartItems], h2[kPartItems];
+    load(t0 + step, r2, g2, h2);
 #pragma unroll
     for (int j = 0; j < kPartItems; ++j) {
       const int64_t pos = t0 + static_cast<int64_t>(j) * NT + threadIdx.x;
@@ -792,6 +801,12 @@ __device__ void partition_count(const GrowArgs& a, const Desc& D, PartShared<NT>
         v[2] += gv[j];
         v[3] += hv[j];
       }
+    }
+#pragma unroll
+    for (int j = 0; j < kPartItems; ++j) {
+      r[j] = r2[j];
+      gv[j] = g2[j];
+      hv[j] = h2[j];
     }
   }
   block_sum_4d1<NT>(v, c, ps);
@@ -836,36 +851,68 @@ __device__ void partition_scatter(const GrowArgs& a, Desc& D, PartShared<NT>& ps
   float* gout = a.g[D.buf_out] + D.begin;
   float* hout = a.h[D.buf_out] + D.begin;
   constexpr int kTile = NT * kPartItems;
-  int32_t* srow = reinterpret_cast<int32_t*>(smem);
-  float* sg = reinterpret_cast<float*>(srow + kTile);
-  float* sh = sg + kTile;
-  uint16_t* slot = reinterpret_cast<uint16_t*>(sh + kTile);  // tile position of output slot i
-  uint8_t* sflag = reinterpret_cast<uint8_t*>(slot + kTile);
-  int64_t lrun = s_before, rrun = s - s_before;  // left / right rows before this tile
+  // two stage buffers (row, g, h, flag) + the output slot map; tile t+1 is
+  // loaded into registers while tile t is ranked and written out
+  struct Stage {
+    int32_t* row;
+    float* g;
+    float* h;
+    uint8_t* flag;
+  };
+  auto stage_of = [&](int b) {  // buffer b of the two (no local-memory array of pointers)
+    Stage st;
+    st.row = reinterpret_cast<int32_t*>(smem + static_cast<size_t>(b) * kTile * 13);
+    st.g = reinterpret_cast<float*>(st.row + kTile);
+    st.h = st.g + kTile;
+    st.flag = reinterpret_cast<uint8_t*>(st.h + kTile);
+    return st;
+  };
+  uint16_t* slot = reinterpret_cast<uint16_t*>(smem + static_cast<size_t>(2) * kTile * 13);  // output slot -> tile position
   const int ipt = part_ipt<NT>(n);
-  for (int64_t t0 = s; t0 < e; t0 += static_cast<int64_t>(NT) * ipt) {
-    const int64_t mrem = e - t0, mcap = static_cast<int64_t>(NT) * ipt;
-    const int m = static_cast<int>(mrem < mcap ? mrem : mcap);
-    // coalesced loads into shared memory
+  const int64_t step = static_cast<int64_t>(NT) * ipt;
+  int32_t rr[kPartItems];
+  float rg[kPartItems], rh[kPartItems];
+  uint8_t rf[kPartItems];
+  auto fetch = [&](int64_t t0) {  // coalesced: tile position j*NT + t
+#pragma unroll
+    for (int j = 0; j < kPartItems; ++j) {
+      const int64_t q = static_cast<int64_t>(j) * NT + threadIdx.x;
+      const bool ok = j < ipt && t0 + q < e;
+      rr[j] = ok ? __ldcg(rin + t0 + q) : 0;
+      rg[j] = ok ? __ldcg(gin + t0 + q) : 0.f;
+      rh[j] = ok ? __ldcg(hin + t0 + q) : 0.f;
+      rf[j] = ok ? __ldcg(a.flags + t0 + q) : 0;
+    }
+  };
+  auto stage = [&](const Stage& b) {
 #pragma unroll
     for (int j = 0; j < kPartItems; ++j) {
       const int q = j * NT + threadIdx.x;
-      if (j < ipt && q < m) {
-        srow[q] = __ldcg(rin + t0 + q);
-        sg[q] = __ldcg(gin + t0 + q);
-        sh[q] = __ldcg(hin + t0 + q);
-        sflag[q] = __ldcg(a.flags + t0 + q);
+      if (j < ipt) {
+        b.row[q] = rr[j];
+        b.g[q] = rg[j];
+        b.h[q] = rh[j];
+        b.flag[q] = rf[j];
       }
     }
-    __syncthreads();
-    // this thread's blocked run of tile positions [t*ipt, t*ipt+ipt): flags, ranks
+  };
+  int64_t lrun = s_before, rrun = s - s_before;  // left / right rows before this tile
+  fetch(s);
+  stage(stage_of(0));
+  __syncthreads();
+  int buf = 0;
+  for (int64_t t0 = s; t0 < e; t0 += step, buf ^= 1) {
+    const int64_t mrem = e - t0;
+    const int m = static_cast<int>(mrem < step ? mrem : step);
+    if (t0 + step < e) fetch(t0 + step);  // next tile in flight
+    const Stage cb = stage_of(buf);
+    // this thread's blocked run of tile positions [t*ipt, t*ipt+ipt): ranks
     uint32_t lf = 0;
     int cl = 0;
     const int q0 = threadIdx.x * ipt;
 #pragma unroll
     for (int j = 0; j < kPartItems; ++j) {
-      const bool ok = j < ipt && q0 + j < m;
-      const bool left = ok && sflag[q0 + j];
+      const bool left = j < ipt && q0 + j < m && cb.flag[q0 + j];
       lf |= left ? 1u << j : 0u;
       cl += left ? 1 : 0;
     }
@@ -888,12 +935,13 @@ __device__ void partition_scatter(const GrowArgs& a, Desc& D, PartShared<NT>& ps
     for (int i = threadIdx.x; i < m; i += NT) {
       const int q = slot[i];
       const int64_t dst = i < tl ? lrun + i : L + rrun + (i - tl);
-      rout[dst] = srow[q];
-      gout[dst] = sg[q];
-      hout[dst] = sh[q];
+      rout[dst] = cb.row[q];
+      gout[dst] = cb.g[q];
+      hout[dst] = cb.h[q];
     }
     lrun += tl;
     rrun += m - tl;
+    if (t0 + step < e) stage(stage_of(buf ^ 1));
     __syncthreads();
   }
 }
@@ -1606,7 +1654,7 @@ GrowGeom grow_geometry(const PersistentGrowArgs& h, int device) {
   // finish: fp64 staging of both children + the direct fixed-point accumulator
   const size_t scan_smem = static_cast<size_t>(g.fchunk) * h.k * (6 * sizeof(double) + 20);
   const size_t part_smem = (scan_smem + 15) / 16 * 16 + static_cast<size_t>(kItems) * g.nt * 12;  // + staging
-  const size_t large_part_smem = static_cast<size_t>(kPartItems) * g.nt * 15;  // row, g, h, slot, flag
+  const size_t large_part_smem = static_cast<size_t>(kPartItems) * g.nt * (2 * 13 + 2);  // 2 x (row, g, h, flag) + slot
   g.smem = std::max({hist_smem, part_smem, large_part_smem});
   require(g.ctas <= g.nt, "more CTAs than threads per CTA (per-CTA records are scanned one per thread)");
   require(g.smem <= smem_max, "tree grower shared memory footprint too large");
