@@ -1646,9 +1646,9 @@ GrowGeom grow_geometry(const PersistentGrowArgs& h, int device) {
   g.wpg = warps / gb;
   g.nblocks = (h.num_groups + gb - 1) / gb;
   g.ctas = h.ctas > 0 ? std::min(h.ctas, sm_count(device)) : sm_count(device);
-  // scan chunks: >= ceil(d / CTAs) features, <= 2048 staged cells
-  const int max_f = std::max(1, 2048 / h.k);  // staged cells per chunk
-  g.fchunk = std::max(1, std::min(max_f, (h.d + g.ctas - 1) / g.ctas));
+  // scan chunks: one per CTA at most (the direct paths give CTA c chunk c), so
+  // at least ceil(d / CTAs) features each; the staging must fit shared memory
+  g.fchunk = std::max(1, (h.d + g.ctas - 1) / g.ctas);
   g.nchunks = std::max(1, (h.d + g.fchunk - 1) / g.fchunk);
   const size_t hist_smem = static_cast<size_t>(g.gb * g.wpg) * ghw + g.gb * cntw;
   // finish: fp64 staging of both children + the direct fixed-point accumulator
@@ -1657,7 +1657,8 @@ GrowGeom grow_geometry(const PersistentGrowArgs& h, int device) {
   const size_t large_part_smem = static_cast<size_t>(kPartItems) * g.nt * (2 * 13 + 2);  // 2 x (row, g, h, flag) + slot
   g.smem = std::max({hist_smem, part_smem, large_part_smem});
   require(g.ctas <= g.nt, "more CTAs than threads per CTA (per-CTA records are scanned one per thread)");
-  require(g.smem <= smem_max, "tree grower shared memory footprint too large");
+  require(g.smem <= smem_max, "tree grower: features x bins per scan chunk exceed shared memory "
+                              "(too many features for one grid)");
   const size_t items = static_cast<size_t>(std::max(g.ctas, g.nblocks));
   g.part_values = items * g.gb * cells;
   return g;
