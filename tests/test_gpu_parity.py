@@ -466,7 +466,8 @@ def test_grow_tree_matches_reference_golden_split_log(hbg, oracle, grower, monke
 @pytest.mark.parametrize("rows,d,k,leaves,min_data,lam,exact", [
     (30000, 28, 64, 63, 50, 0.0, True), (20000, 10, 256, 31, 100, 1.0, True),
     (50000, 40, 16, 127, 100, 0.0, True), (300000, 28, 64, 255, 200, 0.0, True),
-    (30000, 28, 64, 63, 1, 0.0, False), (3000, 3, 64, 255, 1, 0.0, False)])
+    (30000, 28, 64, 63, 1, 0.0, False), (3000, 3, 64, 255, 1, 0.0, False),
+    (3000, 1300, 256, 15, 100, 0.0, True)])  # > 8 features x 256 bins per scan chunk
 @pytest.mark.parametrize("grower", ["persistent", "host"])
 def test_grow_tree_matches_oracle(hbg, oracle, rows, d, k, leaves, min_data, lam, exact, grower, monkeypatch):
     """Both growers (the persistent one-kernel tree and the host loop,
