@@ -542,7 +542,6 @@ PersistentGrowArgs grow_workspace(hbg_dataset* ds, const hbg_grow_params& P, int
   a.scratch_bytes = grow_scratch_bytes(a, L.device);
   a.scratch = ds->grow_scratch.get(a.scratch_bytes);
   a.scratch_bytes = ds->grow_scratch.bytes;
-  a.acc = static_cast<unsigned long long*>(ds->small_acc.get(small_hist_acc_bytes(d, k)));
   a.exps = static_cast<int*>(ds->small_exps.get(16));
   a.root_totals = static_cast<double*>(ds->grow_root.get(4 * sizeof(double)));
   ds->part_scratch.get(gather_scratch_doubles(N) * sizeof(double) + 64);
@@ -600,7 +599,6 @@ void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_h
     return;
   }
   launch_fixed_scale(a.g[0], a.h[0], N, exps, s);
-  HBG_CUDA(cudaMemsetAsync(a.acc, 0, small_hist_acc_bytes(d, k), s));
   build_device(ds, a.rows[0], N, a.g[0], a.h[0], HBG_GH_LEAF_ALIGNED, slots, s);
   if (!sharded) {  // sharded: the kernel sums the ranks' root histograms first, then scans
     hbg_split* root_split = reinterpret_cast<hbg_split*>(static_cast<char*>(a.nodes) + grow_root_split_offset());

@@ -13,22 +13,26 @@
 //   pick        the open leaf with the largest gain, lowest node id on ties
 //               (the reference's pool order, strict > at tree.cpp:212-218)
 //   partition   partition_leaf (tree.cpp:114-128): stable, left rows first,
-//               into the other ordered buffer. Small parents: every CTA ranks
-//               the whole parent (registers), writes its share of the output;
-//               fp64 child totals (gather_leaf_statistics, tree.cpp:244-246)
-//               in a fixed order. Large parents: per-CTA chunks + one barrier.
-//   histogram   of the SMALLER child only (row a10). <= kDirectRows rows: each
-//               scan CTA accumulates its feature chunk directly (int64 fixed
-//               point in shared memory: deterministic); larger: the
-//               shared-memory rows-in-lanes schedule of hist_kernel over
-//               (segment, slice-group) items + a fixed-order fp64 reduction
+//               into the other ordered buffer. Small parents: the scan CTAs
+//               each rank the whole parent (registers) and write a share of
+//               the output; fp64 child totals (gather_leaf_statistics,
+//               tree.cpp:244-246) in a fixed order. Large parents: per-CTA
+//               chunks in pipelined tiles + one barrier.
+//   histogram   of the SMALLER child only (row a10). Small enough: each scan
+//               CTA accumulates its feature chunk directly (int64 fixed point
+//               in shared memory: deterministic); larger: the shared-memory
+//               rows-in-lanes schedule of hist_kernel over (segment,
+//               slice-group) items + a fixed-order fp64 reduction
+//   exchange    row-sharded (nranks > 1): each scan CTA publishes its chunk of
+//               this rank's smaller-child histogram + totals in peer memory and
+//               sums every rank's, in rank order (see "peer exchange" below)
 //   finish      per feature chunk: larger child = parent - small (every node
 //               owns a slot, no aliasing), both children's split scans
 //               (scan_device.cuh: the reference's fp64 operation order)
 //   barrier     then every CTA reduces the per-chunk winners and picks again
 //
 // Cross-CTA data written inside the kernel is read through L2 (__ldcg); only
-// the packed dataset uses the read-only path.
+// the packed and column-major datasets use the read-only path.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -299,8 +303,6 @@ template <int NT>
 struct PartShared {
   double sd[4][NT / 32];
   long long sc[NT / 32];
-  int wl[NT / 32], wn[NT / 32], ol[NT / 32], on[NT / 32];
-  int tl, tn;
   double tot[4];
   long long cnt;
   long long scan[NT / 32];
@@ -355,39 +357,6 @@ __device__ long long block_excl_scan(long long x, PartShared<NT>& ps) {
   return base + inc - x;
 }
 
-// Per-iteration block ranks of the left / valid ballots.
-template <int NT>
-__device__ __forceinline__ void block_ranks(unsigned lm, unsigned vm, PartShared<NT>& ps) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  constexpr int W = NT / 32;
-  if (lane == 0) {
-    ps.wl[w] = __popc(lm);
-    ps.wn[w] = __popc(vm);
-  }
-  __syncthreads();
-  if (w == 0) {
-    int l = lane < W ? ps.wl[lane] : 0, nn = lane < W ? ps.wn[lane] : 0;
-    int il = l, in = nn;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int x = __shfl_up_sync(0xffffffffu, il, off), y = __shfl_up_sync(0xffffffffu, in, off);
-      if (lane >= off) {
-        il += x;
-        in += y;
-      }
-    }
-    if (lane < W) {
-      ps.ol[lane] = il - l;
-      ps.on[lane] = in - nn;
-    }
-    if (lane == W - 1) {
-      ps.tl = il;
-      ps.tn = in;
-    }
-  }
-  __syncthreads();
-}
-
 struct SplitFeat {
   int feature, thr;
 };
@@ -416,15 +385,6 @@ __device__ __forceinline__ hbg_split load_split(const hbg_split* p) {
 #pragma unroll
   for (int j = 0; j < static_cast<int>(sizeof(hbg_split) / 8); ++j) dst[j] = __ldcg(src + j);
   return s;
-}
-
-__device__ __forceinline__ Cand warp_best(Cand c) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const Cand o = shfl_cand(c, (threadIdx.x & 31) ^ off);
-    if (better(o, c)) c = o;
-  }
-  return c;
 }
 
 // Branch-free warp argmax on a 96-bit key (hi, lo), max wins; every lane

@@ -178,7 +178,6 @@ struct PersistentGrowArgs {
   int* counts;           // device, 4 ints: num_splits, num_nodes, error
   void* scratch;         // grow_scratch_bytes()
   size_t scratch_bytes;  // allocated size of `scratch`
-  unsigned long long* acc;
   const int* exps;
   const double* root_totals;  // device {G, H}
   int num_leaves;
