@@ -467,7 +467,9 @@ def test_grow_tree_matches_reference_golden_split_log(hbg, oracle, grower, monke
     (30000, 28, 64, 63, 50, 0.0, True), (20000, 10, 256, 31, 100, 1.0, True),
     (50000, 40, 16, 127, 100, 0.0, True), (300000, 28, 64, 255, 200, 0.0, True),
     (30000, 28, 64, 63, 1, 0.0, False), (3000, 3, 64, 255, 1, 0.0, False),
-    (3000, 1300, 256, 15, 100, 0.0, True)])  # > 8 features x 256 bins per scan chunk
+    (3000, 1300, 256, 15, 100, 0.0, True),  # > 8 features x 256 bins per scan chunk
+    (40000, 20, 100, 31, 100, 0.5, True), (40000, 33, 10, 31, 100, 0.0, True),  # 128-bin slots; 4-bit, 10 bins
+    (25000, 5, 200, 63, 50, 0.0, True)])
 @pytest.mark.parametrize("grower", ["persistent", "host"])
 def test_grow_tree_matches_oracle(hbg, oracle, rows, d, k, leaves, min_data, lam, exact, grower, monkeypatch):
     """Both growers (the persistent one-kernel tree and the host loop,
