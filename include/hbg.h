@@ -216,6 +216,16 @@ int hbg_peer_handle(hbg_peer* p, uint8_t* out /* HBG_PEER_HANDLE_BYTES */);
 int hbg_peer_open(hbg_peer* p, int32_t peer_rank, const uint8_t* handle);
 int hbg_peer_attach(hbg_peer* p, int32_t peer_rank, const hbg_peer* q);
 int hbg_peer_destroy(hbg_peer* p);
+/* Row-sharded histogram of one leaf (this rank's rows, as
+ * hbg_build_histograms_device) with the cross-rank sum FUSED into the
+ * histogram's reduction kernel over peer memory: every rank's d_hist receives
+ * the bit-identical global histogram (rank-order sum), no separate collective.
+ * Every rank calls it for the same leaf (a rank without rows of it too).
+ * Asynchronous on `stream`; hbg_peer_check (device-wide synchronisation)
+ * reports a rank that never published. */
+int hbg_build_histograms_peer(hbg_dataset* ds, const int32_t* d_indices, int64_t count, const float* d_grad,
+                              const float* d_hess, int32_t gh_mode, double* d_hist, hbg_peer* peer, void* stream);
+int hbg_peer_check(hbg_peer* p);
 int hbg_grow_tree_peer(hbg_dataset* ds, const float* d_grad, const float* d_hess, const hbg_grow_params* params,
                        hbg_peer* peer, hbg_split* split_log, int32_t* num_splits, hbg_tree_node* nodes,
                        int32_t* num_nodes, void* stream);

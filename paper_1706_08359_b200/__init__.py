@@ -134,6 +134,8 @@ EXPORTED_SYMBOLS = (
     "hbg_peer_open",
     "hbg_peer_attach",
     "hbg_peer_destroy",
+    "hbg_build_histograms_peer",
+    "hbg_peer_check",
     "hbg_grow_tree_peer",
     "hbg_comm_get_unique_id",
     "hbg_comm_init",
@@ -192,6 +194,8 @@ def lib() -> C.CDLL:
         L.hbg_peer_open.argtypes = [_P, C.c_int32, _P]
         L.hbg_peer_attach.argtypes = [_P, C.c_int32, _P]
         L.hbg_peer_destroy.argtypes = [_P]
+        L.hbg_build_histograms_peer.argtypes = [_P, _P, C.c_int64, _P, _P, C.c_int32, _P, _P, _P]
+        L.hbg_peer_check.argtypes = [_P]
         L.hbg_grow_tree_peer.argtypes = [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P]
         L.hbg_grow_tree_sharded.argtypes = [_P, _P, _P, _P, ALLREDUCE_FN, _P, _P, _P, _P, _P, _P]
         L.hbg_comm_get_unique_id.argtypes = [_P]
@@ -337,6 +341,13 @@ class Dataset:
     def stream(self) -> int:
         """The dataset's own CUDA stream (cudaStream_t as an int)."""
         return lib().hbg_dataset_stream(self.handle) or 0
+
+    def build_histograms_peer(self, indices, count: int, grad, hess, out, peer: "Peer",
+                              gh_mode: int = HBG_GH_LEAF_ALIGNED, stream=None):
+        """This rank's rows of a leaf; `out` receives the histogram summed over
+        all ranks (the sum fused into the reduction kernel, over peer memory)."""
+        check(lib().hbg_build_histograms_peer(self.handle, _ptr(indices), count, _ptr(grad), _ptr(hess), gh_mode,
+                                              _ptr(out), peer.handle, _ptr(stream)))
 
     def grow_tree_peer(self, grad, hess, peer: "Peer", num_leaves: int = 31, min_data_in_leaf: int = 1,
                        lam: float = 0.0, stream=None):
@@ -513,6 +524,10 @@ class Peer:
     def open(self, peer_rank: int, handle: bytes):
         buf = (C.c_uint8 * Peer.HANDLE_BYTES).from_buffer_copy(handle)
         check(lib().hbg_peer_open(self._h, peer_rank, buf))
+
+    def check(self):
+        """Raise if a peer exchange timed out (synchronises the device)."""
+        check(lib().hbg_peer_check(self._h))
 
     def attach(self, other: "Peer"):
         check(lib().hbg_peer_attach(self._h, other.rank, other._h))

@@ -138,7 +138,10 @@ struct hbg_dataset {
 struct hbg_peer {
   int nranks = 1, rank = 0, device = 0, ctas = 0;
   double* xbuf = nullptr;
-  size_t xdoubles = 0;
+  size_t xdoubles = 0;          // tree-exchange region [0, xdoubles)
+  size_t hoff = 0, hdoubles = 0;  // histogram-exchange region [hoff, hoff + hdoubles)
+  unsigned long long hgen = 0;  // histogram-exchange generation
+  int* error = nullptr;         // device flag: a peer never published
   const double* peers[8] = {nullptr};
   void* opened[8] = {nullptr};  // IPC mappings to close
   unsigned long long gen = 0;   // tree generation
@@ -146,6 +149,7 @@ struct hbg_peer {
     for (void* p : opened)
       if (p) cudaIpcCloseMemHandle(p);
     if (xbuf) cudaFree(xbuf);
+    if (error) cudaFree(error);
   }
 };
 
@@ -246,6 +250,58 @@ void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const fl
     launch_histogram(plan, a, s);
   }
   if (!a.direct) launch_reduce_partials(plan, a, L.num_features, L.max_bin, d_hist, s, parent, sibling);
+}
+
+// Row-sharded histogram of one leaf: this rank's rows, the cross-rank sum
+// fused into the reduction over peer memory (reduce_exchange_kernel); every
+// rank must call it (a rank without rows of the leaf still exchanges).
+void build_device_peer(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const float* d_g, const float* d_h,
+                       int gh_mode, double* d_hist, cudaStream_t s, hbg_peer* peer) {
+  const hbg_layout& L = ds->layout;
+  require(count >= 0, "negative leaf size");
+  require(count <= L.num_rows || d_idx != nullptr, "identity leaf larger than the dataset");
+  require(gh_mode == HBG_GH_LEAF_ALIGNED || gh_mode == HBG_GH_ROW_INDEXED, "bad gh_mode");
+  require(d_hist != nullptr, "null histogram output");
+  require(peer->device == L.device, "exchange area on another device");
+  for (int r = 0; r < peer->nranks; ++r) require(peer->peers[r] != nullptr, "exchange area of a rank not attached");
+  require(count == 0 || (d_g != nullptr && d_h != nullptr), "null gradient/hessian pointer");
+  if (d_idx == nullptr && count > 0) d_idx = identity_rows(ds, 0, s);
+  HistPlan plan = plan_histogram(L.bits_per_bin, L.max_bin, L.num_groups, std::max<int64_t>(count, 1), L.device,
+                                 /*allow_direct=*/false);
+  float* part = static_cast<float*>(ds->part.get(plan.part_values * 12 + 16));
+  HistArgs a{};
+  a.packed = reinterpret_cast<const uint8_t*>(ds->packed);
+  a.row_stride = L.row_stride_bytes;
+  a.idx = d_idx;
+  a.n = count;
+  a.g = d_g;
+  a.h = d_h;
+  a.gh_indexed = gh_mode == HBG_GH_ROW_INDEXED;
+  a.num_groups = L.num_groups;
+  a.gb = plan.gb;
+  a.wpg = plan.wpg;
+  a.nblocks = plan.nblocks;
+  a.seg_len = plan.seg_len;
+  a.part_g = part;
+  a.part_h = part + plan.part_values;
+  a.part_c = reinterpret_cast<uint32_t*>(part + 2 * plan.part_values);
+  a.d = L.num_features;
+  a.max_bin = L.max_bin;
+  if (count > 0) {
+    launch_histogram(plan, a, s);
+  } else {
+    plan.nseg = 0;  // nothing of this rank's; still publish zeros and sum
+  }
+  PeerHistArgs x{};
+  x.nranks = peer->nranks;
+  x.rank = peer->rank;
+  x.xown = peer->xbuf + peer->hoff;
+  for (int r = 0; r < peer->nranks; ++r) x.xpeer[r] = peer->peers[r] + peer->hoff;
+  x.tag = ++peer->hgen;
+  x.parity = static_cast<int>(x.tag & 1);
+  x.error = peer->error;
+  x.timeout_cycles = 4000000000LL;
+  launch_reduce_exchange(plan, a, L.num_features, L.max_bin, d_hist, x, s);
 }
 
 double leaf_value(double g, double h, double lambda) {  // tree.cpp:59-64
@@ -1054,8 +1110,14 @@ int hbg_peer_create(hbg_dataset* ds, int32_t nranks, int32_t rank, int32_t ctas,
     p->device = L.device;
     p->ctas = ctas;
     p->xdoubles = grow_exchange_doubles(a, L.device);
-    HBG_CUDA(cudaMalloc(&p->xbuf, p->xdoubles * sizeof(double)));
-    HBG_CUDA(cudaMemset(p->xbuf, 0, p->xdoubles * sizeof(double)));
+    const int k_alloc = L.bits_per_bin == 4 ? 16 : (L.max_bin <= 64 ? 64 : (L.max_bin <= 128 ? 128 : 256));
+    p->hoff = (p->xdoubles + 31) / 32 * 32;
+    p->hdoubles = hist_exchange_doubles(k_alloc, L.max_bin, L.num_groups);
+    const size_t total = p->hoff + p->hdoubles;
+    HBG_CUDA(cudaMalloc(&p->xbuf, total * sizeof(double)));
+    HBG_CUDA(cudaMemset(p->xbuf, 0, total * sizeof(double)));
+    HBG_CUDA(cudaMalloc(&p->error, sizeof(int)));
+    HBG_CUDA(cudaMemset(p->error, 0, sizeof(int)));
     p->peers[rank] = p->xbuf;
     grow_workspace(ds, *params, ctas);  // reserve: no allocation while the ranks' grids exchange
     HBG_CUDA(cudaDeviceSynchronize());
@@ -1102,6 +1164,30 @@ int hbg_peer_attach(hbg_peer* p, int32_t peer_rank, const hbg_peer* q) {
       else HBG_CUDA(e);
     }
     p->peers[peer_rank] = q->xbuf;
+  });
+}
+
+int hbg_build_histograms_peer(hbg_dataset* ds, const int32_t* d_indices, int64_t count, const float* d_grad,
+                              const float* d_hess, int32_t gh_mode, double* d_hist, hbg_peer* peer, void* stream) {
+  return guarded([&] {
+    check_ds(ds);
+    require(peer != nullptr, "null peer");
+    DeviceGuard dg(ds->layout.device);
+    build_device_peer(ds, d_indices, count, d_grad, d_hess, gh_mode, d_hist, pick(ds, stream), peer);
+  });
+}
+
+int hbg_peer_check(hbg_peer* p) {
+  return guarded([&] {
+    require(p != nullptr, "null peer");
+    DeviceGuard dg(p->device);
+    HBG_CUDA(cudaDeviceSynchronize());  // every stream's exchanges have finished (or timed out)
+    int e = 0;
+    HBG_CUDA(cudaMemcpy(&e, p->error, sizeof e, cudaMemcpyDeviceToHost));
+    if (e != 0) {
+      HBG_CUDA(cudaMemset(p->error, 0, sizeof(int)));
+      throw Error(HBG_ERR_CUDA, "peer histogram exchange timed out (a rank never published)");
+    }
   });
 }
 

@@ -71,7 +71,9 @@ struct HistArgs {
   double* sibling;
 };
 
-HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int device);
+// allow_direct = false: always per-CTA partials + a reduction (the row-sharded
+// path fuses its exchange into that reduction).
+HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int device, bool allow_direct = true);
 
 void launch_histogram(const HistPlan& plan, const HistArgs& args, cudaStream_t s);
 // d_hist = reduced histogram; when `parent` is non-null also writes
@@ -80,6 +82,20 @@ void launch_histogram(const HistPlan& plan, const HistArgs& args, cudaStream_t s
 void launch_reduce_partials(const HistPlan& plan, const HistArgs& args, int num_features,
                             int max_bin, double* d_hist, cudaStream_t s,
                             const double* parent = nullptr, double* sibling = nullptr);
+// Row-sharded histogram with the cross-rank sum fused into the reduction
+// (reduce_exchange_kernel): every rank's exchange region is mapped.
+struct PeerHistArgs {
+  int nranks, rank;
+  double* xown;
+  const double* xpeer[8];
+  unsigned long long tag;
+  int parity;
+  int* error;  // device flag: a peer never published (timeout)
+  long long timeout_cycles;
+};
+size_t hist_exchange_doubles(int k_alloc, int max_bin, int num_groups);
+void launch_reduce_exchange(const HistPlan& plan, const HistArgs& args, int num_features, int max_bin,
+                            double* d_hist, const PeerHistArgs& x, cudaStream_t s);
 // Packs features [f0, f0 + nf) (one 32-feature slice group; d_cols holds
 // their column-major bins) into the group's words of every row.
 void launch_pack(const uint8_t* d_cols, int f0, int nf, int num_features, int64_t num_rows,

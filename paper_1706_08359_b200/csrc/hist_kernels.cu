@@ -275,6 +275,108 @@ __global__ void __launch_bounds__(kReduceWarps * 32) reduce_partials_kernel(
   }
 }
 
+// Row-sharded histogram with the allreduce FUSED into the
+// reduction: block (bin, group) reduces its bin row of this rank's partials
+// (as reduce_partials_kernel), publishes the row in this rank's exchange area
+// (data, fence.sys, flag = tag with release semantics), then reads every
+// rank's row over peer memory (NVLink) and sums them in rank order — every
+// rank ends with the bit-identical global histogram, with no separate
+// collective launch. Rows alternate between two parities per call; a rank
+// starts call c only after its call c-1 read every peer's c-1 rows, which the
+// peers published after finishing their c-2 reads (same parity).
+constexpr int kXRow = 16 + 3 * 32;  // doubles per exchanged row: flag + pad, 32 x (g, h, count)
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const double* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys_u64(double* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Block b handles bin rows b, b + gridDim.x, ... (a small grid: blocks that
+// wait for peers must not keep other kernels off the SMs when ranks share a
+// GPU). Phase 1 publishes all its rows, phase 2 sums every rank's rows.
+constexpr int kXBlocks = 32;
+
+__global__ void __launch_bounds__(kReduceWarps * 32) reduce_exchange_kernel(
+    HistArgs a, int nseg, int k_alloc, int d, int max_bin, int nbins, double* out, PeerHistArgs x) {
+  const int cells = k_alloc * 32;
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const int nrows = nbins * a.num_groups;
+  __shared__ double rg[kReduceWarps][32], rh[kReduceWarps][32];
+  __shared__ uint64_t rc[kReduceWarps][32];
+  for (int row = blockIdx.x; row < nrows; row += gridDim.x) {
+    const int group = row / nbins, bin = row - group * nbins;
+    const int c = bin * 32 + lane;
+    const int bi = group / a.gb;
+    const int gl = group - bi * a.gb;
+    double sg = 0.0, sh = 0.0;
+    uint64_t sc = 0;
+#pragma unroll 4
+    for (int s = w; s < nseg; s += kReduceWarps) {
+      const size_t cta = static_cast<size_t>(s) * a.nblocks + bi;
+      const size_t o = (cta * a.gb + gl) * cells + c;
+      sg += static_cast<double>(a.part_g[o]);
+      sh += static_cast<double>(a.part_h[o]);
+      sc += a.part_c[o];
+    }
+    rg[w][lane] = sg;
+    rh[w][lane] = sh;
+    rc[w][lane] = sc;
+    __syncthreads();
+    if (w == 0) {
+      for (int i = 1; i < kReduceWarps; ++i) {
+        sg += rg[i][lane];
+        sh += rh[i][lane];
+        sc += rc[i][lane];
+      }
+      double* mine = x.xown + (static_cast<size_t>(x.parity) * nrows + row) * kXRow;
+      mine[16 + lane] = sg;
+      mine[48 + lane] = sh;
+      mine[80 + lane] = static_cast<double>(sc);
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_system();
+        st_release_sys_u64(mine, x.tag);
+      }
+    }
+    __syncthreads();
+  }
+  if (w != 0) return;
+  for (int row = blockIdx.x; row < nrows; row += gridDim.x) {
+    const int group = row / nbins, bin = row - group * nbins;
+    double tg = 0.0, th = 0.0, tc = 0.0;
+    for (int r = 0; r < x.nranks; ++r) {
+      const double* blk = x.xpeer[r] + (static_cast<size_t>(x.parity) * nrows + row) * kXRow;
+      if (lane == 0) {
+        const long long t0 = clock64();
+        while (ld_acquire_sys_u64(blk) != x.tag) {
+          if (clock64() - t0 > x.timeout_cycles) {
+            atomicCAS(x.error, 0, 1);
+            break;
+          }
+        }
+      }
+      __syncwarp();
+      const double g = __ldcv(blk + 16 + lane), h = __ldcv(blk + 48 + lane), n = __ldcv(blk + 80 + lane);
+      tg = r == 0 ? g : tg + g;
+      th = r == 0 ? h : th + h;
+      tc = r == 0 ? n : tc + n;
+    }
+    const int f = group * 32 + lane;
+    if (f >= d || bin >= max_bin) continue;
+    const size_t D = static_cast<size_t>(d) * max_bin;
+    const size_t o = static_cast<size_t>(f) * max_bin + bin;
+    out[o] = tg;
+    out[D + o] = th;
+    out[2 * D + o] = tc;
+  }
+}
+
 // Column-major uint8 bins -> row-major packed words at pack_feature_tuples
 // bit positions (binning.cpp:141-156): word w of a row holds features
 // w*fpw .. w*fpw+fpw-1 at bits*p. One launch covers one 32-feature slice
@@ -378,7 +480,7 @@ int sm_count(int device) {
 // Leaves up to this many rows take the single-segment direct path.
 constexpr int64_t kDirectRows = 1024;
 
-HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int device) {
+HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int device, bool allow_direct) {
   HistPlan p{};
   p.bits = bits;
   p.k_alloc = bits == 4 ? 16 : (max_bin <= 64 ? 64 : (max_bin <= 128 ? 128 : 256));
@@ -417,7 +519,7 @@ HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int de
   p.warps = gb * p.wpg;
   p.smem = p.warps * ghw + gb * cntw;
   p.nblocks = (num_groups + gb - 1) / gb;
-  if (n <= kDirectRows) {
+  if (allow_direct && n <= kDirectRows) {
     // one row segment: each CTA folds and writes the final histogram itself;
     // as many warps as there are 32-row tiles (the fold runs on all of them)
     const int max_wpg = std::max(1, warps_full / gb);
@@ -470,6 +572,19 @@ void launch_histogram(const HistPlan& plan, const HistArgs& args, cudaStream_t s
   } else {
     (ri ? hist_kernel<8, 256, true> : hist_kernel<8, 256, false>)<<<grid, block, plan.smem, s>>>(args);
   }
+  HBG_LAUNCH_CHECK();
+}
+
+size_t hist_exchange_doubles(int k_alloc, int max_bin, int num_groups) {
+  return static_cast<size_t>(2) * std::min(k_alloc, max_bin) * num_groups * kXRow;
+}
+
+void launch_reduce_exchange(const HistPlan& plan, const HistArgs& args, int num_features, int max_bin,
+                            double* d_hist, const PeerHistArgs& x, cudaStream_t s) {
+  const int nbins = std::min(plan.k_alloc, max_bin);
+  const int blocks = std::min(kXBlocks, nbins * args.num_groups);
+  reduce_exchange_kernel<<<blocks, kReduceWarps * 32, 0, s>>>(args, plan.nseg, plan.k_alloc, num_features, max_bin,
+                                                              nbins, d_hist, x);
   HBG_LAUNCH_CHECK();
 }
 

@@ -196,3 +196,72 @@ def test_peer_exchange_sharded_tree_equals_reference(hbg, oracle, world, rows, d
     from test_gpu_parity import _assert_same_tree
 
     assert _assert_same_tree(results[0][0], results[0][1], want_log, want_nodes) == len(want_log)
+
+
+@pytest.mark.parametrize("world,rows,d,k", [(2, 120000, 28, 64), (3, 50000, 40, 16), (2, 30000, 9, 256)])
+def test_peer_histogram_allreduce_fused(hbg, oracle, world, rows, d, k):
+    """hbg_build_histograms_peer: each rank builds the histogram of ITS rows of
+    a leaf; the cross-rank sum is fused into the reduction kernel over peer
+    memory. Every rank must hold the bit-identical global histogram, equal to
+    the oracle's on the union of the ranks' rows (counts exact, sums 1e-5),
+    including leaves of which some rank holds no row."""
+    import torch
+
+    from test_gpu_parity import assert_hist_close
+
+    cols = oracle.gen_synthetic_bins(rows, d, k, 4)
+    g, h = oracle.gen_grad_hess(rows, 4)
+    cuts = [rows * r // world for r in range(world + 1)]
+    shards = [np.ascontiguousarray(cols[:, cuts[r]:cuts[r + 1]]) for r in range(world)]
+    dss = [hbg.Dataset(shards[r], k) for r in range(world)]  # consecutive streams
+    peers = [hbg.Peer(dss[r], world, r) for r in range(world)]
+    for p in peers:
+        for q in peers:
+            if q is not p:
+                p.attach(q)
+    # leaves (global row ids): the whole data, a sampled leaf, and a leaf whose
+    # rows all live on rank 0
+    rng = np.random.default_rng(1)
+    leaves = [np.arange(rows, dtype=np.int32), np.sort(rng.choice(rows, rows // 7, replace=False)).astype(np.int32),
+              np.arange(5, min(cuts[1], 3000), dtype=np.int32)]
+    gf, hf = g.astype(np.float32), h.astype(np.float32)
+    for leaf in leaves:
+        outs, errors = [None] * world, []
+        tensors = []
+        for r in range(world):
+            mine = leaf[(leaf >= cuts[r]) & (leaf < cuts[r + 1])]
+            idx = torch.from_numpy((mine - cuts[r]).astype(np.int32)).cuda()
+            tensors.append((idx, torch.from_numpy(gf[mine]).cuda(), torch.from_numpy(hf[mine]).cuda(),
+                            torch.empty(3 * d * k, dtype=torch.float64, device="cuda")))
+        torch.cuda.synchronize()
+
+        def run(r):
+            try:
+                idx, tg, th, out = tensors[r]
+                st = dss[r].stream()
+                dss[r].build_histograms_peer(idx, len(idx), tg, th, out, peers[r], stream=st)
+                hbg.check(hbg.lib().hbg_stream_synchronize(C.c_void_p(st)))
+                outs[r] = out.cpu().numpy()
+            except Exception as ex:  # surfaced below
+                errors.append(ex)
+
+        ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        assert not errors, errors
+        peers[0].check()
+        for r in range(1, world):
+            assert outs[r].tobytes() == outs[0].tobytes(), r  # identical on every rank
+        D = d * k
+        got = np.zeros((d, k), dtype=hbg.BIN_DTYPE)
+        got["grad_sum"] = outs[0][:D].reshape(d, k)
+        got["hess_sum"] = outs[0][D:2 * D].reshape(d, k)
+        got["count"] = outs[0][2 * D:].reshape(d, k).astype(np.int64)
+        want = oracle.build_histograms(cols, k, leaf, gf[leaf].astype(np.float64), hf[leaf].astype(np.float64), 64)
+        assert_hist_close(got, want)
+    for p in peers:
+        p.close()
+    for ds in dss:
+        ds.close()
