@@ -254,7 +254,40 @@ def run_hbg(args):
         dist.broadcast_object_list(uid, src=0)
         comm = hbg.Comm(world, rank, uid[0], local)
 
+    # N > 1: every rank maps every rank's exchange area (CUDA IPC); the
+    # per-leaf cross-rank sum is then fused into the histogram's reduction
+    # kernel over NVLink peer memory. NCCL (the allreduce hook) is the
+    # fallback, chosen by all ranks together if any rank cannot map or run it.
+    peer = None
+    exchange = "none (single rank)"
+    if comm is not None:
+        ok = torch.ones(1, device=dev)
+        try:
+            peer = hbg.Peer(ds, world, rank, 0, args.num_leaves)
+            handles = [None] * world
+            dist.all_gather_object(handles, peer.ipc_handle())
+            for r in range(world):
+                if r != rank:
+                    peer.open(r, handles[r])
+            ds.build_histograms_peer(ti, n, tg, th, hist, peer, stream=sp)
+            peer.check()
+        except Exception as e:  # noqa: BLE001 — reported in the JSON line
+            ok.zero_()
+            exchange = f"NCCL allreduce (peer path failed: {str(e)[:80]})"
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() == 0:
+            if peer is not None:
+                peer.close()
+            peer = None
+            if exchange.startswith("none"):
+                exchange = "NCCL allreduce (peer path failed on another rank)"
+        else:
+            exchange = "fused into the reduction kernel over NVLink peer memory (hbg_build_histograms_peer)"
+
     def step():
+        if peer is not None:
+            ds.build_histograms_peer(ti, n, tg, th, hist, peer, stream=sp)
+            return
         ds.build_histograms_device(ti, n, tg, th, hist, hbg.HBG_GH_LEAF_ALIGNED, sp)
         if comm is not None:  # the per-leaf exchange of row-sharded training (NCCL over NVLink)
             hbg.check(hbg.lib().hbg_comm_allreduce(hbg._ptr(hist), hist.numel(), hbg._ptr(sp), comm.handle))
@@ -313,7 +346,7 @@ def run_hbg(args):
             "workload": workload, "rows_per_gpu": n, "features": d, "max_bin": k, "bits_per_bin": bits,
             "leaf_depth": 0, "leaf": "explicit int32 indices + leaf-aligned fp32 g/h",
             "l2": f"inputs {(n * (d * bits / 8 + 12)) / 1e6:.0f} MB > 126 MB L2; no flush needed",
-            "parallelism": f"row-sharded x{world}" + (" + NCCL allreduce of the leaf histogram" if world > 1 else ""),
+            "parallelism": f"row-sharded x{world}" + (f"; leaf-histogram exchange: {exchange}" if world > 1 else ""),
         },
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -402,22 +435,10 @@ def run_hbg(args):
     # mappings of every rank's exchange area); the NCCL-hook host loop is the
     # other sharded path, used only if the peer mapping is unavailable
     if not args.no_tree:
-        peer = None
         tree_path = "persistent kernel, single rank"
         if comm is not None:
-            try:
-                peer = hbg.Peer(ds, world, rank, 0, args.num_leaves)
-                handles = [None] * world
-                dist.all_gather_object(handles, peer.ipc_handle())
-                for r in range(world):
-                    if r != rank:
-                        peer.open(r, handles[r])
-                tree_path = "persistent kernel, in-kernel peer-memory histogram exchange (NVLink)"
-            except Exception as e:  # noqa: BLE001 — reported in the JSON line
-                if peer is not None:
-                    peer.close()
-                peer = None
-                tree_path = f"host loop + NCCL allreduce hook (peer mapping unavailable: {str(e)[:80]})"
+            tree_path = ("persistent kernel, in-kernel peer-memory histogram exchange (NVLink)" if peer is not None
+                         else "host loop + NCCL allreduce hook (peer mapping unavailable)")
 
         def grow():
             if comm is None:
@@ -467,8 +488,6 @@ def run_hbg(args):
             "note": "root + smaller child of every split (larger by subtraction); all splits in one persistent cooperative kernel (grow_persistent.cu)",
             "path": tree_path,
         }
-        if peer is not None:
-            peer.close()
         if comm is None:
             # end to end through the whole-tree drop-in (hbg_grow_tree_host):
             # host fp64 g/h (pinned) in, split log + nodes out, H2D inside
@@ -512,6 +531,8 @@ def run_hbg(args):
                 result["cpu_baseline"] = None
         except Exception as e:  # informational leg; never masks the GPU number
             result["cpu_baseline"] = {"error": str(e)}
+    if peer is not None:
+        peer.close()
     ds.close()
     if comm is not None:
         comm.close()
