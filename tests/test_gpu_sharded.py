@@ -139,7 +139,8 @@ def test_nccl_comm_single_rank_tree(hbg, oracle, monkeypatch):
 
 
 @pytest.mark.parametrize("world,rows,d,k,leaves,min_data", [(2, 60000, 28, 64, 63, 60), (3, 50001, 12, 16, 31, 100),
-                                                           (2, 30000, 9, 256, 31, 80), (2, 200000, 28, 64, 255, 200)])
+                                                           (2, 30000, 9, 256, 31, 80), (2, 200000, 28, 64, 255, 200),
+                                                           (2, 40000, 70, 64, 31, 100)])
 def test_peer_exchange_sharded_tree_equals_reference(hbg, oracle, world, rows, d, k, leaves, min_data):
     """Row sharding INSIDE the persistent grower: `world` ranks as threads on
     one GPU, each a partial grid (SMs / world CTAs) over its own row shard,
