@@ -226,6 +226,12 @@ int hbg_peer_destroy(hbg_peer* p);
 int hbg_build_histograms_peer(hbg_dataset* ds, const int32_t* d_indices, int64_t count, const float* d_grad,
                               const float* d_hess, int32_t gh_mode, double* d_hist, hbg_peer* peer, void* stream);
 int hbg_peer_check(hbg_peer* p);
+/* boost_one_iteration (as hbg_boost_one_iteration) with the tree grown through
+ * hbg_grow_tree_peer: this rank's rows' targets/scores; every rank calls it. */
+int hbg_boost_one_iteration_peer(hbg_dataset* ds, const double* d_targets, double* d_scores, int32_t loss,
+                                 double learning_rate, const hbg_grow_params* params, hbg_peer* peer,
+                                 hbg_split* split_log, int32_t* num_splits, hbg_tree_node* nodes, int32_t* num_nodes,
+                                 void* stream);
 int hbg_grow_tree_peer(hbg_dataset* ds, const float* d_grad, const float* d_hess, const hbg_grow_params* params,
                        hbg_peer* peer, hbg_split* split_log, int32_t* num_splits, hbg_tree_node* nodes,
                        int32_t* num_nodes, void* stream);

@@ -136,6 +136,7 @@ EXPORTED_SYMBOLS = (
     "hbg_peer_destroy",
     "hbg_build_histograms_peer",
     "hbg_peer_check",
+    "hbg_boost_one_iteration_peer",
     "hbg_grow_tree_peer",
     "hbg_comm_get_unique_id",
     "hbg_comm_init",
@@ -196,6 +197,7 @@ def lib() -> C.CDLL:
         L.hbg_peer_destroy.argtypes = [_P]
         L.hbg_build_histograms_peer.argtypes = [_P, _P, C.c_int64, _P, _P, C.c_int32, _P, _P, _P]
         L.hbg_peer_check.argtypes = [_P]
+        L.hbg_boost_one_iteration_peer.argtypes = [_P, _P, _P, C.c_int32, C.c_double, _P, _P, _P, _P, _P, _P, _P]
         L.hbg_grow_tree_peer.argtypes = [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P]
         L.hbg_grow_tree_sharded.argtypes = [_P, _P, _P, _P, ALLREDUCE_FN, _P, _P, _P, _P, _P, _P]
         L.hbg_comm_get_unique_id.argtypes = [_P]
@@ -348,6 +350,21 @@ class Dataset:
         all ranks (the sum fused into the reduction kernel, over peer memory)."""
         check(lib().hbg_build_histograms_peer(self.handle, _ptr(indices), count, _ptr(grad), _ptr(hess), gh_mode,
                                               _ptr(out), peer.handle, _ptr(stream)))
+
+    def boost_one_iteration_peer(self, targets, scores, peer: "Peer", loss: int = HBG_LOSS_SQUARED,
+                                 learning_rate: float = 0.1, num_leaves: int = 31, min_data_in_leaf: int = 1,
+                                 lam: float = 0.0, stream=None):
+        """boost_one_iteration over this rank's rows, the tree grown through the
+        in-kernel peer exchange (every rank calls it)."""
+        p = hbg_grow_params(num_leaves, 0, min_data_in_leaf, lam)
+        log = np.zeros(max(num_leaves - 1, 1), dtype=SPLIT_DTYPE)
+        nodes = np.zeros(max(2 * num_leaves - 1, 1), dtype=NODE_DTYPE)
+        ns = C.c_int32()
+        nn = C.c_int32()
+        check(lib().hbg_boost_one_iteration_peer(self.handle, _ptr(targets), _ptr(scores), loss, learning_rate,
+                                                 C.byref(p), peer.handle, _ptr(log), C.byref(ns), _ptr(nodes),
+                                                 C.byref(nn), _ptr(stream)))
+        return log[: ns.value].copy(), nodes[: nn.value].copy()
 
     def grow_tree_peer(self, grad, hess, peer: "Peer", num_leaves: int = 31, min_data_in_leaf: int = 1,
                        lam: float = 0.0, stream=None):

@@ -728,19 +728,20 @@ void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_h
 // so the update needs no tree traversal.
 void boost_impl(hbg_dataset* ds, const double* d_targets, double* d_scores, int loss, double lr,
                 const hbg_grow_params& P, const Reducer& reduce, hbg_split* split_log,
-                int32_t* num_splits, hbg_tree_node* nodes, int32_t* num_nodes, cudaStream_t s) {
+                int32_t* num_splits, hbg_tree_node* nodes, int32_t* num_nodes, cudaStream_t s,
+                hbg_peer* peer = nullptr) {
   require(loss == HBG_LOSS_SQUARED || loss == HBG_LOSS_LOGISTIC, "unknown loss");
   const int64_t N = ds->layout.num_rows;
   float* g = static_cast<float*>(ds->boost_g.get(static_cast<size_t>(N) * 4 + 4));
   float* h = static_cast<float*>(ds->boost_h.get(static_cast<size_t>(N) * 4 + 4));
   launch_grad_hess(loss, d_scores, d_targets, N, g, h, s);
-  if (reduce.fn == nullptr && !use_host_loop()) {
+  if (reduce.fn == nullptr && (peer != nullptr || !use_host_loop())) {
     std::vector<hbg_tree_node> local;
     if (nodes == nullptr) {
       local.resize(static_cast<size_t>(std::max(1, 2 * P.num_leaves - 1)));
       nodes = local.data();
     }
-    grow_tree_persistent(ds, g, h, P, split_log, num_splits, nodes, num_nodes, s);
+    grow_tree_persistent(ds, g, h, P, split_log, num_splits, nodes, num_nodes, s, peer);
     if (*num_splits == 0) {  // a root-only tree: every row gets the root value
       LeafRange r{0, N, nodes[0].value, 0, 0};
       LeafRange* dl = static_cast<LeafRange*>(ds->boost_leaves.get(sizeof(LeafRange) + 8));
@@ -1119,7 +1120,12 @@ int hbg_peer_create(hbg_dataset* ds, int32_t nranks, int32_t rank, int32_t ctas,
     HBG_CUDA(cudaMalloc(&p->error, sizeof(int)));
     HBG_CUDA(cudaMemset(p->error, 0, sizeof(int)));
     p->peers[rank] = p->xbuf;
-    grow_workspace(ds, *params, ctas);  // reserve: no allocation while the ranks' grids exchange
+    // reserve every buffer of the peer calls (trees, boosting): an allocation
+    // while another rank's grid waits in an exchange serialises behind it
+    grow_workspace(ds, *params, ctas);
+    ds->boost_g.get(static_cast<size_t>(L.num_rows) * 4 + 4);
+    ds->boost_h.get(static_cast<size_t>(L.num_rows) * 4 + 4);
+    ds->boost_leaves.get(sizeof(LeafRange) + 8);
     HBG_CUDA(cudaDeviceSynchronize());
     *out = p.release();
   });
@@ -1245,6 +1251,22 @@ int hbg_boost_one_iteration(hbg_dataset* ds, const double* d_targets, double* d_
     DeviceGuard dg(ds->layout.device);
     boost_impl(ds, d_targets, d_scores, loss, learning_rate, *params, Reducer{allreduce, ctx}, split_log,
                num_splits, nodes, num_nodes, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int hbg_boost_one_iteration_peer(hbg_dataset* ds, const double* d_targets, double* d_scores, int32_t loss,
+                                 double learning_rate, const hbg_grow_params* params, hbg_peer* peer,
+                                 hbg_split* split_log, int32_t* num_splits, hbg_tree_node* nodes, int32_t* num_nodes,
+                                 void* stream) {
+  return guarded([&] {
+    check_ds(ds);
+    require(params != nullptr && peer != nullptr && split_log != nullptr && num_splits != nullptr &&
+                num_nodes != nullptr,
+            "null argument");
+    require(ds->layout.num_rows == 0 || (d_targets != nullptr && d_scores != nullptr), "null targets/scores");
+    DeviceGuard dg(ds->layout.device);
+    boost_impl(ds, d_targets, d_scores, loss, learning_rate, *params, Reducer{nullptr, nullptr}, split_log,
+               num_splits, nodes, num_nodes, static_cast<cudaStream_t>(stream), peer);
   });
 }
 
