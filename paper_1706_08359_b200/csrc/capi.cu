@@ -99,6 +99,9 @@ struct hbg_dataset {
   hbg::DevBuf boost_g, boost_h, boost_leaves;   // boosting: fp32 gradients, final leaf ranges
   hbg::DevBuf small_acc, small_exps;            // fixed-point accumulator for small leaves
   hbg::DevBuf grow_nodes, grow_log, grow_tree, grow_counts, grow_scratch, grow_root, grow_prof;  // persistent grower
+  const void* grow_records = nullptr;  // the last grown tree's score-update input (launch_grow_persistent)
+  bool grow_waves = false;             // ... LeafRange x grow_ranges (wave grower) or node records
+  int grow_ranges = 0;
   void* pinned = nullptr;                      // host staging for per-split results
   // measurement hooks
   bool profiling = false;
@@ -565,13 +568,14 @@ bool use_host_loop() {
 // for row-sharded ranks sharing a GPU, reserved at hbg_peer_create): a
 // cudaMalloc/cudaFree while another rank's grid waits in an exchange would
 // serialise behind it.
-PersistentGrowArgs grow_workspace(hbg_dataset* ds, const hbg_grow_params& P, int ctas) {
+PersistentGrowArgs grow_workspace(hbg_dataset* ds, const hbg_grow_params& P, int ctas, int nranks) {
   const hbg_layout& L = ds->layout;
   const int64_t N = L.num_rows;
   const int d = L.num_features, k = L.max_bin;
   const size_t D3 = 3 * static_cast<size_t>(d) * k;
-  const int max_nodes = std::max(1, 2 * P.num_leaves - 1);
+  const int max_out = std::max(1, 2 * P.num_leaves - 1);
   PersistentGrowArgs a{};
+  a.nranks = nranks;
   a.packed = reinterpret_cast<const uint8_t*>(ds->packed);
   a.colbins = static_cast<const uint8_t*>(ds->colbins.p);
   a.row_stride = L.row_stride_bytes;
@@ -582,15 +586,17 @@ PersistentGrowArgs grow_workspace(hbg_dataset* ds, const hbg_grow_params& P, int
   a.num_groups = L.num_groups;
   a.num_rows = N;
   a.ctas = ctas;
+  a.num_leaves = P.num_leaves;
+  const int max_nodes = grow_max_nodes(a, L.device);
   a.slots = static_cast<double*>(ds->slots.get(static_cast<size_t>(max_nodes) * D3 * sizeof(double) + 8));
   for (int b = 0; b < 2; ++b) {
     a.rows[b] = static_cast<int32_t*>(ds->ord[b][0].get(static_cast<size_t>(N) * 4 + 4));
     a.g[b] = static_cast<float*>(ds->ord[b][1].get(static_cast<size_t>(N) * 4 + 4));
     a.h[b] = static_cast<float*>(ds->ord[b][2].get(static_cast<size_t>(N) * 4 + 4));
   }
-  a.nodes = ds->grow_nodes.get(grow_nodes_bytes(P.num_leaves));
-  a.split_log = static_cast<hbg_split*>(ds->grow_log.get(static_cast<size_t>(max_nodes) * sizeof(hbg_split)));
-  a.tree = static_cast<hbg_tree_node*>(ds->grow_tree.get(static_cast<size_t>(max_nodes) * sizeof(hbg_tree_node)));
+  a.nodes = ds->grow_nodes.get(grow_nodes_bytes(max_nodes));
+  a.split_log = static_cast<hbg_split*>(ds->grow_log.get(static_cast<size_t>(max_out) * sizeof(hbg_split)));
+  a.tree = static_cast<hbg_tree_node*>(ds->grow_tree.get(static_cast<size_t>(max_out) * sizeof(hbg_tree_node)));
   a.counts = static_cast<int*>(ds->grow_counts.get(8 * sizeof(int)));
   a.num_leaves = P.num_leaves;  // (sizes the scratch below)
   a.min_data = P.min_data_in_leaf;
@@ -618,7 +624,7 @@ void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_h
   const int d = L.num_features, k = L.max_bin;
   const int max_nodes = std::max(1, 2 * P.num_leaves - 1);
   const bool sharded = peer != nullptr && peer->nranks > 1;
-  PersistentGrowArgs a = grow_workspace(ds, P, sharded ? peer->ctas : 0);
+  PersistentGrowArgs a = grow_workspace(ds, P, sharded ? peer->ctas : 0, sharded ? peer->nranks : 1);
   double* slots = a.slots;
   int* exps = const_cast<int*>(a.exps);
   double* root = const_cast<double*>(a.root_totals);
@@ -663,11 +669,12 @@ void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_h
   const char* pe = std::getenv("HBG_GROW_PROFILE");
   std::vector<unsigned long long> prof;
   if (pe != nullptr) {  // phase stamps of CTA 0, printed to stderr (development aid)
-    prof.assign(static_cast<size_t>(max_nodes) * 12, 0ull);
+    prof.assign(static_cast<size_t>(4 * max_nodes + 8) * 12, 0ull);
     a.prof = static_cast<unsigned long long*>(ds->grow_prof.get(prof.size() * 8));
     HBG_CUDA(cudaMemsetAsync(a.prof, 0, prof.size() * 8, s));
   }
-  launch_grow_persistent(a, L.device, s);
+  ds->grow_records = launch_grow_persistent(a, L.device, s);
+  const bool waves = ds->grow_records != a.nodes;
   int counts[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   HBG_CUDA(cudaMemcpyAsync(counts, a.counts, sizeof counts, cudaMemcpyDeviceToHost, s));
   HBG_CUDA(cudaStreamSynchronize(s));
@@ -683,7 +690,41 @@ void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_h
   }
   *num_splits = counts[0];
   *num_nodes = counts[1];
-  if (a.prof != nullptr) {
+  ds->grow_waves = waves;
+  ds->grow_ranges = counts[4];
+  if (a.prof != nullptr && waves) {
+    HBG_CUDA(cudaMemcpy(prof.data(), a.prof, prof.size() * 8, cudaMemcpyDeviceToHost));
+    // wave grower stamps: 0 start, 1 partitioned (large), 2 histogram (large), 3 chunks done,
+    // 4 barrier, 5 next wave chosen; slot 7: large, 10: members, 11: splits committed before
+    double tw[2][8] = {{0, 0, 0, 0, 0, 0, 0, 0}, {0, 0, 0, 0, 0, 0, 0, 0}};
+    int nw[2] = {0, 0}, members[2] = {0, 0};
+    for (int i = 0; i < counts[3]; ++i) {
+      const unsigned long long* t = prof.data() + static_cast<size_t>(i) * 12;
+      const int c = t[7] ? 1 : 0;
+      ++nw[c];
+      members[c] += static_cast<int>(t[10]);
+      tw[c][0] += (t[3] - t[0]) * 1e-3;
+      tw[c][1] += (t[4] - t[3]) * 1e-3;
+      tw[c][2] += (t[5] - t[4]) * 1e-3;
+      if (c) tw[c][3] += (t[1] - t[0]) * 1e-3, tw[c][4] += (t[2] - t[1]) * 1e-3;
+      if (t[6] && t[8] && t[9]) {  // select: integrate, replay, speculation choice
+        tw[c][5] += (t[6] - t[4]) * 1e-3;
+        tw[c][6] += (t[8] - t[6]) * 1e-3;
+        tw[c][7] += (t[9] - t[8]) * 1e-3;
+      }
+    }
+    for (int c = 0; c < 2; ++c) {
+      if (!nw[c]) continue;
+      std::fprintf(stderr, "wave grower, %s: %d waves, %d expansions; avg us: work %.2f barrier %.2f select %.2f",
+                   c ? "large parents" : "small-parent waves", nw[c], members[c], tw[c][0] / nw[c], tw[c][1] / nw[c],
+                   tw[c][2] / nw[c]);
+      if (c) std::fprintf(stderr, " (partition %.2f hist %.2f)", tw[c][3] / nw[c], tw[c][4] / nw[c]);
+      std::fprintf(stderr, " [integrate %.2f replay %.2f choose %.2f]", tw[c][5] / nw[c], tw[c][6] / nw[c],
+                   tw[c][7] / nw[c]);
+      std::fprintf(stderr, "\n");
+    }
+    std::fprintf(stderr, "wave grower: %d splits committed, %d expansions\n", counts[0], members[0] + members[1]);
+  } else if (a.prof != nullptr) {
     HBG_CUDA(cudaMemcpy(prof.data(), a.prof, prof.size() * 8, cudaMemcpyDeviceToHost));
     // stamps: 0 start, 1 partitioned, 2 small-child histogram, 3 finish+scans, 4 barrier, 5 picked;
     // slot 7: class = (large parent ? 4 : 0) + path (0 none, 1 direct, 2 shared-memory histogram)
@@ -748,8 +789,12 @@ void boost_impl(hbg_dataset* ds, const double* d_targets, double* d_scores, int 
       HBG_CUDA(cudaMemcpyAsync(dl, &r, sizeof r, cudaMemcpyHostToDevice, s));
       launch_iota(static_cast<int32_t*>(ds->ord[0][0].get(static_cast<size_t>(N) * 4 + 4)), N, s);
       launch_score_update(dl, 1, static_cast<const int32_t*>(ds->ord[0][0].p), nullptr, lr, d_scores, s);
+    } else if (ds->grow_waves) {
+      launch_score_update(static_cast<const LeafRange*>(ds->grow_records), ds->grow_ranges,
+                          static_cast<const int32_t*>(ds->ord[0][0].p), static_cast<const int32_t*>(ds->ord[1][0].p),
+                          lr, d_scores, s);
     } else {
-      launch_score_update_nodes(ds->grow_nodes.p, static_cast<const hbg_tree_node*>(ds->grow_tree.p), *num_nodes,
+      launch_score_update_nodes(ds->grow_records, static_cast<const hbg_tree_node*>(ds->grow_tree.p), *num_nodes,
                                 static_cast<const int32_t*>(ds->ord[0][0].p),
                                 static_cast<const int32_t*>(ds->ord[1][0].p), lr, d_scores, s);
     }
@@ -1105,6 +1150,7 @@ int hbg_peer_create(hbg_dataset* ds, int32_t nranks, int32_t rank, int32_t ctas,
     a.num_groups = L.num_groups;
     a.num_rows = L.num_rows;
     a.ctas = ctas;
+    a.nranks = nranks;
     auto p = std::make_unique<hbg_peer>();
     p->nranks = nranks;
     p->rank = rank;
@@ -1122,7 +1168,7 @@ int hbg_peer_create(hbg_dataset* ds, int32_t nranks, int32_t rank, int32_t ctas,
     p->peers[rank] = p->xbuf;
     // reserve every buffer of the peer calls (trees, boosting): an allocation
     // while another rank's grid waits in an exchange serialises behind it
-    grow_workspace(ds, *params, ctas);
+    grow_workspace(ds, *params, ctas, nranks);
     ds->boost_g.get(static_cast<size_t>(L.num_rows) * 4 + 4);
     ds->boost_h.get(static_cast<size_t>(L.num_rows) * 4 + 4);
     ds->boost_leaves.get(sizeof(LeafRange) + 8);

@@ -36,6 +36,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "hbg_internal.h"
@@ -85,6 +86,8 @@ struct Desc {
   int32_t feature, thr;
   int32_t lsplit, rsplit, small_is_left, path;
   int32_t nseg, items;
+  int32_t mslot;         // partition scratch slot (wave member; 0 for grow_kernel)
+  int32_t pbase;         // first shared-memory histogram item of this split in part_g/h/c
   int64_t begin, count;  // parent range
   int64_t nl, nr;        // rows left / right over all ranks (the split's left_count)
   int64_t seg_len;
@@ -128,6 +131,7 @@ struct GrowArgs {
   int gb, wpg, nblocks;  // histogram: slice groups per CTA item, warps per group
   int rpl;               // rows per lane of the histogram schedule
   int fchunk, nchunks;   // finish/scan: features per chunk
+  int cchunk;            // features per chunk the shared-memory layout holds (>= fchunk)
   long long timeout_cycles;
   unsigned long long* prof;  // optional: [iter][kProfSlots] globaltimer stamps of CTA 0
   // row sharding (nranks > 1): per-split exchange of the smaller child's
@@ -138,6 +142,19 @@ struct GrowArgs {
   size_t xblock;                   // doubles per (parity, chunk) block
   unsigned long long gen;          // tree generation (tags are monotonic across trees)
   int debug;                       // HBG_GROW_DEBUG: CTA 0 prints every pick
+  // wave grower (single rank; see "wave grower" below)
+  Cand* wcand;            // [member][child][wcstride] chunk winners of the current wave
+  size_t wcstride;        // chunks per member and child in wcand
+  unsigned* wcnt;         // [wmax] finished chunks per member (last arriver resets)
+  unsigned char* wstate;  // per-CTA commit log, wstate_stride bytes each
+  size_t wstate_stride;
+  LeafRange* ranges;      // [max_nodes] rows of every unexpanded node -> its final leaf's value (score update)
+  int wmax;               // members per wave
+  int wlarge;             // speculative large members allowed (HBG_WAVE_LARGE)
+  int64_t spec_rows;      // ... up to this many rows (HBG_WAVE_SPEC_ROWS)
+  int wcap;               // features per wave chunk the shared-memory layout holds
+  int ecap;               // speculative expansions allowed up to this total
+  int64_t small_max;      // parents up to this many rows join waves (kItems * NT)
 };
 
 constexpr int kProfSlots = 12;
@@ -498,6 +515,8 @@ __device__ void pick(const GrowArgs& a, int i, int kid_l, const Kid* kid, Desc& 
         const int64_t nl = bs.left_count, nr = gcount - nl;  // over all ranks
         D.done = 0;
         D.iter = i;
+        D.mslot = 0;
+        D.pbase = 0;
         D.parent = p;
         D.left_id = left;
         D.right_id = right;
@@ -606,7 +625,7 @@ struct RegRows {
 };
 
 template <int NT>
-__device__ void partition_redundant(const GrowArgs& a, Desc& D, RegRows& rr, PartShared<NT>& ps, int parts,
+__device__ void partition_redundant(const GrowArgs& a, Desc& D, RegRows& rr, PartShared<NT>& ps, int parts, int part,
                                     unsigned char* stage /* smem, kItems*NT*12 B */) {
   const int64_t n = D.count;
   const int32_t* rin = a.rows[D.buf_in] + D.begin;
@@ -668,9 +687,9 @@ __device__ void partition_redundant(const GrowArgs& a, Desc& D, RegRows& rr, Par
     D.nl_loc = L;
     if (a.nranks == 1 && L != D.nl) set_error(a, kErrPartition);
   }
-  // this CTA's share of the output positions (the first `parts` CTAs partition)
+  // share `part` of the output positions (`parts` CTAs write one share each)
   const int64_t share = (n + parts - 1) / parts;
-  const int64_t s0 = static_cast<int64_t>(blockIdx.x) * share, s1 = min(n, s0 + share);
+  const int64_t s0 = static_cast<int64_t>(part) * share, s1 = min(n, s0 + share);
   int32_t* rout = a.rows[D.buf_out] + D.begin;
   float* gout = a.g[D.buf_out] + D.begin;
   float* hout = a.h[D.buf_out] + D.begin;
@@ -752,7 +771,7 @@ __device__ void partition_count(const GrowArgs& a, const Desc& D, PartShared<NT>
       const int64_t pos = t0 + static_cast<int64_t>(j) * NT + threadIdx.x;
       if (j >= ipt || pos >= e) continue;
       const bool left = bin[j] <= static_cast<uint32_t>(D.thr);  // tree.cpp:117-123
-      a.flags[pos] = left ? 1 : 0;
+      a.flags[D.begin + pos] = left ? 1 : 0;
       if (left) {
         ++c;
         v[0] += gv[j];
@@ -771,8 +790,9 @@ __device__ void partition_count(const GrowArgs& a, const Desc& D, PartShared<NT>
   }
   block_sum_4d1<NT>(v, c, ps);
   if (threadIdx.x == 0) {
-    a.cta_left[blockIdx.x] = ps.cnt;
-    for (int j = 0; j < 4; ++j) a.cta_sums[4 * blockIdx.x + j] = ps.tot[j];
+    const size_t slot = static_cast<size_t>(D.mslot) * gridDim.x + blockIdx.x;
+    a.cta_left[slot] = ps.cnt;
+    for (int j = 0; j < 4; ++j) a.cta_sums[4 * slot + j] = ps.tot[j];
   }
 }
 
@@ -786,9 +806,10 @@ __device__ void partition_scatter(const GrowArgs& a, Desc& D, PartShared<NT>& ps
   double v[4] = {0.0, 0.0, 0.0, 0.0};
   long long c = 0;
   for (int b = threadIdx.x; b < G; b += NT) {  // G <= NT: one CTA record per thread
-    c = __ldcg(a.cta_left + b);
+    const size_t slot = static_cast<size_t>(D.mslot) * G + b;
+    c = __ldcg(a.cta_left + slot);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) v[j] = __ldcg(a.cta_sums + 4 * b + j);
+    for (int j = 0; j < 4; ++j) v[j] = __ldcg(a.cta_sums + 4 * slot + j);
   }
   const long long before_t = block_excl_scan<NT>(c, ps);
   __shared__ long long s_before;
@@ -841,7 +862,7 @@ __device__ void partition_scatter(const GrowArgs& a, Desc& D, PartShared<NT>& ps
       rr[j] = ok ? __ldcg(rin + t0 + q) : 0;
       rg[j] = ok ? __ldcg(gin + t0 + q) : 0.f;
       rh[j] = ok ? __ldcg(hin + t0 + q) : 0.f;
-      rf[j] = ok ? __ldcg(a.flags + t0 + q) : 0;
+      rf[j] = ok ? __ldcg(a.flags + D.begin + t0 + q) : 0;
     }
   };
   auto stage = [&](const Stage& b) {
@@ -959,15 +980,15 @@ __device__ __forceinline__ void direct_accumulate(const GrowArgs& a, unsigned* a
 // ------------------------------------------------------------ finish and scan
 
 // Smem layout of the finish phase: staging [child][stat][bin][feature] fp64
-// (6 * fchunk * k doubles), then the direct accumulator (20 B per cell).
+// (6 * cchunk * k doubles), then the direct accumulator (20 B per cell).
 __device__ __forceinline__ unsigned* direct_acc(const GrowArgs& a, unsigned char* smem) {
-  return reinterpret_cast<unsigned*>(smem + static_cast<size_t>(6) * a.fchunk * a.k * sizeof(double));
+  return reinterpret_cast<unsigned*>(smem + static_cast<size_t>(6) * a.cchunk * a.k * sizeof(double));
 }
 
 // Small-parent partition staging: after the finish phase's staging and the
 // direct accumulator (both live while the partition runs).
 __device__ __forceinline__ unsigned char* part_stage(const GrowArgs& a, unsigned char* smem) {
-  const size_t off = static_cast<size_t>(a.fchunk) * a.k * (6 * sizeof(double) + 20);
+  const size_t off = static_cast<size_t>(a.cchunk) * a.k * (6 * sizeof(double) + 20);
   return smem + (off + 15) / 16 * 16;
 }
 
@@ -976,12 +997,24 @@ __device__ __forceinline__ void zero_direct(const GrowArgs& a, unsigned char* sm
   for (int i = threadIdx.x; i < 5 * cells; i += NT) acc[i] = 0u;
 }
 
+// Where a chunk's per-child winners go: p[r * rep_stride + child * child_stride]
+// for the `reps` replicas.
+struct CandOut {
+  Cand* p;
+  int reps;
+  size_t rep_stride, child_stride;
+};
+
+__device__ __forceinline__ CandOut legacy_out(const GrowArgs& a, int c) {
+  return CandOut{a.cand + c, kRep, static_cast<size_t>(2) * a.nchunks, static_cast<size_t>(a.nchunks)};
+}
+
 // Both children's scans of one staged feature chunk at once: threads
 // [0, NT/2) child 0 (staging st[0..3*stride)), the rest child 1; per-child
-// chunk winner -> a.cand[child][c]. Whole CTA.
+// chunk winner -> out. Whole CTA.
 template <int NT>
-__device__ void scan_chunk(const GrowArgs& a, double* st, int chunk_cells, int nf, int f0, int c_idx, bool want0,
-                           bool want1, const double* tot, int64_t n0, int64_t n1) {
+__device__ void scan_chunk(const GrowArgs& a, double* st, int chunk_cells, int nf, int f0, const CandOut& out,
+                           bool want0, bool want1, const double* tot, int64_t n0, int64_t n1) {
   const int k = a.k;
   constexpr int half = NT / 2, W = NT / 32;
   const int child = static_cast<int>(threadIdx.x) < half ? 0 : 1;
@@ -1018,7 +1051,7 @@ __device__ void scan_chunk(const GrowArgs& a, double* st, int chunk_cells, int n
         c = Cand{__longlong_as_double(static_cast<long long>(hk)), f, b, base[t], base[chunk_cells + t],
                  static_cast<int64_t>(base[2 * chunk_cells + t])};
       }
-      for (int r = 0; r < kRep; ++r) a.cand[(r * 2 + child) * a.nchunks + c_idx] = c;
+      for (int r = 0; r < out.reps; ++r) out.p[r * out.rep_stride + child * out.child_stride] = c;
     }
   }
   __syncthreads();
@@ -1048,8 +1081,8 @@ __device__ void exchange_totals_chunk(const GrowArgs& a, Desc& D, int c) {
 // child = parent - small, both written to their node slots and staged for
 // the two scans; per-chunk winners -> a.cand.
 template <int K, int NT>
-__device__ void finish_chunk(const GrowArgs& a, const Desc& D, int c_idx, unsigned char* smem, Cand* wb) {
-  const int c = c_idx;
+__device__ void finish_range(const GrowArgs& a, const Desc& D, int f0, int nf, int c, unsigned char* smem,
+                             const CandOut& out) {
   constexpr int kCells = K * 32;
   const int d = a.d, k = a.k;
   const size_t Dc = static_cast<size_t>(d) * k;
@@ -1059,11 +1092,9 @@ __device__ void finish_chunk(const GrowArgs& a, const Desc& D, int c_idx, unsign
   double* so = slot_of(a, small_id);
   double* lo = slot_of(a, large_id);
   double* st = reinterpret_cast<double*>(smem);
-  const int chunk_cells = a.fchunk * k;
+  const int chunk_cells = a.cchunk * k;
   double* sm = st + (D.small_is_left ? 0 : 3 * chunk_cells);
   double* lg = st + (D.small_is_left ? 3 * chunk_cells : 0);
-  const int f0 = c * a.fchunk;
-  const int nf = min(a.fchunk, d - f0);
   const int cells = nf * k;
   if (D.path == kDirect) {
     const double sg = ldexp(1.0, -a.exps[0]), sh = ldexp(1.0, -a.exps[1]);
@@ -1094,7 +1125,7 @@ __device__ void finish_chunk(const GrowArgs& a, const Desc& D, int c_idx, unsign
         const int cl = b * 32 + (f & 31);
 #pragma unroll 4
         for (int s = j; s < D.nseg; s += tpc) {
-          const size_t o = ((static_cast<size_t>(s) * a.nblocks + bi) * a.gb + gl) * kCells + cl;
+          const size_t o = ((static_cast<size_t>(D.pbase) + static_cast<size_t>(s) * a.nblocks + bi) * a.gb + gl) * kCells + cl;
           vg += static_cast<double>(__ldcg(a.part_g + o));
           vh += static_cast<double>(__ldcg(a.part_h + o));
           vc += __ldcg(a.part_c + o);
@@ -1148,7 +1179,14 @@ __device__ void finish_chunk(const GrowArgs& a, const Desc& D, int c_idx, unsign
     lg[2 * chunk_cells + t] = xc;
   }
   __syncthreads();
-  scan_chunk<NT>(a, st, chunk_cells, nf, f0, c_idx, D.lsplit, D.rsplit, D.tot, D.nl, D.nr);
+  scan_chunk<NT>(a, st, chunk_cells, nf, f0, out, D.lsplit, D.rsplit, D.tot, D.nl, D.nr);
+}
+
+// Feature chunk c of the one-split-at-a-time grower (winners -> a.cand).
+template <int K, int NT>
+__device__ void finish_chunk(const GrowArgs& a, const Desc& D, int c, unsigned char* smem, Cand* /*wb*/) {
+  const int f0 = c * a.fchunk;
+  finish_range<K, NT>(a, D, f0, min(a.fchunk, a.d - f0), c, smem, legacy_out(a, c));
 }
 
 // Every CTA (warp 0): per-child winner over the chunks (bit-identical in every
@@ -1290,9 +1328,10 @@ __device__ __forceinline__ void accumulate_rows(const GrowArgs& a, const int32_t
 }
 
 // Shared-memory histogram of the smaller child: items = (row segment, slice
-// group block); each item -> one fp32/u32 partial per group of the block.
+// group block); each item -> one fp32/u32 partial per group of the block
+// (part_g/h/c item D.pbase + item).
 template <int BITS, int K, int NT>
-__device__ void hist_smem(const GrowArgs& a, const Desc& D, unsigned char* smem) {
+__device__ void hist_smem_item(const GrowArgs& a, const Desc& D, int item, unsigned char* smem) {
   constexpr int kCells = K * 32;
   const int32_t* rows;
   const float* g;
@@ -1303,42 +1342,44 @@ __device__ void hist_smem(const GrowArgs& a, const Desc& D, unsigned char* smem)
   float2* gh = reinterpret_cast<float2*>(smem);
   uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + static_cast<size_t>(warps) * kCells * 8);
   const int w = threadIdx.x >> 5;
-  for (int item = blockIdx.x; item < D.items; item += gridDim.x) {
-    const int bi = item % a.nblocks, seg = item / a.nblocks;
-    {
-      const int n16 = (warps * kCells * 8 + a.gb * kCells * 4) / 16;
-      uint4* z = reinterpret_cast<uint4*>(smem);
-      for (int i = threadIdx.x; i < n16; i += NT) z[i] = make_uint4(0, 0, 0, 0);
-    }
-    __syncthreads();
-    if (w < warps) {
-      const int gl = w % a.gb, sub = w / a.gb;
-      const int group = bi * a.gb + gl;
-      if (group < a.num_groups) {
-        const int64_t s0 = static_cast<int64_t>(seg) * D.seg_len;
-        const int64_t s1 = min(s0 + D.seg_len, n);
-        const uint32_t gh_base = smem_addr(gh + static_cast<size_t>(w) * kCells);
-        const unsigned char* base = a.packed + static_cast<size_t>(group) * Slice<BITS>::kWords * 4;
-        accumulate_rows<BITS, K>(a, rows, g, h, s0, s1, sub, base, gh_base,
-                                 cnt + static_cast<size_t>(gl) * kCells);
-      }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < a.gb * kCells; i += NT) {
-      const int g2 = i / kCells, c = i - g2 * kCells;
-      float sg = 0.f, sh = 0.f;
-      for (int s = 0; s < a.wpg; ++s) {  // warps of the group in a fixed order
-        const float2 v = gh[static_cast<size_t>(s * a.gb + g2) * kCells + c];
-        sg += v.x;
-        sh += v.y;
-      }
-      const size_t o = (static_cast<size_t>(item) * a.gb + g2) * kCells + c;
-      a.part_g[o] = sg;
-      a.part_h[o] = sh;
-      a.part_c[o] = cnt[static_cast<size_t>(g2) * kCells + c];
-    }
-    __syncthreads();
+  const int bi = item % a.nblocks, seg = item / a.nblocks;
+  {
+    const int n16 = (warps * kCells * 8 + a.gb * kCells * 4) / 16;
+    uint4* z = reinterpret_cast<uint4*>(smem);
+    for (int i = threadIdx.x; i < n16; i += NT) z[i] = make_uint4(0, 0, 0, 0);
   }
+  __syncthreads();
+  if (w < warps) {
+    const int gl = w % a.gb, sub = w / a.gb;
+    const int group = bi * a.gb + gl;
+    if (group < a.num_groups) {
+      const int64_t s0 = static_cast<int64_t>(seg) * D.seg_len;
+      const int64_t s1 = min(s0 + D.seg_len, n);
+      const uint32_t gh_base = smem_addr(gh + static_cast<size_t>(w) * kCells);
+      const unsigned char* base = a.packed + static_cast<size_t>(group) * Slice<BITS>::kWords * 4;
+      accumulate_rows<BITS, K>(a, rows, g, h, s0, s1, sub, base, gh_base, cnt + static_cast<size_t>(gl) * kCells);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < a.gb * kCells; i += NT) {
+    const int g2 = i / kCells, c = i - g2 * kCells;
+    float sg = 0.f, sh = 0.f;
+    for (int s = 0; s < a.wpg; ++s) {  // warps of the group in a fixed order
+      const float2 v = gh[static_cast<size_t>(s * a.gb + g2) * kCells + c];
+      sg += v.x;
+      sh += v.y;
+    }
+    const size_t o = ((static_cast<size_t>(D.pbase) + item) * a.gb + g2) * kCells + c;
+    a.part_g[o] = sg;
+    a.part_h[o] = sh;
+    a.part_c[o] = cnt[static_cast<size_t>(g2) * kCells + c];
+  }
+  __syncthreads();
+}
+
+template <int BITS, int K, int NT>
+__device__ void hist_smem(const GrowArgs& a, const Desc& D, unsigned char* smem) {
+  for (int item = blockIdx.x; item < D.items; item += gridDim.x) hist_smem_item<BITS, K, NT>(a, D, item, smem);
 }
 
 template <int BITS, int K>
@@ -1396,7 +1437,7 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
       __syncthreads();
       const int64_t N = static_cast<int64_t>(rt[5]);
       const bool ok = a.num_leaves >= 2 && splittable(N, a.min_data);  // tree.cpp:165
-      scan_chunk<NT>(a, st, cc, nf, f0, c, ok, false, rt, N, 0);
+      scan_chunk<NT>(a, st, cc, nf, f0, legacy_out(a, c), ok, false, rt, N, 0);
     }
     grid_sync(a);
     if (threadIdx.x == 0) {  // the root "split" descriptor for winners(): child 0 = the root
@@ -1442,7 +1483,7 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
       if (chunk_cta) {
         RegRows rr;
         if (D.path == kDirect) zero_direct(a, smem, nf * a.k, NT);
-        partition_redundant<NT>(a, D, rr, ps, a.nchunks, part_stage(a, smem));
+        partition_redundant<NT>(a, D, rr, ps, a.nchunks, blockIdx.x, part_stage(a, smem));
         set_children(a, D, kid);
         stamp(a, it, 1);
         if (D.path == kDirect) {
@@ -1462,7 +1503,7 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
         // this rank's left count is needed for the children's row ranges:
         // rank the parent like the scan CTAs (no share of the scatter)
         RegRows rr;
-        partition_redundant<NT>(a, D, rr, ps, a.nchunks, part_stage(a, smem));
+        partition_redundant<NT>(a, D, rr, ps, a.nchunks, blockIdx.x, part_stage(a, smem));
         set_children(a, D, kid);
       } else {
         if (threadIdx.x == 0) {
@@ -1540,6 +1581,741 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
   }
 }
 
+// ---------------------------------------------------------------- wave grower
+//
+// Best-first growth expands ONE leaf per step (tree.cpp:210-258), and
+// grow_kernel above pays one split's latency chain (partition, histogram,
+// scans, barrier, pick: ~15 us) 254 times per 255-leaf tree while most splits
+// touch a few thousand rows. The wave grower (single rank) expands SEVERAL
+// leaves per wave and replays the reference's pick order over the results:
+//
+//  * A leaf's children (rows, histograms, best splits) depend only on the
+//    leaf, never on when it is split: the partitions are stable, the
+//    direct-path histograms exact fixed point, the shared-memory histograms a
+//    fixed-order sum over the same segments, the scans per feature. So the
+//    tree is bit-identical to grow_kernel's (tested).
+//  * Every CTA replays the reference loop on its own copy of the open-leaf
+//    pool: while the best open leaf (max gain, lowest output id on ties: the
+//    pool order, strict > at tree.cpp:212-218) is already expanded, COMMIT it
+//    — its children join the pool with output ids 2i+1, 2i+2 as
+//    tree.cpp:224-236 numbers them. The first best open leaf that is not
+//    expanded yet is the reference's next split, for certain.
+//  * The next wave expands that leaf plus up to wmax-1 speculative ones: the
+//    expandable nodes of the speculative tree with the largest min-gain along
+//    their path (best-first expands in that order up to ties). Speculation is
+//    bounded in total by `ecap`; an expansion the replay never commits is
+//    not emitted (its rows moved into the other ordered buffer, its own range
+//    in its buffer is intact, its children never enter the pool).
+//
+// A wave runs its small members (parent <= small_max rows) as (member,
+// feature chunk) items in one phase — each CTA ranks its member's parent in
+// registers, accumulates its chunk exactly, subtracts and scans — and its
+// large members through grow_kernel's paths, every CTA taking a chunk of
+// every large member: two-pass partition, direct or shared-memory histogram
+// of the smaller child, chunk finishes. The last CTA to finish a member's
+// chunks (atomic count) reduces the chunk winners and publishes the
+// children's records. Barriers per wave: 1 (small members only) to 4. The
+// output (split log, tree, committed records) is written once at the end
+// from the replayed commit log.
+
+constexpr int kWN = 1280;  // node ids per tree (shared-memory state)
+constexpr int kWL = 256;   // open leaves: num_leaves <= kWL
+constexpr int kWMax = 16;  // members per wave
+
+struct WaveSmem {
+  unsigned long long gkey[kWN];  // gain key of node n's best split (0: none)
+  float prio[kWN];               // min gain along the path from the root
+  short kid[kWN];                // left child once expanded, -1 before
+  unsigned char large[kWN];      // 0: small; runs the large-parent paths: 1 (<= spec_rows rows), 2
+  short avail[kWN];              // expandable: discovered, gain > 0, not expanded
+  unsigned long long fkey[kWL];  // the replay's open leaves with a split: gain key, node, output id
+  short fnode[kWL], fout[kWL];
+  short wave[kWMax];             // members: small ones first
+  int nav, nfr, committed, next, expanded, done, W, nsmall, nwc, wc, nwaves, hitems, ditems;
+};
+
+// Per-CTA state in global memory (written by the CTA's warp 0, read back by
+// the same CTA): the commit log [L][4] = node, left child node, output id,
+// bit c: child c was split later; the parent of each child pair; each node's
+// output id; whether a node was committed as a split.
+__host__ __device__ inline size_t wave_state_bytes(int num_leaves, int max_nodes) {
+  const size_t b = 16 * static_cast<size_t>(num_leaves) + 2 * static_cast<size_t>(max_nodes / 2 + 1) +
+                   2 * static_cast<size_t>(max_nodes) + static_cast<size_t>(max_nodes);
+  return (b + 255) / 256 * 256;
+}
+
+struct WaveLog {
+  int* clog;
+  short* ppar;
+  short* nout;
+  unsigned char* splitf;
+};
+
+__device__ __forceinline__ WaveLog wave_log(const GrowArgs& a) {
+  unsigned char* p = a.wstate + static_cast<size_t>(blockIdx.x) * a.wstate_stride;
+  WaveLog l;
+  l.clog = reinterpret_cast<int*>(p);
+  l.ppar = reinterpret_cast<short*>(l.clog + 4 * static_cast<size_t>(a.num_leaves));
+  l.nout = l.ppar + (a.max_nodes / 2 + 1);
+  l.splitf = reinterpret_cast<unsigned char*>(l.nout + a.max_nodes);
+  return l;
+}
+
+// Would the split of a node with these sizes run the shared-memory histogram
+// (grow_kernel's choice at pick time: kept, so the trees stay bit-identical)?
+__device__ __forceinline__ bool runs_large(const GrowArgs& a, int64_t count, int64_t nl) {
+  const int64_t nr = count - nl;
+  if (count > a.small_max) return true;
+  const bool ls = splittable(nl, a.min_data), rs = splittable(nr, a.min_data);
+  const int64_t ns = nl <= nr ? nl : nr;
+  return (ls || rs) && !(ns <= kDirectRows && ns * a.fchunk <= kDirectBudget);
+}
+
+// Warp 0 after a wave's barrier: the members' children (records published
+// before it) join the speculative tree.
+__device__ void wave_integrate(const GrowArgs& a, WaveSmem& w) {
+  const int lane = threadIdx.x;
+  const int rep = blockIdx.x % kRep;
+  const int W = w.W;
+  bool add = false;
+  int id = 0;
+  if (lane < 2 * W) {
+    const int x = w.wave[lane >> 1];
+    id = w.kid[x] + (lane & 1);
+    const NodeDev* P = a.nodes + static_cast<size_t>(rep) * a.max_nodes + id;
+    const double g = __ldcg(a.node_gain + static_cast<size_t>(rep) * a.max_nodes + id);
+    const int64_t n = __ldcg(&P->count);
+    const int64_t nl = __ldcg(&P->best.left_count);
+    const unsigned long long key = gain_key(g);
+    w.gkey[id] = key;
+    w.kid[id] = -1;
+    w.large[id] = runs_large(a, n, nl) ? (n <= a.spec_rows ? 1 : 2) : 0;
+    w.prio[id] = fminf(w.prio[x], static_cast<float>(g));
+    add = key != 0ull;
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, add);
+  if (add) w.avail[w.nav + __popc(bal & ((1u << lane) - 1u))] = static_cast<short>(id);
+  __syncwarp();
+  if (lane == 0) w.nav += __popc(bal);
+  __syncwarp();
+}
+
+// Speculation order: prio buckets of 1/4 octave (a positive float's bits >> 21).
+__device__ __forceinline__ int prio_bucket(float p) { return static_cast<int>(__float_as_uint(p) >> 21); }
+
+// Warp 0: bucket histogram (1024 counters in `hist`, shared memory) of the
+// expandable nodes with pred(node); returns the highest bucket B such that at
+// least `want` (>= 1) of them lie in buckets >= B (0 when fewer exist).
+template <typename Pred>
+__device__ int bucket_select(const WaveSmem& w, unsigned* hist, int nav, int want, Pred pred) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int u = 0; u < 32; ++u) hist[u * 32 + lane] = 0u;
+  __syncwarp();
+  for (int i = lane; i < nav; i += 32) {
+    const int n = w.avail[i];
+    if (pred(n)) atomicAdd(hist + prio_bucket(w.prio[n]), 1u);
+  }
+  __syncwarp();
+  // lane l owns buckets [32 l, 32 l + 32); counts from the top
+  unsigned mine = 0u;
+#pragma unroll 8
+  for (int u = 0; u < 32; ++u) mine += hist[lane * 32 + u];
+  // inclusive suffix sum over lanes (lane 31 = top buckets)
+  unsigned suf = mine;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned v = __shfl_down_sync(0xffffffffu, suf, off);
+    if (lane + off < 32) suf += v;
+  }
+  const unsigned above = suf - mine;  // nodes in the buckets of the lanes above
+  const bool cross = above < static_cast<unsigned>(want) && suf >= static_cast<unsigned>(want);
+  const unsigned bal = __ballot_sync(0xffffffffu, cross);
+  if (bal == 0u) return 0;  // fewer than `want`: every bucket
+  const int l = 31 - __clz(bal);  // the only crossing lane
+  int B = 0;
+  if (lane == l) {
+    unsigned c = above;
+    for (int u = 31; u >= 0; --u) {
+      c += hist[lane * 32 + u];
+      if (c >= static_cast<unsigned>(want)) {
+        B = lane * 32 + u;
+        break;
+      }
+    }
+  }
+  return __shfl_sync(0xffffffffu, B, l);
+}
+
+// Every CTA (warp 0, identical everywhere): replay the reference's picks over
+// the expanded leaves (commit), then choose the next wave. Whole CTA.
+template <int NT>
+__device__ void wave_select(const GrowArgs& a, WaveSmem& w, unsigned char* smem_dyn) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const int L1 = a.num_leaves - 1;
+    const WaveLog lg = wave_log(a);
+    int* clog = lg.clog;
+    int nfr = w.nfr, committed = w.committed;
+    int err = lane == 0 ? error_of(a) : 0;
+    err = __shfl_sync(0xffffffffu, err, 0);
+    int best = -1;
+    while (err == kErrNone && committed < L1) {
+      unsigned long long hk = 0ull;
+      unsigned lk = 0u;
+      int idx = -1;
+#pragma unroll 8
+      for (int i = lane; i < nfr; i += 32) {
+        const unsigned long long h = w.fkey[i];
+        const unsigned l = 0xFFFFFFFFu - static_cast<unsigned>(w.fout[i]);
+        const bool take = h > hk || (h == hk && l > lk);
+        hk = take ? h : hk;
+        lk = take ? l : lk;
+        idx = take ? i : idx;
+      }
+      unsigned long long H = hk;
+      unsigned Lk = lk;
+      warp_argmax_key(H, Lk);
+      if (H == 0ull) break;
+      const unsigned bal = __ballot_sync(0xffffffffu, hk == H && lk == Lk);
+      const int e = __shfl_sync(0xffffffffu, idx, __ffs(bal) - 1);
+      const int x = w.fnode[e];
+      const int kd = w.kid[x];
+      if (kd < 0) {
+        best = e;
+        break;
+      }
+      // commit: the reference splits x now (tree.cpp:220-256)
+      if (lane == 0) {
+        const int o = w.fout[e];
+        clog[4 * committed] = x;
+        clog[4 * committed + 1] = kd;
+        clog[4 * committed + 2] = o;
+        clog[4 * committed + 3] = 0;
+        if (o > 0) clog[4 * ((o - 1) >> 1) + 3] |= 1 << ((o - 1) & 1);
+        lg.splitf[x] = 1;
+        lg.nout[kd] = static_cast<short>(2 * committed + 1);
+        lg.nout[kd + 1] = static_cast<short>(2 * committed + 2);
+        const int t = nfr - 1;  // the last entry fills the hole
+        w.fkey[e] = w.fkey[t];
+        w.fnode[e] = w.fnode[t];
+        w.fout[e] = w.fout[t];
+        int m = t;
+        for (int c = 0; c < 2; ++c) {
+          if (w.gkey[kd + c] == 0ull) continue;
+          w.fkey[m] = w.gkey[kd + c];
+          w.fnode[m] = static_cast<short>(kd + c);
+          w.fout[m] = static_cast<short>(2 * committed + 1 + c);
+          ++m;
+        }
+      }
+      __syncwarp();
+      nfr += (w.gkey[kd] != 0ull ? 1 : 0) + (w.gkey[kd + 1] != 0ull ? 1 : 0) - 1;
+      ++committed;
+    }
+    if (lane == 0 && w.nwaves > 0) stamp(a, w.nwaves - 1, 8);
+    int W = 0, nsmall = 0;
+    if (best >= 0 && committed < L1 && err == kErrNone) {
+      const int ps = w.fnode[best];
+      int m = min(L1 - committed, a.wmax);
+      m = max(1, min(m, a.ecap - w.expanded));
+      const int nav = w.nav;
+      // speculation: ~the m-1 best other expandable nodes by prio (1/4-octave
+      // buckets, index order within one), small ones only unless
+      // HBG_WAVE_LARGE admits large ones of <= spec_rows rows among the R best
+      // (R = the commits still to come): a speculative large expansion costs a
+      // partition and histogram pass over its rows
+      unsigned* hist = reinterpret_cast<unsigned*>(smem_dyn);
+      int br = 1 << 30;
+      if (a.wlarge > 0 && L1 - committed - 1 > 0)
+        br = bucket_select(w, hist, nav, L1 - committed - 1, [&](int n) { return n != ps; });
+      const auto cand = [&](int n) {
+        return n != ps && (!w.large[n] || (w.large[n] == 1 && prio_bucket(w.prio[n]) >= br));
+      };
+      const int want = m - 1;
+      const int B = want > 0 ? bucket_select(w, hist, nav, want, cand) : 1 << 30;
+      if (lane == 0) w.wave[0] = static_cast<short>(ps);
+      __syncwarp();
+      W = 1;
+      if (want > 0) {
+        // every candidate in the buckets above B (fewer than want) ...
+        for (int i0 = 0; i0 < nav; i0 += 32) {
+          const int i = i0 + lane;
+          const int n = i < nav ? w.avail[i] : -1;
+          const bool el = n >= 0 && cand(n) && prio_bucket(w.prio[n]) > B;
+          const unsigned bal = __ballot_sync(0xffffffffu, el);
+          if (el) w.wave[W + __popc(bal & ((1u << lane) - 1u))] = static_cast<short>(n);
+          W += __popc(bal);
+        }
+        __syncwarp();
+        // ... then the best of bucket B by exact prio (ties: lowest node id),
+        // from its first 32 candidates, one per lane
+        int mine = -1, got = 0;
+        for (int i0 = 0; i0 < nav && got < 32; i0 += 32) {
+          const int i = i0 + lane;
+          const int n = i < nav ? w.avail[i] : -1;
+          const bool el = n >= 0 && cand(n) && prio_bucket(w.prio[n]) == B;
+          const unsigned bal = __ballot_sync(0xffffffffu, el);
+          // lane r of the collected list receives the r-th hit
+          const int src = got;
+          for (unsigned bb = bal; bb != 0u && got < 32; bb &= bb - 1u) {
+            const int from = __ffs(bb) - 1;
+            const int v = __shfl_sync(0xffffffffu, n, from);
+            if (lane == got) mine = v;
+            ++got;
+          }
+          (void)src;
+        }
+        unsigned long long key = mine >= 0 ? ((static_cast<unsigned long long>(__float_as_uint(w.prio[mine])) << 32) |
+                                              (0xFFFFFFFFu - static_cast<unsigned>(mine)))
+                                           : 0ull;
+        while (W < 1 + want) {
+          unsigned long long best_key = key;
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            const unsigned long long o = __shfl_xor_sync(0xffffffffu, best_key, off);
+            best_key = o > best_key ? o : best_key;
+          }
+          if (best_key == 0ull) break;
+          const int n = static_cast<int>(0xFFFFFFFFu - static_cast<unsigned>(best_key));
+          if (lane == 0) w.wave[W] = static_cast<short>(n);
+          if (key == best_key) key = 0ull;
+          ++W;
+        }
+        __syncwarp();
+      }
+      if (lane == 0 && w.nwaves > 0) stamp(a, w.nwaves - 1, 9);
+      // members leave the expandable list; small members first
+      for (int j = lane; j < W; j += 32) w.kid[w.wave[j]] = -2;  // mark
+      __syncwarp();
+      int nav2 = 0;  // compaction in place: a round's reads precede its writes, which land below them
+      for (int i0 = 0; i0 < nav; i0 += 32) {
+        const int i = i0 + lane;
+        const short n = i < nav ? w.avail[i] : static_cast<short>(0);
+        const bool keep = i < nav && w.kid[n] != -2;
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        __syncwarp();
+        if (keep) w.avail[nav2 + __popc(bal & ((1u << lane) - 1u))] = n;
+        nav2 += __popc(bal);
+        __syncwarp();
+      }
+      short mem = lane < W ? w.wave[lane] : 0;
+      const bool sm = lane < W && !w.large[mem];
+      const unsigned bs = __ballot_sync(0xffffffffu, sm), bl = __ballot_sync(0xffffffffu, lane < W && !sm);
+      nsmall = __popc(bs);
+      const int pos = sm ? __popc(bs & ((1u << lane) - 1u)) : nsmall + __popc(bl & ((1u << lane) - 1u));
+      __syncwarp();
+      if (lane < W) {
+        w.wave[pos] = mem;
+        w.kid[mem] = static_cast<short>(w.next + 2 * pos);
+        lg.ppar[(w.next + 2 * pos - 1) >> 1] = mem;
+        lg.splitf[w.next + 2 * pos] = lg.splitf[w.next + 2 * pos + 1] = 0;
+      }
+      __syncwarp();
+      if (lane == 0) w.nav = nav2;
+    }
+    if (lane == 0) {
+      w.nfr = nfr;
+      w.committed = committed;
+      w.done = W == 0 ? 1 : 0;
+      w.W = W;
+      w.nsmall = nsmall;
+      w.next += 2 * W;
+      w.expanded += W;
+      // small members' feature chunks: ~one (member, chunk) item per CTA
+      const int target = nsmall > 0 ? max(1, static_cast<int>(gridDim.x) / nsmall) : 1;
+      w.wc = min(a.wcap, max(1, (a.d + target - 1) / target));
+      w.nwc = (a.d + w.wc - 1) / w.wc;
+    }
+  }
+  __syncthreads();
+}
+
+// Warp 0 (lane j: member j): the members' splits as Descs (the parents'
+// records were published before an earlier barrier); thread 0 then lays out
+// the shared-memory histogram items. Whole CTA.
+__device__ void load_members(const GrowArgs& a, WaveSmem& w, Desc* Dm) {
+  const int lane = threadIdx.x;
+  if (lane < w.W) {
+    Desc& D = Dm[lane];
+    const int x = w.wave[lane], kd = w.kid[x];
+    const bool large = lane >= w.nsmall;
+    const NodeDev* P = a.nodes + static_cast<size_t>(blockIdx.x % kRep) * a.max_nodes + x;
+    const int64_t begin = __ldcg(&P->begin), count = __ldcg(&P->count), gcount = __ldcg(&P->gcount);
+    const int buf = __ldcg(&P->buf);
+    const int64_t nl = __ldcg(&P->best.left_count);
+    D.done = 0;
+    D.iter = w.nwaves;
+    D.mslot = lane;
+    D.pbase = 0;
+    D.parent = x;
+    D.left_id = kd;
+    D.right_id = kd + 1;
+    D.buf_in = buf;
+    D.buf_out = 1 - buf;
+    D.begin = begin;
+    D.count = count;
+    D.feature = __ldcg(&P->best.feature);
+    D.thr = __ldcg(&P->best.threshold_bin);
+    D.nl = nl;
+    D.nr = gcount - nl;
+    if (D.nl <= 0 || D.nr <= 0) set_error(a, kErrEmptySide);  // tree.cpp:124-126
+    D.lsplit = splittable(D.nl, a.min_data);
+    D.rsplit = splittable(D.nr, a.min_data);
+    D.small_is_left = D.nl <= D.nr;
+    const int64_t ns = D.nl <= D.nr ? D.nl : D.nr;
+    D.items = 0;
+    if (!(D.lsplit || D.rsplit)) {
+      D.path = kNoHist;
+    } else if (!large || (ns <= kDirectRows && ns * a.fchunk <= kDirectBudget)) {
+      D.path = kDirect;
+    } else {  // grow_kernel's segment plan (pick)
+      D.path = kSmem;
+      const int64_t min_rows = static_cast<int64_t>(a.wpg) * 32 * 2 * a.rpl;
+      int64_t nseg = gridDim.x / a.nblocks;
+      if (nseg < 1) nseg = 1;
+      const int64_t cap = (ns + min_rows - 1) / min_rows;
+      if (nseg > cap) nseg = cap;
+      int64_t seg_len = (ns + nseg - 1) / nseg;
+      seg_len = (seg_len + 31) / 32 * 32;
+      nseg = (ns + seg_len - 1) / seg_len;
+      D.seg_len = seg_len;
+      D.nseg = static_cast<int32_t>(nseg);
+      D.items = static_cast<int32_t>(nseg * a.nblocks);
+    }
+  }
+  __syncwarp();
+  if (threadIdx.x == 0) {
+    int h = 0, dd = 0;
+    for (int j = w.nsmall; j < w.W; ++j) {
+      Dm[j].pbase = h;
+      h += Dm[j].items;
+      dd += Dm[j].path == kDirect ? a.nchunks : 0;
+    }
+    w.hitems = h;
+    w.ditems = dd;
+  }
+  __syncthreads();
+}
+
+// The last CTA to finish member D's chunks: per-child winner over the chunk
+// winners (as winners()), the children's records and gains, every replica.
+template <int NT>
+__device__ void publish_member(const GrowArgs& a, const Desc& D, int nwc) {
+  __shared__ NodeDev rec[2];
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x, child = lane >> 4, sub = lane & 15;
+    const bool want = D.path != kNoHist && (child == 0 ? D.lsplit : D.rsplit);
+    Cand c{0.0, -1, -1, 0.0, 0.0, 0};
+    unsigned long long hk = 0ull;
+    unsigned lk = 0u;
+    if (want) {
+      const Cand* base = a.wcand + (static_cast<size_t>(D.mslot) * 2 + child) * a.wcstride;
+      for (int i = sub; i < nwc; i += 16) {
+        Cand o;
+        o.gain = __ldcg(&base[i].gain);
+        o.f = __ldcg(&base[i].f);
+        o.b = __ldcg(&base[i].b);
+        o.lg = __ldcg(&base[i].lg);
+        o.lh = __ldcg(&base[i].lh);
+        o.lc = __ldcg(&base[i].lc);
+        const unsigned long long h = o.f >= 0 ? gain_key(o.gain) : 0ull;
+        const unsigned l = 0xFFFFFFFFu - ((static_cast<unsigned>(o.f) << 12) | static_cast<unsigned>(o.b));
+        const bool take = h > hk || (h == hk && l > lk);
+        hk = take ? h : hk;
+        lk = take ? l : lk;
+        if (take) c = o;
+      }
+    }
+    warp_argmax_key(hk, lk, 16);
+    {
+      const unsigned mine = (hk != 0ull && c.f >= 0 && gain_key(c.gain) == hk &&
+                             0xFFFFFFFFu - ((static_cast<unsigned>(c.f) << 12) | static_cast<unsigned>(c.b)) == lk)
+                                ? 1u : 0u;
+      const unsigned bal = __ballot_sync(0xffffffffu, mine) & (child == 0 ? 0x0000FFFFu : 0xFFFF0000u);
+      const int src = bal ? __ffs(bal) - 1 : lane;
+      const Cand wv = shfl_cand(c, src);
+      c = hk == 0ull ? Cand{0.0, -1, -1, 0.0, 0.0, 0} : wv;
+    }
+    if (sub == 0) {
+      NodeDev& r = rec[child];
+      r.begin = child == 0 ? D.begin : D.begin + D.nl_loc;
+      r.count = child == 0 ? D.nl_loc : D.count - D.nl_loc;
+      r.gcount = child == 0 ? D.nl : D.nr;
+      r.grad = D.tot[2 * child];
+      r.hess = D.tot[2 * child + 1];
+      r.buf = D.buf_out;
+      if (want) {
+        write_split(c, r.grad, r.hess, r.gcount, a.lambda, &r.best);
+        r.has_best = c.f >= 0 ? 1 : 0;
+      } else {
+        r.best = hbg_split{};
+        r.best.feature = -1;
+        r.has_best = 0;
+      }
+    }
+  }
+  __syncthreads();
+  constexpr int Wd = static_cast<int>(sizeof(NodeDev) / 8);
+  for (int t = threadIdx.x; t < 2 * kRep * Wd; t += NT) {
+    const int ch = t / (kRep * Wd), r = (t / Wd) % kRep, q = t % Wd;
+    reinterpret_cast<double*>(a.nodes + static_cast<size_t>(r) * a.max_nodes + D.left_id + ch)[q] =
+        reinterpret_cast<const double*>(&rec[ch])[q];
+  }
+  if (threadIdx.x < 2 * kRep) {
+    const int ch = threadIdx.x / kRep, r = threadIdx.x % kRep;
+    a.node_gain[static_cast<size_t>(r) * a.max_nodes + D.left_id + ch] = rec[ch].has_best ? rec[ch].best.gain : -1.0;
+  }
+  __syncthreads();
+}
+
+// One chunk of member D is done (its winners are in wcand): count it; the
+// last of the member's nwc chunks publishes the children. Whole CTA.
+template <int NT>
+__device__ void chunk_done(const GrowArgs& a, const Desc& D, int nwc) {
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned old = atomicAdd(a.wcnt + D.mslot, 1u);
+    s_last = old == static_cast<unsigned>(nwc - 1) ? 1 : 0;
+    if (s_last) {
+      a.wcnt[D.mslot] = 0u;  // every chunk has arrived: reset for the next wave
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  if (s_last) publish_member<NT>(a, D, nwc);
+}
+
+__device__ __forceinline__ CandOut wave_out(const GrowArgs& a, const Desc& D, int c) {
+  return CandOut{a.wcand + static_cast<size_t>(D.mslot) * 2 * a.wcstride + c, 1, 0, a.wcstride};
+}
+
+// CTA owning (member, chunk) item x of I items over G CTAs (contiguous runs).
+__device__ __forceinline__ int item_cta(int x, int I, int G) {
+  return I <= G ? x : static_cast<int>((static_cast<int64_t>(x + 1) * G + I - 1) / I) - 1;
+}
+
+// Small members: items (member, feature chunk of wc features); every CTA of a
+// member ranks its parent in registers and writes one share of the output.
+template <int K, int NT>
+__device__ void wave_small(const GrowArgs& a, const WaveSmem& w, Desc* Dm, PartShared<NT>& ps, unsigned char* smem,
+                           double eg, double eh) {
+  const int G = gridDim.x, b = blockIdx.x;
+  const int nwc = w.nwc, wc = w.wc, I = w.nsmall * nwc;
+  int x0, x1;
+  if (I <= G) {
+    x0 = b < I ? b : I;
+    x1 = b < I ? b + 1 : I;
+  } else {
+    x0 = static_cast<int>(static_cast<int64_t>(b) * I / G);
+    x1 = static_cast<int>(static_cast<int64_t>(b + 1) * I / G);
+  }
+  int cur = -1;
+  RegRows rr;
+  for (int x = x0; x < x1; ++x) {
+    const int j = x / nwc, c = x - j * nwc;
+    Desc& D = Dm[j];
+    if (j != cur) {
+      const int bj0 = item_cta(j * nwc, I, G), bj1 = item_cta((j + 1) * nwc - 1, I, G);
+      partition_redundant<NT>(a, D, rr, ps, bj1 - bj0 + 1, b - bj0, part_stage(a, smem));
+      cur = j;
+    }
+    if (D.path == kDirect) {
+      const int f0 = c * wc, nf = min(wc, a.d - f0);
+      zero_direct(a, smem, nf * a.k, NT);
+      __syncthreads();
+      const uint32_t valid = rr.nvalid >= 32 ? ~0u : ((1u << rr.nvalid) - 1u);
+      const uint32_t want = (D.small_is_left ? rr.left : ~rr.left) & valid;
+      direct_accumulate(a, direct_acc(a, smem), nf * a.k, f0, nf, rr.row, rr.g, rr.h, want, eg, eh);
+      __syncthreads();
+      finish_range<K, NT>(a, D, f0, nf, 0, smem, wave_out(a, D, c));
+    }
+    chunk_done<NT>(a, D, nwc);
+  }
+}
+
+// Large members after their partition: direct-path items (member, chunk) and
+// shared-memory histogram items (member, segment, slice block) over all CTAs;
+// then (barrier) the shared-memory members' chunk finishes.
+template <int BITS, int K, int NT>
+__device__ void wave_large_hist(const GrowArgs& a, const WaveSmem& w, Desc* Dm, unsigned char* smem, double eg,
+                                double eh) {
+  const int G = gridDim.x;
+  const int hitems = w.hitems, total = w.hitems + w.ditems;
+  for (int x = blockIdx.x; x < total; x += G) {
+    if (x < hitems) {  // heavy items first
+      int j = w.nsmall;
+      while (Dm[j].path != kSmem || x >= Dm[j].pbase + Dm[j].items) ++j;
+      hist_smem_item<BITS, K, NT>(a, Dm[j], x - Dm[j].pbase, smem);
+      continue;
+    }
+    int r = x - hitems, j = w.nsmall;
+    while (Dm[j].path != kDirect || r >= a.nchunks) {
+      if (Dm[j].path == kDirect) r -= a.nchunks;
+      ++j;
+    }
+    const Desc& D = Dm[j];
+    const int c = r, f0 = c * a.fchunk, nf = min(a.fchunk, a.d - f0);
+    zero_direct(a, smem, nf * a.k, NT);
+    __syncthreads();
+    const int32_t* rows;
+    const float* g;
+    const float* h;
+    int64_t n;
+    small_child(a, D, rows, g, h, n);
+    for (int64_t j0 = 0; j0 < n; j0 += static_cast<int64_t>(NT) * kItems) {
+      int32_t rw[kItems];
+      float gg[kItems], hh[kItems];
+      uint32_t mask = 0;
+#pragma unroll
+      for (int u = 0; u < kItems; ++u) {
+        const int64_t q = j0 + static_cast<int64_t>(u) * NT + threadIdx.x;
+        const bool ok = q < n;
+        rw[u] = ok ? __ldcg(rows + q) : 0;
+        gg[u] = ok ? __ldcg(g + q) : 0.f;
+        hh[u] = ok ? __ldcg(h + q) : 0.f;
+        mask |= ok ? 1u << u : 0u;
+      }
+      direct_accumulate(a, direct_acc(a, smem), nf * a.k, f0, nf, rw, gg, hh, mask, eg, eh);
+    }
+    __syncthreads();
+    finish_range<K, NT>(a, D, f0, nf, 0, smem, wave_out(a, D, c));
+    chunk_done<NT>(a, D, a.nchunks);
+  }
+  if (hitems == 0) return;
+  grid_sync(a);
+  int nsm = 0;
+  for (int j = w.nsmall; j < w.W; ++j) nsm += Dm[j].path == kSmem ? 1 : 0;
+  for (int x = blockIdx.x; x < nsm * a.nchunks; x += G) {
+    int q = x / a.nchunks, j = w.nsmall;
+    const int c = x - q * a.nchunks;
+    while (Dm[j].path != kSmem || q > 0) {
+      if (Dm[j].path == kSmem) --q;
+      ++j;
+    }
+    const Desc& D = Dm[j];
+    const int f0 = c * a.fchunk;
+    finish_range<K, NT>(a, D, f0, min(a.fchunk, a.d - f0), 0, smem, wave_out(a, D, c));
+    chunk_done<NT>(a, D, a.nchunks);
+  }
+}
+
+// The output from the replayed commit log (every CTA holds the same log):
+// split i, the split node, its two children (tree.cpp:224-246). And for the
+// score update: the rows of every unexpanded node (the leaves of the
+// speculative tree partition the rows; an unexpanded node's range in its
+// buffer is never written after its creation) with the value of the final
+// leaf that contains it.
+__device__ void wave_emit(const GrowArgs& a, const WaveSmem& w) {
+  const WaveLog lg = wave_log(a);
+  const int committed = w.committed;
+  const int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < committed; i += stride) {
+    const int x = lg.clog[4 * i], kd = lg.clog[4 * i + 1], o = lg.clog[4 * i + 2], later = lg.clog[4 * i + 3];
+    const hbg_split bs = load_split(&a.nodes[x].best);
+    a.split_log[i] = bs;
+    a.tree[o] = hbg_tree_node{bs.feature, bs.threshold_bin, 2 * i + 1, 2 * i + 2, 0.0};
+    for (int c = 0; c < 2; ++c) {
+      if ((later >> c) & 1) continue;  // a child split later is written by its own commit
+      const NodeDev* q = a.nodes + kd + c;
+      a.tree[2 * i + 1 + c] = hbg_tree_node{-1, -1, -1, -1, leaf_value(__ldcg(&q->grad), __ldcg(&q->hess), a.lambda)};
+    }
+  }
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < w.next; u += stride) {
+    LeafRange r{0, 0, 0.0, 0, 0};
+    if (w.kid[u] < 0) {
+      int z = u;  // the final leaf above u: the first node whose parent was committed as a split
+      while (z != 0 && !lg.splitf[lg.ppar[(z - 1) >> 1]]) z = lg.ppar[(z - 1) >> 1];
+      const NodeDev* q = a.nodes + u;
+      const NodeDev* f = a.nodes + z;
+      r = LeafRange{__ldcg(&q->begin), __ldcg(&q->count), leaf_value(__ldcg(&f->grad), __ldcg(&f->hess), a.lambda),
+                    __ldcg(&q->buf), 0};
+    }
+    a.ranges[u] = r;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.counts[0] = committed;
+    a.counts[1] = 1 + 2 * committed;
+    a.counts[4] = w.next;
+  }
+}
+
+template <int BITS, int K>
+__global__ void __launch_bounds__(grow_threads<K>(), 1) grow_wave_kernel(GrowArgs a) {
+  constexpr int NT = grow_threads<K>();
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ PartShared<NT> ps;
+  __shared__ Desc Dm[kWMax];
+  __shared__ WaveSmem w;
+  // the root (histogram, totals, best split computed by host-launched kernels)
+  if (threadIdx.x == 0) {
+    const double G = __ldcg(a.root_tot), H = __ldcg(a.root_tot + 1);
+    const hbg_split bs = load_split(&a.nodes[0].best);
+    const int hb = bs.feature >= 0 ? 1 : 0;
+    if (blockIdx.x == 0) {
+      const NodeDev rec{0, a.root_count, a.root_count, G, H, bs, 0, hb};
+      for (int q = 0; q < kRep; ++q) a.nodes[static_cast<size_t>(q) * a.max_nodes] = rec;
+      for (int q = 0; q < kRep; ++q) a.node_gain[static_cast<size_t>(q) * a.max_nodes] = hb ? bs.gain : -1.0;
+      a.tree[0] = hbg_tree_node{-1, -1, -1, -1, leaf_value(G, H, a.lambda)};
+    }
+    const WaveLog lg = wave_log(a);
+    lg.nout[0] = 0;
+    lg.splitf[0] = 0;
+    const unsigned long long k0 = hb ? gain_key(bs.gain) : 0ull;
+    w.gkey[0] = k0;
+    w.prio[0] = hb ? static_cast<float>(bs.gain) : 0.f;
+    w.kid[0] = -1;
+    w.large[0] = runs_large(a, a.root_count, hb ? bs.left_count : 0) ? (a.root_count <= a.spec_rows ? 1 : 2) : 0;
+    w.nav = w.nfr = 0;
+    w.committed = w.expanded = w.done = w.W = w.nsmall = w.nwaves = 0;
+    w.next = 1;
+    if (k0 != 0ull && a.num_leaves >= 2) {
+      w.fkey[0] = k0;
+      w.fnode[0] = 0;
+      w.fout[0] = 0;
+      w.avail[0] = 0;
+      w.nfr = w.nav = 1;
+    }
+  }
+  grid_sync(a);  // CTA 0's root records
+  wave_select<NT>(a, w, smem);
+  const double eg = ldexp(1.0, a.exps[0]), eh = ldexp(1.0, a.exps[1]);  // fixed-point scales
+  while (!w.done) {
+    if (a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long* t = a.prof + static_cast<size_t>(w.nwaves) * kProfSlots;
+      t[7] = static_cast<unsigned long long>(w.W - w.nsmall);
+      t[10] = static_cast<unsigned long long>(w.W);
+      t[11] = static_cast<unsigned long long>(w.committed);
+    }
+    stamp(a, w.nwaves, 0);
+    load_members(a, w, Dm);
+    for (int j = w.nsmall; j < w.W; ++j) partition_count<NT>(a, Dm[j], ps);
+    if (w.nsmall > 0) wave_small<K, NT>(a, w, Dm, ps, smem, eg, eh);
+    stamp(a, w.nwaves, 1);
+    if (w.W > w.nsmall) {
+      grid_sync(a);
+      for (int j = w.nsmall; j < w.W; ++j) partition_scatter<NT>(a, Dm[j], ps, smem);
+      stamp(a, w.nwaves, 2);
+      grid_sync(a);
+      for (int j = w.nsmall; j < w.W; ++j)
+        if (Dm[j].path == kNoHist && blockIdx.x == 0) publish_member<NT>(a, Dm[j], 0);
+      wave_large_hist<BITS, K, NT>(a, w, Dm, smem, eg, eh);
+    }
+    stamp(a, w.nwaves, 3);
+    grid_sync(a);
+    stamp(a, w.nwaves, 4);
+    if (threadIdx.x < 32) wave_integrate(a, w);
+    stamp(a, w.nwaves, 6);
+    if (threadIdx.x == 0) ++w.nwaves;
+    wave_select<NT>(a, w, smem);
+    stamp(a, w.nwaves - 1, 5);
+  }
+  wave_emit(a, w);
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.counts[3] = w.nwaves;
+}
+
 // scores[row] += lr * value for every leaf node (tree[i].left < 0) of a grown
 // tree (boosting.cpp:48-50); every leaf owns a contiguous ordered-buffer range.
 __global__ void score_update_nodes_kernel(const NodeDev* __restrict__ nodes,
@@ -1558,14 +2334,41 @@ __global__ void score_update_nodes_kernel(const NodeDev* __restrict__ nodes,
 
 template <int BITS, int K>
 struct GrowKernel {
-  static void* fn() { return reinterpret_cast<void*>(grow_kernel<BITS, K>); }
+  static void* fn(bool wave) {
+    return wave ? reinterpret_cast<void*>(grow_wave_kernel<BITS, K>) : reinterpret_cast<void*>(grow_kernel<BITS, K>);
+  }
 };
 
-void* grow_fn(int bits, int k_alloc) {
-  if (bits == 4) return GrowKernel<4, 16>::fn();
-  if (k_alloc == 64) return GrowKernel<8, 64>::fn();
-  if (k_alloc == 128) return GrowKernel<8, 128>::fn();
-  return GrowKernel<8, 256>::fn();
+void* grow_fn(int bits, int k_alloc, bool wave) {
+  if (bits == 4) return GrowKernel<4, 16>::fn(wave);
+  if (k_alloc == 64) return GrowKernel<8, 64>::fn(wave);
+  if (k_alloc == 128) return GrowKernel<8, 128>::fn(wave);
+  return GrowKernel<8, 256>::fn(wave);
+}
+
+// The wave grower runs single-rank trees unless HBG_GROW=legacy, and only
+// while its node slots (speculative expansions included) fit kWaveSlotBudget.
+constexpr size_t kWaveSlotBudget = size_t(4) << 30;
+
+// Speculative expansions allowed beyond the num_leaves-1 the tree commits;
+// -1: the wave grower does not apply (row shards, > kWL leaves, 256-bin
+// slots — the shared-memory state would cost the histogram a third of its
+// warps — or node slots beyond kWN / kWaveSlotBudget).
+int wave_extra(const PersistentGrowArgs& h) {
+  const char* e = std::getenv("HBG_GROW");
+  if (h.nranks > 1 || (e != nullptr && std::strcmp(e, "legacy") == 0)) return -1;
+  if (h.num_leaves > kWL || (h.bits != 4 && h.k > 128)) return -1;
+  const int L1 = std::max(0, h.num_leaves - 1);
+  const size_t slot = static_cast<size_t>(3) * h.d * h.k * sizeof(double);
+  const long long fit = std::min<long long>(kWN, static_cast<long long>(kWaveSlotBudget / std::max<size_t>(slot, 1)));
+  const long long x = std::min<long long>(L1, (fit - 1) / 2 - 2LL * L1);
+  return x < 0 ? -1 : static_cast<int>(x);
+}
+
+int wave_max_members() {
+  const char* e = std::getenv("HBG_WAVE_MAX");
+  const int m = e != nullptr ? std::atoi(e) : 16;
+  return std::max(1, std::min(kWMax, m));
 }
 
 int grow_nt(int k_alloc) { return k_alloc >= 256 ? grow_threads<256>() : grow_threads<64>(); }
@@ -1580,6 +2383,10 @@ size_t grow_static_smem(void* fn) {
 
 struct GrowGeom {
   int k_alloc, nt, gb, wpg, nblocks, fchunk, nchunks, ctas;
+  int cchunk, wcap;  // chunk capacity of the shared-memory layout; wave chunk limit
+  bool wave;
+  int extra, ecap, wmax, max_nodes;
+  size_t wcstride;
   size_t smem, part_values;
 };
 
@@ -1589,7 +2396,14 @@ GrowGeom grow_geometry(const PersistentGrowArgs& h, int device) {
   g.nt = grow_nt(g.k_alloc);
   const size_t cells = static_cast<size_t>(g.k_alloc) * 32;
   const size_t ghw = cells * 8, cntw = cells * 4;
-  const size_t smem_max = kSmemMax - grow_static_smem(grow_fn(h.bits, g.k_alloc));
+  g.extra = wave_extra(h);
+  g.wave = g.extra >= 0;
+  // both kernels lay out the shared-memory histogram for the same budget
+  // when the wave kernel applies to this shape (the partials, hence the
+  // trees, are then bit-identical between them)
+  const bool wave_shape = h.num_leaves <= kWL && (h.bits == 4 || h.k <= 128);
+  const size_t smem_max = kSmemMax - std::max(grow_static_smem(grow_fn(h.bits, g.k_alloc, false)),
+                                              wave_shape ? grow_static_smem(grow_fn(h.bits, g.k_alloc, true)) : 0);
   const int max_warps = g.nt / 32;
   int gb = 0, warps = 0;
   for (int cand = 1; cand <= std::min(h.num_groups, max_warps); ++cand) {
@@ -1612,8 +2426,15 @@ GrowGeom grow_geometry(const PersistentGrowArgs& h, int device) {
   g.nchunks = std::max(1, (h.d + g.fchunk - 1) / g.fchunk);
   const size_t hist_smem = static_cast<size_t>(g.gb * g.wpg) * ghw + g.gb * cntw;
   // finish: fp64 staging of both children + the direct fixed-point accumulator
-  const size_t scan_smem = static_cast<size_t>(g.fchunk) * h.k * (6 * sizeof(double) + 20);
-  const size_t part_smem = (scan_smem + 15) / 16 * 16 + static_cast<size_t>(kItems) * g.nt * 12;  // + staging
+  // (+ the small-parent partition staging), per feature of a chunk
+  const size_t per_feature = static_cast<size_t>(h.k) * (6 * sizeof(double) + 20);
+  const size_t stage_smem = static_cast<size_t>(kItems) * g.nt * 12;
+  auto part_smem_of = [&](int f) { return (f * per_feature + 15) / 16 * 16 + stage_smem; };
+  // wave chunks: as many features as the shared memory holds (up to d)
+  g.wcap = 1;
+  while (g.wcap < h.d && part_smem_of(g.wcap + 1) <= smem_max) ++g.wcap;
+  g.cchunk = std::max(g.fchunk, g.wave ? g.wcap : g.fchunk);
+  const size_t part_smem = part_smem_of(g.cchunk);
   const size_t large_part_smem = static_cast<size_t>(kPartItems) * g.nt * (2 * 13 + 2);  // 2 x (row, g, h, flag) + slot
   g.smem = std::max({hist_smem, part_smem, large_part_smem});
   require(g.ctas <= g.nt, "more CTAs than threads per CTA (per-CTA records are scanned one per thread)");
@@ -1621,13 +2442,23 @@ GrowGeom grow_geometry(const PersistentGrowArgs& h, int device) {
                               "(too many features for one grid)");
   const size_t items = static_cast<size_t>(std::max(g.ctas, g.nblocks));
   g.part_values = items * g.gb * cells;
+  const int L1 = std::max(0, h.num_leaves - 1);
+  g.wmax = wave_max_members();
+  g.wcstride = static_cast<size_t>(std::max({g.ctas, g.nchunks, (h.d + g.wcap - 1) / g.wcap}));
+  if (g.wave) g.part_values *= static_cast<size_t>(g.wmax);  // every large member of a wave
+  g.ecap = L1 + std::max(0, g.extra);
+  // node ids: the root + 2 per expansion; speculative expansions stop at
+  // ecap, the certain ones (<= L1) may go past it
+  g.max_nodes = g.wave ? 1 + 2 * (g.ecap + L1) : std::max(1, 2 * h.num_leaves - 1);
   return g;
 }
 
 }  // namespace
 
-size_t grow_nodes_bytes(int num_leaves) {  // kRep replicas; replica 0 first
-  return static_cast<size_t>(kRep) * std::max(1, 2 * num_leaves - 1) * sizeof(NodeDev);
+int grow_max_nodes(const PersistentGrowArgs& h, int device) { return grow_geometry(h, device).max_nodes; }
+
+size_t grow_nodes_bytes(int max_nodes) {  // kRep replicas; replica 0 first
+  return static_cast<size_t>(kRep) * std::max(1, max_nodes) * sizeof(NodeDev);
 }
 
 size_t grow_root_split_offset() { return offsetof(NodeDev, best); }
@@ -1640,24 +2471,30 @@ size_t grow_exchange_doubles(const PersistentGrowArgs& h, int device) {
 
 size_t grow_scratch_bytes(const PersistentGrowArgs& h, int device) {
   const GrowGeom g = grow_geometry(h, device);
-  const size_t max_nodes = static_cast<size_t>(std::max(1, 2 * h.num_leaves - 1));
+  const size_t max_nodes = static_cast<size_t>(g.max_nodes);
   size_t b = 0;
   auto add = [&](size_t n) { b += (n + 255) / 256 * 256; };
   add(sizeof(unsigned));                      // barrier
   add(kRep * max_nodes * sizeof(double));     // node_gain
   add(kRep * max_nodes * sizeof(int));        // picked
   add(static_cast<size_t>(h.num_rows) + 16);  // flags
-  add(static_cast<size_t>(g.ctas) * 8);       // cta_left
-  add(static_cast<size_t>(g.ctas) * 32);      // cta_sums
+  add(static_cast<size_t>(g.ctas) * 8 * (g.wave ? g.wmax : 1));   // cta_left
+  add(static_cast<size_t>(g.ctas) * 32 * (g.wave ? g.wmax : 1));  // cta_sums
   add(g.part_values * 4 * 3);                 // part_g/h/c
   add(static_cast<size_t>(kRep * 2 * g.nchunks) * sizeof(Cand));
+  if (g.wave) {
+    add(static_cast<size_t>(2 * g.wmax) * g.wcstride * sizeof(Cand));           // wcand
+    add(static_cast<size_t>(g.wmax) * sizeof(unsigned));                        // wcnt
+    add(static_cast<size_t>(g.ctas) * wave_state_bytes(h.num_leaves, g.max_nodes));  // wstate
+    add(static_cast<size_t>(g.max_nodes) * sizeof(LeafRange));                       // ranges
+  }
   return b;
 }
 
 void configure_grow_kernels() {
-  for (int v = 0; v < 4; ++v) {
-    const int bits = v == 0 ? 4 : 8, k = v == 0 ? 16 : (v == 1 ? 64 : (v == 2 ? 128 : 256));
-    void* fn = grow_fn(bits, k);
+  for (int v = 0; v < 8; ++v) {
+    const int bits = (v & 3) == 0 ? 4 : 8, k = (v & 3) == 0 ? 16 : ((v & 3) == 1 ? 64 : ((v & 3) == 2 ? 128 : 256));
+    void* fn = grow_fn(bits, k, v >= 4);
     HBG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kSmemMax - grow_static_smem(fn))));
     set_max_shared_carveout(fn);
@@ -1673,7 +2510,7 @@ void launch_score_update_nodes(const void* nodes, const hbg_tree_node* tree, int
   HBG_LAUNCH_CHECK();
 }
 
-void launch_grow_persistent(const PersistentGrowArgs& h, int device, cudaStream_t s) {
+const void* launch_grow_persistent(const PersistentGrowArgs& h, int device, cudaStream_t s) {
   const GrowGeom g = grow_geometry(h, device);
   GrowArgs a{};
   a.packed = h.packed;
@@ -1707,6 +2544,14 @@ void launch_grow_persistent(const PersistentGrowArgs& h, int device, cudaStream_
   a.rpl = g.k_alloc >= 256 ? rows_per_lane<256>() : rows_per_lane<64>();
   a.fchunk = g.fchunk;
   a.nchunks = g.nchunks;
+  a.cchunk = g.cchunk;
+  a.wcap = g.wcap;
+  a.wmax = g.wmax;
+  a.wlarge = std::getenv("HBG_WAVE_LARGE") != nullptr ? std::atoi(std::getenv("HBG_WAVE_LARGE")) : 1;
+  a.spec_rows = std::getenv("HBG_WAVE_SPEC_ROWS") != nullptr ? std::atoll(std::getenv("HBG_WAVE_SPEC_ROWS")) : 262144;
+  a.wcstride = g.wcstride;
+  a.ecap = g.ecap;
+  a.small_max = static_cast<int64_t>(kItems) * g.nt;
   a.timeout_cycles = 4000000000LL;  // ~2 s: a hung barrier becomes an error, not a hang
   a.prof = h.prof;
   a.nranks = std::max(1, h.nranks);
@@ -1729,25 +2574,33 @@ void launch_grow_persistent(const PersistentGrowArgs& h, int device, cudaStream_
     p += (n + 255) / 256 * 256;
     return q;
   };
-  const size_t max_nodes = static_cast<size_t>(std::max(1, 2 * h.num_leaves - 1));
+  const size_t max_nodes = static_cast<size_t>(g.max_nodes);
   a.bar = reinterpret_cast<unsigned*>(take(sizeof(unsigned)));
   a.max_nodes = static_cast<int>(max_nodes);
   a.node_gain = reinterpret_cast<double*>(take(kRep * max_nodes * sizeof(double)));
   a.picked = reinterpret_cast<int*>(take(kRep * max_nodes * sizeof(int)));
   a.flags = take(static_cast<size_t>(h.num_rows) + 16);
-  a.cta_left = reinterpret_cast<int64_t*>(take(static_cast<size_t>(g.ctas) * 8));
-  a.cta_sums = reinterpret_cast<double*>(take(static_cast<size_t>(g.ctas) * 32));
+  a.cta_left = reinterpret_cast<int64_t*>(take(static_cast<size_t>(g.ctas) * 8 * (g.wave ? g.wmax : 1)));
+  a.cta_sums = reinterpret_cast<double*>(take(static_cast<size_t>(g.ctas) * 32 * (g.wave ? g.wmax : 1)));
   float* part = reinterpret_cast<float*>(take(g.part_values * 12));
   a.part_g = part;
   a.part_h = part + g.part_values;
   a.part_c = reinterpret_cast<uint32_t*>(part + 2 * g.part_values);
   a.cand = reinterpret_cast<Cand*>(take(static_cast<size_t>(kRep * 2 * g.nchunks) * sizeof(Cand)));
+  if (g.wave) {
+    a.wcand = reinterpret_cast<Cand*>(take(static_cast<size_t>(2 * g.wmax) * g.wcstride * sizeof(Cand)));
+    a.wcnt = reinterpret_cast<unsigned*>(take(static_cast<size_t>(g.wmax) * sizeof(unsigned)));
+    a.wstate_stride = wave_state_bytes(h.num_leaves, g.max_nodes);
+    a.wstate = take(static_cast<size_t>(g.ctas) * a.wstate_stride);
+    a.ranges = reinterpret_cast<LeafRange*>(take(static_cast<size_t>(g.max_nodes) * sizeof(LeafRange)));
+  }
   require(static_cast<size_t>(p - static_cast<unsigned char*>(h.scratch)) <= h.scratch_bytes,
           "grow scratch smaller than its layout");
   HBG_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned), s));
   HBG_CUDA(cudaMemsetAsync(a.picked, 0, kRep * max_nodes * sizeof(int), s));
   HBG_CUDA(cudaMemsetAsync(a.counts, 0, 8 * sizeof(int), s));
-  void* fn = grow_fn(h.bits, g.k_alloc);
+  if (g.wave) HBG_CUDA(cudaMemsetAsync(a.wcnt, 0, static_cast<size_t>(g.wmax) * sizeof(unsigned), s));
+  void* fn = grow_fn(h.bits, g.k_alloc, g.wave);
   int occ = 0;
   HBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, g.nt, g.smem));
   require(occ >= 1, "tree grower kernel cannot be resident");
@@ -1759,6 +2612,7 @@ void launch_grow_persistent(const PersistentGrowArgs& h, int device, cudaStream_
     // of one CTA per SM; every CTA of it is resident while the SMs suffice
     HBG_CUDA(cudaLaunchKernel(fn, dim3(g.ctas), dim3(g.nt), args, g.smem, s));
   }
+  return g.wave ? static_cast<const void*>(a.ranges) : h.nodes;
 }
 
 }  // namespace hbg

@@ -187,7 +187,7 @@ struct PersistentGrowArgs {
   int32_t* rows[2];
   float* g[2];
   float* h[2];
-  double* slots;         // (2*num_leaves-1) node slots of 3*d*k doubles
+  double* slots;         // grow_max_nodes() node slots of 3*d*k doubles
   void* nodes;           // grow_nodes_bytes(num_leaves), nodes[0].best = root split
   hbg_split* split_log;  // device, num_leaves-1
   hbg_tree_node* tree;   // device, 2*num_leaves-1
@@ -208,11 +208,15 @@ struct PersistentGrowArgs {
   unsigned long long gen;
 };
 size_t grow_exchange_doubles(const PersistentGrowArgs& a, int device);
-size_t grow_nodes_bytes(int num_leaves);
+int grow_max_nodes(const PersistentGrowArgs& a, int device);  // node-table entries of the kernel used
+size_t grow_nodes_bytes(int max_nodes);
 size_t grow_root_split_offset();
 size_t grow_scratch_bytes(const PersistentGrowArgs& a, int device);
 void configure_grow_kernels();
-void launch_grow_persistent(const PersistentGrowArgs& a, int device, cudaStream_t s);
+// Returns what the score update reads: the node records by output id
+// (grow_kernel; launch_score_update_nodes) or, for the wave grower, counts[4]
+// LeafRange entries (launch_score_update).
+const void* launch_grow_persistent(const PersistentGrowArgs& a, int device, cudaStream_t s);
 // scores[row] += lr * value for the rows of every leaf node of a persistent-grown tree
 void launch_score_update_nodes(const void* nodes, const hbg_tree_node* tree, int num_nodes,
                                const int32_t* rows0, const int32_t* rows1, double lr, double* scores,
