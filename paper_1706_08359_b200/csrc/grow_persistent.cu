@@ -1619,6 +1619,10 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
 // from the replayed commit log.
 
 constexpr int kWN = 1280;  // node ids per tree (shared-memory state)
+static_assert(kWN <= 2048, "node ids are packed in 11 bits");
+
+// Speculation order: prio buckets of 1/4 octave (a positive float's bits >> 21).
+__device__ __forceinline__ int prio_bucket(float p) { return static_cast<int>(__float_as_uint(p) >> 21); }
 constexpr int kWL = 256;   // open leaves: num_leaves <= kWL
 constexpr int kWMax = 16;  // members per wave
 
@@ -1627,12 +1631,21 @@ struct WaveSmem {
   float prio[kWN];               // min gain along the path from the root
   short kid[kWN];                // left child once expanded, -1 before
   unsigned char large[kWN];      // 0: small; runs the large-parent paths: 1 (<= spec_rows rows), 2
-  short avail[kWN];              // expandable: discovered, gain > 0, not expanded
+  unsigned avail[kWN];           // expandable (discovered, gain > 0, not expanded): av_pack()
   unsigned long long fkey[kWL];  // the replay's open leaves with a split: gain key, node, output id
   short fnode[kWL], fout[kWL];
   short wave[kWMax];             // members: small ones first
-  int nav, nfr, committed, next, expanded, done, W, nsmall, nwc, wc, nwaves, hitems, ditems;
+  unsigned char later[kWL];      // commit i: bit c = child c was split later
+  int nav, nfr, committed, next, expanded, done, W, nsmall, nwc, wc, nwaves, hitems, ditems, err;
 };
+
+// An expandable-list entry: node id, size class (w.large), prio bucket.
+__device__ __forceinline__ unsigned av_pack(int node, int cls, int bucket) {
+  return static_cast<unsigned>(node) | (static_cast<unsigned>(cls) << 11) | (static_cast<unsigned>(bucket) << 13);
+}
+__device__ __forceinline__ int av_node(unsigned v) { return static_cast<int>(v & 0x7FFu); }
+__device__ __forceinline__ int av_class(unsigned v) { return static_cast<int>((v >> 11) & 3u); }
+__device__ __forceinline__ int av_bucket(unsigned v) { return static_cast<int>(v >> 13); }
 
 // Per-CTA state in global memory (written by the CTA's warp 0, read back by
 // the same CTA): the commit log [L][4] = node, left child node, output id,
@@ -1689,19 +1702,21 @@ __device__ void wave_integrate(const GrowArgs& a, WaveSmem& w) {
     const unsigned long long key = gain_key(g);
     w.gkey[id] = key;
     w.kid[id] = -1;
-    w.large[id] = runs_large(a, n, nl) ? (n <= a.spec_rows ? 1 : 2) : 0;
-    w.prio[id] = fminf(w.prio[x], static_cast<float>(g));
+    const int cls = runs_large(a, n, nl) ? (n <= a.spec_rows ? 1 : 2) : 0;
+    const float pr = fminf(w.prio[x], static_cast<float>(g));
+    w.large[id] = static_cast<unsigned char>(cls);
+    w.prio[id] = pr;
     add = key != 0ull;
+    id = static_cast<int>(av_pack(id, cls, prio_bucket(pr)));
   }
+  const int err = lane == 31 ? error_of(a) : 0;  // (one L2 round trip with the loads above)
   const unsigned bal = __ballot_sync(0xffffffffu, add);
-  if (add) w.avail[w.nav + __popc(bal & ((1u << lane) - 1u))] = static_cast<short>(id);
+  if (add) w.avail[w.nav + __popc(bal & ((1u << lane) - 1u))] = static_cast<unsigned>(id);
   __syncwarp();
   if (lane == 0) w.nav += __popc(bal);
+  if (lane == 31) w.err = err;
   __syncwarp();
 }
-
-// Speculation order: prio buckets of 1/4 octave (a positive float's bits >> 21).
-__device__ __forceinline__ int prio_bucket(float p) { return static_cast<int>(__float_as_uint(p) >> 21); }
 
 // Warp 0: bucket histogram (1024 counters in `hist`, shared memory) of the
 // expandable nodes with pred(node); returns the highest bucket B such that at
@@ -1712,9 +1727,15 @@ __device__ int bucket_select(const WaveSmem& w, unsigned* hist, int nav, int wan
 #pragma unroll
   for (int u = 0; u < 32; ++u) hist[u * 32 + lane] = 0u;
   __syncwarp();
-  for (int i = lane; i < nav; i += 32) {
-    const int n = w.avail[i];
-    if (pred(n)) atomicAdd(hist + prio_bucket(w.prio[n]), 1u);
+  for (int i0 = 0; i0 < nav; i0 += 32) {  // warp-aggregated: many nodes share their parent's prio
+    const int i = i0 + lane;
+    const unsigned v = i < nav ? w.avail[i] : 0u;
+    const bool el = i < nav && pred(v);
+    const unsigned act = __ballot_sync(0xffffffffu, el);
+    if (el) {
+      const unsigned peers = __match_any_sync(act, av_bucket(v));
+      if (lane == __ffs(peers) - 1) atomicAdd(hist + av_bucket(v), static_cast<unsigned>(__popc(peers)));
+    }
   }
   __syncwarp();
   // lane l owns buckets [32 l, 32 l + 32); counts from the top
@@ -1732,19 +1753,16 @@ __device__ int bucket_select(const WaveSmem& w, unsigned* hist, int nav, int wan
   const bool cross = above < static_cast<unsigned>(want) && suf >= static_cast<unsigned>(want);
   const unsigned bal = __ballot_sync(0xffffffffu, cross);
   if (bal == 0u) return 0;  // fewer than `want`: every bucket
-  const int l = 31 - __clz(bal);  // the only crossing lane
-  int B = 0;
-  if (lane == l) {
-    unsigned c = above;
-    for (int u = 31; u >= 0; --u) {
-      c += hist[lane * 32 + u];
-      if (c >= static_cast<unsigned>(want)) {
-        B = lane * 32 + u;
-        break;
-      }
-    }
+  const int l = 31 - __clz(bal);  // the only crossing lane; its 32 buckets one per lane
+  const unsigned base = __shfl_sync(0xffffffffu, above, l);
+  unsigned sb = hist[l * 32 + lane];
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned v = __shfl_down_sync(0xffffffffu, sb, off);
+    if (lane + off < 32) sb += v;
   }
-  return __shfl_sync(0xffffffffu, B, l);
+  const unsigned ok = __ballot_sync(0xffffffffu, base + sb >= static_cast<unsigned>(want));
+  return l * 32 + (31 - __clz(ok));
 }
 
 // Every CTA (warp 0, identical everywhere): replay the reference's picks over
@@ -1757,17 +1775,17 @@ __device__ void wave_select(const GrowArgs& a, WaveSmem& w, unsigned char* smem_
     const WaveLog lg = wave_log(a);
     int* clog = lg.clog;
     int nfr = w.nfr, committed = w.committed;
-    int err = lane == 0 ? error_of(a) : 0;
-    err = __shfl_sync(0xffffffffu, err, 0);
+    const int err = w.err;  // read with the integrate loads
     int best = -1;
     while (err == kErrNone && committed < L1) {
       unsigned long long hk = 0ull;
       unsigned lk = 0u;
       int idx = -1;
-#pragma unroll 8
-      for (int i = lane; i < nfr; i += 32) {
-        const unsigned long long h = w.fkey[i];
-        const unsigned l = 0xFFFFFFFFu - static_cast<unsigned>(w.fout[i]);
+#pragma unroll
+      for (int u = 0; u < kWL / 32; ++u) {
+        const int i = u * 32 + lane;
+        const unsigned long long h = i < nfr ? w.fkey[i] : 0ull;
+        const unsigned l = i < nfr ? 0xFFFFFFFFu - static_cast<unsigned>(w.fout[i]) : 0u;
         const bool take = h > hk || (h == hk && l > lk);
         hk = take ? h : hk;
         lk = take ? l : lk;
@@ -1791,8 +1809,8 @@ __device__ void wave_select(const GrowArgs& a, WaveSmem& w, unsigned char* smem_
         clog[4 * committed] = x;
         clog[4 * committed + 1] = kd;
         clog[4 * committed + 2] = o;
-        clog[4 * committed + 3] = 0;
-        if (o > 0) clog[4 * ((o - 1) >> 1) + 3] |= 1 << ((o - 1) & 1);
+        w.later[committed] = 0;
+        if (o > 0) w.later[(o - 1) >> 1] |= static_cast<unsigned char>(1 << ((o - 1) & 1));
         lg.splitf[x] = 1;
         lg.nout[kd] = static_cast<short>(2 * committed + 1);
         lg.nout[kd + 1] = static_cast<short>(2 * committed + 2);
@@ -1828,9 +1846,11 @@ __device__ void wave_select(const GrowArgs& a, WaveSmem& w, unsigned char* smem_
       unsigned* hist = reinterpret_cast<unsigned*>(smem_dyn);
       int br = 1 << 30;
       if (a.wlarge > 0 && L1 - committed - 1 > 0)
-        br = bucket_select(w, hist, nav, L1 - committed - 1, [&](int n) { return n != ps; });
-      const auto cand = [&](int n) {
-        return n != ps && (!w.large[n] || (w.large[n] == 1 && prio_bucket(w.prio[n]) >= br));
+        br = nav - 1 <= L1 - committed - 1
+                 ? 0  // all of them
+                 : bucket_select(w, hist, nav, L1 - committed - 1, [&](unsigned v) { return av_node(v) != ps; });
+      const auto cand = [&](unsigned v) {
+        return av_node(v) != ps && (av_class(v) == 0 || (av_class(v) == 1 && av_bucket(v) >= br));
       };
       const int want = m - 1;
       const int B = want > 0 ? bucket_select(w, hist, nav, want, cand) : 1 << 30;
@@ -1841,31 +1861,28 @@ __device__ void wave_select(const GrowArgs& a, WaveSmem& w, unsigned char* smem_
         // every candidate in the buckets above B (fewer than want) ...
         for (int i0 = 0; i0 < nav; i0 += 32) {
           const int i = i0 + lane;
-          const int n = i < nav ? w.avail[i] : -1;
-          const bool el = n >= 0 && cand(n) && prio_bucket(w.prio[n]) > B;
+          const unsigned v = i < nav ? w.avail[i] : 0u;
+          const bool el = i < nav && cand(v) && av_bucket(v) > B;
           const unsigned bal = __ballot_sync(0xffffffffu, el);
-          if (el) w.wave[W + __popc(bal & ((1u << lane) - 1u))] = static_cast<short>(n);
+          if (el) w.wave[W + __popc(bal & ((1u << lane) - 1u))] = static_cast<short>(av_node(v));
           W += __popc(bal);
         }
         __syncwarp();
         // ... then the best of bucket B by exact prio (ties: lowest node id),
-        // from its first 32 candidates, one per lane
-        int mine = -1, got = 0;
+        // from its first 32 candidates (collected in shared memory), one per lane
+        unsigned* lst = hist + 1024;
+        int got = 0;
         for (int i0 = 0; i0 < nav && got < 32; i0 += 32) {
           const int i = i0 + lane;
-          const int n = i < nav ? w.avail[i] : -1;
-          const bool el = n >= 0 && cand(n) && prio_bucket(w.prio[n]) == B;
+          const unsigned v = i < nav ? w.avail[i] : 0u;
+          const bool el = i < nav && cand(v) && av_bucket(v) == B;
           const unsigned bal = __ballot_sync(0xffffffffu, el);
-          // lane r of the collected list receives the r-th hit
-          const int src = got;
-          for (unsigned bb = bal; bb != 0u && got < 32; bb &= bb - 1u) {
-            const int from = __ffs(bb) - 1;
-            const int v = __shfl_sync(0xffffffffu, n, from);
-            if (lane == got) mine = v;
-            ++got;
-          }
-          (void)src;
+          const int r = got + __popc(bal & ((1u << lane) - 1u));
+          if (el && r < 32) lst[r] = static_cast<unsigned>(av_node(v));
+          got += __popc(bal);
         }
+        __syncwarp();
+        const int mine = lane < min(got, 32) ? static_cast<int>(lst[lane]) : -1;
         unsigned long long key = mine >= 0 ? ((static_cast<unsigned long long>(__float_as_uint(w.prio[mine])) << 32) |
                                               (0xFFFFFFFFu - static_cast<unsigned>(mine)))
                                            : 0ull;
@@ -1891,8 +1908,8 @@ __device__ void wave_select(const GrowArgs& a, WaveSmem& w, unsigned char* smem_
       int nav2 = 0;  // compaction in place: a round's reads precede its writes, which land below them
       for (int i0 = 0; i0 < nav; i0 += 32) {
         const int i = i0 + lane;
-        const short n = i < nav ? w.avail[i] : static_cast<short>(0);
-        const bool keep = i < nav && w.kid[n] != -2;
+        const unsigned n = i < nav ? w.avail[i] : 0u;
+        const bool keep = i < nav && w.kid[av_node(n)] != -2;
         const unsigned bal = __ballot_sync(0xffffffffu, keep);
         __syncwarp();
         if (keep) w.avail[nav2 + __popc(bal & ((1u << lane) - 1u))] = n;
@@ -2213,7 +2230,7 @@ __device__ void wave_emit(const GrowArgs& a, const WaveSmem& w) {
   const int committed = w.committed;
   const int stride = gridDim.x * blockDim.x;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < committed; i += stride) {
-    const int x = lg.clog[4 * i], kd = lg.clog[4 * i + 1], o = lg.clog[4 * i + 2], later = lg.clog[4 * i + 3];
+    const int x = lg.clog[4 * i], kd = lg.clog[4 * i + 1], o = lg.clog[4 * i + 2], later = w.later[i];
     const hbg_split bs = load_split(&a.nodes[x].best);
     a.split_log[i] = bs;
     a.tree[o] = hbg_tree_node{bs.feature, bs.threshold_bin, 2 * i + 1, 2 * i + 2, 0.0};
@@ -2269,13 +2286,13 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_wave_kernel(GrowArg
     w.kid[0] = -1;
     w.large[0] = runs_large(a, a.root_count, hb ? bs.left_count : 0) ? (a.root_count <= a.spec_rows ? 1 : 2) : 0;
     w.nav = w.nfr = 0;
-    w.committed = w.expanded = w.done = w.W = w.nsmall = w.nwaves = 0;
+    w.committed = w.expanded = w.done = w.W = w.nsmall = w.nwaves = w.err = 0;
     w.next = 1;
     if (k0 != 0ull && a.num_leaves >= 2) {
       w.fkey[0] = k0;
       w.fnode[0] = 0;
       w.fout[0] = 0;
-      w.avail[0] = 0;
+      w.avail[0] = av_pack(0, w.large[0], prio_bucket(w.prio[0]));
       w.nfr = w.nav = 1;
     }
   }
