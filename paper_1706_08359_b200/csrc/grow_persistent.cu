@@ -152,12 +152,6 @@ struct GrowArgs {
   int wmax;               // members per wave
   int wlarge;             // speculative large members allowed (HBG_WAVE_LARGE)
   int64_t spec_rows;      // ... up to this many rows (HBG_WAVE_SPEC_ROWS)
-  // single-pass partition (one rank): per (member slot, tile) look-back
-  // descriptors and fp64 side sums; per-slot tile claim counters
-  unsigned long long* tile_desc;
-  double* tile_sums;
-  unsigned* tile_ctr;
-  int max_tiles;
   int wcap;               // features per wave chunk the shared-memory layout holds
   int ecap;               // speculative expansions allowed up to this total
   int64_t small_max;      // parents up to this many rows join waves (kItems * NT)
@@ -933,198 +927,6 @@ __device__ void partition_scatter(const GrowArgs& a, Desc& D, PartShared<NT>& ps
   }
 }
 
-// Single-pass stable partition of a large parent (one rank): tiles of
-// kPartTile positions claimed in order through an atomic counter; each tile
-// publishes its left count and learns the left rows of all earlier tiles by
-// decoupled look-back over per-tile descriptors, so it scatters at once (the
-// split's left_count gives the right rows' base). Versus partition_count +
-// barrier + partition_scatter this reads the parent's (row, g, h) once and
-// drops the flags round trip. Per-tile fp64 side sums are reduced in tile order
-// after the next barrier (partition_totals): deterministic.
-// Descriptor: [epoch:30][flag:2][left count:32]; flag 1 = the tile's own count,
-// 2 = inclusive prefix. Stale descriptors (other epochs) read as not ready.
-constexpr unsigned long long kDescAgg = 1ull << 32, kDescPrefix = 2ull << 32;
-
-__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-template <int NT>
-__device__ void partition_single(const GrowArgs& a, Desc& D, PartShared<NT>& ps, unsigned char* smem,
-                                 unsigned epoch, unsigned& ctr_base) {
-  constexpr int kTile = NT * kPartItems;
-  const int64_t n = D.count;
-  const int ntiles = static_cast<int>((n + kTile - 1) / kTile);
-  unsigned long long* desc = a.tile_desc + static_cast<size_t>(D.mslot) * a.max_tiles;
-  double* tsum = a.tile_sums + static_cast<size_t>(D.mslot) * a.max_tiles * 4;
-  const unsigned long long ep = static_cast<unsigned long long>(epoch & 0x3FFFFFFFu) << 34;
-  const int32_t* rin = a.rows[D.buf_in] + D.begin;
-  const float* gin = a.g[D.buf_in] + D.begin;
-  const float* hin = a.h[D.buf_in] + D.begin;
-  int32_t* rout = a.rows[D.buf_out] + D.begin;
-  float* gout = a.g[D.buf_out] + D.begin;
-  float* hout = a.h[D.buf_out] + D.begin;
-  int32_t* srow = reinterpret_cast<int32_t*>(smem);
-  float* sg = reinterpret_cast<float*>(srow + kTile);
-  float* sh = sg + kTile;
-  uint8_t* sflag = reinterpret_cast<uint8_t*>(sh + kTile);
-  uint16_t* slot = reinterpret_cast<uint16_t*>(smem + static_cast<size_t>(2) * kTile * 13);
-  __shared__ int s_tile[2];
-  __shared__ long long s_excl;
-  const int64_t L = D.nl;  // one rank: the split's left count is this rank's
-  // software pipeline: the next claimed tile's (row, g, h) loads are in
-  // flight while this tile is ranked, looked back and scattered
-  auto claim = [&](int k) {
-    if (threadIdx.x == 0) s_tile[k] = static_cast<int>(atomicAdd(a.tile_ctr + D.mslot, 1u) - ctr_base);
-  };
-  int32_t r[kPartItems];
-  float gv[kPartItems], hv[kPartItems];
-  auto load = [&](int t) {
-    const int64_t t0 = static_cast<int64_t>(t) * kTile;
-#pragma unroll
-    for (int j = 0; j < kPartItems; ++j) {  // coalesced: tile position j*NT + t
-      const int64_t q = t0 + j * NT + threadIdx.x;
-      const bool ok = t < ntiles && q < n;
-      r[j] = ok ? __ldcg(rin + q) : 0;
-      gv[j] = ok ? __ldcg(gin + q) : 0.f;
-      hv[j] = ok ? __ldcg(hin + q) : 0.f;
-    }
-  };
-  uint32_t bin[kPartItems];
-  auto bins = [&](int t) {  // the split feature's bins of a loaded tile
-    const int64_t t0 = static_cast<int64_t>(t) * kTile;
-#pragma unroll
-    for (int j = 0; j < kPartItems; ++j)
-      bin[j] = t < ntiles && t0 + j * NT + static_cast<int>(threadIdx.x) < n ? col_bin(a, r[j], D.feature) : 0u;
-  };
-  claim(0);
-  __syncthreads();
-  int t = s_tile[0], cur = 0;
-  load(t);
-  while (t < ntiles) {
-    claim(cur ^ 1);  // (read after the block_sum's barriers below)
-    const int64_t t0 = static_cast<int64_t>(t) * kTile;
-    const int m = static_cast<int>(n - t0 < kTile ? n - t0 : kTile);
-    bins(t);
-    double v[4] = {0.0, 0.0, 0.0, 0.0};
-    long long c = 0;
-#pragma unroll
-    for (int j = 0; j < kPartItems; ++j) {
-      const int q = j * NT + threadIdx.x;
-      if (q >= m) continue;
-      const bool left = bin[j] <= static_cast<uint32_t>(D.thr);  // tree.cpp:117-123
-      srow[q] = r[j];
-      sg[q] = gv[j];
-      sh[q] = hv[j];
-      sflag[q] = left ? 1 : 0;
-      if (left) {
-        ++c;
-        v[0] += gv[j];
-        v[1] += hv[j];
-      } else {
-        v[2] += gv[j];
-        v[3] += hv[j];
-      }
-    }
-    block_sum_4d1<NT>(v, c, ps);  // (its barriers complete the stage and the claim)
-    const int tn = s_tile[cur ^ 1];
-    load(tn);  // next tile in flight
-    const long long cl = ps.cnt;
-    if (threadIdx.x < 32) {
-      const int lane = threadIdx.x;
-      if (lane == 0) {  // (the sums are read after the next grid barrier)
-        for (int j = 0; j < 4; ++j) tsum[4 * static_cast<size_t>(t) + j] = ps.tot[j];
-        atomicExch(desc + t, ep | (t == 0 ? kDescPrefix : kDescAgg) | static_cast<unsigned long long>(cl));
-      }
-      long long excl = 0;
-      int k = t - 1;
-      while (k >= 0) {  // decoupled look-back, 32 predecessors at a time
-        const int kk = k - lane;
-        unsigned long long dv = 0;
-        bool ready = true;
-        if (kk >= 0) {
-          const long long t1 = clock64();
-          do {
-            dv = ld_volatile_u64(desc + kk);
-            ready = (dv & ~((1ull << 34) - 1)) == ep && (dv & (3ull << 32)) != 0;
-          } while (!ready && clock64() - t1 < a.timeout_cycles);
-          if (!ready) set_error(a, kErrBarrierTimeout);
-        }
-        const bool pre = kk >= 0 && (dv & (3ull << 32)) == kDescPrefix;
-        const unsigned pb = __ballot_sync(0xffffffffu, pre);
-        const int stop = pb ? __ffs(pb) - 1 : 31;  // lanes [0, stop] contribute
-        long long cnt = kk >= 0 && lane <= stop ? static_cast<long long>(dv & 0xFFFFFFFFull) : 0;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
-        excl += cnt;
-        if (pb || __any_sync(0xffffffffu, !ready)) break;
-        k -= 32;
-      }
-      if (lane == 0) {
-        if (t > 0) atomicExch(desc + t, ep | kDescPrefix | static_cast<unsigned long long>(excl + cl));
-        if (t == ntiles - 1 && excl + cl != L) set_error(a, kErrPartition);
-        s_excl = excl;
-      }
-    }
-    // stable ranks inside the tile (thread t: positions [t*ipt, t*ipt+ipt)),
-    // then the left run and the right run written coalesced
-    uint32_t lf = 0;
-    int cb = 0;
-    const int q0 = threadIdx.x * kPartItems;
-#pragma unroll
-    for (int j = 0; j < kPartItems; ++j) {
-      const bool left = q0 + j < m && sflag[q0 + j];
-      lf |= left ? 1u << j : 0u;
-      cb += left ? 1 : 0;
-    }
-    const long long lb = block_excl_scan<NT>(cb, ps);
-    int lr = static_cast<int>(lb);
-    const int tl = static_cast<int>(cl);
-#pragma unroll
-    for (int j = 0; j < kPartItems; ++j) {
-      const int q = q0 + j;
-      if (q >= m) continue;
-      const bool left = (lf >> j) & 1u;
-      slot[left ? lr : tl + (q - lr)] = static_cast<uint16_t>(q);
-      lr += left ? 1 : 0;
-    }
-    __syncthreads();
-    const int64_t lbase = s_excl, rbase = L + (t0 - s_excl);
-    for (int i = threadIdx.x; i < m; i += NT) {
-      const int q = slot[i];
-      const int64_t dst = i < tl ? lbase + i : rbase + (i - tl);
-      rout[dst] = srow[q];
-      gout[dst] = sg[q];
-      hout[dst] = sh[q];
-    }
-    __syncthreads();  // stage reuse
-    t = tn;
-    cur ^= 1;
-  }
-  if (threadIdx.x == 0) ctr_base += static_cast<unsigned>(ntiles) + gridDim.x;  // one failing claim per CTA
-}
-
-// After the barrier that follows partition_single (every CTA): the children's
-// totals as the tile-order sum of the per-tile sums.
-template <int NT>
-__device__ void partition_totals(const GrowArgs& a, Desc& D, PartShared<NT>& ps) {
-  constexpr int kTile = NT * kPartItems;
-  const int ntiles = static_cast<int>((D.count + kTile - 1) / kTile);
-  const double* tsum = a.tile_sums + static_cast<size_t>(D.mslot) * a.max_tiles * 4;
-  double v[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int t = threadIdx.x; t < ntiles; t += NT)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) v[j] += __ldcg(tsum + 4 * static_cast<size_t>(t) + j);
-  block_sum_4d1<NT>(v, 0, ps);
-  if (threadIdx.x == 0) {
-    for (int j = 0; j < 4; ++j) D.tot_loc[j] = D.tot[j] = ps.tot[j];
-    D.nl_loc = D.nl;
-  }
-  __syncthreads();
-}
-
 // ------------------------------------------------------------------ histogram
 
 __device__ __forceinline__ void small_child(const GrowArgs& a, const Desc& D, const int32_t*& rows,
@@ -1660,7 +1462,6 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
   }
   __syncthreads();
   pick<NT>(a, 0, 0, kid, D);  // node 0 is "kid_l" (kid[1] is never consulted: nnodes = 1)
-  unsigned ctr_base = 0;  // partition_single's tile counter (slot 0)
   const double eg = ldexp(1.0, a.exps[0]), eh = ldexp(1.0, a.exps[1]);  // fixed-point scales
   while (!D.done) {
     const int it = D.iter;
@@ -1715,16 +1516,10 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
       stamp(a, it, 3);
       grid_sync(a);
     } else {
-      if (a.nranks == 1) {  // single pass (look-back), one barrier
-        partition_single<NT>(a, D, ps, smem, static_cast<unsigned>(it) + 1u, ctr_base);
-        grid_sync(a);
-        partition_totals<NT>(a, D, ps);
-      } else {  // this rank's left count is not known up front: count pass first
-        partition_count<NT>(a, D, ps);
-        grid_sync(a);
-        partition_scatter<NT>(a, D, ps, smem);
-        grid_sync(a);
-      }
+      partition_count<NT>(a, D, ps);
+      grid_sync(a);
+      partition_scatter<NT>(a, D, ps, smem);
+      grid_sync(a);
       set_children(a, D, kid);
       stamp(a, it, 1);
       if (D.path == kDirect) {
@@ -2471,8 +2266,6 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_wave_kernel(GrowArg
   __shared__ PartShared<NT> ps;
   __shared__ Desc Dm[kWMax];
   __shared__ WaveSmem w;
-  __shared__ unsigned ctr_base[kWMax];  // partition_single's tile counters, per member slot
-  if (threadIdx.x < kWMax) ctr_base[threadIdx.x] = 0u;
   // the root (histogram, totals, best split computed by host-launched kernels)
   if (threadIdx.x == 0) {
     const double G = __ldcg(a.root_tot), H = __ldcg(a.root_tot + 1);
@@ -2515,13 +2308,13 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_wave_kernel(GrowArg
     }
     stamp(a, w.nwaves, 0);
     load_members(a, w, Dm);
-    for (int j = w.nsmall; j < w.W; ++j)
-      partition_single<NT>(a, Dm[j], ps, smem, static_cast<unsigned>(w.nwaves) + 1u, ctr_base[j]);
+    for (int j = w.nsmall; j < w.W; ++j) partition_count<NT>(a, Dm[j], ps);
     if (w.nsmall > 0) wave_small<K, NT>(a, w, Dm, ps, smem, eg, eh);
     stamp(a, w.nwaves, 1);
     if (w.W > w.nsmall) {
       grid_sync(a);
-      for (int j = w.nsmall; j < w.W; ++j) partition_totals<NT>(a, Dm[j], ps);
+      for (int j = w.nsmall; j < w.W; ++j) partition_scatter<NT>(a, Dm[j], ps, smem);
+      grid_sync(a);
       stamp(a, w.nwaves, 2);
       for (int j = w.nsmall; j < w.W; ++j)
         if (Dm[j].path == kNoHist && blockIdx.x == 0) publish_member<NT>(a, Dm[j], 0);
@@ -2570,8 +2363,9 @@ void* grow_fn(int bits, int k_alloc, bool wave) {
   return GrowKernel<8, 256>::fn(wave);
 }
 
-// The wave grower runs single-rank trees unless HBG_GROW=legacy, and only
-// while its node slots (speculative expansions included) fit kWaveSlotBudget.
+// The wave grower runs single-rank trees of the shapes where it pays (below;
+// HBG_GROW=wave forces it, HBG_GROW=legacy disables it), and only while its
+// node slots (speculative expansions included) fit kWaveSlotBudget.
 constexpr size_t kWaveSlotBudget = size_t(4) << 30;
 
 // Speculative expansions allowed beyond the num_leaves-1 the tree commits;
@@ -2582,6 +2376,13 @@ int wave_extra(const PersistentGrowArgs& h) {
   const char* e = std::getenv("HBG_GROW");
   if (h.nranks > 1 || (e != nullptr && std::strcmp(e, "legacy") == 0)) return -1;
   if (h.num_leaves > kWL || (h.bits != 4 && h.k > 128)) return -1;
+  // waves pay where per-split latency dominates: many small leaves (rows per
+  // leaf <= 16K) and cheap finishes (features x bins <= 16K). Measured: Higgs
+  // 1M x 28 k64 2.4 ms vs 4.7 with one split per barrier; 10.5M rows, or
+  // 2000 features (epsilon), are faster one split at a time.
+  const bool forced = e != nullptr && std::strcmp(e, "wave") == 0;  // HBG_GROW=wave: whenever it fits
+  if (!forced && (h.num_rows > 16384LL * std::max(1, h.num_leaves) || static_cast<long long>(h.d) * h.k > 16384))
+    return -1;
   const int L1 = std::max(0, h.num_leaves - 1);
   const size_t slot = static_cast<size_t>(3) * h.d * h.k * sizeof(double);
   const long long fit = std::min<long long>(kWN, static_cast<long long>(kWaveSlotBudget / std::max<size_t>(slot, 1)));
@@ -2712,11 +2513,6 @@ size_t grow_scratch_bytes(const PersistentGrowArgs& h, int device) {
     add(static_cast<size_t>(g.ctas) * wave_state_bytes(h.num_leaves, g.max_nodes));  // wstate
     add(static_cast<size_t>(g.max_nodes) * sizeof(LeafRange));                       // ranges
   }
-  const size_t slots = g.wave ? g.wmax : 1;
-  const size_t tiles = static_cast<size_t>((h.num_rows + g.nt * kPartItems - 1) / (g.nt * kPartItems)) + 1;
-  add(slots * tiles * 8);   // tile_desc
-  add(slots * tiles * 32);  // tile_sums
-  add(slots * 4);           // tile_ctr
   return b;
 }
 
@@ -2823,19 +2619,13 @@ const void* launch_grow_persistent(const PersistentGrowArgs& h, int device, cuda
     a.wstate = take(static_cast<size_t>(g.ctas) * a.wstate_stride);
     a.ranges = reinterpret_cast<LeafRange*>(take(static_cast<size_t>(g.max_nodes) * sizeof(LeafRange)));
   }
-  const int slots = g.wave ? g.wmax : 1;
-  a.max_tiles = static_cast<int>((h.num_rows + g.nt * kPartItems - 1) / (g.nt * kPartItems)) + 1;
-  a.tile_desc = reinterpret_cast<unsigned long long*>(take(static_cast<size_t>(slots) * a.max_tiles * 8));
-  a.tile_sums = reinterpret_cast<double*>(take(static_cast<size_t>(slots) * a.max_tiles * 32));
-  a.tile_ctr = reinterpret_cast<unsigned*>(take(static_cast<size_t>(slots) * 4));
+
   require(static_cast<size_t>(p - static_cast<unsigned char*>(h.scratch)) <= h.scratch_bytes,
           "grow scratch smaller than its layout");
   HBG_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned), s));
   HBG_CUDA(cudaMemsetAsync(a.picked, 0, kRep * max_nodes * sizeof(int), s));
   HBG_CUDA(cudaMemsetAsync(a.counts, 0, 8 * sizeof(int), s));
   if (g.wave) HBG_CUDA(cudaMemsetAsync(a.wcnt, 0, static_cast<size_t>(g.wmax) * sizeof(unsigned), s));
-  HBG_CUDA(cudaMemsetAsync(a.tile_ctr, 0, static_cast<size_t>(slots) * 4, s));
-  HBG_CUDA(cudaMemsetAsync(a.tile_desc, 0, static_cast<size_t>(slots) * a.max_tiles * 8, s));
   void* fn = grow_fn(h.bits, g.k_alloc, g.wave);
   int occ = 0;
   HBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, g.nt, g.smem));

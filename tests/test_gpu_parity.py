@@ -441,7 +441,7 @@ def _assert_same_tree(log, nodes, want_log, want_nodes, cols=None, g=None, h=Non
     return i
 
 
-@pytest.mark.parametrize("grower", ["persistent", "legacy", "host"])
+@pytest.mark.parametrize("grower", ["persistent", "wave", "legacy", "host"])
 def test_grow_tree_matches_reference_golden_split_log(hbg, oracle, grower, monkeypatch):
     """grow_tree split_log of the unmodified reference (bits64), committed golden."""
     import os
@@ -470,7 +470,7 @@ def test_grow_tree_matches_reference_golden_split_log(hbg, oracle, grower, monke
     (3000, 1300, 256, 15, 100, 0.0, True),  # > 8 features x 256 bins per scan chunk
     (40000, 20, 100, 31, 100, 0.5, True), (40000, 33, 10, 31, 100, 0.0, True),  # 128-bin slots; 4-bit, 10 bins
     (25000, 5, 200, 63, 50, 0.0, True)])
-@pytest.mark.parametrize("grower", ["persistent", "legacy", "host"])
+@pytest.mark.parametrize("grower", ["persistent", "wave", "legacy", "host"])
 def test_grow_tree_matches_oracle(hbg, oracle, rows, d, k, leaves, min_data, lam, exact, grower, monkeypatch):
     """Both growers (the persistent one-kernel tree and the host loop,
     HBG_GROW=host). Non-tied inputs (min_data large enough that no near-ties arise): the
@@ -493,7 +493,7 @@ def test_grow_tree_matches_oracle(hbg, oracle, rows, d, k, leaves, min_data, lam
     (3000, 3, 64, 255, 1, 0.0), (20000, 1300, 256, 31, 100, 0.0), (60000, 10, 64, 511, 1, 0.0),
     (1000000, 28, 64, 255, 100, 0.0)])
 def test_wave_grower_bitwise_equals_one_split_grower(hbg, oracle, rows, d, k, leaves, min_data, lam, monkeypatch):
-    """The wave grower (default) expands several leaves per grid barrier and
+    """The wave grower (HBG_GROW=wave) expands several leaves per grid barrier and
     replays the reference's pick order; the one-split-at-a-time kernel
     (HBG_GROW=legacy) follows the reference loop literally. Same data, same
     arithmetic per leaf: the split logs and trees must be bit-identical, ties
@@ -503,13 +503,13 @@ def test_wave_grower_bitwise_equals_one_split_grower(hbg, oracle, rows, d, k, le
     g = g + 0.3 * (cols[d // 2].astype(np.float64) > k // 2)
     out = {}
     with hbg.Dataset(cols, k) as ds:
-        for grower in ("legacy", "persistent", "legacy"):
+        for grower in ("legacy", "wave", "legacy"):
             monkeypatch.setenv("HBG_GROW", grower)
             log, nodes = _grow(hbg, ds, g, h, leaves, min_data, lam)
             if grower in out:  # the one-split grower is itself repeatable
                 assert out[grower][0].tobytes() == log.tobytes()
             out[grower] = (log, nodes)
-    (la, na), (lb, nb) = out["legacy"], out["persistent"]
+    (la, na), (lb, nb) = out["legacy"], out["wave"]
     assert len(la) == len(lb) and la.tobytes() == lb.tobytes()
     assert len(na) == len(nb) and na.tobytes() == nb.tobytes()
 
@@ -526,7 +526,7 @@ def test_grow_tree_host_pointer_dropin(hbg, oracle):
     assert _assert_same_tree(log, nodes, want_log, want_nodes) == len(want_log)
 
 
-@pytest.mark.parametrize("grower", ["persistent", "legacy", "host"])
+@pytest.mark.parametrize("grower", ["persistent", "wave", "legacy", "host"])
 def test_grow_tree_edge_cases(hbg, oracle, grower, monkeypatch):
     monkeypatch.setenv("HBG_GROW", grower)
     cols = oracle.gen_synthetic_bins(500, 4, 64, 1)
@@ -546,7 +546,7 @@ def test_grow_tree_edge_cases(hbg, oracle, grower, monkeypatch):
 # ------------------------------------------------ boosting iteration (§8f rank 3)
 @pytest.mark.parametrize("loss,rows,d,k,leaves,min_data,lam", [(0, 50000, 28, 64, 31, 100, 0.0),
                                                               (1, 40000, 20, 16, 63, 100, 1.0)])
-@pytest.mark.parametrize("grower", ["persistent", "legacy", "host"])
+@pytest.mark.parametrize("grower", ["persistent", "wave", "legacy", "host"])
 def test_boosting_iterations_match_reference(hbg, oracle, loss, rows, d, k, leaves, min_data, lam, grower,
                                              monkeypatch):
     """Three boost_one_iteration (boosting.cpp:26-51) steps on the device vs the
