@@ -157,7 +157,7 @@ struct GrowArgs {
   int64_t small_max;      // parents up to this many rows join waves (kItems * NT)
 };
 
-constexpr int kProfSlots = 12;
+constexpr int kProfSlots = 16;
 
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
@@ -1636,7 +1636,8 @@ struct WaveSmem {
   short fnode[kWL], fout[kWL];
   short wave[kWMax];             // members: small ones first
   unsigned char later[kWL];      // commit i: bit c = child c was split later
-  int nav, nfr, committed, next, expanded, done, W, nsmall, nwc, wc, nwaves, hitems, ditems, err;
+  short clist[32];               // speculation candidates by prio (wave_candidates)
+  int nav, nfr, committed, next, expanded, done, W, nsmall, nwc, wc, nwaves, hitems, ditems, err, ncl;
 };
 
 // An expandable-list entry: node id, size class (w.large), prio bucket.
@@ -1765,18 +1766,97 @@ __device__ int bucket_select(const WaveSmem& w, unsigned* hist, int nav, int wan
   return l * 32 + (31 - __clz(ok));
 }
 
-// Every CTA (warp 0, identical everywhere): replay the reference's picks over
-// the expanded leaves (commit), then choose the next wave. Whole CTA.
+// Warp 1, while warp 0 replays: the speculation candidates — ~the wmax
+// expandable nodes with the largest prio (1/4-octave buckets, then exact prio
+// and node id inside the threshold bucket), small ones, plus large ones of
+// <= spec_rows rows among the R best (R = the commits still to come before this
+// replay, an upper bound) when HBG_WAVE_LARGE allows: a speculative large
+// expansion costs a partition and histogram pass over its rows. Sorted by
+// prio into w.clist (w.ncl entries). The certain pick may be among them.
+__device__ void wave_candidates(const GrowArgs& a, WaveSmem& w, unsigned char* smem_dyn) {
+  const int lane = threadIdx.x & 31;
+  const int nav = w.nav;
+  const int r0 = a.num_leaves - 1 - w.committed;
+  unsigned* hist = reinterpret_cast<unsigned*>(smem_dyn);
+  int br = 1 << 30;
+  if (a.wlarge > 0 && r0 > 0)
+    br = nav <= r0 ? 0 : bucket_select(w, hist, nav, r0, [&](unsigned) { return true; });
+  const auto cand = [&](unsigned v) { return av_class(v) == 0 || (av_class(v) == 1 && av_bucket(v) >= br); };
+  const int want = a.wmax;
+  const int B = bucket_select(w, hist, nav, want, cand);
+  // every candidate above bucket B (fewer than want), then bucket B's best by
+  // exact prio from its first 32 (one per lane)
+  unsigned long long key = 0ull;  // this lane's list entry: prio bits << 32 | ~node
+  int W = 0;
+  for (int i0 = 0; i0 < nav; i0 += 32) {
+    const int i = i0 + lane;
+    const unsigned v = i < nav ? w.avail[i] : 0u;
+    const bool el = i < nav && cand(v) && av_bucket(v) > B;
+    const unsigned bal = __ballot_sync(0xffffffffu, el);
+    const int n = av_node(v);
+    const unsigned long long k = (static_cast<unsigned long long>(__float_as_uint(w.prio[n])) << 32) |
+                                 (0xFFFFFFFFu - static_cast<unsigned>(n));
+    // entry W + rank goes to lane W + rank
+    for (unsigned bb = bal; bb != 0u; bb &= bb - 1u) {
+      const int from = __ffs(bb) - 1;
+      const unsigned long long kv = __shfl_sync(0xffffffffu, k, from);
+      if (lane == W) key = kv;
+      ++W;
+    }
+  }
+  unsigned* lst = hist + 1024;
+  int got = 0;
+  for (int i0 = 0; i0 < nav && got < 32; i0 += 32) {
+    const int i = i0 + lane;
+    const unsigned v = i < nav ? w.avail[i] : 0u;
+    const bool el = i < nav && cand(v) && av_bucket(v) == B;
+    const unsigned bal = __ballot_sync(0xffffffffu, el);
+    const int r = got + __popc(bal & ((1u << lane) - 1u));
+    if (el && r < 32) lst[r] = static_cast<unsigned>(av_node(v));
+    got += __popc(bal);
+  }
+  __syncwarp();
+  const int mine = lane < min(got, 32) ? static_cast<int>(lst[lane]) : -1;
+  unsigned long long bk = mine >= 0 ? ((static_cast<unsigned long long>(__float_as_uint(w.prio[mine])) << 32) |
+                                       (0xFFFFFFFFu - static_cast<unsigned>(mine)))
+                                    : 0ull;
+  // bitonic sort of bucket B's keys, descending; its best fill the list after
+  // the entries above B (which all rank higher)
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const unsigned long long o = __shfl_xor_sync(0xffffffffu, bk, j);
+      const bool up = (lane & k) == 0;
+      const bool lower = (lane & j) == 0;
+      bk = (lower == up ? o > bk : o < bk) ? o : bk;
+    }
+  }
+  const int take = min(want - W, min(got, 32));
+  const unsigned long long moved = __shfl_sync(0xffffffffu, bk, (lane - W) & 31);
+  if (lane >= W && lane < W + take) key = moved;
+  W += take;
+  if (lane < W) w.clist[lane] = static_cast<short>(0xFFFFFFFFu - static_cast<unsigned>(key));
+  if (lane == 0) w.ncl = W;
+  __syncwarp();
+}
+
+// Every CTA (identical everywhere): warp 0 replays the reference's picks over
+// the expanded leaves (commit) while warp 1 ranks the speculation
+// candidates; then warp 0 forms the next wave. Whole CTA.
 template <int NT>
 __device__ void wave_select(const GrowArgs& a, WaveSmem& w, unsigned char* smem_dyn) {
+  __shared__ int s_best, s_committed, s_nfr, s_w;
+  const int L1 = a.num_leaves - 1;
+  __syncthreads();  // warp 0's integrate is complete for warp 1
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
-    const int L1 = a.num_leaves - 1;
     const WaveLog lg = wave_log(a);
     int* clog = lg.clog;
     int nfr = w.nfr, committed = w.committed;
     const int err = w.err;  // read with the integrate loads
     int best = -1;
+    const long long rc0 = clock64();
     while (err == kErrNone && committed < L1) {
       unsigned long long hk = 0ull;
       unsigned lk = 0u;
@@ -1831,80 +1911,52 @@ __device__ void wave_select(const GrowArgs& a, WaveSmem& w, unsigned char* smem_
       nfr += (w.gkey[kd] != 0ull ? 1 : 0) + (w.gkey[kd + 1] != 0ull ? 1 : 0) - 1;
       ++committed;
     }
-    if (lane == 0 && w.nwaves > 0) stamp(a, w.nwaves - 1, 8);
+    if (lane == 0) {
+      s_best = best >= 0 && committed < L1 && err == kErrNone ? best : -1;
+      s_committed = committed;
+      s_nfr = nfr;
+      if (w.nwaves > 0) {
+        stamp(a, w.nwaves - 1, 8);
+        if (a.prof != nullptr && blockIdx.x == 0) {
+          unsigned long long* t = a.prof + static_cast<size_t>(w.nwaves - 1) * kProfSlots;
+          t[12] = static_cast<unsigned long long>(committed - w.committed);
+          t[11] = static_cast<unsigned long long>(clock64() - rc0);  // replay cycles (overrides slot 11)
+          t[14] = static_cast<unsigned long long>(w.nav);
+          t[15] = static_cast<unsigned long long>(nfr);
+        }
+      }
+    }
+  } else if (threadIdx.x < 64) {
+    const long long c0 = clock64();
+    if (a.wmax > 1 && w.err == kErrNone) wave_candidates(a, w, smem_dyn);
+    else if (threadIdx.x == 32) w.ncl = 0;
+    if (threadIdx.x == 32 && a.prof != nullptr && blockIdx.x == 0 && w.nwaves > 0)
+      a.prof[static_cast<size_t>(w.nwaves - 1) * kProfSlots + 13] = static_cast<unsigned long long>(clock64() - c0);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const WaveLog lg = wave_log(a);
+    const int best = s_best, committed = s_committed;
     int W = 0, nsmall = 0;
-    if (best >= 0 && committed < L1 && err == kErrNone) {
+    if (best >= 0) {
       const int ps = w.fnode[best];
       int m = min(L1 - committed, a.wmax);
       m = max(1, min(m, a.ecap - w.expanded));
-      const int nav = w.nav;
-      // speculation: ~the m-1 best other expandable nodes by prio (1/4-octave
-      // buckets, index order within one), small ones only unless
-      // HBG_WAVE_LARGE admits large ones of <= spec_rows rows among the R best
-      // (R = the commits still to come): a speculative large expansion costs a
-      // partition and histogram pass over its rows
-      unsigned* hist = reinterpret_cast<unsigned*>(smem_dyn);
-      int br = 1 << 30;
-      if (a.wlarge > 0 && L1 - committed - 1 > 0)
-        br = nav - 1 <= L1 - committed - 1
-                 ? 0  // all of them
-                 : bucket_select(w, hist, nav, L1 - committed - 1, [&](unsigned v) { return av_node(v) != ps; });
-      const auto cand = [&](unsigned v) {
-        return av_node(v) != ps && (av_class(v) == 0 || (av_class(v) == 1 && av_bucket(v) >= br));
-      };
-      const int want = m - 1;
-      const int B = want > 0 ? bucket_select(w, hist, nav, want, cand) : 1 << 30;
-      if (lane == 0) w.wave[0] = static_cast<short>(ps);
-      __syncwarp();
-      W = 1;
-      if (want > 0) {
-        // every candidate in the buckets above B (fewer than want) ...
-        for (int i0 = 0; i0 < nav; i0 += 32) {
-          const int i = i0 + lane;
-          const unsigned v = i < nav ? w.avail[i] : 0u;
-          const bool el = i < nav && cand(v) && av_bucket(v) > B;
-          const unsigned bal = __ballot_sync(0xffffffffu, el);
-          if (el) w.wave[W + __popc(bal & ((1u << lane) - 1u))] = static_cast<short>(av_node(v));
-          W += __popc(bal);
-        }
-        __syncwarp();
-        // ... then the best of bucket B by exact prio (ties: lowest node id),
-        // from its first 32 candidates (collected in shared memory), one per lane
-        unsigned* lst = hist + 1024;
-        int got = 0;
-        for (int i0 = 0; i0 < nav && got < 32; i0 += 32) {
-          const int i = i0 + lane;
-          const unsigned v = i < nav ? w.avail[i] : 0u;
-          const bool el = i < nav && cand(v) && av_bucket(v) == B;
-          const unsigned bal = __ballot_sync(0xffffffffu, el);
-          const int r = got + __popc(bal & ((1u << lane) - 1u));
-          if (el && r < 32) lst[r] = static_cast<unsigned>(av_node(v));
-          got += __popc(bal);
-        }
-        __syncwarp();
-        const int mine = lane < min(got, 32) ? static_cast<int>(lst[lane]) : -1;
-        unsigned long long key = mine >= 0 ? ((static_cast<unsigned long long>(__float_as_uint(w.prio[mine])) << 32) |
-                                              (0xFFFFFFFFu - static_cast<unsigned>(mine)))
-                                           : 0ull;
-        while (W < 1 + want) {
-          unsigned long long best_key = key;
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) {
-            const unsigned long long o = __shfl_xor_sync(0xffffffffu, best_key, off);
-            best_key = o > best_key ? o : best_key;
-          }
-          if (best_key == 0ull) break;
-          const int n = static_cast<int>(0xFFFFFFFFu - static_cast<unsigned>(best_key));
-          if (lane == 0) w.wave[W] = static_cast<short>(n);
-          if (key == best_key) key = 0ull;
-          ++W;
-        }
-        __syncwarp();
+      if (lane == 0) {
+        w.wave[0] = static_cast<short>(ps);
+        int n = 1;
+        for (int c = 0; c < w.ncl && n < m; ++c)
+          if (w.clist[c] != ps) w.wave[n++] = w.clist[c];
+        s_w = n;
       }
+      __syncwarp();
+      W = s_w;
       if (lane == 0 && w.nwaves > 0) stamp(a, w.nwaves - 1, 9);
       // members leave the expandable list; small members first
       for (int j = lane; j < W; j += 32) w.kid[w.wave[j]] = -2;  // mark
       __syncwarp();
+      const int nav = w.nav;
       int nav2 = 0;  // compaction in place: a round's reads precede its writes, which land below them
       for (int i0 = 0; i0 < nav; i0 += 32) {
         const int i = i0 + lane;
@@ -1932,7 +1984,7 @@ __device__ void wave_select(const GrowArgs& a, WaveSmem& w, unsigned char* smem_
       if (lane == 0) w.nav = nav2;
     }
     if (lane == 0) {
-      w.nfr = nfr;
+      w.nfr = s_nfr;
       w.committed = committed;
       w.done = W == 0 ? 1 : 0;
       w.W = W;
