@@ -3,7 +3,7 @@ usage: prof_tree_shape.py rows d k [trees] [zero_prob]"""
 import sys, os, time
 import numpy as np
 import torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("HBG_PKG_ROOT", os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_1706_08359_b200 as hbg  # noqa: E402
 
 rows, d, k = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
