@@ -5,10 +5,14 @@
 // HBG_ERR_LOGIC), device memory ownership, launch planning. There is no CPU
 // fallback anywhere: a missing GPU or CUDA failure is an error status.
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -103,6 +107,8 @@ struct hbg_dataset {
   bool grow_waves = false;             // ... LeafRange x grow_ranges (wave grower) or node records
   int grow_ranges = 0;
   void* pinned = nullptr;                      // host staging for per-split results
+  void* stage = nullptr;                       // pinned staging of pageable host inputs (stage_bytes)
+  size_t stage_bytes = 0;
   // measurement hooks
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;  // recorded, not yet read
@@ -120,6 +126,11 @@ struct hbg_dataset {
   }
   ~hbg_dataset() {
     if (pinned) cudaFreeHost(pinned);
+    if (stage) {
+      if (stream) cudaStreamSynchronize(stream);
+      if (copy_stream) cudaStreamSynchronize(copy_stream);
+      cudaFreeHost(stage);
+    }
     for (auto& e : events) spare.push_back(e);
     for (auto& e : spare) {
       cudaEventDestroy(e.first);
@@ -188,6 +199,143 @@ bool leaf_is_contiguous(const int32_t* idx, int64_t n) {
   for (auto& x : th) x.join();
   return std::all_of(ok.begin(), ok.end(), [](char c) { return c != 0; });
 }
+
+// ---- pageable host inputs -----------------------------------------------------
+// The reference's LeafState arrays are std::vectors: pageable memory, which a
+// cudaMemcpy moves through the driver's bounce buffers at ~11 GB/s (15-16 ms
+// for the 168 MB of fp64 g/h of the 10.5M-row leaf vs 3.0 ms pinned,
+// microbench/h2d_convert.cu). For such inputs the host pool converts fp64 ->
+// fp32 (round to nearest: the same floats the device conversion makes) into a
+// pinned stage chunk by chunk and the copy engine moves each finished chunk at
+// once: 8 B/row over PCIe, the conversion (host-memory bound, ~4.3 G rows/s on
+// 16 threads) the only exposed cost.
+bool is_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();  // (an unknown pointer is pageable; clear the sticky error)
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeManaged;
+}
+
+// A fixed pool of host workers (one per core up to 16), created on first use.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool pool;
+    return pool;
+  }
+  int size() const { return static_cast<int>(th_.size()); }
+  // fn(w) on every worker w; returns at once (wait() blocks until all finish)
+  void run(std::function<void(int)> fn) {
+    std::unique_lock<std::mutex> lk(m_);
+    job_ = std::move(fn);
+    pending_ = size();
+    ++gen_;
+    cv_.notify_all();
+  }
+  void wait() {
+    std::unique_lock<std::mutex> lk(m_);
+    done_.wait(lk, [&] { return pending_ == 0; });
+  }
+  ~HostPool() {
+    {
+      std::unique_lock<std::mutex> lk(m_);
+      stop_ = true;
+      cv_.notify_all();
+    }
+    for (auto& t : th_) t.join();
+  }
+
+ private:
+  HostPool() {
+    const int T = static_cast<int>(std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency())));
+    for (int w = 0; w < T; ++w) th_.emplace_back([this, w] { loop(w); });
+  }
+  void loop(int w) {
+    uint64_t seen = 0;
+    for (;;) {
+      std::function<void(int)> fn;
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        fn = job_;
+      }
+      fn(w);
+      std::unique_lock<std::mutex> lk(m_);
+      if (--pending_ == 0) done_.notify_all();
+    }
+  }
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  std::function<void(int)> job_;
+  uint64_t gen_ = 0;
+  int pending_ = 0;
+  bool stop_ = false;
+  std::vector<std::thread> th_;
+};
+
+void* stage_buffer(hbg_dataset* ds, size_t bytes) {
+  if (ds->stage_bytes < bytes) {
+    if (ds->stage) {
+      HBG_CUDA(cudaStreamSynchronize(ds->stream));
+      if (ds->copy_stream) HBG_CUDA(cudaStreamSynchronize(ds->copy_stream));
+      HBG_CUDA(cudaFreeHost(ds->stage));
+      ds->stage = nullptr;
+      ds->stage_bytes = 0;
+    }
+    HBG_CUDA(cudaHostAlloc(&ds->stage, bytes, cudaHostAllocDefault));
+    ds->stage_bytes = bytes;
+  }
+  return ds->stage;
+}
+
+// Stage rows [0, n) of fp64 g/h (and, when idx != nullptr, the int32 row ids)
+// into the pinned stage as fp32 (g | h | idx), in chunks of `chunk` rows
+// converted by the host pool; copy(c, b, e, gf, hf, id) runs on the calling
+// thread, in chunk order, as soon as chunk c is staged. Returns after the last
+// copy was issued.
+template <typename Copy>
+void stage_chunks(hbg_dataset* ds, const double* g, const double* h, const int32_t* idx, int64_t n, int64_t chunk,
+                  Copy copy) {
+  const size_t rows = static_cast<size_t>(n);
+  char* st = static_cast<char*>(stage_buffer(ds, rows * (idx ? 12 : 8) + 64));
+  float* gf = reinterpret_cast<float*>(st);
+  float* hf = gf + rows;
+  int32_t* id = reinterpret_cast<int32_t*>(hf + rows);
+  const int C = static_cast<int>((n + chunk - 1) / chunk);
+  HostPool& pool = HostPool::get();
+  const int T = pool.size();
+  std::unique_ptr<std::atomic<int>[]> done(new std::atomic<int>[static_cast<size_t>(C)]);
+  for (int c = 0; c < C; ++c) done[static_cast<size_t>(c)].store(0, std::memory_order_relaxed);
+  pool.run([&, C, T](int w) {
+    for (int c = 0; c < C; ++c) {
+      const int64_t b = chunk * c, e = std::min<int64_t>(n, b + chunk);
+      const int64_t s0 = b + (e - b) * w / T, s1 = b + (e - b) * (w + 1) / T;
+      for (int64_t i = s0; i < s1; ++i) {
+        gf[i] = static_cast<float>(g[i]);
+        hf[i] = static_cast<float>(h[i]);
+      }
+      if (idx) std::memcpy(id + s0, idx + s0, static_cast<size_t>(s1 - s0) * 4);
+      done[static_cast<size_t>(c)].fetch_add(1, std::memory_order_release);
+    }
+  });
+  try {
+    for (int c = 0; c < C; ++c) {
+      while (done[static_cast<size_t>(c)].load(std::memory_order_acquire) < T) std::this_thread::yield();
+      const int64_t b = chunk * c, e = std::min<int64_t>(n, b + chunk);
+      copy(c, b, e, gf, hf, id);
+    }
+  } catch (...) {
+    pool.wait();  // the workers still use `done` and the stage
+    throw;
+  }
+  pool.wait();
+}
+
+constexpr int64_t kStageRows = int64_t(1) << 19;  // rows per staged chunk (4 MB of fp32 g/h)
 
 // Device row ids [first, first + n) of the dataset: the resident iota array.
 const int32_t* identity_rows(hbg_dataset* ds, int64_t first, cudaStream_t s) {
@@ -933,7 +1081,50 @@ int hbg_build_histograms(hbg_dataset* ds, const int32_t* indices, int64_t count,
     const size_t D = static_cast<size_t>(L.num_features) * L.max_bin;
     double* d_hist = static_cast<double*>(ds->host_hist.get(3 * D * sizeof(double) + 8));
     hbg_bin* d_bins = static_cast<hbg_bin*>(ds->host_bins.get(D * sizeof(hbg_bin) + 8));
-    if (count > 0) {
+    if (count > 0 && !(is_pinned(gradients) && is_pinned(hessians))) {
+      // pageable LeafState arrays: fp32 g/h staged by the host pool (see
+      // stage_chunks); histogram chunk c runs as soon as its rows have landed
+      const size_t n = static_cast<size_t>(count);
+      float* d_gf = static_cast<float*>(ds->host_gf.get(n * 4));
+      float* d_hf = static_cast<float*>(ds->host_hf.get(n * 4));
+      const int C = count >= (int64_t{1} << 21) ? 4 : 1;  // as the pinned path: the same sums
+      if (!ds->copy_stream) HBG_CUDA(cudaStreamCreateWithFlags(&ds->copy_stream, cudaStreamNonBlocking));
+      for (int c = 0; c < 5; ++c)
+        if (!ds->chunk_ev[c]) HBG_CUDA(cudaEventCreateWithFlags(&ds->chunk_ev[c], cudaEventDisableTiming));
+      HBG_CUDA(cudaEventRecord(ds->chunk_ev[4], s));
+      HBG_CUDA(cudaStreamWaitEvent(ds->copy_stream, ds->chunk_ev[4], 0));
+      const int32_t first = indices[0];
+      const bool contiguous = leaf_is_contiguous(indices, count);
+      const int32_t* d_idx;
+      int32_t* di = nullptr;
+      if (contiguous) {
+        require(first >= 0 && first + count <= L.num_rows, "leaf row index out of range");
+        d_idx = identity_rows(ds, first, s);
+      } else {
+        di = static_cast<int32_t*>(ds->host_idx.get(n * 4));
+        d_idx = di;
+      }
+      double* parts = C > 1 ? static_cast<double*>(ds->host_parts.get(static_cast<size_t>(C) * 3 * D * sizeof(double) + 8))
+                            : d_hist;
+      std::vector<const double*> part_ptrs;
+      int next = 0;
+      stage_chunks(ds, gradients, hessians, contiguous ? nullptr : indices, count, kStageRows,
+                   [&](int, int64_t b, int64_t e, const float* gs, const float* hs, const int32_t* is) {
+                     const size_t m = static_cast<size_t>(e - b);
+                     HBG_CUDA(cudaMemcpyAsync(d_gf + b, gs + b, m * 4, cudaMemcpyHostToDevice, ds->copy_stream));
+                     HBG_CUDA(cudaMemcpyAsync(d_hf + b, hs + b, m * 4, cudaMemcpyHostToDevice, ds->copy_stream));
+                     if (di) HBG_CUDA(cudaMemcpyAsync(di + b, is + b, m * 4, cudaMemcpyHostToDevice, ds->copy_stream));
+                     for (; next < C && count * (next + 1) / C <= e; ++next) {
+                       const int64_t cb = count * next / C, ce = count * (next + 1) / C;
+                       HBG_CUDA(cudaEventRecord(ds->chunk_ev[next], ds->copy_stream));
+                       HBG_CUDA(cudaStreamWaitEvent(s, ds->chunk_ev[next], 0));
+                       double* hc = parts + static_cast<size_t>(next) * (C > 1 ? 3 * D : 0);
+                       build_device(ds, d_idx + cb, ce - cb, d_gf + cb, d_hf + cb, HBG_GH_LEAF_ALIGNED, hc, s);
+                       part_ptrs.push_back(hc);
+                     }
+                   });
+      if (C > 1) launch_reduce_parts(part_ptrs, static_cast<int64_t>(3 * D), d_hist, s);
+    } else if (count > 0) {
       const size_t n = static_cast<size_t>(count);
       double* d_gd = static_cast<double*>(ds->host_gd.get(n * 8));
       double* d_hd = static_cast<double*>(ds->host_hd.get(n * 8));
@@ -1123,7 +1314,17 @@ int hbg_grow_tree_host(hbg_dataset* ds, const double* gradients, const double* h
     DeviceGuard dg(ds->layout.device);
     cudaStream_t s = ds->stream;
     float *gf = nullptr, *hf = nullptr;
-    if (N > 0) {
+    if (N > 0 && !(is_pinned(gradients) && is_pinned(hessians))) {  // pageable: staged as fp32 (stage_chunks)
+      const size_t n = static_cast<size_t>(N);
+      gf = static_cast<float*>(ds->boost_g.get(n * 4 + 4));
+      hf = static_cast<float*>(ds->boost_h.get(n * 4 + 4));
+      stage_chunks(ds, gradients, hessians, nullptr, N, kStageRows,
+                   [&](int, int64_t b, int64_t e, const float* gs, const float* hs, const int32_t*) {
+                     const size_t m = static_cast<size_t>(e - b);
+                     HBG_CUDA(cudaMemcpyAsync(gf + b, gs + b, m * 4, cudaMemcpyHostToDevice, s));
+                     HBG_CUDA(cudaMemcpyAsync(hf + b, hs + b, m * 4, cudaMemcpyHostToDevice, s));
+                   });
+    } else if (N > 0) {
       const size_t n = static_cast<size_t>(N);
       double* gd = static_cast<double*>(ds->host_gd.get(n * 8));
       double* hd = static_cast<double*>(ds->host_hd.get(n * 8));

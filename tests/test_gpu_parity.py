@@ -149,6 +149,33 @@ def test_host_dropin_contiguous_leaf_shortcut(hbg, oracle):
             assert_hist_close(got, oracle.build_histograms(cols, 64, idx, g, h, 64), tol=1e-4)
 
 
+def test_host_dropin_pageable_and_pinned_agree(hbg, oracle):
+    """Pageable LeafState arrays (numpy: the reference's std::vectors) take the
+    host-staged fp32 path (host pool converts chunks into a pinned stage while
+    the copy engine moves finished ones), pinned arrays the fp64 DMA path: the
+    same floats, the same chunked sums — bit-identical histograms and trees."""
+    torch = torch_cuda()
+    rng = np.random.default_rng(23)
+    rows = 2_500_000  # > 2 Mi rows: four histogram chunks, several staged chunks each
+    cols = rng.integers(0, 64, size=(28, rows), dtype=np.uint8)
+
+    def pinned(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+
+    with hbg.Dataset(cols, 64) as ds:
+        for idx in (np.arange(rows, dtype=np.int32),                        # contiguous: no index upload
+                    np.sort(rng.choice(rows, size=2_200_000, replace=False)).astype(np.int32),
+                    rng.permutation(rows)[:700_001].astype(np.int32)):
+            g, h = rng.normal(size=len(idx)), rng.random(len(idx))
+            a = hbg.build_histograms_partitioned(ds, hbg.LeafState(idx, g, h))
+            b = hbg.build_histograms_partitioned(ds, hbg.LeafState(pinned(idx), pinned(g), pinned(h)))
+            assert a.tobytes() == b.tobytes()
+        g, h = rng.normal(size=rows), rng.random(rows)
+        la, na = ds.grow_tree_host(g, h, 63, 20, 0.0)
+        lb, nb = ds.grow_tree_host(pinned(g), pinned(h), 63, 20, 0.0)
+        assert la.tobytes() == lb.tobytes() and na.tobytes() == nb.tobytes()
+
+
 def test_unsorted_and_duplicate_free_indices(hbg, oracle):
     """Leaf order only changes fp32 rounding; counts stay exact."""
     rng = np.random.default_rng(9)
