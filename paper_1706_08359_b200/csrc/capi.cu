@@ -249,7 +249,9 @@ class HostPool {
 
  private:
   HostPool() {
-    const int T = static_cast<int>(std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency())));
+    // one core stays with the calling thread, which issues the copies
+    const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+    const int T = static_cast<int>(std::min<unsigned>(16, hw - 1));
     for (int w = 0; w < T; ++w) th_.emplace_back([this, w] { loop(w); });
   }
   void loop(int w) {
@@ -1093,27 +1095,20 @@ int hbg_build_histograms(hbg_dataset* ds, const int32_t* indices, int64_t count,
         if (!ds->chunk_ev[c]) HBG_CUDA(cudaEventCreateWithFlags(&ds->chunk_ev[c], cudaEventDisableTiming));
       HBG_CUDA(cudaEventRecord(ds->chunk_ev[4], s));
       HBG_CUDA(cudaStreamWaitEvent(ds->copy_stream, ds->chunk_ev[4], 0));
-      const int32_t first = indices[0];
-      const bool contiguous = leaf_is_contiguous(indices, count);
-      const int32_t* d_idx;
-      int32_t* di = nullptr;
-      if (contiguous) {
-        require(first >= 0 && first + count <= L.num_rows, "leaf row index out of range");
-        d_idx = identity_rows(ds, first, s);
-      } else {
-        di = static_cast<int32_t*>(ds->host_idx.get(n * 4));
-        d_idx = di;
-      }
+      // the row ids ride along with g/h (a contiguity check would be one more
+      // serial pass over the ids; their 4 B/row fit under the conversion)
+      int32_t* di = static_cast<int32_t*>(ds->host_idx.get(n * 4));
+      const int32_t* d_idx = di;
       double* parts = C > 1 ? static_cast<double*>(ds->host_parts.get(static_cast<size_t>(C) * 3 * D * sizeof(double) + 8))
                             : d_hist;
       std::vector<const double*> part_ptrs;
       int next = 0;
-      stage_chunks(ds, gradients, hessians, contiguous ? nullptr : indices, count, kStageRows,
+      stage_chunks(ds, gradients, hessians, indices, count, kStageRows,
                    [&](int, int64_t b, int64_t e, const float* gs, const float* hs, const int32_t* is) {
                      const size_t m = static_cast<size_t>(e - b);
                      HBG_CUDA(cudaMemcpyAsync(d_gf + b, gs + b, m * 4, cudaMemcpyHostToDevice, ds->copy_stream));
                      HBG_CUDA(cudaMemcpyAsync(d_hf + b, hs + b, m * 4, cudaMemcpyHostToDevice, ds->copy_stream));
-                     if (di) HBG_CUDA(cudaMemcpyAsync(di + b, is + b, m * 4, cudaMemcpyHostToDevice, ds->copy_stream));
+                     HBG_CUDA(cudaMemcpyAsync(di + b, is + b, m * 4, cudaMemcpyHostToDevice, ds->copy_stream));
                      for (; next < C && count * (next + 1) / C <= e; ++next) {
                        const int64_t cb = count * next / C, ce = count * (next + 1) / C;
                        HBG_CUDA(cudaEventRecord(ds->chunk_ev[next], ds->copy_stream));

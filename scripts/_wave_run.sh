@@ -1,8 +1,4 @@
 export CUDA_DEVICE_MAX_CONNECTIONS=32
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "wave_grower or grow_tree or boosting" 2>&1 | tail -1
 for i in 1 2; do
-echo "== old"; HBG_PKG_ROOT=$PWD/_ab_old timeout 120 python scripts/prof_tree_shape.py 10500000 28 16 3 2>&1 | tail -1
-echo "== new"; timeout 120 python scripts/prof_tree_shape.py 10500000 28 16 3 2>&1 | tail -1
+timeout 300 python bench.py --steps 20 --warmup 3 --no-variants --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('e2e', d['e2e']['ms_per_step'], 'pageable', d['e2e']['pageable_ms_per_step'], 'tree', d['tree']['sec_per_tree'], d['tree']['e2e_sec_per_tree'], d['tree']['e2e_pageable_sec_per_tree'])"
 done
-echo "== new k64"; timeout 120 python scripts/prof_tree_shape.py 10500000 28 64 3 2>&1 | tail -1
-echo "== new 1M"; timeout 120 python scripts/prof_tree_shape.py 1000000 28 64 3 2>&1 | tail -1
