@@ -884,7 +884,7 @@ void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_h
       nfr += static_cast<double>(t[15]);
     }
     if (counts[3] > 0)
-      std::fprintf(stderr, "wave grower: per wave %.2f commits replayed in %.2f us (clock64), candidates %.2f us (warp 1), "
+      std::fprintf(stderr, "wave grower: per wave %.2f commits replayed in %.2f us (clock64), choice %.2f us, "
                    "%.0f expandable, %.0f open leaves\n", commits / counts[3], rep / counts[3], cand / counts[3],
                    nav / counts[3], nfr / counts[3]);
   } else if (a.prof != nullptr) {

@@ -1625,8 +1625,8 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
 constexpr int kWN = 1280;  // node ids per tree (shared-memory state)
 static_assert(kWN <= 2048, "node ids are packed in 11 bits");
 
-// Speculation order: prio buckets of 1/4 octave (a positive float's bits >> 21).
-__device__ __forceinline__ int prio_bucket(float p) { return static_cast<int>(__float_as_uint(p) >> 21); }
+// Speculation order: prio buckets of 1/32 octave (a positive float's top 13 bits).
+__device__ __forceinline__ int prio_bucket(float p) { return static_cast<int>(__float_as_uint(p) >> 18); }
 constexpr int kWL = 256;   // open leaves: num_leaves <= kWL
 constexpr int kWMax = 16;  // members per wave
 
@@ -1635,21 +1635,24 @@ struct WaveSmem {
   float prio[kWN];               // min gain along the path from the root
   short kid[kWN];                // left child once expanded, -1 before
   unsigned char large[kWN];      // 0: small; runs the large-parent paths: 1 (<= spec_rows rows), 2
-  unsigned avail[kWN];           // expandable (discovered, gain > 0, not expanded): av_pack()
+  unsigned avail[kWN];           // expandable (discovered, gain > 0, not expanded): av_pack(), sorted descending
   unsigned long long fkey[kWL];  // the replay's open leaves with a split: gain key, node, output id
   short fnode[kWL], fout[kWL];
   short wave[kWMax];             // members: small ones first
   unsigned char later[kWL];      // commit i: bit c = child c was split later
-  short clist[32];               // speculation candidates by prio (wave_candidates)
-  int nav, nfr, committed, next, expanded, done, W, nsmall, nwc, wc, nwaves, hitems, ditems, err, ncl;
+  unsigned fresh[32];            // the last wave's new expandable entries, sorted (wave_integrate)
+  int nav, nfr, committed, next, expanded, done, W, nsmall, nwc, wc, nwaves, hitems, ditems, err, nfresh;
 };
 
-// An expandable-list entry: node id, size class (w.large), prio bucket.
+// An expandable-list entry, ordered as the speculation ranks nodes: prio
+// bucket (descending), then the lowest node id; the size class rides along.
+// 13 + 11 + 2 bits.
 __device__ __forceinline__ unsigned av_pack(int node, int cls, int bucket) {
-  return static_cast<unsigned>(node) | (static_cast<unsigned>(cls) << 11) | (static_cast<unsigned>(bucket) << 13);
+  return (static_cast<unsigned>(bucket) << 13) | (static_cast<unsigned>(2047 - node) << 2) |
+         static_cast<unsigned>(cls);
 }
-__device__ __forceinline__ int av_node(unsigned v) { return static_cast<int>(v & 0x7FFu); }
-__device__ __forceinline__ int av_class(unsigned v) { return static_cast<int>((v >> 11) & 3u); }
+__device__ __forceinline__ int av_node(unsigned v) { return 2047 - static_cast<int>((v >> 2) & 0x7FFu); }
+__device__ __forceinline__ int av_class(unsigned v) { return static_cast<int>(v & 3u); }
 __device__ __forceinline__ int av_bucket(unsigned v) { return static_cast<int>(v >> 13); }
 
 // Per-CTA state in global memory (written by the CTA's warp 0, read back by
@@ -1715,144 +1718,80 @@ __device__ void wave_integrate(const GrowArgs& a, WaveSmem& w) {
     id = static_cast<int>(av_pack(id, cls, prio_bucket(pr)));
   }
   const int err = lane == 31 ? error_of(a) : 0;  // (one L2 round trip with the loads above)
-  const unsigned bal = __ballot_sync(0xffffffffu, add);
-  if (add) w.avail[w.nav + __popc(bal & ((1u << lane) - 1u))] = static_cast<unsigned>(id);
-  __syncwarp();
-  if (lane == 0) w.nav += __popc(bal);
-  if (lane == 31) w.err = err;
-  __syncwarp();
-}
-
-// Warp 0: bucket histogram (1024 counters in `hist`, shared memory) of the
-// expandable nodes with pred(node); returns the highest bucket B such that at
-// least `want` (>= 1) of them lie in buckets >= B (0 when fewer exist).
-template <typename Pred>
-__device__ int bucket_select(const WaveSmem& w, unsigned* hist, int nav, int want, Pred pred) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int u = 0; u < 32; ++u) hist[u * 32 + lane] = 0u;
-  __syncwarp();
-  for (int i0 = 0; i0 < nav; i0 += 32) {  // warp-aggregated: many nodes share their parent's prio
-    const int i = i0 + lane;
-    const unsigned v = i < nav ? w.avail[i] : 0u;
-    const bool el = i < nav && pred(v);
-    const unsigned act = __ballot_sync(0xffffffffu, el);
-    if (el) {
-      const unsigned peers = __match_any_sync(act, av_bucket(v));
-      if (lane == __ffs(peers) - 1) atomicAdd(hist + av_bucket(v), static_cast<unsigned>(__popc(peers)));
-    }
-  }
-  __syncwarp();
-  // lane l owns buckets [32 l, 32 l + 32); counts from the top
-  unsigned mine = 0u;
-#pragma unroll 8
-  for (int u = 0; u < 32; ++u) mine += hist[lane * 32 + u];
-  // inclusive suffix sum over lanes (lane 31 = top buckets)
-  unsigned suf = mine;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const unsigned v = __shfl_down_sync(0xffffffffu, suf, off);
-    if (lane + off < 32) suf += v;
-  }
-  const unsigned above = suf - mine;  // nodes in the buckets of the lanes above
-  const bool cross = above < static_cast<unsigned>(want) && suf >= static_cast<unsigned>(want);
-  const unsigned bal = __ballot_sync(0xffffffffu, cross);
-  if (bal == 0u) return 0;  // fewer than `want`: every bucket
-  const int l = 31 - __clz(bal);  // the only crossing lane; its 32 buckets one per lane
-  const unsigned base = __shfl_sync(0xffffffffu, above, l);
-  unsigned sb = hist[l * 32 + lane];
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const unsigned v = __shfl_down_sync(0xffffffffu, sb, off);
-    if (lane + off < 32) sb += v;
-  }
-  const unsigned ok = __ballot_sync(0xffffffffu, base + sb >= static_cast<unsigned>(want));
-  return l * 32 + (31 - __clz(ok));
-}
-
-// Warp 1, while warp 0 replays: the speculation candidates — ~the wmax
-// expandable nodes with the largest prio (1/4-octave buckets, then exact prio
-// and node id inside the threshold bucket), small ones, plus large ones of
-// <= spec_rows rows among the R best (R = the commits still to come before this
-// replay, an upper bound) when HBG_WAVE_LARGE allows: a speculative large
-// expansion costs a partition and histogram pass over its rows. Sorted by
-// prio into w.clist (w.ncl entries). The certain pick may be among them.
-__device__ void wave_candidates(const GrowArgs& a, WaveSmem& w, unsigned char* smem_dyn) {
-  const int lane = threadIdx.x & 31;
-  const int nav = w.nav;
-  const int r0 = a.num_leaves - 1 - w.committed;
-  unsigned* hist = reinterpret_cast<unsigned*>(smem_dyn);
-  int br = 1 << 30;
-  if (a.wlarge > 0 && r0 > 0)
-    br = nav <= r0 ? 0 : bucket_select(w, hist, nav, r0, [&](unsigned) { return true; });
-  const auto cand = [&](unsigned v) { return av_class(v) == 0 || (av_class(v) == 1 && av_bucket(v) >= br); };
-  const int want = a.wmax;
-  const int B = bucket_select(w, hist, nav, want, cand);
-  // every candidate above bucket B (fewer than want), then bucket B's best by
-  // exact prio from its first 32 (one per lane)
-  unsigned long long key = 0ull;  // this lane's list entry: prio bits << 32 | ~node
-  int W = 0;
-  for (int i0 = 0; i0 < nav; i0 += 32) {
-    const int i = i0 + lane;
-    const unsigned v = i < nav ? w.avail[i] : 0u;
-    const bool el = i < nav && cand(v) && av_bucket(v) > B;
-    const unsigned bal = __ballot_sync(0xffffffffu, el);
-    const int n = av_node(v);
-    const unsigned long long k = (static_cast<unsigned long long>(__float_as_uint(w.prio[n])) << 32) |
-                                 (0xFFFFFFFFu - static_cast<unsigned>(n));
-    // entry W + rank goes to lane W + rank
-    for (unsigned bb = bal; bb != 0u; bb &= bb - 1u) {
-      const int from = __ffs(bb) - 1;
-      const unsigned long long kv = __shfl_sync(0xffffffffu, k, from);
-      if (lane == W) key = kv;
-      ++W;
-    }
-  }
-  unsigned* lst = hist + 1024;
-  int got = 0;
-  for (int i0 = 0; i0 < nav && got < 32; i0 += 32) {
-    const int i = i0 + lane;
-    const unsigned v = i < nav ? w.avail[i] : 0u;
-    const bool el = i < nav && cand(v) && av_bucket(v) == B;
-    const unsigned bal = __ballot_sync(0xffffffffu, el);
-    const int r = got + __popc(bal & ((1u << lane) - 1u));
-    if (el && r < 32) lst[r] = static_cast<unsigned>(av_node(v));
-    got += __popc(bal);
-  }
-  __syncwarp();
-  const int mine = lane < min(got, 32) ? static_cast<int>(lst[lane]) : -1;
-  unsigned long long bk = mine >= 0 ? ((static_cast<unsigned long long>(__float_as_uint(w.prio[mine])) << 32) |
-                                       (0xFFFFFFFFu - static_cast<unsigned>(mine)))
-                                    : 0ull;
-  // bitonic sort of bucket B's keys, descending; its best fill the list after
-  // the entries above B (which all rank higher)
+  // the new entries, sorted descending across the lanes (bitonic), merged into
+  // the sorted list from its end (every entry moves right by the number of new
+  // entries above it; a round's reads precede its writes, which land at or
+  // above the rows still to be read)
+  unsigned key = add ? static_cast<unsigned>(id) : 0u;
 #pragma unroll
   for (int k = 2; k <= 32; k <<= 1) {
 #pragma unroll
     for (int j = k >> 1; j > 0; j >>= 1) {
-      const unsigned long long o = __shfl_xor_sync(0xffffffffu, bk, j);
-      const bool up = (lane & k) == 0;
-      const bool lower = (lane & j) == 0;
-      bk = (lower == up ? o > bk : o < bk) ? o : bk;
+      const unsigned o = __shfl_xor_sync(0xffffffffu, key, j);
+      const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+      key = (lower == up ? o > key : o < key) ? o : key;
     }
   }
-  const int take = min(want - W, min(got, 32));
-  const unsigned long long moved = __shfl_sync(0xffffffffu, bk, (lane - W) & 31);
-  if (lane >= W && lane < W + take) key = moved;
-  W += take;
-  if (lane < W) w.clist[lane] = static_cast<short>(0xFFFFFFFFu - static_cast<unsigned>(key));
-  if (lane == 0) w.ncl = W;
+  w.fresh[lane] = key;
+  if (lane == 0) w.nfresh = __popc(__ballot_sync(0xffffffffu, add));
+  else __ballot_sync(0xffffffffu, add);
+  if (lane == 31) w.err = err;
   __syncwarp();
 }
 
-// Every CTA (identical everywhere): warp 0 replays the reference's picks over
-// the expanded leaves (commit) while warp 1 ranks the speculation
-// candidates; then warp 0 forms the next wave. Whole CTA.
+// Warp 1, while warp 0 replays: merge the sorted new entries (w.fresh) into
+// the sorted expandable list from its end — every entry moves right by the
+// number of new entries above it; a round's reads precede its writes, which
+// land at or above the rows still to be read; entries above the largest new
+// one stay put (the loop stops there).
+__device__ void wave_merge(WaveSmem& w) {
+  const int lane = threadIdx.x & 31;
+  const int m = w.nfresh, n = w.nav;
+  if (m == 0) return;
+  const unsigned key = w.fresh[lane];
+  int above = 0;  // new entry `lane`'s position: lane + the old entries above it
+  if (lane < m) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (w.avail[mid] > key) lo = mid + 1; else hi = mid;
+    }
+    above = lo;
+  }
+  const unsigned top = w.fresh[0];
+  for (int i0 = n - 1; i0 >= 0; i0 -= 32) {
+    const int i = i0 - lane;
+    const unsigned v = i >= 0 ? w.avail[i] : 0xFFFFFFFFu;
+    int s_new = 0;  // new entries above v
+    if (v < top) {
+      int lo = 0, hi = m;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (w.fresh[mid] > v) lo = mid + 1; else hi = mid;
+      }
+      s_new = lo;
+    }
+    __syncwarp();
+    if (i >= 0 && s_new > 0) w.avail[i + s_new] = v;
+    if (!__any_sync(0xffffffffu, s_new > 0)) break;  // every earlier entry ranks above all new ones
+  }
+  __syncwarp();
+  if (lane < m) w.avail[lane + above] = key;
+  if (lane == 0) w.nav = n + m;
+  __syncwarp();
+}
+
+// Every CTA (warp 0, identical everywhere): replay the reference's picks over
+// the expanded leaves (commit), then form the next wave: the certain pick plus
+// the first entries of the sorted expandable list — small nodes, and large
+// ones of <= spec_rows rows ranked within the R best (R = the commits still to
+// come) when HBG_WAVE_LARGE allows: a speculative large expansion costs a
+// partition and histogram pass over its rows. Whole CTA.
 template <int NT>
-__device__ void wave_select(const GrowArgs& a, WaveSmem& w, unsigned char* smem_dyn) {
-  __shared__ int s_best, s_committed, s_nfr, s_w;
+__device__ void wave_select(const GrowArgs& a, WaveSmem& w) {
+  __shared__ int s_best, s_committed, s_nfr;
   const int L1 = a.num_leaves - 1;
-  __syncthreads();  // warp 0's integrate is complete for warp 1
+  __syncthreads();  // warp 0's integrate is complete for warp 1's merge
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     const WaveLog lg = wave_log(a);
@@ -1920,7 +1859,7 @@ __device__ void wave_select(const GrowArgs& a, WaveSmem& w, unsigned char* smem_
       s_committed = committed;
       s_nfr = nfr;
       if (w.nwaves > 0) {
-        stamp(a, w.nwaves - 1, 8);
+        stamp(a, w.nwaves - 1, 8);  // (the merge ran alongside)
         if (a.prof != nullptr && blockIdx.x == 0) {
           unsigned long long* t = a.prof + static_cast<size_t>(w.nwaves - 1) * kProfSlots;
           t[12] = static_cast<unsigned long long>(committed - w.committed);
@@ -1931,11 +1870,7 @@ __device__ void wave_select(const GrowArgs& a, WaveSmem& w, unsigned char* smem_
       }
     }
   } else if (threadIdx.x < 64) {
-    const long long c0 = clock64();
-    if (a.wmax > 1 && w.err == kErrNone) wave_candidates(a, w, smem_dyn);
-    else if (threadIdx.x == 32) w.ncl = 0;
-    if (threadIdx.x == 32 && a.prof != nullptr && blockIdx.x == 0 && w.nwaves > 0)
-      a.prof[static_cast<size_t>(w.nwaves - 1) * kProfSlots + 13] = static_cast<unsigned long long>(clock64() - c0);
+    wave_merge(w);
   }
   __syncthreads();
   if (threadIdx.x < 32) {
@@ -1947,20 +1882,30 @@ __device__ void wave_select(const GrowArgs& a, WaveSmem& w, unsigned char* smem_
       const int ps = w.fnode[best];
       int m = min(L1 - committed, a.wmax);
       m = max(1, min(m, a.ecap - w.expanded));
-      if (lane == 0) {
-        w.wave[0] = static_cast<short>(ps);
-        int n = 1;
-        for (int c = 0; c < w.ncl && n < m; ++c)
-          if (w.clist[c] != ps) w.wave[n++] = w.clist[c];
-        s_w = n;
+      const int nav = w.nav;
+      const long long c0 = clock64();
+      // large entries qualify down to the R-th entry's key
+      const int r = L1 - committed - 1;
+      const unsigned tr = a.wlarge > 0 && r > 0 ? (nav > r ? w.avail[r] : 0u) : 0xFFFFFFFFu;
+      if (lane == 0) w.wave[0] = static_cast<short>(ps);
+      W = 1;
+      for (int i0 = 0; i0 < nav && W < m; i0 += 32) {
+        const int i = i0 + lane;
+        const unsigned v = i < nav ? w.avail[i] : 0u;
+        const int cls = av_class(v);
+        const bool el = i < nav && av_node(v) != ps && (cls == 0 || (cls == 1 && v >= tr));
+        const unsigned bal = __ballot_sync(0xffffffffu, el);
+        const int r2 = W + __popc(bal & ((1u << lane) - 1u));
+        if (el && r2 < m) w.wave[r2] = static_cast<short>(av_node(v));
+        W = min(m, W + __popc(bal));
       }
       __syncwarp();
-      W = s_w;
+      if (lane == 0 && a.prof != nullptr && blockIdx.x == 0 && w.nwaves > 0)
+        a.prof[static_cast<size_t>(w.nwaves - 1) * kProfSlots + 13] = static_cast<unsigned long long>(clock64() - c0);
       if (lane == 0 && w.nwaves > 0) stamp(a, w.nwaves - 1, 9);
       // members leave the expandable list; small members first
       for (int j = lane; j < W; j += 32) w.kid[w.wave[j]] = -2;  // mark
       __syncwarp();
-      const int nav = w.nav;
       int nav2 = 0;  // compaction in place: a round's reads precede its writes, which land below them
       for (int i0 = 0; i0 < nav; i0 += 32) {
         const int i = i0 + lane;
@@ -2341,7 +2286,7 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_wave_kernel(GrowArg
     w.prio[0] = hb ? static_cast<float>(bs.gain) : 0.f;
     w.kid[0] = -1;
     w.large[0] = runs_large(a, a.root_count, hb ? bs.left_count : 0) ? (a.root_count <= a.spec_rows ? 1 : 2) : 0;
-    w.nav = w.nfr = 0;
+    w.nav = w.nfr = w.nfresh = 0;
     w.committed = w.expanded = w.done = w.W = w.nsmall = w.nwaves = w.err = 0;
     w.next = 1;
     if (k0 != 0ull && a.num_leaves >= 2) {
@@ -2353,7 +2298,7 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_wave_kernel(GrowArg
     }
   }
   grid_sync(a);  // CTA 0's root records
-  wave_select<NT>(a, w, smem);
+  wave_select<NT>(a, w);
   const double eg = ldexp(1.0, a.exps[0]), eh = ldexp(1.0, a.exps[1]);  // fixed-point scales
   while (!w.done) {
     if (a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -2382,7 +2327,7 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_wave_kernel(GrowArg
     if (threadIdx.x < 32) wave_integrate(a, w);
     stamp(a, w.nwaves, 6);
     if (threadIdx.x == 0) ++w.nwaves;
-    wave_select<NT>(a, w, smem);
+    wave_select<NT>(a, w);
     stamp(a, w.nwaves - 1, 5);
   }
   wave_emit(a, w);
@@ -2432,13 +2377,14 @@ int wave_extra(const PersistentGrowArgs& h) {
   const char* e = std::getenv("HBG_GROW");
   if (h.nranks > 1 || (e != nullptr && std::strcmp(e, "legacy") == 0)) return -1;
   if (h.num_leaves > kWL || (h.bits != 4 && h.k > 128)) return -1;
-  // waves pay where per-split latency dominates: many small leaves (rows per
-  // leaf <= 16K) and cheap finishes (features x bins <= 16K). Measured: Higgs
-  // 1M x 28 k64 2.4 ms vs 4.7 with one split per barrier; 10.5M rows, or
-  // 2000 features (epsilon), are faster one split at a time.
+  // waves pay where the per-split chain (partition, histogram, scans,
+  // barrier, pick) dominates and a speculative expansion is cheap: 8-bit data
+  // with <= 4096 feature x bin cells. Measured (255 leaves, min_data 1) against
+  // one split per barrier: Higgs 28 x k64 at 1M rows 2.4 vs 4.6 ms, 3M 2.6 vs
+  // 5.3, 10.5M 5.4 vs 6.0; but 200 features 7.3 vs 5.2 and the 4-bit k16
+  // kernel 6.8 vs 6.0 (10.5M rows).
   const bool forced = e != nullptr && std::strcmp(e, "wave") == 0;  // HBG_GROW=wave: whenever it fits
-  if (!forced && (h.num_rows > 16384LL * std::max(1, h.num_leaves) || static_cast<long long>(h.d) * h.k > 16384))
-    return -1;
+  if (!forced && (h.bits == 4 || static_cast<long long>(h.d) * h.k > 4096)) return -1;
   const int L1 = std::max(0, h.num_leaves - 1);
   const size_t slot = static_cast<size_t>(3) * h.d * h.k * sizeof(double);
   const long long fit = std::min<long long>(kWN, static_cast<long long>(kWaveSlotBudget / std::max<size_t>(slot, 1)));
