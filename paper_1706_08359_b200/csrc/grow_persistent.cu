@@ -1605,11 +1605,14 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
 //    tree.cpp:224-236 numbers them. The first best open leaf that is not
 //    expanded yet is the reference's next split, for certain.
 //  * The next wave expands that leaf plus up to wmax-1 speculative ones: the
-//    expandable nodes of the speculative tree with the largest min-gain along
-//    their path (best-first expands in that order up to ties). Speculation is
-//    bounded in total by `ecap`; an expansion the replay never commits is
-//    not emitted (its rows moved into the other ordered buffer, its own range
-//    in its buffer is intact, its children never enter the pool).
+//    expandable nodes of the speculative tree (children of expanded nodes,
+//    committed or not) with the largest min-gain along their path
+//    (best-first expands in that order up to ties). Speculation is bounded in
+//    total by `ecap`; an expansion the replay never commits is not emitted,
+//    and its children never enter the pool. Rows stay partitioned among the
+//    unexpanded nodes of the speculative tree (an unexpanded node's range is
+//    never rewritten after its creation), so the score update walks those
+//    with the value of the final leaf above each (wave_emit).
 //
 // A wave runs its small members (parent <= small_max rows) as (member,
 // feature chunk) items in one phase — each CTA ranks its member's parent in
@@ -1619,7 +1622,7 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
 // of the smaller child, chunk finishes. The last CTA to finish a member's
 // chunks (atomic count) reduces the chunk winners and publishes the
 // children's records. Barriers per wave: 1 (small members only) to 4. The
-// output (split log, tree, committed records) is written once at the end
+// output (split log, tree, score-update ranges) is written once at the end
 // from the replayed commit log.
 
 constexpr int kWN = 1280;  // node ids per tree (shared-memory state)
@@ -1781,8 +1784,9 @@ __device__ void wave_merge(WaveSmem& w) {
   __syncwarp();
 }
 
-// Every CTA (warp 0, identical everywhere): replay the reference's picks over
-// the expanded leaves (commit), then form the next wave: the certain pick plus
+// Every CTA (identical everywhere): warp 0 replays the reference's picks over
+// the expanded leaves (commit) while warp 1 merges the last wave's new
+// expandable entries (wave_merge); then warp 0 forms the next wave: the certain pick plus
 // the first entries of the sorted expandable list — small nodes, and large
 // ones of <= spec_rows rows ranked within the R best (R = the commits still to
 // come) when HBG_WAVE_LARGE allows: a speculative large expansion costs a
