@@ -410,6 +410,14 @@ __device__ __forceinline__ hbg_split load_split(const hbg_split* p) {
 // ~((f << 12) | b) so the lowest feature, then the lowest bin wins ties —
 // the reference's strict `>` scans (tree.cpp:95,172).
 __device__ __forceinline__ void warp_argmax_key(unsigned long long& hi, unsigned& lo, int width = 32) {
+  if (width == 32) {  // three single-instruction integer reductions (redux.sync), lexicographic
+    const unsigned h1 = static_cast<unsigned>(hi >> 32), h0 = static_cast<unsigned>(hi);
+    const unsigned m1 = __reduce_max_sync(0xffffffffu, h1);
+    const unsigned m0 = __reduce_max_sync(0xffffffffu, h1 == m1 ? h0 : 0u);
+    lo = __reduce_max_sync(0xffffffffu, h1 == m1 && h0 == m0 ? lo : 0u);
+    hi = (static_cast<unsigned long long>(m1) << 32) | m0;
+    return;
+  }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     if (off >= width) continue;
