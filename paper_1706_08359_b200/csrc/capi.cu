@@ -819,7 +819,7 @@ void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_h
   const char* pe = std::getenv("HBG_GROW_PROFILE");
   std::vector<unsigned long long> prof;
   if (pe != nullptr) {  // phase stamps of CTA 0, printed to stderr (development aid)
-    prof.assign(static_cast<size_t>(4 * max_nodes + 8) * 16, 0ull);
+    prof.assign(static_cast<size_t>(4 * max_nodes + 8) * 20, 0ull);
     a.prof = static_cast<unsigned long long*>(ds->grow_prof.get(prof.size() * 8));
     HBG_CUDA(cudaMemsetAsync(a.prof, 0, prof.size() * 8, s));
   }
@@ -849,7 +849,7 @@ void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_h
     double tw[2][8] = {{0, 0, 0, 0, 0, 0, 0, 0}, {0, 0, 0, 0, 0, 0, 0, 0}};
     int nw[2] = {0, 0}, members[2] = {0, 0};
     for (int i = 0; i < counts[3]; ++i) {
-      const unsigned long long* t = prof.data() + static_cast<size_t>(i) * 16;
+      const unsigned long long* t = prof.data() + static_cast<size_t>(i) * 20;
       const int c = t[7] ? 1 : 0;
       ++nw[c];
       members[c] += static_cast<int>(t[10]);
@@ -874,12 +874,14 @@ void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_h
       std::fprintf(stderr, "\n");
     }
     std::fprintf(stderr, "wave grower: %d splits committed, %d expansions\n", counts[0], members[0] + members[1]);
-    double cand = 0, commits = 0, nav = 0, nfr = 0, rep = 0;
+    double cand = 0, commits = 0, nav = 0, nfr = 0, rep = 0, imb = 0, lat = 0;
     for (int i = 0; i < counts[3]; ++i) {
-      const unsigned long long* t = prof.data() + static_cast<size_t>(i) * 16;
+      const unsigned long long* t = prof.data() + static_cast<size_t>(i) * 20;
       commits += static_cast<double>(t[12]);
       cand += t[13] / 1965.0;  // SM cycles at 1965 MHz
       rep += t[11] / 1965.0;
+      if (t[16] > t[3]) imb += (t[16] - t[3]) * 1e-3;  // last CTA's arrival after CTA 0's
+      if (t[4] > t[16]) lat += (t[4] - t[16]) * 1e-3;  // release after the last arrival
       nav += static_cast<double>(t[14]);
       nfr += static_cast<double>(t[15]);
     }
@@ -887,6 +889,9 @@ void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_h
       std::fprintf(stderr, "wave grower: per wave %.2f commits replayed in %.2f us (clock64), choice %.2f us, "
                    "%.0f expandable, %.0f open leaves\n", commits / counts[3], rep / counts[3], cand / counts[3],
                    nav / counts[3], nfr / counts[3]);
+    if (counts[3] > 0)
+      std::fprintf(stderr, "wave grower: barrier phase = %.2f us waiting for the last CTA + %.2f us release\n",
+                   imb / counts[3], lat / counts[3]);
   } else if (a.prof != nullptr) {
     HBG_CUDA(cudaMemcpy(prof.data(), a.prof, prof.size() * 8, cudaMemcpyDeviceToHost));
     // stamps: 0 start, 1 partitioned, 2 small-child histogram, 3 finish+scans, 4 barrier, 5 picked;
@@ -897,18 +902,18 @@ void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_h
       double acc[7] = {0, 0, 0, 0, 0, 0, 0};
       int n[7] = {0, 0, 0, 0, 0, 0, 0}, splits = 0;
       for (int i = 0; i < counts[0]; ++i) {
-        const unsigned long long* t = prof.data() + static_cast<size_t>(i) * 16;
+        const unsigned long long* t = prof.data() + static_cast<size_t>(i) * 20;
         if (static_cast<int>(t[7]) != cls) continue;
         ++splits;
         for (int j = 0; j < 5; ++j)
           if (t[j] && t[j + 1]) acc[j] += (t[j + 1] - t[j]) * 1e-3, ++n[j];
-        if (i + 1 < counts[0] && t[5] && t[16]) acc[5] += (t[16] - t[5]) * 1e-3, ++n[5];
+        if (i + 1 < counts[0] && t[5] && t[20]) acc[5] += (t[20] - t[5]) * 1e-3, ++n[5];
         if (t[4] && t[8]) acc[6] += (t[8] - t[4]) * 1e-3, ++n[6];
       }
       if (splits == 0) continue;
       if (cls == 6)  // the shared-memory histogram splits one by one
         for (int i = 0; i < counts[0]; ++i) {
-          const unsigned long long* t = prof.data() + static_cast<size_t>(i) * 16;
+          const unsigned long long* t = prof.data() + static_cast<size_t>(i) * 20;
           if (static_cast<int>(t[7]) != cls) continue;
           std::fprintf(stderr, "   split %3d parent %9llu small %9llu: partition %7.1f hist %7.1f finish %7.1f us\n", i,
                        t[10], t[11], (t[1] - t[0]) * 1e-3, (t[2] - t[1]) * 1e-3, (t[3] - t[2]) * 1e-3);

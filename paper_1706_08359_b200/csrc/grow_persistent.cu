@@ -157,7 +157,7 @@ struct GrowArgs {
   int64_t small_max;      // parents up to this many rows join waves (kItems * NT)
 };
 
-constexpr int kProfSlots = 16;
+constexpr int kProfSlots = 20;
 
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
@@ -2334,6 +2334,10 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_wave_kernel(GrowArg
       wave_large_hist<BITS, K, NT>(a, w, Dm, smem, eg, eh);
     }
     stamp(a, w.nwaves, 3);
+    if (a.prof != nullptr) {  // slot 16: the last CTA's arrival at the wave's final barrier
+      __syncthreads();
+      if (threadIdx.x == 0) atomicMax(a.prof + static_cast<size_t>(w.nwaves) * kProfSlots + 16, global_ns());
+    }
     grid_sync(a);
     stamp(a, w.nwaves, 4);
     if (threadIdx.x < 32) wave_integrate(a, w);
