@@ -89,7 +89,11 @@ int hbg_dataset_packed_words(const hbg_dataset* ds, uint32_t* host_words);
  * Host drop-in for build_histograms_partitioned: indices/gradients/hessians
  * are the LeafState arrays (leaf-aligned doubles, leaf.hpp:13-21); `out`
  * receives num_features * max_bin bins, feature-major (HistogramSet order).
- * Synchronous. count == 0 gives an all-zero histogram. */
+ * Synchronous. count == 0 gives an all-zero histogram. Pinned host arrays
+ * (cudaHostAlloc/cudaHostRegister) are copied directly (fp64 over PCIe);
+ * pageable ones are converted to fp32 by a library thread pool into a pinned
+ * stage chunk by chunk while finished chunks are copied — the same floats,
+ * bit-identical results either way. */
 int hbg_build_histograms(hbg_dataset* ds, const int32_t* indices, int64_t count,
                          const double* gradients, const double* hessians, hbg_bin* out);
 
@@ -161,15 +165,21 @@ typedef struct hbg_tree_node {
 /* d_grad/d_hess: fp32 per-row gradients/hessians (device, num_rows each).
  * split_log: host, num_leaves-1 entries (SplitInfo order of execution);
  * nodes: host, 2*num_leaves-1 entries. Synchronous on `stream`.
- * Not re-entrant per handle. */
+ * Not re-entrant per handle. The whole tree runs in one persistent kernel:
+ * one split per grid barrier, or (8-bit data, <= 4096 feature x bin cells,
+ * <= 256 leaves) several speculative expansions per barrier with the
+ * reference's pick order replayed — bit-identical trees. Environment:
+ * HBG_GROW=legacy | wave | host forces the one-split kernel, the wave kernel
+ * (where it fits) or the per-split host loop. */
 int hbg_grow_tree(hbg_dataset* ds, const float* d_grad, const float* d_hess,
                   const hbg_grow_params* params, hbg_split* split_log, int32_t* num_splits,
                   hbg_tree_node* nodes, int32_t* num_nodes, void* stream);
 
 /* Host-pointer drop-in for grow_tree (tree.cpp:186-261): fp64 per-row
  * gradients/hessians in host memory (the reference's std::span<const double>
- * arguments), uploaded and cast to fp32 on the device (the bits32 per-element
- * cast, histogram.cpp:97-98), then grown as hbg_grow_tree. split_log: host,
+ * arguments), cast to fp32 (the bits32 per-element cast, histogram.cpp:97-98;
+ * on the device for pinned arrays, by the staging pool for pageable ones),
+ * then grown as hbg_grow_tree. split_log: host,
  * num_leaves-1 entries; nodes: host, 2*num_leaves-1 entries. Synchronous. */
 int hbg_grow_tree_host(hbg_dataset* ds, const double* gradients, const double* hessians,
                        const hbg_grow_params* params, hbg_split* split_log, int32_t* num_splits,
