@@ -1651,6 +1651,7 @@ struct WaveSmem {
   short fnode[kWL], fout[kWL];
   short wave[kWMax];             // members: small ones first
   unsigned char later[kWL];      // commit i: bit c = child c was split later
+  short cnode[kWL], ckid[kWL], cout[kWL];  // commit i: node, left child node, output id
   unsigned fresh[32];            // the last wave's new expandable entries, sorted (wave_integrate)
   int nav, nfr, committed, next, expanded, done, W, nsmall, nwc, wc, nwaves, hitems, ditems, err, nfresh;
 };
@@ -1666,31 +1667,14 @@ __device__ __forceinline__ int av_node(unsigned v) { return 2047 - static_cast<i
 __device__ __forceinline__ int av_class(unsigned v) { return static_cast<int>(v & 3u); }
 __device__ __forceinline__ int av_bucket(unsigned v) { return static_cast<int>(v >> 13); }
 
-// Per-CTA state in global memory (written by the CTA's warp 0, read back by
-// the same CTA): the commit log [L][4] = node, left child node, output id,
-// bit c: child c was split later; the parent of each child pair; each node's
-// output id; whether a node was committed as a split.
-__host__ __device__ inline size_t wave_state_bytes(int num_leaves, int max_nodes) {
-  const size_t b = 16 * static_cast<size_t>(num_leaves) + 2 * static_cast<size_t>(max_nodes / 2 + 1) +
-                   2 * static_cast<size_t>(max_nodes) + static_cast<size_t>(max_nodes);
-  return (b + 255) / 256 * 256;
+// Per-CTA state in global memory (written by the CTA's warp 0 when it forms
+// a wave, read back by the same CTA at the end): the parent of each child pair.
+__host__ __device__ inline size_t wave_state_bytes(int /*num_leaves*/, int max_nodes) {
+  return (2 * static_cast<size_t>(max_nodes / 2 + 1) + 255) / 256 * 256;
 }
 
-struct WaveLog {
-  int* clog;
-  short* ppar;
-  short* nout;
-  unsigned char* splitf;
-};
-
-__device__ __forceinline__ WaveLog wave_log(const GrowArgs& a) {
-  unsigned char* p = a.wstate + static_cast<size_t>(blockIdx.x) * a.wstate_stride;
-  WaveLog l;
-  l.clog = reinterpret_cast<int*>(p);
-  l.ppar = reinterpret_cast<short*>(l.clog + 4 * static_cast<size_t>(a.num_leaves));
-  l.nout = l.ppar + (a.max_nodes / 2 + 1);
-  l.splitf = reinterpret_cast<unsigned char*>(l.nout + a.max_nodes);
-  return l;
+__device__ __forceinline__ short* wave_ppar(const GrowArgs& a) {
+  return reinterpret_cast<short*>(a.wstate + static_cast<size_t>(blockIdx.x) * a.wstate_stride);
 }
 
 // Would the split of a node with these sizes run the shared-memory histogram
@@ -1806,8 +1790,6 @@ __device__ void wave_select(const GrowArgs& a, WaveSmem& w) {
   __syncthreads();  // warp 0's integrate is complete for warp 1's merge
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
-    const WaveLog lg = wave_log(a);
-    int* clog = lg.clog;
     int nfr = w.nfr, committed = w.committed;
     const int err = w.err;  // read with the integrate loads
     int best = -1;
@@ -1841,14 +1823,11 @@ __device__ void wave_select(const GrowArgs& a, WaveSmem& w) {
       // commit: the reference splits x now (tree.cpp:220-256)
       if (lane == 0) {
         const int o = w.fout[e];
-        clog[4 * committed] = x;
-        clog[4 * committed + 1] = kd;
-        clog[4 * committed + 2] = o;
+        w.cnode[committed] = static_cast<short>(x);
+        w.ckid[committed] = static_cast<short>(kd);
+        w.cout[committed] = static_cast<short>(o);
         w.later[committed] = 0;
         if (o > 0) w.later[(o - 1) >> 1] |= static_cast<unsigned char>(1 << ((o - 1) & 1));
-        lg.splitf[x] = 1;
-        lg.nout[kd] = static_cast<short>(2 * committed + 1);
-        lg.nout[kd + 1] = static_cast<short>(2 * committed + 2);
         const int t = nfr - 1;  // the last entry fills the hole
         w.fkey[e] = w.fkey[t];
         w.fnode[e] = w.fnode[t];
@@ -1887,7 +1866,7 @@ __device__ void wave_select(const GrowArgs& a, WaveSmem& w) {
   __syncthreads();
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
-    const WaveLog lg = wave_log(a);
+    short* ppar = wave_ppar(a);
     const int best = s_best, committed = s_committed;
     int W = 0, nsmall = 0;
     if (best >= 0) {
@@ -1938,8 +1917,7 @@ __device__ void wave_select(const GrowArgs& a, WaveSmem& w) {
       if (lane < W) {
         w.wave[pos] = mem;
         w.kid[mem] = static_cast<short>(w.next + 2 * pos);
-        lg.ppar[(w.next + 2 * pos - 1) >> 1] = mem;
-        lg.splitf[w.next + 2 * pos] = lg.splitf[w.next + 2 * pos + 1] = 0;
+        ppar[(w.next + 2 * pos - 1) >> 1] = mem;
       }
       __syncwarp();
       if (lane == 0) w.nav = nav2;
@@ -2238,12 +2216,17 @@ __device__ void wave_large_hist(const GrowArgs& a, const WaveSmem& w, Desc* Dm, 
 // speculative tree partition the rows; an unexpanded node's range in its
 // buffer is never written after its creation) with the value of the final
 // leaf that contains it.
-__device__ void wave_emit(const GrowArgs& a, const WaveSmem& w) {
-  const WaveLog lg = wave_log(a);
+__device__ void wave_emit(const GrowArgs& a, const WaveSmem& w, unsigned char* smem) {
+  const short* ppar = wave_ppar(a);
   const int committed = w.committed;
   const int stride = gridDim.x * blockDim.x;
+  unsigned char* split = smem;  // node committed as a split (from the log)
+  for (int u = threadIdx.x; u < w.next; u += blockDim.x) split[u] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < committed; i += blockDim.x) split[w.cnode[i]] = 1;
+  __syncthreads();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < committed; i += stride) {
-    const int x = lg.clog[4 * i], kd = lg.clog[4 * i + 1], o = lg.clog[4 * i + 2], later = w.later[i];
+    const int x = w.cnode[i], kd = w.ckid[i], o = w.cout[i], later = w.later[i];
     const hbg_split bs = load_split(&a.nodes[x].best);
     a.split_log[i] = bs;
     a.tree[o] = hbg_tree_node{bs.feature, bs.threshold_bin, 2 * i + 1, 2 * i + 2, 0.0};
@@ -2257,7 +2240,7 @@ __device__ void wave_emit(const GrowArgs& a, const WaveSmem& w) {
     LeafRange r{0, 0, 0.0, 0, 0};
     if (w.kid[u] < 0) {
       int z = u;  // the final leaf above u: the first node whose parent was committed as a split
-      while (z != 0 && !lg.splitf[lg.ppar[(z - 1) >> 1]]) z = lg.ppar[(z - 1) >> 1];
+      while (z != 0 && !split[ppar[(z - 1) >> 1]]) z = ppar[(z - 1) >> 1];
       const NodeDev* q = a.nodes + u;
       const NodeDev* f = a.nodes + z;
       r = LeafRange{__ldcg(&q->begin), __ldcg(&q->count), leaf_value(__ldcg(&f->grad), __ldcg(&f->hess), a.lambda),
@@ -2290,9 +2273,6 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_wave_kernel(GrowArg
       for (int q = 0; q < kRep; ++q) a.node_gain[static_cast<size_t>(q) * a.max_nodes] = hb ? bs.gain : -1.0;
       a.tree[0] = hbg_tree_node{-1, -1, -1, -1, leaf_value(G, H, a.lambda)};
     }
-    const WaveLog lg = wave_log(a);
-    lg.nout[0] = 0;
-    lg.splitf[0] = 0;
     const unsigned long long k0 = hb ? gain_key(bs.gain) : 0ull;
     w.gkey[0] = k0;
     w.prio[0] = hb ? static_cast<float>(bs.gain) : 0.f;
@@ -2346,7 +2326,7 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_wave_kernel(GrowArg
     wave_select<NT>(a, w);
     stamp(a, w.nwaves - 1, 5);
   }
-  wave_emit(a, w);
+  wave_emit(a, w, smem);
   if (blockIdx.x == 0 && threadIdx.x == 0) a.counts[3] = w.nwaves;
 }
 
