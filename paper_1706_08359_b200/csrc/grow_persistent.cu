@@ -447,8 +447,17 @@ struct Kid {
 // in every CTA: same data, same order). kid_l/kid_l+1: the newest nodes,
 // whose state comes from the CTA's own `kid` copies (CTA 0's global writes
 // of them are not yet visible). CTA 0 records the split.
+// The open leaves with a split, kept by every CTA in shared memory (trees of
+// up to kPickPool leaves): the pick is an argmax over them, no L2 round trip.
+constexpr int kPickPool = 256;
+struct PickPool {
+  unsigned long long key[kPickPool];  // gain key
+  short node[kPickPool];
+  int n;
+};
+
 template <int NT>
-__device__ void pick(const GrowArgs& a, int i, int kid_l, const Kid* kid, Desc& D) {
+__device__ void pick(const GrowArgs& a, int i, int kid_l, const Kid* kid, Desc& D, PickPool* pool) {
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     const int nnodes = 1 + 2 * i;
@@ -457,7 +466,46 @@ __device__ void pick(const GrowArgs& a, int i, int kid_l, const Kid* kid, Desc& 
     err = __shfl_sync(0xffffffffu, err, 0);
     unsigned long long hk = 0ull;
     unsigned lk = 0u;
-    if (i < a.num_leaves - 1 && err == kErrNone) {
+    if (pool != nullptr) {
+      // the newest nodes join the pool (the root at i == 0); the best leaves it
+      if (lane == 0) {
+        if (i == 0) pool->n = 0;
+        for (int c = 0; c < (i == 0 ? 1 : 2); ++c) {
+          const Kid& q = kid[c];
+          const unsigned long long k = q.has_best ? gain_key(q.best.gain) : 0ull;
+          if (k == 0ull) continue;
+          pool->key[pool->n] = k;
+          pool->node[pool->n] = static_cast<short>(kid_l + c);
+          ++pool->n;
+        }
+      }
+      __syncwarp();
+      const int n = pool->n;
+      int idx = -1;
+      if (i < a.num_leaves - 1 && err == kErrNone) {
+#pragma unroll
+        for (int u = 0; u < kPickPool / 32; ++u) {
+          const int e = u * 32 + lane;
+          const unsigned long long h = e < n ? pool->key[e] : 0ull;
+          const unsigned l = e < n ? 0xFFFFFFFFu - static_cast<unsigned>(pool->node[e]) : 0u;  // lowest id on ties
+          const bool take = h > hk || (h == hk && l > lk);
+          hk = take ? h : hk;
+          lk = take ? l : lk;
+          idx = take ? e : idx;
+        }
+      }
+      const unsigned long long h0 = hk;
+      const unsigned l0 = lk;
+      warp_argmax_key(hk, lk);
+      const unsigned bal = __ballot_sync(0xffffffffu, hk != 0ull && h0 == hk && l0 == lk);
+      const int e = bal ? __shfl_sync(0xffffffffu, idx, __ffs(bal) - 1) : -1;
+      if (lane == 0 && e >= 0) {  // remove it: the last entry fills the hole
+        pool->key[e] = pool->key[n - 1];
+        pool->node[e] = pool->node[n - 1];
+        pool->n = n - 1;
+      }
+      __syncwarp();
+    } else if (i < a.num_leaves - 1 && err == kErrNone) {
       constexpr int kU = 16;  // 16 x 32 lanes >= 509 nodes: one round of loads
       for (int n0 = 0; n0 < nnodes; n0 += kU * 32) {
         double gain[kU];
@@ -1402,6 +1450,11 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
   __shared__ PartShared<NT> ps;
   __shared__ Desc D;
   __shared__ Kid kid[2];
+  // the pick's shared-memory pool (not at 256 bins: its 3 KB would cost the
+  // histogram one of its three 64 KB warps)
+  __shared__ __align__(8) unsigned char pool_raw[K >= 256 ? 8 : sizeof(PickPool)];
+  PickPool* pool = nullptr;
+  if constexpr (K < 256) pool = a.num_leaves <= kPickPool ? reinterpret_cast<PickPool*>(pool_raw) : nullptr;
   if (a.nranks == 1) {
     // root: histogram, totals and best split were computed by the
     // host-launched kernels; every CTA builds the root record
@@ -1473,7 +1526,7 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
     for (int q = 0; q < kRep; ++q) a.node_gain[q * a.max_nodes] = r.has_best ? r.best.gain : -1.0;
   }
   __syncthreads();
-  pick<NT>(a, 0, 0, kid, D);  // node 0 is "kid_l" (kid[1] is never consulted: nnodes = 1)
+  pick<NT>(a, 0, 0, kid, D, pool);  // node 0 is "kid_l" (kid[1] is never consulted: nnodes = 1)
   const double eg = ldexp(1.0, a.exps[0]), eh = ldexp(1.0, a.exps[1]);  // fixed-point scales
   while (!D.done) {
     const int it = D.iter;
@@ -1581,7 +1634,7 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
     stamp(a, it, 8);
     store_children(a, D, kid);
     stamp(a, it, 6);
-    pick<NT>(a, it + 1, D.left_id, kid, D);
+    pick<NT>(a, it + 1, D.left_id, kid, D, pool);
     stamp(a, it, 5);
   }
   if (a.nranks > 1 && blockIdx.x == 0 && threadIdx.x == 0) {
