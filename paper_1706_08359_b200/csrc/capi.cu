@@ -94,7 +94,7 @@ struct hbg_dataset {
   hbg::DevBuf colbins;  // column-major uint8 bins [feature][row] (the a1 layout), for partitions
   hbg::DevBuf host_parts;                 // host drop-in: per-chunk histograms
   cudaStream_t copy_stream = nullptr;     // host drop-in: H2D copies overlapped with the kernels
-  cudaEvent_t chunk_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t chunk_ev[17] = {};  // per histogram chunk (<= 16) + [16]: the copy stream's start
   hbg::DevBuf part, iota, host_idx, host_gd, host_hd, host_gf, host_hf, host_hist, host_bins;
   int64_t iota_rows = 0;
   // tree growth workspace
@@ -338,6 +338,14 @@ void stage_chunks(hbg_dataset* ds, const double* g, const double* h, const int32
 }
 
 constexpr int64_t kStageRows = int64_t(1) << 19;  // rows per staged chunk (4 MB of fp32 g/h)
+
+// Histogram chunks of a host drop-in call: only the last chunk's conversion
+// and histogram are exposed after the PCIe copies.
+int host_chunks(int64_t count) {
+  const char* e = std::getenv("HBG_HOST_CHUNKS");
+  if (e != nullptr) return std::max(1, std::min(16, std::atoi(e)));
+  return count >= (int64_t{1} << 21) ? 4 : 1;
+}
 
 // Device row ids [first, first + n) of the dataset: the resident iota array.
 const int32_t* identity_rows(hbg_dataset* ds, int64_t first, cudaStream_t s) {
@@ -1094,12 +1102,12 @@ int hbg_build_histograms(hbg_dataset* ds, const int32_t* indices, int64_t count,
       const size_t n = static_cast<size_t>(count);
       float* d_gf = static_cast<float*>(ds->host_gf.get(n * 4));
       float* d_hf = static_cast<float*>(ds->host_hf.get(n * 4));
-      const int C = count >= (int64_t{1} << 21) ? 4 : 1;  // as the pinned path: the same sums
+      const int C = host_chunks(count);  // as the pinned path: the same sums
       if (!ds->copy_stream) HBG_CUDA(cudaStreamCreateWithFlags(&ds->copy_stream, cudaStreamNonBlocking));
-      for (int c = 0; c < 5; ++c)
+      for (int c = 0; c < 17; ++c)
         if (!ds->chunk_ev[c]) HBG_CUDA(cudaEventCreateWithFlags(&ds->chunk_ev[c], cudaEventDisableTiming));
-      HBG_CUDA(cudaEventRecord(ds->chunk_ev[4], s));
-      HBG_CUDA(cudaStreamWaitEvent(ds->copy_stream, ds->chunk_ev[4], 0));
+      HBG_CUDA(cudaEventRecord(ds->chunk_ev[16], s));
+      HBG_CUDA(cudaStreamWaitEvent(ds->copy_stream, ds->chunk_ev[16], 0));
       // the row ids ride along with g/h (a contiguity check would be one more
       // serial pass over the ids; their 4 B/row fit under the conversion)
       int32_t* di = static_cast<int32_t*>(ds->host_idx.get(n * 4));
@@ -1134,12 +1142,12 @@ int hbg_build_histograms(hbg_dataset* ds, const int32_t* indices, int64_t count,
       // chunk c's conversion and histogram run on the compute stream as soon
       // as its bytes have landed, so only the last chunk's work is exposed.
       // The chunk histograms are summed in chunk order (deterministic).
-      const int C = count >= (int64_t{1} << 21) ? 4 : 1;
+      const int C = host_chunks(count);
       if (!ds->copy_stream) HBG_CUDA(cudaStreamCreateWithFlags(&ds->copy_stream, cudaStreamNonBlocking));
-      for (int c = 0; c < 5; ++c)
+      for (int c = 0; c < 17; ++c)
         if (!ds->chunk_ev[c]) HBG_CUDA(cudaEventCreateWithFlags(&ds->chunk_ev[c], cudaEventDisableTiming));
-      HBG_CUDA(cudaEventRecord(ds->chunk_ev[4], s));  // the copy stream starts after prior work on s
-      HBG_CUDA(cudaStreamWaitEvent(ds->copy_stream, ds->chunk_ev[4], 0));
+      HBG_CUDA(cudaEventRecord(ds->chunk_ev[16], s));  // the copy stream starts after prior work on s
+      HBG_CUDA(cudaStreamWaitEvent(ds->copy_stream, ds->chunk_ev[16], 0));
       auto chunk = [&](int c, int64_t& b, int64_t& e) {
         b = count * c / C;
         e = count * (c + 1) / C;
@@ -1164,8 +1172,8 @@ int hbg_build_histograms(hbg_dataset* ds, const int32_t* indices, int64_t count,
       } else {
         int32_t* di = static_cast<int32_t*>(ds->host_idx.get(n * 4));
         HBG_CUDA(cudaMemcpyAsync(di, indices, n * 4, cudaMemcpyHostToDevice, ds->copy_stream));
-        HBG_CUDA(cudaEventRecord(ds->chunk_ev[4], ds->copy_stream));
-        HBG_CUDA(cudaStreamWaitEvent(s, ds->chunk_ev[4], 0));
+        HBG_CUDA(cudaEventRecord(ds->chunk_ev[16], ds->copy_stream));
+        HBG_CUDA(cudaStreamWaitEvent(s, ds->chunk_ev[16], 0));
         d_idx = di;
       }
       double* parts = C > 1 ? static_cast<double*>(ds->host_parts.get(static_cast<size_t>(C) * 3 * D * sizeof(double) + 8))
