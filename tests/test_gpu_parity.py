@@ -518,7 +518,8 @@ def test_grow_tree_matches_oracle(hbg, oracle, rows, d, k, leaves, min_data, lam
 @pytest.mark.parametrize("rows,d,k,leaves,min_data,lam", [
     (300000, 28, 64, 255, 1, 0.0), (200000, 28, 16, 255, 20, 0.0), (100000, 70, 200, 127, 5, 1.0),
     (3000, 3, 64, 255, 1, 0.0), (20000, 1300, 256, 31, 100, 0.0), (60000, 10, 64, 511, 1, 0.0),
-    (1000000, 28, 64, 255, 100, 0.0)])
+    (1000000, 28, 64, 255, 100, 0.0), (20000, 1, 2, 31, 1, 0.0), (5000, 2, 3, 63, 1, 0.5),
+    (200000, 28, 16, 255, 1, 0.0)])
 def test_wave_grower_bitwise_equals_one_split_grower(hbg, oracle, rows, d, k, leaves, min_data, lam, monkeypatch):
     """The wave grower (HBG_GROW=wave) expands several leaves per grid barrier and
     replays the reference's pick order; the one-split-at-a-time kernel
