@@ -34,6 +34,16 @@ extern "C" {
 #define HBG_GH_LEAF_ALIGNED 0 /* g[i] belongs to leaf position i (LeafState::gradients, leaf.hpp:15-16) */
 #define HBG_GH_ROW_INDEXED 1  /* g[indices[i]] — gather fused into the histogram kernel */
 
+/* Accumulation precision: the values of histoboost::PrecisionMode
+ * (histogram_set.hpp:11, enum class PrecisionMode { bits32, bits64 }).
+ * BITS32: g/h cast to fp32 per element (histogram.cpp:97-98), fp32 per-warp
+ *         sums reduced in fp64 — the fast path (stats_tolerance 1e-4).
+ * BITS64: fp64 g/h in HBM, fp64 shared-memory cells and fp64 partials
+ *         (reference_impl<double>, histogram.cpp:131-145) — meets the
+ *         reference's stats_tolerance(bits64) = 1e-12. */
+#define HBG_PRECISION_BITS32 0
+#define HBG_PRECISION_BITS64 1
+
 /* One histogram bin; identical layout to histoboost::HistogramBin (histogram_set.hpp:17-21). */
 typedef struct hbg_bin {
   double grad_sum;
@@ -96,6 +106,13 @@ int hbg_dataset_packed_words(const hbg_dataset* ds, uint32_t* host_words);
  * bit-identical results either way. */
 int hbg_build_histograms(hbg_dataset* ds, const int32_t* indices, int64_t count,
                          const double* gradients, const double* hessians, hbg_bin* out);
+/* The same call with the reference's PrecisionMode argument
+ * (build_histograms_partitioned(data, leaf, precision), histogram.hpp:133):
+ * HBG_PRECISION_BITS32 is hbg_build_histograms; HBG_PRECISION_BITS64 uploads
+ * the fp64 LeafState arrays as they are (16 B/row) and accumulates in fp64. */
+int hbg_build_histograms_ex(hbg_dataset* ds, const int32_t* indices, int64_t count,
+                            const double* gradients, const double* hessians, int32_t precision,
+                            hbg_bin* out);
 
 /* Device builder (the performance path). d_indices may be NULL for the
  * identity leaf [0, count) (the root). d_grad/d_hess are fp32, addressed per
@@ -105,6 +122,12 @@ int hbg_build_histograms(hbg_dataset* ds, const int32_t* indices, int64_t count,
 int hbg_build_histograms_device(hbg_dataset* ds, const int32_t* d_indices, int64_t count,
                                 const float* d_grad, const float* d_hess, int32_t gh_mode,
                                 double* d_hist, void* stream);
+
+/* bits64 device builder: d_grad/d_hess are fp64 (addressed per gh_mode),
+ * accumulated in fp64 shared-memory cells and reduced in fp64. */
+int hbg_build_histograms_device_f64(hbg_dataset* ds, const int32_t* d_indices, int64_t count,
+                                    const double* d_grad, const double* d_hess, int32_t gh_mode,
+                                    double* d_hist, void* stream);
 
 /* Device SoA histogram -> hbg_bin[num_features * max_bin] (device pointer). */
 int hbg_hist_to_bins_device(const double* d_hist, int32_t num_features, int32_t max_bin,
@@ -120,6 +143,14 @@ int hbg_subtract_device(const double* d_parent, const double* d_child, double* d
 int hbg_gather_leaf_device(const int32_t* d_indices, int64_t count, const float* d_grad,
                            const float* d_hess, float* d_leaf_grad, float* d_leaf_hess,
                            double* d_totals, void* stream);
+
+/* gather_leaf_statistics (tree.cpp:11-25) for host callers: leaf_g[i] =
+ * g[indices[i]], leaf_h[i] = h[indices[i]] (fp64, host arrays of count) and
+ * totals[0..1] = fp64 grad/hess totals in a fixed order, computed on `device`
+ * (g/h: host fp64 arrays of num_rows; every index must be < num_rows). */
+int hbg_gather_leaf_statistics(const int32_t* indices, int64_t count, const double* gradients,
+                               const double* hessians, int64_t num_rows, double* leaf_grad,
+                               double* leaf_hess, double* totals, int32_t device);
 
 /* ---- best-split scan (row a11): find_best_split (tree.cpp:163-182) over a device
  * SoA histogram, fp64, the reference's tie rules (smallest bin, then lowest
@@ -149,7 +180,10 @@ int hbg_find_best_split(const hbg_bin* hists, int32_t num_features, int32_t max_
  * histogram of the SMALLER child only and the larger one by subtraction. */
 typedef struct hbg_grow_params {
   int32_t num_leaves;       /* GrowParams::num_leaves (tree.hpp:81) */
-  int32_t reserved;
+  int32_t precision;        /* GrowParams::precision (tree.hpp:84): HBG_PRECISION_BITS32 grows
+                               with fp32 g/h in the persistent kernel; HBG_PRECISION_BITS64
+                               grows with fp64 g/h and fp64 histograms at every leaf (host-
+                               driven loop; hbg_grow_tree_host / hbg_grow_tree_f64 only) */
   int64_t min_data_in_leaf; /* GrowParams::min_data_in_leaf */
   double lambda;            /* GrowParams::lambda */
 } hbg_grow_params;
@@ -175,11 +209,18 @@ int hbg_grow_tree(hbg_dataset* ds, const float* d_grad, const float* d_hess,
                   const hbg_grow_params* params, hbg_split* split_log, int32_t* num_splits,
                   hbg_tree_node* nodes, int32_t* num_nodes, void* stream);
 
+/* bits64 tree on fp64 device gradients/hessians (params->precision must be
+ * HBG_PRECISION_BITS64). */
+int hbg_grow_tree_f64(hbg_dataset* ds, const double* d_grad, const double* d_hess,
+                      const hbg_grow_params* params, hbg_split* split_log, int32_t* num_splits,
+                      hbg_tree_node* nodes, int32_t* num_nodes, void* stream);
+
 /* Host-pointer drop-in for grow_tree (tree.cpp:186-261): fp64 per-row
  * gradients/hessians in host memory (the reference's std::span<const double>
- * arguments), cast to fp32 (the bits32 per-element cast, histogram.cpp:97-98;
- * on the device for pinned arrays, by the staging pool for pageable ones),
- * then grown as hbg_grow_tree. split_log: host,
+ * arguments). params->precision BITS32: cast to fp32 (the bits32 per-element
+ * cast, histogram.cpp:97-98; on the device for pinned arrays, by the staging
+ * pool for pageable ones), then grown as hbg_grow_tree; BITS64: uploaded as
+ * fp64 and grown as hbg_grow_tree_f64. split_log: host,
  * num_leaves-1 entries; nodes: host, 2*num_leaves-1 entries. Synchronous. */
 int hbg_grow_tree_host(hbg_dataset* ds, const double* gradients, const double* hessians,
                        const hbg_grow_params* params, hbg_split* split_log, int32_t* num_splits,

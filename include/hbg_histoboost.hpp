@@ -13,8 +13,12 @@
 // CUDA failures surface as std::runtime_error — there is no CPU fallback).
 //
 // Requires the reference headers on the include path (histoboost/*.hpp) and
-// linking libhbg.so. Dense features only: the reference runs sparse features
-// on the CPU pair path (sparse.cpp), as the paper does.
+// linking libhbg.so. Sparse features (BinnedDataset::sparse_features,
+// classify_features, binning.cpp:98-109) are served from the dense bins that
+// bin_dataset keeps for every column (binning.cpp:218-224: sparse_storage is
+// added, columns[f].bins stays): the device histogram of such a feature is the
+// same HistogramEntry the pair path (sparse.cpp:9-56) builds, within the
+// reference's own sparse == dense tolerance (test_histogram.cpp:96-116).
 #pragma once
 
 #include <algorithm>
@@ -49,12 +53,14 @@ class DeviceDataset {
  public:
   explicit DeviceDataset(const histoboost::BinnedDataset& data, int device = 0)
       : num_features_(data.num_features()), max_bin_(data.max_bin) {
-    if (!data.sparse_features.empty()) {
-      throw std::invalid_argument("hbg backend: sparse features stay on the CPU pair path");
-    }
+    // every column, dense or sparse, by feature id: the HistogramSet index
     std::vector<const std::uint8_t*> cols(static_cast<std::size_t>(num_features_));
     for (int f = 0; f < num_features_; ++f) {
-      cols[static_cast<std::size_t>(f)] = data.columns[static_cast<std::size_t>(f)].bins.data();
+      const auto& bins = data.columns[static_cast<std::size_t>(f)].bins;
+      if (static_cast<std::int64_t>(bins.size()) != data.num_rows) {
+        throw std::invalid_argument("hbg backend: column " + std::to_string(f) + " has no dense bins");
+      }
+      cols[static_cast<std::size_t>(f)] = bins.data();
     }
     hbg_dataset* h = nullptr;
     check(hbg_dataset_create(cols.data(), num_features_, data.num_rows, max_bin_, device, &h));
@@ -73,17 +79,24 @@ class DeviceDataset {
   int max_bin_;
 };
 
-// The drop-in for build_histograms_partitioned. `precision` is accepted for
-// signature parity: the device accumulates fp32 partials reduced in fp64,
-// which meets stats_tolerance(bits32) = 1e-4 and, on the BASELINE shapes,
-// 1e-5 against bits64.
+inline std::int32_t to_hbg(histoboost::PrecisionMode p) {
+  return p == histoboost::PrecisionMode::bits64 ? HBG_PRECISION_BITS64 : HBG_PRECISION_BITS32;
+}
+
+// The drop-in for build_histograms_partitioned, honouring PrecisionMode:
+//  bits32 — fp32 inputs (the reference's per-element cast), fp32 per-warp
+//           sums reduced in fp64: within stats_tolerance(bits32) = 1e-4 of the
+//           reference (tests: <= 1e-5 vs bits64 up to 300K-row leaves, <= 1e-4
+//           at the 10.5M-row root);
+//  bits64 — fp64 inputs, fp64 accumulation: within stats_tolerance(bits64) =
+//           1e-12 of the reference's bits64 (tests up to the 10.5M-row root).
 inline histoboost::HistogramSet build_histograms_cuda(const DeviceDataset& dev,
                                                       const histoboost::LeafState& leaf,
                                                       histoboost::PrecisionMode precision) {
   const int d = dev.num_features(), k = dev.max_bin();
   std::vector<hbg_bin> bins(static_cast<std::size_t>(d) * static_cast<std::size_t>(k));
-  check(hbg_build_histograms(dev.get(), leaf.indices.data(), leaf.count(), leaf.gradients.data(),
-                             leaf.hessians.data(), bins.data()));
+  check(hbg_build_histograms_ex(dev.get(), leaf.indices.data(), leaf.count(), leaf.gradients.data(),
+                                leaf.hessians.data(), to_hbg(precision), bins.data()));
   histoboost::HistogramSet out(static_cast<std::size_t>(d));
   for (int f = 0; f < d; ++f) {
     auto& e = out[static_cast<std::size_t>(f)];
@@ -102,8 +115,9 @@ inline histoboost::HistogramSet build_histograms_cuda(const DeviceDataset& dev,
 // log), same Tree (node numbering, values from the children's fp64 totals,
 // threshold_value from data.boundaries as find_best_split does,
 // tree.cpp:174-180). The histogram, subtraction, split scans and partitions
-// run on the device; `params.backend`/`precision` are accepted for signature
-// parity (the device builds fp32 histograms reduced in fp64).
+// run on the device with params.precision honoured (bits32: fp32 g/h in the
+// persistent one-kernel grower; bits64: fp64 g/h and fp64 histograms at
+// every leaf); `params.backend` selects nothing here (this IS the backend).
 inline histoboost::Tree grow_tree_cuda(const DeviceDataset& dev, const histoboost::BinnedDataset& data,
                                        std::span<const double> gradients, std::span<const double> hessians,
                                        const histoboost::GrowParams& params,
@@ -113,7 +127,7 @@ inline histoboost::Tree grow_tree_cuda(const DeviceDataset& dev, const histoboos
       hessians.size() != static_cast<std::size_t>(data.num_rows)) {
     throw std::invalid_argument("gradient/hessian length differs from the row count");
   }
-  const hbg_grow_params p{params.num_leaves, 0, params.min_data_in_leaf, params.lambda};
+  const hbg_grow_params p{params.num_leaves, to_hbg(params.precision), params.min_data_in_leaf, params.lambda};
   std::vector<hbg_split> log(static_cast<std::size_t>(std::max(1, params.num_leaves - 1)));
   std::vector<hbg_tree_node> nodes(static_cast<std::size_t>(std::max(1, 2 * params.num_leaves - 1)));
   std::int32_t ns = 0, nn = 0;

@@ -39,6 +39,19 @@ HBG_GH_LEAF_ALIGNED = 0
 HBG_GH_ROW_INDEXED = 1
 HBG_LOSS_SQUARED = 0
 HBG_LOSS_LOGISTIC = 1
+#: PrecisionMode (histogram_set.hpp:11): bits32 / bits64
+HBG_PRECISION_BITS32 = 0
+HBG_PRECISION_BITS64 = 1
+
+
+def _precision(p) -> int:
+    """32 / 64 / 'bits32' / 'bits64' / HBG_PRECISION_* -> HBG_PRECISION_*."""
+    table = {32: HBG_PRECISION_BITS32, 64: HBG_PRECISION_BITS64, "bits32": HBG_PRECISION_BITS32,
+             "bits64": HBG_PRECISION_BITS64, HBG_PRECISION_BITS32: HBG_PRECISION_BITS32,
+             HBG_PRECISION_BITS64: HBG_PRECISION_BITS64}
+    if p not in table:
+        raise InvalidArgument(HBG_ERR_INVALID_ARGUMENT, f"unknown precision {p!r}")
+    return table[p]
 
 #: numpy view of ``hbg_bin`` == ``histoboost::HistogramBin`` (histogram_set.hpp:17-21)
 BIN_DTYPE = np.dtype([("grad_sum", "<f8"), ("hess_sum", "<f8"), ("count", "<i8")])
@@ -66,7 +79,7 @@ NODE_DTYPE = np.dtype([("feature", "<i4"), ("threshold_bin", "<i4"), ("left", "<
 
 
 class hbg_grow_params(C.Structure):
-    _fields_ = [("num_leaves", C.c_int32), ("reserved", C.c_int32), ("min_data_in_leaf", C.c_int64),
+    _fields_ = [("num_leaves", C.c_int32), ("precision", C.c_int32), ("min_data_in_leaf", C.c_int64),
                 ("lambda_", C.c_double)]
 
 
@@ -118,15 +131,19 @@ EXPORTED_SYMBOLS = (
     "hbg_dataset_layout",
     "hbg_dataset_packed_words",
     "hbg_build_histograms",
+    "hbg_build_histograms_ex",
     "hbg_build_histograms_device",
+    "hbg_build_histograms_device_f64",
     "hbg_hist_to_bins_device",
     "hbg_subtract_device",
     "hbg_gather_leaf_device",
+    "hbg_gather_leaf_statistics",
     "hbg_best_split_device",
     "hbg_best_split_device_totals",
     "hbg_find_best_split",
     "hbg_grow_tree",
     "hbg_grow_tree_host",
+    "hbg_grow_tree_f64",
     "hbg_grow_tree_sharded",
     "hbg_dataset_stream",
     "hbg_peer_create",
@@ -176,7 +193,11 @@ def lib() -> C.CDLL:
         L.hbg_dataset_layout.argtypes = [_P, _P]
         L.hbg_dataset_packed_words.argtypes = [_P, _P]
         L.hbg_build_histograms.argtypes = [_P, _P, C.c_int64, _P, _P, _P]
+        L.hbg_build_histograms_ex.argtypes = [_P, _P, C.c_int64, _P, _P, C.c_int32, _P]
         L.hbg_build_histograms_device.argtypes = [_P, _P, C.c_int64, _P, _P, C.c_int32, _P, _P]
+        L.hbg_build_histograms_device_f64.argtypes = [_P, _P, C.c_int64, _P, _P, C.c_int32, _P, _P]
+        L.hbg_gather_leaf_statistics.argtypes = [_P, C.c_int64, _P, _P, C.c_int64, _P, _P, _P, C.c_int32]
+        L.hbg_grow_tree_f64.argtypes = [_P, _P, _P, _P, _P, _P, _P, _P, _P]
         L.hbg_hist_to_bins_device.argtypes = [_P, C.c_int32, C.c_int32, _P, _P]
         L.hbg_subtract_device.argtypes = [_P, _P, _P, C.c_int64, _P]
         L.hbg_gather_leaf_device.argtypes = [_P, C.c_int64, _P, _P, _P, _P, _P, _P]
@@ -249,19 +270,21 @@ class LeafState:
         return int(len(self.indices))
 
 
-def gather_leaf_statistics(indices, gradients, hessians) -> LeafState:
-    """tree.cpp:11-25 (host arrays): leaf-aligned g/h and double totals in index order."""
+def gather_leaf_statistics(indices, gradients, hessians, device: int = 0) -> LeafState:
+    """gather_leaf_statistics (tree.cpp:11-25) on the device: leaf-aligned fp64
+    g/h and fp64 totals (fixed-order sums) from host per-row arrays."""
     idx = np.ascontiguousarray(indices, dtype=np.int32)
-    g = np.asarray(gradients, dtype=np.float64)[idx]
-    h = np.asarray(hessians, dtype=np.float64)[idx]
-    gt = 0.0
-    ht = 0.0
-    # sequential double sums, as the reference loop does
-    for v in g.tolist():
-        gt += v
-    for v in h.tolist():
-        ht += v
-    return LeafState(idx, g, h, gt, ht)
+    g = np.ascontiguousarray(gradients, dtype=np.float64)
+    h = np.ascontiguousarray(hessians, dtype=np.float64)
+    if len(g) != len(h):
+        raise InvalidArgument(HBG_ERR_INVALID_ARGUMENT, "gradients and hessians disagree on length")
+    n = len(idx)
+    lg = np.empty(n, dtype=np.float64)
+    lh = np.empty(n, dtype=np.float64)
+    tot = np.zeros(2, dtype=np.float64)
+    check(lib().hbg_gather_leaf_statistics(_ptr(idx), n, _ptr(g), _ptr(h), len(g), _ptr(lg), _ptr(lh),
+                                           _ptr(tot), device))
+    return LeafState(idx, lg, lh, float(tot[0]), float(tot[1]))
 
 
 class Dataset:
@@ -312,6 +335,12 @@ class Dataset:
         check(lib().hbg_build_histograms_device(self.handle, _ptr(indices), count, _ptr(grad),
                                                 _ptr(hess), gh_mode, _ptr(hist), _ptr(stream)))
 
+    def build_histograms_device_f64(self, indices, count: int, grad, hess, hist,
+                                    gh_mode: int = HBG_GH_LEAF_ALIGNED, stream=None) -> None:
+        """bits64 device builder: fp64 g/h tensors, fp64 accumulation."""
+        check(lib().hbg_build_histograms_device_f64(self.handle, _ptr(indices), count, _ptr(grad),
+                                                    _ptr(hess), gh_mode, _ptr(hist), _ptr(stream)))
+
     def grow_tree(self, grad, hess, num_leaves: int = 31, min_data_in_leaf: int = 1, lam: float = 0.0,
                   stream=None):
         """grow_tree (tree.cpp:186-261) on the device; grad/hess are fp32 device
@@ -326,18 +355,31 @@ class Dataset:
         return log[: ns.value].copy(), nodes[: nn.value].copy()
 
     def grow_tree_host(self, gradients: np.ndarray, hessians: np.ndarray, num_leaves: int = 31,
-                       min_data_in_leaf: int = 1, lam: float = 0.0):
+                       min_data_in_leaf: int = 1, lam: float = 0.0, precision=32):
         """grow_tree (tree.cpp:186-261) from host fp64 per-row gradients/hessians
-        (the reference's span<const double> arguments). Returns (split_log, nodes)."""
+        (the reference's span<const double> arguments), GrowParams::precision
+        = ``precision`` (32 or 64). Returns (split_log, nodes)."""
         g = np.ascontiguousarray(gradients, dtype=np.float64)
         h = np.ascontiguousarray(hessians, dtype=np.float64)
-        p = hbg_grow_params(num_leaves, 0, min_data_in_leaf, lam)
+        p = hbg_grow_params(num_leaves, _precision(precision), min_data_in_leaf, lam)
         log = np.zeros(max(num_leaves - 1, 1), dtype=SPLIT_DTYPE)
         nodes = np.zeros(max(2 * num_leaves - 1, 1), dtype=NODE_DTYPE)
         ns = C.c_int32()
         nn = C.c_int32()
         check(lib().hbg_grow_tree_host(self.handle, g.ctypes.data, h.ctypes.data, C.byref(p), log.ctypes.data,
                                        C.byref(ns), nodes.ctypes.data, C.byref(nn)))
+        return log[: ns.value].copy(), nodes[: nn.value].copy()
+
+    def grow_tree_f64(self, grad, hess, num_leaves: int = 31, min_data_in_leaf: int = 1, lam: float = 0.0,
+                      stream=None):
+        """bits64 grow_tree on fp64 device tensors of num_rows."""
+        p = hbg_grow_params(num_leaves, HBG_PRECISION_BITS64, min_data_in_leaf, lam)
+        log = np.zeros(max(num_leaves - 1, 1), dtype=SPLIT_DTYPE)
+        nodes = np.zeros(max(2 * num_leaves - 1, 1), dtype=NODE_DTYPE)
+        ns = C.c_int32()
+        nn = C.c_int32()
+        check(lib().hbg_grow_tree_f64(self.handle, _ptr(grad), _ptr(hess), C.byref(p), _ptr(log), C.byref(ns),
+                                      _ptr(nodes), C.byref(nn), _ptr(stream)))
         return log[: ns.value].copy(), nodes[: nn.value].copy()
 
     def stream(self) -> int:
@@ -439,12 +481,14 @@ class Dataset:
 
 
 # --------------------------------------------------------------------- operators
-def build_histograms_partitioned(data: Dataset, leaf: LeafState) -> np.ndarray:
-    """Drop-in for ``build_histograms_partitioned`` (histogram.hpp:133-134).
+def build_histograms_partitioned(data: Dataset, leaf: LeafState, precision=32) -> np.ndarray:
+    """Drop-in for ``build_histograms_partitioned(data, leaf, precision)``
+    (histogram.hpp:133-134).
 
     Returns the HistogramSet as a (num_features, max_bin) ``BIN_DTYPE`` array
-    (feature-major, one entry per feature id). Counts are exact; sums are fp32
-    accumulations reduced in fp64 (tolerance documented in DESIGN.md §5).
+    (feature-major, one entry per feature id). Counts are exact. ``precision``
+    32 (bits32): fp32 inputs and per-warp sums reduced in fp64; 64 (bits64):
+    fp64 inputs and fp64 accumulation throughout.
     """
     n = leaf.count()
     idx = np.ascontiguousarray(leaf.indices, dtype=np.int32)
@@ -453,7 +497,8 @@ def build_histograms_partitioned(data: Dataset, leaf: LeafState) -> np.ndarray:
     if len(g) != n or len(h) != n:
         raise InvalidArgument(HBG_ERR_INVALID_ARGUMENT, "leaf arrays disagree on length")
     out = np.zeros((data.num_features, data.max_bin), dtype=BIN_DTYPE)
-    check(lib().hbg_build_histograms(data.handle, _ptr(idx), n, _ptr(g), _ptr(h), _ptr(out)))
+    check(lib().hbg_build_histograms_ex(data.handle, _ptr(idx), n, _ptr(g), _ptr(h), _precision(precision),
+                                        _ptr(out)))
     return out
 
 

@@ -360,9 +360,10 @@ const int32_t* identity_rows(hbg_dataset* ds, int64_t first, cudaStream_t s) {
 
 // Device histogram of one leaf into d_hist; with `parent` also writes
 // sibling = parent - d_hist in the same pass (sibling may alias parent).
-void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const float* d_g,
-                  const float* d_h, int gh_mode, double* d_hist, cudaStream_t s,
-                  const double* parent = nullptr, double* sibling = nullptr) {
+// acc_bytes 4: d_g/d_h are fp32 (bits32); 8: fp64 with fp64 accumulation (bits64).
+void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const void* d_g,
+                  const void* d_h, int gh_mode, double* d_hist, cudaStream_t s,
+                  const double* parent = nullptr, double* sibling = nullptr, int acc_bytes = 4) {
   const hbg_layout& L = ds->layout;
   require(count >= 0, "negative leaf size");
   require(count <= L.num_rows || d_idx != nullptr, "identity leaf larger than the dataset");
@@ -377,8 +378,8 @@ void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const fl
   }
   require(d_g != nullptr && d_h != nullptr, "null gradient/hessian pointer");
   if (d_idx == nullptr) d_idx = identity_rows(ds, 0, s);  // identity leaf [0, count)
-  HistPlan plan = plan_histogram(L.bits_per_bin, L.max_bin, L.num_groups, count, L.device);
-  float* part = static_cast<float*>(ds->part.get(plan.part_values * 12 + 16));
+  HistPlan plan = plan_histogram(L.bits_per_bin, L.max_bin, L.num_groups, count, L.device, true, acc_bytes);
+  char* part = static_cast<char*>(ds->part.get(hist_part_bytes(plan)));
   HistArgs a{};
   a.packed = reinterpret_cast<const uint8_t*>(ds->packed);
   a.row_stride = L.row_stride_bytes;
@@ -393,8 +394,8 @@ void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const fl
   a.nblocks = plan.nblocks;
   a.seg_len = plan.seg_len;
   a.part_g = part;
-  a.part_h = part + plan.part_values;
-  a.part_c = reinterpret_cast<uint32_t*>(part + 2 * plan.part_values);
+  a.part_h = part + plan.part_values * plan.acc_bytes;
+  a.part_c = reinterpret_cast<uint32_t*>(part + 2 * plan.part_values * plan.acc_bytes);
   a.direct = plan.nseg == 1 ? 1 : 0;
   a.d = L.num_features;
   a.max_bin = L.max_bin;
@@ -429,7 +430,7 @@ void build_device_peer(hbg_dataset* ds, const int32_t* d_idx, int64_t count, con
   if (d_idx == nullptr && count > 0) d_idx = identity_rows(ds, 0, s);
   HistPlan plan = plan_histogram(L.bits_per_bin, L.max_bin, L.num_groups, std::max<int64_t>(count, 1), L.device,
                                  /*allow_direct=*/false);
-  float* part = static_cast<float*>(ds->part.get(plan.part_values * 12 + 16));
+  char* part = static_cast<char*>(ds->part.get(hist_part_bytes(plan)));
   HistArgs a{};
   a.packed = reinterpret_cast<const uint8_t*>(ds->packed);
   a.row_stride = L.row_stride_bytes;
@@ -444,8 +445,8 @@ void build_device_peer(hbg_dataset* ds, const int32_t* d_idx, int64_t count, con
   a.nblocks = plan.nblocks;
   a.seg_len = plan.seg_len;
   a.part_g = part;
-  a.part_h = part + plan.part_values;
-  a.part_c = reinterpret_cast<uint32_t*>(part + 2 * plan.part_values);
+  a.part_h = part + plan.part_values * plan.acc_bytes;
+  a.part_c = reinterpret_cast<uint32_t*>(part + 2 * plan.part_values * plan.acc_bytes);
   a.d = L.num_features;
   a.max_bin = L.max_bin;
   if (count > 0) {
@@ -503,13 +504,19 @@ struct Reducer {
   }
 };
 
-void grow_tree_impl(hbg_dataset* ds, const float* d_grad, const float* d_hess,
+// d_grad/d_hess: fp32 (P.precision == HBG_PRECISION_BITS32) or fp64
+// (HBG_PRECISION_BITS64: fp64 ordered buffers, partitions and fp64-accumulated
+// histograms for every leaf — the reference's reference_impl<double>).
+void grow_tree_impl(hbg_dataset* ds, const void* d_grad, const void* d_hess,
                     const hbg_grow_params& P, const Reducer& reduce, hbg_split* split_log,
                     int32_t* num_splits, hbg_tree_node* nodes_out, int32_t* num_nodes, cudaStream_t s,
                     std::vector<LeafRange>* final_leaves = nullptr) {
   const hbg_layout& L = ds->layout;
   require(P.num_leaves >= 1, "num_leaves must be at least 1");
   require(P.min_data_in_leaf >= 0, "min_data_in_leaf must be non-negative");
+  require(P.precision == HBG_PRECISION_BITS32 || P.precision == HBG_PRECISION_BITS64, "unknown precision");
+  const bool f64 = P.precision == HBG_PRECISION_BITS64;
+  const size_t es = f64 ? 8 : 4;  // bytes per g/h element
   const bool sharded = reduce.fn != nullptr;
   const int64_t N = L.num_rows;
   const int d = L.num_features, k = L.max_bin;
@@ -517,13 +524,15 @@ void grow_tree_impl(hbg_dataset* ds, const float* d_grad, const float* d_hess,
   const int max_slots = std::max(1, P.num_leaves);
   double* slots = static_cast<double*>(ds->slots.get(max_slots * D3 * sizeof(double) + 8));
   int32_t* rows[2];
-  float* gb[2];
-  float* hb[2];
+  char* gb[2];
+  char* hb[2];
   for (int b = 0; b < 2; ++b) {
     rows[b] = static_cast<int32_t*>(ds->ord[b][0].get(static_cast<size_t>(N) * 4 + 4));
-    gb[b] = static_cast<float*>(ds->ord[b][1].get(static_cast<size_t>(N) * 4 + 4));
-    hb[b] = static_cast<float*>(ds->ord[b][2].get(static_cast<size_t>(N) * 4 + 4));
+    gb[b] = static_cast<char*>(ds->ord[b][1].get(static_cast<size_t>(N) * es + 8));
+    hb[b] = static_cast<char*>(ds->ord[b][2].get(static_cast<size_t>(N) * es + 8));
   }
+  auto G = [&](int b, int64_t i) { return gb[b] + static_cast<size_t>(i) * es; };
+  auto H = [&](int b, int64_t i) { return hb[b] + static_cast<size_t>(i) * es; };
   void* scratch = ds->part_scratch.get(std::max(partition_scratch_bytes(N),
                                                 gather_scratch_doubles(N) * sizeof(double)) + 64);
   SplitResults* dres = static_cast<SplitResults*>(ds->tree_small.get(sizeof(SplitResults)));
@@ -545,27 +554,36 @@ void grow_tree_impl(hbg_dataset* ds, const float* d_grad, const float* d_hess,
   // totals and row count (summed across ranks).
   launch_iota(rows[0], N, s);
   if (N > 0) {
-    HBG_CUDA(cudaMemcpyAsync(gb[0], d_grad, static_cast<size_t>(N) * 4, cudaMemcpyDeviceToDevice, s));
-    HBG_CUDA(cudaMemcpyAsync(hb[0], d_hess, static_cast<size_t>(N) * 4, cudaMemcpyDeviceToDevice, s));
+    HBG_CUDA(cudaMemcpyAsync(gb[0], d_grad, static_cast<size_t>(N) * es, cudaMemcpyDeviceToDevice, s));
+    HBG_CUDA(cudaMemcpyAsync(hb[0], d_hess, static_cast<size_t>(N) * es, cudaMemcpyDeviceToDevice, s));
   }
-  launch_gather(rows[0], N, d_grad, d_hess, nullptr, nullptr, dres->root,
-                static_cast<double*>(scratch), s);
-  // fixed-point scale for the small-leaf histogram path, accumulator cleared
+  if (f64)
+    launch_gather_f64(rows[0], N, static_cast<const double*>(d_grad), static_cast<const double*>(d_hess), nullptr,
+                      nullptr, dres->root, static_cast<double*>(scratch), s);
+  else
+    launch_gather(rows[0], N, static_cast<const float*>(d_grad), static_cast<const float*>(d_hess), nullptr,
+                  nullptr, dres->root, static_cast<double*>(scratch), s);
+  // fixed-point scale for the bits32 small-leaf histogram path, accumulator
+  // cleared (bits64 builds every leaf with fp64 accumulation instead)
   int* exps = static_cast<int*>(ds->small_exps.get(16));
   void* acc = ds->small_acc.get(small_hist_acc_bytes(d, k));
-  launch_fixed_scale(gb[0], hb[0], N, exps, s);
-  HBG_CUDA(cudaMemsetAsync(acc, 0, small_hist_acc_bytes(d, k), s));
+  if (!f64) {
+    launch_fixed_scale(reinterpret_cast<const float*>(gb[0]), reinterpret_cast<const float*>(hb[0]), N, exps, s);
+    HBG_CUDA(cudaMemsetAsync(acc, 0, small_hist_acc_bytes(d, k), s));
+  }
   const uint32_t* packed = ds->packed;
   const int stride_words = L.row_stride_bytes / 4;
+  const int acc_bytes = f64 ? 8 : 4;
   // histogram of one leaf range into `out` (+ sibling = parent - out)
   auto leaf_hist = [&](int buf, int64_t begin, int64_t count, double* out, const double* parent,
                        double* sibling) {
-    if (count <= kAtomicHistRows) {
-      launch_small_hist(rows[buf] + begin, gb[buf] + begin, hb[buf] + begin, count, packed, stride_words,
+    if (!f64 && count <= kAtomicHistRows) {
+      launch_small_hist(rows[buf] + begin, reinterpret_cast<const float*>(G(buf, begin)),
+                        reinterpret_cast<const float*>(H(buf, begin)), count, packed, stride_words,
                         L.words_per_row, L.bits_per_bin, d, k, exps, acc, out, parent, sibling, s);
     } else {
-      build_device(ds, rows[buf] + begin, count, gb[buf] + begin, hb[buf] + begin, HBG_GH_LEAF_ALIGNED,
-                   out, s, parent, sibling);
+      build_device(ds, rows[buf] + begin, count, G(buf, begin), H(buf, begin), HBG_GH_LEAF_ALIGNED, out, s, parent,
+                   sibling, acc_bytes);
     }
   };
   hres->root[2] = static_cast<double>(N);  // pinned staging; the stream orders the copy
@@ -580,7 +598,8 @@ void grow_tree_impl(hbg_dataset* ds, const float* d_grad, const float* d_hess,
     if (splittable(NG)) {
       root.slot = free_slots.back();
       free_slots.pop_back();
-      build_device(ds, rows[0], N, gb[0], hb[0], HBG_GH_LEAF_ALIGNED, slot_ptr(root.slot), s);
+      build_device(ds, rows[0], N, gb[0], hb[0], HBG_GH_LEAF_ALIGNED, slot_ptr(root.slot), s, nullptr, nullptr,
+                   acc_bytes);
       reduce(slot_ptr(root.slot), static_cast<int64_t>(D3), s);
       launch_best_split(slot_ptr(root.slot), d, k, dres->root, nullptr, 0.0, 0.0, NG,
                         P.min_data_in_leaf, P.lambda, &dres->split[0], s);
@@ -607,11 +626,20 @@ void grow_tree_impl(hbg_dataset* ds, const float* d_grad, const float* d_hess,
     const int out = 1 - parent.buf;
     const int64_t gl_n = sp.left_count, gr_n = parent.gcount - sp.left_count;  // global sizes
     if (gl_n <= 0 || gr_n <= 0) throw Error(HBG_ERR_LOGIC, "split produced an empty side");
-    launch_partition(rows[parent.buf] + parent.begin, gb[parent.buf] + parent.begin,
-                     hb[parent.buf] + parent.begin, parent.count,
-                     reinterpret_cast<const uint8_t*>(ds->packed), L.row_stride_bytes, sp.feature,
-                     L.bits_per_bin, sp.threshold_bin, rows[out] + parent.begin, gb[out] + parent.begin,
-                     hb[out] + parent.begin, scratch, dres->totals, &dres->left, s);
+    if (f64)
+      launch_partition_f64(rows[parent.buf] + parent.begin, reinterpret_cast<const double*>(G(parent.buf, parent.begin)),
+                           reinterpret_cast<const double*>(H(parent.buf, parent.begin)), parent.count,
+                           reinterpret_cast<const uint8_t*>(ds->packed), L.row_stride_bytes, sp.feature,
+                           L.bits_per_bin, sp.threshold_bin, rows[out] + parent.begin,
+                           reinterpret_cast<double*>(G(out, parent.begin)), reinterpret_cast<double*>(H(out, parent.begin)),
+                           scratch, dres->totals, &dres->left, s);
+    else
+      launch_partition(rows[parent.buf] + parent.begin, reinterpret_cast<const float*>(G(parent.buf, parent.begin)),
+                       reinterpret_cast<const float*>(H(parent.buf, parent.begin)), parent.count,
+                       reinterpret_cast<const uint8_t*>(ds->packed), L.row_stride_bytes, sp.feature,
+                       L.bits_per_bin, sp.threshold_bin, rows[out] + parent.begin,
+                       reinterpret_cast<float*>(G(out, parent.begin)), reinterpret_cast<float*>(H(out, parent.begin)),
+                       scratch, dres->totals, &dres->left, s);
     reduce(dres->totals, 4, s);  // global child totals
     int64_t nl_local = gl_n;
     if (sharded) {  // this rank's left count is needed before the children can be addressed
@@ -645,12 +673,12 @@ void grow_tree_impl(hbg_dataset* ds, const float* d_grad, const float* d_hess,
       free_slots.pop_back();
       large.slot = parent.slot;
       parent.slot = -1;
-      if (!sharded && small.count <= kAtomicHistRows) {
+      if (!f64 && !sharded && small.count <= kAtomicHistRows) {
         // small child: L2-atomic histogram, then one fused launch for the
         // conversion, the subtraction and both children's scans
-        launch_small_hist_atomic(rows[out] + small.begin, gb[out] + small.begin, hb[out] + small.begin,
-                                 small.count, packed, stride_words, L.words_per_row, L.bits_per_bin, d, k,
-                                 exps, acc, s);
+        launch_small_hist_atomic(rows[out] + small.begin, reinterpret_cast<const float*>(G(out, small.begin)),
+                                 reinterpret_cast<const float*>(H(out, small.begin)), small.count, packed,
+                                 stride_words, L.words_per_row, L.bits_per_bin, d, k, exps, acc, s);
         FinishScanArgsHost fa{acc, exps, d, k, slot_ptr(small.slot), slot_ptr(large.slot),
                               &small == &lo ? 1 : 0, dres->totals, gl_n, gr_n, lsplit ? 1 : 0,
                               rsplit ? 1 : 0, P.min_data_in_leaf, P.lambda, &dres->split[0]};
@@ -767,7 +795,7 @@ PersistentGrowArgs grow_workspace(hbg_dataset* ds, const hbg_grow_params& P, int
   ds->part_scratch.get(gather_scratch_doubles(N) * sizeof(double) + 64);
   if (N > 0 && d > 0) {  // the root histogram's partials (build_device)
     const HistPlan plan = plan_histogram(L.bits_per_bin, L.max_bin, L.num_groups, N, L.device);
-    ds->part.get(plan.part_values * 12 + 16);
+    ds->part.get(hist_part_bytes(plan));
   }
   return a;
 }
@@ -778,6 +806,7 @@ void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_h
   const hbg_layout& L = ds->layout;
   require(P.num_leaves >= 1, "num_leaves must be at least 1");
   require(P.min_data_in_leaf >= 0, "min_data_in_leaf must be non-negative");
+  require(P.precision == HBG_PRECISION_BITS32, "the persistent grower runs bits32 (fp32 g/h) trees");
   const int64_t N = L.num_rows;
   const int d = L.num_features, k = L.max_bin;
   const int max_nodes = std::max(1, 2 * P.num_leaves - 1);
@@ -948,6 +977,7 @@ void boost_impl(hbg_dataset* ds, const double* d_targets, double* d_scores, int 
                 int32_t* num_splits, hbg_tree_node* nodes, int32_t* num_nodes, cudaStream_t s,
                 hbg_peer* peer = nullptr) {
   require(loss == HBG_LOSS_SQUARED || loss == HBG_LOSS_LOGISTIC, "unknown loss");
+  require(P.precision == HBG_PRECISION_BITS32, "boosting iterations run bits32 (fp32 g/h) trees");
   const int64_t N = ds->layout.num_rows;
   float* g = static_cast<float*>(ds->boost_g.get(static_cast<size_t>(N) * 4 + 4));
   float* h = static_cast<float*>(ds->boost_h.get(static_cast<size_t>(N) * 4 + 4));
@@ -1085,8 +1115,15 @@ int hbg_dataset_packed_words(const hbg_dataset* ds, uint32_t* host_words) {
 
 int hbg_build_histograms(hbg_dataset* ds, const int32_t* indices, int64_t count,
                          const double* gradients, const double* hessians, hbg_bin* out) {
+  return hbg_build_histograms_ex(ds, indices, count, gradients, hessians, HBG_PRECISION_BITS32, out);
+}
+
+int hbg_build_histograms_ex(hbg_dataset* ds, const int32_t* indices, int64_t count,
+                            const double* gradients, const double* hessians, int32_t precision,
+                            hbg_bin* out) {
   return guarded([&] {
     check_ds(ds);
+    require(precision == HBG_PRECISION_BITS32 || precision == HBG_PRECISION_BITS64, "unknown precision");
     const hbg_layout& L = ds->layout;
     require(count >= 0, "negative leaf size");
     require(out != nullptr, "null output");
@@ -1096,7 +1133,26 @@ int hbg_build_histograms(hbg_dataset* ds, const int32_t* indices, int64_t count,
     const size_t D = static_cast<size_t>(L.num_features) * L.max_bin;
     double* d_hist = static_cast<double*>(ds->host_hist.get(3 * D * sizeof(double) + 8));
     hbg_bin* d_bins = static_cast<hbg_bin*>(ds->host_bins.get(D * sizeof(hbg_bin) + 8));
-    if (count > 0 && !(is_pinned(gradients) && is_pinned(hessians))) {
+    if (count > 0 && precision == HBG_PRECISION_BITS64) {
+      // bits64: the fp64 LeafState arrays go up as they are (no per-element
+      // cast); pinned ones at full PCIe rate, pageable ones through the
+      // driver's staging. One histogram launch accumulates in fp64.
+      const size_t n = static_cast<size_t>(count);
+      double* d_gd = static_cast<double*>(ds->host_gd.get(n * 8));
+      double* d_hd = static_cast<double*>(ds->host_hd.get(n * 8));
+      HBG_CUDA(cudaMemcpyAsync(d_gd, gradients, n * 8, cudaMemcpyHostToDevice, s));
+      HBG_CUDA(cudaMemcpyAsync(d_hd, hessians, n * 8, cudaMemcpyHostToDevice, s));
+      const int32_t* d_idx;
+      if (leaf_is_contiguous(indices, count)) {
+        require(indices[0] >= 0 && indices[0] + count <= L.num_rows, "leaf row index out of range");
+        d_idx = identity_rows(ds, indices[0], s);
+      } else {
+        int32_t* di = static_cast<int32_t*>(ds->host_idx.get(n * 4));
+        HBG_CUDA(cudaMemcpyAsync(di, indices, n * 4, cudaMemcpyHostToDevice, s));
+        d_idx = di;
+      }
+      build_device(ds, d_idx, count, d_gd, d_hd, HBG_GH_LEAF_ALIGNED, d_hist, s, nullptr, nullptr, 8);
+    } else if (count > 0 && !(is_pinned(gradients) && is_pinned(hessians))) {
       // pageable LeafState arrays: fp32 g/h staged by the host pool (see
       // stage_chunks); histogram chunk c runs as soon as its rows have landed
       const size_t n = static_cast<size_t>(count);
@@ -1209,6 +1265,16 @@ int hbg_build_histograms_device(hbg_dataset* ds, const int32_t* d_indices, int64
   });
 }
 
+int hbg_build_histograms_device_f64(hbg_dataset* ds, const int32_t* d_indices, int64_t count,
+                                    const double* d_grad, const double* d_hess, int32_t gh_mode,
+                                    double* d_hist, void* stream) {
+  return guarded([&] {
+    check_ds(ds);
+    DeviceGuard dg(ds->layout.device);
+    build_device(ds, d_indices, count, d_grad, d_hess, gh_mode, d_hist, pick(ds, stream), nullptr, nullptr, 8);
+  });
+}
+
 int hbg_hist_to_bins_device(const double* d_hist, int32_t num_features, int32_t max_bin,
                             hbg_bin* d_bins, void* stream) {
   return guarded([&] {
@@ -1233,12 +1299,46 @@ int hbg_gather_leaf_device(const int32_t* d_indices, int64_t count, const float*
     require(count >= 0, "negative leaf size");
     require(d_totals != nullptr, "null totals");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    static thread_local DevBuf scratch;
+    // scratch per (thread, device): a buffer allocated on one device must not
+    // serve a launch on another
+    static thread_local DevBuf scratch[64];
     int dev = 0;
     HBG_CUDA(cudaGetDevice(&dev));
-    (void)dev;
-    double* sc = static_cast<double*>(scratch.get(gather_scratch_doubles(count) * sizeof(double)));
+    double* sc = static_cast<double*>(scratch[dev & 63].get(gather_scratch_doubles(count) * sizeof(double)));
     launch_gather(d_indices, count, d_grad, d_hess, d_leaf_grad, d_leaf_hess, d_totals, sc, s);
+  });
+}
+
+int hbg_gather_leaf_statistics(const int32_t* indices, int64_t count, const double* gradients,
+                               const double* hessians, int64_t num_rows, double* leaf_grad,
+                               double* leaf_hess, double* totals, int32_t device) {
+  return guarded([&] {
+    require(count >= 0 && num_rows >= 0, "negative size");
+    require(totals != nullptr, "null totals");
+    require(count == 0 || (indices && gradients && hessians && leaf_grad && leaf_hess), "null leaf arrays");
+    for (int64_t i = 0; i < count; ++i)  // the reference leaves this UB (tree.cpp:19); here it is an error
+      require(indices[i] >= 0 && indices[i] < num_rows, "leaf row index out of range");
+    DeviceGuard dg(device);
+    DevBuf di, dg_, dh, dlg, dlh, dt, sc;
+    const size_t n = static_cast<size_t>(count), N = static_cast<size_t>(num_rows);
+    int32_t* d_idx = static_cast<int32_t*>(di.get(n * 4 + 4));
+    double* d_g = static_cast<double*>(dg_.get(N * 8 + 8));
+    double* d_h = static_cast<double*>(dh.get(N * 8 + 8));
+    double* d_lg = static_cast<double*>(dlg.get(n * 8 + 8));
+    double* d_lh = static_cast<double*>(dlh.get(n * 8 + 8));
+    double* d_t = static_cast<double*>(dt.get(2 * sizeof(double)));
+    double* d_sc = static_cast<double*>(sc.get(gather_scratch_doubles(count) * sizeof(double)));
+    if (count > 0) {
+      HBG_CUDA(cudaMemcpy(d_idx, indices, n * 4, cudaMemcpyHostToDevice));
+      HBG_CUDA(cudaMemcpy(d_g, gradients, N * 8, cudaMemcpyHostToDevice));
+      HBG_CUDA(cudaMemcpy(d_h, hessians, N * 8, cudaMemcpyHostToDevice));
+    }
+    launch_gather_f64(d_idx, count, d_g, d_h, d_lg, d_lh, d_t, d_sc, nullptr);
+    if (count > 0) {
+      HBG_CUDA(cudaMemcpy(leaf_grad, d_lg, n * 8, cudaMemcpyDeviceToHost));
+      HBG_CUDA(cudaMemcpy(leaf_hess, d_lh, n * 8, cudaMemcpyDeviceToHost));
+    }
+    HBG_CUDA(cudaMemcpy(totals, d_t, 2 * sizeof(double), cudaMemcpyDeviceToHost));
   });
 }
 
@@ -1300,6 +1400,8 @@ int hbg_grow_tree(hbg_dataset* ds, const float* d_grad, const float* d_hess,
             "null argument");
     require(ds->layout.num_rows == 0 || (d_grad != nullptr && d_hess != nullptr),
             "null gradient/hessian pointer");
+    require(params->precision == HBG_PRECISION_BITS32,
+            "hbg_grow_tree takes fp32 gradients (bits32); bits64 trees: hbg_grow_tree_f64 / hbg_grow_tree_host");
     DeviceGuard dg(ds->layout.device);
     if (use_host_loop())
       grow_tree_impl(ds, d_grad, d_hess, *params, Reducer{nullptr, nullptr}, split_log, num_splits,
@@ -1307,6 +1409,22 @@ int hbg_grow_tree(hbg_dataset* ds, const float* d_grad, const float* d_hess,
     else
       grow_tree_persistent(ds, d_grad, d_hess, *params, split_log, num_splits, nodes, num_nodes,
                            static_cast<cudaStream_t>(stream));
+  });
+}
+
+int hbg_grow_tree_f64(hbg_dataset* ds, const double* d_grad, const double* d_hess,
+                      const hbg_grow_params* params, hbg_split* split_log, int32_t* num_splits,
+                      hbg_tree_node* nodes, int32_t* num_nodes, void* stream) {
+  return guarded([&] {
+    check_ds(ds);
+    require(params != nullptr && split_log != nullptr && num_splits != nullptr && num_nodes != nullptr,
+            "null argument");
+    require(ds->layout.num_rows == 0 || (d_grad != nullptr && d_hess != nullptr),
+            "null gradient/hessian pointer");
+    require(params->precision == HBG_PRECISION_BITS64, "hbg_grow_tree_f64 grows bits64 trees");
+    DeviceGuard dg(ds->layout.device);
+    grow_tree_impl(ds, d_grad, d_hess, *params, Reducer{nullptr, nullptr}, split_log, num_splits, nodes,
+                   num_nodes, static_cast<cudaStream_t>(stream));
   });
 }
 
@@ -1319,8 +1437,22 @@ int hbg_grow_tree_host(hbg_dataset* ds, const double* gradients, const double* h
             "null argument");
     const int64_t N = ds->layout.num_rows;
     require(N == 0 || (gradients != nullptr && hessians != nullptr), "null gradient/hessian pointer");
+    require(params->precision == HBG_PRECISION_BITS32 || params->precision == HBG_PRECISION_BITS64,
+            "unknown precision");
     DeviceGuard dg(ds->layout.device);
     cudaStream_t s = ds->stream;
+    if (params->precision == HBG_PRECISION_BITS64) {  // fp64 g/h as they are, fp64 everywhere
+      const size_t n = static_cast<size_t>(N);
+      double* gd = static_cast<double*>(ds->host_gd.get(n * 8 + 8));
+      double* hd = static_cast<double*>(ds->host_hd.get(n * 8 + 8));
+      if (N > 0) {
+        HBG_CUDA(cudaMemcpyAsync(gd, gradients, n * 8, cudaMemcpyHostToDevice, s));
+        HBG_CUDA(cudaMemcpyAsync(hd, hessians, n * 8, cudaMemcpyHostToDevice, s));
+      }
+      grow_tree_impl(ds, gd, hd, *params, Reducer{nullptr, nullptr}, split_log, num_splits, nodes, num_nodes, s);
+      HBG_CUDA(cudaStreamSynchronize(s));
+      return;
+    }
     float *gf = nullptr, *hf = nullptr;
     if (N > 0 && !(is_pinned(gradients) && is_pinned(hessians))) {  // pageable: staged as fp32 (stage_chunks)
       const size_t n = static_cast<size_t>(N);
@@ -1500,6 +1632,7 @@ int hbg_grow_tree_sharded(hbg_dataset* ds, const float* d_grad, const float* d_h
             "null argument");
     require(ds->layout.num_rows == 0 || (d_grad != nullptr && d_hess != nullptr),
             "null gradient/hessian pointer");
+    require(params->precision == HBG_PRECISION_BITS32, "hbg_grow_tree_sharded takes fp32 gradients (bits32)");
     DeviceGuard dg(ds->layout.device);
     grow_tree_impl(ds, d_grad, d_hess, *params, Reducer{allreduce, ctx}, split_log, num_splits,
                    nodes, num_nodes, static_cast<cudaStream_t>(stream));

@@ -45,6 +45,7 @@ struct HistPlan {
   int ctas;         // nblocks * nseg
   size_t smem;      // dynamic shared memory per CTA
   size_t part_values;  // entries in each partial array (ctas * gb * 32 * k_alloc)
+  int acc_bytes;       // 4: fp32 g/h and cells (bits32); 8: fp64 (bits64)
 };
 
 struct HistArgs {
@@ -52,14 +53,14 @@ struct HistArgs {
   int64_t row_stride;  // bytes
   const int32_t* idx;  // nullptr: identity leaf
   int64_t n;
-  const float* g;
-  const float* h;
+  const void* g;  // float (bits32) or double (bits64) per HistPlan::acc_bytes
+  const void* h;
   int gh_indexed;
   int num_groups;
   int gb, wpg, nblocks;
   int64_t seg_len;
-  float* part_g;
-  float* part_h;
+  void* part_g;  // per-CTA partials, same type as g/h
+  void* part_h;
   uint32_t* part_c;
   // direct mode (a single row segment): the CTAs write the final fp64
   // histogram (and the fused sibling) themselves, no partials / reduce launch
@@ -73,7 +74,12 @@ struct HistArgs {
 
 // allow_direct = false: always per-CTA partials + a reduction (the row-sharded
 // path fuses its exchange into that reduction).
-HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int device, bool allow_direct = true);
+// acc_bytes: 4 = fp32 g/h inputs, cells and partials (PrecisionMode::bits32);
+// 8 = fp64 throughout (PrecisionMode::bits64).
+HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int device, bool allow_direct = true,
+                        int acc_bytes = 4);
+// Bytes of the partial buffers of a plan (g, h: acc_bytes each; count: 4).
+inline size_t hist_part_bytes(const HistPlan& p) { return p.part_values * (2 * p.acc_bytes + 4) + 16; }
 
 void launch_histogram(const HistPlan& plan, const HistArgs& args, cudaStream_t s);
 // d_hist = reduced histogram; when `parent` is non-null also writes
@@ -107,6 +113,9 @@ void launch_hist_to_bins(const double* d_hist, int64_t cells, hbg_bin* d_bins, c
 void launch_subtract(const double* a, const double* b, double* out, int64_t n, cudaStream_t s);
 void launch_gather(const int32_t* idx, int64_t n, const float* g, const float* h, float* lg,
                    float* lh, double* totals, double* scratch, cudaStream_t s);
+// fp64 g/h (bits64): leaf-aligned copies (optional) and fixed-order totals.
+void launch_gather_f64(const int32_t* idx, int64_t n, const double* g, const double* h, double* lg,
+                       double* lh, double* totals, double* scratch, cudaStream_t s);
 size_t gather_scratch_doubles(int64_t n);
 // Split scans of 1-2 histograms in one launch (one CTA each): histogram i at
 // d_hist + i*hist_stride, totals at d_totals + i*totals_stride, count
@@ -127,6 +136,11 @@ void launch_partition(const int32_t* rows, const float* g, const float* h, int64
                       const uint8_t* packed, int64_t row_stride, int feature, int bits, int thr,
                       int32_t* orow, float* og, float* oh, void* scratch, double* d_totals,
                       int64_t* d_left, cudaStream_t s);
+// The same with fp64 g/h (PrecisionMode::bits64 trees).
+void launch_partition_f64(const int32_t* rows, const double* g, const double* h, int64_t n,
+                          const uint8_t* packed, int64_t row_stride, int feature, int bits, int thr,
+                          int32_t* orow, double* og, double* oh, void* scratch, double* d_totals,
+                          int64_t* d_left, cudaStream_t s);
 
 // One final leaf of a grown tree: its rows' range in ordered buffer `buf`.
 struct LeafRange {

@@ -21,6 +21,16 @@ __device__ __forceinline__ void sts_f2(uint32_t a, float x, float y) {
   asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(x), "f"(y));
 }
 
+// fp64 cells of the bits64 (PrecisionMode::bits64) kernels: one 16-byte
+// {g,h} pair per cell, LDS.128 / STS.128.
+__device__ __forceinline__ void lds_f2(uint32_t a, double& x, double& y) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
+}
+
+__device__ __forceinline__ void sts_f2(uint32_t a, double x, double y) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(x), "d"(y));
+}
+
 template <int BITS>
 struct Slice {
   static constexpr int kWords = BITS == 8 ? 8 : 4;  // 32 features per slice
@@ -71,9 +81,11 @@ __device__ __forceinline__ void rotate_slice(Slice<BITS>& s, int lane) {
   for (int j = 0; j < W; ++j) s.w[j] = t[j];
 }
 
-template <int BITS, int K, bool kTail>
+// T = float (bits32: the reference's per-element fp32 cast, histogram.cpp:97-98)
+// or double (bits64); a cell is the {g,h} pair of T at gh_base + cell * 2 * sizeof(T).
+template <int BITS, int K, bool kTail, typename T = float>
 __device__ __forceinline__ void update_step(const Slice<BITS>& s, int p, int lane, uint32_t gh_base,
-                                            uint32_t* cnt, float g, float h, bool active) {
+                                            uint32_t* cnt, T g, T h, bool active) {
   // Lane l's step-p cell and lane (l-1)'s step-(p+1) cell can coincide, so
   // consecutive steps must be ordered across lanes: __syncwarp is the
   // warp-scope memory-ordering point for that (all lanes execute it).
@@ -82,8 +94,8 @@ __device__ __forceinline__ void update_step(const Slice<BITS>& s, int p, int lan
   constexpr int fpw = Slice<BITS>::kFeatPerWord;
   const uint32_t b = (s.w[p / fpw] >> (BITS * (p % fpw))) & (K - 1);
   const uint32_t cell = (b << 5) | ((lane + p) & 31);
-  const uint32_t a = gh_base + cell * 8u;
-  float x, y;
+  const uint32_t a = gh_base + cell * static_cast<uint32_t>(2 * sizeof(T));
+  T x, y;
   lds_f2(a, x, y);
   x += g;
   y += h;
@@ -96,21 +108,22 @@ __device__ __forceinline__ void update_step(const Slice<BITS>& s, int p, int lan
 // per ordered step, i.e. more independent MIO traffic per warp); when two of
 // a lane's rows hit the same cell, the later one builds on the earlier sum so
 // the last store carries both.
-template <int BITS, int K, int R>
+template <int BITS, int K, int R, typename T = float>
 __device__ __forceinline__ void update_step_rows(const Slice<BITS> (&s)[R], int p, int lane,
-                                                 uint32_t gh_base, uint32_t* cnt, const float (&g)[R],
-                                                 const float (&h)[R]) {
+                                                 uint32_t gh_base, uint32_t* cnt, const T (&g)[R],
+                                                 const T (&h)[R]) {
   asm volatile("bar.warp.sync -1;" ::: "memory");
   constexpr int fpw = Slice<BITS>::kFeatPerWord;
+  constexpr uint32_t kCellBytes = 2 * sizeof(T);
   uint32_t c[R];
-  float x[R], y[R];
+  T x[R], y[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const uint32_t b = (s[r].w[p / fpw] >> (BITS * (p % fpw))) & (K - 1);
     c[r] = (b << 5) | ((lane + p) & 31);
   }
 #pragma unroll
-  for (int r = 0; r < R; ++r) lds_f2(gh_base + c[r] * 8u, x[r], y[r]);
+  for (int r = 0; r < R; ++r) lds_f2(gh_base + c[r] * kCellBytes, x[r], y[r]);
 #pragma unroll
   for (int r = 0; r < R; ++r) {
 #pragma unroll
@@ -124,7 +137,7 @@ __device__ __forceinline__ void update_step_rows(const Slice<BITS> (&s)[R], int 
     y[r] += h[r];
   }
 #pragma unroll
-  for (int r = 0; r < R; ++r) sts_f2(gh_base + c[r] * 8u, x[r], y[r]);
+  for (int r = 0; r < R; ++r) sts_f2(gh_base + c[r] * kCellBytes, x[r], y[r]);
 #pragma unroll
   for (int r = 0; r < R; ++r) atomicAdd(cnt + c[r], 1u);  // ATOMS.POPC.INC
 }
@@ -133,11 +146,16 @@ __device__ __forceinline__ void update_step_rows(const Slice<BITS> (&s)[R], int 
 // k<=128 kernels at their measured best (the shared-memory data pipe is ~85%
 // busy either way); k=256 runs 3 warps/SM and needs the extra independent work
 // (4 rows per lane = 12 independent chains per SM).
-template <int K>
+// fp64 cells (bits64) take twice the shared memory per warp, so half the
+// warps fit: two rows per lane at k=64 and four from k=128 restore the
+// independent read-modify-write chains per SM.
+template <int K, typename T = float>
 __host__ __device__ constexpr int rows_per_lane() {
-  return K >= 256 ? 4 : 1;
+  return sizeof(T) == 8 ? (K >= 128 ? 4 : (K >= 64 ? 2 : 1)) : (K >= 256 ? 4 : 1);
 }
-__host__ inline int rows_per_lane_of(int k_alloc) { return k_alloc >= 256 ? 4 : 1; }
+__host__ inline int rows_per_lane_of(int k_alloc, int acc_bytes = 4) {
+  return acc_bytes == 8 ? (k_alloc >= 128 ? 4 : (k_alloc >= 64 ? 2 : 1)) : (k_alloc >= 256 ? 4 : 1);
+}
 
 }  // namespace dev
 }  // namespace hbg

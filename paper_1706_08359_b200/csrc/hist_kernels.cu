@@ -22,6 +22,8 @@
 //    reduction (histogram.cpp:159-215).
 #include <algorithm>
 #include <mutex>
+#include <type_traits>
+#include <vector>
 
 #include "hbg_internal.h"
 #include "hist_device.cuh"
@@ -32,21 +34,29 @@ namespace {
 
 using namespace dev;
 
+template <typename T>
 struct TileIn {
   int32_t row;  // raw int32 row id (row_index_t): widening it right after the
                 // load would make the load's consumer immediate and stall on it
-  float g, h;
+  T g, h;
 };
 
-template <int BITS, int K, bool kRowIndexed>
+// T = float: bits32 (the reference's per-element fp32 cast, histogram.cpp:97-98);
+// T = double: bits64 (reference_impl<double>, histogram.cpp:131-145) — fp64
+// inputs, fp64 per-warp cells, fp64 partials.
+template <int BITS, int K, bool kRowIndexed, typename T>
 __global__ void __launch_bounds__(K >= 256 ? 128 : 512, BITS == 4 ? 2 : 1) hist_kernel(HistArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int kCells = K * 32;
+  constexpr int kCellBytes = 2 * sizeof(T);
   const int warps = blockDim.x >> 5;
-  float2* gh = reinterpret_cast<float2*>(smem);
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + static_cast<size_t>(warps) * kCells * 8);
+  using T2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
+  T2* gh = reinterpret_cast<T2*>(smem);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + static_cast<size_t>(warps) * kCells * kCellBytes);
+  const T* __restrict__ ag = static_cast<const T*>(a.g);
+  const T* __restrict__ ah = static_cast<const T*>(a.h);
   {
-    const int n16 = (warps * kCells * 8 + a.gb * kCells * 4) / 16;
+    const int n16 = (warps * kCells * kCellBytes + a.gb * kCells * 4) / 16;
     uint4* z = reinterpret_cast<uint4*>(smem);
     for (int i = threadIdx.x; i < n16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
   }
@@ -65,7 +75,7 @@ __global__ void __launch_bounds__(K >= 256 ? 128 : 512, BITS == 4 ? 2 : 1) hist_
     const uint32_t gh_base = smem_addr(gh + static_cast<size_t>(w) * kCells);
     uint32_t* cnt_g = cnt + static_cast<size_t>(gl) * kCells;
     const unsigned char* base = a.packed + static_cast<size_t>(group) * Slice<BITS>::kWords * 4;
-    constexpr int R = rows_per_lane<K>();
+    constexpr int R = rows_per_lane<K, T>();
     const int64_t step = static_cast<int64_t>(a.wpg) * 32 * R;
 
     // Two-stage software pipeline, so no load waits on another load in the
@@ -74,30 +84,30 @@ __global__ void __launch_bounds__(K >= 256 ? 128 : 512, BITS == 4 ? 2 : 1) hist_
     // t+s using the row ids stage A delivered one iteration earlier, and the
     // update loop consumes tile t. A tile is 32*R rows; lane l owns rows
     // t + 32r + l.
-    auto fetch_entry = [&](int64_t t, TileIn (&in)[R]) {
+    auto fetch_entry = [&](int64_t t, TileIn<T> (&in)[R]) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int64_t pos = t + 32 * r + lane;
         if (pos < s1) {
           in[r].row = __ldg(a.idx + pos);  // never null: the identity leaf uses an iota array
           if constexpr (!kRowIndexed) {
-            in[r].g = __ldg(a.g + pos);
-            in[r].h = __ldg(a.h + pos);
+            in[r].g = __ldg(ag + pos);
+            in[r].h = __ldg(ah + pos);
           }
         } else {
           in[r].row = -1;
-          in[r].g = 0.f;
-          in[r].h = 0.f;
+          in[r].g = T(0);
+          in[r].h = T(0);
         }
       }
     };
-    auto fetch_slice = [&](TileIn (&in)[R], Slice<BITS> (&sl)[R]) {
+    auto fetch_slice = [&](TileIn<T> (&in)[R], Slice<BITS> (&sl)[R]) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (in[r].row >= 0) {
           if constexpr (kRowIndexed) {
-            in[r].g = __ldg(a.g + in[r].row);
-            in[r].h = __ldg(a.h + in[r].row);
+            in[r].g = __ldg(ag + in[r].row);
+            in[r].h = __ldg(ah + in[r].row);
           }
           load_slice<BITS>(base + static_cast<int64_t>(in[r].row) * a.row_stride, sl[r]);
         } else {
@@ -108,34 +118,34 @@ __global__ void __launch_bounds__(K >= 256 ? 128 : 512, BITS == 4 ? 2 : 1) hist_
     };
 
     int64_t t = s0 + static_cast<int64_t>(sub) * 32 * R;
-    TileIn e0[R], e1[R];
+    TileIn<T> e0[R], e1[R];
     Slice<BITS> cur[R];
     fetch_entry(t, e0);
     fetch_entry(t + step, e1);
     fetch_slice(e0, cur);
     for (; t < s1; t += step) {
-      TileIn e2[R];
+      TileIn<T> e2[R];
       Slice<BITS> nxt[R];
       fetch_entry(t + 2 * step, e2);  // stage A (t + 2s)
       fetch_slice(e1, nxt);           // stage B (t + s)
 #pragma unroll
       for (int r = 0; r < R; ++r) rotate_slice<BITS>(cur[r], lane);
       if (t + 32 * R <= s1) {
-        float g[R], h[R];
+        T g[R], h[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           g[r] = e0[r].g;
           h[r] = e0[r].h;
         }
 #pragma unroll
-        for (int p = 0; p < 32; ++p) update_step_rows<BITS, K, R>(cur, p, lane, gh_base, cnt_g, g, h);
+        for (int p = 0; p < 32; ++p) update_step_rows<BITS, K, R, T>(cur, p, lane, gh_base, cnt_g, g, h);
       } else {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const bool valid = e0[r].row >= 0;
 #pragma unroll
           for (int p = 0; p < 32; ++p)
-            update_step<BITS, K, true>(cur[r], p, lane, gh_base, cnt_g, e0[r].g, e0[r].h, valid);
+            update_step<BITS, K, true, T>(cur[r], p, lane, gh_base, cnt_g, e0[r].g, e0[r].h, valid);
         }
       }
 #pragma unroll
@@ -149,11 +159,11 @@ __global__ void __launch_bounds__(K >= 256 ? 128 : 512, BITS == 4 ? 2 : 1) hist_
   __syncthreads();
 
   // Fold the warps of each group in a fixed order.
-  auto fold = [&](int g2, int c, float& sg, float& sh) {
-    sg = 0.f;
-    sh = 0.f;
+  auto fold = [&](int g2, int c, T& sg, T& sh) {
+    sg = T(0);
+    sh = T(0);
     for (int s = 0; s < a.wpg; ++s) {
-      const float2 v = gh[static_cast<size_t>(s * a.gb + g2) * kCells + c];
+      const T2 v = gh[static_cast<size_t>(s * a.gb + g2) * kCells + c];
       sg += v.x;
       sh += v.y;
     }
@@ -178,7 +188,7 @@ __global__ void __launch_bounds__(K >= 256 ? 128 : 512, BITS == 4 ? 2 : 1) hist_
           const int fl = i / a.max_bin, bin = i - fl * a.max_bin;
           const int g2 = fl >> 5;
           const int c = (bin << 5) | (fl & 31);
-          float sg, sh;
+          T sg, sh;
           fold(g2, c, sg, sh);
           vg[j] = sg;
           vh[j] = sh;
@@ -207,15 +217,17 @@ __global__ void __launch_bounds__(K >= 256 ? 128 : 512, BITS == 4 ? 2 : 1) hist_
     }
     return;
   }
-  // One fp32/u32 partial per CTA.
+  // One partial per CTA (T sums, u32 counts).
+  T* part_g = static_cast<T*>(a.part_g);
+  T* part_h = static_cast<T*>(a.part_h);
   for (int i = threadIdx.x; i < a.gb * kCells; i += blockDim.x) {
     const int g2 = i / kCells;
     const int c = i - g2 * kCells;
-    float sg, sh;
+    T sg, sh;
     fold(g2, c, sg, sh);
     const size_t o = (static_cast<size_t>(blockIdx.x) * a.gb + g2) * kCells + c;
-    a.part_g[o] = sg;
-    a.part_h[o] = sh;
+    part_g[o] = sg;
+    part_h[o] = sh;
     a.part_c[o] = cnt[static_cast<size_t>(g2) * kCells + c];
   }
 }
@@ -227,9 +239,12 @@ __global__ void __launch_bounds__(K >= 256 ? 128 : 512, BITS == 4 ? 2 : 1) hist_
 // partial reads are 128-byte coalesced with W independent streams per cell.
 constexpr int kReduceWarps = 16;
 
+template <typename T>
 __global__ void __launch_bounds__(kReduceWarps * 32) reduce_partials_kernel(
     HistArgs a, int nseg, int k_alloc, int d, int max_bin, double* out, const double* parent,
     double* sibling) {
+  const T* part_g = static_cast<const T*>(a.part_g);
+  const T* part_h = static_cast<const T*>(a.part_h);
   const int cells = k_alloc * 32;
   const int group = blockIdx.y;
   const int bin = blockIdx.x;
@@ -244,8 +259,8 @@ __global__ void __launch_bounds__(kReduceWarps * 32) reduce_partials_kernel(
   for (int s = w; s < nseg; s += kReduceWarps) {
     const size_t cta = static_cast<size_t>(s) * a.nblocks + bi;
     const size_t o = (cta * a.gb + gl) * cells + c;
-    sg += static_cast<double>(a.part_g[o]);
-    sh += static_cast<double>(a.part_h[o]);
+    sg += static_cast<double>(part_g[o]);
+    sh += static_cast<double>(part_h[o]);
     sc += a.part_c[o];
   }
   __shared__ double rg[kReduceWarps][32], rh[kReduceWarps][32];
@@ -301,8 +316,11 @@ __device__ __forceinline__ void st_release_sys_u64(double* p, unsigned long long
 // GPU). Phase 1 publishes all its rows, phase 2 sums every rank's rows.
 constexpr int kXBlocks = 32;
 
+template <typename T>
 __global__ void __launch_bounds__(kReduceWarps * 32) reduce_exchange_kernel(
     HistArgs a, int nseg, int k_alloc, int d, int max_bin, int nbins, double* out, PeerHistArgs x) {
+  const T* part_g = static_cast<const T*>(a.part_g);
+  const T* part_h = static_cast<const T*>(a.part_h);
   const int cells = k_alloc * 32;
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
@@ -320,8 +338,8 @@ __global__ void __launch_bounds__(kReduceWarps * 32) reduce_exchange_kernel(
     for (int s = w; s < nseg; s += kReduceWarps) {
       const size_t cta = static_cast<size_t>(s) * a.nblocks + bi;
       const size_t o = (cta * a.gb + gl) * cells + c;
-      sg += static_cast<double>(a.part_g[o]);
-      sh += static_cast<double>(a.part_h[o]);
+      sg += static_cast<double>(part_g[o]);
+      sh += static_cast<double>(part_h[o]);
       sc += a.part_c[o];
     }
     rg[w][lane] = sg;
@@ -417,33 +435,61 @@ void set_max_shared_carveout(const void* func) {
 
 namespace {
 
-template <int BITS, int K>
-void set_smem_attr(int device) {
+template <int BITS, int K, typename T>
+void set_smem_attr_t(int device) {
   static std::once_flag once[64];
   std::call_once(once[device & 63], [] {
-    HBG_CUDA(cudaFuncSetAttribute(hist_kernel<BITS, K, false>,
+    HBG_CUDA(cudaFuncSetAttribute(hist_kernel<BITS, K, false, T>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
-    HBG_CUDA(cudaFuncSetAttribute(hist_kernel<BITS, K, true>,
+    HBG_CUDA(cudaFuncSetAttribute(hist_kernel<BITS, K, true, T>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
-    set_max_shared_carveout(reinterpret_cast<const void*>(hist_kernel<BITS, K, false>));
-    set_max_shared_carveout(reinterpret_cast<const void*>(hist_kernel<BITS, K, true>));
+    set_max_shared_carveout(reinterpret_cast<const void*>(hist_kernel<BITS, K, false, T>));
+    set_max_shared_carveout(reinterpret_cast<const void*>(hist_kernel<BITS, K, true, T>));
   });
 }
 
 template <int BITS, int K>
+void set_smem_attr(int device) {
+  set_smem_attr_t<BITS, K, float>(device);
+  set_smem_attr_t<BITS, K, double>(device);
+}
+
+template <int BITS, int K, typename T>
 int occupancy(int threads, size_t smem, int device) {
   set_smem_attr<BITS, K>(device);
   int blocks = 0;
-  HBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, hist_kernel<BITS, K, false>, threads,
+  HBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, hist_kernel<BITS, K, false, T>, threads,
                                                          smem));
   return std::max(blocks, 1);
 }
 
-int occupancy_for(int bits, int k_alloc, int threads, size_t smem, int device) {
-  if (bits == 4) return occupancy<4, 16>(threads, smem, device);
-  if (k_alloc == 64) return occupancy<8, 64>(threads, smem, device);
-  if (k_alloc == 128) return occupancy<8, 128>(threads, smem, device);
-  return occupancy<8, 256>(threads, smem, device);
+// Occupancy queries are cached per (device, variant, block, smem): the plan
+// is recomputed for every leaf of the per-leaf drop-in, where a driver query
+// per call was a measurable part of a deep leaf's few microseconds.
+int occupancy_for(int bits, int k_alloc, int threads, size_t smem, int device, int acc_bytes) {
+  struct Key {
+    int device, bits, k, threads, acc;
+    size_t smem;
+    int occ;
+  };
+  static std::mutex m;
+  static std::vector<Key> cache;
+  {
+    std::lock_guard<std::mutex> lk(m);
+    for (const Key& c : cache)
+      if (c.device == device && c.bits == bits && c.k == k_alloc && c.threads == threads && c.acc == acc_bytes &&
+          c.smem == smem)
+        return c.occ;
+  }
+  int occ;
+  const bool f64 = acc_bytes == 8;
+  if (bits == 4) occ = f64 ? occupancy<4, 16, double>(threads, smem, device) : occupancy<4, 16, float>(threads, smem, device);
+  else if (k_alloc == 64) occ = f64 ? occupancy<8, 64, double>(threads, smem, device) : occupancy<8, 64, float>(threads, smem, device);
+  else if (k_alloc == 128) occ = f64 ? occupancy<8, 128, double>(threads, smem, device) : occupancy<8, 128, float>(threads, smem, device);
+  else occ = f64 ? occupancy<8, 256, double>(threads, smem, device) : occupancy<8, 256, float>(threads, smem, device);
+  std::lock_guard<std::mutex> lk(m);
+  cache.push_back(Key{device, bits, k_alloc, threads, acc_bytes, smem, occ});
+  return occ;
 }
 
 }  // namespace
@@ -455,7 +501,8 @@ void configure_hist_kernels(int device) {
   set_smem_attr<8, 64>(device);
   set_smem_attr<8, 128>(device);
   set_smem_attr<8, 256>(device);
-  set_max_shared_carveout(reinterpret_cast<const void*>(reduce_partials_kernel));
+  set_max_shared_carveout(reinterpret_cast<const void*>(reduce_partials_kernel<float>));
+  set_max_shared_carveout(reinterpret_cast<const void*>(reduce_partials_kernel<double>));
   set_max_shared_carveout(reinterpret_cast<const void*>(pack_kernel));
   set_max_shared_carveout(reinterpret_cast<const void*>(f64_to_f32_kernel));
 }
@@ -480,12 +527,14 @@ int sm_count(int device) {
 // Leaves up to this many rows take the single-segment direct path.
 constexpr int64_t kDirectRows = 1024;
 
-HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int device, bool allow_direct) {
+HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int device, bool allow_direct,
+                        int acc_bytes) {
   HistPlan p{};
   p.bits = bits;
+  p.acc_bytes = acc_bytes;
   p.k_alloc = bits == 4 ? 16 : (max_bin <= 64 ? 64 : (max_bin <= 128 ? 128 : 256));
   const size_t cells = static_cast<size_t>(p.k_alloc) * 32;
-  const size_t ghw = cells * 8;   // per-warp private {g,h}
+  const size_t ghw = cells * 2 * static_cast<size_t>(acc_bytes);  // per-warp private {g,h}
   const size_t cntw = cells * 4;  // per-group shared counts
   const size_t smem_max = 232448;
   const int max_warps = 16;
@@ -507,7 +556,7 @@ HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int de
   // Small leaves: shrink the CTA (less shared memory to clear and fold) so the
   // grid still spreads over the SMs with >= 4 tiles per warp.
   {
-    const int64_t tile_rows = static_cast<int64_t>(32) * rows_per_lane_of(p.k_alloc);
+    const int64_t tile_rows = static_cast<int64_t>(32) * rows_per_lane_of(p.k_alloc, acc_bytes);
     const int64_t warps_needed =
         std::max<int64_t>(1, (n + 4 * tile_rows - 1) / (4 * tile_rows)) * num_groups;
     const int64_t per_cta = (warps_needed + sm_count(device) - 1) / sm_count(device);
@@ -533,7 +582,7 @@ HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int de
     p.part_values = 0;
     return p;
   }
-  const int occ = occupancy_for(bits, p.k_alloc, p.warps * 32, p.smem, device);
+  const int occ = occupancy_for(bits, p.k_alloc, p.warps * 32, p.smem, device, acc_bytes);
   const int64_t slots = static_cast<int64_t>(sm_count(device)) * occ;  // CTAs per wave
   // Row segments: fill whole waves (1..4) as evenly as possible.
   int64_t nseg = 1;
@@ -549,7 +598,7 @@ HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int de
       }
     }
   }
-  const int64_t min_rows = static_cast<int64_t>(p.wpg) * 32 * rows_per_lane_of(p.k_alloc) * 2;  // >= 2 tiles per warp
+  const int64_t min_rows = static_cast<int64_t>(p.wpg) * 32 * rows_per_lane_of(p.k_alloc, acc_bytes) * 2;  // >= 2 tiles per warp
   nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, (n + min_rows - 1) / min_rows));
   int64_t seg_len = (n + nseg - 1) / nseg;
   seg_len = std::max<int64_t>(32, (seg_len + 31) / 32 * 32);
@@ -560,19 +609,25 @@ HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int de
   return p;
 }
 
-void launch_histogram(const HistPlan& plan, const HistArgs& args, cudaStream_t s) {
+template <typename T>
+void launch_histogram_t(const HistPlan& plan, const HistArgs& args, cudaStream_t s) {
   const dim3 grid(plan.ctas), block(plan.warps * 32);
   const bool ri = args.gh_indexed != 0;
   if (plan.bits == 4) {
-    (ri ? hist_kernel<4, 16, true> : hist_kernel<4, 16, false>)<<<grid, block, plan.smem, s>>>(args);
+    (ri ? hist_kernel<4, 16, true, T> : hist_kernel<4, 16, false, T>)<<<grid, block, plan.smem, s>>>(args);
   } else if (plan.k_alloc == 64) {
-    (ri ? hist_kernel<8, 64, true> : hist_kernel<8, 64, false>)<<<grid, block, plan.smem, s>>>(args);
+    (ri ? hist_kernel<8, 64, true, T> : hist_kernel<8, 64, false, T>)<<<grid, block, plan.smem, s>>>(args);
   } else if (plan.k_alloc == 128) {
-    (ri ? hist_kernel<8, 128, true> : hist_kernel<8, 128, false>)<<<grid, block, plan.smem, s>>>(args);
+    (ri ? hist_kernel<8, 128, true, T> : hist_kernel<8, 128, false, T>)<<<grid, block, plan.smem, s>>>(args);
   } else {
-    (ri ? hist_kernel<8, 256, true> : hist_kernel<8, 256, false>)<<<grid, block, plan.smem, s>>>(args);
+    (ri ? hist_kernel<8, 256, true, T> : hist_kernel<8, 256, false, T>)<<<grid, block, plan.smem, s>>>(args);
   }
   HBG_LAUNCH_CHECK();
+}
+
+void launch_histogram(const HistPlan& plan, const HistArgs& args, cudaStream_t s) {
+  if (plan.acc_bytes == 8) launch_histogram_t<double>(plan, args, s);
+  else launch_histogram_t<float>(plan, args, s);
 }
 
 size_t hist_exchange_doubles(int k_alloc, int max_bin, int num_groups) {
@@ -583,8 +638,8 @@ void launch_reduce_exchange(const HistPlan& plan, const HistArgs& args, int num_
                             double* d_hist, const PeerHistArgs& x, cudaStream_t s) {
   const int nbins = std::min(plan.k_alloc, max_bin);
   const int blocks = std::min(kXBlocks, nbins * args.num_groups);
-  reduce_exchange_kernel<<<blocks, kReduceWarps * 32, 0, s>>>(args, plan.nseg, plan.k_alloc, num_features, max_bin,
-                                                              nbins, d_hist, x);
+  (plan.acc_bytes == 8 ? reduce_exchange_kernel<double> : reduce_exchange_kernel<float>)<<<blocks, kReduceWarps * 32, 0, s>>>(
+      args, plan.nseg, plan.k_alloc, num_features, max_bin, nbins, d_hist, x);
   HBG_LAUNCH_CHECK();
 }
 
@@ -592,8 +647,8 @@ void launch_reduce_partials(const HistPlan& plan, const HistArgs& args, int num_
                             int max_bin, double* d_hist, cudaStream_t s, const double* parent,
                             double* sibling) {
   const dim3 block(kReduceWarps * 32), grid(std::min(plan.k_alloc, max_bin), args.num_groups);
-  reduce_partials_kernel<<<grid, block, 0, s>>>(args, plan.nseg, plan.k_alloc, num_features,
-                                                max_bin, d_hist, parent, sibling);
+  (plan.acc_bytes == 8 ? reduce_partials_kernel<double> : reduce_partials_kernel<float>)<<<grid, block, 0, s>>>(
+      args, plan.nseg, plan.k_alloc, num_features, max_bin, d_hist, parent, sibling);
   HBG_LAUNCH_CHECK();
 }
 

@@ -21,16 +21,17 @@ constexpr int kGatherMaxBlocks = 1184;  // 8 x 148 SMs
 // leaf_g[i] = g[idx[i]] (fp32) and a per-block fp64 partial of the totals.
 // Each block owns a contiguous chunk; the in-block reduction order is fixed,
 // so totals are deterministic for a given count.
-__global__ void gather_kernel(const int32_t* __restrict__ idx, int64_t n, const float* __restrict__ g,
-                              const float* __restrict__ h, float* __restrict__ lg,
-                              float* __restrict__ lh, int64_t chunk, double* __restrict__ partial) {
+template <typename T>
+__global__ void gather_kernel(const int32_t* __restrict__ idx, int64_t n, const T* __restrict__ g,
+                              const T* __restrict__ h, T* __restrict__ lg,
+                              T* __restrict__ lh, int64_t chunk, double* __restrict__ partial) {
   const int64_t b0 = static_cast<int64_t>(blockIdx.x) * chunk;
   const int64_t b1 = min(b0 + chunk, n);
   double sg = 0.0, sh = 0.0;
   for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
     const int32_t r = __ldg(idx + i);
-    const float gv = __ldg(g + r);
-    const float hv = __ldg(h + r);
+    const T gv = __ldg(g + r);
+    const T hv = __ldg(h + r);
     if (lg) lg[i] = gv;
     if (lh) lh[i] = hv;
     sg += gv;
@@ -330,7 +331,7 @@ __global__ void iota_kernel(int32_t* out, int64_t n) {
 }  // namespace
 
 void configure_leaf_kernels() {
-  for (const void* f : {reinterpret_cast<const void*>(gather_kernel),
+  for (const void* f : {reinterpret_cast<const void*>(gather_kernel<float>), reinterpret_cast<const void*>(gather_kernel<double>),
                         reinterpret_cast<const void*>(gather_finalize_kernel),
                         reinterpret_cast<const void*>(subtract_kernel),
                         reinterpret_cast<const void*>(hist_to_bins_kernel),
@@ -384,15 +385,26 @@ size_t gather_scratch_doubles(int64_t n) {
   return static_cast<size_t>(2 * blocks);
 }
 
-void launch_gather(const int32_t* idx, int64_t n, const float* g, const float* h, float* lg,
-                   float* lh, double* totals, double* scratch, cudaStream_t s) {
+template <typename T>
+void launch_gather_t(const int32_t* idx, int64_t n, const T* g, const T* h, T* lg, T* lh, double* totals,
+                     double* scratch, cudaStream_t s) {
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(kGatherMaxBlocks, (n + 2047) / 2048));
   const int64_t chunk = (n + blocks - 1) / blocks;
-  gather_kernel<<<static_cast<unsigned>(blocks), kGatherThreads, 0, s>>>(idx, n, g, h, lg, lh,
-                                                                         std::max<int64_t>(chunk, 1), scratch);
+  gather_kernel<T><<<static_cast<unsigned>(blocks), kGatherThreads, 0, s>>>(idx, n, g, h, lg, lh,
+                                                                            std::max<int64_t>(chunk, 1), scratch);
   HBG_LAUNCH_CHECK();
   gather_finalize_kernel<<<1, 256, 0, s>>>(scratch, static_cast<int>(blocks), totals);
   HBG_LAUNCH_CHECK();
+}
+
+void launch_gather(const int32_t* idx, int64_t n, const float* g, const float* h, float* lg,
+                   float* lh, double* totals, double* scratch, cudaStream_t s) {
+  launch_gather_t<float>(idx, n, g, h, lg, lh, totals, scratch, s);
+}
+
+void launch_gather_f64(const int32_t* idx, int64_t n, const double* g, const double* h, double* lg,
+                       double* lh, double* totals, double* scratch, cudaStream_t s) {
+  launch_gather_t<double>(idx, n, g, h, lg, lh, totals, scratch, s);
 }
 
 void launch_subtract(const double* a, const double* b, double* out, int64_t n, cudaStream_t s) {

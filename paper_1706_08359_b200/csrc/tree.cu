@@ -23,10 +23,11 @@ constexpr int kPartThreads = 512;
 constexpr int kPartItems = 8;
 constexpr int kPartTile = kPartThreads * kPartItems;  // positions per block
 
+template <typename T>
 struct PartArgs {
   const int32_t* rows;
-  const float* g;
-  const float* h;
+  const T* g;  // float (bits32) or double (bits64) leaf-aligned g/h
+  const T* h;
   int64_t n;
   const uint8_t* packed;
   int64_t row_stride;
@@ -107,7 +108,8 @@ __device__ __forceinline__ void block_ranks(unsigned lm, unsigned vm, RankScratc
 
 // Pass 1: side flag per position (bin <= thr goes left, tree.cpp:117-123),
 // per-block left count and fp64 per-side g/h sums.
-__global__ void __launch_bounds__(kPartThreads) partition_count_kernel(PartArgs a) {
+template <typename T>
+__global__ void __launch_bounds__(kPartThreads) partition_count_kernel(PartArgs<T> a) {
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kPartTile;
   double v[4] = {0.0, 0.0, 0.0, 0.0};
   int c = 0;
@@ -192,11 +194,12 @@ __global__ void __launch_bounds__(kScanT) partition_scan_kernel(const int32_t* b
 }
 
 // Pass 3: stable scatter of (row, g, h) into the other buffer, left side first.
+template <typename T>
 __global__ void __launch_bounds__(kPartThreads) partition_scatter_kernel(
-    const int32_t* __restrict__ rows, const float* __restrict__ g, const float* __restrict__ h,
+    const int32_t* __restrict__ rows, const T* __restrict__ g, const T* __restrict__ h,
     const uint8_t* __restrict__ flags, int64_t n, const int64_t* __restrict__ block_off,
-    const int64_t* __restrict__ left_total, int32_t* __restrict__ orow, float* __restrict__ og,
-    float* __restrict__ oh) {
+    const int64_t* __restrict__ left_total, int32_t* __restrict__ orow, T* __restrict__ og,
+    T* __restrict__ oh) {
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kPartTile;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   __shared__ RankScratch rs;
@@ -230,8 +233,9 @@ __global__ void __launch_bounds__(kPartThreads) partition_scatter_kernel(
 
 // Leaves of at most one tile: flags, totals, ranks and the stable scatter in a
 // single CTA (one launch instead of three).
-__global__ void __launch_bounds__(kPartThreads) partition_small_kernel(PartArgs a, int32_t* __restrict__ orow,
-                                                                       float* __restrict__ og, float* __restrict__ oh,
+template <typename T>
+__global__ void __launch_bounds__(kPartThreads) partition_small_kernel(PartArgs<T> a, int32_t* __restrict__ orow,
+                                                                       T* __restrict__ og, T* __restrict__ oh,
                                                                        double* out_totals, int64_t* left_total) {
   __shared__ uint8_t flag[kPartTile];
   __shared__ double sd[4][kPartThreads / 32];
@@ -440,10 +444,13 @@ void configure_tree_kernels() {
   set_max_shared_carveout(reinterpret_cast<const void*>(fixed_scale_kernel));
   set_max_shared_carveout(reinterpret_cast<const void*>(small_hist_atomic_kernel));
   set_max_shared_carveout(reinterpret_cast<const void*>(small_hist_finish_kernel));
-  set_max_shared_carveout(reinterpret_cast<const void*>(partition_small_kernel));
-  set_max_shared_carveout(reinterpret_cast<const void*>(partition_count_kernel));
+  set_max_shared_carveout(reinterpret_cast<const void*>(partition_small_kernel<float>));
+  set_max_shared_carveout(reinterpret_cast<const void*>(partition_count_kernel<float>));
   set_max_shared_carveout(reinterpret_cast<const void*>(partition_scan_kernel));
-  set_max_shared_carveout(reinterpret_cast<const void*>(partition_scatter_kernel));
+  set_max_shared_carveout(reinterpret_cast<const void*>(partition_scatter_kernel<float>));
+  set_max_shared_carveout(reinterpret_cast<const void*>(partition_small_kernel<double>));
+  set_max_shared_carveout(reinterpret_cast<const void*>(partition_count_kernel<double>));
+  set_max_shared_carveout(reinterpret_cast<const void*>(partition_scatter_kernel<double>));
 }
 
 // One split of a leaf's range: flags/counts/totals, scan, scatter. `scratch`
@@ -453,10 +460,12 @@ size_t partition_scratch_bytes(int64_t n) {
   return static_cast<size_t>(n) + 16 + static_cast<size_t>(nb) * (4 + 32 + 8) + 64;
 }
 
-void launch_partition(const int32_t* rows, const float* g, const float* h, int64_t n,
-                      const uint8_t* packed, int64_t row_stride, int feature, int bits, int thr,
-                      int32_t* orow, float* og, float* oh, void* scratch, double* d_totals,
-                      int64_t* d_left, cudaStream_t s) {
+namespace {
+
+template <typename T>
+void launch_partition_t(const int32_t* rows, const T* g, const T* h, int64_t n, const uint8_t* packed,
+                        int64_t row_stride, int feature, int bits, int thr, int32_t* orow, T* og, T* oh,
+                        void* scratch, double* d_totals, int64_t* d_left, cudaStream_t s) {
   const int64_t nb = std::max<int64_t>(1, (n + kPartTile - 1) / kPartTile);
   uint8_t* p = static_cast<uint8_t*>(scratch);
   uint8_t* flags = p;
@@ -466,7 +475,7 @@ void launch_partition(const int32_t* rows, const float* g, const float* h, int64
   int64_t* block_off = reinterpret_cast<int64_t*>(p);
   p += static_cast<size_t>(nb) * 8;
   int32_t* block_left = reinterpret_cast<int32_t*>(p);
-  PartArgs a{};
+  PartArgs<T> a{};
   a.rows = rows;
   a.g = g;
   a.h = h;
@@ -488,18 +497,36 @@ void launch_partition(const int32_t* rows, const float* g, const float* h, int64
   a.block_left = block_left;
   a.block_sums = block_sums;
   if (n <= kPartTile) {
-    partition_small_kernel<<<1, kPartThreads, 0, s>>>(a, orow, og, oh, d_totals, d_left);
+    partition_small_kernel<T><<<1, kPartThreads, 0, s>>>(a, orow, og, oh, d_totals, d_left);
     HBG_LAUNCH_CHECK();
     return;
   }
-  partition_count_kernel<<<static_cast<unsigned>(nb), kPartThreads, 0, s>>>(a);
+  partition_count_kernel<T><<<static_cast<unsigned>(nb), kPartThreads, 0, s>>>(a);
   HBG_LAUNCH_CHECK();
   partition_scan_kernel<<<1, kScanT, 0, s>>>(block_left, block_sums, static_cast<int>(nb), block_off,
                                            d_totals, d_left);
   HBG_LAUNCH_CHECK();
-  partition_scatter_kernel<<<static_cast<unsigned>(nb), kPartThreads, 0, s>>>(
+  partition_scatter_kernel<T><<<static_cast<unsigned>(nb), kPartThreads, 0, s>>>(
       rows, g, h, flags, n, block_off, d_left, orow, og, oh);
   HBG_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+void launch_partition(const int32_t* rows, const float* g, const float* h, int64_t n,
+                      const uint8_t* packed, int64_t row_stride, int feature, int bits, int thr,
+                      int32_t* orow, float* og, float* oh, void* scratch, double* d_totals,
+                      int64_t* d_left, cudaStream_t s) {
+  launch_partition_t<float>(rows, g, h, n, packed, row_stride, feature, bits, thr, orow, og, oh, scratch,
+                            d_totals, d_left, s);
+}
+
+void launch_partition_f64(const int32_t* rows, const double* g, const double* h, int64_t n,
+                          const uint8_t* packed, int64_t row_stride, int feature, int bits, int thr,
+                          int32_t* orow, double* og, double* oh, void* scratch, double* d_totals,
+                          int64_t* d_left, cudaStream_t s) {
+  launch_partition_t<double>(rows, g, h, n, packed, row_stride, feature, bits, thr, orow, og, oh, scratch,
+                             d_totals, d_left, s);
 }
 
 }  // namespace hbg

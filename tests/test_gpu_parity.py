@@ -420,25 +420,33 @@ def rows_of_node(cols, nodes, j):
 
 
 def exact_gain(cols, g, h, rows, f, b, lam):
-    """split_gain (tree.cpp:66-74) of (f, b) on `rows`, in float64 from the fp64 inputs."""
+    """split_gain (tree.cpp:66-74) of (f, b) on `rows`, from exactly-rounded
+    sums (math.fsum) of the fp64 inputs."""
+    import math
+
     left = cols[f, rows] <= b
-    lg, lh = g[rows][left].sum(), h[rows][left].sum()
-    G, H = g[rows].sum(), h[rows].sum()
+    gr, hr = g[rows], h[rows]
+    lg, lh = math.fsum(gr[left]), math.fsum(hr[left])
+    G, H = math.fsum(gr), math.fsum(hr)
     rg, rh = G - lg, H - lh
     if lh + lam <= 0 or rh + lam <= 0 or H + lam <= 0:
         return 0.0
     return lg * lg / (lh + lam) + rg * rg / (rh + lam) - (lg + rg) ** 2 / (lh + rh + lam)
 
 
-def _assert_same_tree(log, nodes, want_log, want_nodes, cols=None, g=None, h=None, lam=0.0):
+def _assert_same_tree(log, nodes, want_log, want_nodes, cols=None, g=None, h=None, lam=0.0, tie_tol=1e-6):
     """The GPU tree equals the reference's until the first near-tie.
 
     Identical (feature, threshold, counts) step by step. A divergence is only
-    accepted (when cols/g/h are given) if it is a near-tie: the reference's
-    split is optimal in fp64 and ours has the same fp64 gain to 1e-6 relative
-    — fp32 inputs cannot order candidates closer than that (the reference's
-    own bits32 mode flips the same ones). Returns the number of identical
-    leading steps (== len(want_log) when the trees are identical)."""
+    accepted (when cols/g/h are given) if it is a near-tie: the two choices'
+    gains, each evaluated with exactly-rounded sums (math.fsum) over its
+    leaf's rows from the fp64 inputs, agree to `tie_tol` relative. bits32
+    trees use 1e-6 — fp32 inputs cannot order candidates closer than that
+    (the reference's own bits32 mode flips the same ones); bits64 trees use
+    1e-12 — what is left there are true ties, typically two features that cut
+    a leaf into the same two row sets, ordered by fp64 rounding alone.
+    Returns the number of identical leading steps (== len(want_log) when the
+    trees are identical)."""
     n = min(len(log), len(want_log))
     i = 0
     while i < n:
@@ -459,12 +467,14 @@ def _assert_same_tree(log, nodes, want_log, want_nodes, cols=None, g=None, h=Non
         return i
     assert cols is not None, ("trees diverge at split", i, log[i:i + 1], want_log[i:i + 1])
     assert i < n, "one tree stopped early without a divergence"
-    j = int(np.nonzero(nodes["left"] == 2 * i + 1)[0][0])
-    rows = rows_of_node(cols, nodes, j)
-    ours = exact_gain(cols, g, h, rows, int(log["feature"][i]), int(log["threshold_bin"][i]), lam)
-    ref = float(want_log["gain"][i])
-    assert ours <= ref * (1 + 1e-12) + 1e-12, (ours, ref)  # the reference's choice is the fp64 optimum
-    assert ref - ours <= 1e-6 * max(1.0, abs(ref)), ("not a near-tie", i, ours, ref)
+    # both leaves exist in both trees with the same ancestry (every earlier split agreed)
+    jo = int(np.nonzero(nodes["left"] == 2 * i + 1)[0][0])
+    jr = int(np.nonzero(np.asarray(want_nodes["left"]) == 2 * i + 1)[0][0])
+    ours = exact_gain(cols, g, h, rows_of_node(cols, nodes, jo), int(log["feature"][i]),
+                      int(log["threshold_bin"][i]), lam)
+    ref = exact_gain(cols, g, h, rows_of_node(cols, nodes, jr), int(want_log["feature"][i]),
+                     int(want_log["threshold_bin"][i]), lam)
+    assert abs(ref - ours) <= tie_tol * max(1.0, abs(ref)), ("not a near-tie", i, ours, ref)
     return i
 
 
