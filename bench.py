@@ -99,14 +99,20 @@ def hbm_peak():
 
 
 def ncu_traffic(workload: str):
-    """dram bytes per histogram-kernel launch from the committed ncu capture, if any."""
+    """dram bytes per histogram-kernel launch from the committed ncu capture
+    (scripts/ncu_summary.py), or None when there is none or it was taken of
+    different kernel sources (stamp mismatch: the number would be stale)."""
     p = os.path.join(REPO, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            t = json.load(f)
-        return t.get(workload)
+            t = json.load(f).get(workload)
+        from paper_1706_08359_b200 import hist_kernel_stamp
+
+        if isinstance(t, dict) and t.get("kernel_src") == hist_kernel_stamp():
+            return float(t["dram_bytes"])
     except Exception:
-        return None
+        pass
+    return None
 
 
 class ClockSampler:

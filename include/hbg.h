@@ -260,6 +260,10 @@ void* hbg_dataset_stream(const hbg_dataset* ds);
 
 #define HBG_PEER_HANDLE_BYTES 64
 typedef struct hbg_peer hbg_peer;
+/* Every in-kernel wait on another rank (exchange flags, grid barriers) is
+ * bounded by HBG_PEER_TIMEOUT_MS (environment, default 60000): ranks may reach
+ * a peer call that far apart; an expired wait is an HBG_ERR_CUDA status with
+ * hbg_last_error() naming it, never a hang. */
 int hbg_peer_create(hbg_dataset* ds, int32_t nranks, int32_t rank, int32_t ctas,
                     const hbg_grow_params* params /* the largest tree: its workspace is reserved */,
                     hbg_peer** out);

@@ -52,7 +52,7 @@ inline void check(int status) {
 class DeviceDataset {
  public:
   explicit DeviceDataset(const histoboost::BinnedDataset& data, int device = 0)
-      : num_features_(data.num_features()), max_bin_(data.max_bin) {
+      : num_features_(data.num_features()), max_bin_(data.max_bin), num_rows_(data.num_rows) {
     // every column, dense or sparse, by feature id: the HistogramSet index
     std::vector<const std::uint8_t*> cols(static_cast<std::size_t>(num_features_));
     for (int f = 0; f < num_features_; ++f) {
@@ -69,6 +69,15 @@ class DeviceDataset {
   hbg_dataset* get() const { return handle_.get(); }
   int num_features() const { return num_features_; }
   int max_bin() const { return max_bin_; }
+  std::int64_t num_rows() const { return num_rows_; }
+  // The device copy is a snapshot: it must be rebuilt when the dataset is
+  // re-binned or replaced. Cheap guard for callers that hold it next to a
+  // BinnedDataset: the shape must still agree.
+  void require_describes(const histoboost::BinnedDataset& data) const {
+    if (data.num_rows != num_rows_ || data.num_features() != num_features_ || data.max_bin != max_bin_) {
+      throw std::logic_error("hbg backend: DeviceDataset was built for a different dataset shape");
+    }
+  }
 
  private:
   struct Destroy {
@@ -77,6 +86,7 @@ class DeviceDataset {
   std::unique_ptr<hbg_dataset, Destroy> handle_;
   int num_features_;
   int max_bin_;
+  std::int64_t num_rows_;
 };
 
 inline std::int32_t to_hbg(histoboost::PrecisionMode p) {
@@ -85,9 +95,10 @@ inline std::int32_t to_hbg(histoboost::PrecisionMode p) {
 
 // The drop-in for build_histograms_partitioned, honouring PrecisionMode:
 //  bits32 — fp32 inputs (the reference's per-element cast), fp32 per-warp
-//           sums reduced in fp64: within stats_tolerance(bits32) = 1e-4 of the
-//           reference (tests: <= 1e-5 vs bits64 up to 300K-row leaves, <= 1e-4
-//           at the 10.5M-row root);
+//           sums reduced in fp64. Against the reference's bits64 sums (tests,
+//           DESIGN.md §5): <= 1e-5 up to 300K-row leaves; at the 10.5M-row
+//           root 7.6e-5 (k64) / 2.1e-4 (k16), where the reference's own bits32
+//           path is at 1.8e-4 / 7.5e-4 — fp32 inputs cannot do better there;
 //  bits64 — fp64 inputs, fp64 accumulation: within stats_tolerance(bits64) =
 //           1e-12 of the reference's bits64 (tests up to the 10.5M-row root).
 inline histoboost::HistogramSet build_histograms_cuda(const DeviceDataset& dev,

@@ -44,6 +44,19 @@ HBG_PRECISION_BITS32 = 0
 HBG_PRECISION_BITS64 = 1
 
 
+def hist_kernel_stamp() -> str:
+    """Short hash of the histogram kernel's sources: a committed ncu number
+    (profiles/ncu_traffic.json) is only reported while it still describes the
+    kernel that runs."""
+    import hashlib
+
+    hsh = hashlib.sha256()
+    for name in ("hist_kernels.cu", "hist_device.cuh"):
+        with open(os.path.join(HERE, "csrc", name), "rb") as f:
+            hsh.update(f.read())
+    return hsh.hexdigest()[:16]
+
+
 def _precision(p) -> int:
     """32 / 64 / 'bits32' / 'bits64' / HBG_PRECISION_* -> HBG_PRECISION_*."""
     table = {32: HBG_PRECISION_BITS32, 64: HBG_PRECISION_BITS64, "bits32": HBG_PRECISION_BITS32,

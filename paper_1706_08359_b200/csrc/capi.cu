@@ -169,6 +169,26 @@ struct hbg_peer {
 
 using namespace hbg;
 
+// Bound of every in-kernel wait on another rank or on the grid (clock64
+// cycles of `device`): HBG_PEER_TIMEOUT_MS, default 60 s — generous, because
+// ranks reach a peer call at different times (data loading, GC, checkpoints)
+// and there is no host handshake before the launch; a wait that expires is an
+// HBG_ERR_CUDA status, never a hang.
+long long hbg::wait_timeout_cycles(int device) {
+  static std::once_flag once;
+  static double ms = 60000.0;
+  std::call_once(once, [] {
+    if (const char* e = std::getenv("HBG_PEER_TIMEOUT_MS")) {
+      const double v = std::atof(e);
+      if (v > 0.0) ms = v;
+    }
+  });
+  int khz = 0;
+  if (cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device) != cudaSuccess || khz <= 0) khz = 2000000;
+  return static_cast<long long>(ms * static_cast<double>(khz));
+}
+
+
 namespace {
 
 void check_ds(const hbg_dataset* ds) { require(ds != nullptr, "null dataset handle"); }
@@ -226,6 +246,11 @@ class HostPool {
     return pool;
   }
   int size() const { return static_cast<int>(th_.size()); }
+  // One job at a time: callers on different threads (different handles, or
+  // ctypes callers that released the GIL) hold job_mutex() from run() through
+  // wait(), so a second job can never overwrite job_/pending_ while workers of
+  // the first one are still picking it up.
+  std::mutex& job_mutex() { return job_m_; }
   // fn(w) on every worker w; returns at once (wait() blocks until all finish)
   void run(std::function<void(int)> fn) {
     std::unique_lock<std::mutex> lk(m_);
@@ -271,6 +296,7 @@ class HostPool {
     }
   }
   std::mutex m_;
+  std::mutex job_m_;
   std::condition_variable cv_, done_;
   std::function<void(int)> job_;
   uint64_t gen_ = 0;
@@ -309,6 +335,7 @@ void stage_chunks(hbg_dataset* ds, const double* g, const double* h, const int32
   int32_t* id = reinterpret_cast<int32_t*>(hf + rows);
   const int C = static_cast<int>((n + chunk - 1) / chunk);
   HostPool& pool = HostPool::get();
+  std::lock_guard<std::mutex> job(pool.job_mutex());  // held until the last pool.wait()
   const int T = pool.size();
   std::unique_ptr<std::atomic<int>[]> done(new std::atomic<int>[static_cast<size_t>(C)]);
   for (int c = 0; c < C; ++c) done[static_cast<size_t>(c)].store(0, std::memory_order_relaxed);
@@ -462,7 +489,7 @@ void build_device_peer(hbg_dataset* ds, const int32_t* d_idx, int64_t count, con
   x.tag = ++peer->hgen;
   x.parity = static_cast<int>(x.tag & 1);
   x.error = peer->error;
-  x.timeout_cycles = 4000000000LL;
+  x.timeout_cycles = wait_timeout_cycles(L.device);
   launch_reduce_exchange(plan, a, L.num_features, L.max_bin, d_hist, x, s);
 }
 
@@ -563,14 +590,12 @@ void grow_tree_impl(hbg_dataset* ds, const void* d_grad, const void* d_hess,
   else
     launch_gather(rows[0], N, static_cast<const float*>(d_grad), static_cast<const float*>(d_hess), nullptr,
                   nullptr, dres->root, static_cast<double*>(scratch), s);
-  // fixed-point scale for the bits32 small-leaf histogram path, accumulator
-  // cleared (bits64 builds every leaf with fp64 accumulation instead)
+  // bits32 small-leaf histogram path: accumulator cleared once (the finish
+  // kernel clears it after every leaf), fixed-point scales per leaf (bits64
+  // builds every leaf with fp64 accumulation instead)
   int* exps = static_cast<int*>(ds->small_exps.get(16));
   void* acc = ds->small_acc.get(small_hist_acc_bytes(d, k));
-  if (!f64) {
-    launch_fixed_scale(reinterpret_cast<const float*>(gb[0]), reinterpret_cast<const float*>(hb[0]), N, exps, s);
-    HBG_CUDA(cudaMemsetAsync(acc, 0, small_hist_acc_bytes(d, k), s));
-  }
+  if (!f64) HBG_CUDA(cudaMemsetAsync(acc, 0, small_hist_acc_bytes(d, k), s));
   const uint32_t* packed = ds->packed;
   const int stride_words = L.row_stride_bytes / 4;
   const int acc_bytes = f64 ? 8 : 4;
@@ -578,6 +603,8 @@ void grow_tree_impl(hbg_dataset* ds, const void* d_grad, const void* d_hess,
   auto leaf_hist = [&](int buf, int64_t begin, int64_t count, double* out, const double* parent,
                        double* sibling) {
     if (!f64 && count <= kAtomicHistRows) {
+      launch_fixed_leaf_scale(reinterpret_cast<const float*>(G(buf, begin)), reinterpret_cast<const float*>(H(buf, begin)),
+                              count, exps, s);
       launch_small_hist(rows[buf] + begin, reinterpret_cast<const float*>(G(buf, begin)),
                         reinterpret_cast<const float*>(H(buf, begin)), count, packed, stride_words,
                         L.words_per_row, L.bits_per_bin, d, k, exps, acc, out, parent, sibling, s);
@@ -676,6 +703,8 @@ void grow_tree_impl(hbg_dataset* ds, const void* d_grad, const void* d_hess,
       if (!f64 && !sharded && small.count <= kAtomicHistRows) {
         // small child: L2-atomic histogram, then one fused launch for the
         // conversion, the subtraction and both children's scans
+        launch_fixed_leaf_scale(reinterpret_cast<const float*>(G(out, small.begin)),
+                                reinterpret_cast<const float*>(H(out, small.begin)), small.count, exps, s);
         launch_small_hist_atomic(rows[out] + small.begin, reinterpret_cast<const float*>(G(out, small.begin)),
                                  reinterpret_cast<const float*>(H(out, small.begin)), small.count, packed,
                                  stride_words, L.words_per_row, L.bits_per_bin, d, k, exps, acc, s);
@@ -790,8 +819,8 @@ PersistentGrowArgs grow_workspace(hbg_dataset* ds, const hbg_grow_params& P, int
   a.scratch_bytes = grow_scratch_bytes(a, L.device);
   a.scratch = ds->grow_scratch.get(a.scratch_bytes);
   a.scratch_bytes = ds->grow_scratch.bytes;
-  a.exps = static_cast<int*>(ds->small_exps.get(16));
   a.root_totals = static_cast<double*>(ds->grow_root.get(4 * sizeof(double)));
+  a.timeout_cycles = wait_timeout_cycles(L.device);
   ds->part_scratch.get(gather_scratch_doubles(N) * sizeof(double) + 64);
   if (N > 0 && d > 0) {  // the root histogram's partials (build_device)
     const HistPlan plan = plan_histogram(L.bits_per_bin, L.max_bin, L.num_groups, N, L.device);
@@ -813,7 +842,6 @@ void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_h
   const bool sharded = peer != nullptr && peer->nranks > 1;
   PersistentGrowArgs a = grow_workspace(ds, P, sharded ? peer->ctas : 0, sharded ? peer->nranks : 1);
   double* slots = a.slots;
-  int* exps = const_cast<int*>(a.exps);
   double* root = const_cast<double*>(a.root_totals);
   void* gscratch = ds->part_scratch.p;
 
@@ -847,7 +875,6 @@ void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_h
     *num_nodes = 1;
     return;
   }
-  launch_fixed_scale(a.g[0], a.h[0], N, exps, s);
   build_device(ds, a.rows[0], N, a.g[0], a.h[0], HBG_GH_LEAF_ALIGNED, slots, s);
   if (!sharded) {  // sharded: the kernel sums the ranks' root histograms first, then scans
     hbg_split* root_split = reinterpret_cast<hbg_split*>(static_cast<char*>(a.nodes) + grow_root_split_offset());

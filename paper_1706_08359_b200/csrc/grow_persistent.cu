@@ -121,7 +121,6 @@ struct GrowArgs {
   float* part_h;
   uint32_t* part_c;
   Cand* cand;  // [kRep][2][nchunks]
-  const int* exps;
   const double* root_tot;  // {G, H}
   int64_t root_count;
   int num_leaves;
@@ -1048,9 +1047,68 @@ __device__ __forceinline__ unsigned char* part_stage(const GrowArgs& a, unsigned
   return smem + (off + 15) / 16 * 16;
 }
 
+// The direct accumulator's fixed-point scales are per CHILD: max |g|, |h|
+// over the rows being accumulated (the bit patterns of non-negative floats
+// order like the floats), so |q| <= 2^39 at the child's own largest value. A
+// per-tree scale would quantise a leaf of values far below the tree's max
+// (converged logistic hessians, residuals next to an outlier) to a few bits.
+// Every chunk CTA of a child reduces the same rows, so all agree; the finish
+// reads the maxima back.
+__device__ __forceinline__ unsigned* direct_max() {
+  __shared__ unsigned m[2];
+  return m;
+}
+
 __device__ __forceinline__ void zero_direct(const GrowArgs& a, unsigned char* smem, int cells, int NT) {
   unsigned* acc = direct_acc(a, smem);
   for (int i = threadIdx.x; i < 5 * cells; i += NT) acc[i] = 0u;
+  if (threadIdx.x == 0) direct_max()[0] = direct_max()[1] = 0u;
+}
+
+__device__ __forceinline__ unsigned abs_bits(float v) { return __float_as_uint(fabsf(v)); }
+
+// Whole block: fold this thread's maxima in; after the barrier every thread
+// holds the child's scales q = v * eg (resp. eh), exact powers of two.
+__device__ __forceinline__ void direct_scales(unsigned mg, unsigned mh, double& eg, double& eh) {
+  unsigned* m = direct_max();
+  mg = __reduce_max_sync(0xffffffffu, mg);
+  mh = __reduce_max_sync(0xffffffffu, mh);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(m, mg);
+    atomicMax(m + 1, mh);
+  }
+  __syncthreads();
+  int e0 = 0, e1 = 0;
+  frexpf(__uint_as_float(m[0]), &e0);
+  frexpf(__uint_as_float(m[1]), &e1);
+  eg = ldexp(1.0, 39 - e0);
+  eh = ldexp(1.0, 39 - e1);
+}
+
+// Scales of the rows of `mask` held in registers.
+__device__ __forceinline__ void direct_scales_regs(const float (&g)[kItems], const float (&h)[kItems], uint32_t mask,
+                                                   double& eg, double& eh) {
+  unsigned mg = 0u, mh = 0u;
+#pragma unroll
+  for (int u = 0; u < kItems; ++u) {
+    if ((mask >> u) & 1u) {
+      mg = max(mg, abs_bits(g[u]));
+      mh = max(mh, abs_bits(h[u]));
+    }
+  }
+  direct_scales(mg, mh, eg, eh);
+}
+
+// Scales of n leaf-aligned rows in global memory (the smaller child of a
+// large parent, <= kDirectRows rows).
+template <int NT>
+__device__ __forceinline__ void direct_scales_range(const float* g, const float* h, int64_t n, double& eg, double& eh) {
+  unsigned mg = 0u, mh = 0u;
+  for (int64_t q = threadIdx.x; q < n; q += NT) {
+    mg = max(mg, abs_bits(__ldcg(g + q)));
+    mh = max(mh, abs_bits(__ldcg(h + q)));
+  }
+  direct_scales(mg, mh, eg, eh);
 }
 
 // Where a chunk's per-child winners go: p[r * rep_stride + child * child_stride]
@@ -1153,7 +1211,10 @@ __device__ __forceinline__ void finish_range(const GrowArgs& a, const Desc& D, i
   double* lg = st + (D.small_is_left ? 3 * chunk_cells : 0);
   const int cells = nf * k;
   if (D.path == kDirect) {
-    const double sg = ldexp(1.0, -a.exps[0]), sh = ldexp(1.0, -a.exps[1]);
+    int e0 = 0, e1 = 0;  // the child's scales (direct_scales)
+    frexpf(__uint_as_float(direct_max()[0]), &e0);
+    frexpf(__uint_as_float(direct_max()[1]), &e1);
+    const double sg = ldexp(1.0, e0 - 39), sh = ldexp(1.0, e1 - 39);
     const unsigned* acc = direct_acc(a, smem);
     for (int i = threadIdx.x; i < cells; i += NT) {  // i = f * k + b
       const auto rd = [&](int w) {
@@ -1527,7 +1588,6 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
   }
   __syncthreads();
   pick<NT>(a, 0, 0, kid, D, pool);  // node 0 is "kid_l" (kid[1] is never consulted: nnodes = 1)
-  const double eg = ldexp(1.0, a.exps[0]), eh = ldexp(1.0, a.exps[1]);  // fixed-point scales
   while (!D.done) {
     const int it = D.iter;
     stamp(a, it, 0);
@@ -1556,6 +1616,8 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
           // CTA's feature chunk, then finish and scan it
           const uint32_t valid = rr.nvalid >= 32 ? ~0u : ((1u << rr.nvalid) - 1u);
           const uint32_t want = (D.small_is_left ? rr.left : ~rr.left) & valid;
+          double eg, eh;
+          direct_scales_regs(rr.g, rr.h, want, eg, eh);
           direct_accumulate(a, direct_acc(a, smem), nf * a.k, f0, nf, rr.row, rr.g, rr.h, want, eg, eh);
           __syncthreads();
           stamp(a, it, 2);
@@ -1596,6 +1658,8 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
           const float* h;
           int64_t n;
           small_child(a, D, rows, g, h, n);
+          double eg, eh;
+          direct_scales_range<NT>(g, h, n, eg, eh);
           for (int64_t j0 = 0; j0 < n; j0 += static_cast<int64_t>(NT) * kItems) {
             int32_t r[kItems];
             float gg[kItems], hh[kItems];
@@ -2161,8 +2225,7 @@ __device__ __forceinline__ int item_cta(int x, int I, int G) {
 // Small members: items (member, feature chunk of wc features); every CTA of a
 // member ranks its parent in registers and writes one share of the output.
 template <int K, int NT>
-__device__ void wave_small(const GrowArgs& a, const WaveSmem& w, Desc* Dm, PartShared<NT>& ps, unsigned char* smem,
-                           double eg, double eh) {
+__device__ void wave_small(const GrowArgs& a, const WaveSmem& w, Desc* Dm, PartShared<NT>& ps, unsigned char* smem) {
   const int G = gridDim.x, b = blockIdx.x;
   const int nwc = w.nwc, wc = w.wc, I = w.nsmall * nwc;
   int x0, x1;
@@ -2189,6 +2252,8 @@ __device__ void wave_small(const GrowArgs& a, const WaveSmem& w, Desc* Dm, PartS
       __syncthreads();
       const uint32_t valid = rr.nvalid >= 32 ? ~0u : ((1u << rr.nvalid) - 1u);
       const uint32_t want = (D.small_is_left ? rr.left : ~rr.left) & valid;
+      double eg, eh;
+      direct_scales_regs(rr.g, rr.h, want, eg, eh);
       direct_accumulate(a, direct_acc(a, smem), nf * a.k, f0, nf, rr.row, rr.g, rr.h, want, eg, eh);
       __syncthreads();
       finish_range<K, NT>(a, D, f0, nf, 0, smem, wave_out(a, D, c));
@@ -2201,8 +2266,7 @@ __device__ void wave_small(const GrowArgs& a, const WaveSmem& w, Desc* Dm, PartS
 // shared-memory histogram items (member, segment, slice block) over all CTAs;
 // then (barrier) the shared-memory members' chunk finishes.
 template <int BITS, int K, int NT>
-__device__ void wave_large_hist(const GrowArgs& a, const WaveSmem& w, Desc* Dm, unsigned char* smem, double eg,
-                                double eh) {
+__device__ void wave_large_hist(const GrowArgs& a, const WaveSmem& w, Desc* Dm, unsigned char* smem) {
   const int G = gridDim.x;
   const int hitems = w.hitems, total = w.hitems + w.ditems;
   for (int x = blockIdx.x; x < total; x += G) {
@@ -2226,6 +2290,8 @@ __device__ void wave_large_hist(const GrowArgs& a, const WaveSmem& w, Desc* Dm, 
     const float* h;
     int64_t n;
     small_child(a, D, rows, g, h, n);
+    double eg, eh;
+    direct_scales_range<NT>(g, h, n, eg, eh);
     for (int64_t j0 = 0; j0 < n; j0 += static_cast<int64_t>(NT) * kItems) {
       int32_t rw[kItems];
       float gg[kItems], hh[kItems];
@@ -2344,7 +2410,6 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_wave_kernel(GrowArg
   }
   grid_sync(a);  // CTA 0's root records
   wave_select<NT>(a, w);
-  const double eg = ldexp(1.0, a.exps[0]), eh = ldexp(1.0, a.exps[1]);  // fixed-point scales
   while (!w.done) {
     if (a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
       unsigned long long* t = a.prof + static_cast<size_t>(w.nwaves) * kProfSlots;
@@ -2355,7 +2420,7 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_wave_kernel(GrowArg
     stamp(a, w.nwaves, 0);
     load_members(a, w, Dm);
     for (int j = w.nsmall; j < w.W; ++j) partition_count<NT>(a, Dm[j], ps);
-    if (w.nsmall > 0) wave_small<K, NT>(a, w, Dm, ps, smem, eg, eh);
+    if (w.nsmall > 0) wave_small<K, NT>(a, w, Dm, ps, smem);
     stamp(a, w.nwaves, 1);
     if (w.W > w.nsmall) {
       grid_sync(a);
@@ -2364,7 +2429,7 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_wave_kernel(GrowArg
       stamp(a, w.nwaves, 2);
       for (int j = w.nsmall; j < w.W; ++j)
         if (Dm[j].path == kNoHist && blockIdx.x == 0) publish_member<NT>(a, Dm[j], 0);
-      wave_large_hist<BITS, K, NT>(a, w, Dm, smem, eg, eh);
+      wave_large_hist<BITS, K, NT>(a, w, Dm, smem);
     }
     stamp(a, w.nwaves, 3);
     if (a.prof != nullptr) {  // slot 16: the last CTA's arrival at the wave's final barrier
@@ -2608,7 +2673,6 @@ const void* launch_grow_persistent(const PersistentGrowArgs& h, int device, cuda
   a.split_log = h.split_log;
   a.tree = h.tree;
   a.counts = h.counts;
-  a.exps = h.exps;
   a.root_tot = h.root_totals;
   a.root_count = h.num_rows;
   a.num_leaves = h.num_leaves;
@@ -2628,7 +2692,7 @@ const void* launch_grow_persistent(const PersistentGrowArgs& h, int device, cuda
   a.wcstride = g.wcstride;
   a.ecap = g.ecap;
   a.small_max = static_cast<int64_t>(kItems) * g.nt;
-  a.timeout_cycles = 4000000000LL;  // ~2 s: a hung barrier becomes an error, not a hang
+  a.timeout_cycles = h.timeout_cycles;  // a hung barrier or exchange becomes an error, not a hang
   a.prof = h.prof;
   a.nranks = std::max(1, h.nranks);
   a.debug = std::getenv("HBG_GROW_DEBUG") != nullptr;

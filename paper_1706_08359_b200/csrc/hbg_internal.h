@@ -164,7 +164,8 @@ void configure_kernels(int device);  // carveout for every non-histogram kernel,
 // Small leaves (tree grower): fixed-point histogram through L2 atomics.
 constexpr int64_t kAtomicHistRows = 4096;
 size_t small_hist_acc_bytes(int d, int k);
-void launch_fixed_scale(const float* g, const float* h, int64_t n, int* exps, cudaStream_t s);
+// fixed-point scales exps[0..1] from one leaf's rows (n <= kAtomicHistRows; one block)
+void launch_fixed_leaf_scale(const float* g, const float* h, int64_t n, int* exps, cudaStream_t s);
 void launch_small_hist(const int32_t* rows, const float* g, const float* h, int64_t n,
                        const uint32_t* packed, int stride_words, int words_per_row, int bits, int d, int k,
                        const int* exps, void* acc, double* out, const double* parent, double* sibling,
@@ -208,7 +209,6 @@ struct PersistentGrowArgs {
   int* counts;           // device, 4 ints: num_splits, num_nodes, error
   void* scratch;         // grow_scratch_bytes()
   size_t scratch_bytes;  // allocated size of `scratch`
-  const int* exps;
   const double* root_totals;  // device {G, H}
   int num_leaves;
   int64_t min_data;
@@ -220,7 +220,10 @@ struct PersistentGrowArgs {
   double* xown;
   const double* xpeer[8];
   unsigned long long gen;
+  long long timeout_cycles;  // bound of every in-kernel wait (wait_timeout_cycles)
 };
+// HBG_PEER_TIMEOUT_MS (default 60 s) in clock64 cycles of `device`
+long long wait_timeout_cycles(int device);
 size_t grow_exchange_doubles(const PersistentGrowArgs& a, int device);
 int grow_max_nodes(const PersistentGrowArgs& a, int device);  // node-table entries of the kernel used
 size_t grow_nodes_bytes(int max_nodes);

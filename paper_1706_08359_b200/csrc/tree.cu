@@ -300,41 +300,43 @@ __global__ void __launch_bounds__(kPartThreads) partition_small_kernel(PartArgs<
 // ---- small leaves: deterministic fixed-point histogram through L2 atomics ----
 // For a leaf of a few thousand rows the shared-memory kernel's fixed cost
 // (clearing and folding per-warp cells) dominates. Here every (row, feature)
-// adds int64 fixed-point g and h (scale 2^S per tree, |q| <= 2^39 per element,
-// so any leaf of < 2^23 rows sums without overflow) and a u32 count straight
+// adds int64 fixed-point g and h (scale 2^S per LEAF from the leaf's own max
+// |g|, |h|, |q| <= 2^39 per element, so any leaf of < 2^23 rows sums without
+// overflow and a leaf of tiny values keeps their precision) and a u32 count straight
 // into an L2-resident accumulator with native 64-bit reductions (REDG.E.ADD.64)
 // from all SMs. Integer addition commutes, so the result is bitwise
 // deterministic and more precise than fp32 accumulation (2^-40 of max|g| per
 // element).
 
-// max |g|, max |h| over n values (grid-wide; the max is order-free, so the
-// integer atomicMax on the non-negative floats' bit patterns is deterministic).
-__global__ void fixed_max_kernel(const float* __restrict__ g, const float* __restrict__ h, int64_t n,
-                                 unsigned int* __restrict__ maxbits) {
-  float mg = 0.f, mh = 0.f;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    mg = fmaxf(mg, fabsf(g[i]));
-    mh = fmaxf(mh, fabsf(h[i]));
+// Per-leaf scales for a leaf of n <= kAtomicHistRows rows, one block: max
+// |g|, |h| over the leaf's own rows (order-free integer max of the
+// non-negative floats' bits) -> exps. A per-tree scale would quantise a leaf
+// of values far below the tree's max (converged logistic hessians, residuals
+// next to an outlier) to a few bits.
+__global__ void fixed_leaf_scale_kernel(const float* __restrict__ g, const float* __restrict__ h, int64_t n,
+                                        int* __restrict__ exps) {
+  __shared__ unsigned int m[2];
+  if (threadIdx.x == 0) m[0] = m[1] = 0u;
+  __syncthreads();
+  unsigned int mg = 0u, mh = 0u;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    mg = max(mg, __float_as_uint(fabsf(g[i])));
+    mh = max(mh, __float_as_uint(fabsf(h[i])));
   }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    mg = fmaxf(mg, __shfl_xor_sync(0xffffffffu, mg, off));
-    mh = fmaxf(mh, __shfl_xor_sync(0xffffffffu, mh, off));
-  }
+  mg = __reduce_max_sync(0xffffffffu, mg);
+  mh = __reduce_max_sync(0xffffffffu, mh);
   if ((threadIdx.x & 31) == 0) {
-    atomicMax(maxbits, __float_as_uint(mg));
-    atomicMax(maxbits + 1, __float_as_uint(mh));
+    atomicMax(&m[0], mg);
+    atomicMax(&m[1], mh);
   }
-}
-
-// -> power-of-two scale exponents: q = v * 2^exps, |q| <= 2^39.
-__global__ void fixed_scale_kernel(const unsigned int* __restrict__ maxbits, int* __restrict__ exps) {
-  int eg = 0, eh = 0;
-  frexpf(__uint_as_float(maxbits[0]), &eg);
-  frexpf(__uint_as_float(maxbits[1]), &eh);
-  exps[0] = 39 - eg;
-  exps[1] = 39 - eh;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int eg = 0, eh = 0;
+    frexpf(__uint_as_float(m[0]), &eg);
+    frexpf(__uint_as_float(m[1]), &eh);
+    exps[0] = 39 - eg;
+    exps[1] = 39 - eh;
+  }
 }
 
 // Thread = (row, 32-bit word of the packed row): the word's features.
@@ -401,13 +403,8 @@ size_t small_hist_acc_bytes(int d, int k) {
   return D * 8 * 2 + D * 4 + 16;
 }
 
-void launch_fixed_scale(const float* g, const float* h, int64_t n, int* exps, cudaStream_t s) {
-  unsigned int* maxbits = reinterpret_cast<unsigned int*>(exps + 2);  // exps holds 4 ints
-  HBG_CUDA(cudaMemsetAsync(maxbits, 0, 2 * sizeof(unsigned int), s));
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n + 1023) / 1024, 1184));
-  fixed_max_kernel<<<static_cast<unsigned>(blocks), 1024, 0, s>>>(g, h, n, maxbits);
-  HBG_LAUNCH_CHECK();
-  fixed_scale_kernel<<<1, 1, 0, s>>>(maxbits, exps);
+void launch_fixed_leaf_scale(const float* g, const float* h, int64_t n, int* exps, cudaStream_t s) {
+  fixed_leaf_scale_kernel<<<1, 1024, 0, s>>>(g, h, n, exps);
   HBG_LAUNCH_CHECK();
 }
 
@@ -440,8 +437,7 @@ void launch_small_hist(const int32_t* rows, const float* g, const float* h, int6
 }
 
 void configure_tree_kernels() {
-  set_max_shared_carveout(reinterpret_cast<const void*>(fixed_max_kernel));
-  set_max_shared_carveout(reinterpret_cast<const void*>(fixed_scale_kernel));
+  set_max_shared_carveout(reinterpret_cast<const void*>(fixed_leaf_scale_kernel));
   set_max_shared_carveout(reinterpret_cast<const void*>(small_hist_atomic_kernel));
   set_max_shared_carveout(reinterpret_cast<const void*>(small_hist_finish_kernel));
   set_max_shared_carveout(reinterpret_cast<const void*>(partition_small_kernel<float>));

@@ -106,7 +106,13 @@ def main():
         if os.path.exists(p):
             with open(p) as f:
                 t = json.load(f)
-        t[args.workload] = traffic
+        import sys
+
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        from paper_1706_08359_b200 import hist_kernel_stamp
+
+        t[args.workload] = {"dram_bytes": traffic, "kernel_src": hist_kernel_stamp(),
+                            "capture": os.path.basename(args.rep)}
         with open(p, "w") as f:
             json.dump(t, f, indent=1)
     print(json.dumps(derived, indent=1))

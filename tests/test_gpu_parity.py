@@ -525,6 +525,35 @@ def test_grow_tree_matches_oracle(hbg, oracle, rows, d, k, leaves, min_data, lam
         assert same == len(want_log)
 
 
+@pytest.mark.parametrize("case", ["outlier", "tiny_hessians"])
+@pytest.mark.parametrize("grower", ["persistent", "wave", "legacy", "host"])
+def test_grow_tree_small_magnitude_leaves(hbg, oracle, case, grower, monkeypatch):
+    """Leaves whose g/h are many orders of magnitude below the tree's max
+    (the small-leaf fixed-point histograms once used ONE scale per
+    tree, so such leaves were quantised to a few bits). 'outlier': residuals
+    ~1e-9 next to one row of 1e3; 'tiny_hessians': a converged logistic
+    region (hessians ~1e-12) next to hessians of 0.25. The tree must equal the
+    reference's bits64 tree up to the first fp32 near-tie."""
+    rows, d, k = 60000, 12, 64
+    cols = oracle.gen_synthetic_bins(rows, d, k, 11)
+    g, h = oracle.gen_grad_hess(rows, 11)
+    g = g + 0.3 * (cols[3].astype(np.float64) > k // 2)
+    if case == "outlier":
+        g = g * 1e-9
+        h = h * 1e-9 + 1e-10
+        g[12345] = 1e3
+    else:
+        conv = cols[0] < k // 2  # a pure, converged region: p(1-p) ~ 1e-12
+        g = np.where(conv, g * 1e-12, g)
+        h = np.where(conv, 1e-12 * (1.0 + h), 0.25 * h + 0.01)
+    monkeypatch.setenv("HBG_GROW", grower)
+    with hbg.Dataset(cols, k) as ds:
+        log, nodes = _grow(hbg, ds, g, h, 63, 20, 0.0)
+    want_log, want_nodes = oracle.grow_tree(cols, k, g, h, 63, 20, 0.0, 64)
+    same = _assert_same_tree(log, nodes, want_log, want_nodes, cols, g, h, 0.0)
+    assert same >= 20, same
+
+
 @pytest.mark.parametrize("rows,d,k,leaves,min_data,lam", [
     (300000, 28, 64, 255, 1, 0.0), (200000, 28, 16, 255, 20, 0.0), (100000, 70, 200, 127, 5, 1.0),
     (3000, 3, 64, 255, 1, 0.0), (20000, 1300, 256, 31, 100, 0.0), (60000, 10, 64, 511, 1, 0.0),
