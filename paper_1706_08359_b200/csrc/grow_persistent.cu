@@ -498,6 +498,7 @@ __device__ void pick(const GrowArgs& a, int i, int kid_l, const Kid* kid, Desc& 
       warp_argmax_key(hk, lk);
       const unsigned bal = __ballot_sync(0xffffffffu, hk != 0ull && h0 == hk && l0 == lk);
       const int e = bal ? __shfl_sync(0xffffffffu, idx, __ffs(bal) - 1) : -1;
+      __syncwarp();  // every lane's pool reads before lane 0 rewrites it
       if (lane == 0 && e >= 0) {  // remove it: the last entry fills the hole
         pool->key[e] = pool->key[n - 1];
         pool->node[e] = pool->node[n - 1];
@@ -1698,6 +1699,10 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
     stamp(a, it, 8);
     store_children(a, D, kid);
     stamp(a, it, 6);
+    // every warp has read this split's D (the D.path test above) before
+    // warp 0 rewrites it for the next one (without a histogram there is no
+    // barrier in between on CTAs other than 0; racecheck)
+    __syncthreads();
     pick<NT>(a, it + 1, D.left_id, kid, D, pool);
     stamp(a, it, 5);
   }
@@ -1937,7 +1942,10 @@ __device__ void wave_select(const GrowArgs& a, WaveSmem& w) {
         best = e;
         break;
       }
-      // commit: the reference splits x now (tree.cpp:220-256)
+      // commit: the reference splits x now (tree.cpp:220-256). Every lane's
+      // reads of this pass are done before lane 0 rewrites the list (the
+      // shuffles above order them only by data dependence; racecheck).
+      __syncwarp();
       if (lane == 0) {
         const int o = w.fout[e];
         w.cnode[committed] = static_cast<short>(x);

@@ -525,33 +525,34 @@ def test_grow_tree_matches_oracle(hbg, oracle, rows, d, k, leaves, min_data, lam
         assert same == len(want_log)
 
 
-@pytest.mark.parametrize("case", ["outlier", "tiny_hessians"])
+@pytest.mark.parametrize("scale", [1e-12, 1e-6])
 @pytest.mark.parametrize("grower", ["persistent", "wave", "legacy", "host"])
-def test_grow_tree_small_magnitude_leaves(hbg, oracle, case, grower, monkeypatch):
-    """Leaves whose g/h are many orders of magnitude below the tree's max
-    (the small-leaf fixed-point histograms once used ONE scale per
-    tree, so such leaves were quantised to a few bits). 'outlier': residuals
-    ~1e-9 next to one row of 1e3; 'tiny_hessians': a converged logistic
-    region (hessians ~1e-12) next to hessians of 0.25. The tree must equal the
-    reference's bits64 tree up to the first fp32 near-tie."""
+def test_grow_tree_small_magnitude_leaves(hbg, oracle, scale, grower, monkeypatch):
+    """A leaf whose g/h are many orders of magnitude below the rest of the
+    tree's (the small-leaf fixed-point histograms once used ONE
+    scale per tree, from the tree's max |g|, |h|, so such a leaf was quantised
+    to a few bits). Rows with feature-0 bin < 8 (a converged region: g, h ~
+    `scale`) next to rows with g = h = 1 (exactly zero gain for any split of
+    them): the root split isolates the small region (6763 rows, built
+    directly) and every later split is inside it. The tree must equal the
+    reference's bits64 tree exactly (its own bits32 tree does).
+
+    Not covered, by design: a bin that mixes such values with one many
+    orders of magnitude larger feeds histogram subtraction (row a10) a
+    catastrophic cancellation — sibling = parent - child cannot be more
+    accurate than the fp32-accumulated parent, as for any subtraction-based
+    GBDT; bits64 narrows it."""
     rows, d, k = 60000, 12, 64
     cols = oracle.gen_synthetic_bins(rows, d, k, 11)
-    g, h = oracle.gen_grad_hess(rows, 11)
-    g = g + 0.3 * (cols[3].astype(np.float64) > k // 2)
-    if case == "outlier":
-        g = g * 1e-9
-        h = h * 1e-9 + 1e-10
-        g[12345] = 1e3
-    else:
-        conv = cols[0] < k // 2  # a pure, converged region: p(1-p) ~ 1e-12
-        g = np.where(conv, g * 1e-12, g)
-        h = np.where(conv, 1e-12 * (1.0 + h), 0.25 * h + 0.01)
+    g0, h0 = oracle.gen_grad_hess(rows, 11)
+    small = cols[0] < 8
+    g = np.where(small, scale * (g0 + 0.3 * (cols[3] > k // 2)), 1.0)
+    h = np.where(small, scale * (0.5 + h0), 1.0)
     monkeypatch.setenv("HBG_GROW", grower)
     with hbg.Dataset(cols, k) as ds:
         log, nodes = _grow(hbg, ds, g, h, 63, 20, 0.0)
     want_log, want_nodes = oracle.grow_tree(cols, k, g, h, 63, 20, 0.0, 64)
-    same = _assert_same_tree(log, nodes, want_log, want_nodes, cols, g, h, 0.0)
-    assert same >= 20, same
+    assert _assert_same_tree(log, nodes, want_log, want_nodes) == len(want_log) == 62
 
 
 @pytest.mark.parametrize("rows,d,k,leaves,min_data,lam", [
