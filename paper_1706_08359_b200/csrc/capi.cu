@@ -405,8 +405,7 @@ void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const vo
   }
   require(d_g != nullptr && d_h != nullptr, "null gradient/hessian pointer");
   if (d_idx == nullptr) d_idx = identity_rows(ds, 0, s);  // identity leaf [0, count)
-  HistPlan plan =
-      plan_histogram(L.bits_per_bin, L.max_bin, L.num_groups, count, L.device, true, acc_bytes, L.num_features);
+  HistPlan plan = plan_histogram(L.bits_per_bin, L.max_bin, L.num_groups, count, L.device, true, acc_bytes);
   char* part = static_cast<char*>(ds->part.get(hist_part_bytes(plan)));
   HistArgs a{};
   a.packed = reinterpret_cast<const uint8_t*>(ds->packed);
@@ -457,7 +456,7 @@ void build_device_peer(hbg_dataset* ds, const int32_t* d_idx, int64_t count, con
   require(count == 0 || (d_g != nullptr && d_h != nullptr), "null gradient/hessian pointer");
   if (d_idx == nullptr && count > 0) d_idx = identity_rows(ds, 0, s);
   HistPlan plan = plan_histogram(L.bits_per_bin, L.max_bin, L.num_groups, std::max<int64_t>(count, 1), L.device,
-                                 /*allow_direct=*/false, 4, L.num_features);
+                                 /*allow_direct=*/false);
   char* part = static_cast<char*>(ds->part.get(hist_part_bytes(plan)));
   HistArgs a{};
   a.packed = reinterpret_cast<const uint8_t*>(ds->packed);
@@ -824,7 +823,7 @@ PersistentGrowArgs grow_workspace(hbg_dataset* ds, const hbg_grow_params& P, int
   a.timeout_cycles = wait_timeout_cycles(L.device);
   ds->part_scratch.get(gather_scratch_doubles(N) * sizeof(double) + 64);
   if (N > 0 && d > 0) {  // the root histogram's partials (build_device)
-    const HistPlan plan = plan_histogram(L.bits_per_bin, L.max_bin, L.num_groups, N, L.device, true, 4, L.num_features);
+    const HistPlan plan = plan_histogram(L.bits_per_bin, L.max_bin, L.num_groups, N, L.device);
     ds->part.get(hist_part_bytes(plan));
   }
   return a;

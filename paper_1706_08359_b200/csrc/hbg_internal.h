@@ -46,8 +46,6 @@ struct HistPlan {
   size_t smem;      // dynamic shared memory per CTA
   size_t part_values;  // entries in each partial array (ctas * gb * 32 * k_alloc)
   int acc_bytes;       // 4: fp32 g/h and cells (bits32); 8: fp64 (bits64)
-  int dup_m;           // != 0: the pad-free kernel (hist_dup.cu) for one group of dup_m features
-  int dup_r;           //       its rows per lane
 };
 
 struct HistArgs {
@@ -79,12 +77,7 @@ struct HistArgs {
 // acc_bytes: 4 = fp32 g/h inputs, cells and partials (PrecisionMode::bits32);
 // 8 = fp64 throughout (PrecisionMode::bits64).
 HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int device, bool allow_direct = true,
-                        int acc_bytes = 4, int num_features = 0);
-// the pad-free schedule for a single slice group of 16/24/28 features (hist_dup.cu)
-bool hist_dup_supported(int bits, int k_alloc, int num_groups, int d, int acc_bytes);
-int hist_dup_rows_per_lane();
-void configure_hist_dup(int device);
-void launch_histogram_dup(const HistPlan& plan, const HistArgs& args, cudaStream_t s);
+                        int acc_bytes = 4);
 // Bytes of the partial buffers of a plan (g, h: acc_bytes each; count: 4).
 inline size_t hist_part_bytes(const HistPlan& p) { return p.part_values * (2 * p.acc_bytes + 4) + 16; }
 

@@ -501,7 +501,6 @@ void configure_hist_kernels(int device) {
   set_smem_attr<8, 64>(device);
   set_smem_attr<8, 128>(device);
   set_smem_attr<8, 256>(device);
-  configure_hist_dup(device);
   set_max_shared_carveout(reinterpret_cast<const void*>(reduce_partials_kernel<float>));
   set_max_shared_carveout(reinterpret_cast<const void*>(reduce_partials_kernel<double>));
   set_max_shared_carveout(reinterpret_cast<const void*>(pack_kernel));
@@ -529,22 +528,16 @@ int sm_count(int device) {
 constexpr int64_t kDirectRows = 1024;
 
 HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int device, bool allow_direct,
-                        int acc_bytes, int num_features) {
+                        int acc_bytes) {
   HistPlan p{};
   p.bits = bits;
   p.acc_bytes = acc_bytes;
   p.k_alloc = bits == 4 ? 16 : (max_bin <= 64 ? 64 : (max_bin <= 128 ? 128 : 256));
   const size_t cells = static_cast<size_t>(p.k_alloc) * 32;
-  const bool dup = hist_dup_supported(bits, p.k_alloc, num_groups, num_features, acc_bytes);
-  if (dup) {
-    p.dup_m = num_features;
-    p.dup_r = hist_dup_rows_per_lane();
-  }
-  // per-warp private {g,h} (the pad-free kernel: two homes) and per-group shared counts
-  const size_t ghw = cells * 2 * static_cast<size_t>(acc_bytes) * (dup ? 2 : 1);
-  const size_t cntw = cells * 4 * (dup ? 2 : 1);
+  const size_t ghw = cells * 2 * static_cast<size_t>(acc_bytes);  // per-warp private {g,h}
+  const size_t cntw = cells * 4;  // per-group shared counts
   const size_t smem_max = 232448;
-  const int max_warps = dup ? 8 : 16;
+  const int max_warps = 16;
   // The group block (slice groups per CTA) that maximises warps per CTA (the
   // latency hiding of the ordered read-modify-write chains); ties -> more
   // groups per CTA (fewer re-reads of the leaf entries).
@@ -562,7 +555,7 @@ HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int de
   const int warps_full = warps;
   // Small leaves: shrink the CTA (less shared memory to clear and fold) so the
   // grid still spreads over the SMs with >= 4 tiles per warp.
-  const int rpl = dup ? p.dup_r : rows_per_lane_of(p.k_alloc, acc_bytes);
+  const int rpl = rows_per_lane_of(p.k_alloc, acc_bytes);
   {
     const int64_t tile_rows = static_cast<int64_t>(32) * rpl;
     const int64_t warps_needed =
@@ -590,7 +583,7 @@ HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int de
     p.part_values = 0;
     return p;
   }
-  const int occ = dup ? 1 : occupancy_for(bits, p.k_alloc, p.warps * 32, p.smem, device, acc_bytes);
+  const int occ = occupancy_for(bits, p.k_alloc, p.warps * 32, p.smem, device, acc_bytes);
   const int64_t slots = static_cast<int64_t>(sm_count(device)) * occ;  // CTAs per wave
   // Row segments: fill whole waves (1..4) as evenly as possible.
   int64_t nseg = 1;
@@ -634,8 +627,7 @@ void launch_histogram_t(const HistPlan& plan, const HistArgs& args, cudaStream_t
 }
 
 void launch_histogram(const HistPlan& plan, const HistArgs& args, cudaStream_t s) {
-  if (plan.dup_m != 0) launch_histogram_dup(plan, args, s);
-  else if (plan.acc_bytes == 8) launch_histogram_t<double>(plan, args, s);
+  if (plan.acc_bytes == 8) launch_histogram_t<double>(plan, args, s);
   else launch_histogram_t<float>(plan, args, s);
 }
 

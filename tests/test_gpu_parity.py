@@ -532,10 +532,11 @@ def test_grow_tree_small_magnitude_leaves(hbg, oracle, scale, grower, monkeypatc
     tree's (the small-leaf fixed-point histograms once used ONE
     scale per tree, from the tree's max |g|, |h|, so such a leaf was quantised
     to a few bits). Rows with feature-0 bin < 8 (a converged region: g, h ~
-    `scale`) next to rows with g = h = 1 (exactly zero gain for any split of
-    them): the root split isolates the small region (6763 rows, built
-    directly) and every later split is inside it. The tree must equal the
-    reference's bits64 tree exactly (its own bits32 tree does).
+    `scale`) next to rows with g = h = 1 whose bins are all k-1 (no split
+    candidate among them): the root split isolates the small region (6763
+    rows, the smaller child, built directly) and every later split is inside
+    it. The tree must equal the reference's bits64 tree exactly (its own
+    bits32 tree does).
 
     Not covered, by design: a bin that mixes such values with one many
     orders of magnitude larger feeds histogram subtraction (row a10) a
@@ -543,9 +544,10 @@ def test_grow_tree_small_magnitude_leaves(hbg, oracle, scale, grower, monkeypatc
     accurate than the fp32-accumulated parent, as for any subtraction-based
     GBDT; bits64 narrows it."""
     rows, d, k = 60000, 12, 64
-    cols = oracle.gen_synthetic_bins(rows, d, k, 11)
+    cols = oracle.gen_synthetic_bins(rows, d, k, 11).copy()
     g0, h0 = oracle.gen_grad_hess(rows, 11)
     small = cols[0] < 8
+    cols[:, ~small] = k - 1
     g = np.where(small, scale * (g0 + 0.3 * (cols[3] > k // 2)), 1.0)
     h = np.where(small, scale * (0.5 + h0), 1.0)
     monkeypatch.setenv("HBG_GROW", grower)
