@@ -398,11 +398,24 @@ def run_hbg(args):
         "steps": e2e_steps,
         "pageable_ms_per_step": page_ms,
     }
+    # a depth-1 leaf (half the rows, random and sorted: bench.cpp's leaf
+    # shape) through the same drop-in: its row ids travel too (informational)
+    i1 = leaf_sample(n, 1, 101)
+    leaf1 = hbg.LeafState(torch.from_numpy(i1).pin_memory().numpy(), torch.from_numpy(g[i1]).pin_memory().numpy(),
+                          torch.from_numpy(h[i1]).pin_memory().numpy())
+    hbg.build_histograms_partitioned(ds, leaf1)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        hbg.build_histograms_partitioned(ds, leaf1)
+    d1_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
+    result["e2e"]["depth1_leaf"] = {"rows": int(len(i1)), "ms_per_step": d1_ms,
+                                    "rows_features_per_s": len(i1) * d / (d1_ms / 1e3),
+                                    "h2d_bytes_per_step": int(len(i1) * (4 + 8 + 8))}
 
     # --- variants (informational): 4-bit 16-bin kernel, deeper leaves
     if not args.no_variants:
         var = {}
-        for depth in (2, 4, 6, 8):
+        for depth in (2, 4, 6, 8, 10, 12):
             li = torch.from_numpy(leaf_sample(n, depth, 100 + depth)).to(dev)
             m = len(li)
             lg = torch.empty(m, dtype=torch.float32, device=dev)
@@ -411,7 +424,7 @@ def run_hbg(args):
             hbg.gather_leaf_device(li, m, tg, th, lg, lh, tot, sp)
             for _ in range(3):
                 ds.build_histograms_device(li, m, lg, lh, hist, hbg.HBG_GH_LEAF_ALIGNED, sp)
-            reps = 20
+            reps = 100
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             for _ in range(reps):

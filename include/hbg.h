@@ -114,6 +114,13 @@ int hbg_build_histograms_ex(hbg_dataset* ds, const int32_t* indices, int64_t cou
                             const double* gradients, const double* hessians, int32_t precision,
                             hbg_bin* out);
 
+/* Development aid: with HBG_HIST_PROFILE set in the environment, every
+ * histogram launch records %globaltimer stamps (ns) of its CTA 0 — start,
+ * shared memory cleared, rows done, partials written, grid barrier passed,
+ * reduced; [6] the reduction's first loads, [7] unused — and this copies the
+ * last launch's eight to host `out`. */
+int hbg_debug_hist_stamps(hbg_dataset* ds, unsigned long long* out);
+
 /* Device builder (the performance path). d_indices may be NULL for the
  * identity leaf [0, count) (the root). d_grad/d_hess are fp32, addressed per
  * gh_mode. d_hist receives the device histogram: SoA fp64

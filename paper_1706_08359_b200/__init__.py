@@ -139,6 +139,7 @@ class hbg_layout(C.Structure):
 EXPORTED_SYMBOLS = (
     "hbg_last_error",
     "hbg_version",
+    "hbg_debug_hist_stamps",
     "hbg_dataset_create",
     "hbg_dataset_destroy",
     "hbg_dataset_layout",

@@ -102,6 +102,8 @@ struct hbg_dataset {
   hbg::DevBuf slots, part_scratch, tree_small;  // leaf histograms, partition scratch, splits/totals
   hbg::DevBuf boost_g, boost_h, boost_leaves;   // boosting: fp32 gradients, final leaf ranges
   hbg::DevBuf small_acc, small_exps;            // fixed-point accumulator for small leaves
+  hbg::DevBuf hist_bar;                         // fused histogram's grid-barrier counter (zeroed once)
+  hbg::DevBuf hist_prof;                        // HBG_HIST_PROFILE phase stamps of the last launch
   hbg::DevBuf grow_nodes, grow_log, grow_tree, grow_counts, grow_scratch, grow_root, grow_prof;  // persistent grower
   const void* grow_records = nullptr;  // the last grown tree's score-update input (launch_grow_persistent)
   bool grow_waves = false;             // ... LeafRange x grow_ranges (wave grower) or node records
@@ -388,9 +390,13 @@ const int32_t* identity_rows(hbg_dataset* ds, int64_t first, cudaStream_t s) {
 // Device histogram of one leaf into d_hist; with `parent` also writes
 // sibling = parent - d_hist in the same pass (sibling may alias parent).
 // acc_bytes 4: d_g/d_h are fp32 (bits32); 8: fp64 with fp64 accumulation (bits64).
+// allow_fused: the leaf may take the single-launch cluster mode (histogram +
+// DSMEM reduction in one kernel). Off where ranks share a GPU and wait on each
+// other inside kernels (a cluster could wait for SMs a waiting grid holds).
 void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const void* d_g,
                   const void* d_h, int gh_mode, double* d_hist, cudaStream_t s,
-                  const double* parent = nullptr, double* sibling = nullptr, int acc_bytes = 4) {
+                  const double* parent = nullptr, double* sibling = nullptr, int acc_bytes = 4,
+                  bool allow_fused = false) {
   const hbg_layout& L = ds->layout;
   require(count >= 0, "negative leaf size");
   require(count <= L.num_rows || d_idx != nullptr, "identity leaf larger than the dataset");
@@ -405,7 +411,8 @@ void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const vo
   }
   require(d_g != nullptr && d_h != nullptr, "null gradient/hessian pointer");
   if (d_idx == nullptr) d_idx = identity_rows(ds, 0, s);  // identity leaf [0, count)
-  HistPlan plan = plan_histogram(L.bits_per_bin, L.max_bin, L.num_groups, count, L.device, true, acc_bytes);
+  HistPlan plan = plan_histogram(L.bits_per_bin, L.max_bin, L.num_groups, count, L.device, true, acc_bytes,
+                                 allow_fused);
   char* part = static_cast<char*>(ds->part.get(hist_part_bytes(plan)));
   HistArgs a{};
   a.packed = reinterpret_cast<const uint8_t*>(ds->packed);
@@ -421,14 +428,30 @@ void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const vo
   a.nblocks = plan.nblocks;
   a.seg_len = plan.seg_len;
   a.part_g = part;
-  a.part_h = part + plan.part_values * plan.acc_bytes;
-  a.part_c = reinterpret_cast<uint32_t*>(part + 2 * plan.part_values * plan.acc_bytes);
+  a.part_h = part + plan.part_values * part_elem_bytes(plan);
+  a.part_c = reinterpret_cast<uint32_t*>(part + 2 * plan.part_values * part_elem_bytes(plan));
   a.direct = plan.nseg == 1 ? 1 : 0;
   a.d = L.num_features;
   a.max_bin = L.max_bin;
   a.out = d_hist;
   a.parent = parent;
   a.sibling = sibling;
+  a.nseg = plan.nseg;
+  a.cluster = plan.cluster;
+  a.nclusters = plan.nclusters;
+  static const bool prof = std::getenv("HBG_HIST_PROFILE") != nullptr;  // development aid
+  if (prof) {
+    a.prof = static_cast<unsigned long long*>(ds->hist_prof.get(64));
+    HBG_CUDA(cudaMemsetAsync(a.prof, 0, 64, s));
+  }
+  if (plan.nclusters > 1) {  // counters zeroed once; every launch leaves them 0
+    const size_t need = static_cast<size_t>(std::max(plan.nblocks, 1)) * sizeof(unsigned) + 64;
+    if (ds->hist_bar.bytes < need) {
+      ds->hist_bar.get(need);
+      HBG_CUDA(cudaMemsetAsync(ds->hist_bar.p, 0, ds->hist_bar.bytes, s));
+    }
+    a.bar = static_cast<unsigned*>(ds->hist_bar.p);
+  }
   if (ds->profiling) {
     auto ev = ds->event_pair();
     HBG_CUDA(cudaEventRecord(ev.first, s));
@@ -438,7 +461,7 @@ void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const vo
   } else {
     launch_histogram(plan, a, s);
   }
-  if (!a.direct) launch_reduce_partials(plan, a, L.num_features, L.max_bin, d_hist, s, parent, sibling);
+  if (!a.direct && a.cluster <= 1) launch_reduce_partials(plan, a, L.num_features, L.max_bin, d_hist, s, parent, sibling);
 }
 
 // Row-sharded histogram of one leaf: this rank's rows, the cross-rank sum
@@ -875,7 +898,7 @@ void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_h
     *num_nodes = 1;
     return;
   }
-  build_device(ds, a.rows[0], N, a.g[0], a.h[0], HBG_GH_LEAF_ALIGNED, slots, s);
+  build_device(ds, a.rows[0], N, a.g[0], a.h[0], HBG_GH_LEAF_ALIGNED, slots, s, nullptr, nullptr, 4, !sharded);
   if (!sharded) {  // sharded: the kernel sums the ranks' root histograms first, then scans
     hbg_split* root_split = reinterpret_cast<hbg_split*>(static_cast<char*>(a.nodes) + grow_root_split_offset());
     launch_best_split(slots, d, k, root, nullptr, 0.0, 0.0, N, P.min_data_in_leaf, P.lambda, root_split, s);
@@ -1178,7 +1201,7 @@ int hbg_build_histograms_ex(hbg_dataset* ds, const int32_t* indices, int64_t cou
         HBG_CUDA(cudaMemcpyAsync(di, indices, n * 4, cudaMemcpyHostToDevice, s));
         d_idx = di;
       }
-      build_device(ds, d_idx, count, d_gd, d_hd, HBG_GH_LEAF_ALIGNED, d_hist, s, nullptr, nullptr, 8);
+      build_device(ds, d_idx, count, d_gd, d_hd, HBG_GH_LEAF_ALIGNED, d_hist, s, nullptr, nullptr, 8, true);
     } else if (count > 0 && !(is_pinned(gradients) && is_pinned(hessians))) {
       // pageable LeafState arrays: fp32 g/h staged by the host pool (see
       // stage_chunks); histogram chunk c runs as soon as its rows have landed
@@ -1210,7 +1233,8 @@ int hbg_build_histograms_ex(hbg_dataset* ds, const int32_t* indices, int64_t cou
                        HBG_CUDA(cudaEventRecord(ds->chunk_ev[next], ds->copy_stream));
                        HBG_CUDA(cudaStreamWaitEvent(s, ds->chunk_ev[next], 0));
                        double* hc = parts + static_cast<size_t>(next) * (C > 1 ? 3 * D : 0);
-                       build_device(ds, d_idx + cb, ce - cb, d_gf + cb, d_hf + cb, HBG_GH_LEAF_ALIGNED, hc, s);
+                       build_device(ds, d_idx + cb, ce - cb, d_gf + cb, d_hf + cb, HBG_GH_LEAF_ALIGNED, hc, s,
+                                    nullptr, nullptr, 4, true);
                        part_ptrs.push_back(hc);
                      }
                    });
@@ -1269,7 +1293,7 @@ int hbg_build_histograms_ex(hbg_dataset* ds, const int32_t* indices, int64_t cou
         launch_f64_to_f32(d_gd + b, d_gf + b, e - b, s);
         launch_f64_to_f32(d_hd + b, d_hf + b, e - b, s);
         double* hc = parts + static_cast<size_t>(c) * (C > 1 ? 3 * D : 0);
-        build_device(ds, d_idx + b, e - b, d_gf + b, d_hf + b, HBG_GH_LEAF_ALIGNED, hc, s);
+        build_device(ds, d_idx + b, e - b, d_gf + b, d_hf + b, HBG_GH_LEAF_ALIGNED, hc, s, nullptr, nullptr, 4, true);
         part_ptrs.push_back(hc);
       }
       if (C > 1) launch_reduce_parts(part_ptrs, static_cast<int64_t>(3 * D), d_hist, s);
@@ -1282,13 +1306,24 @@ int hbg_build_histograms_ex(hbg_dataset* ds, const int32_t* indices, int64_t cou
   });
 }
 
+// Development aid: the HBG_HIST_PROFILE %globaltimer stamps (ns) of the last
+// histogram launch's CTA 0 (start, cleared, rows done, partials written,
+// barrier passed, reduced), copied to host `out[6]`.
+int hbg_debug_hist_stamps(hbg_dataset* ds, unsigned long long* out) {
+  return guarded([&] {
+    check_ds(ds);
+    require(ds->hist_prof.p != nullptr, "no stamps: set HBG_HIST_PROFILE");
+    HBG_CUDA(cudaMemcpy(out, ds->hist_prof.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  });
+}
+
 int hbg_build_histograms_device(hbg_dataset* ds, const int32_t* d_indices, int64_t count,
                                 const float* d_grad, const float* d_hess, int32_t gh_mode,
                                 double* d_hist, void* stream) {
   return guarded([&] {
     check_ds(ds);
     DeviceGuard dg(ds->layout.device);
-    build_device(ds, d_indices, count, d_grad, d_hess, gh_mode, d_hist, pick(ds, stream));
+    build_device(ds, d_indices, count, d_grad, d_hess, gh_mode, d_hist, pick(ds, stream), nullptr, nullptr, 4, true);
   });
 }
 
@@ -1298,7 +1333,7 @@ int hbg_build_histograms_device_f64(hbg_dataset* ds, const int32_t* d_indices, i
   return guarded([&] {
     check_ds(ds);
     DeviceGuard dg(ds->layout.device);
-    build_device(ds, d_indices, count, d_grad, d_hess, gh_mode, d_hist, pick(ds, stream), nullptr, nullptr, 8);
+    build_device(ds, d_indices, count, d_grad, d_hess, gh_mode, d_hist, pick(ds, stream), nullptr, nullptr, 8, true);
   });
 }
 

@@ -46,7 +46,16 @@ struct HistPlan {
   size_t smem;      // dynamic shared memory per CTA
   size_t part_values;  // entries in each partial array (ctas * gb * 32 * k_alloc)
   int acc_bytes;       // 4: fp32 g/h and cells (bits32); 8: fp64 (bits64)
+  int cluster;         // > 1: ONE launch of clusters of this many CTAs (one per row segment);
+                       //    the segments' sub-histograms are summed over distributed shared
+                       //    memory inside each cluster (no grid barrier); with nclusters > 1
+                       //    the clusters' fp64 sums meet in HBM and the last cluster to
+                       //    finish adds them up
+  int nclusters;       // clusters per group block (cluster mode)
 };
+// Bytes of one g/h partial element: the CTAs' own type, or fp64 for the
+// cluster sums of the multi-cluster mode.
+inline int part_elem_bytes(const HistPlan& p) { return p.cluster > 1 ? 8 : p.acc_bytes; }
 
 struct HistArgs {
   const uint8_t* packed;
@@ -70,16 +79,26 @@ struct HistArgs {
   double* out;
   const double* parent;
   double* sibling;
+  // fused mode (HistPlan::fused): the grid barrier's counter (self-resetting,
+  // one per dataset) and the segment count the reduction runs over
+  int nseg;
+  int cluster;  // HistPlan::cluster
+  int nclusters;
+  unsigned* bar;  // multi-cluster mode: one arrival counter per group block
+  unsigned long long* prof;  // optional %globaltimer stamps of CTA 0 (HBG_HIST_PROFILE), 8 slots
 };
 
 // allow_direct = false: always per-CTA partials + a reduction (the row-sharded
 // path fuses its exchange into that reduction).
 // acc_bytes: 4 = fp32 g/h inputs, cells and partials (PrecisionMode::bits32);
 // 8 = fp64 throughout (PrecisionMode::bits64).
+// allow_fused: leaves up to ~4 tiles per row warp on the resident clusters
+// take the single-launch cluster mode (not where several ranks share a GPU
+// and wait on each other inside kernels: clusters need whole GPCs free).
 HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int device, bool allow_direct = true,
-                        int acc_bytes = 4);
+                        int acc_bytes = 4, bool allow_fused = false);
 // Bytes of the partial buffers of a plan (g, h: acc_bytes each; count: 4).
-inline size_t hist_part_bytes(const HistPlan& p) { return p.part_values * (2 * p.acc_bytes + 4) + 16; }
+inline size_t hist_part_bytes(const HistPlan& p) { return p.part_values * (2 * part_elem_bytes(p) + 4) + 16; }
 
 void launch_histogram(const HistPlan& plan, const HistArgs& args, cudaStream_t s);
 // d_hist = reduced histogram; when `parent` is non-null also writes

@@ -25,6 +25,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "hbg_internal.h"
 #include "hist_device.cuh"
 
@@ -41,6 +43,14 @@ struct TileIn {
   T g, h;
 };
 
+__device__ __forceinline__ void hist_stamp(const HistArgs& a, int slot) {
+  if (a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.prof[slot] = t;
+  }
+}
+
 // T = float: bits32 (the reference's per-element fp32 cast, histogram.cpp:97-98);
 // T = double: bits64 (reference_impl<double>, histogram.cpp:131-145) — fp64
 // inputs, fp64 per-warp cells, fp64 partials.
@@ -49,27 +59,39 @@ __global__ void __launch_bounds__(K >= 256 ? 128 : 512, BITS == 4 ? 2 : 1) hist_
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int kCells = K * 32;
   constexpr int kCellBytes = 2 * sizeof(T);
-  const int warps = blockDim.x >> 5;
   using T2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
+  // warps [0, gb * wpg) own {g,h} cells and process rows; a fused launch may
+  // add warps that only help clear, fold and reduce
+  const int cw = a.gb * a.wpg;
   T2* gh = reinterpret_cast<T2*>(smem);
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + static_cast<size_t>(warps) * kCells * kCellBytes);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + static_cast<size_t>(cw) * kCells * kCellBytes);
   const T* __restrict__ ag = static_cast<const T*>(a.g);
   const T* __restrict__ ah = static_cast<const T*>(a.h);
+  // Programmatic dependent launch: the next kernel in the stream may start
+  // launching now (its CTAs become resident as ours exit); everything before
+  // griddepcontrol.wait touches only this CTA's shared memory, so the clear
+  // overlaps the previous kernel's tail. (Both are no-ops without PDL.)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   {
-    const int n16 = (warps * kCells * kCellBytes + a.gb * kCells * 4) / 16;
+    const int n16 = (cw * kCells * kCellBytes + a.gb * kCells * 4) / 16;
     uint4* z = reinterpret_cast<uint4*>(smem);
     for (int i = threadIdx.x; i < n16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
   }
-  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // inputs and outputs of earlier kernels settled
+  hist_stamp(a, 0);
 
-  const int bi = blockIdx.x % a.nblocks;
-  const int seg = blockIdx.x / a.nblocks;
+  // a cluster's CTAs are consecutive: there, nclusters clusters per group block
+  const int clu = a.cluster > 1 ? static_cast<int>(blockIdx.x) / a.cluster : 0;
+  const int bi = a.cluster > 1 ? clu / a.nclusters : blockIdx.x % a.nblocks;
+  const int seg = a.cluster > 1 ? (clu % a.nclusters) * a.cluster + static_cast<int>(blockIdx.x) % a.cluster
+                                : blockIdx.x / a.nblocks;
   const int w = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int gl = w % a.gb;
   const int sub = w / a.gb;
   const int group = bi * a.gb + gl;
-  if (sub < a.wpg && group < a.num_groups) {
+  const bool row_warp = sub < a.wpg && group < a.num_groups;
+  {
     const int64_t s0 = static_cast<int64_t>(seg) * a.seg_len;
     const int64_t s1 = min(s0 + a.seg_len, a.n);
     const uint32_t gh_base = smem_addr(gh + static_cast<size_t>(w) * kCells);
@@ -120,10 +142,15 @@ __global__ void __launch_bounds__(K >= 256 ? 128 : 512, BITS == 4 ? 2 : 1) hist_
     int64_t t = s0 + static_cast<int64_t>(sub) * 32 * R;
     TileIn<T> e0[R], e1[R];
     Slice<BITS> cur[R];
-    fetch_entry(t, e0);
-    fetch_entry(t + step, e1);
-    fetch_slice(e0, cur);
-    for (; t < s1; t += step) {
+    // the pipeline's first loads are in flight while the cells are cleared
+    if (row_warp) {
+      fetch_entry(t, e0);
+      fetch_entry(t + step, e1);
+      fetch_slice(e0, cur);
+    }
+    __syncthreads();  // cells cleared
+    hist_stamp(a, 1);
+    for (; row_warp && t < s1; t += step) {
       TileIn<T> e2[R];
       Slice<BITS> nxt[R];
       fetch_entry(t + 2 * step, e2);  // stage A (t + 2s)
@@ -157,17 +184,115 @@ __global__ void __launch_bounds__(K >= 256 ? 128 : 512, BITS == 4 ? 2 : 1) hist_
     }
   }
   __syncthreads();
+  hist_stamp(a, 2);
 
   // Fold the warps of each group in a fixed order.
   auto fold = [&](int g2, int c, T& sg, T& sh) {
     sg = T(0);
     sh = T(0);
+#pragma unroll 4
     for (int s = 0; s < a.wpg; ++s) {
       const T2 v = gh[static_cast<size_t>(s * a.gb + g2) * kCells + c];
       sg += v.x;
       sh += v.y;
     }
   };
+  if (a.cluster > 1) {
+    // Cluster mode: this CTA folds its warps into its own sub-histogram in
+    // shared memory; after a cluster barrier, CTA r sums cells [r*per, ...)
+    // over the cluster's C sub-histograms through distributed shared memory
+    // (ranks in order: deterministic). One cluster per group block writes the
+    // fp64 histogram directly; with several, each writes its fp64 sums to HBM
+    // and the last cluster to arrive (device-scope counter) adds the clusters'
+    // sums in cluster order and writes the histogram.
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int ncell = a.gb * kCells;
+    T* sub_g = reinterpret_cast<T*>(smem + static_cast<size_t>(cw) * kCells * kCellBytes +
+                                    static_cast<size_t>(a.gb) * kCells * 4);
+    T* sub_h = sub_g + ncell;
+    uint32_t* sub_c = reinterpret_cast<uint32_t*>(sub_h + ncell);
+    int& last_flag = *reinterpret_cast<int*>(sub_c + ncell);  // (dynamic: the limit is for all shared memory)
+    for (int i = threadIdx.x; i < ncell; i += blockDim.x) {
+      const int g2 = i / kCells, c = i - g2 * kCells;
+      T sg, sh;
+      fold(g2, c, sg, sh);
+      sub_g[i] = sg;
+      sub_h[i] = sh;
+      sub_c[i] = cnt[i];
+    }
+    hist_stamp(a, 3);
+    cl.sync();
+    hist_stamp(a, 4);
+    const int C = static_cast<int>(cl.num_blocks()), r = static_cast<int>(cl.block_rank());
+    const int per = (ncell + C - 1) / C;
+    const int i0 = r * per, i1 = min(ncell, (r + 1) * per);
+    const size_t D = static_cast<size_t>(a.d) * a.max_bin;
+    const int nk = a.nclusters, kk = clu % nk;
+    double* cg_ = static_cast<double*>(a.part_g);
+    double* ch_ = static_cast<double*>(a.part_h);
+    auto emit = [&](int i, double vg, double vh, unsigned long long vc) {
+      const int g2 = i / kCells, c = i - g2 * kCells;
+      const int bin = c >> 5, f = (bi * a.gb + g2) * 32 + (c & 31);
+      if (f >= a.d || bin >= a.max_bin) return;
+      const size_t o = static_cast<size_t>(f) * a.max_bin + bin;
+      a.out[o] = vg;
+      a.out[D + o] = vh;
+      a.out[2 * D + o] = static_cast<double>(vc);
+      if (a.parent) {
+        const double pg = a.parent[o], ph = a.parent[D + o], pc = a.parent[2 * D + o];
+        a.sibling[o] = pg - vg;
+        a.sibling[D + o] = ph - vh;
+        a.sibling[2 * D + o] = pc - static_cast<double>(vc);
+      }
+    };
+    for (int i = i0 + static_cast<int>(threadIdx.x); i < i1; i += blockDim.x) {
+      double vg = 0.0, vh = 0.0;
+      unsigned long long vc = 0;
+#pragma unroll 4
+      for (int q = 0; q < C; ++q) {
+        vg += static_cast<double>(*cl.map_shared_rank(sub_g + i, q));
+        vh += static_cast<double>(*cl.map_shared_rank(sub_h + i, q));
+        vc += *cl.map_shared_rank(sub_c + i, q);
+      }
+      if (nk == 1) {
+        emit(i, vg, vh, vc);
+      } else {
+        const size_t o = (static_cast<size_t>(bi) * nk + kk) * ncell + i;
+        cg_[o] = vg;
+        ch_[o] = vh;
+        a.part_c[o] = static_cast<uint32_t>(vc);
+      }
+    }
+    if (nk > 1) {
+      __threadfence();  // this cluster's sums are visible before it is counted
+      cl.sync();
+      if (r == 0 && threadIdx.x == 0) {
+        const unsigned old = atomicAdd(a.bar + bi, 1u);
+        last_flag = old == static_cast<unsigned>(nk - 1);
+        if (last_flag) a.bar[bi] = 0u;  // every cluster has arrived: reset for the next launch
+      }
+      cl.sync();
+      if (*cl.map_shared_rank(&last_flag, 0)) {
+        __threadfence();
+        for (int i = i0 + static_cast<int>(threadIdx.x); i < i1; i += blockDim.x) {
+          double vg = 0.0, vh = 0.0;
+          unsigned long long vc = 0;
+#pragma unroll 4
+          for (int q = 0; q < nk; ++q) {
+            const size_t o = (static_cast<size_t>(bi) * nk + q) * ncell + i;
+            vg += __ldcg(cg_ + o);
+            vh += __ldcg(ch_ + o);
+            vc += __ldcg(a.part_c + o);
+          }
+          emit(i, vg, vh, vc);
+        }
+      }
+    }
+    cl.sync();  // no CTA leaves while another still reads its shared memory
+    hist_stamp(a, 5);
+    return;
+  }
   if (a.direct) {
     // Single row segment: write the final fp64 histogram (and the fused
     // sibling = parent - this) in output order, so global accesses coalesce;
@@ -215,6 +340,7 @@ __global__ void __launch_bounds__(K >= 256 ? 128 : 512, BITS == 4 ? 2 : 1) hist_
         }
       }
     }
+    hist_stamp(a, 5);
     return;
   }
   // One partial per CTA (T sums, u32 counts).
@@ -230,6 +356,7 @@ __global__ void __launch_bounds__(K >= 256 ? 128 : 512, BITS == 4 ? 2 : 1) hist_
     part_h[o] = sh;
     a.part_c[o] = cnt[static_cast<size_t>(g2) * kCells + c];
   }
+  hist_stamp(a, 3);
 }
 
 // out (SoA fp64 [3][d][max_bin]) = fixed-order fp64 sum of the CTA partials
@@ -243,6 +370,7 @@ template <typename T>
 __global__ void __launch_bounds__(kReduceWarps * 32) reduce_partials_kernel(
     HistArgs a, int nseg, int k_alloc, int d, int max_bin, double* out, const double* parent,
     double* sibling) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the histogram kernel's partials (PDL launch)
   const T* part_g = static_cast<const T*>(a.part_g);
   const T* part_h = static_cast<const T*>(a.part_h);
   const int cells = k_alloc * 32;
@@ -445,6 +573,8 @@ void set_smem_attr_t(int device) {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
     set_max_shared_carveout(reinterpret_cast<const void*>(hist_kernel<BITS, K, false, T>));
     set_max_shared_carveout(reinterpret_cast<const void*>(hist_kernel<BITS, K, true, T>));
+    HBG_CUDA(cudaFuncSetAttribute(hist_kernel<BITS, K, false, T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    HBG_CUDA(cudaFuncSetAttribute(hist_kernel<BITS, K, true, T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   });
 }
 
@@ -492,6 +622,63 @@ int occupancy_for(int bits, int k_alloc, int threads, size_t smem, int device, i
   return occ;
 }
 
+using HistKernel = void (*)(HistArgs);
+
+template <typename T>
+HistKernel hist_kernel_ptr_t(int bits, int k_alloc, bool ri) {
+  if (bits == 4) return ri ? hist_kernel<4, 16, true, T> : hist_kernel<4, 16, false, T>;
+  if (k_alloc == 64) return ri ? hist_kernel<8, 64, true, T> : hist_kernel<8, 64, false, T>;
+  if (k_alloc == 128) return ri ? hist_kernel<8, 128, true, T> : hist_kernel<8, 128, false, T>;
+  return ri ? hist_kernel<8, 256, true, T> : hist_kernel<8, 256, false, T>;
+}
+
+HistKernel hist_kernel_ptr(int bits, int k_alloc, bool ri, int acc_bytes) {
+  return acc_bytes == 8 ? hist_kernel_ptr_t<double>(bits, k_alloc, ri) : hist_kernel_ptr_t<float>(bits, k_alloc, ri);
+}
+
+// How many clusters of C CTAs (block `threads`, `smem` bytes each) can be
+// resident at once on `device` (0: none). Cached.
+int max_active_clusters(int bits, int k_alloc, int threads, size_t smem, int device, int acc_bytes, int C) {
+  struct Key {
+    int device, bits, k, threads, acc, C;
+    size_t smem;
+    int n;
+  };
+  static std::mutex m;
+  static std::vector<Key> cache;
+  {
+    std::lock_guard<std::mutex> lk(m);
+    for (const Key& c : cache)
+      if (c.device == device && c.bits == bits && c.k == k_alloc && c.threads == threads && c.acc == acc_bytes &&
+          c.smem == smem && c.C == C)
+        return c.n;
+  }
+  set_smem_attr<8, 64>(device);
+  set_smem_attr<4, 16>(device);
+  set_smem_attr<8, 128>(device);
+  set_smem_attr<8, 256>(device);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, reinterpret_cast<const void*>(hist_kernel_ptr(bits, k_alloc, false, acc_bytes)),
+                                     &cfg) != cudaSuccess) {
+    n = 0;
+    (void)cudaGetLastError();
+  }
+  std::lock_guard<std::mutex> lk(m);
+  cache.push_back(Key{device, bits, k_alloc, threads, acc_bytes, C, smem, n});
+  return n;
+}
+
 }  // namespace
 
 void configure_hist_kernels(int device) {
@@ -528,7 +715,7 @@ int sm_count(int device) {
 constexpr int64_t kDirectRows = 1024;
 
 HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int device, bool allow_direct,
-                        int acc_bytes) {
+                        int acc_bytes, bool allow_fused) {
   HistPlan p{};
   p.bits = bits;
   p.acc_bytes = acc_bytes;
@@ -569,7 +756,7 @@ HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int de
   p.warps = gb * p.wpg;
   p.smem = p.warps * ghw + gb * cntw;
   p.nblocks = (num_groups + gb - 1) / gb;
-  if (allow_direct && n <= kDirectRows) {
+  if (allow_direct && !allow_fused && n <= kDirectRows) {
     // one row segment: each CTA folds and writes the final histogram itself;
     // as many warps as there are 32-row tiles (the fold runs on all of them)
     const int max_wpg = std::max(1, warps_full / gb);
@@ -582,6 +769,54 @@ HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int de
     p.ctas = p.nblocks;
     p.part_values = 0;
     return p;
+  }
+  if (allow_fused) {
+    const int64_t tiles = (n + 32 * rpl - 1) / (32 * rpl);
+    const int max_wpg = std::max(1, warps_full / gb);
+    // Up to ~4 tiles per row warp on the clusters that fit: clusters of C
+    // CTAs, one row segment per CTA, the segments' sub-histograms summed over
+    // distributed shared memory (hist_kernel's cluster mode) — no grid
+    // barrier, no cooperative launch (so PDL overlaps consecutive calls).
+    {
+      const size_t subw = cells * (2 * static_cast<size_t>(acc_bytes) + 4);  // a CTA's sub-histogram, per group
+      const size_t fixed = gb * (cntw + subw) + 16;
+      const int max_wpg_c = fixed >= smem_max ? 0 : static_cast<int>(std::min<size_t>(
+          max_wpg, (smem_max - fixed) / (static_cast<size_t>(gb) * ghw)));
+      const int cta_cap = p.k_alloc >= 256 ? 4 : 16;
+      if (max_wpg_c >= 1 && gb * max_wpg_c <= cta_cap) {
+        const size_t smem_full = static_cast<size_t>(gb * max_wpg_c) * ghw + gb * (cntw + subw) + 16;
+        const int warps_full_c = std::min(cta_cap, std::max(gb * max_wpg_c, 8));
+        int C = 0, kmax = 0;
+        for (int c : {16, 8}) {
+          const int m = max_active_clusters(bits, p.k_alloc, warps_full_c * 32, smem_full, device, acc_bytes, c);
+          if (m / p.nblocks >= 1) {
+            C = c;
+            kmax = m / p.nblocks;
+            break;
+          }
+        }
+        const int64_t slots = static_cast<int64_t>(C) * max_wpg_c;  // row warps per cluster
+        if (C > 0 && tiles <= 4 * slots * kmax) {
+          const int K = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kmax, (tiles + 2 * slots - 1) / (2 * slots))));
+          // the fewest row warps that keep every warp at <= 2 tiles (or all of them)
+          const int64_t want = (tiles + 2 * static_cast<int64_t>(K) * C - 1) / (2 * static_cast<int64_t>(K) * C);
+          const int wpg_c = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max_wpg_c, want)));
+          const int cta_warps = std::min(cta_cap, std::max(gb * wpg_c, 8));
+          int64_t seg_len = (n + static_cast<int64_t>(K) * C - 1) / (static_cast<int64_t>(K) * C);
+          seg_len = std::max<int64_t>(32, (seg_len + 31) / 32 * 32);
+          p.wpg = wpg_c;
+          p.warps = std::max(cta_warps, gb * wpg_c);
+          p.smem = static_cast<size_t>(gb * wpg_c) * ghw + gb * (cntw + subw) + 16;
+          p.seg_len = seg_len;
+          p.nseg = K * C;
+          p.cluster = C;
+          p.nclusters = K;
+          p.ctas = p.nblocks * K * C;
+          p.part_values = K > 1 ? static_cast<size_t>(p.nblocks) * K * gb * cells : 0;
+          return p;
+        }
+      }
+    }
   }
   const int occ = occupancy_for(bits, p.k_alloc, p.warps * 32, p.smem, device, acc_bytes);
   const int64_t slots = static_cast<int64_t>(sm_count(device)) * occ;  // CTAs per wave
@@ -610,25 +845,35 @@ HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int de
   return p;
 }
 
-template <typename T>
-void launch_histogram_t(const HistPlan& plan, const HistArgs& args, cudaStream_t s) {
-  const dim3 grid(plan.ctas), block(plan.warps * 32);
-  const bool ri = args.gh_indexed != 0;
-  if (plan.bits == 4) {
-    (ri ? hist_kernel<4, 16, true, T> : hist_kernel<4, 16, false, T>)<<<grid, block, plan.smem, s>>>(args);
-  } else if (plan.k_alloc == 64) {
-    (ri ? hist_kernel<8, 64, true, T> : hist_kernel<8, 64, false, T>)<<<grid, block, plan.smem, s>>>(args);
-  } else if (plan.k_alloc == 128) {
-    (ri ? hist_kernel<8, 128, true, T> : hist_kernel<8, 128, false, T>)<<<grid, block, plan.smem, s>>>(args);
-  } else {
-    (ri ? hist_kernel<8, 256, true, T> : hist_kernel<8, 256, false, T>)<<<grid, block, plan.smem, s>>>(args);
-  }
-  HBG_LAUNCH_CHECK();
-}
-
 void launch_histogram(const HistPlan& plan, const HistArgs& args, cudaStream_t s) {
-  if (plan.acc_bytes == 8) launch_histogram_t<double>(plan, args, s);
-  else launch_histogram_t<float>(plan, args, s);
+  const dim3 grid(plan.ctas), block(plan.warps * 32);
+  const HistKernel kern = hist_kernel_ptr(plan.bits, plan.k_alloc, args.gh_indexed != 0, plan.acc_bytes);
+  // Every variant is launched with programmatic stream serialization (PDL):
+  // its launch and shared-memory clear overlap the previous kernel's tail
+  // (the kernel waits in griddepcontrol.wait before touching global memory).
+  static const bool pdl = std::getenv("HBG_NO_PDL") == nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = plan.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[3];
+  int na = 0;
+  if (pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (plan.cluster > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = plan.cluster;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  HBG_CUDA(cudaLaunchKernelEx(&cfg, kern, args));
 }
 
 size_t hist_exchange_doubles(int k_alloc, int max_bin, int num_groups) {
@@ -647,10 +892,17 @@ void launch_reduce_exchange(const HistPlan& plan, const HistArgs& args, int num_
 void launch_reduce_partials(const HistPlan& plan, const HistArgs& args, int num_features,
                             int max_bin, double* d_hist, cudaStream_t s, const double* parent,
                             double* sibling) {
-  const dim3 block(kReduceWarps * 32), grid(std::min(plan.k_alloc, max_bin), args.num_groups);
-  (plan.acc_bytes == 8 ? reduce_partials_kernel<double> : reduce_partials_kernel<float>)<<<grid, block, 0, s>>>(
-      args, plan.nseg, plan.k_alloc, num_features, max_bin, d_hist, parent, sibling);
-  HBG_LAUNCH_CHECK();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(std::min(plan.k_alloc, max_bin), args.num_groups);
+  cfg.blockDim = dim3(kReduceWarps * 32);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // launch overlaps the histogram's tail
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = std::getenv("HBG_NO_PDL") == nullptr ? 1 : 0;
+  HBG_CUDA(cudaLaunchKernelEx(&cfg, plan.acc_bytes == 8 ? reduce_partials_kernel<double> : reduce_partials_kernel<float>,
+                              args, plan.nseg, plan.k_alloc, num_features, max_bin, d_hist, parent, sibling));
 }
 
 void launch_pack(const uint8_t* d_cols, int f0, int nf, int num_features, int64_t num_rows,
