@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["hbg", "reference"], default="hbg")
     ap.add_argument("--rows", type=int, default=ROWS)
+    ap.add_argument("--rows-total", type=int, default=0,
+                    help="strong scaling: this many rows in total, sharded over the ranks (sec/tree per N)")
     ap.add_argument("--features", type=int, default=FEATURES)
     ap.add_argument("--max-bin", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -239,6 +241,13 @@ def run_hbg(args):
         dist.init_process_group("nccl", device_id=dev)
 
     n, d, k = args.rows, args.features, args.max_bin
+    strong = args.rows_total > 0
+    if strong:  # fixed total work: rank r owns its shard of rows_total rows (dist.shard_rows)
+        from paper_1706_08359_b200.dist import shard_rows
+
+        b0, e0 = shard_rows(args.rows_total, rank, world)
+        n = e0 - b0
+    total = args.rows_total if strong else world * n
     bits = 4 if k <= 16 else 8
     cols, g, h = synthetic(n, d, k, seed=rank)
     idx = leaf_sample(n, 0, rank)
@@ -326,14 +335,14 @@ def run_hbg(args):
     if world > 1:
         dist.all_reduce(ms_step, op=dist.ReduceOp.MAX)
     ms_step = float(ms_step.item())
-    value = world * n * d / (ms_step / 1e3)
+    value = total * d / (ms_step / 1e3)
 
     # --- roofline of the dominant kernel (the histogram kernel)
     kern_avg_s = kern_ms / max(launches, 1) / 1e3
     alg = algorithmic_bytes(n, d, k, bits)
     peak, peak_src = hbm_peak()
     achieved = alg / kern_avg_s / 1e9
-    workload = f"higgs-{n}x{d}-k{k}-root-leaf"
+    workload = f"higgs-{total}x{d}-k{k}-root-leaf" + (f"-sharded{world}" if strong and world > 1 else "")
 
     result = {
         "metric": "histogram build rows*features/sec",
@@ -344,12 +353,13 @@ def run_hbg(args):
         "warmup": args.warmup,
         "ms_per_step": ms_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if strong else "weak",
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (numpy; reference generator distribution: bins U[1,k-1], g=2u-1, h=u)",
         "config": {
-            "workload": workload, "rows_per_gpu": n, "features": d, "max_bin": k, "bits_per_bin": bits,
+            "workload": workload, "rows_per_gpu": n, "rows_total": total, "features": d, "max_bin": k,
+            "bits_per_bin": bits,
             "leaf_depth": 0, "leaf": "explicit int32 indices + leaf-aligned fp32 g/h",
             "l2": f"inputs {(n * (d * bits / 8 + 12)) / 1e6:.0f} MB > 126 MB L2; no flush needed",
             "parallelism": f"row-sharded x{world}" + (f"; leaf-histogram exchange: {exchange}" if world > 1 else ""),
@@ -390,7 +400,7 @@ def run_hbg(args):
         hbg.build_histograms_partitioned(ds, page_leaf)
     page_ms = (time.perf_counter() - t0p) * 1e3 / e2e_steps
     result["e2e"] = {
-        "value": world * n * d / (e2e_ms / 1e3), "unit": "rows*features/s",
+        "value": total * d / (e2e_ms / 1e3), "unit": "rows*features/s",
         # a contiguous leaf (the root) uploads no indices: the library checks
         # idx[i] == idx[0] + i on the host while g/h are in flight
         "h2d_bytes_per_step": int(n * (8 + 8) + (0 if contiguous else 4 * n)), "d2h_bytes_per_step": int(out.nbytes),
@@ -506,10 +516,10 @@ def run_hbg(args):
             dist.all_reduce(t_tree, op=dist.ReduceOp.MAX)
         t_tree = float(t_tree.item())
         km, kl = ds.kernel_time()
-        built = world * n + int(np.minimum(log["left_count"], log["right_count"])[: max(len(log) - 1, 0)].sum())
+        built = total + int(np.minimum(log["left_count"], log["right_count"])[: max(len(log) - 1, 0)].sum())
         result["tree"] = {
             "num_leaves": args.num_leaves, "splits": int(len(log)), "sec_per_tree": t_tree,
-            "rows_total": world * n,
+            "rows_total": total,
             "hist_rows_built": built, "hist_launches_per_tree": kl / args.trees,
             "hist_kernel_ms_per_tree": km / args.trees,
             "rows_features_per_s_built": built * d / t_tree,
