@@ -71,6 +71,42 @@ def gpu_hist_and_tree(cols, g, h, k, stream, trees=2, leaves=255, min_data=1):
     return res
 
 
+def bits64_tree_parity(cols, g, h, k, leaves=255, min_data=1):
+    """The PrecisionMode::bits64 device tree against the unmodified reference's
+    bits64 grow_tree on the same data: identical splits until the first fp64
+    tie (the two choices' exactly-summed gains equal to 1e-12), which is what
+    tests/test_gpu_precision.py requires."""
+    sys.path.insert(0, os.path.join(REPO, "tests"))
+    from oracle import ffi
+    from test_gpu_parity import exact_gain, rows_of_node
+
+    with hbg.Dataset(cols, k) as ds:
+        t0 = time.perf_counter()
+        log, nodes = ds.grow_tree_host(g, h, leaves, min_data, 0.0, precision=64)
+        t_gpu = time.perf_counter() - t0
+    rd = ffi.RefDataset(cols, k)
+    t_ref, rlog = rd.grow_tree_timed(g, h, leaves, min_data, 0.0, 64)
+    rd.close()
+    _, rnodes = ffi.grow_tree(cols, k, g, h, leaves, min_data, 0.0, 64)
+    same = 0
+    while (same < min(len(log), len(rlog)) and log["feature"][same] == rlog["feature"][same]
+           and log["threshold_bin"][same] == rlog["threshold_bin"][same]
+           and log["left_count"][same] == rlog["left_count"][same]):
+        same += 1
+    out = {"splits_identical": same, "splits_total": int(len(rlog)), "gpu_host_dropin_s": t_gpu,
+           "cpu_reference_s": t_ref}
+    if same < len(rlog):
+        jo = int(np.nonzero(nodes["left"] == 2 * same + 1)[0][0])
+        jr = int(np.nonzero(np.asarray(rnodes["left"]) == 2 * same + 1)[0][0])
+        ours = exact_gain(cols, g, h, rows_of_node(cols, nodes, jo), int(log["feature"][same]),
+                          int(log["threshold_bin"][same]), 0.0)
+        ref = exact_gain(cols, g, h, rows_of_node(cols, rnodes, jr), int(rlog["feature"][same]),
+                         int(rlog["threshold_bin"][same]), 0.0)
+        out["first_divergence_exact_gains"] = [ours, ref]
+        out["first_divergence_is_fp64_tie"] = bool(abs(ours - ref) <= 1e-12 * max(1.0, abs(ref)))
+    return out
+
+
 def cpu_reference(cols, g, h, k, leaves=255, min_data=1, tree=True):
     from oracle import ffi
 
@@ -91,7 +127,7 @@ def cpu_reference(cols, g, h, k, leaves=255, min_data=1, tree=True):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="1,2,3,4,5")
-    ap.add_argument("--out", default=os.path.join(REPO, "profiles", "r01_configs.json"))
+    ap.add_argument("--out", default=os.path.join(REPO, "profiles", "r02_configs.json"))
     ap.add_argument("--expo-rows", type=int, default=250_000_000)
     args = ap.parse_args()
     want = {int(c) for c in args.configs.split(",")}
@@ -123,11 +159,13 @@ def main():
     if 1 in want:  # Higgs 1M x 28, k64, 255-leaf tree (the CPU parity config)
         cols, g, h = synthetic(1_000_000, 28, 64, 1)
         record("config1_higgs_1Mx28_k64", gpu_hist_and_tree(cols, g, h, 64, stream), cpu_reference(cols, g, h, 64))
+        results["config1_higgs_1Mx28_k64"]["bits64_tree"] = bits64_tree_parity(cols, g, h, 64)
     if 2 in want:  # Higgs 10.5M x 28: 16-bin 4-bit vs 64-bin 8-bit
         for k in (16, 64):
             cols, g, h = synthetic(10_500_000, 28, k, 2)
             record(f"config2_higgs_10.5Mx28_k{k}", gpu_hist_and_tree(cols, g, h, k, stream),
                    cpu_reference(cols, g, h, k))
+            results[f"config2_higgs_10.5Mx28_k{k}"]["bits64_tree"] = bits64_tree_parity(cols, g, h, k)
     if 3 in want:  # epsilon 400K x 2000, k64: one full boosting iteration
         cols, g, h = synthetic(400_000, 2000, 64, 3)
         gpu = gpu_hist_and_tree(cols, g, h, 64, stream, trees=1)
