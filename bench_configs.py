@@ -100,7 +100,8 @@ def bits64_tree_parity(cols, g, h, k, leaves=255, min_data=1):
         jr = int(np.nonzero(np.asarray(rnodes["left"]) == 2 * same + 1)[0][0])
         ours = exact_gain(cols, g, h, rows_of_node(cols, nodes, jo), int(log["feature"][same]),
                           int(log["threshold_bin"][same]), 0.0)
-        ref = exact_gain(cols, g, h, rows_of_node(cols, rnodes, jr), int(rlog["feature"][same]),
+        # every split before `same` agreed, so leaf jr has the same rows in both trees
+        ref = exact_gain(cols, g, h, rows_of_node(cols, nodes, jr), int(rlog["feature"][same]),
                          int(rlog["threshold_bin"][same]), 0.0)
         out["first_divergence_exact_gains"] = [ours, ref]
         out["first_divergence_is_fp64_tie"] = bool(abs(ours - ref) <= 1e-12 * max(1.0, abs(ref)))
