@@ -75,10 +75,13 @@ typedef struct hbg_layout {
   int32_t bits_per_bin;      /* 4 iff max_bin <= 16 (prepare_packed, binning.cpp:230) else 8 */
   int32_t features_per_word; /* 8 or 4 */
   int32_t words_per_row;     /* ceil(num_features / features_per_word) */
-  int32_t row_stride_bytes;  /* num_groups * slice_bytes */
+  int32_t row_stride_bytes;  /* slice_bytes: rows of one slice group are contiguous */
   int32_t slice_bytes;       /* 16 (4-bit) or 32 (8-bit) */
   int32_t num_groups;        /* ceil(num_features / 32) */
   int32_t device;
+  int64_t group_stride_bytes; /* slice group g of row r at packed + g*group_stride + r*row_stride
+                                 (group-planar: a warp's 32 consecutive rows of one group are one
+                                 contiguous 1 KB, whatever the number of groups) */
 } hbg_layout;
 
 const char* hbg_last_error(void);

@@ -132,6 +132,7 @@ class hbg_layout(C.Structure):
         ("slice_bytes", C.c_int32),
         ("num_groups", C.c_int32),
         ("device", C.c_int32),
+        ("group_stride_bytes", C.c_int64),
     ]
 
 

@@ -100,7 +100,7 @@ struct GrowArgs {
   const uint8_t* packed;
   const uint8_t* colbins;  // [d][N] uint8: one byte per (feature, row)
   int64_t nrows;
-  int64_t row_stride;
+  int64_t row_stride, group_stride;  // group-planar packed layout
   int words_per_row, bits, d, k, num_groups;
   int32_t* rows[2];
   float* g[2];
@@ -1478,7 +1478,7 @@ __device__ void hist_smem_item(const GrowArgs& a, const Desc& D, int item, unsig
       const int64_t s0 = static_cast<int64_t>(seg) * D.seg_len;
       const int64_t s1 = min(s0 + D.seg_len, n);
       const uint32_t gh_base = smem_addr(gh + static_cast<size_t>(w) * kCells);
-      const unsigned char* base = a.packed + static_cast<size_t>(group) * Slice<BITS>::kWords * 4;
+      const unsigned char* base = a.packed + static_cast<int64_t>(group) * a.group_stride;
       accumulate_rows<BITS, K>(a, rows, g, h, s0, s1, sub, base, gh_base, cnt + static_cast<size_t>(gl) * kCells);
     }
   }
@@ -2666,6 +2666,7 @@ const void* launch_grow_persistent(const PersistentGrowArgs& h, int device, cuda
   a.colbins = h.colbins;
   a.nrows = h.num_rows;
   a.row_stride = h.row_stride;
+  a.group_stride = h.group_stride;
   a.words_per_row = h.words_per_row;
   a.bits = h.bits;
   a.d = h.d;

@@ -59,7 +59,8 @@ inline int part_elem_bytes(const HistPlan& p) { return p.cluster > 1 ? 8 : p.acc
 
 struct HistArgs {
   const uint8_t* packed;
-  int64_t row_stride;  // bytes
+  int64_t row_stride;  // bytes between rows of one slice group (slice_bytes)
+  int64_t group_stride;  // bytes between slice groups (group-planar layout)
   const int32_t* idx;  // nullptr: identity leaf
   int64_t n;
   const void* g;  // float (bits32) or double (bits64) per HistPlan::acc_bytes
@@ -124,7 +125,7 @@ void launch_reduce_exchange(const HistPlan& plan, const HistArgs& args, int num_
 // Packs features [f0, f0 + nf) (one 32-feature slice group; d_cols holds
 // their column-major bins) into the group's words of every row.
 void launch_pack(const uint8_t* d_cols, int f0, int nf, int num_features, int64_t num_rows,
-                 int max_bin, int bits, int row_stride_words, uint32_t* d_packed, int* d_bad,
+                 int max_bin, int bits, int64_t group_stride_words, uint32_t* d_packed, int* d_bad,
                  cudaStream_t s);
 void launch_iota(int32_t* out, int64_t n, cudaStream_t s);
 void launch_f64_to_f32(const double* in, float* out, int64_t n, cudaStream_t s);
@@ -186,7 +187,7 @@ size_t small_hist_acc_bytes(int d, int k);
 // fixed-point scales exps[0..1] from one leaf's rows (n <= kAtomicHistRows; one block)
 void launch_fixed_leaf_scale(const float* g, const float* h, int64_t n, int* exps, cudaStream_t s);
 void launch_small_hist(const int32_t* rows, const float* g, const float* h, int64_t n,
-                       const uint32_t* packed, int stride_words, int words_per_row, int bits, int d, int k,
+                       const uint32_t* packed, int64_t group_stride_words, int words_per_row, int bits, int d, int k,
                        const int* exps, void* acc, double* out, const double* parent, double* sibling,
                        cudaStream_t s);
 
@@ -207,7 +208,7 @@ struct FinishScanArgsHost {
 };
 void launch_finish_scan(const FinishScanArgsHost& a, cudaStream_t s);
 void launch_small_hist_atomic(const int32_t* rows, const float* g, const float* h, int64_t n,
-                              const uint32_t* packed, int stride_words, int words_per_row, int bits, int d,
+                              const uint32_t* packed, int64_t group_stride_words, int words_per_row, int bits, int d,
                               int k, const int* exps, void* acc, cudaStream_t s);
 
 // Persistent tree grower (grow_persistent.cu): all splits of one tree in a
@@ -216,6 +217,7 @@ struct PersistentGrowArgs {
   const uint8_t* packed;
   const uint8_t* colbins;  // [d][num_rows] uint8 bins
   int64_t row_stride;
+  int64_t group_stride;  // group-planar packed layout
   int words_per_row, bits, d, k, num_groups;
   int64_t num_rows;
   int32_t* rows[2];

@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(K >= 256 ? 128 : 512, BITS == 4 ? 2 : 1) hist_
     const int64_t s1 = min(s0 + a.seg_len, a.n);
     const uint32_t gh_base = smem_addr(gh + static_cast<size_t>(w) * kCells);
     uint32_t* cnt_g = cnt + static_cast<size_t>(gl) * kCells;
-    const unsigned char* base = a.packed + static_cast<size_t>(group) * Slice<BITS>::kWords * 4;
+    const unsigned char* base = a.packed + static_cast<int64_t>(group) * a.group_stride;
     constexpr int R = rows_per_lane<K, T>();
     const int64_t step = static_cast<int64_t>(a.wpg) * 32 * R;
 
@@ -528,7 +528,7 @@ __global__ void __launch_bounds__(kReduceWarps * 32) reduce_exchange_kernel(
 // w*fpw .. w*fpw+fpw-1 at bits*p. One launch covers one 32-feature slice
 // group (its words_per_slice words); pad slots are 0.
 __global__ void pack_kernel(const uint8_t* cols, int f0, int nf, int64_t n, int max_bin, int bits,
-                            int stride_words, uint32_t* packed, int* bad) {
+                            int64_t gs_words, uint32_t* packed, int* bad) {
   const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const int fpw = 32 / bits;
@@ -541,7 +541,8 @@ __global__ void pack_kernel(const uint8_t* cols, int f0, int nf, int64_t n, int 
     if (b >= static_cast<uint32_t>(max_bin)) atomicOr(bad, 1);
     word |= b << (bits * p);
   }
-  packed[static_cast<size_t>(r) * stride_words + w] = word;
+  const int wps = 32 / fpw;  // words per 32-feature slice (group-planar layout)
+  packed[static_cast<size_t>(w / wps) * gs_words + static_cast<size_t>(r) * wps + w % wps] = word;
 }
 
 __global__ void f64_to_f32_kernel(const double* in, float* out, int64_t n) {
@@ -906,13 +907,13 @@ void launch_reduce_partials(const HistPlan& plan, const HistArgs& args, int num_
 }
 
 void launch_pack(const uint8_t* d_cols, int f0, int nf, int num_features, int64_t num_rows,
-                 int max_bin, int bits, int row_stride_words, uint32_t* d_packed, int* d_bad,
+                 int max_bin, int bits, int64_t group_stride_words, uint32_t* d_packed, int* d_bad,
                  cudaStream_t s) {
   (void)num_features;
   if (num_rows == 0) return;
   const int words_per_slice = bits == 4 ? 4 : 8;  // 32 features per slice
   const dim3 block(256), grid(static_cast<unsigned>((num_rows + 255) / 256), words_per_slice);
-  pack_kernel<<<grid, block, 0, s>>>(d_cols, f0, nf, num_rows, max_bin, bits, row_stride_words,
+  pack_kernel<<<grid, block, 0, s>>>(d_cols, f0, nf, num_rows, max_bin, bits, group_stride_words,
                                      d_packed, d_bad);
   HBG_LAUNCH_CHECK();
 }

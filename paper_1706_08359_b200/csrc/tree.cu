@@ -342,7 +342,7 @@ __global__ void fixed_leaf_scale_kernel(const float* __restrict__ g, const float
 // Thread = (row, 32-bit word of the packed row): the word's features.
 __global__ void small_hist_atomic_kernel(const int32_t* __restrict__ rows, const float* __restrict__ g,
                                          const float* __restrict__ h, int64_t n,
-                                         const uint32_t* __restrict__ packed, int stride_words,
+                                         const uint32_t* __restrict__ packed, int64_t gs_words,
                                          int words_per_row, int bits, int d, int k,
                                          const int* __restrict__ exps, unsigned long long* __restrict__ acc) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -350,7 +350,9 @@ __global__ void small_hist_atomic_kernel(const int32_t* __restrict__ rows, const
   const int64_t pos = t / words_per_row;
   const int w = static_cast<int>(t - pos * words_per_row);
   const int32_t row = rows[pos];
-  const uint32_t word = __ldg(packed + static_cast<int64_t>(row) * stride_words + w);
+  // group-planar layout: word w of a row sits in slice group w / wps
+  const int wps = bits == 8 ? 8 : 4;  // words per 32-feature slice
+  const uint32_t word = __ldg(packed + (w / wps) * gs_words + static_cast<int64_t>(row) * wps + w % wps);
   const int64_t qg = __double2ll_rn(ldexp(static_cast<double>(g[pos]), exps[0]));
   const int64_t qh = __double2ll_rn(ldexp(static_cast<double>(h[pos]), exps[1]));
   const int fpw = 32 / bits;
@@ -409,25 +411,25 @@ void launch_fixed_leaf_scale(const float* g, const float* h, int64_t n, int* exp
 }
 
 void launch_small_hist_atomic(const int32_t* rows, const float* g, const float* h, int64_t n,
-                              const uint32_t* packed, int stride_words, int words_per_row, int bits, int d,
+                              const uint32_t* packed, int64_t gs_words, int words_per_row, int bits, int d,
                               int k, const int* exps, void* acc, cudaStream_t s) {
   const int64_t items = n * words_per_row;
   if (items == 0) return;
   small_hist_atomic_kernel<<<static_cast<unsigned>((items + 255) / 256), 256, 0, s>>>(
-      rows, g, h, n, packed, stride_words, words_per_row, bits, d, k, exps,
+      rows, g, h, n, packed, gs_words, words_per_row, bits, d, k, exps,
       static_cast<unsigned long long*>(acc));
   HBG_LAUNCH_CHECK();
 }
 
 void launch_small_hist(const int32_t* rows, const float* g, const float* h, int64_t n,
-                       const uint32_t* packed, int stride_words, int words_per_row, int bits, int d, int k,
+                       const uint32_t* packed, int64_t gs_words, int words_per_row, int bits, int d, int k,
                        const int* exps, void* acc, double* out, const double* parent, double* sibling,
                        cudaStream_t s) {
   unsigned long long* a = static_cast<unsigned long long*>(acc);
   const int64_t items = n * words_per_row;
   if (items > 0) {
     small_hist_atomic_kernel<<<static_cast<unsigned>((items + 255) / 256), 256, 0, s>>>(
-        rows, g, h, n, packed, stride_words, words_per_row, bits, d, k, exps, a);
+        rows, g, h, n, packed, gs_words, words_per_row, bits, d, k, exps, a);
     HBG_LAUNCH_CHECK();
   }
   const int64_t cells = static_cast<int64_t>(d) * k;
