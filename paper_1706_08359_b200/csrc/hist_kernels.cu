@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(K >= 256 ? 128 : 512, BITS == 4 ? 2 : 1) hist_
 // feature) x kReduceWarps warps; warp w sums segments w, w+W, ... in order,
 // then the warps' sums are combined in warp order: deterministic, and the
 // partial reads are 128-byte coalesced with W independent streams per cell.
-constexpr int kReduceWarps = 16;
+constexpr int kReduceWarps = 32;
 
 template <typename T>
 __global__ void __launch_bounds__(kReduceWarps * 32) reduce_partials_kernel(
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(kReduceWarps * 32) reduce_partials_kernel(
   const int gl = group - bi * a.gb;
   double sg = 0.0, sh = 0.0;
   uint64_t sc = 0;
-#pragma unroll 4
+#pragma unroll 8
   for (int s = w; s < nseg; s += kReduceWarps) {
     const size_t cta = static_cast<size_t>(s) * a.nblocks + bi;
     const size_t o = (cta * a.gb + gl) * cells + c;
