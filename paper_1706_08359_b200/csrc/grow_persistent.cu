@@ -116,6 +116,7 @@ struct GrowArgs {
   unsigned* bar;  // grid barrier word
   uint8_t* flags;
   int64_t* cta_left;
+  int* warp_left;  // per (member, CTA, warp): left rows of the warp's run (large-parent partition)
   double* cta_sums;
   float* part_g;
   float* part_h;
@@ -766,44 +767,42 @@ __device__ void partition_redundant(const GrowArgs& a, Desc& D, RegRows& rr, Par
   __syncthreads();
 }
 
-// Large parents: CTA b owns positions [b*chunk, (b+1)*chunk), processed in
-// tiles of NT*ipt positions (ipt <= kPartItems). Loads and stores are
-// coalesced: position j*NT + t of a tile belongs to thread t (pass 1), and
-// pass 2 stages the tile in shared memory, ranks it there in position order,
-// and writes the left and the right rows of the tile as two contiguous runs.
-template <int NT>
-__device__ __forceinline__ int part_ipt(int64_t n) {
-  const int64_t per = (n + static_cast<int64_t>(gridDim.x) * NT - 1) / (static_cast<int64_t>(gridDim.x) * NT);
-  return static_cast<int>(per < 1 ? 1 : (per > kPartItems ? kPartItems : per));
-}
-
+// Large parents: CTA b owns the positions [b*chunk, (b+1)*chunk) of the
+// parent, and warp w of it the contiguous run [b*chunk + w*wchunk, ...)
+// (wchunk a multiple of 32). Both passes stream a warp's run 32 positions at a
+// time — every load and store coalesced — with kPartItems steps in flight;
+// pass 1 also records each warp's left count, so pass 2 knows where every
+// warp's rows go and places them by warp ballots: no shared-memory staging,
+// no block-wide scan inside the loop.
 template <int NT>
 __device__ __forceinline__ int64_t part_chunk(int64_t n) {
-  const int64_t tile = static_cast<int64_t>(NT) * part_ipt<NT>(n);
+  constexpr int64_t kRun = 32 * (NT / 32);  // one 32-position step per warp
   const int64_t per = (n + gridDim.x - 1) / gridDim.x;
-  return (per + tile - 1) / tile * tile;
+  return (per + kRun - 1) / kRun * kRun;
 }
 
-// Pass 1 (every CTA, its chunk): side flags, left count, fp64 side sums
-// (each thread in its fixed position order, then a fixed-order block sum).
+// Pass 1 (every CTA, its chunk): side flags, fp64 side sums (each lane in its
+// fixed position order, then a fixed-order block sum), the CTA's and each
+// warp's left counts.
 template <int NT>
 __device__ void partition_count(const GrowArgs& a, const Desc& D, PartShared<NT>& ps) {
-  const int64_t n = D.count, chunk = part_chunk<NT>(n);
-  const int64_t s = static_cast<int64_t>(blockIdx.x) * chunk, e = min(n, s + chunk);
+  constexpr int W = NT / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t n = D.count, chunk = part_chunk<NT>(n), wchunk = chunk / W;
+  const int64_t ws = static_cast<int64_t>(blockIdx.x) * chunk + w * wchunk;
+  const int64_t we = min(n, ws + wchunk);
   const int32_t* rin = a.rows[D.buf_in] + D.begin;
   const float* gin = a.g[D.buf_in] + D.begin;
   const float* hin = a.h[D.buf_in] + D.begin;
   double v[4] = {0.0, 0.0, 0.0, 0.0};
   long long c = 0;
-  const int ipt = part_ipt<NT>(n);
-  const int64_t step = static_cast<int64_t>(NT) * ipt;
-  // software pipeline: tile t+1's (row, g, h) loads are in flight while tile
-  // t's bins (dependent on its rows) are fetched and its flags written
-  auto load = [&](int64_t t0, int32_t(&r)[kPartItems], float(&gv)[kPartItems], float(&hv)[kPartItems]) {
+  // software pipeline: the next steps' (row, g, h) loads are in flight while
+  // this batch's bins (dependent on its rows) are gathered and its flags written
+  auto load = [&](int64_t p0, int32_t(&r)[kPartItems], float(&gv)[kPartItems], float(&hv)[kPartItems]) {
 #pragma unroll
     for (int j = 0; j < kPartItems; ++j) {
-      const int64_t pos = t0 + static_cast<int64_t>(j) * NT + threadIdx.x;
-      const bool ok = j < ipt && pos < e;
+      const int64_t pos = p0 + 32 * j + lane;
+      const bool ok = pos < we;
       r[j] = ok ? __ldcg(rin + pos) : 0;
       gv[j] = ok ? __ldcg(gin + pos) : 0.f;
       hv[j] = ok ? __ldcg(hin + pos) : 0.f;
@@ -811,21 +810,18 @@ __device__ void partition_count(const GrowArgs& a, const Desc& D, PartShared<NT>
   };
   int32_t r[kPartItems];
   float gv[kPartItems], hv[kPartItems];
-  load(s, r, gv, hv);
-  for (int64_t t0 = s; t0 < e; t0 += step) {
+  load(ws, r, gv, hv);
+  for (int64_t p0 = ws; p0 < we; p0 += 32 * kPartItems) {
     uint32_t bin[kPartItems];
 #pragma unroll
-    for (int j = 0; j < kPartItems; ++j) {
-      const int64_t pos = t0 + static_cast<int64_t>(j) * NT + threadIdx.x;
-      bin[j] = j < ipt && pos < e ? col_bin(a, r[j], D.feature) : 0u;
-    }
+    for (int j = 0; j < kPartItems; ++j) bin[j] = p0 + 32 * j + lane < we ? col_bin(a, r[j], D.feature) : 0u;
     int32_t r2[kPartItems];
     float g2[kPartItems], h2[kPartItems];
-    load(t0 + step, r2, g2, h2);
+    load(p0 + 32 * kPartItems, r2, g2, h2);
 #pragma unroll
     for (int j = 0; j < kPartItems; ++j) {
-      const int64_t pos = t0 + static_cast<int64_t>(j) * NT + threadIdx.x;
-      if (j >= ipt || pos >= e) continue;
+      const int64_t pos = p0 + 32 * j + lane;
+      if (pos >= we) continue;
       const bool left = bin[j] <= static_cast<uint32_t>(D.thr);  // tree.cpp:117-123
       a.flags[D.begin + pos] = left ? 1 : 0;
       if (left) {
@@ -844,6 +840,8 @@ __device__ void partition_count(const GrowArgs& a, const Desc& D, PartShared<NT>
       hv[j] = h2[j];
     }
   }
+  const int wl = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(c));
+  if (lane == 0) a.warp_left[(static_cast<size_t>(D.mslot) * gridDim.x + blockIdx.x) * W + w] = wl;
   block_sum_4d1<NT>(v, c, ps);
   if (threadIdx.x == 0) {
     const size_t slot = static_cast<size_t>(D.mslot) * gridDim.x + blockIdx.x;
@@ -852,13 +850,15 @@ __device__ void partition_count(const GrowArgs& a, const Desc& D, PartShared<NT>
   }
 }
 
-// After the barrier (every CTA, redundantly): this CTA's offset among the
-// left rows, the left total and the children's totals (fixed-order sum over
-// CTAs), then pass 2: the stable scatter of this CTA's chunk, tile by tile
-// through shared memory (smem: NT*kPartItems x (row, g, h, flag, slot)).
+// Pass 2 (every CTA, its chunk): the parent's totals and left count L, this
+// CTA's and warp's left rows before them, then each warp moves its run: per
+// 32-position step a ballot of the left flags gives every lane its slot —
+// left rows to [lb, ...), right rows to [L + (position - lefts before), ...).
 template <int NT>
-__device__ void partition_scatter(const GrowArgs& a, Desc& D, PartShared<NT>& ps, unsigned char* smem) {
+__device__ void partition_scatter(const GrowArgs& a, Desc& D, PartShared<NT>& ps, unsigned char* /*smem*/) {
+  constexpr int W = NT / 32;
   const int G = gridDim.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   double v[4] = {0.0, 0.0, 0.0, 0.0};
   long long c = 0;
   for (int b = threadIdx.x; b < G; b += NT) {  // G <= NT: one CTA record per thread
@@ -878,108 +878,64 @@ __device__ void partition_scatter(const GrowArgs& a, Desc& D, PartShared<NT>& ps
     if (a.nranks == 1 && L != D.nl) set_error(a, kErrPartition);
   }
   __syncthreads();
-  const int64_t n = D.count, chunk = part_chunk<NT>(n);
-  const int64_t s = static_cast<int64_t>(blockIdx.x) * chunk, e = min(n, s + chunk);
-  if (s >= e) return;
+  const int64_t n = D.count, chunk = part_chunk<NT>(n), wchunk = chunk / W;
+  const int64_t ws = static_cast<int64_t>(blockIdx.x) * chunk + w * wchunk;
+  const int64_t we = min(n, ws + wchunk);
+  if (ws >= we) return;
+  // left rows before this warp: the CTA's prefix + the warps before it in the CTA
+  const int* wl = a.warp_left + (static_cast<size_t>(D.mslot) * G + blockIdx.x) * W;
+  const int mine = lane < w ? __ldcg(wl + lane) : 0;
+  int64_t lb = s_before + static_cast<int64_t>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(mine)));
   const int32_t* rin = a.rows[D.buf_in] + D.begin;
   const float* gin = a.g[D.buf_in] + D.begin;
   const float* hin = a.h[D.buf_in] + D.begin;
+  const uint8_t* fin = a.flags + D.begin;
   int32_t* rout = a.rows[D.buf_out] + D.begin;
   float* gout = a.g[D.buf_out] + D.begin;
   float* hout = a.h[D.buf_out] + D.begin;
-  constexpr int kTile = NT * kPartItems;
-  // two stage buffers (row, g, h, flag) + the output slot map; tile t+1 is
-  // loaded into registers while tile t is ranked and written out
-  struct Stage {
-    int32_t* row;
-    float* g;
-    float* h;
-    uint8_t* flag;
-  };
-  auto stage_of = [&](int b) {  // buffer b of the two (no local-memory array of pointers)
-    Stage st;
-    st.row = reinterpret_cast<int32_t*>(smem + static_cast<size_t>(b) * kTile * 13);
-    st.g = reinterpret_cast<float*>(st.row + kTile);
-    st.h = st.g + kTile;
-    st.flag = reinterpret_cast<uint8_t*>(st.h + kTile);
-    return st;
-  };
-  uint16_t* slot = reinterpret_cast<uint16_t*>(smem + static_cast<size_t>(2) * kTile * 13);  // output slot -> tile position
-  const int ipt = part_ipt<NT>(n);
-  const int64_t step = static_cast<int64_t>(NT) * ipt;
-  int32_t rr[kPartItems];
-  float rg[kPartItems], rh[kPartItems];
-  uint8_t rf[kPartItems];
-  auto fetch = [&](int64_t t0) {  // coalesced: tile position j*NT + t
+  const unsigned below = (1u << lane) - 1u;
+  auto load = [&](int64_t p0, int32_t(&r)[kPartItems], float(&gv)[kPartItems], float(&hv)[kPartItems],
+                  uint8_t(&f)[kPartItems]) {
 #pragma unroll
     for (int j = 0; j < kPartItems; ++j) {
-      const int64_t q = static_cast<int64_t>(j) * NT + threadIdx.x;
-      const bool ok = j < ipt && t0 + q < e;
-      rr[j] = ok ? __ldcg(rin + t0 + q) : 0;
-      rg[j] = ok ? __ldcg(gin + t0 + q) : 0.f;
-      rh[j] = ok ? __ldcg(hin + t0 + q) : 0.f;
-      rf[j] = ok ? __ldcg(a.flags + D.begin + t0 + q) : 0;
+      const int64_t pos = p0 + 32 * j + lane;
+      const bool ok = pos < we;
+      r[j] = ok ? __ldcg(rin + pos) : 0;
+      gv[j] = ok ? __ldcg(gin + pos) : 0.f;
+      hv[j] = ok ? __ldcg(hin + pos) : 0.f;
+      f[j] = ok ? __ldcg(fin + pos) : 0;
     }
   };
-  auto stage = [&](const Stage& b) {
+  int32_t r[kPartItems];
+  float gv[kPartItems], hv[kPartItems];
+  uint8_t f[kPartItems];
+  load(ws, r, gv, hv, f);
+  for (int64_t p0 = ws; p0 < we; p0 += 32 * kPartItems) {
+    int32_t r2[kPartItems];
+    float g2[kPartItems], h2[kPartItems];
+    uint8_t f2[kPartItems];
+    load(p0 + 32 * kPartItems, r2, g2, h2, f2);  // the next batch in flight while this one is placed
 #pragma unroll
     for (int j = 0; j < kPartItems; ++j) {
-      const int q = j * NT + threadIdx.x;
-      if (j < ipt) {
-        b.row[q] = rr[j];
-        b.g[q] = rg[j];
-        b.h[q] = rh[j];
-        b.flag[q] = rf[j];
+      const int64_t pos = p0 + 32 * j + lane;
+      const bool ok = pos < we;
+      const unsigned bl = __ballot_sync(0xffffffffu, ok && f[j]);
+      const int lp = __popc(bl & below);
+      if (ok) {
+        const int64_t dst = f[j] ? lb + lp : L + (pos - lb - lp);
+        rout[dst] = r[j];
+        gout[dst] = gv[j];
+        hout[dst] = hv[j];
       }
+      lb += __popc(bl);
     }
-  };
-  int64_t lrun = s_before, rrun = s - s_before;  // left / right rows before this tile
-  fetch(s);
-  stage(stage_of(0));
-  __syncthreads();
-  int buf = 0;
-  for (int64_t t0 = s; t0 < e; t0 += step, buf ^= 1) {
-    const int64_t mrem = e - t0;
-    const int m = static_cast<int>(mrem < step ? mrem : step);
-    if (t0 + step < e) fetch(t0 + step);  // next tile in flight
-    const Stage cb = stage_of(buf);
-    // this thread's blocked run of tile positions [t*ipt, t*ipt+ipt): ranks
-    uint32_t lf = 0;
-    int cl = 0;
-    const int q0 = threadIdx.x * ipt;
 #pragma unroll
     for (int j = 0; j < kPartItems; ++j) {
-      const bool left = j < ipt && q0 + j < m && cb.flag[q0 + j];
-      lf |= left ? 1u << j : 0u;
-      cl += left ? 1 : 0;
+      r[j] = r2[j];
+      gv[j] = g2[j];
+      hv[j] = h2[j];
+      f[j] = f2[j];
     }
-    const long long lb = block_excl_scan<NT>(cl, ps);  // left rows of the tile before q0
-    __shared__ int s_tile_left;
-    if (threadIdx.x == NT - 1) s_tile_left = static_cast<int>(lb + cl);
-    __syncthreads();
-    const int tl = s_tile_left;
-    int lr = static_cast<int>(lb);
-#pragma unroll
-    for (int j = 0; j < kPartItems; ++j) {
-      const int q = q0 + j;
-      if (j >= ipt || q >= m) continue;
-      const bool left = (lf >> j) & 1u;
-      slot[left ? lr : tl + (q - lr)] = static_cast<uint16_t>(q);
-      lr += left ? 1 : 0;
-    }
-    __syncthreads();
-    // the tile's left rows -> [lrun, lrun+tl), right rows -> [L+rrun, ...): coalesced
-    for (int i = threadIdx.x; i < m; i += NT) {
-      const int q = slot[i];
-      const int64_t dst = i < tl ? lrun + i : L + rrun + (i - tl);
-      rout[dst] = cb.row[q];
-      gout[dst] = cb.g[q];
-      hout[dst] = cb.h[q];
-    }
-    lrun += tl;
-    rrun += m - tl;
-    if (t0 + step < e) stage(stage_of(buf ^ 1));
-    __syncthreads();
   }
 }
 
@@ -2584,8 +2540,7 @@ GrowGeom grow_geometry(const PersistentGrowArgs& h, int device) {
   while (g.wcap < h.d && part_smem_of(g.wcap + 1) <= smem_max) ++g.wcap;
   g.cchunk = std::max(g.fchunk, g.wave ? g.wcap : g.fchunk);
   const size_t part_smem = part_smem_of(g.cchunk);
-  const size_t large_part_smem = static_cast<size_t>(kPartItems) * g.nt * (2 * 13 + 2);  // 2 x (row, g, h, flag) + slot
-  g.smem = std::max({hist_smem, part_smem, large_part_smem});
+  g.smem = std::max(hist_smem, part_smem);
   require(g.ctas <= g.nt, "more CTAs than threads per CTA (per-CTA records are scanned one per thread)");
   require(g.smem <= smem_max, "tree grower: features x bins per scan chunk exceed shared memory "
                               "(too many features for one grid)");
@@ -2628,6 +2583,7 @@ size_t grow_scratch_bytes(const PersistentGrowArgs& h, int device) {
   add(kRep * max_nodes * sizeof(int));        // picked
   add(static_cast<size_t>(h.num_rows) + 16);  // flags
   add(static_cast<size_t>(g.ctas) * 8 * (g.wave ? g.wmax : 1));   // cta_left
+  add(static_cast<size_t>(g.ctas) * (g.nt / 32) * 4 * (g.wave ? g.wmax : 1));  // warp_left
   add(static_cast<size_t>(g.ctas) * 32 * (g.wave ? g.wmax : 1));  // cta_sums
   add(g.part_values * 4 * 3);                 // part_g/h/c
   add(static_cast<size_t>(kRep * 2 * g.nchunks) * sizeof(Cand));
@@ -2730,6 +2686,7 @@ const void* launch_grow_persistent(const PersistentGrowArgs& h, int device, cuda
   a.picked = reinterpret_cast<int*>(take(kRep * max_nodes * sizeof(int)));
   a.flags = take(static_cast<size_t>(h.num_rows) + 16);
   a.cta_left = reinterpret_cast<int64_t*>(take(static_cast<size_t>(g.ctas) * 8 * (g.wave ? g.wmax : 1)));
+  a.warp_left = reinterpret_cast<int*>(take(static_cast<size_t>(g.ctas) * (g.nt / 32) * 4 * (g.wave ? g.wmax : 1)));
   a.cta_sums = reinterpret_cast<double*>(take(static_cast<size_t>(g.ctas) * 32 * (g.wave ? g.wmax : 1)));
   float* part = reinterpret_cast<float*>(take(g.part_values * 12));
   a.part_g = part;
