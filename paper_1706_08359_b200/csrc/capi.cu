@@ -973,8 +973,13 @@ void grow_tree_persistent(hbg_dataset* ds, const float* d_grad, const float* d_h
         const unsigned long long* t = prof.data() + static_cast<size_t>(i) * 20;
         if (!t[7]) continue;
         std::fprintf(stderr, "  wave %3d: %2llu large of %2llu members: count+small %7.2f scatter %7.2f hist %7.2f "
-                     "barrier %5.2f select %5.2f us\n", i, t[7], t[10], (t[1] - t[0]) * 1e-3, (t[2] - t[1]) * 1e-3,
-                     (t[3] - t[2]) * 1e-3, (t[4] - t[3]) * 1e-3, (t[5] - t[4]) * 1e-3);
+                     "barrier %5.2f select %5.2f us",
+                     i, t[7], t[10], (t[1] - t[0]) * 1e-3, (t[2] - t[1]) * 1e-3, (t[3] - t[2]) * 1e-3,
+                     (t[4] - t[3]) * 1e-3, (t[5] - t[4]) * 1e-3);
+        if (t[17] && t[19])  // inside hist: CTA 0's items, the last CTA's items, the finishes
+          std::fprintf(stderr, "  [items cta0 %.2f last %.2f finish %.2f]", (t[17] - t[2]) * 1e-3,
+                       (t[18] - t[2]) * 1e-3, (t[3] - t[19]) * 1e-3);
+        std::fprintf(stderr, "\n");
       }
     }
     double cand = 0, commits = 0, nav = 0, nfr = 0, rep = 0, imb = 0, lat = 0;

@@ -1184,39 +1184,56 @@ __device__ __forceinline__ void finish_range(const GrowArgs& a, const Desc& D, i
       sm[2 * chunk_cells + t] = static_cast<double>(acc[4 * cells + i]);
     }
   } else {
-    // tpc threads per cell sum strided segments; combined in a fixed order
-    int tpc = NT / cells;
-    tpc = tpc >= 32 ? 32 : (tpc >= 16 ? 16 : (tpc >= 8 ? 8 : (tpc >= 4 ? 4 : (tpc >= 2 ? 2 : 1))));
-    const int per_pass = NT / tpc;
-    for (int i0 = 0; i0 < cells; i0 += per_pass) {
-      const int i = i0 + static_cast<int>(threadIdx.x) / tpc;
-      const int j = threadIdx.x % tpc;
+    // Thread t takes cell i = t mod cells (i = f * k + b: lanes are consecutive
+    // bins, one line per warp-load of the feature-major partials) and segment
+    // stream t / cells; the streams (NT / cells of them when the CTA has more
+    // threads than cells) are combined in order through shared memory: a
+    // fixed shape, so the sums are deterministic.
+    const int streams = cells >= NT ? 1 : NT / cells;
+    double* red = reinterpret_cast<double*>(part_stage(a, smem));  // streams x cells x 3
+    for (int i0 = 0; i0 < cells; i0 += NT) {
+      const int t = static_cast<int>(threadIdx.x);
+      const int i = i0 + (streams > 1 ? t % cells : t), j = streams > 1 ? t / cells : 0;
       double vg = 0.0, vh = 0.0;
       unsigned long long vc = 0;
-      if (i < cells) {
+      const bool mine = i < cells && j < streams;
+      if (mine) {
         const int f = f0 + i / k, b = i % k;
         const int gr = f >> 5, bi = gr / a.gb, gl = gr - bi * a.gb;
-        const int cl = b * 32 + (f & 31);
+        const int cl = (f & 31) * K + b;
 #pragma unroll 4
-        for (int s = j; s < D.nseg; s += tpc) {
+        for (int s = j; s < D.nseg; s += streams) {
           const size_t o = ((static_cast<size_t>(D.pbase) + static_cast<size_t>(s) * a.nblocks + bi) * a.gb + gl) * kCells + cl;
           vg += static_cast<double>(__ldcg(a.part_g + o));
           vh += static_cast<double>(__ldcg(a.part_h + o));
           vc += __ldcg(a.part_c + o);
         }
       }
-      for (int off = tpc >> 1; off > 0; off >>= 1) {  // fixed-shape tree within the group
-        vg += __shfl_down_sync(0xffffffffu, vg, off, tpc);
-        vh += __shfl_down_sync(0xffffffffu, vh, off, tpc);
-        vc += __shfl_down_sync(0xffffffffu, vc, off, tpc);
+      if (streams > 1) {
+        if (mine) {
+          double* r = red + (static_cast<size_t>(j) * cells + i) * 3;
+          r[0] = vg;
+          r[1] = vh;
+          r[2] = static_cast<double>(vc);
+        }
+        __syncthreads();
+        if (mine && j == 0) {
+          for (int q = 1; q < streams; ++q) {
+            const double* r = red + (static_cast<size_t>(q) * cells + i) * 3;
+            vg += r[0];
+            vh += r[1];
+            vc += static_cast<unsigned long long>(r[2]);
+          }
+        }
       }
-      if (j == 0 && i < cells) {
+      if (mine && j == 0) {
         const int f = i / k, b = i - f * k;
-        const int t = b * nf + f;
-        sm[t] = vg;
-        sm[chunk_cells + t] = vh;
-        sm[2 * chunk_cells + t] = static_cast<double>(vc);
+        const int tt = b * nf + f;
+        sm[tt] = vg;
+        sm[chunk_cells + tt] = vh;
+        sm[2 * chunk_cells + tt] = static_cast<double>(vc);
       }
+      if (streams > 1) __syncthreads();
     }
   }
   __syncthreads();
@@ -1447,7 +1464,9 @@ __device__ void hist_smem_item(const GrowArgs& a, const Desc& D, int item, unsig
       sg += v.x;
       sh += v.y;
     }
-    const size_t o = ((static_cast<size_t>(D.pbase) + item) * a.gb + g2) * kCells + c;
+    // feature-major partial ([feature][bin]): the finish's warp-loads of
+    // consecutive bins are one line each
+    const size_t o = ((static_cast<size_t>(D.pbase) + item) * a.gb + g2) * kCells + (c & 31) * K + (c >> 5);
     a.part_g[o] = sg;
     a.part_h[o] = sh;
     a.part_c[o] = cnt[static_cast<size_t>(g2) * kCells + c];
@@ -2276,7 +2295,13 @@ __device__ void wave_large_hist(const GrowArgs& a, const WaveSmem& w, Desc* Dm, 
     chunk_done<NT>(a, D, a.nchunks);
   }
   if (hitems == 0) return;
+  stamp(a, w.nwaves, 17);  // CTA 0's items done
+  if (a.prof != nullptr) {  // slot 18: the last CTA's arrival at the items' barrier
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(a.prof + static_cast<size_t>(w.nwaves) * kProfSlots + 18, global_ns());
+  }
   grid_sync(a);
+  stamp(a, w.nwaves, 19);
   int nsm = 0;
   for (int j = w.nsmall; j < w.W; ++j) nsm += Dm[j].path == kSmem ? 1 : 0;
   for (int x = blockIdx.x; x < nsm * a.nchunks; x += G) {
