@@ -80,6 +80,21 @@ __global__ void kern(float* out, unsigned long long* cycles, int warps_priv) {
         asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(pbase + c * 8), "f"(x), "f"(y));
         atomicAdd(shared_cells + c, 1u);
       }
+    } else if (MODE == 9) {  // red.shared.add.u32, 20% of the lanes active
+      if ((lcg(s) & 1023u) < 205u) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(sbase + c * 4), "r"(s) : "memory");
+    } else if (MODE == 10 || MODE == 11) {  // red.shared.add.u64 (all / 20% lanes)
+      if (MODE == 10 || (lcg(s) & 1023u) < 205u)
+        asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(sbase + c * 8), "l"(static_cast<unsigned long long>(s))
+                     : "memory");
+    } else if (MODE == 12 || MODE == 13) {
+      // the CTA-shared fixed-point update: g and h as int64 (64-bit reds),
+      // count (POPC.INC) — all lanes / 20% of the lanes (bin-0 elision)
+      if (MODE == 12 || (lcg(s) & 1023u) < 205u) {
+        const unsigned long long q = static_cast<unsigned long long>(s) * 2654435761ull;
+        asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(sbase + c * 8), "l"(q) : "memory");
+        asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(sbase + CELLS * 8 + c * 8), "l"(q >> 3) : "memory");
+        atomicAdd(shared_cells + 4 * CELLS + c, 1u);
+      }
     } else if (MODE == 6) {
       // all lanes on one feature column (f = it & 31): aggregate equal bins
       const uint32_t cell = b * 32 + (it & 31);
@@ -112,7 +127,7 @@ __global__ void kern(float* out, unsigned long long* cycles, int warps_priv) {
 
 template <int MODE, int K>
 void run(const char* name, int sms, int warps, int warps_priv, double wf_per_op) {
-  const size_t smem = static_cast<size_t>(K) * 32 * 4 + static_cast<size_t>(warps_priv) * K * 32 * 8;
+  const size_t smem = static_cast<size_t>(K) * 32 * 4 * (MODE >= 10 ? 5 : 1) + static_cast<size_t>(warps_priv) * K * 32 * 8;
   auto fn = kern<MODE, K>;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   float* out;
@@ -158,6 +173,11 @@ int main() {
     run<6, 32>("match_agg", sms, w, wp, 0);
     run<8, 32>("rmw5", sms, w, wp, 5);
     run<7, 32>("rmw5_p20", sms, w, wp, 5);
+    run<9, 64>("red_u32_p20", sms, w, 1, 1);
+    run<10, 64>("red_u64", sms, w, 1, 2);
+    run<11, 64>("red_u64_p20", sms, w, 1, 2);
+    run<12, 64>("fx64_upd", sms, w, 1, 5);
+    run<13, 64>("fx64_p20", sms, w, 1, 5);
   }
   return 0;
 }
