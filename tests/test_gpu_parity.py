@@ -197,6 +197,32 @@ def test_deterministic_across_calls(hbg, oracle):
     assert a.tobytes() == b.tobytes()
 
 
+def test_leaf_sequence_on_one_dataset(hbg, oracle):
+    """A tree's per-leaf calls alternate leaf sizes on one dataset, so every
+    launch plan alternates too — on the drop-in: single-cluster, multi-cluster (sub-histograms summed over DSMEM, the last
+    cluster adding the clusters' sums), and the resident-grid plans whose last
+    CTAs reduce in the same launch (a ticket counter shared by the dataset's
+    launches). Each leaf equals the oracle and repeats bit for bit when it
+    comes round again."""
+    rows, d, k = 1_200_000, 28, 64
+    cols = oracle.gen_synthetic_bins(rows, d, k, 21)
+    g, h = oracle.gen_grad_hess(rows, 21)
+    rng = np.random.default_rng(3)
+    sizes = [rows, 300_000, 9_000, 150_000, 1_000, 600_000, 40_000, 70, 1_100_000]
+    leaves = [np.sort(rng.choice(rows, n, replace=False)).astype(np.int32) for n in sizes]
+    with hbg.Dataset(cols, k) as ds:
+        first = []
+        for idx in leaves:
+            leaf = hbg.gather_leaf_statistics(idx, g, h)
+            got = hbg.build_histograms_partitioned(ds, leaf)
+            want = oracle.build_histograms(cols, k, idx, leaf.gradients, leaf.hessians, 64)
+            assert_hist_close(got, want, tol=1e-4)
+            first.append(got.tobytes())
+        for idx, b in zip(reversed(leaves), reversed(first)):  # the plans in the other order
+            leaf = hbg.gather_leaf_statistics(idx, g, h)
+            assert hbg.build_histograms_partitioned(ds, leaf).tobytes() == b
+
+
 # --------------------------------------------------------------- device paths
 def test_device_row_indexed_and_leaf_aligned_agree(hbg, oracle):
     torch = torch_cuda()
