@@ -4,7 +4,7 @@
 # a summary table gpurun_out/sanitize_summary.txt.
 #   bash scripts/sanitize.sh [cases...]
 mkdir -p gpurun_out
-CASES=${@:-smoke hist tree_wave tree_onesplit tree_host tree_bits64 peer2}
+CASES=${@:-smoke hist leafseq tree_wave tree_onesplit tree_host tree_bits64 peer2}
 export HBG_PEER_TIMEOUT_MS=${HBG_PEER_TIMEOUT_MS:-120000}
 export CUDA_DEVICE_MAX_CONNECTIONS=32
 SUM=gpurun_out/sanitize_summary.txt
@@ -13,7 +13,7 @@ for tool in memcheck racecheck synccheck; do
   for c in $CASES; do
     log=gpurun_out/sanitize_${tool}_${c}.log
     start=$(date +%s)
-    timeout ${SAN_TIMEOUT:-900} compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 20 \
+    timeout -s KILL ${SAN_TIMEOUT:-900} compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 20 \
       python scripts/sanitize_cases.py $c > $log 2>&1
     rc=$?
     t=$(( $(date +%s) - start ))

@@ -2,7 +2,7 @@
 
     python scripts/sanitize_cases.py CASE
 
-CASE: smoke | hist | tree_wave | tree_onesplit | tree_host | tree_bits64 | peer2
+CASE: smoke | hist | leafseq | tree_wave | tree_onesplit | tree_host | tree_bits64 | peer2
 Each case is small (the tools replay every memory access), checks its result
 against the oracle, and exits 0 on success.
 """
@@ -47,6 +47,26 @@ def hist():
                 want = ffi.build_histograms(cols, k, idx, leaf.gradients, leaf.hessians, 64)
                 assert (got["count"] == want["count"]).all()
     print("hist: counts exact on 4 shapes x 2 precisions")
+
+
+def leafseq():
+    """Leaves of alternating sizes on one dataset: cluster, multi-cluster and
+    tail-reduction launch plans (the latter two share per-dataset counters)."""
+    import paper_1706_08359_b200 as hbg
+    from oracle import ffi
+
+    rows, d, k = 400_000, 28, 64
+    cols = ffi.gen_synthetic_bins(rows, d, k, 21)
+    g, h = ffi.gen_grad_hess(rows, 21)
+    rng = np.random.default_rng(3)
+    with hbg.Dataset(cols, k) as ds:
+        for n in (rows, 100_000, 3_000, 60_000, 400, 250_000):
+            idx = np.sort(rng.choice(rows, n, replace=False)).astype(np.int32)
+            leaf = hbg.gather_leaf_statistics(idx, g, h)
+            got = hbg.build_histograms_partitioned(ds, leaf)
+            want = ffi.build_histograms(cols, k, idx, leaf.gradients, leaf.hessians, 64)
+            assert (got["count"] == want["count"]).all()
+    print("leafseq: counts exact on 6 leaf sizes")
 
 
 def peer2():
@@ -108,6 +128,8 @@ def main():
         tree("host")
     elif case == "tree_bits64":
         tree("host", precision=64)
+    elif case == "leafseq":
+        leafseq()
     elif case == "peer2":
         peer2()
     else:
