@@ -43,6 +43,29 @@ struct TileIn {
   T g, h;
 };
 
+// Distributed shared memory: this CTA's address of `p`, in cluster rank q's
+// shared memory (mapa + ld.shared::cluster — not a generic load).
+__device__ __forceinline__ uint32_t dsmem_addr(const void* p, int q) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(dev::smem_addr(p)), "r"(q));
+  return r;
+}
+__device__ __forceinline__ float ld_dsmem(const float* p, int q) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(dsmem_addr(p, q)) : "memory");
+  return v;
+}
+__device__ __forceinline__ double ld_dsmem(const double* p, int q) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(dsmem_addr(p, q)) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_dsmem(const uint32_t* p, int q) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(dsmem_addr(p, q)) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void hist_stamp(const HistArgs& a, int slot) {
   if (a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long t;
@@ -327,9 +350,9 @@ __global__ void __launch_bounds__(K >= 256 ? 128 : 512, BITS == 4 ? 2 : 1) hist_
       unsigned long long vc = 0;
 #pragma unroll 4
       for (int q = 0; q < C; ++q) {
-        vg += static_cast<double>(*cl.map_shared_rank(sub_g + i, q));
-        vh += static_cast<double>(*cl.map_shared_rank(sub_h + i, q));
-        vc += *cl.map_shared_rank(sub_c + i, q);
+        vg += static_cast<double>(ld_dsmem(sub_g + i, q));
+        vh += static_cast<double>(ld_dsmem(sub_h + i, q));
+        vc += ld_dsmem(sub_c + i, q);
       }
       if (nk == 1) {
         emit(i, vg, vh, vc);
@@ -340,6 +363,7 @@ __global__ void __launch_bounds__(K >= 256 ? 128 : 512, BITS == 4 ? 2 : 1) hist_
         a.part_c[o] = static_cast<uint32_t>(vc);
       }
     }
+    hist_stamp(a, 6);  // this CTA's share reduced
     if (nk > 1) {
       __threadfence();  // this cluster's sums are visible before it is counted
       cl.sync();
