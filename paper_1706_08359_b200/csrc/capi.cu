@@ -103,8 +103,6 @@ struct hbg_dataset {
   hbg::DevBuf boost_g, boost_h, boost_leaves;   // boosting: fp32 gradients, final leaf ranges
   hbg::DevBuf small_acc, small_exps;            // fixed-point accumulator for small leaves
   hbg::DevBuf hist_bar;                         // multi-cluster arrival counters (zeroed once)
-  hbg::DevBuf hist_tickets;                     // tail-reduction ticket counter (zeroed once, only grows)
-  unsigned long long tickets_issued = 0;        // tickets the dataset's launches have taken so far
   hbg::DevBuf hist_prof;                        // HBG_HIST_PROFILE phase stamps of the last launch
   hbg::DevBuf grow_nodes, grow_log, grow_tree, grow_counts, grow_scratch, grow_root, grow_prof;  // persistent grower
   const void* grow_records = nullptr;  // the last grown tree's score-update input (launch_grow_persistent)
@@ -444,17 +442,6 @@ void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const vo
   a.nseg = plan.nseg;
   a.cluster = plan.cluster;
   a.nclusters = plan.nclusters;
-  a.tail_reduce = plan.tail_reduce;
-  if (plan.tail_reduce) {
-    if (ds->hist_tickets.p == nullptr) {
-      ds->hist_tickets.get(64);
-      HBG_CUDA(cudaMemsetAsync(ds->hist_tickets.p, 0, 64, s));
-    }
-    a.tickets = static_cast<unsigned long long*>(ds->hist_tickets.p);
-    a.ticket_base = ds->tickets_issued;  // calls on one dataset are serialised (the API contract)
-    ds->tickets_issued += static_cast<unsigned long long>(plan.ctas);
-    a.timeout_cycles = wait_timeout_cycles(L.device);
-  }
   static const bool prof = std::getenv("HBG_HIST_PROFILE") != nullptr;  // development aid
   if (prof) {
     a.prof = static_cast<unsigned long long*>(ds->hist_prof.get(64));
@@ -477,7 +464,7 @@ void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const vo
   } else {
     launch_histogram(plan, a, s);
   }
-  if (!a.direct && a.cluster <= 1 && !a.tail_reduce) launch_reduce_partials(plan, a, L.num_features, L.max_bin, d_hist, s, parent, sibling);
+  if (!a.direct && a.cluster <= 1) launch_reduce_partials(plan, a, L.num_features, L.max_bin, d_hist, s, parent, sibling);
 }
 
 // Row-sharded histogram of one leaf: this rank's rows, the cross-rank sum

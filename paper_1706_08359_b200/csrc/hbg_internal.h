@@ -52,7 +52,6 @@ struct HistPlan {
                        //    the clusters' fp64 sums meet in HBM and the last cluster to
                        //    finish adds them up
   int nclusters;       // clusters per group block (cluster mode)
-  int tail_reduce;     // 1: the last CTAs to finish reduce the partials in the same launch
 };
 // Bytes of one g/h partial element: the CTAs' own type, or fp64 for the
 // cluster sums of the multi-cluster mode.
@@ -87,10 +86,6 @@ struct HistArgs {
   int cluster;  // HistPlan::cluster
   int nclusters;
   unsigned* bar;  // multi-cluster mode: one arrival counter per group block
-  int tail_reduce;                 // HistPlan::tail_reduce
-  unsigned long long* tickets;     // tail reduction: the dataset's launch-spanning arrival counter
-  unsigned long long ticket_base;  //   tickets issued by this dataset's earlier launches (host-tracked)
-  long long timeout_cycles;        //   bound of the wait (a broken invariant is an error, never a hang)
   unsigned long long* prof;  // optional %globaltimer stamps of CTA 0 (HBG_HIST_PROFILE), 8 slots
 };
 

@@ -74,82 +74,6 @@ __device__ __forceinline__ void hist_stamp(const HistArgs& a, int slot) {
   }
 }
 
-// Tail reduction (HistPlan::tail_reduce: every CTA resident, (bin, group)
-// rows R <= CTAs): each CTA takes a ticket from the dataset's 64-bit counter,
-// which only grows (the host passes the tickets issued by the dataset's
-// earlier launches — grids differ from leaf to leaf); the first G - R to
-// arrive are done, the last R each wait until all G have arrived and reduce one row
-// of the partials — warps over segments in order, combined in warp order
-// (deterministic) — into the fp64 histogram (+ sibling). It replaces the
-// reduction launch: no second kernel, no launch gap.
-template <int K, typename T>
-__device__ void tail_reduce(const HistArgs& a, unsigned char* smem) {
-  constexpr int kCells = K * 32;
-  const int G = gridDim.x;
-  const int nbins = min(K, a.max_bin);
-  const int R = nbins * a.num_groups;
-  __syncthreads();  // this CTA's partial stores are issued (and its cells read)
-  __threadfence();
-  unsigned long long* s_t = reinterpret_cast<unsigned long long*>(smem);
-  if (threadIdx.x == 0) *s_t = atomicAdd(a.tickets, 1ull);
-  __syncthreads();
-  const unsigned long long t = *s_t;
-  const int pos = static_cast<int>(t - a.ticket_base);
-  if (pos < G - R) return;
-  const int item = pos - (G - R);
-  if (threadIdx.x == 0) {
-    const unsigned long long all = a.ticket_base + static_cast<unsigned long long>(G);
-    const long long t0 = clock64();
-    unsigned long long cur;
-    do {
-      asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(cur) : "l"(a.tickets) : "memory");
-    } while (cur < all && clock64() - t0 < a.timeout_cycles);
-  }
-  __syncthreads();
-  __threadfence();
-  const T* part_g = static_cast<const T*>(a.part_g);
-  const T* part_h = static_cast<const T*>(a.part_h);
-  const int W = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int group = item / nbins, bin = item - group * nbins;
-  const int bi = group / a.gb, gl = group - bi * a.gb;
-  const int c = bin * 32 + lane;
-  double sg = 0.0, sh = 0.0;
-  unsigned long long sc = 0;
-#pragma unroll 8
-  for (int s = w; s < a.nseg; s += W) {
-    const size_t o = ((static_cast<size_t>(s) * a.nblocks + bi) * a.gb + gl) * kCells + c;
-    sg += static_cast<double>(__ldcg(part_g + o));
-    sh += static_cast<double>(__ldcg(part_h + o));
-    sc += __ldcg(a.part_c + o);
-  }
-  double* rg = reinterpret_cast<double*>(smem + 16);
-  double* rh = rg + W * 32;
-  unsigned long long* rc = reinterpret_cast<unsigned long long*>(rh + W * 32);
-  rg[w * 32 + lane] = sg;
-  rh[w * 32 + lane] = sh;
-  rc[w * 32 + lane] = sc;
-  __syncthreads();
-  if (w != 0) return;
-  for (int i = 1; i < W; ++i) {
-    sg += rg[i * 32 + lane];
-    sh += rh[i * 32 + lane];
-    sc += rc[i * 32 + lane];
-  }
-  const int f = group * 32 + lane;
-  if (f >= a.d) return;
-  const size_t D = static_cast<size_t>(a.d) * a.max_bin;
-  const size_t o = static_cast<size_t>(f) * a.max_bin + bin;
-  a.out[o] = sg;
-  a.out[D + o] = sh;
-  a.out[2 * D + o] = static_cast<double>(sc);
-  if (a.parent) {
-    const double pg = a.parent[o], ph = a.parent[D + o], pc = a.parent[2 * D + o];
-    a.sibling[o] = pg - sg;
-    a.sibling[D + o] = ph - sh;
-    a.sibling[2 * D + o] = pc - static_cast<double>(sc);
-  }
-}
-
 // T = float: bits32 (the reference's per-element fp32 cast, histogram.cpp:97-98);
 // T = double: bits64 (reference_impl<double>, histogram.cpp:131-145) — fp64
 // inputs, fp64 per-warp cells, fp64 partials.
@@ -457,7 +381,6 @@ __global__ void __launch_bounds__(K >= 256 ? 128 : 512, BITS == 4 ? 2 : 1) hist_
     a.part_c[o] = cnt[static_cast<size_t>(g2) * kCells + c];
   }
   hist_stamp(a, 3);
-  if (a.tail_reduce) tail_reduce<K, T>(a, smem);
 }
 
 // out (SoA fp64 [3][d][max_bin]) = fixed-order fp64 sum of the CTA partials
@@ -944,11 +867,6 @@ HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int de
   p.nseg = static_cast<int>(std::max<int64_t>(1, (n + seg_len - 1) / seg_len));
   p.ctas = p.nblocks * p.nseg;
   p.part_values = static_cast<size_t>(p.ctas) * gb * cells;
-  // the last CTAs reduce in the same launch when every CTA is resident at once
-  // and there are enough of them for the (bin, group) rows
-  const int rows_to_reduce = std::min(p.k_alloc, max_bin) * num_groups;
-  p.tail_reduce = allow_fused && p.nseg > 1 && p.ctas <= slots && rows_to_reduce <= p.ctas &&
-                  std::getenv("HBG_NO_TAIL_REDUCE") == nullptr ? 1 : 0;
   return p;
 }
 

@@ -51,7 +51,7 @@ def hist():
 
 def leafseq():
     """Leaves of alternating sizes on one dataset: cluster, multi-cluster and
-    tail-reduction launch plans (the latter two share per-dataset counters)."""
+    two-launch plans (multi-cluster plans share per-dataset counters)."""
     import paper_1706_08359_b200 as hbg
     from oracle import ffi
 
