@@ -185,10 +185,14 @@ long long hbg::wait_timeout_cycles(int device) {
       if (v > 0.0) ms = v;
     }
   });
-  // the clock-rate query costs ~1 ms on this driver: once per device
-  static int khz_of[64] = {0};
-  int& khz = khz_of[device & 63];
-  if (khz <= 0 && (cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device) != cudaSuccess || khz <= 0)) khz = 2000000;
+  // the clock-rate query costs ~1 ms on this driver: once per device (a
+  // racing first call just queries twice)
+  static std::atomic<int> khz_of[64];
+  int khz = khz_of[device & 63].load(std::memory_order_relaxed);
+  if (khz <= 0) {
+    if (cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device) != cudaSuccess || khz <= 0) khz = 2000000;
+    khz_of[device & 63].store(khz, std::memory_order_relaxed);
+  }
   return static_cast<long long>(ms * static_cast<double>(khz));
 }
 
