@@ -235,10 +235,20 @@ def run_hbg(args):
     rank, world, local = dist_env()
     if world != args.gpus and rank == 0:
         print(f"# note: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+    # Development check of the N > 1 plumbing on a one-GPU box: every rank on
+    # the same device (their contexts time-slice), torch.distributed over gloo,
+    # no NCCL (it refuses two ranks on one GPU), the CUDA-IPC peer path only.
+    shared_gpu = os.environ.get("HBG_BENCH_SHARED_GPU") is not None and world > 1
+    if shared_gpu:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    red_dev = torch.device("cpu") if shared_gpu else dev  # tensors the collectives reduce
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     n, d, k = args.rows, args.features, args.max_bin
     strong = args.rows_total > 0
@@ -264,7 +274,7 @@ def run_hbg(args):
     sp = stream.cuda_stream
 
     comm = None
-    if world > 1:  # NCCL communicator of the library (the sharded allreduce hook)
+    if world > 1 and not shared_gpu:  # NCCL communicator of the library (the sharded allreduce hook)
         uid = [hbg.Comm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = hbg.Comm(world, rank, uid[0], local)
@@ -275,8 +285,8 @@ def run_hbg(args):
     # fallback, chosen by all ranks together if any rank cannot map or run it.
     peer = None
     exchange = "none (single rank)"
-    if comm is not None:
-        ok = torch.ones(1, device=dev)
+    if world > 1:
+        ok = torch.ones(1, device=red_dev)
         try:
             peer = hbg.Peer(ds, world, rank, 0, args.num_leaves)
             handles = [None] * world
@@ -294,6 +304,8 @@ def run_hbg(args):
             if peer is not None:
                 peer.close()
             peer = None
+            if comm is None:
+                raise RuntimeError(f"peer exchange unavailable and no NCCL fallback: {exchange}")
             if exchange.startswith("none"):
                 exchange = "NCCL allreduce (peer path failed on another rank)"
         else:
@@ -331,7 +343,7 @@ def run_hbg(args):
     ds.set_profiling(False)
     ms_total = e0.elapsed_time(e1)
     kern_ms, launches = ds.kernel_time()
-    ms_step = torch.tensor([ms_total / args.steps], dtype=torch.float64, device=dev)
+    ms_step = torch.tensor([ms_total / args.steps], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(ms_step, op=dist.ReduceOp.MAX)
     ms_step = float(ms_step.item())
@@ -387,7 +399,7 @@ def run_hbg(args):
     for _ in range(e2e_steps):
         out = hbg.build_histograms_partitioned(ds, leaf)
     t1 = time.perf_counter()
-    e2e_ms = torch.tensor([(t1 - t0) * 1e3 / e2e_steps], dtype=torch.float64, device=dev)
+    e2e_ms = torch.tensor([(t1 - t0) * 1e3 / e2e_steps], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_ms.item())
@@ -474,19 +486,19 @@ def run_hbg(args):
     # other sharded path, used only if the peer mapping is unavailable
     if not args.no_tree:
         tree_path = "persistent kernel, single rank"
-        if comm is not None:
+        if world > 1:
             tree_path = ("persistent kernel, in-kernel peer-memory histogram exchange (NVLink)" if peer is not None
                          else "host loop + NCCL allreduce hook (peer mapping unavailable)")
 
         def grow():
-            if comm is None:
+            if world == 1:
                 return ds.grow_tree(tg, th, args.num_leaves, 1, 0.0, sp)
             if peer is not None:
                 return ds.grow_tree_peer(tg, th, peer, args.num_leaves, 1, 0.0, sp)
             return ds.grow_tree_sharded(tg, th, comm.allreduce_fn, comm.handle, args.num_leaves, 1, 0.0, sp)
 
         if peer is not None:  # warm-up through the peer path; every rank falls back together on failure
-            ok = torch.ones(1, device=dev)
+            ok = torch.ones(1, device=red_dev)
             try:
                 grow()
             except Exception as e:  # noqa: BLE001 — reported in the JSON line
@@ -511,7 +523,7 @@ def run_hbg(args):
         b.record(stream)
         torch.cuda.synchronize()
         ds.set_profiling(False)
-        t_tree = torch.tensor([a.elapsed_time(b) / args.trees / 1e3], dtype=torch.float64, device=dev)
+        t_tree = torch.tensor([a.elapsed_time(b) / args.trees / 1e3], dtype=torch.float64, device=red_dev)
         if world > 1:
             dist.all_reduce(t_tree, op=dist.ReduceOp.MAX)
         t_tree = float(t_tree.item())
@@ -526,7 +538,7 @@ def run_hbg(args):
             "note": "root + smaller child of every split (larger by subtraction); all splits in one persistent cooperative kernel (grow_persistent.cu)",
             "path": tree_path,
         }
-        if comm is None:
+        if world == 1:
             # end to end through the whole-tree drop-in (hbg_grow_tree_host):
             # host fp64 g/h (pinned) in, split log + nodes out, H2D inside
             pg64 = torch.from_numpy(g.astype(np.float64)).pin_memory().numpy()
