@@ -353,7 +353,7 @@ def run_hbg(args):
     kern_avg_s = kern_ms / max(launches, 1) / 1e3
     alg = algorithmic_bytes(n, d, k, bits)
     peak, peak_src = hbm_peak()
-    achieved = alg / kern_avg_s / 1e9
+    achieved = alg / kern_avg_s / 1e9 if kern_avg_s > 0 else 0.0
     workload = f"higgs-{total}x{d}-k{k}-root-leaf" + (f"-sharded{world}" if strong and world > 1 else "")
 
     result = {
@@ -416,7 +416,9 @@ def run_hbg(args):
         # a contiguous leaf (the root) uploads no indices: the library checks
         # idx[i] == idx[0] + i on the host while g/h are in flight
         "h2d_bytes_per_step": int(n * (8 + 8) + (0 if contiguous else 4 * n)), "d2h_bytes_per_step": int(out.nbytes),
-        "ms_per_step": e2e_ms, "api": "hbg_build_histograms (host LeafState arrays: int32 indices, fp64 g/h)",
+        "ms_per_step": e2e_ms,
+        "api": "hbg_build_histograms (host LeafState arrays: int32 indices, fp64 g/h)"
+               + ("; per rank, the cross-rank sum not included" if world > 1 else ""),
         "steps": e2e_steps,
         "pageable_ms_per_step": page_ms,
     }

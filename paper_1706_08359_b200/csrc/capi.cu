@@ -508,7 +508,15 @@ void build_device_peer(hbg_dataset* ds, const int32_t* d_idx, int64_t count, con
   a.d = L.num_features;
   a.max_bin = L.max_bin;
   if (count > 0) {
-    launch_histogram(plan, a, s);
+    if (ds->profiling) {  // the histogram kernel's own time (bench.py's roofline), as build_device
+      auto ev = ds->event_pair();
+      HBG_CUDA(cudaEventRecord(ev.first, s));
+      launch_histogram(plan, a, s);
+      HBG_CUDA(cudaEventRecord(ev.second, s));
+      ds->events.push_back(ev);
+    } else {
+      launch_histogram(plan, a, s);
+    }
   } else {
     plan.nseg = 0;  // nothing of this rank's; still publish zeros and sum
   }
