@@ -197,7 +197,7 @@ def run_reference(args):
     if not ffi.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libhistoboost_ref.so not built"}))
         return
-    n, d, k = args.rows, args.features, args.max_bin
+    n, d, k = args.rows_total if args.rows_total > 0 else args.rows, args.features, args.max_bin
     cols, g, h = synthetic(n, d, k, seed=0)
     idx = leaf_sample(n, 0, 0)
     rd = ffi.RefDataset(cols, k)
