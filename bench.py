@@ -458,6 +458,30 @@ def run_hbg(args):
             t = a.elapsed_time(b) / reps
             var[f"k{k}_D{depth}"] = {"rows": m, "ms": t, "rows_features_per_s": m * d / (t / 1e3),
                                      "alg_GBps": algorithmic_bytes(m, d, k, bits) / (t / 1e3) / 1e9}
+        # PrecisionMode::bits64 on the same root: fp64 g/h in HBM, fp64 cells and
+        # partials (the exact mode; 16 B/row of g/h instead of 8)
+        tg64 = torch.from_numpy(g.astype(np.float64)).to(dev)
+        th64 = torch.from_numpy(h.astype(np.float64)).to(dev)
+        for _ in range(3):
+            ds.build_histograms_device_f64(ti, n, tg64, th64, hist, hbg.HBG_GH_LEAF_ALIGNED, sp)
+        ds.kernel_time()
+        ds.set_profiling(True)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 20
+        a.record(stream)
+        for _ in range(reps):
+            ds.build_histograms_device_f64(ti, n, tg64, th64, hist, hbg.HBG_GH_LEAF_ALIGNED, sp)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ds.set_profiling(False)
+        t = a.elapsed_time(b) / reps
+        km, kl = ds.kernel_time()
+        alg64 = n * (d * bits / 8.0 + 20.0) + 12.0 * d * k  # int32 id + fp64 g + fp64 h
+        var[f"k{k}_bits64_D0"] = {"rows": n, "ms": t, "rows_features_per_s": n * d / (t / 1e3),
+                                  "kernel_ms": km / max(kl, 1),
+                                  "kernel_alg_GBps": alg64 / (km / max(kl, 1) / 1e3) / 1e9,
+                                  "precision": "bits64 (fp64 g/h, cells and partials)"}
+        del tg64, th64
         if k != 16:
             cols16 = (cols % 15 + 1).astype(np.uint8)
             ds16 = hbg.Dataset(cols16, 16, device=local)
