@@ -798,7 +798,9 @@ HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int de
   if (allow_fused) {
     const int64_t tiles = (n + 32 * rpl - 1) / (32 * rpl);
     const int max_wpg = std::max(1, warps_full / gb);
-    // Up to ~4 tiles per row warp on the clusters that fit: clusters of C
+    // Up to ~2 tiles per row warp on the clusters that fit (measured: beyond
+    // that the two-launch plan with PDL is as fast or faster — D6 12.6 vs
+    // 16.2 us; below ~12K rows one cluster wins, D12 8.5 vs 12.9 us): clusters of C
     // CTAs, one row segment per CTA, the segments' sub-histograms summed over
     // distributed shared memory (hist_kernel's cluster mode) — no grid
     // barrier, no cooperative launch (so PDL overlaps consecutive calls).
@@ -821,7 +823,8 @@ HistPlan plan_histogram(int bits, int max_bin, int num_groups, int64_t n, int de
           }
         }
         const int64_t slots = static_cast<int64_t>(C) * max_wpg_c;  // row warps per cluster
-        if (C > 0 && tiles <= 4 * slots * kmax) {
+        static const int tpw = std::getenv("HBG_CLUSTER_TPW") ? std::atoi(std::getenv("HBG_CLUSTER_TPW")) : 2;
+        if (C > 0 && tiles <= tpw * slots * kmax) {
           const int K = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kmax, (tiles + 2 * slots - 1) / (2 * slots))));
           // the fewest row warps that keep every warp at <= 2 tiles (or all of them)
           const int64_t want = (tiles + 2 * static_cast<int64_t>(K) * C - 1) / (2 * static_cast<int64_t>(K) * C);
