@@ -86,6 +86,18 @@ def leaf_sample(rows: int, depth: int, seed: int) -> np.ndarray:
     return np.sort(rng.choice(rows, rows >> depth, replace=False)).astype(np.int32)
 
 
+def workload_config(n: int, total: int, d: int, k: int, world: int, strong: bool) -> dict:
+    """The bench line's `config`, identical for both arms (the driver compares them)."""
+    bits = 4 if k <= 16 else 8
+    workload = f"higgs-{total}x{d}-k{k}-root-leaf" + (f"-sharded{world}" if strong and world > 1 else "")
+    return {
+        "workload": workload, "rows_per_gpu": n, "rows_total": total, "features": d, "max_bin": k,
+        "bits_per_bin": bits, "leaf_depth": 0, "leaf": "explicit int32 indices + leaf-aligned g/h (the root LeafState)",
+        "l2": f"inputs {(n * (d * bits / 8 + 12)) / 1e6:.0f} MB > 126 MB L2; no flush needed",
+        "parallelism": f"row-sharded x{world}",
+    }
+
+
 def algorithmic_bytes(n: int, d: int, k: int, bits: int) -> float:
     """B = N_r (d b/8 + 12) + 12 d k per histogram pass."""
     return n * (d * bits / 8.0 + 12.0) + 12.0 * d * k
@@ -197,7 +209,10 @@ def run_reference(args):
     if not ffi.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libhistoboost_ref.so not built"}))
         return
-    n, d, k = args.rows_total if args.rows_total > 0 else args.rows, args.features, args.max_bin
+    # the hbg arm's whole job at this world size (weak: rows per GPU x N; strong: rows_total)
+    world = dist_env()[1]
+    strong = args.rows_total > 0
+    n, d, k = args.rows_total if strong else world * args.rows, args.features, args.max_bin
     cols, g, h = synthetic(n, d, k, seed=0)
     idx = leaf_sample(n, 0, 0)
     rd = ffi.RefDataset(cols, k)
@@ -214,8 +229,9 @@ def run_reference(args):
         "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (numpy, reference generator distribution)",
-        "config": {"workload": f"higgs-{n}x{d}-k{k}-root-leaf", "rows": n, "features": d, "max_bin": k,
-                   "leaf_depth": 0, "precision": "bits32", "path": "build_histograms_partitioned"},
+        "config": workload_config((args.rows_total if strong else n) // world, n, d, k, world, strong),
+        "reference": {"precision": "bits32", "path": "build_histograms_partitioned (unmodified reference, oracle/_ref)",
+                      "rows": n},
         "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "reference",
                          "sample": f"{args.steps} root-leaf builds of the {n}x{d} k{k} workload"},
         "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -354,7 +370,8 @@ def run_hbg(args):
     alg = algorithmic_bytes(n, d, k, bits)
     peak, peak_src = hbm_peak()
     achieved = alg / kern_avg_s / 1e9 if kern_avg_s > 0 else 0.0
-    workload = f"higgs-{total}x{d}-k{k}-root-leaf" + (f"-sharded{world}" if strong and world > 1 else "")
+    cfg = workload_config(n, total, d, k, world, strong)
+    workload = cfg["workload"]
 
     result = {
         "metric": "histogram build rows*features/sec",
@@ -369,13 +386,8 @@ def run_hbg(args):
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (numpy; reference generator distribution: bins U[1,k-1], g=2u-1, h=u)",
-        "config": {
-            "workload": workload, "rows_per_gpu": n, "rows_total": total, "features": d, "max_bin": k,
-            "bits_per_bin": bits,
-            "leaf_depth": 0, "leaf": "explicit int32 indices + leaf-aligned fp32 g/h",
-            "l2": f"inputs {(n * (d * bits / 8 + 12)) / 1e6:.0f} MB > 126 MB L2; no flush needed",
-            "parallelism": f"row-sharded x{world}" + (f"; leaf-histogram exchange: {exchange}" if world > 1 else ""),
-        },
+        "config": cfg,
+        "exchange": exchange,
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": ncu_traffic(workload), "kernel": "hist_kernel<8,64>" if bits == 8 else "hist_kernel<4,16>",

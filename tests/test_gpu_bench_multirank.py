@@ -31,5 +31,5 @@ def test_bench_two_ranks_on_one_gpu():
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["value"] > 0
     assert line["config"]["rows_total"] == 600000
-    assert "peer memory" in line["config"]["parallelism"]  # the fused exchange, not the NCCL fallback
+    assert "peer memory" in line["exchange"]  # the fused exchange, not the NCCL fallback
     assert line["tree"]["splits"] == 30 and "peer-memory" in line["tree"]["path"]
