@@ -402,7 +402,6 @@ def run_hbg(args):
     pin_g = torch.from_numpy(g).pin_memory().numpy()
     pin_h = torch.from_numpy(h).pin_memory().numpy()
     leaf = hbg.LeafState(pin_idx, pin_g, pin_h)
-    contiguous = bool(len(idx) == 0 or (np.diff(idx) == 1).all())
     hbg.build_histograms_partitioned(ds, leaf)  # warm the workspace
     torch.cuda.synchronize()
     if world > 1:
@@ -415,6 +414,7 @@ def run_hbg(args):
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_ms.item())
+    pin_h2d, pin_d2h = ds.host_copy_bytes()
     # the same call with pageable arrays (numpy, like the reference's
     # std::vectors): staged as fp32 by the library's host pool (informational)
     page_leaf = hbg.LeafState(np.array(idx), np.array(g, dtype=np.float64), np.array(h, dtype=np.float64))
@@ -425,9 +425,10 @@ def run_hbg(args):
     page_ms = (time.perf_counter() - t0p) * 1e3 / e2e_steps
     result["e2e"] = {
         "value": total * d / (e2e_ms / 1e3), "unit": "rows*features/s",
-        # a contiguous leaf (the root) uploads no indices: the library checks
-        # idx[i] == idx[0] + i on the host while g/h are in flight
-        "h2d_bytes_per_step": int(n * (8 + 8) + (0 if contiguous else 4 * n)), "d2h_bytes_per_step": int(out.nbytes),
+        # counted by the library: each staged chunk of g/h goes as host-
+        # converted fp32 (8 B/row) or fp64 (16 B/row, converted on the
+        # device); a contiguous leaf (the root) uploads no row ids
+        "h2d_bytes_per_step": pin_h2d, "d2h_bytes_per_step": pin_d2h,
         "ms_per_step": e2e_ms,
         "api": "hbg_build_histograms (host LeafState arrays: int32 indices, fp64 g/h)"
                + ("; per rank, the cross-rank sum not included" if world > 1 else ""),
@@ -446,7 +447,7 @@ def run_hbg(args):
     d1_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
     result["e2e"]["depth1_leaf"] = {"rows": int(len(i1)), "ms_per_step": d1_ms,
                                     "rows_features_per_s": len(i1) * d / (d1_ms / 1e3),
-                                    "h2d_bytes_per_step": int(len(i1) * (4 + 8 + 8))}
+                                    "h2d_bytes_per_step": ds.host_copy_bytes()[0]}
 
     # --- variants (informational): 4-bit 16-bin kernel, deeper leaves
     if not args.no_variants:

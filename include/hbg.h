@@ -124,6 +124,12 @@ int hbg_build_histograms_ex(hbg_dataset* ds, const int32_t* indices, int64_t cou
  * last launch's eight to host `out`. */
 int hbg_debug_hist_stamps(hbg_dataset* ds, unsigned long long* out);
 
+/* Development aid: bytes the last host histogram call on `ds`
+ * (hbg_build_histograms, _ex) copied host->device and device->host — each staged
+ * chunk goes as fp32 (8 B/row) or fp64 (16 B/row), row ids only for chunks
+ * that are not one contiguous range — written to out[0] and out[1]. */
+int hbg_debug_host_copy_bytes(hbg_dataset* ds, int64_t* out);
+
 /* Device builder (the performance path). d_indices may be NULL for the
  * identity leaf [0, count) (the root). d_grad/d_hess are fp32, addressed per
  * gh_mode. d_hist receives the device histogram: SoA fp64

@@ -141,6 +141,7 @@ EXPORTED_SYMBOLS = (
     "hbg_last_error",
     "hbg_version",
     "hbg_debug_hist_stamps",
+    "hbg_debug_host_copy_bytes",
     "hbg_dataset_create",
     "hbg_dataset_destroy",
     "hbg_dataset_layout",
@@ -400,6 +401,12 @@ class Dataset:
     def stream(self) -> int:
         """The dataset's own CUDA stream (cudaStream_t as an int)."""
         return lib().hbg_dataset_stream(self.handle) or 0
+
+    def host_copy_bytes(self) -> tuple:
+        """(host->device, device->host) bytes of the last host drop-in call."""
+        out = (C.c_int64 * 2)()
+        check(lib().hbg_debug_host_copy_bytes(self.handle, out))
+        return int(out[0]), int(out[1])
 
     def build_histograms_peer(self, indices, count: int, grad, hess, out, peer: "Peer",
                               gh_mode: int = HBG_GH_LEAF_ALIGNED, stream=None):

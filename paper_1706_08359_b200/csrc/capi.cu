@@ -6,6 +6,8 @@
 // fallback anywhere: a missing GPU or CUDA failure is an error status.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cmath>
 #include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
@@ -16,6 +18,9 @@
 #include <string>
 #include <thread>
 #include <vector>
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
 
 #include "hbg_internal.h"
 
@@ -97,6 +102,7 @@ struct hbg_dataset {
   cudaEvent_t chunk_ev[17] = {};  // per histogram chunk (<= 16) + [16]: the copy stream's start
   hbg::DevBuf part, iota, host_idx, host_gd, host_hd, host_gf, host_hf, host_hist, host_bins;
   int64_t iota_rows = 0;
+  int64_t copy_h2d = 0, copy_d2h = 0;  // bytes of the last host drop-in call
   // tree growth workspace
   hbg::DevBuf ord[2][3];  // ping-pong (row, g, h) ordered buffers
   hbg::DevBuf slots, part_scratch, tree_small;  // leaf histograms, partition scratch, splits/totals
@@ -284,7 +290,8 @@ class HostPool {
   HostPool() {
     // one core stays with the calling thread, which issues the copies
     const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
-    const int T = static_cast<int>(std::min<unsigned>(16, hw - 1));
+    int T = static_cast<int>(std::min<unsigned>(16, hw - 1));
+    if (const char* e = std::getenv("HBG_HOST_THREADS")) T = std::max(1, std::min(64, std::atoi(e)));
     for (int w = 0; w < T; ++w) th_.emplace_back([this, w] { loop(w); });
   }
   void loop(int w) {
@@ -328,14 +335,46 @@ void* stage_buffer(hbg_dataset* ds, size_t bytes) {
   return ds->stage;
 }
 
+// Host staging stores (x86-64: SSE2 is baseline) — non-temporal, so the
+// pinned stage lines are not read into the cache before being overwritten.
+inline void convert_stream(const double* src, float* dst, int64_t n) {
+  int64_t i = 0;
+#if defined(__SSE2__)
+  for (; i < n && (reinterpret_cast<uintptr_t>(dst + i) & 15) != 0; ++i) dst[i] = static_cast<float>(src[i]);
+  for (; i + 4 <= n; i += 4) {
+    const __m128 lo = _mm_cvtpd_ps(_mm_loadu_pd(src + i));
+    const __m128 hi = _mm_cvtpd_ps(_mm_loadu_pd(src + i + 2));
+    _mm_stream_ps(dst + i, _mm_movelh_ps(lo, hi));
+  }
+#endif
+  for (; i < n; ++i) dst[i] = static_cast<float>(src[i]);
+}
+inline void copy_stream(const int32_t* src, int32_t* dst, int64_t n) {
+  int64_t i = 0;
+#if defined(__SSE2__)
+  for (; i < n && (reinterpret_cast<uintptr_t>(dst + i) & 15) != 0; ++i) dst[i] = src[i];
+  for (; i + 4 <= n; i += 4)
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i)));
+#endif
+  for (; i < n; ++i) dst[i] = src[i];
+}
+inline void store_fence() {
+#if defined(__SSE2__)
+  _mm_sfence();
+#endif
+}
+
 // Stage rows [0, n) of fp64 g/h (and, when idx != nullptr, the int32 row ids)
 // into the pinned stage as fp32 (g | h | idx), in chunks of `chunk` rows
-// converted by the host pool; copy(c, b, e, gf, hf, id) runs on the calling
-// thread, in chunk order, as soon as chunk c is staged. Returns after the last
-// copy was issued.
+// converted by the host pool (chunks with direct[c] set are only checked:
+// their g/h go up as fp64 straight from pinned caller memory); copy(c, b, e, gf, hf, id, contiguous) runs on
+// the calling thread, in chunk order, as soon as chunk c is staged;
+// `contiguous` says chunk c's ids are idx[0] + i (checked by the staging pass,
+// which then stores no ids for it); a copy() that uploads ids of chunk c
+// first calls fill_ids(c). Returns after the last copy was issued.
 template <typename Copy>
 void stage_chunks(hbg_dataset* ds, const double* g, const double* h, const int32_t* idx, int64_t n, int64_t chunk,
-                  Copy copy) {
+                  const std::vector<char>& direct, Copy copy) {
   const size_t rows = static_cast<size_t>(n);
   char* st = static_cast<char*>(stage_buffer(ds, rows * (idx ? 12 : 8) + 64));
   float* gf = reinterpret_cast<float*>(st);
@@ -345,31 +384,71 @@ void stage_chunks(hbg_dataset* ds, const double* g, const double* h, const int32
   HostPool& pool = HostPool::get();
   std::lock_guard<std::mutex> job(pool.job_mutex());  // held until the last pool.wait()
   const int T = pool.size();
-  std::unique_ptr<std::atomic<int>[]> done(new std::atomic<int>[static_cast<size_t>(C)]);
-  for (int c = 0; c < C; ++c) done[static_cast<size_t>(c)].store(0, std::memory_order_relaxed);
+  const int64_t first = idx && n > 0 ? idx[0] : 0;
+  // done[c]: workers finished with chunk c; broken[c]: some id of chunk c is
+  // not first + i (the chunk is not a piece of one contiguous row range)
+  std::unique_ptr<std::atomic<int>[]> done(new std::atomic<int>[static_cast<size_t>(2 * C)]);
+  std::atomic<int>* broken = done.get() + C;
+  for (int c = 0; c < 2 * C; ++c) done[static_cast<size_t>(c)].store(0, std::memory_order_relaxed);
+  static const bool prof = std::getenv("HBG_STAGE_PROFILE") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  auto us = [&] { return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count(); };
+  // written[c*T + w]: worker w stored its slice of chunk c's ids (it does so
+  // only when the slice is not first + i; copy() never needs a slice that
+  // passed unless its chunk's histogram reads uploaded ids: fill_ids below)
+  std::vector<char> written(static_cast<size_t>(C) * T, 0);
   pool.run([&, C, T](int w) {
     for (int c = 0; c < C; ++c) {
       const int64_t b = chunk * c, e = std::min<int64_t>(n, b + chunk);
       const int64_t s0 = b + (e - b) * w / T, s1 = b + (e - b) * (w + 1) / T;
-      for (int64_t i = s0; i < s1; ++i) {
-        gf[i] = static_cast<float>(g[i]);
-        hf[i] = static_cast<float>(h[i]);
+      // the stage is read by the copy engine only: streaming stores (no
+      // read-for-ownership of the destination lines)
+      if (!direct[static_cast<size_t>(c)]) {
+        convert_stream(g + s0, gf + s0, s1 - s0);
+        convert_stream(h + s0, hf + s0, s1 - s0);
       }
-      if (idx) std::memcpy(id + s0, idx + s0, static_cast<size_t>(s1 - s0) * 4);
+      if (idx) {
+        bool bad = false;
+        for (int64_t i = s0; i < s1; ++i) bad |= static_cast<int64_t>(idx[i]) != first + i;
+        if (bad) {
+          copy_stream(idx + s0, id + s0, s1 - s0);
+          written[static_cast<size_t>(c) * T + w] = 1;
+          broken[c].store(1, std::memory_order_relaxed);
+        }
+      }
+      store_fence();
       done[static_cast<size_t>(c)].fetch_add(1, std::memory_order_release);
     }
   });
+  // ids of chunk c in the stage, for a copy() that uploads them: the slices
+  // the workers skipped are first + i
+  auto fill_ids = [&](int c) {
+    const int64_t b = chunk * c, e = std::min<int64_t>(n, b + chunk);
+    for (int w = 0; w < T; ++w) {
+      char& f = written[static_cast<size_t>(c) * T + w];
+      if (f) continue;
+      const int64_t s0 = b + (e - b) * w / T, s1 = b + (e - b) * (w + 1) / T;
+      for (int64_t i = s0; i < s1; ++i) id[i] = static_cast<int32_t>(first + i);
+      f = 1;
+    }
+  };
+  double t_first = 0, t_last = 0;
   try {
     for (int c = 0; c < C; ++c) {
       while (done[static_cast<size_t>(c)].load(std::memory_order_acquire) < T) std::this_thread::yield();
+      if (prof) (c == 0 ? t_first : t_last) = us();
       const int64_t b = chunk * c, e = std::min<int64_t>(n, b + chunk);
-      copy(c, b, e, gf, hf, id);
+      copy(c, b, e, gf, hf, id, idx != nullptr && broken[c].load(std::memory_order_relaxed) == 0, fill_ids);
     }
   } catch (...) {
     pool.wait();  // the workers still use `done` and the stage
     throw;
   }
+  const double t_issue = prof ? us() : 0;
   pool.wait();
+  if (prof)
+    std::fprintf(stderr, "[hbg stage] rows=%lld chunks=%d threads=%d: chunk0 %.0f us, last chunk %.0f us, issued %.0f us, joined %.0f us\n",
+                 static_cast<long long>(n), C, T, t_first, t_last, t_issue, us());
 }
 
 constexpr int64_t kStageRows = int64_t(1) << 19;  // rows per staged chunk (4 MB of fp32 g/h)
@@ -380,6 +459,23 @@ int host_chunks(int64_t count) {
   const char* e = std::getenv("HBG_HOST_CHUNKS");
   if (e != nullptr) return std::max(1, std::min(16, std::atoi(e)));
   return count >= (int64_t{1} << 21) ? 4 : 1;
+}
+
+// Staged chunks copied as fp64 straight from pinned caller memory (the rest
+// are converted to fp32 by the host pool first): a fraction f of them,
+// spread evenly, starting with chunk 0 so the copy engine starts at once.
+// f balances host memory traffic (32 B/row converted, 16 B/row direct)
+// against PCIe (8 vs 16 B/row); HBG_PINNED_DMA_FRAC overrides it.
+std::vector<char> direct_chunks(int64_t n, int64_t chunk, bool pinned) {
+  const int C = static_cast<int>((n + chunk - 1) / chunk);
+  std::vector<char> d(static_cast<size_t>(C), 0);
+  if (!pinned) return d;  // pageable memory crosses PCIe at a fraction of the pinned rate
+  static const double f = [] {
+    const char* e = std::getenv("HBG_PINNED_DMA_FRAC");
+    return e ? std::max(0.0, std::min(1.0, std::atof(e))) : 0.25;
+  }();
+  for (int c = 0; c < C; ++c) d[static_cast<size_t>(c)] = std::ceil((c + 1) * f) > std::ceil(c * f);
+  return d;
 }
 
 // Device row ids [first, first + n) of the dataset: the resident iota array.
@@ -1228,6 +1324,9 @@ int hbg_build_histograms_ex(hbg_dataset* ds, const int32_t* indices, int64_t cou
     const size_t D = static_cast<size_t>(L.num_features) * L.max_bin;
     double* d_hist = static_cast<double*>(ds->host_hist.get(3 * D * sizeof(double) + 8));
     hbg_bin* d_bins = static_cast<hbg_bin*>(ds->host_bins.get(D * sizeof(hbg_bin) + 8));
+    int64_t& h2d = ds->copy_h2d;
+    h2d = 0;
+    ds->copy_d2h = static_cast<int64_t>(D * sizeof(hbg_bin));
     if (count > 0 && precision == HBG_PRECISION_BITS64) {
       // bits64: the fp64 LeafState arrays go up as they are (no per-element
       // cast); pinned ones at full PCIe rate, pageable ones through the
@@ -1237,6 +1336,7 @@ int hbg_build_histograms_ex(hbg_dataset* ds, const int32_t* indices, int64_t cou
       double* d_hd = static_cast<double*>(ds->host_hd.get(n * 8));
       HBG_CUDA(cudaMemcpyAsync(d_gd, gradients, n * 8, cudaMemcpyHostToDevice, s));
       HBG_CUDA(cudaMemcpyAsync(d_hd, hessians, n * 8, cudaMemcpyHostToDevice, s));
+      h2d += static_cast<int64_t>(n) * 16;
       const int32_t* d_idx;
       if (leaf_is_contiguous(indices, count)) {
         require(indices[0] >= 0 && indices[0] + count <= L.num_rows, "leaf row index out of range");
@@ -1244,103 +1344,97 @@ int hbg_build_histograms_ex(hbg_dataset* ds, const int32_t* indices, int64_t cou
       } else {
         int32_t* di = static_cast<int32_t*>(ds->host_idx.get(n * 4));
         HBG_CUDA(cudaMemcpyAsync(di, indices, n * 4, cudaMemcpyHostToDevice, s));
+        h2d += static_cast<int64_t>(n) * 4;
         d_idx = di;
       }
       build_device(ds, d_idx, count, d_gd, d_hd, HBG_GH_LEAF_ALIGNED, d_hist, s, nullptr, nullptr, 8, true);
-    } else if (count > 0 && !(is_pinned(gradients) && is_pinned(hessians))) {
-      // pageable LeafState arrays: fp32 g/h staged by the host pool (see
-      // stage_chunks); histogram chunk c runs as soon as its rows have landed
-      const size_t n = static_cast<size_t>(count);
-      float* d_gf = static_cast<float*>(ds->host_gf.get(n * 4));
-      float* d_hf = static_cast<float*>(ds->host_hf.get(n * 4));
-      const int C = host_chunks(count);  // as the pinned path: the same sums
-      if (!ds->copy_stream) HBG_CUDA(cudaStreamCreateWithFlags(&ds->copy_stream, cudaStreamNonBlocking));
-      for (int c = 0; c < 17; ++c)
-        if (!ds->chunk_ev[c]) HBG_CUDA(cudaEventCreateWithFlags(&ds->chunk_ev[c], cudaEventDisableTiming));
-      HBG_CUDA(cudaEventRecord(ds->chunk_ev[16], s));
-      HBG_CUDA(cudaStreamWaitEvent(ds->copy_stream, ds->chunk_ev[16], 0));
-      // the row ids ride along with g/h (a contiguity check would be one more
-      // serial pass over the ids; their 4 B/row fit under the conversion)
-      int32_t* di = static_cast<int32_t*>(ds->host_idx.get(n * 4));
-      const int32_t* d_idx = di;
-      double* parts = C > 1 ? static_cast<double*>(ds->host_parts.get(static_cast<size_t>(C) * 3 * D * sizeof(double) + 8))
-                            : d_hist;
-      std::vector<const double*> part_ptrs;
-      int next = 0;
-      stage_chunks(ds, gradients, hessians, indices, count, kStageRows,
-                   [&](int, int64_t b, int64_t e, const float* gs, const float* hs, const int32_t* is) {
-                     const size_t m = static_cast<size_t>(e - b);
-                     HBG_CUDA(cudaMemcpyAsync(d_gf + b, gs + b, m * 4, cudaMemcpyHostToDevice, ds->copy_stream));
-                     HBG_CUDA(cudaMemcpyAsync(d_hf + b, hs + b, m * 4, cudaMemcpyHostToDevice, ds->copy_stream));
-                     HBG_CUDA(cudaMemcpyAsync(di + b, is + b, m * 4, cudaMemcpyHostToDevice, ds->copy_stream));
-                     for (; next < C && count * (next + 1) / C <= e; ++next) {
-                       const int64_t cb = count * next / C, ce = count * (next + 1) / C;
-                       HBG_CUDA(cudaEventRecord(ds->chunk_ev[next], ds->copy_stream));
-                       HBG_CUDA(cudaStreamWaitEvent(s, ds->chunk_ev[next], 0));
-                       double* hc = parts + static_cast<size_t>(next) * (C > 1 ? 3 * D : 0);
-                       build_device(ds, d_idx + cb, ce - cb, d_gf + cb, d_hf + cb, HBG_GH_LEAF_ALIGNED, hc, s,
-                                    nullptr, nullptr, 4, true);
-                       part_ptrs.push_back(hc);
-                     }
-                   });
-      if (C > 1) launch_reduce_parts(part_ptrs, static_cast<int64_t>(3 * D), d_hist, s);
     } else if (count > 0) {
+      // fp32 g/h in staged chunks of kStageRows rows. Each staged chunk is
+      // either converted to fp32 by the host pool into the pinned stage and
+      // copied as 8 B/row, or (pinned caller arrays only: `direct`) copied as
+      // fp64 16 B/row straight from the caller's memory and converted on the
+      // device — the split balances host memory bandwidth against PCIe. The
+      // row ids are staged with g/h, each staged chunk checked for
+      // idx[i] == idx[0] + i in the same pass: a histogram chunk whose rows
+      // all pass reads the resident iota (the root, or any leaf of an ordered
+      // layout, uploads no ids); the others upload the ids not yet sent.
+      // Histogram chunk c runs as soon as its rows have landed; the C chunk
+      // histograms are summed in chunk order — the same floats and sums
+      // whichever route each row took (deterministic, bit-identical).
       const size_t n = static_cast<size_t>(count);
-      double* d_gd = static_cast<double*>(ds->host_gd.get(n * 8));
-      double* d_hd = static_cast<double*>(ds->host_hd.get(n * 8));
+      const bool pinned = is_pinned(gradients) && is_pinned(hessians);
       float* d_gf = static_cast<float*>(ds->host_gf.get(n * 4));
       float* d_hf = static_cast<float*>(ds->host_hf.get(n * 4));
-      // The PCIe copies (16 B/row of g/h) go on the copy stream in C chunks;
-      // chunk c's conversion and histogram run on the compute stream as soon
-      // as its bytes have landed, so only the last chunk's work is exposed.
-      // The chunk histograms are summed in chunk order (deterministic).
+      double* d_gd = pinned ? static_cast<double*>(ds->host_gd.get(n * 8)) : nullptr;
+      double* d_hd = pinned ? static_cast<double*>(ds->host_hd.get(n * 8)) : nullptr;
+      const std::vector<char> direct = direct_chunks(count, kStageRows, pinned);
       const int C = host_chunks(count);
       if (!ds->copy_stream) HBG_CUDA(cudaStreamCreateWithFlags(&ds->copy_stream, cudaStreamNonBlocking));
       for (int c = 0; c < 17; ++c)
         if (!ds->chunk_ev[c]) HBG_CUDA(cudaEventCreateWithFlags(&ds->chunk_ev[c], cudaEventDisableTiming));
       HBG_CUDA(cudaEventRecord(ds->chunk_ev[16], s));  // the copy stream starts after prior work on s
       HBG_CUDA(cudaStreamWaitEvent(ds->copy_stream, ds->chunk_ev[16], 0));
-      auto chunk = [&](int c, int64_t& b, int64_t& e) {
-        b = count * c / C;
-        e = count * (c + 1) / C;
-      };
-      for (int c = 0; c < C; ++c) {
-        int64_t b, e;
-        chunk(c, b, e);
-        const size_t m = static_cast<size_t>(e - b);
-        HBG_CUDA(cudaMemcpyAsync(d_gd + b, gradients + b, m * 8, cudaMemcpyHostToDevice, ds->copy_stream));
-        HBG_CUDA(cudaMemcpyAsync(d_hd + b, hessians + b, m * 8, cudaMemcpyHostToDevice, ds->copy_stream));
-        HBG_CUDA(cudaEventRecord(ds->chunk_ev[c], ds->copy_stream));
-      }
-      // while the copy engine moves them, the host checks whether the leaf is
-      // one contiguous row range (the root, or any leaf of an ordered layout):
-      // such a leaf needs no index upload (the kernel reads the resident iota
-      // at the range's start)
-      const int32_t first = indices[0];
-      const int32_t* d_idx;
-      if (leaf_is_contiguous(indices, count)) {
-        require(first >= 0 && first + count <= L.num_rows, "leaf row index out of range");
-        d_idx = identity_rows(ds, first, s);
-      } else {
-        int32_t* di = static_cast<int32_t*>(ds->host_idx.get(n * 4));
-        HBG_CUDA(cudaMemcpyAsync(di, indices, n * 4, cudaMemcpyHostToDevice, ds->copy_stream));
-        HBG_CUDA(cudaEventRecord(ds->chunk_ev[16], ds->copy_stream));
-        HBG_CUDA(cudaStreamWaitEvent(s, ds->chunk_ev[16], 0));
-        d_idx = di;
-      }
+      int32_t* di = static_cast<int32_t*>(ds->host_idx.get(n * 4));
+      const int64_t first = indices[0];
       double* parts = C > 1 ? static_cast<double*>(ds->host_parts.get(static_cast<size_t>(C) * 3 * D * sizeof(double) + 8))
                             : d_hist;
       std::vector<const double*> part_ptrs;
-      for (int c = 0; c < C; ++c) {
-        int64_t b, e;
-        chunk(c, b, e);
-        HBG_CUDA(cudaStreamWaitEvent(s, ds->chunk_ev[c], 0));
-        launch_f64_to_f32(d_gd + b, d_gf + b, e - b, s);
-        launch_f64_to_f32(d_hd + b, d_hf + b, e - b, s);
-        double* hc = parts + static_cast<size_t>(c) * (C > 1 ? 3 * D : 0);
-        build_device(ds, d_idx + b, e - b, d_gf + b, d_hf + b, HBG_GH_LEAF_ALIGNED, hc, s, nullptr, nullptr, 4, true);
-        part_ptrs.push_back(hc);
-      }
+      int next = 0;
+      int64_t sent = 0;         // ids [0, sent) are on the device (or not needed)
+      int64_t converted = 0;    // rows [0, converted) of d_gf/d_hf are final (or queued on s)
+      bool run_contig = true;   // every staged chunk of histogram chunk `next` so far passed
+      stage_chunks(ds, gradients, hessians, indices, count, kStageRows, direct,
+                   [&](int k, int64_t b, int64_t e, const float* gs, const float* hs, const int32_t* is, bool contig,
+                       auto&& fill_ids) {
+                     const size_t m = static_cast<size_t>(e - b);
+                     if (direct[static_cast<size_t>(k)]) {
+                       HBG_CUDA(cudaMemcpyAsync(d_gd + b, gradients + b, m * 8, cudaMemcpyHostToDevice, ds->copy_stream));
+                       HBG_CUDA(cudaMemcpyAsync(d_hd + b, hessians + b, m * 8, cudaMemcpyHostToDevice, ds->copy_stream));
+                       h2d += static_cast<int64_t>(m) * 16;
+                     } else {
+                       HBG_CUDA(cudaMemcpyAsync(d_gf + b, gs + b, m * 4, cudaMemcpyHostToDevice, ds->copy_stream));
+                       HBG_CUDA(cudaMemcpyAsync(d_hf + b, hs + b, m * 4, cudaMemcpyHostToDevice, ds->copy_stream));
+                       h2d += static_cast<int64_t>(m) * 8;
+                     }
+                     run_contig = run_contig && contig;
+                     for (; next < C && count * (next + 1) / C <= e; ++next) {
+                       const int64_t cb = count * next / C, ce = count * (next + 1) / C;
+                       const int32_t* rows_c;
+                       if (run_contig && ce > cb) {
+                         require(first + cb >= 0 && first + ce <= L.num_rows, "leaf row index out of range");
+                         rows_c = identity_rows(ds, first + cb, s);
+                       } else {
+                         if (sent < ce) {
+                           const int64_t from = std::max(sent, cb);
+                           for (int64_t j = from / kStageRows; j <= (ce - 1) / kStageRows; ++j)
+                             fill_ids(static_cast<int>(j));
+                           HBG_CUDA(cudaMemcpyAsync(di + from, is + from, static_cast<size_t>(ce - from) * 4,
+                                                    cudaMemcpyHostToDevice, ds->copy_stream));
+                           h2d += (ce - from) * 4;
+                           sent = ce;
+                         }
+                         rows_c = di + cb;
+                       }
+                       HBG_CUDA(cudaEventRecord(ds->chunk_ev[next], ds->copy_stream));
+                       HBG_CUDA(cudaStreamWaitEvent(s, ds->chunk_ev[next], 0));
+                       // device conversion of the direct rows up to ce
+                       for (int64_t j = converted / kStageRows; converted < ce; ++j) {
+                         const int64_t je = std::min<int64_t>(ce, (j + 1) * kStageRows);
+                         if (direct[static_cast<size_t>(j)]) {
+                           launch_f64_to_f32(d_gd + converted, d_gf + converted, je - converted, s);
+                           launch_f64_to_f32(d_hd + converted, d_hf + converted, je - converted, s);
+                         }
+                         converted = je;
+                       }
+                       double* hc = parts + static_cast<size_t>(next) * (C > 1 ? 3 * D : 0);
+                       build_device(ds, rows_c, ce - cb, d_gf + cb, d_hf + cb, HBG_GH_LEAF_ALIGNED, hc, s,
+                                    nullptr, nullptr, 4, true);
+                       part_ptrs.push_back(hc);
+                       // the staged chunk straddling the boundary also holds
+                       // rows of the next histogram chunk
+                       run_contig = contig;
+                     }
+                   });
       if (C > 1) launch_reduce_parts(part_ptrs, static_cast<int64_t>(3 * D), d_hist, s);
     } else {
       build_device(ds, nullptr, 0, nullptr, nullptr, HBG_GH_LEAF_ALIGNED, d_hist, s);
@@ -1359,6 +1453,15 @@ int hbg_debug_hist_stamps(hbg_dataset* ds, unsigned long long* out) {
     check_ds(ds);
     require(ds->hist_prof.p != nullptr, "no stamps: set HBG_HIST_PROFILE");
     HBG_CUDA(cudaMemcpy(out, ds->hist_prof.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  });
+}
+
+int hbg_debug_host_copy_bytes(hbg_dataset* ds, int64_t* out) {
+  return guarded([&] {
+    check_ds(ds);
+    require(out != nullptr, "null argument");
+    out[0] = ds->copy_h2d;
+    out[1] = ds->copy_d2h;
   });
 }
 
@@ -1561,26 +1664,27 @@ int hbg_grow_tree_host(hbg_dataset* ds, const double* gradients, const double* h
       return;
     }
     float *gf = nullptr, *hf = nullptr;
-    if (N > 0 && !(is_pinned(gradients) && is_pinned(hessians))) {  // pageable: staged as fp32 (stage_chunks)
+    if (N > 0) {  // fp32 g/h through stage_chunks (pinned arrays: a share of the chunks as fp64 directly)
       const size_t n = static_cast<size_t>(N);
+      const bool pinned = is_pinned(gradients) && is_pinned(hessians);
       gf = static_cast<float*>(ds->boost_g.get(n * 4 + 4));
       hf = static_cast<float*>(ds->boost_h.get(n * 4 + 4));
-      stage_chunks(ds, gradients, hessians, nullptr, N, kStageRows,
-                   [&](int, int64_t b, int64_t e, const float* gs, const float* hs, const int32_t*) {
+      double* gd = pinned ? static_cast<double*>(ds->host_gd.get(n * 8)) : nullptr;
+      double* hd = pinned ? static_cast<double*>(ds->host_hd.get(n * 8)) : nullptr;
+      const std::vector<char> direct = direct_chunks(N, kStageRows, pinned);
+      stage_chunks(ds, gradients, hessians, nullptr, N, kStageRows, direct,
+                   [&](int k, int64_t b, int64_t e, const float* gs, const float* hs, const int32_t*, bool, auto&&) {
                      const size_t m = static_cast<size_t>(e - b);
-                     HBG_CUDA(cudaMemcpyAsync(gf + b, gs + b, m * 4, cudaMemcpyHostToDevice, s));
-                     HBG_CUDA(cudaMemcpyAsync(hf + b, hs + b, m * 4, cudaMemcpyHostToDevice, s));
+                     if (direct[static_cast<size_t>(k)]) {
+                       HBG_CUDA(cudaMemcpyAsync(gd + b, gradients + b, m * 8, cudaMemcpyHostToDevice, s));
+                       HBG_CUDA(cudaMemcpyAsync(hd + b, hessians + b, m * 8, cudaMemcpyHostToDevice, s));
+                       launch_f64_to_f32(gd + b, gf + b, e - b, s);
+                       launch_f64_to_f32(hd + b, hf + b, e - b, s);
+                     } else {
+                       HBG_CUDA(cudaMemcpyAsync(gf + b, gs + b, m * 4, cudaMemcpyHostToDevice, s));
+                       HBG_CUDA(cudaMemcpyAsync(hf + b, hs + b, m * 4, cudaMemcpyHostToDevice, s));
+                     }
                    });
-    } else if (N > 0) {
-      const size_t n = static_cast<size_t>(N);
-      double* gd = static_cast<double*>(ds->host_gd.get(n * 8));
-      double* hd = static_cast<double*>(ds->host_hd.get(n * 8));
-      gf = static_cast<float*>(ds->boost_g.get(n * 4 + 4));
-      hf = static_cast<float*>(ds->boost_h.get(n * 4 + 4));
-      HBG_CUDA(cudaMemcpyAsync(gd, gradients, n * 8, cudaMemcpyHostToDevice, s));
-      HBG_CUDA(cudaMemcpyAsync(hd, hessians, n * 8, cudaMemcpyHostToDevice, s));
-      launch_f64_to_f32(gd, gf, N, s);
-      launch_f64_to_f32(hd, hf, N, s);
     }
     if (use_host_loop())
       grow_tree_impl(ds, gf, hf, *params, Reducer{nullptr, nullptr}, split_log, num_splits, nodes, num_nodes, s);

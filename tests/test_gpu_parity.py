@@ -165,11 +165,31 @@ def test_host_dropin_pageable_and_pinned_agree(hbg, oracle):
     with hbg.Dataset(cols, 64) as ds:
         for idx in (np.arange(rows, dtype=np.int32),                        # contiguous: no index upload
                     np.sort(rng.choice(rows, size=2_200_000, replace=False)).astype(np.int32),
-                    rng.permutation(rows)[:700_001].astype(np.int32)):
+                    rng.permutation(rows)[:700_001].astype(np.int32),
+                    # mixed: the pageable path checks each staged chunk and uses
+                    # the resident iota only for histogram chunks that pass
+                    np.arange(7, 2_300_007, dtype=np.int32),              # one range, not from row 0
+                    np.concatenate([np.arange(1_300_000), np.sort(rng.choice(np.arange(1_300_000, rows), 900_000,
+                                                                              replace=False))]).astype(np.int32),
+                    np.concatenate([np.sort(rng.choice(1_000_000, 400_000, replace=False)),
+                                    np.arange(1_000_000, rows)]).astype(np.int32),
+                    np.concatenate([np.arange(600_000), np.arange(600_001, 2_400_000)]).astype(np.int32)):
             g, h = rng.normal(size=len(idx)), rng.random(len(idx))
+            n = len(idx)
+            contiguous = bool((np.diff(idx) == 1).all())
+            ids_bytes = 0 if contiguous else 4 * n
             a = hbg.build_histograms_partitioned(ds, hbg.LeafState(idx, g, h))
+            page_h2d, d2h = ds.host_copy_bytes()
             b = hbg.build_histograms_partitioned(ds, hbg.LeafState(pinned(idx), pinned(g), pinned(h)))
+            pin_h2d, _ = ds.host_copy_bytes()
             assert a.tobytes() == b.tobytes()
+            assert d2h == a.nbytes
+            if contiguous or (np.diff(idx) != 1).any() and n == 700_001:  # all chunks one route for the ids
+                assert page_h2d == 8 * n + ids_bytes
+                # pinned: some staged chunks go as fp64 (16 B/row), the rest as fp32
+                assert 8 * n + ids_bytes < pin_h2d < 16 * n + ids_bytes
+            else:
+                assert 8 * n <= page_h2d <= 12 * n
         g, h = rng.normal(size=rows), rng.random(rows)
         la, na = ds.grow_tree_host(g, h, 63, 20, 0.0)
         lb, nb = ds.grow_tree_host(pinned(g), pinned(h), 63, 20, 0.0)
