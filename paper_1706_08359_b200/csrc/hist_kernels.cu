@@ -52,17 +52,24 @@ __device__ __forceinline__ uint32_t dsmem_addr(const void* p, int q) {
 }
 __device__ __forceinline__ float ld_dsmem(const float* p, int q) {
   float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(dsmem_addr(p, q)) : "memory");
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(dsmem_addr(p, q)));
   return v;
 }
 __device__ __forceinline__ double ld_dsmem(const double* p, int q) {
   double v;
-  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(dsmem_addr(p, q)) : "memory");
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(dsmem_addr(p, q)));
+  return v;
+}
+__device__ __forceinline__ uint4 ld_dsmem_v4(const void* p, int q) {  // 16-byte aligned
+  uint4 v;
+  asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(dsmem_addr(p, q)));
   return v;
 }
 __device__ __forceinline__ uint32_t ld_dsmem(const uint32_t* p, int q) {
   uint32_t v;
-  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(dsmem_addr(p, q)) : "memory");
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(dsmem_addr(p, q)));
   return v;
 }
 
@@ -269,14 +276,59 @@ __global__ void __launch_bounds__(K >= 256 ? 128 : 512, BITS == 4 ? 2 : 1) hist_
         a.sibling[2 * D + o] = pc - static_cast<double>(vc);
       }
     };
+    // Gather cells [i0, i1) of the C sub-histograms into local staging (the
+    // per-warp cells and the count cells are free once folded) as 16-byte
+    // remote loads, all of a thread's loads in flight at once; the CTAs start
+    // at different ranks so they do not all read the same CTA's shared memory
+    // at the same time. Then the sums, in rank order (deterministic).
+    {
+      T* st_g = reinterpret_cast<T*>(smem);  // [C][per]: C * per == ncell <= cw * kCells
+      T* st_h = st_g + static_cast<size_t>(C) * per;
+      uint32_t* st_c = cnt;                  // [C][per]: the count cells
+      const int nloc = max(0, i1 - i0);
+      const int vgh = nloc * static_cast<int>(sizeof(T)) / 16, vc = nloc / 4;  // 16-B vectors per array
+      const int per_rank = 2 * vgh + vc;
+      const int items = C * per_rank;
+      constexpr int kBatch = 8;
+      for (int base = 0; base < items; base += kBatch * static_cast<int>(blockDim.x)) {
+        uint4 v[kBatch];
+        uint4* dst[kBatch];
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+          const int it = base + b * static_cast<int>(blockDim.x) + static_cast<int>(threadIdx.x);
+          dst[b] = nullptr;
+          if (it < items) {
+            const int qq = it / per_rank, k = it - qq * per_rank;
+            const int q = qq + r < C ? qq + r : qq + r - C;
+            const void* src;
+            if (k < vgh) {
+              src = reinterpret_cast<const uint4*>(sub_g + i0) + k;
+              dst[b] = reinterpret_cast<uint4*>(st_g + static_cast<size_t>(q) * per) + k;
+            } else if (k < 2 * vgh) {
+              src = reinterpret_cast<const uint4*>(sub_h + i0) + (k - vgh);
+              dst[b] = reinterpret_cast<uint4*>(st_h + static_cast<size_t>(q) * per) + (k - vgh);
+            } else {
+              src = reinterpret_cast<const uint4*>(sub_c + i0) + (k - 2 * vgh);
+              dst[b] = reinterpret_cast<uint4*>(st_c + static_cast<size_t>(q) * per) + (k - 2 * vgh);
+            }
+            v[b] = ld_dsmem_v4(src, q);
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b)
+          if (dst[b] != nullptr) *dst[b] = v[b];
+      }
+      __syncthreads();
+    }
     for (int i = i0 + static_cast<int>(threadIdx.x); i < i1; i += blockDim.x) {
+      const T* st_g = reinterpret_cast<const T*>(smem);
+      const T* st_h = st_g + static_cast<size_t>(C) * per;
       double vg = 0.0, vh = 0.0;
       unsigned long long vc = 0;
-#pragma unroll 4
       for (int q = 0; q < C; ++q) {
-        vg += static_cast<double>(ld_dsmem(sub_g + i, q));
-        vh += static_cast<double>(ld_dsmem(sub_h + i, q));
-        vc += ld_dsmem(sub_c + i, q);
+        vg += static_cast<double>(st_g[q * per + (i - i0)]);
+        vh += static_cast<double>(st_h[q * per + (i - i0)]);
+        vc += cnt[q * per + (i - i0)];
       }
       if (nk == 1) {
         emit(i, vg, vh, vc);

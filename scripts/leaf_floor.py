@@ -3,11 +3,13 @@
 For leaves of the Higgs 10.5M x 28 k64 dataset at depth D (rows >> D, random
 sorted rows, leaf-aligned fp32 g/h), prints per call:
   host_loop_us  — Python loop of build_histograms_device (ctypes + launches)
+  issue_us      — host time per call of that loop (no synchronisation)
   graph_us      — the same call captured in a CUDA graph, replayed (GPU only)
   kernel_us     — the histogram kernel alone (library CUDA events)
 """
 import os
 import sys
+import time
 
 import numpy as np
 import torch
@@ -44,8 +46,10 @@ def main():
         reps = 200
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(s)
+        t0 = time.perf_counter()
         for _ in range(reps):
             ds.build_histograms_device(li, m, lg, lh, hist, hbg.HBG_GH_LEAF_ALIGNED, sp)
+        issue_us = (time.perf_counter() - t0) / reps * 1e6
         b.record(s)
         torch.cuda.synchronize()
         host_us = a.elapsed_time(b) / reps * 1e3
@@ -73,17 +77,19 @@ def main():
             with torch.cuda.graph(gr, stream=s):
                 for _ in range(10):
                     ds.build_histograms_device(li, m, lg, lh, hist, hbg.HBG_GH_LEAF_ALIGNED, torch.cuda.current_stream().cuda_stream)
-            gr.replay()
-            torch.cuda.synchronize()
-            a.record(s)
-            for _ in range(20):
+            with torch.cuda.stream(s):  # replay on s, where the events are recorded
                 gr.replay()
-            b.record(s)
+                torch.cuda.synchronize()
+                a.record(s)
+                for _ in range(20):
+                    gr.replay()
+                b.record(s)
             torch.cuda.synchronize()
             graph_us = a.elapsed_time(b) / 200 * 1e3
         except Exception as e:  # noqa: BLE001
             print("graph capture failed:", str(e)[:120])
-        print(f"D{depth:2d} rows {m:9d}  host_loop_us {host_us:8.1f}  graph_us {graph_us:8.1f}  kernel_us {kern_us:8.1f}",
+        print(f"D{depth:2d} rows {m:9d}  host_loop_us {host_us:8.1f}  issue_us {issue_us:6.1f}  graph_us {graph_us:8.1f}"
+              f"  kernel_us {kern_us:8.1f}",
               flush=True)
     ds.close()
 
