@@ -4,7 +4,7 @@
 # a summary table gpurun_out/sanitize_summary.txt.
 #   bash scripts/sanitize.sh [cases...]
 mkdir -p gpurun_out
-CASES=${@:-smoke hist leafseq tree_wave tree_onesplit tree_host tree_bits64 peer2}
+CASES=${@:-smoke hist leafseq dropin tree_wave tree_onesplit tree_host tree_bits64 peer2}
 export HBG_PEER_TIMEOUT_MS=${HBG_PEER_TIMEOUT_MS:-120000}
 export CUDA_DEVICE_MAX_CONNECTIONS=32
 SUM=gpurun_out/sanitize_summary.txt

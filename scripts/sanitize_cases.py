@@ -2,7 +2,7 @@
 
     python scripts/sanitize_cases.py CASE
 
-CASE: smoke | hist | leafseq | tree_wave | tree_onesplit | tree_host | tree_bits64 | peer2
+CASE: smoke | hist | leafseq | dropin | tree_wave | tree_onesplit | tree_host | tree_bits64 | peer2
 Each case is small (the tools replay every memory access), checks its result
 against the oracle, and exits 0 on success.
 """
@@ -69,6 +69,30 @@ def leafseq():
     print("leafseq: counts exact on 6 leaf sizes")
 
 
+def dropin():
+    """The host drop-in with pageable and pinned LeafState arrays: staged fp32
+    and fp64-direct chunks, contiguous (iota) and uploaded row ids."""
+    import torch
+
+    import paper_1706_08359_b200 as hbg
+    from oracle import ffi
+
+    rows, d, k = 1_200_000, 28, 64
+    cols = ffi.gen_synthetic_bins(rows, d, k, 5)
+    g, h = ffi.gen_grad_hess(rows, 5)
+    rng = np.random.default_rng(5)
+    with hbg.Dataset(cols, k) as ds:
+        for idx in (np.arange(rows, dtype=np.int32), np.sort(rng.choice(rows, 900_000, replace=False)).astype(np.int32)):
+            lg, lh = g[idx], h[idx]
+            a = hbg.build_histograms_partitioned(ds, hbg.LeafState(idx, lg, lh))
+            pin = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy() for x in (idx, lg, lh)]
+            b = hbg.build_histograms_partitioned(ds, hbg.LeafState(*pin))
+            assert a.tobytes() == b.tobytes()
+            want = ffi.build_histograms(cols, k, idx, lg, lh, 64)
+            assert (a["count"] == want["count"]).all()
+    print("dropin: pageable and pinned identical, counts exact")
+
+
 def peer2():
     """Two ranks as threads on one GPU exchanging through peer memory."""
     import torch
@@ -130,6 +154,8 @@ def main():
         tree("host", precision=64)
     elif case == "leafseq":
         leafseq()
+    elif case == "dropin":
+        dropin()
     elif case == "peer2":
         peer2()
     else:
