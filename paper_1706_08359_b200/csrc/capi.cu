@@ -1430,9 +1430,9 @@ int hbg_build_histograms_ex(hbg_dataset* ds, const int32_t* indices, int64_t cou
                        build_device(ds, rows_c, ce - cb, d_gf + cb, d_hf + cb, HBG_GH_LEAF_ALIGNED, hc, s,
                                     nullptr, nullptr, 4, true);
                        part_ptrs.push_back(hc);
-                       // the staged chunk straddling the boundary also holds
+                       // a staged chunk straddling the boundary also holds
                        // rows of the next histogram chunk
-                       run_contig = contig;
+                       run_contig = ce < e ? contig : true;
                      }
                    });
       if (C > 1) launch_reduce_parts(part_ptrs, static_cast<int64_t>(3 * D), d_hist, s);

@@ -173,7 +173,10 @@ def test_host_dropin_pageable_and_pinned_agree(hbg, oracle):
                                                                               replace=False))]).astype(np.int32),
                     np.concatenate([np.sort(rng.choice(1_000_000, 400_000, replace=False)),
                                     np.arange(1_000_000, rows)]).astype(np.int32),
-                    np.concatenate([np.arange(600_000), np.arange(600_001, 2_400_000)]).astype(np.int32)):
+                    np.concatenate([np.arange(600_000), np.arange(600_001, 2_400_000)]).astype(np.int32),
+                    # 2^21 rows: histogram chunks = staged chunks; the first scattered, the rest one range
+                    np.concatenate([[0], np.sort(rng.choice(np.arange(1, 2 * 524_288), 524_287, replace=False)),
+                                    np.arange(524_288, 1 << 21)]).astype(np.int32)):
             g, h = rng.normal(size=len(idx)), rng.random(len(idx))
             n = len(idx)
             contiguous = bool((np.diff(idx) == 1).all())
@@ -188,6 +191,8 @@ def test_host_dropin_pageable_and_pinned_agree(hbg, oracle):
                 assert page_h2d == 8 * n + ids_bytes
                 # pinned: some staged chunks go as fp64 (16 B/row), the rest as fp32
                 assert 8 * n + ids_bytes < pin_h2d < 16 * n + ids_bytes
+            elif n == 1 << 21:  # only the first histogram chunk's ids travel
+                assert page_h2d == 8 * n + 4 * 524_288
             else:
                 assert 8 * n <= page_h2d <= 12 * n
         g, h = rng.normal(size=rows), rng.random(rows)
