@@ -515,6 +515,10 @@ void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const vo
   if (d_idx == nullptr) d_idx = identity_rows(ds, 0, s);  // identity leaf [0, count)
   HistPlan plan = plan_histogram(L.bits_per_bin, L.max_bin, L.num_groups, count, L.device, true, acc_bytes,
                                  allow_fused);
+  if (std::getenv("HBG_PLAN_DEBUG"))  // development aid
+    std::fprintf(stderr, "[hbg plan] n=%lld ctas=%d warps=%d wpg=%d gb=%d nseg=%d seg_len=%lld cluster=%d x %d smem=%zu\n",
+                 static_cast<long long>(count), plan.ctas, plan.warps, plan.wpg, plan.gb, plan.nseg,
+                 static_cast<long long>(plan.seg_len), plan.cluster, plan.nclusters, plan.smem);
   char* part = static_cast<char*>(ds->part.get(hist_part_bytes(plan)));
   HistArgs a{};
   a.packed = reinterpret_cast<const uint8_t*>(ds->packed);
@@ -546,6 +550,8 @@ void build_device(hbg_dataset* ds, const int32_t* d_idx, int64_t count, const vo
   if (prof) {
     a.prof = static_cast<unsigned long long*>(ds->hist_prof.get(64));
     HBG_CUDA(cudaMemsetAsync(a.prof, 0, 64, s));
+    static const int cta = std::getenv("HBG_HIST_PROFILE_CTA") ? std::atoi(std::getenv("HBG_HIST_PROFILE_CTA")) : 0;
+    a.prof_cta = std::min(cta, plan.ctas - 1);
   }
   if (plan.nclusters > 1) {  // counters zeroed once; every launch leaves them 0
     const size_t need = static_cast<size_t>(std::max(plan.nblocks, 1)) * sizeof(unsigned) + 64;

@@ -86,7 +86,8 @@ struct HistArgs {
   int cluster;  // HistPlan::cluster
   int nclusters;
   unsigned* bar;  // multi-cluster mode: one arrival counter per group block
-  unsigned long long* prof;  // optional %globaltimer stamps of CTA 0 (HBG_HIST_PROFILE), 8 slots
+  unsigned long long* prof;  // optional %globaltimer stamps of one CTA (HBG_HIST_PROFILE), 8 slots
+  int prof_cta;              // the stamped CTA (HBG_HIST_PROFILE_CTA, default 0)
 };
 
 // allow_direct = false: always per-CTA partials + a reduction (the row-sharded

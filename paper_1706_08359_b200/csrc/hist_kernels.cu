@@ -74,7 +74,7 @@ __device__ __forceinline__ uint32_t ld_dsmem(const uint32_t* p, int q) {
 }
 
 __device__ __forceinline__ void hist_stamp(const HistArgs& a, int slot) {
-  if (a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+  if (a.prof != nullptr && blockIdx.x == static_cast<unsigned>(a.prof_cta) && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     a.prof[slot] = t;
