@@ -102,11 +102,13 @@ int hbg_dataset_packed_words(const hbg_dataset* ds, uint32_t* host_words);
  * Host drop-in for build_histograms_partitioned: indices/gradients/hessians
  * are the LeafState arrays (leaf-aligned doubles, leaf.hpp:13-21); `out`
  * receives num_features * max_bin bins, feature-major (HistogramSet order).
- * Synchronous. count == 0 gives an all-zero histogram. Pinned host arrays
- * (cudaHostAlloc/cudaHostRegister) are copied directly (fp64 over PCIe);
- * pageable ones are converted to fp32 by a library thread pool into a pinned
- * stage chunk by chunk while finished chunks are copied — the same floats,
- * bit-identical results either way. */
+ * Synchronous. count == 0 gives an all-zero histogram. The arrays go up in
+ * chunks, each either converted to fp32 by a library thread pool into a
+ * pinned stage and copied (8 B/row), or — for pinned host arrays
+ * (cudaHostAlloc/cudaHostRegister), a share of the chunks — copied as fp64
+ * (16 B/row) and converted on the device; row ids travel only for chunks that
+ * are not one contiguous range. The same floats and sums on every route:
+ * bit-identical results. */
 int hbg_build_histograms(hbg_dataset* ds, const int32_t* indices, int64_t count,
                          const double* gradients, const double* hessians, hbg_bin* out);
 /* The same call with the reference's PrecisionMode argument
@@ -234,8 +236,8 @@ int hbg_grow_tree_f64(hbg_dataset* ds, const double* d_grad, const double* d_hes
 /* Host-pointer drop-in for grow_tree (tree.cpp:186-261): fp64 per-row
  * gradients/hessians in host memory (the reference's std::span<const double>
  * arguments). params->precision BITS32: cast to fp32 (the bits32 per-element
- * cast, histogram.cpp:97-98; on the device for pinned arrays, by the staging
- * pool for pageable ones), then grown as hbg_grow_tree; BITS64: uploaded as
+ * cast, histogram.cpp:97-98; by the staging pool, or on the device for a
+ * share of the chunks of pinned arrays), then grown as hbg_grow_tree; BITS64: uploaded as
  * fp64 and grown as hbg_grow_tree_f64. split_log: host,
  * num_leaves-1 entries; nodes: host, 2*num_leaves-1 entries. Synchronous. */
 int hbg_grow_tree_host(hbg_dataset* ds, const double* gradients, const double* hessians,
