@@ -1730,7 +1730,7 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
 // output (split log, tree, score-update ranges) is written once at the end
 // from the replayed commit log.
 
-constexpr int kWN = 1280;  // node ids per tree (shared-memory state)
+constexpr int kWN = 2048;  // node ids per tree (shared-memory state)
 static_assert(kWN <= 2048, "node ids are packed in 11 bits");
 
 // Speculation order: prio buckets of 1/32 octave (a positive float's top 13 bits).

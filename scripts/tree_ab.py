@@ -1,5 +1,5 @@
 """A/B of the device tree (255 leaves, Higgs 10.5M x 28 k64) between two
-builds of the library: python scripts/tree_ab.py REPO_DIR [trees]
+builds of the library: python scripts/tree_ab.py REPO_DIR [trees] [rows]
 Prints per-tree device time (CUDA events) and the host drop-in's wall time."""
 import os
 import sys
@@ -13,7 +13,7 @@ sys.path.insert(0, root)
 import paper_1706_08359_b200 as hbg  # noqa: E402
 
 trees = int(sys.argv[2]) if len(sys.argv) > 2 else 20
-rows, d, k = 10_500_000, 28, 64
+rows, d, k = (int(sys.argv[3]) if len(sys.argv) > 3 else 10_500_000), 28, 64
 rng = np.random.default_rng(0)
 cols = rng.integers(1, k, size=(d, rows), dtype=np.uint8)
 g = 2.0 * rng.random(rows) - 1.0
