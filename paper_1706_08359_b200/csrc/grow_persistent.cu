@@ -197,7 +197,9 @@ __device__ __forceinline__ void set_error(const GrowArgs& a, int e) { atomicCAS(
 __device__ __forceinline__ void grid_sync(const GrowArgs& a) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();  // as cooperative_groups' grid sync: the CTA's writes before the arrival
+    // The arrival is a release and the poll an acquire at gpu scope, both
+    // cumulative over the CTA's writes ordered before them by __syncthreads:
+    // no separate fences.
     const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
     const unsigned old = atom_add_acq_rel(a.bar, inc);
     const long long t0 = clock64();
@@ -207,7 +209,6 @@ __device__ __forceinline__ void grid_sync(const GrowArgs& a) {
         break;
       }
     }
-    __threadfence();
   }
   __syncthreads();
 }
@@ -2184,13 +2185,11 @@ __device__ void chunk_done(const GrowArgs& a, const Desc& D, int nwc) {
   __shared__ int s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned old = atomicAdd(a.wcnt + D.mslot, 1u);
+    // acq_rel: releases this CTA's winners (ordered before by __syncthreads)
+    // and, for the last arrival, acquires every other chunk's
+    const unsigned old = atom_add_acq_rel(a.wcnt + D.mslot, 1u);
     s_last = old == static_cast<unsigned>(nwc - 1) ? 1 : 0;
-    if (s_last) {
-      a.wcnt[D.mslot] = 0u;  // every chunk has arrived: reset for the next wave
-      __threadfence();
-    }
+    if (s_last) a.wcnt[D.mslot] = 0u;  // every chunk has arrived: reset for the next wave (a grid barrier follows)
   }
   __syncthreads();
   if (s_last) publish_member<NT>(a, D, nwc);
