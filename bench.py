@@ -587,7 +587,7 @@ def run_hbg(args):
             for _ in range(args.trees):
                 ds.grow_tree_host(pg64, ph64, args.num_leaves, 1, 0.0)
             result["tree"]["e2e_sec_per_tree"] = (time.perf_counter() - t0) / args.trees
-            result["tree"]["e2e_api"] = "hbg_grow_tree_host (host fp64 g/h, 16 B/row H2D; split log + nodes D2H)"
+            result["tree"]["e2e_api"] = "hbg_grow_tree_host (host fp64 g/h: staged chunks as fp32, a share of pinned chunks as fp64; split log + nodes D2H)"
             g64, h64 = g.astype(np.float64), h.astype(np.float64)  # pageable: the host-staged fp32 path
             ds.grow_tree_host(g64, h64, args.num_leaves, 1, 0.0)
             t0 = time.perf_counter()
