@@ -114,7 +114,8 @@ int hbg_build_histograms(hbg_dataset* ds, const int32_t* indices, int64_t count,
 /* The same call with the reference's PrecisionMode argument
  * (build_histograms_partitioned(data, leaf, precision), histogram.hpp:133):
  * HBG_PRECISION_BITS32 is hbg_build_histograms; HBG_PRECISION_BITS64 uploads
- * the fp64 LeafState arrays as they are (16 B/row) and accumulates in fp64. */
+ * the fp64 LeafState arrays as they are (16 B/row; pageable ones through the
+ * library's pinned stage) and accumulates in fp64. */
 int hbg_build_histograms_ex(hbg_dataset* ds, const int32_t* indices, int64_t count,
                             const double* gradients, const double* hessians, int32_t precision,
                             hbg_bin* out);

@@ -349,6 +349,14 @@ inline void convert_stream(const double* src, float* dst, int64_t n) {
 #endif
   for (; i < n; ++i) dst[i] = static_cast<float>(src[i]);
 }
+inline void convert_stream(const double* src, double* dst, int64_t n) {  // bits64: a plain copy
+  int64_t i = 0;
+#if defined(__SSE2__)
+  for (; i < n && (reinterpret_cast<uintptr_t>(dst + i) & 15) != 0; ++i) dst[i] = src[i];
+  for (; i + 2 <= n; i += 2) _mm_stream_pd(dst + i, _mm_loadu_pd(src + i));
+#endif
+  for (; i < n; ++i) dst[i] = src[i];
+}
 inline void copy_stream(const int32_t* src, int32_t* dst, int64_t n) {
   int64_t i = 0;
 #if defined(__SSE2__)
@@ -365,20 +373,21 @@ inline void store_fence() {
 }
 
 // Stage rows [0, n) of fp64 g/h (and, when idx != nullptr, the int32 row ids)
-// into the pinned stage as fp32 (g | h | idx), in chunks of `chunk` rows
+// into the pinned stage as Out (g | h | idx; float: the bits32 cast, double:
+// a copy for bits64), in chunks of `chunk` rows
 // converted by the host pool (chunks with direct[c] set are only checked:
 // their g/h go up as fp64 straight from pinned caller memory); copy(c, b, e, gf, hf, id, contiguous) runs on
 // the calling thread, in chunk order, as soon as chunk c is staged;
 // `contiguous` says chunk c's ids are idx[0] + i (checked by the staging pass,
 // which then stores no ids for it); a copy() that uploads ids of chunk c
 // first calls fill_ids(c). Returns after the last copy was issued.
-template <typename Copy>
+template <typename Out = float, typename Copy>
 void stage_chunks(hbg_dataset* ds, const double* g, const double* h, const int32_t* idx, int64_t n, int64_t chunk,
                   const std::vector<char>& direct, Copy copy) {
   const size_t rows = static_cast<size_t>(n);
-  char* st = static_cast<char*>(stage_buffer(ds, rows * (idx ? 12 : 8) + 64));
-  float* gf = reinterpret_cast<float*>(st);
-  float* hf = gf + rows;
+  char* st = static_cast<char*>(stage_buffer(ds, rows * (2 * sizeof(Out) + (idx ? 4 : 0)) + 64));
+  Out* gf = reinterpret_cast<Out*>(st);
+  Out* hf = gf + rows;
   int32_t* id = reinterpret_cast<int32_t*>(hf + rows);
   const int C = static_cast<int>((n + chunk - 1) / chunk);
   HostPool& pool = HostPool::get();
@@ -1335,23 +1344,62 @@ int hbg_build_histograms_ex(hbg_dataset* ds, const int32_t* indices, int64_t cou
     ds->copy_d2h = static_cast<int64_t>(D * sizeof(hbg_bin));
     if (count > 0 && precision == HBG_PRECISION_BITS64) {
       // bits64: the fp64 LeafState arrays go up as they are (no per-element
-      // cast); pinned ones at full PCIe rate, pageable ones through the
-      // driver's staging. One histogram launch accumulates in fp64.
+      // cast): pinned ones straight from the caller's memory, pageable ones
+      // copied chunk by chunk into the pinned stage by the host pool (the
+      // driver's own pageable path runs at ~11 GB/s). One histogram launch
+      // accumulates in fp64.
       const size_t n = static_cast<size_t>(count);
       double* d_gd = static_cast<double*>(ds->host_gd.get(n * 8));
       double* d_hd = static_cast<double*>(ds->host_hd.get(n * 8));
-      HBG_CUDA(cudaMemcpyAsync(d_gd, gradients, n * 8, cudaMemcpyHostToDevice, s));
-      HBG_CUDA(cudaMemcpyAsync(d_hd, hessians, n * 8, cudaMemcpyHostToDevice, s));
-      h2d += static_cast<int64_t>(n) * 16;
       const int32_t* d_idx;
-      if (leaf_is_contiguous(indices, count)) {
-        require(indices[0] >= 0 && indices[0] + count <= L.num_rows, "leaf row index out of range");
-        d_idx = identity_rows(ds, indices[0], s);
+      if (is_pinned(gradients) && is_pinned(hessians)) {
+        HBG_CUDA(cudaMemcpyAsync(d_gd, gradients, n * 8, cudaMemcpyHostToDevice, s));
+        HBG_CUDA(cudaMemcpyAsync(d_hd, hessians, n * 8, cudaMemcpyHostToDevice, s));
+        h2d += static_cast<int64_t>(n) * 16;
+        if (leaf_is_contiguous(indices, count)) {
+          require(indices[0] >= 0 && indices[0] + count <= L.num_rows, "leaf row index out of range");
+          d_idx = identity_rows(ds, indices[0], s);
+        } else {
+          int32_t* di = static_cast<int32_t*>(ds->host_idx.get(n * 4));
+          HBG_CUDA(cudaMemcpyAsync(di, indices, n * 4, cudaMemcpyHostToDevice, s));
+          h2d += static_cast<int64_t>(n) * 4;
+          d_idx = di;
+        }
       } else {
+        if (!ds->copy_stream) HBG_CUDA(cudaStreamCreateWithFlags(&ds->copy_stream, cudaStreamNonBlocking));
+        for (int c = 0; c < 17; ++c)
+          if (!ds->chunk_ev[c]) HBG_CUDA(cudaEventCreateWithFlags(&ds->chunk_ev[c], cudaEventDisableTiming));
+        HBG_CUDA(cudaEventRecord(ds->chunk_ev[16], s));
+        HBG_CUDA(cudaStreamWaitEvent(ds->copy_stream, ds->chunk_ev[16], 0));
         int32_t* di = static_cast<int32_t*>(ds->host_idx.get(n * 4));
-        HBG_CUDA(cudaMemcpyAsync(di, indices, n * 4, cudaMemcpyHostToDevice, s));
-        h2d += static_cast<int64_t>(n) * 4;
-        d_idx = di;
+        // the ids travel unless every chunk is one range from idx[0]: chunks
+        // that pass are held back until one fails (then all go)
+        bool all_contig = true;
+        int64_t sent = 0;
+        stage_chunks<double>(ds, gradients, hessians, indices, count, kStageRows, direct_chunks(count, kStageRows, false),
+                             [&](int k, int64_t b, int64_t e, const double* gs, const double* hs, const int32_t* is,
+                                 bool contig, auto&& fill_ids) {
+                               const size_t m = static_cast<size_t>(e - b);
+                               HBG_CUDA(cudaMemcpyAsync(d_gd + b, gs + b, m * 8, cudaMemcpyHostToDevice, ds->copy_stream));
+                               HBG_CUDA(cudaMemcpyAsync(d_hd + b, hs + b, m * 8, cudaMemcpyHostToDevice, ds->copy_stream));
+                               h2d += static_cast<int64_t>(m) * 16;
+                               all_contig = all_contig && contig;
+                               if (!all_contig) {
+                                 for (int j = static_cast<int>(sent / kStageRows); j <= k; ++j) fill_ids(j);
+                                 HBG_CUDA(cudaMemcpyAsync(di + sent, is + sent, static_cast<size_t>(e - sent) * 4,
+                                                          cudaMemcpyHostToDevice, ds->copy_stream));
+                                 h2d += (e - sent) * 4;
+                                 sent = e;
+                               }
+                             });
+        HBG_CUDA(cudaEventRecord(ds->chunk_ev[0], ds->copy_stream));
+        HBG_CUDA(cudaStreamWaitEvent(s, ds->chunk_ev[0], 0));
+        if (all_contig) {
+          require(indices[0] >= 0 && indices[0] + count <= L.num_rows, "leaf row index out of range");
+          d_idx = identity_rows(ds, indices[0], s);
+        } else {
+          d_idx = di;
+        }
       }
       build_device(ds, d_idx, count, d_gd, d_hd, HBG_GH_LEAF_ALIGNED, d_hist, s, nullptr, nullptr, 8, true);
     } else if (count > 0) {
@@ -1661,9 +1709,17 @@ int hbg_grow_tree_host(hbg_dataset* ds, const double* gradients, const double* h
       const size_t n = static_cast<size_t>(N);
       double* gd = static_cast<double*>(ds->host_gd.get(n * 8 + 8));
       double* hd = static_cast<double*>(ds->host_hd.get(n * 8 + 8));
-      if (N > 0) {
+      if (N > 0 && is_pinned(gradients) && is_pinned(hessians)) {
         HBG_CUDA(cudaMemcpyAsync(gd, gradients, n * 8, cudaMemcpyHostToDevice, s));
         HBG_CUDA(cudaMemcpyAsync(hd, hessians, n * 8, cudaMemcpyHostToDevice, s));
+      } else if (N > 0) {  // pageable: copied into the pinned stage by the host pool, chunk by chunk
+        stage_chunks<double>(ds, gradients, hessians, nullptr, N, kStageRows, direct_chunks(N, kStageRows, false),
+                             [&](int, int64_t b, int64_t e, const double* gs, const double* hs, const int32_t*, bool,
+                                 auto&&) {
+                               const size_t m = static_cast<size_t>(e - b);
+                               HBG_CUDA(cudaMemcpyAsync(gd + b, gs + b, m * 8, cudaMemcpyHostToDevice, s));
+                               HBG_CUDA(cudaMemcpyAsync(hd + b, hs + b, m * 8, cudaMemcpyHostToDevice, s));
+                             });
       }
       grow_tree_impl(ds, gd, hd, *params, Reducer{nullptr, nullptr}, split_log, num_splits, nodes, num_nodes, s);
       HBG_CUDA(cudaStreamSynchronize(s));
