@@ -451,6 +451,11 @@ void stage_chunks(hbg_dataset* ds, const double* g, const double* h, const int32
     }
   } catch (...) {
     pool.wait();  // the workers still use `done` and the stage
+    // copies already issued may still read the stage or the caller's pinned
+    // arrays: let them finish before the caller gets control back
+    if (ds->copy_stream) (void)cudaStreamSynchronize(ds->copy_stream);
+    (void)cudaStreamSynchronize(ds->stream);
+    (void)cudaGetLastError();
     throw;
   }
   const double t_issue = prof ? us() : 0;
