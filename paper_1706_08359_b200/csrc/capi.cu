@@ -212,27 +212,6 @@ void check_ds(const hbg_dataset* ds) { require(ds != nullptr, "null dataset hand
 // the synchronous host drop-in.
 cudaStream_t pick(hbg_dataset*, void* stream) { return static_cast<cudaStream_t>(stream); }
 
-// idx[i] == idx[0] + i for all i? O(1) reject on the endpoints, then a
-// parallel scan (host threads; runs while the g/h copies are in flight).
-bool leaf_is_contiguous(const int32_t* idx, int64_t n) {
-  if (n <= 0) return false;
-  if (static_cast<int64_t>(idx[n - 1]) - idx[0] != n - 1) return false;
-  const int64_t first = idx[0];
-  auto check = [&](int64_t b, int64_t e) {
-    for (int64_t i = b; i < e; ++i)
-      if (idx[i] != first + i) return false;
-    return true;
-  };
-  const int T = n < (1 << 20) ? 1 : static_cast<int>(std::min<unsigned>(8, std::max(1u, std::thread::hardware_concurrency())));
-  if (T == 1) return check(0, n);
-  std::vector<char> ok(static_cast<size_t>(T), 1);
-  std::vector<std::thread> th;
-  for (int t = 1; t < T; ++t)
-    th.emplace_back([&, t] { ok[static_cast<size_t>(t)] = check(n * t / T, n * (t + 1) / T); });
-  ok[0] = check(0, n / T);
-  for (auto& x : th) x.join();
-  return std::all_of(ok.begin(), ok.end(), [](char c) { return c != 0; });
-}
 
 // ---- pageable host inputs -----------------------------------------------------
 // The reference's LeafState arrays are std::vectors: pageable memory, which a
@@ -396,9 +375,11 @@ void stage_chunks(hbg_dataset* ds, const double* g, const double* h, const int32
   const int64_t first = idx && n > 0 ? idx[0] : 0;
   // done[c]: workers finished with chunk c; broken[c]: some id of chunk c is
   // not first + i (the chunk is not a piece of one contiguous row range)
-  std::unique_ptr<std::atomic<int>[]> done(new std::atomic<int>[static_cast<size_t>(2 * C)]);
+  std::unique_ptr<std::atomic<int>[]> done(new std::atomic<int>[static_cast<size_t>(3 * C)]);
   std::atomic<int>* broken = done.get() + C;
-  for (int c = 0; c < 2 * C; ++c) done[static_cast<size_t>(c)].store(0, std::memory_order_relaxed);
+  std::atomic<int>* outside = done.get() + 2 * C;  // some id of chunk c is not a row of the dataset
+  for (int c = 0; c < 3 * C; ++c) done[static_cast<size_t>(c)].store(0, std::memory_order_relaxed);
+  const uint32_t limit = static_cast<uint32_t>(ds->layout.num_rows);
   static const bool prof = std::getenv("HBG_STAGE_PROFILE") != nullptr;
   const auto t0 = std::chrono::steady_clock::now();
   auto us = [&] { return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count(); };
@@ -417,8 +398,12 @@ void stage_chunks(hbg_dataset* ds, const double* g, const double* h, const int32
         convert_stream(h + s0, hf + s0, s1 - s0);
       }
       if (idx) {
-        bool bad = false;
-        for (int64_t i = s0; i < s1; ++i) bad |= static_cast<int64_t>(idx[i]) != first + i;
+        bool bad = false, oor = false;
+        for (int64_t i = s0; i < s1; ++i) {
+          bad |= static_cast<int64_t>(idx[i]) != first + i;
+          oor |= static_cast<uint32_t>(idx[i]) >= limit;  // negative ids wrap above the limit
+        }
+        if (oor) outside[c].store(1, std::memory_order_relaxed);
         if (bad) {
           copy_stream(idx + s0, id + s0, s1 - s0);
           written[static_cast<size_t>(c) * T + w] = 1;
@@ -446,6 +431,8 @@ void stage_chunks(hbg_dataset* ds, const double* g, const double* h, const int32
     for (int c = 0; c < C; ++c) {
       while (done[static_cast<size_t>(c)].load(std::memory_order_acquire) < T) std::this_thread::yield();
       if (prof) (c == 0 ? t_first : t_last) = us();
+      if (outside[c].load(std::memory_order_relaxed))
+        throw Error(HBG_ERR_INVALID_ARGUMENT, "leaf row index out of range");
       const int64_t b = chunk * c, e = std::min<int64_t>(n, b + chunk);
       copy(c, b, e, gf, hf, id, idx != nullptr && broken[c].load(std::memory_order_relaxed) == 0, fill_ids);
     }
@@ -1351,60 +1338,51 @@ int hbg_build_histograms_ex(hbg_dataset* ds, const int32_t* indices, int64_t cou
       // bits64: the fp64 LeafState arrays go up as they are (no per-element
       // cast): pinned ones straight from the caller's memory, pageable ones
       // copied chunk by chunk into the pinned stage by the host pool (the
-      // driver's own pageable path runs at ~11 GB/s). One histogram launch
-      // accumulates in fp64.
+      // driver's own pageable path runs at ~11 GB/s); the pool checks the
+      // ids either way. One histogram launch accumulates in fp64.
       const size_t n = static_cast<size_t>(count);
       double* d_gd = static_cast<double*>(ds->host_gd.get(n * 8));
       double* d_hd = static_cast<double*>(ds->host_hd.get(n * 8));
       const int32_t* d_idx;
-      if (is_pinned(gradients) && is_pinned(hessians)) {
-        HBG_CUDA(cudaMemcpyAsync(d_gd, gradients, n * 8, cudaMemcpyHostToDevice, s));
-        HBG_CUDA(cudaMemcpyAsync(d_hd, hessians, n * 8, cudaMemcpyHostToDevice, s));
-        h2d += static_cast<int64_t>(n) * 16;
-        if (leaf_is_contiguous(indices, count)) {
-          require(indices[0] >= 0 && indices[0] + count <= L.num_rows, "leaf row index out of range");
-          d_idx = identity_rows(ds, indices[0], s);
-        } else {
-          int32_t* di = static_cast<int32_t*>(ds->host_idx.get(n * 4));
-          HBG_CUDA(cudaMemcpyAsync(di, indices, n * 4, cudaMemcpyHostToDevice, s));
-          h2d += static_cast<int64_t>(n) * 4;
-          d_idx = di;
-        }
+      const bool pinned = is_pinned(gradients) && is_pinned(hessians);
+      if (!ds->copy_stream) HBG_CUDA(cudaStreamCreateWithFlags(&ds->copy_stream, cudaStreamNonBlocking));
+      for (int c = 0; c < 17; ++c)
+        if (!ds->chunk_ev[c]) HBG_CUDA(cudaEventCreateWithFlags(&ds->chunk_ev[c], cudaEventDisableTiming));
+      HBG_CUDA(cudaEventRecord(ds->chunk_ev[16], s));
+      HBG_CUDA(cudaStreamWaitEvent(ds->copy_stream, ds->chunk_ev[16], 0));
+      int32_t* di = static_cast<int32_t*>(ds->host_idx.get(n * 4));
+      // the ids travel unless every chunk is one range from idx[0]: chunks
+      // that pass are held back until one fails (then all go). Pinned g/h
+      // go straight from the caller's memory (every chunk `direct`: the pool
+      // only checks the ids), pageable ones through the pinned stage.
+      bool all_contig = true;
+      int64_t sent = 0;
+      const std::vector<char> direct(static_cast<size_t>((count + kStageRows - 1) / kStageRows), pinned ? 1 : 0);
+      stage_chunks<double>(ds, gradients, hessians, indices, count, kStageRows, direct,
+                           [&](int k, int64_t b, int64_t e, const double* gs, const double* hs, const int32_t* is,
+                               bool contig, auto&& fill_ids) {
+                             const size_t m = static_cast<size_t>(e - b);
+                             const double* sg = pinned ? gradients : gs;
+                             const double* sh = pinned ? hessians : hs;
+                             HBG_CUDA(cudaMemcpyAsync(d_gd + b, sg + b, m * 8, cudaMemcpyHostToDevice, ds->copy_stream));
+                             HBG_CUDA(cudaMemcpyAsync(d_hd + b, sh + b, m * 8, cudaMemcpyHostToDevice, ds->copy_stream));
+                             h2d += static_cast<int64_t>(m) * 16;
+                             all_contig = all_contig && contig;
+                             if (!all_contig) {
+                               for (int j = static_cast<int>(sent / kStageRows); j <= k; ++j) fill_ids(j);
+                               HBG_CUDA(cudaMemcpyAsync(di + sent, is + sent, static_cast<size_t>(e - sent) * 4,
+                                                        cudaMemcpyHostToDevice, ds->copy_stream));
+                               h2d += (e - sent) * 4;
+                               sent = e;
+                             }
+                           });
+      HBG_CUDA(cudaEventRecord(ds->chunk_ev[0], ds->copy_stream));
+      HBG_CUDA(cudaStreamWaitEvent(s, ds->chunk_ev[0], 0));
+      if (all_contig) {
+        require(indices[0] >= 0 && indices[0] + count <= L.num_rows, "leaf row index out of range");
+        d_idx = identity_rows(ds, indices[0], s);
       } else {
-        if (!ds->copy_stream) HBG_CUDA(cudaStreamCreateWithFlags(&ds->copy_stream, cudaStreamNonBlocking));
-        for (int c = 0; c < 17; ++c)
-          if (!ds->chunk_ev[c]) HBG_CUDA(cudaEventCreateWithFlags(&ds->chunk_ev[c], cudaEventDisableTiming));
-        HBG_CUDA(cudaEventRecord(ds->chunk_ev[16], s));
-        HBG_CUDA(cudaStreamWaitEvent(ds->copy_stream, ds->chunk_ev[16], 0));
-        int32_t* di = static_cast<int32_t*>(ds->host_idx.get(n * 4));
-        // the ids travel unless every chunk is one range from idx[0]: chunks
-        // that pass are held back until one fails (then all go)
-        bool all_contig = true;
-        int64_t sent = 0;
-        stage_chunks<double>(ds, gradients, hessians, indices, count, kStageRows, direct_chunks(count, kStageRows, false),
-                             [&](int k, int64_t b, int64_t e, const double* gs, const double* hs, const int32_t* is,
-                                 bool contig, auto&& fill_ids) {
-                               const size_t m = static_cast<size_t>(e - b);
-                               HBG_CUDA(cudaMemcpyAsync(d_gd + b, gs + b, m * 8, cudaMemcpyHostToDevice, ds->copy_stream));
-                               HBG_CUDA(cudaMemcpyAsync(d_hd + b, hs + b, m * 8, cudaMemcpyHostToDevice, ds->copy_stream));
-                               h2d += static_cast<int64_t>(m) * 16;
-                               all_contig = all_contig && contig;
-                               if (!all_contig) {
-                                 for (int j = static_cast<int>(sent / kStageRows); j <= k; ++j) fill_ids(j);
-                                 HBG_CUDA(cudaMemcpyAsync(di + sent, is + sent, static_cast<size_t>(e - sent) * 4,
-                                                          cudaMemcpyHostToDevice, ds->copy_stream));
-                                 h2d += (e - sent) * 4;
-                                 sent = e;
-                               }
-                             });
-        HBG_CUDA(cudaEventRecord(ds->chunk_ev[0], ds->copy_stream));
-        HBG_CUDA(cudaStreamWaitEvent(s, ds->chunk_ev[0], 0));
-        if (all_contig) {
-          require(indices[0] >= 0 && indices[0] + count <= L.num_rows, "leaf row index out of range");
-          d_idx = identity_rows(ds, indices[0], s);
-        } else {
-          d_idx = di;
-        }
+        d_idx = di;
       }
       build_device(ds, d_idx, count, d_gd, d_hd, HBG_GH_LEAF_ALIGNED, d_hist, s, nullptr, nullptr, 8, true);
     } else if (count > 0) {

@@ -57,3 +57,38 @@ def test_upload_routes_bit_identical(tmp_path):
                      ("odd_pool", {"HBG_HOST_THREADS": "7"})):
         got = _run(tmp_path, tag, env)
         assert got.shape == base.shape and (got == base).all(), tag
+
+
+def test_contiguous_leaf_past_the_last_row_is_rejected(hbg_mod=None):
+    """Row ids outside the dataset fail with std::invalid_argument — a
+    contiguous range (read from the resident ids, never uploaded) and
+    scattered ids (checked by the staging pass) — on the pageable and pinned
+    routes and both precisions; the handle stays usable."""
+    import torch
+
+    sys.path.insert(0, REPO)
+    import paper_1706_08359_b200 as hbg
+
+    rows = 1_200_000
+    rng = np.random.default_rng(8)
+    cols = rng.integers(0, 64, size=(28, rows), dtype=np.uint8)
+    with hbg.Dataset(cols, 64) as ds:
+        for pin in (False, True):
+            idx = np.arange(rows - 600_000, rows + 600_000, dtype=np.int32)
+            g, h = rng.normal(size=len(idx)), rng.random(len(idx))
+            if pin:
+                idx, g, h = (torch.from_numpy(x).pin_memory().numpy() for x in (idx, g, h))
+            with pytest.raises(hbg.InvalidArgument):
+                hbg.build_histograms_partitioned(ds, hbg.LeafState(idx, g, h))
+            # scattered ids with one past the last row: the staging pass's range check
+            bad = np.sort(rng.choice(rows, 700_000, replace=False)).astype(np.int32)
+            bad[-1] = rows
+            gb, hb = rng.normal(size=len(bad)), rng.random(len(bad))
+            if pin:
+                bad, gb, hb = (torch.from_numpy(x).pin_memory().numpy() for x in (bad, gb, hb))
+            for prec in (32, 64):
+                with pytest.raises(hbg.InvalidArgument):
+                    hbg.build_histograms_partitioned(ds, hbg.LeafState(bad, gb, hb), precision=prec)
+        ok = np.arange(10, 500_010, dtype=np.int32)
+        out = hbg.build_histograms_partitioned(ds, hbg.LeafState(ok, rng.normal(size=len(ok)), rng.random(len(ok))))
+        assert int(out["count"].sum()) == len(ok) * 28
