@@ -108,7 +108,8 @@ int hbg_dataset_packed_words(const hbg_dataset* ds, uint32_t* host_words);
  * (cudaHostAlloc/cudaHostRegister), a share of the chunks — copied as fp64
  * (16 B/row) and converted on the device; row ids travel only for chunks that
  * are not one contiguous range. The same floats and sums on every route:
- * bit-identical results. */
+ * bit-identical results. A row id outside [0, num_rows) returns
+ * HBG_ERR_INVALID_ARGUMENT (checked while the ids are staged). */
 int hbg_build_histograms(hbg_dataset* ds, const int32_t* indices, int64_t count,
                          const double* gradients, const double* hessians, hbg_bin* out);
 /* The same call with the reference's PrecisionMode argument
