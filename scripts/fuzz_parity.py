@@ -31,6 +31,9 @@ from oracle import ffi  # noqa: E402
 from test_gpu_parity import _assert_same_tree  # noqa: E402
 
 
+MAX_ROWS = int(os.environ.get("FUZZ_MAX_ROWS", "300000"))  # > 2M rows: several staged and histogram chunks
+
+
 def leaf_of(rng, rows):
     kind = rng.integers(0, 4)
     if rows == 0:
@@ -53,7 +56,7 @@ def pinned(a):
 def one_case(rng, case):
     d = int(rng.integers(1, 81))
     k = int(rng.choice([2, 3, 4, 7, 16, 17, 32, 64, 100, 128, 200, 256]))
-    rows = int(rng.choice([1, 31, 1000, int(rng.integers(1, 300_001))]))
+    rows = int(rng.choice([1, 31, 1000, int(rng.integers(1, MAX_ROWS + 1))]))
     cols = rng.integers(0, k, size=(d, rows), dtype=np.uint8)
     if rng.random() < 0.3:  # skewed columns
         cols[rng.random(cols.shape) < 0.8] = 0
