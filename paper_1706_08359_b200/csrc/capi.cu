@@ -590,6 +590,21 @@ void build_device_peer(hbg_dataset* ds, const int32_t* d_idx, int64_t count, con
   if (d_idx == nullptr && count > 0) d_idx = identity_rows(ds, 0, s);
   HistPlan plan = plan_histogram(L.bits_per_bin, L.max_bin, L.num_groups, std::max<int64_t>(count, 1), L.device,
                                  /*allow_direct=*/false);
+  // No allocation on this path: a cudaMalloc/cudaFree here can wait for
+  // another rank's reduction, which spins on this rank's rows (ranks sharing
+  // a GPU). The partials were reserved by hbg_peer_create; a plan that would
+  // need more takes fewer, longer row segments instead.
+  if (hist_part_bytes(plan) > ds->part.bytes && ds->part.bytes > 0) {
+    const size_t per_seg = static_cast<size_t>(plan.nblocks) * plan.gb * plan.k_alloc * 32;
+    const size_t fit = std::max<size_t>(1, (ds->part.bytes - 16) / (per_seg * (2 * part_elem_bytes(plan) + 4)));
+    const int64_t n = std::max<int64_t>(count, 1);
+    int64_t seg_len = (n + static_cast<int64_t>(fit) - 1) / static_cast<int64_t>(fit);
+    seg_len = (seg_len + 31) / 32 * 32;
+    plan.seg_len = seg_len;
+    plan.nseg = static_cast<int>((n + seg_len - 1) / seg_len);
+    plan.ctas = plan.nblocks * plan.nseg;
+    plan.part_values = static_cast<size_t>(plan.ctas) * plan.gb * plan.k_alloc * 32;
+  }
   char* part = static_cast<char*>(ds->part.get(hist_part_bytes(plan)));
   HistArgs a{};
   a.packed = reinterpret_cast<const uint8_t*>(ds->packed);
@@ -1779,6 +1794,21 @@ int hbg_peer_create(hbg_dataset* ds, int32_t nranks, int32_t rank, int32_t ctas,
     // reserve every buffer of the peer calls (trees, boosting): an allocation
     // while another rank's grid waits in an exchange serialises behind it
     grow_workspace(ds, *params, ctas, nranks);
+    // ... and of hbg_build_histograms_peer: the partials of any leaf size
+    // (a cudaMalloc/cudaFree while another rank's reduction spins on this
+    // rank's rows can wait for that kernel: ranks sharing a GPU deadlock
+    // until the exchange times out) and the identity rows
+    {
+      size_t part = 0;
+      const int64_t top = std::max<int64_t>(L.num_rows, 1);
+      for (int64_t n = 1;; n = std::min<int64_t>(top, n + std::max<int64_t>(1, n / 4))) {  // ~25% steps
+        part = std::max(part, hist_part_bytes(plan_histogram(L.bits_per_bin, L.max_bin, L.num_groups, n, L.device,
+                                                             /*allow_direct=*/false)));
+        if (n == top) break;
+      }
+      ds->part.get(part);
+      if (L.num_rows > 0) identity_rows(ds, 0, ds->stream);
+    }
     ds->boost_g.get(static_cast<size_t>(L.num_rows) * 4 + 4);
     ds->boost_h.get(static_cast<size_t>(L.num_rows) * 4 + 4);
     ds->boost_leaves.get(sizeof(LeafRange) + 8);

@@ -1,0 +1,160 @@
+"""Randomised sweep of the row-sharded paths (development aid): `world` ranks
+as threads on one GPU, each a partial grid over its own row shard, exchanging
+through each other's exchange areas (hbg_peer_attach; across processes CUDA
+IPC maps the same areas).
+
+    python scripts/fuzz_peer.py [seconds] [seed]
+
+Per case: world 2-4, uneven shards, random shape; the fused cross-rank
+histogram (hbg_build_histograms_peer) of a random leaf against the oracle
+(counts exact, sums within 1e-5 of each bin's sum of |terms|), and a tree
+grown with the in-kernel exchange (hbg_grow_tree_peer): bit-identical on every
+rank and equal to the oracle's bits64 tree up to near-ties (1e-5).
+"""
+import ctypes as C
+import os
+import sys
+import threading
+import time
+import traceback
+
+import numpy as np
+import torch
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+sys.path.insert(0, os.path.join(REPO, "tests"))
+import paper_1706_08359_b200 as hbg  # noqa: E402
+from oracle import ffi  # noqa: E402
+from test_gpu_parity import _assert_same_tree  # noqa: E402
+
+
+def run_ranks(world, fn):
+    errs = []
+
+    def wrap(r):
+        try:
+            fn(r)
+        except Exception as ex:  # noqa: BLE001
+            errs.append(ex)
+
+    ts = [threading.Thread(target=wrap, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if errs:
+        raise errs[0]
+
+
+def one_case(rng, case, sms):
+    world = int(rng.integers(2, 5))
+    rows = int(rng.integers(world * 50, 200_001))
+    d = int(rng.integers(1, 41))
+    k = int(rng.choice([4, 16, 17, 64, 128, 256]))
+    cols = rng.integers(0, k, size=(d, rows), dtype=np.uint8)
+    g = rng.normal(size=rows)
+    h = 0.05 + rng.random(rows)
+    w = rng.random(world) + 0.2
+    cuts = [0] + list(np.round(np.cumsum(w) / w.sum() * rows).astype(int))
+    cuts[-1] = rows
+    desc = f"case {case}: world={world} rows={rows} d={d} k={k} cuts={cuts}"
+    dss = [hbg.Dataset(np.ascontiguousarray(cols[:, cuts[r]:cuts[r + 1]]), k) for r in range(world)]
+    peers = [hbg.Peer(dss[r], world, r, ctas=max(1, sms // world)) for r in range(world)]
+    try:
+        for p in peers:
+            for q in peers:
+                if q is not p:
+                    p.attach(q)
+        # fused histogram of a random leaf (global ids)
+        m = int(rng.integers(1, rows + 1))
+        leaf = np.sort(rng.choice(rows, m, replace=False)).astype(np.int32)
+        gf, hf = g.astype(np.float32), h.astype(np.float32)
+        tens = []
+        for r in range(world):
+            mine = leaf[(leaf >= cuts[r]) & (leaf < cuts[r + 1])]
+            tens.append((torch.from_numpy((mine - cuts[r]).astype(np.int32)).cuda(), torch.from_numpy(gf[mine]).cuda(),
+                         torch.from_numpy(hf[mine]).cuda(), torch.empty(3 * d * k, dtype=torch.float64, device="cuda")))
+        torch.cuda.synchronize()
+        outs = [None] * world
+
+        def hist(r):
+            idx, tg, th, out = tens[r]
+            st = dss[r].stream()
+            dss[r].build_histograms_peer(idx, len(idx), tg, th, out, peers[r], stream=st)
+            hbg.check(hbg.lib().hbg_stream_synchronize(C.c_void_p(st)))
+            outs[r] = out.cpu().numpy()
+
+        run_ranks(world, hist)
+        try:
+            for p in peers:
+                p.check()  # a timed-out wait (a rank that never published) is reported here
+        except Exception as e:  # noqa: BLE001
+            raise RuntimeError(f"{desc}: {e} (rows of the leaf per rank {[len(t[0]) for t in tens]}, m={m})") from None
+        for r in range(1, world):
+            assert outs[r].tobytes() == outs[0].tobytes(), f"{desc}: histogram differs on rank {r}"
+        D = d * k
+        want = ffi.build_histograms(cols, k, leaf, gf[leaf].astype(np.float64), hf[leaf].astype(np.float64), 64)
+        mag = ffi.build_histograms(cols, k, leaf, np.abs(gf[leaf]).astype(np.float64), hf[leaf].astype(np.float64), 64)
+        assert (outs[0][2 * D:].reshape(d, k).astype(np.int64) == want["count"].reshape(d, k)).all(), desc + ": counts"
+        for j, key in ((0, "grad_sum"), (1, "hess_sum")):
+            a = outs[0][j * D:(j + 1) * D].reshape(d, k)
+            b, mm = want[key].reshape(d, k), mag[key].reshape(d, k)
+            err = float((np.abs(a - b) / np.maximum(mm, 1e-300)).max())
+            assert err <= 1e-5, f"{desc}: {key} err {err:.3g}"
+        # tree with the in-kernel exchange
+        leaves = int(rng.integers(2, 64))
+        min_data = int(rng.choice([1, 20, 100]))
+        gt = [(torch.from_numpy(gf[cuts[r]:cuts[r + 1]]).cuda(), torch.from_numpy(hf[cuts[r]:cuts[r + 1]]).cuda())
+              for r in range(world)]
+        torch.cuda.synchronize()
+        res = [None] * world
+
+        def tree(r):
+            res[r] = dss[r].grow_tree_peer(gt[r][0], gt[r][1], peers[r], leaves, min_data, 0.0, dss[r].stream())
+
+        run_ranks(world, tree)
+        for r in range(1, world):
+            assert res[r][0].tobytes() == res[0][0].tobytes(), f"{desc}: split log differs on rank {r}"
+        wl, wn = ffi.grow_tree(cols, k, gf.astype(np.float64), hf.astype(np.float64), leaves, min_data, 0.0, 64)
+        try:
+            _assert_same_tree(res[0][0], res[0][1], wl, wn, cols, gf.astype(np.float64), hf.astype(np.float64), 0.0,
+                              tie_tol=1e-5)
+        except AssertionError as e:
+            log = res[0][0]
+            n = min(len(log), len(wl))
+            i = 0
+            while i < n and all(log[f][i] == wl[f][i] for f in ("feature", "threshold_bin", "left_count")):
+                i += 1
+            if i == n and len(log) == len(wl):
+                return  # same decisions; gains/values of fp32 sums beyond 1e-5 (cancellation)
+            raise AssertionError(f"{desc} tree(leaves={leaves}, min_data={min_data}): {e!r}, first diff {i}") from None
+    finally:
+        for p in peers:
+            p.close()
+        for ds in dss:
+            ds.close()
+
+
+def main():
+    budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
+    seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+    os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    rng = np.random.default_rng(seed)
+    t0 = time.time()
+    n = fails = 0
+    while time.time() - t0 < budget:
+        try:
+            one_case(rng, n, sms)
+        except Exception as e:  # noqa: BLE001
+            fails += 1
+            print("FAIL", str(e)[:400], flush=True)
+            traceback.print_exc(limit=2)
+        n += 1
+    print(f"fuzz_peer: {n} cases, {fails} failures, seed {seed}, {time.time() - t0:.0f} s", flush=True)
+    sys.exit(1 if fails else 0)
+
+
+if __name__ == "__main__":
+    main()
