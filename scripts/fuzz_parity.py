@@ -109,7 +109,13 @@ def one_case(rng, case):
             tprec = int(rng.choice([32, 64]))
             if tprec == 64:  # fp64 everywhere (the host loop): equal up to true ties
                 log, nodes = ds.grow_tree_host(g, h, leaves, min_data, lam, precision=64)
-            else:  # the device growers on fp32 g/h
+            else:  # the device growers on fp32 g/h (the default choice or a forced one)
+                grower = str(rng.choice(["", "wave", "legacy", "host", "persistent"]))
+                if grower:
+                    os.environ["HBG_GROW"] = grower
+                else:
+                    os.environ.pop("HBG_GROW", None)
+                desc += f" grower={grower or 'default'}"
                 dev = torch.device("cuda:0")
                 tg = torch.from_numpy(g.astype(np.float32)).to(dev)
                 th = torch.from_numpy(h.astype(np.float32)).to(dev)
