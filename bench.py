@@ -226,8 +226,10 @@ def run_reference(args):
     unit = "rows*features/s"
     line = {
         "metric": "histogram build rows*features/sec", "value": value, "unit": unit, "impl": "reference",
-        "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        # the same job shape as our arm's line (N = the launch's world size);
+        # the reference itself runs on the host cores of rank 0 (`cpu_baseline`)
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (numpy, reference generator distribution)",
         "config": workload_config((args.rows_total if strong else n) // world, n, d, k, world, strong),
         "reference": {"precision": "bits32", "path": "build_histograms_partitioned (unmodified reference, oracle/_ref)",
