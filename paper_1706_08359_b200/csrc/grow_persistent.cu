@@ -145,7 +145,7 @@ struct GrowArgs {
   // wave grower (single rank; see "wave grower" below)
   Cand* wcand;            // [member][child][wcstride] chunk winners of the current wave
   size_t wcstride;        // chunks per member and child in wcand
-  unsigned* wcnt;         // [wmax] finished chunks per member (last arriver resets)
+  double* wtot;           // [wmax][4] the members' children totals (gl, hl, gr, hr), from their item CTAs
   unsigned char* wstate;  // per-CTA commit log, wstate_stride bytes each
   size_t wstate_stride;
   LeafRange* ranges;      // [max_nodes] rows of every unexpanded node -> its final leaf's value (score update)
@@ -1731,7 +1731,7 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_kernel(GrowArgs a) 
 // output (split log, tree, score-update ranges) is written once at the end
 // from the replayed commit log.
 
-constexpr int kWN = 2048;  // node ids per tree (shared-memory state)
+constexpr int kWN = 1536;  // node ids per tree (shared-memory state): 254 speculative expansions beyond 255 leaves
 static_assert(kWN <= 2048, "node ids are packed in 11 bits");
 
 // Speculation order: prio buckets of 1/32 octave (a positive float's top 13 bits).
@@ -1751,6 +1751,7 @@ struct WaveSmem {
   unsigned char later[kWL];      // commit i: bit c = child c was split later
   short cnode[kWL], ckid[kWL], cout[kWL];  // commit i: node, left child node, output id
   unsigned fresh[32];            // the last wave's new expandable entries, sorted (wave_integrate)
+  NodeDev wrec[2 * kWMax];       // the last wave's children records (wave_publish), member-major
   int nav, nfr, committed, next, expanded, done, W, nsmall, nwc, wc, nwaves, hitems, ditems, err, nfresh;
 };
 
@@ -1785,21 +1786,20 @@ __device__ __forceinline__ bool runs_large(const GrowArgs& a, int64_t count, int
   return (ls || rs) && !(ns <= kDirectRows && ns * a.fchunk <= kDirectBudget);
 }
 
-// Warp 0 after a wave's barrier: the members' children (records published
-// before it) join the speculative tree.
+// Warp 0 after a wave's barrier: the members' children (records built by
+// wave_publish) join the speculative tree.
 __device__ void wave_integrate(const GrowArgs& a, WaveSmem& w) {
   const int lane = threadIdx.x;
-  const int rep = blockIdx.x % kRep;
   const int W = w.W;
   bool add = false;
   int id = 0;
   if (lane < 2 * W) {
     const int x = w.wave[lane >> 1];
     id = w.kid[x] + (lane & 1);
-    const NodeDev* P = a.nodes + static_cast<size_t>(rep) * a.max_nodes + id;
-    const double g = __ldcg(a.node_gain + static_cast<size_t>(rep) * a.max_nodes + id);
-    const int64_t n = __ldcg(&P->count);
-    const int64_t nl = __ldcg(&P->best.left_count);
+    const NodeDev& P = w.wrec[lane];  // wave_publish: member lane >> 1, child lane & 1
+    const double g = P.has_best ? P.best.gain : -1.0;
+    const int64_t n = P.count;
+    const int64_t nl = P.best.left_count;
     const unsigned long long key = gain_key(g);
     w.gkey[id] = key;
     w.kid[id] = -1;
@@ -2107,13 +2107,23 @@ __device__ void load_members(const GrowArgs& a, WaveSmem& w, Desc* Dm) {
   __syncthreads();
 }
 
-// The last CTA to finish member D's chunks: per-child winner over the chunk
-// winners (as winners()), the children's records and gains, every replica.
+// After the wave's last barrier, every CTA: warp j builds member j's
+// children records — per child, the winner over its chunk winners (as
+// winners()), the totals from the partition (large members: every CTA's own
+// Desc; small members: a.wtot, written by their item CTAs) — into shared
+// memory for wave_integrate, and writes them to the CTA's own replica of the
+// node records (the copies any CTA reads later are then its own writes, or
+// identical writes of another CTA with the same replica: no barrier needed
+// before this CTA's next load_members). Replaces a last-arriver publish
+// before the barrier (an atomic and a load round trip on the critical CTA).
 template <int NT>
-__device__ void publish_member(const GrowArgs& a, const Desc& D, int nwc) {
-  __shared__ NodeDev rec[2];
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x, child = lane >> 4, sub = lane & 15;
+__device__ void wave_publish(const GrowArgs& a, WaveSmem& w, const Desc* Dm) {
+  const int W = w.W, wp = static_cast<int>(threadIdx.x >> 5);
+  if (wp < W) {
+    const Desc& D = Dm[wp];
+    const int lane = threadIdx.x & 31, child = lane >> 4, sub = lane & 15;
+    const bool small = wp < w.nsmall;
+    const int nwc = small ? w.nwc : a.nchunks;
     const bool want = D.path != kNoHist && (child == 0 ? D.lsplit : D.rsplit);
     Cand c{0.0, -1, -1, 0.0, 0.0, 0};
     unsigned long long hk = 0ull;
@@ -2136,6 +2146,11 @@ __device__ void publish_member(const GrowArgs& a, const Desc& D, int nwc) {
         if (take) c = o;
       }
     }
+    double tg = 0.0, th = 0.0;
+    if (sub == 0) {
+      tg = small ? __ldcg(a.wtot + 4 * D.mslot + 2 * child) : D.tot[2 * child];
+      th = small ? __ldcg(a.wtot + 4 * D.mslot + 2 * child + 1) : D.tot[2 * child + 1];
+    }
     warp_argmax_key(hk, lk, 16);
     {
       const unsigned mine = (hk != 0ull && c.f >= 0 && gain_key(c.gain) == hk &&
@@ -2147,12 +2162,13 @@ __device__ void publish_member(const GrowArgs& a, const Desc& D, int nwc) {
       c = hk == 0ull ? Cand{0.0, -1, -1, 0.0, 0.0, 0} : wv;
     }
     if (sub == 0) {
-      NodeDev& r = rec[child];
-      r.begin = child == 0 ? D.begin : D.begin + D.nl_loc;
-      r.count = child == 0 ? D.nl_loc : D.count - D.nl_loc;
+      NodeDev& r = w.wrec[2 * wp + child];
+      // one rank (the wave grower's only case): this rank's rows are all rows
+      r.begin = child == 0 ? D.begin : D.begin + D.nl;
+      r.count = child == 0 ? D.nl : D.count - D.nl;
       r.gcount = child == 0 ? D.nl : D.nr;
-      r.grad = D.tot[2 * child];
-      r.hess = D.tot[2 * child + 1];
+      r.grad = tg;
+      r.hess = th;
       r.buf = D.buf_out;
       if (want) {
         write_split(c, r.grad, r.hess, r.gcount, a.lambda, &r.best);
@@ -2165,34 +2181,22 @@ __device__ void publish_member(const GrowArgs& a, const Desc& D, int nwc) {
     }
   }
   __syncthreads();
+  const size_t rep = static_cast<size_t>(blockIdx.x % kRep);
   constexpr int Wd = static_cast<int>(sizeof(NodeDev) / 8);
-  for (int t = threadIdx.x; t < 2 * kRep * Wd; t += NT) {
-    const int ch = t / (kRep * Wd), r = (t / Wd) % kRep, q = t % Wd;
-    reinterpret_cast<double*>(a.nodes + static_cast<size_t>(r) * a.max_nodes + D.left_id + ch)[q] =
-        reinterpret_cast<const double*>(&rec[ch])[q];
+  for (int t = threadIdx.x; t < 2 * W * Wd; t += NT) {
+    const int m = t / (2 * Wd), ch = (t / Wd) % 2, q = t % Wd;
+    reinterpret_cast<double*>(a.nodes + rep * a.max_nodes + Dm[m].left_id + ch)[q] =
+        reinterpret_cast<const double*>(&w.wrec[2 * m + ch])[q];
   }
-  if (threadIdx.x < 2 * kRep) {
-    const int ch = threadIdx.x / kRep, r = threadIdx.x % kRep;
-    a.node_gain[static_cast<size_t>(r) * a.max_nodes + D.left_id + ch] = rec[ch].has_best ? rec[ch].best.gain : -1.0;
-  }
+  for (int t = threadIdx.x; t < 2 * W; t += NT)
+    a.node_gain[rep * a.max_nodes + Dm[t >> 1].left_id + (t & 1)] = w.wrec[t].has_best ? w.wrec[t].best.gain : -1.0;
   __syncthreads();
 }
 
-// One chunk of member D is done (its winners are in wcand): count it; the
-// last of the member's nwc chunks publishes the children. Whole CTA.
-template <int NT>
-__device__ void chunk_done(const GrowArgs& a, const Desc& D, int nwc) {
-  __shared__ int s_last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    // acq_rel: releases this CTA's winners (ordered before by __syncthreads)
-    // and, for the last arrival, acquires every other chunk's
-    const unsigned old = atom_add_acq_rel(a.wcnt + D.mslot, 1u);
-    s_last = old == static_cast<unsigned>(nwc - 1) ? 1 : 0;
-    if (s_last) a.wcnt[D.mslot] = 0u;  // every chunk has arrived: reset for the next wave (a grid barrier follows)
-  }
-  __syncthreads();
-  if (s_last) publish_member<NT>(a, D, nwc);
+// A small member's item CTA: the children totals it ranked (wave_publish reads them).
+__device__ __forceinline__ void member_totals(const GrowArgs& a, const Desc& D) {
+  if (threadIdx.x == 0)
+    for (int q = 0; q < 4; ++q) a.wtot[4 * D.mslot + q] = D.tot[q];
 }
 
 __device__ __forceinline__ CandOut wave_out(const GrowArgs& a, const Desc& D, int c) {
@@ -2240,7 +2244,7 @@ __device__ void wave_small(const GrowArgs& a, const WaveSmem& w, Desc* Dm, PartS
       __syncthreads();
       finish_range<K, NT>(a, D, f0, nf, 0, smem, wave_out(a, D, c));
     }
-    chunk_done<NT>(a, D, nwc);
+    member_totals(a, D);
   }
 }
 
@@ -2291,7 +2295,6 @@ __device__ void wave_large_hist(const GrowArgs& a, const WaveSmem& w, Desc* Dm, 
     }
     __syncthreads();
     finish_range<K, NT>(a, D, f0, nf, 0, smem, wave_out(a, D, c));
-    chunk_done<NT>(a, D, a.nchunks);
   }
   if (hitems == 0) return;
   stamp(a, w.nwaves, 17);  // CTA 0's items done
@@ -2313,7 +2316,6 @@ __device__ void wave_large_hist(const GrowArgs& a, const WaveSmem& w, Desc* Dm, 
     const Desc& D = Dm[j];
     const int f0 = c * a.fchunk;
     finish_range<K, NT>(a, D, f0, min(a.fchunk, a.d - f0), 0, smem, wave_out(a, D, c));
-    chunk_done<NT>(a, D, a.nchunks);
   }
 }
 
@@ -2415,8 +2417,6 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_wave_kernel(GrowArg
       for (int j = w.nsmall; j < w.W; ++j) partition_scatter<NT>(a, Dm[j], ps, smem);
       grid_sync(a);
       stamp(a, w.nwaves, 2);
-      for (int j = w.nsmall; j < w.W; ++j)
-        if (Dm[j].path == kNoHist && blockIdx.x == 0) publish_member<NT>(a, Dm[j], 0);
       wave_large_hist<BITS, K, NT>(a, w, Dm, smem);
     }
     stamp(a, w.nwaves, 3);
@@ -2426,6 +2426,7 @@ __global__ void __launch_bounds__(grow_threads<K>(), 1) grow_wave_kernel(GrowArg
     }
     grid_sync(a);
     stamp(a, w.nwaves, 4);
+    wave_publish<NT>(a, w, Dm);
     if (threadIdx.x < 32) wave_integrate(a, w);
     stamp(a, w.nwaves, 6);
     if (threadIdx.x == 0) ++w.nwaves;
@@ -2613,7 +2614,7 @@ size_t grow_scratch_bytes(const PersistentGrowArgs& h, int device) {
   add(static_cast<size_t>(kRep * 2 * g.nchunks) * sizeof(Cand));
   if (g.wave) {
     add(static_cast<size_t>(2 * g.wmax) * g.wcstride * sizeof(Cand));           // wcand
-    add(static_cast<size_t>(g.wmax) * sizeof(unsigned));                        // wcnt
+    add(static_cast<size_t>(g.wmax) * 4 * sizeof(double));                      // wtot
     add(static_cast<size_t>(g.ctas) * wave_state_bytes(h.num_leaves, g.max_nodes));  // wstate
     add(static_cast<size_t>(g.max_nodes) * sizeof(LeafRange));                       // ranges
   }
@@ -2719,7 +2720,7 @@ const void* launch_grow_persistent(const PersistentGrowArgs& h, int device, cuda
   a.cand = reinterpret_cast<Cand*>(take(static_cast<size_t>(kRep * 2 * g.nchunks) * sizeof(Cand)));
   if (g.wave) {
     a.wcand = reinterpret_cast<Cand*>(take(static_cast<size_t>(2 * g.wmax) * g.wcstride * sizeof(Cand)));
-    a.wcnt = reinterpret_cast<unsigned*>(take(static_cast<size_t>(g.wmax) * sizeof(unsigned)));
+    a.wtot = reinterpret_cast<double*>(take(static_cast<size_t>(g.wmax) * 4 * sizeof(double)));
     a.wstate_stride = wave_state_bytes(h.num_leaves, g.max_nodes);
     a.wstate = take(static_cast<size_t>(g.ctas) * a.wstate_stride);
     a.ranges = reinterpret_cast<LeafRange*>(take(static_cast<size_t>(g.max_nodes) * sizeof(LeafRange)));
@@ -2730,7 +2731,6 @@ const void* launch_grow_persistent(const PersistentGrowArgs& h, int device, cuda
   HBG_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(unsigned), s));
   HBG_CUDA(cudaMemsetAsync(a.picked, 0, kRep * max_nodes * sizeof(int), s));
   HBG_CUDA(cudaMemsetAsync(a.counts, 0, 8 * sizeof(int), s));
-  if (g.wave) HBG_CUDA(cudaMemsetAsync(a.wcnt, 0, static_cast<size_t>(g.wmax) * sizeof(unsigned), s));
   void* fn = grow_fn(h.bits, g.k_alloc, g.wave);
   int occ = 0;
   HBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, g.nt, g.smem));
