@@ -399,7 +399,7 @@ def run_hbg(args):
     }
 
     # --- e2e through the host C-ABI drop-in (pinned host buffers)
-    e2e_steps = max(1, min(args.steps, 10))
+    e2e_steps = max(1, min(args.steps, 30))  # host-side noise: a longer mean
     pin_idx = torch.from_numpy(idx).pin_memory().numpy()
     pin_g = torch.from_numpy(g).pin_memory().numpy()
     pin_h = torch.from_numpy(h).pin_memory().numpy()
