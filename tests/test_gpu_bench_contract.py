@@ -46,3 +46,23 @@ def test_bench_line_contract():
     cpu = line["cpu_baseline"]
     assert cpu["kind"] in ("reference", "port") and cpu["cores"] >= 1 and cpu["value"] > 0
     assert "sm_mhz" in line["clocks"] and "reasons" in line["clocks"]
+
+
+def test_reference_arm_line_matches_our_arm():
+    """`bench.py --impl reference`: the reference's own CPU path on the same
+    workload — the same metric, unit and config as our arm's line."""
+    ours = [sys.executable, os.path.join(REPO, "bench.py"), "--steps", "3", "--warmup", "3", "--no-variants",
+            "--no-cpu-baseline", "--rows", "300000", "--trees", "1"]
+    ref = [sys.executable, os.path.join(REPO, "bench.py"), "--impl", "reference", "--steps", "2", "--warmup", "1",
+           "--rows", "300000"]
+    lines = []
+    for cmd in (ours, ref):
+        r = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr[-3000:]
+        lines.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    a, b = lines
+    assert b["impl"] == "reference"
+    for key in ("metric", "unit", "higher_is_better", "n_gpus", "scaling", "config"):
+        assert a[key] == b[key], key
+    assert b["value"] > 0 and b["cpu_baseline"]["kind"] in ("reference", "port")
+    assert b["e2e"]["value"] == b["value"] and b["e2e"]["h2d_bytes_per_step"] == 0
